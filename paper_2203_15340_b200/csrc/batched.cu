@@ -1,0 +1,374 @@
+// batched.cu -- K4: many independent small ILS instances, one CTA (one warp) per instance.
+//
+// Each CTA runs a complete solve of its instance with shared-memory-resident A1 (column-major):
+//   method 0  SP         (Alg. 1): Gram, Cholesky, explicit P, x <- P c_k
+//   method 1  SP-RK-RGS  (Alg. 2)
+//   method 2  SP-SCD     (Alg. 5); weighted = SP-RCD
+// n <= 32: lane j owns coordinate j of x, c, z, beta, r (SCD); every reduction is a warp shuffle;
+// no block, cluster or grid synchronisation. Instance i uses seed + i (include/ils.h).
+#include <climits>
+
+#include "common.cuh"
+#include "ils_internal.h"
+
+namespace ils {
+
+struct BatchParams {
+  const double* A;   // [batch][m][n]
+  const double* b;   // [batch][m]
+  int64_t batch;
+  int p, q, n;
+  const double* x0;    // [batch][n] or null
+  double* x;           // [batch][n]
+  const double* xref;  // [batch][n] or null
+  double tol;
+  int64_t max_iter;
+  int stop, method;
+  double inner_tol;
+  int64_t max_inner, check_every;
+  uint64_t seed;
+  int alpha_mode, alpha_k, weighted;
+  int64_t* inst_iters;
+  int32_t* inst_status;
+  unsigned long long* inner_total;
+};
+
+struct BKey {
+  uint32_t alpha;
+  int32_t j;
+  uint32_t key[kFeistelRounds];
+};
+
+__device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+
+template <int UP>
+__global__ void __launch_bounds__(32) batched_kernel(BatchParams P) {
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x;
+  const int64_t inst = blockIdx.x;
+  const int p = P.p, q = P.q, n = P.n, m = p + q;
+  const double* A = P.A + inst * (int64_t)m * n;
+  const double* b = P.b + inst * (int64_t)m;
+  const uint64_t seed = P.seed + (uint64_t)inst;
+  double* A1T = sm;                       // [n][p]
+  double* G = A1T + n * p;                // [n][n]  Gram, then P (SP)
+  double* az = G + n * n;                 // [p]
+  uint64_t* S = reinterpret_cast<uint64_t*>(az + p);   // [32]
+  BKey* keys = reinterpret_cast<BKey*>(S + 32);        // [32]
+
+  for (int e = lane; e < n * p; e += 32) {
+    const int j = e / p, i = e % p;
+    A1T[e] = A[(int64_t)i * n + j];
+  }
+  __syncwarp();
+  const bool act = lane < n;
+  // N_j sequential in i without FMA (include/ils.h), A1^T b1
+  double Nj = 0.0, a1tb1 = 0.0;
+  if (act) {
+    for (int i = 0; i < p; ++i) {
+      const double v = A1T[lane * p + i];
+      Nj = __dadd_rn(Nj, __dmul_rn(v, v));
+      a1tb1 = fma(v, b[i], a1tb1);
+    }
+  }
+  double x = (act && P.x0) ? P.x0[inst * n + lane] : 0.0;
+  const double xr = (act && P.xref) ? P.xref[inst * n + lane] : 0.0;
+  double xr2 = warp_sum(xr * xr);
+
+  if (P.method == 1 || P.weighted) {   // weights for the column-norm sampler
+    double mx = act ? Nj : 0.0;
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    uint64_t w = 0;
+    if (act) {
+      const uint64_t f = (uint64_t)floor(scalbn(__ddiv_rn(Nj, mx), 32));
+      w = f < 1 ? 1 : f;
+    }
+    for (int o = 1; o < 32; o <<= 1) {   // inclusive warp scan (exact integers)
+      const uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    S[lane] = w;
+  }
+  if (P.method != 1) {   // Gram A1bar (lane j: column j)
+    if (act) {
+      for (int i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int k = 0; k < p; ++k) s = fma(A1T[i * p + k], A1T[lane * p + k], s);
+        G[i * n + lane] = s;
+      }
+    }
+  }
+  __syncwarp();
+  if (P.method == 0) {
+    // Cholesky (lower, in place in G), then P = L^{-T} L^{-1}: lane c solves column c.
+    for (int k = 0; k < n; ++k) {
+      if (lane == 0) G[k * n + k] = sqrt(G[k * n + k]);
+      __syncwarp();
+      const double d = G[k * n + k];
+      if (act && lane > k) G[lane * n + k] /= d;
+      __syncwarp();
+      if (act && lane > k)
+        for (int j = k + 1; j <= lane; ++j) G[lane * n + j] -= G[lane * n + k] * G[j * n + k];
+      __syncwarp();
+    }
+    double y[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) y[i] = 0.0;
+    if (act) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        if (i < n) {
+          double s = (i == lane) ? 1.0 : 0.0;
+          for (int k = 0; k < i; ++k) s -= G[i * n + k] * y[k];
+          y[i] = s / G[i * n + i];
+        }
+      }
+#pragma unroll
+      for (int i = 31; i >= 0; --i) {
+        if (i < n) {
+          double s = y[i];
+          for (int k = i + 1; k < n; ++k) s -= G[k * n + i] * y[k];
+          y[i] = s / G[i * n + i];
+        }
+      }
+    }
+    __syncwarp();
+    if (act)
+      for (int i = 0; i < n; ++i) G[i * n + lane] = y[i];   // P[i][lane] (symmetric)
+    __syncwarp();
+  }
+
+  int64_t it = 0;
+  int conv = 0;
+  unsigned long long inner_sum = 0;
+  for (; it < P.max_iter; ++it) {
+    // c_k = A1^T b1 + A2^T (A2 x_k - b2)  (Alg. 2 step 5)
+    double c = a1tb1;
+    for (int i0 = 0; i0 < q; i0 += 32) {
+      const int i = i0 + lane;
+      double d = 0.0;
+      if (i < q) {
+        const double* ar = A + (int64_t)(p + i) * n;
+        for (int j = 0; j < n; ++j) d = fma(ar[j], shfl(x, j), d);
+        d -= b[p + i];
+      } else {
+        for (int j = 0; j < n; ++j) (void)shfl(x, j);
+      }
+      const int cnt = (q - i0 < 32) ? q - i0 : 32;
+      for (int ii = 0; ii < cnt; ++ii) {
+        const double di = shfl(d, ii);
+        if (act) c = fma(A[(int64_t)(p + i0 + ii) * n + lane], di, c);
+      }
+    }
+    double xn = 0.0;
+    if (P.method == 0) {
+      for (int i = 0; i < n; ++i) {
+        const double ci = shfl(c, i);
+        if (act) xn = fma(G[i * n + lane], ci, xn);
+      }
+    } else {
+      const double cn2 = warp_sum(act ? c * c : 0.0);
+      const double cnorm = sqrt(cn2);
+      int64_t steps = 0;
+      if (cnorm != 0.0 && P.method == 1) {
+        // ---- SP-RK-RGS inner (Alg. 2 steps 6-12)
+        double w[UP], r[UP];
+#pragma unroll
+        for (int u = 0; u < UP; ++u) w[u] = r[u] = 0.0;
+        double z = 0.0;
+        int my1 = 0, my2 = 0;
+        for (int64_t t = 0; t < P.max_inner; ++t) {
+          if ((t & 31) == 0) {
+            const U4 xw = draw(seed, (uint32_t)it, (uint64_t)(t + lane), kTagRkRgs);
+            my1 = sample_weighted(((uint64_t)xw.y << 32) | xw.x, S, n);
+            my2 = sample_weighted(((uint64_t)xw.w << 32) | xw.z, S, n);
+          }
+          const int j1 = __shfl_sync(0xffffffffu, my1, (int)(t & 31));
+          const int j2 = __shfl_sync(0xffffffffu, my2, (int)(t & 31));
+          const double* a1 = A1T + j1 * p;
+          const double* a2 = A1T + j2 * p;
+          double d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+          for (int u = 0; u < UP; ++u) {
+            const int i = lane + 32 * u;
+            if (i < p) {
+              const double x1 = a1[i], x2 = a2[i];
+              d1 = fma(x1, w[u], d1);
+              d2 = fma(x2, r[u], d2);
+              d3 = fma(x2, x1, d3);
+            }
+          }
+          d1 = warp_sum(d1);
+          d2 = warp_sum(d2);
+          d3 = warp_sum(d3);
+          const double cj1 = shfl(c, j1), n1 = shfl(Nj, j1), n2 = shfl(Nj, j2);
+          const double s1 = (cj1 - d1) / n1;
+          const double s2 = (d2 + s1 * d3) / n2;
+#pragma unroll
+          for (int u = 0; u < UP; ++u) {
+            const int i = lane + 32 * u;
+            if (i < p) {
+              const double x1 = a1[i], x2 = a2[i];
+              w[u] = fma(s1, x1, w[u]);
+              r[u] = fma(s1, x1, r[u]);
+              r[u] = fma(-s2, x2, r[u]);
+            }
+          }
+          if (lane == j2) z += s2;
+          steps = t + 1;
+          if ((t + 1) % P.check_every == 0) {
+#pragma unroll
+            for (int u = 0; u < UP; ++u) {
+              const int i = lane + 32 * u;
+              double a = 0.0;
+              for (int j = 0; j < n; ++j) {
+                const double zj = shfl(z, j);
+                if (i < p) a = fma(A1T[j * p + i], zj, a);
+              }
+              if (i < p) {
+                az[i] = a;
+                r[u] = w[u] - a;
+              }
+            }
+            __syncwarp();
+            double g = 0.0;
+            if (act) {
+              for (int i = 0; i < p; ++i) g = fma(A1T[lane * p + i], az[i], g);
+              g -= c;
+            }
+            __syncwarp();
+            const double g2 = warp_sum(act ? g * g : 0.0);
+            if (sqrt(g2) <= P.inner_tol * cnorm) break;
+          }
+        }
+        xn = z;
+      } else if (cnorm != 0.0) {
+        // ---- SP-SCD / SP-RCD inner (Alg. 5 steps 5-12)
+        double rr = act ? c : 0.0, beta = 0.0;
+        const uint32_t hb = feistel_half_bits((uint32_t)n), msk = (1u << hb) - 1u;
+        for (int64_t t = 0; t < P.max_inner; ++t) {
+          if ((t & 31) == 0) {
+            BKey e;
+            const uint64_t tt = (uint64_t)(t + lane);
+            if (P.weighted) {
+              const U4 xw = draw(seed, (uint32_t)it, tt, kTagRcd);
+              e.j = sample_weighted(((uint64_t)xw.y << 32) | xw.x, S, n);
+              e.alpha = 1;
+            } else {
+              const U4 a = draw(seed, (uint32_t)it, tt, kTagScdA);
+              const U4 bb = draw(seed, (uint32_t)it, tt, kTagScdB);
+              const U4 cc = draw(seed, (uint32_t)it, tt, kTagScdC);
+              const U4 dd = draw(seed, (uint32_t)it, tt, kTagScdD);
+              e.alpha = P.alpha_mode == ILS_ALPHA_UNIFORM ? 1u + mulhi32(a.x, (uint32_t)n)
+                                                          : (uint32_t)(P.alpha_k < n ? P.alpha_k : n);
+              e.j = -1;
+              e.key[0] = a.y; e.key[1] = a.z; e.key[2] = a.w;
+              e.key[3] = bb.x; e.key[4] = bb.y; e.key[5] = bb.z; e.key[6] = bb.w;
+              e.key[7] = cc.x; e.key[8] = cc.y; e.key[9] = cc.z; e.key[10] = cc.w;
+              e.key[11] = dd.x;
+            }
+            __syncwarp();
+            keys[lane] = e;
+            __syncwarp();
+          }
+          const BKey& e = keys[t & 31];
+          int j;
+          double rj;
+          if (P.weighted) {
+            j = e.j;
+            rj = shfl(rr, j);
+          } else {
+            ArgMax best{-1.0, INT_MAX, 0.0};
+            if (act) {
+              const uint32_t mm = feistel_inverse((uint32_t)lane, e.key, hb, msk, (uint32_t)n);
+              if (mm < e.alpha) best = ArgMax{rr * rr, lane, rr};
+            }
+            best = warp_argmax(best);
+            j = best.idx;
+            rj = best.pay;
+          }
+          const double sc = rj / shfl(Nj, j);
+          if (act) rr = fma(-sc, G[j * n + lane], rr);
+          if (lane == j) beta += sc;
+          steps = t + 1;
+          if ((t + 1) % P.check_every == 0) {
+            double a = 0.0;
+            for (int jj = 0; jj < n; ++jj) {
+              const double bj = shfl(beta, jj);
+              if (act) a = fma(G[jj * n + lane], bj, a);
+            }
+            rr = act ? c - a : 0.0;
+            const double r2 = warp_sum(rr * rr);
+            if (sqrt(r2) <= P.inner_tol * cnorm) break;
+          }
+        }
+        xn = beta;
+      }
+      inner_sum += (unsigned long long)steps;
+    }
+    x = act ? xn : 0.0;
+    // stop test (XREF)
+    const double e = act ? x - xr : 0.0;
+    const double e2 = warp_sum(e * e);
+    if (P.stop == ILS_STOP_XREF && P.xref && sqrt(e2) <= P.tol * sqrt(xr2)) {
+      conv = 1;
+      ++it;
+      break;
+    }
+  }
+  if (act) P.x[inst * n + lane] = x;
+  if (lane == 0) {
+    if (P.inst_iters) P.inst_iters[inst] = it;
+    if (P.inst_status) P.inst_status[inst] = conv;
+    atomicAdd(P.inner_total, inner_sum);
+  }
+}
+
+int batched_solve(Handle& h, int method, const double* x0, double* x, double tol, int64_t max_iter,
+                  const ils_opts& o, int64_t* inst_iters_dev, int32_t* inst_status_dev) {
+  if (h.n > 32 || h.p > 256 || h.q > 4096) {
+    set_error("batched path supports n <= 32, p <= 256");
+    return ILS_ERR_UNSUPPORTED;
+  }
+  BatchParams P{};
+  P.A = h.Ab;
+  P.b = h.bb;
+  P.batch = h.batch;
+  P.p = (int)h.p;
+  P.q = (int)h.q;
+  P.n = (int)h.n;
+  P.x0 = x0;
+  P.x = x;
+  P.xref = o.x_ref;
+  P.tol = tol;
+  P.max_iter = max_iter;
+  P.stop = o.stop;
+  P.method = method;
+  P.inner_tol = o.inner_tol;
+  P.max_inner = o.max_inner;
+  P.check_every = o.check_every > 0 ? o.check_every : h.n;
+  P.seed = o.seed;
+  P.alpha_mode = o.alpha_mode;
+  P.alpha_k = o.alpha_k;
+  P.weighted = (method == 2) ? o.weighted : 0;
+  P.inst_iters = inst_iters_dev;
+  P.inst_status = inst_status_dev;
+  P.inner_total = reinterpret_cast<unsigned long long*>(&h.dstat->inner_steps);
+  const size_t smem = (size_t)(h.n * h.p + h.n * h.n + h.p) * 8 + 32 * 8 + 32 * sizeof(BKey);
+  const int up = (int)((h.p + 31) / 32);
+#define BLAUNCH(UU)                                                                                   \
+  do {                                                                                                \
+    ILS_CU(cudaFuncSetAttribute(batched_kernel<UU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    batched_kernel<UU><<<(unsigned)h.batch, 32, smem, h.stream>>>(P);                                 \
+    ILS_LAUNCHED("batched_kernel");                                                                   \
+  } while (0)
+  if (up <= 1) BLAUNCH(1);
+  else if (up <= 2) BLAUNCH(2);
+  else if (up <= 3) BLAUNCH(3);
+  else if (up <= 4) BLAUNCH(4);
+  else BLAUNCH(8);
+#undef BLAUNCH
+  return ILS_OK;
+}
+
+}  // namespace ils

@@ -1,0 +1,402 @@
+// dla.cu -- K3: the only dense contractions of the method, on fp64 tensor cores (DMMA).
+//
+//   Gram  A1bar = A1^T A1             (Alg. 1 step 2 / Alg. 5 step 2)
+//   Cholesky A1bar = L L^T, Z = L^{-1} (recursive, DMMA GEMMs at every level)
+//   P = (A1^T A1)^{-1} = Z^T Z        (Alg. 1 step 2 explicit inverse)
+//   M = A1^T A1 - A2^T A2             (normal matrix; reference solve only)
+//
+// GEMM convention: C[M x N] = alpha * sum_k opA(i,k) * opB(j,k) + beta * C
+//   opA(i,k) = A[i*lda + k] (K-contiguous) or A[k*lda + i] (M-contiguous, a_mc)
+//   opB(j,k) = B[j*ldb + k] (K-contiguous) or B[k*ldb + j] (N-contiguous, b_nc)
+// All dimensions are multiples of 64 (M, N) and 32 (K): the handle pads every dense
+// operand with zeros (identity on the padded diagonal), so there are no tails.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "ils_internal.h"
+
+namespace ils {
+
+constexpr int BM = 64, BN = 64, BK = 32, GEMM_THREADS = 128, GEMM_STAGES = 3;
+constexpr int LDK = BK + 4;   // K-contiguous smem tile row stride (doubles)
+constexpr int LDM = BM + 4;   // M-contiguous smem tile row stride (doubles)
+constexpr int TILE_DBL = (BM * LDK > BK * LDM) ? BM * LDK : BK * LDM;   // doubles per operand tile
+constexpr size_t GEMM_SMEM = (size_t)GEMM_STAGES * 2 * TILE_DBL * sizeof(double);
+
+template <bool MC>
+__device__ __forceinline__ void load_tile(double* __restrict__ s, const double* __restrict__ g, int64_t ld,
+                                          int64_t row0, int64_t k0) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < (BM * BK / 2) / GEMM_THREADS; ++u) {
+    const int q = tid + u * GEMM_THREADS;
+    if (!MC) {  // rows of 32 k-values: 16 chunks of 2 doubles
+      const int r = q >> 4, c = q & 15;
+      cp_async16(s + r * LDK + 2 * c, g + (row0 + r) * ld + k0 + 2 * c);
+    } else {    // k-rows of 64 m-values: 32 chunks
+      const int kk = q >> 5, c = q & 31;
+      cp_async16(s + kk * LDM + 2 * c, g + (k0 + kk) * ld + row0 + 2 * c);
+    }
+  }
+}
+
+template <bool MC>
+__device__ __forceinline__ double frag(const double* __restrict__ s, int r, int k) {
+  return MC ? s[k * LDM + r] : s[r * LDK + k];
+}
+
+// grid: (tiles, 1, splits). lower_only: tiles enumerate bm >= bn. tri_k: K starts at max(bm,bn)*64.
+template <bool AMC, bool BNC>
+__global__ void __launch_bounds__(GEMM_THREADS) gemm_dmma_kernel(
+    int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
+    const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
+    int lower_only, int tri_k, int splits, double* __restrict__ ws) {
+  extern __shared__ __align__(128) double smem[];
+  const int64_t nt = N / BN;
+  int64_t bm, bn;
+  const int64_t t = blockIdx.x;
+  if (lower_only) {
+    bm = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    while ((bm + 1) * (bm + 2) / 2 <= t) ++bm;
+    while (bm * (bm + 1) / 2 > t) --bm;
+    bn = t - bm * (bm + 1) / 2;
+  } else {
+    bm = t / nt;
+    bn = t % nt;
+  }
+  const int64_t row0 = bm * BM, col0 = bn * BN;
+  int64_t kbeg = tri_k ? (row0 > col0 ? row0 : col0) : 0;
+  const int64_t klen = K - kbeg;
+  int64_t kc = (klen + splits - 1) / splits;
+  kc = (kc + BK - 1) / BK * BK;
+  const int64_t z = blockIdx.z;
+  const int64_t ks = kbeg + z * kc;
+  const int64_t ke = (ks + kc < K) ? ks + kc : K;
+  const int nk = ke > ks ? (int)((ke - ks) / BK) : 0;
+
+  double* sA = smem;
+  double* sB = smem + GEMM_STAGES * TILE_DBL;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int fr = lane >> 2, fk = lane & 3;
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < GEMM_STAGES - 1; ++s) {
+    if (s < nk) {
+      load_tile<AMC>(sA + s * TILE_DBL, A, lda, row0, ks + (int64_t)s * BK);
+      load_tile<BNC>(sB + s * TILE_DBL, B, ldb, col0, ks + (int64_t)s * BK);
+    }
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<GEMM_STAGES - 2>();
+    __syncthreads();
+    {
+      const int pf = kt + GEMM_STAGES - 1;
+      if (pf < nk) {
+        const int st = pf % GEMM_STAGES;
+        load_tile<AMC>(sA + st * TILE_DBL, A, lda, row0, ks + (int64_t)pf * BK);
+        load_tile<BNC>(sB + st * TILE_DBL, B, ldb, col0, ks + (int64_t)pf * BK);
+      }
+      cp_async_commit();
+    }
+    const double* a = sA + (kt % GEMM_STAGES) * TILE_DBL;
+    const double* b = sB + (kt % GEMM_STAGES) * TILE_DBL;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = frag<AMC>(a, wm + 8 * i + fr, kk + fk);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = frag<BNC>(b, wn + 8 * j + fr, kk + fk);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue: lane holds C[8i + fr][8j + 2fk + {0,1}] of the warp tile
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = row0 + wm + 8 * i + fr;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t c = col0 + wn + 8 * j + 2 * fk;
+      if (splits > 1 || ws != nullptr) {
+        double2* dst = reinterpret_cast<double2*>(ws + ((int64_t)z * M + r) * N + c);
+        *dst = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else {
+        double2* dst = reinterpret_cast<double2*>(C + r * ldc + c);
+        double2 v = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
+        if (beta != 0.0) {
+          const double2 o = *dst;
+          v.x += beta * o.x;
+          v.y += beta * o.y;
+        }
+        *dst = v;
+      }
+    }
+  }
+}
+
+// C = alpha * sum_z ws[z] + beta * C over the tiles in scope (fixed z order: deterministic)
+__global__ void splitk_reduce_kernel(int64_t M, int64_t N, int splits, const double* __restrict__ ws,
+                                     double alpha, double beta, double* __restrict__ C, int64_t ldc,
+                                     int lower_only) {
+  const int64_t total = M * N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / N, c = e % N;
+    if (lower_only && (r / BM) < (c / BN)) continue;
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += ws[(int64_t)z * total + e];
+    double v = alpha * s;
+    if (beta != 0.0) v += beta * C[r * ldc + c];
+    C[r * ldc + c] = v;
+  }
+}
+
+static int ensure_ws(Handle& h, size_t bytes) {
+  if (h.wsA_bytes >= bytes) return ILS_OK;
+  if (h.wsA) cudaFreeAsync(h.wsA, h.stream);
+  h.wsA = nullptr;
+  h.wsA_bytes = 0;
+  cudaError_t e = cudaMallocAsync(&h.wsA, bytes, h.stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(ws)");
+  h.wsA_bytes = bytes;
+  return ILS_OK;
+}
+
+template <bool AMC, bool BNC>
+static int gemm_launch(Handle& h, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                       int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                       bool lower_only, bool tri_k, int splits, bool force_ws) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    ILS_CU(cudaFuncSetAttribute(gemm_dmma_kernel<AMC, BNC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)GEMM_SMEM));
+    attr_set = true;
+  }
+  const int64_t mt = M / BM, nt = N / BN;
+  const int64_t tiles = lower_only ? mt * (mt + 1) / 2 : mt * nt;
+  if (tiles == 0) return ILS_OK;
+  double* ws = nullptr;
+  if (splits > 1 || force_ws) {
+    int r = ensure_ws(h, (size_t)splits * M * N * sizeof(double));
+    if (r) return r;
+    ws = h.wsA;
+  }
+  dim3 grid((unsigned)tiles, 1, (unsigned)splits);
+  gemm_dmma_kernel<AMC, BNC><<<grid, GEMM_THREADS, GEMM_SMEM, h.stream>>>(
+      M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower_only ? 1 : 0, tri_k ? 1 : 0, splits, ws);
+  ILS_LAUNCHED("gemm_dmma_kernel");
+  if (ws) {
+    const int64_t total = M * N;
+    int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)h.num_sms * 8);
+    splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, h.stream>>>(M, N, splits, ws, alpha, beta, C, ldc,
+                                                                 lower_only ? 1 : 0);
+    ILS_LAUNCHED("splitk_reduce_kernel");
+  }
+  return ILS_OK;
+}
+
+int gemm_dmma(Handle& h, bool a_mc, bool b_nc, int64_t M, int64_t N, int64_t K, double alpha,
+              const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+              int64_t ldc, bool lower_only, int splits) {
+  if (a_mc && b_nc)
+    return gemm_launch<true, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower_only, false,
+                                   splits, false);
+  if (a_mc)
+    return gemm_launch<true, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower_only, false,
+                                    splits, false);
+  if (b_nc)
+    return gemm_launch<false, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower_only, false,
+                                    splits, false);
+  return gemm_launch<false, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower_only, false,
+                                   splits, false);
+}
+
+// Split count so that the launch covers the SMs ~2x.
+static int pick_splits(Handle& h, int64_t tiles, int64_t K) {
+  int s = 1;
+  while (tiles * s < 2LL * h.num_sms && K / (BK * (s * 2)) >= 8 && s < 32) s *= 2;
+  return s;
+}
+
+// C[j][i] = C[i][j] for i > j (copy lower -> upper); set C[j][j] = 1 for n_real <= j < n.
+__global__ void mirror_kernel(double* C, int64_t ld, int64_t n, int64_t n_real) {
+  __shared__ double tile[32][33];
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;   // target tile (bi, bj) in upper part: bi < bj
+  if (bi > bj) return;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t i = bj * 32 + r, j = bi * 32 + threadIdx.x;   // source: lower tile (bj, bi)
+    tile[r][threadIdx.x] = C[i * ld + j];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t i = bi * 32 + r, j = bj * 32 + threadIdx.x;
+    if (j > i) C[i * ld + j] = tile[threadIdx.x][r];
+    if (j == i && i >= n_real) C[i * ld + j] = 1.0;
+  }
+}
+
+int mirror_lower(Handle& h, double* C, int64_t ld, int64_t n, int64_t n_real) {
+  dim3 grid((unsigned)(n / 32), (unsigned)(n / 32));
+  mirror_kernel<<<grid, dim3(32, 8), 0, h.stream>>>(C, ld, n, n_real);
+  ILS_LAUNCHED("mirror_kernel");
+  return ILS_OK;
+}
+
+// ---------------------------------------------------------------- 64x64 base: potf2 + trtri
+// Lower-triangle Cholesky of the 64x64 block at (s,s) of L, and its inverse into Z.
+__global__ void __launch_bounds__(256) potf2_trtri_kernel(double* __restrict__ L, double* __restrict__ Z,
+                                                          int64_t ld, int64_t s0, int32_t* err) {
+  extern __shared__ __align__(16) double potf_smem[];
+  double (*a)[65] = reinterpret_cast<double (*)[65]>(potf_smem);
+  double (*zi)[65] = reinterpret_cast<double (*)[65]>(potf_smem + 64 * 65);
+  const int tid = threadIdx.x;
+  double* blk = L + s0 * ld + s0;
+  for (int e = tid; e < 64 * 64; e += 256) {
+    const int i = e >> 6, j = e & 63;
+    a[i][j] = (j <= i) ? blk[i * ld + j] : 0.0;
+  }
+  __syncthreads();
+  __shared__ int bad;
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int k = 0; k < 64; ++k) {
+    if (tid == 0) {
+      const double d = a[k][k];
+      if (!(d > 0.0) || !isfinite(d)) bad = 1;
+      a[k][k] = sqrt(fmax(d, 0.0));
+    }
+    __syncthreads();
+    const double dk = a[k][k];
+    for (int i = k + 1 + tid; i < 64; i += 256) a[i][k] = (dk > 0.0) ? a[i][k] / dk : 0.0;
+    __syncthreads();
+    const int rem = 63 - k;
+    for (int e = tid; e < rem * rem; e += 256) {
+      const int i = k + 1 + e / rem, j = k + 1 + e % rem;
+      if (j <= i) a[i][j] -= a[i][k] * a[j][k];
+    }
+    __syncthreads();
+  }
+  // inverse of the lower-triangular block: column c by thread c (forward substitution)
+  if (tid < 64) {
+    const int c = tid;
+    for (int i = 0; i < c; ++i) zi[i][c] = 0.0;
+    for (int i = c; i < 64; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int k = c; k < i; ++k) s -= a[i][k] * zi[k][c];
+      zi[i][c] = (a[i][i] > 0.0) ? s / a[i][i] : 0.0;
+    }
+  }
+  __syncthreads();
+  double* zb = Z + s0 * ld + s0;
+  for (int e = tid; e < 64 * 64; e += 256) {
+    const int i = e >> 6, j = e & 63;
+    blk[i * ld + j] = a[i][j];   // upper part of a is zero
+    zb[i * ld + j] = zi[i][j];
+  }
+  if (tid == 0 && bad) atomicExch(err, 1);
+}
+
+// Recursive Cholesky + inverse on blocks [s, e) (units of 64).
+static int chol_rec(Handle& h, double* L, double* Z, int64_t ld, int64_t s, int64_t e, double* tmp) {
+  if (e - s == 1) {
+    const int smem = 2 * 64 * 65 * (int)sizeof(double);
+    ILS_CU(cudaFuncSetAttribute(potf2_trtri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    potf2_trtri_kernel<<<1, 256, smem, h.stream>>>(L, Z, ld, s * 64, &h.dstat->flag_err);
+    ILS_LAUNCHED("potf2_trtri_kernel");
+    return ILS_OK;
+  }
+  const int64_t hmid = s + (e - s) / 2;
+  const int64_t n1 = (hmid - s) * 64, n2 = (e - hmid) * 64;
+  double* L21 = L + hmid * 64 * ld + s * 64;
+  double* L22 = L + hmid * 64 * ld + hmid * 64;
+  double* Z11 = Z + s * 64 * ld + s * 64;
+  double* Z21 = Z + hmid * 64 * ld + s * 64;
+  double* Z22 = Z + hmid * 64 * ld + hmid * 64;
+  int r = chol_rec(h, L, Z, ld, s, hmid, tmp);
+  if (r) return r;
+  // L21 = A21 Z11^T  (tmp, then copy back: in-place operands)
+  const int sp1 = pick_splits(h, (n2 / 64) * (n1 / 64), n1);
+  r = gemm_launch<false, false>(h, n2, n1, n1, 1.0, L21, ld, Z11, ld, 0.0, tmp, n1, false, false, sp1,
+                                sp1 > 1);
+  if (r) return r;
+  ILS_CU(cudaMemcpy2DAsync(L21, ld * sizeof(double), tmp, n1 * sizeof(double), n1 * sizeof(double), n2,
+                           cudaMemcpyDeviceToDevice, h.stream));
+  // A22 -= L21 L21^T (lower tiles)
+  const int sp2 = pick_splits(h, (n2 / 64) * (n2 / 64 + 1) / 2, n1);
+  r = gemm_launch<false, false>(h, n2, n2, n1, -1.0, L21, ld, L21, ld, 1.0, L22, ld, true, false, sp2,
+                                false);
+  if (r) return r;
+  r = chol_rec(h, L, Z, ld, hmid, e, tmp);
+  if (r) return r;
+  // Z21 = -Z22 (L21 Z11): T1 = L21 Z11 -> tmp (opB(j,k) = Z11[k][j], N-contiguous)
+  r = gemm_launch<false, true>(h, n2, n1, n1, 1.0, L21, ld, Z11, ld, 0.0, tmp, n1, false, false, sp1,
+                               sp1 > 1);
+  if (r) return r;
+  const int sp3 = pick_splits(h, (n2 / 64) * (n1 / 64), n2);
+  r = gemm_launch<false, true>(h, n2, n1, n2, -1.0, Z22, ld, tmp, n1, 0.0, Z21, ld, false, false, sp3,
+                               false);
+  return r;
+}
+
+int cholesky_inverse(Handle& h, double* L, double* Z, int64_t npad) {
+  ILS_CU(cudaMemsetAsync(Z, 0, (size_t)npad * npad * sizeof(double), h.stream));
+  double* tmp = nullptr;
+  ILS_CU(cudaMallocAsync(&tmp, (size_t)npad * npad * sizeof(double), h.stream));
+  int r = chol_rec(h, L, Z, npad, 0, npad / 64, tmp);
+  cudaFreeAsync(tmp, h.stream);
+  return r;
+}
+
+int build_gram(Handle& h) {
+  if (h.have_gram) return ILS_OK;
+  const int64_t np = h.npad;
+  if (!h.G) ILS_CU(cudaMallocAsync(&h.G, (size_t)np * np * sizeof(double), h.stream));
+  const int64_t tiles = (np / 64) * (np / 64 + 1) / 2;
+  const int sp = pick_splits(h, tiles, h.ppad);
+  int r = gemm_launch<false, false>(h, np, np, h.ppad, 1.0, h.A1T, h.ppad, h.A1T, h.ppad, 0.0, h.G, np,
+                                    true, false, sp, false);
+  if (r) return r;
+  r = mirror_lower(h, h.G, np, np, h.n);
+  if (r) return r;
+  h.have_gram = true;
+  return ILS_OK;
+}
+
+int build_inverse(Handle& h) {
+  if (h.have_P) return ILS_OK;
+  int r = build_gram(h);
+  if (r) return r;
+  const int64_t np = h.npad;
+  const size_t bytes = (size_t)np * np * sizeof(double);
+  if (!h.L) ILS_CU(cudaMallocAsync(&h.L, bytes, h.stream));
+  if (!h.Z) ILS_CU(cudaMallocAsync(&h.Z, bytes, h.stream));
+  if (!h.P) ILS_CU(cudaMallocAsync(&h.P, bytes, h.stream));
+  ILS_CU(cudaMemcpyAsync(h.L, h.G, bytes, cudaMemcpyDeviceToDevice, h.stream));
+  r = cholesky_inverse(h, h.L, h.Z, np);
+  if (r) return r;
+  // P = Z^T Z: opA(i,k) = Z[k][i] (M-contiguous), opB(j,k) = Z[k][j] (N-contiguous); K from max(i,j)
+  const int64_t tiles = (np / 64) * (np / 64 + 1) / 2;
+  const int sp = pick_splits(h, tiles, np / 2);
+  r = gemm_launch<true, true>(h, np, np, np, 1.0, h.Z, np, h.Z, np, 0.0, h.P, np, true, true, sp, false);
+  if (r) return r;
+  r = mirror_lower(h, h.P, np, np, np);
+  if (r) return r;
+  h.have_P = true;
+  return ILS_OK;
+}
+
+}  // namespace ils

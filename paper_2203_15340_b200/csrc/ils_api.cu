@@ -1,0 +1,681 @@
+// ils_api.cu -- the C ABI of libils (include/ils.h): validation, handle, host<->device staging,
+// outer loops and reports. All arithmetic runs in the kernels of this library.
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "ils_internal.h"
+
+namespace ils {
+
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_err = msg; }
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  if (e == cudaErrorMemoryAllocation) return ILS_ERR_NOMEM;
+  return ILS_ERR_CUDA;
+}
+void count_launch(int64_t k) { g_launches += k; }
+
+void hot_account(Handle& h, int c, double work) {
+  float ms = 0.f;
+  cudaEventSynchronize(h.evk1);
+  cudaEventElapsedTime(&ms, h.evk0, h.evk1);
+  h.hot_ms[c] += ms;
+  h.hot_work[c] += work;
+  h.hot_n[c] += 1;
+}
+int64_t launches_now() { return g_launches.load(); }
+
+static bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Device view of a caller buffer: the pointer itself if it is device memory, else a staged copy.
+struct Staged {
+  void* dev = nullptr;
+  bool owned = false;
+  const void* user = nullptr;
+  size_t bytes = 0;
+  cudaStream_t st = nullptr;
+  int in(const void* u, size_t b, cudaStream_t s) {
+    user = u;
+    bytes = b;
+    st = s;
+    if (!u || b == 0) return ILS_OK;
+    if (is_device_ptr(u)) {
+      dev = const_cast<void*>(u);
+      return ILS_OK;
+    }
+    ILS_CU(cudaMallocAsync(&dev, b, s));
+    owned = true;
+    ILS_CU(cudaMemcpyAsync(dev, u, b, cudaMemcpyHostToDevice, s));
+    return ILS_OK;
+  }
+  int out(void* u, size_t b, cudaStream_t s) {   // output buffer (not copied in)
+    user = u;
+    bytes = b;
+    st = s;
+    if (!u || b == 0) return ILS_OK;
+    if (is_device_ptr(u)) {
+      dev = u;
+      return ILS_OK;
+    }
+    ILS_CU(cudaMallocAsync(&dev, b, s));
+    owned = true;
+    return ILS_OK;
+  }
+  int writeback(size_t b) {
+    if (owned && user && b) ILS_CU(cudaMemcpyAsync(const_cast<void*>(user), dev, b, cudaMemcpyDeviceToHost, st));
+    return ILS_OK;
+  }
+  ~Staged() {
+    if (owned && dev) cudaFreeAsync(dev, st);
+  }
+  double* d() const { return static_cast<double*>(dev); }
+};
+
+__global__ void nonfinite_kernel(const double* __restrict__ a, int64_t rows, int64_t cols, int64_t ld,
+                                 int32_t* flag) {
+  int bad = 0;
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const double v = a[(e / cols) * ld + (e % cols)];
+    bad |= !isfinite(v);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(flag, 1);
+}
+
+static int check_finite(Handle& h, const double* a, int64_t rows, int64_t cols, int64_t ld, bool* ok) {
+  ILS_CU(cudaMemsetAsync(&h.dstat->flag_err, 0, sizeof(int32_t), h.stream));
+  if (rows * cols > 0) {
+    nonfinite_kernel<<<h.num_sms * 4, 256, 0, h.stream>>>(a, rows, cols, ld, &h.dstat->flag_err);
+    ILS_LAUNCHED("nonfinite_kernel");
+  }
+  int32_t f = 0;
+  ILS_CU(cudaMemcpyAsync(&f, &h.dstat->flag_err, sizeof(int32_t), cudaMemcpyDeviceToHost, h.stream));
+  ILS_CU(cudaStreamSynchronize(h.stream));
+  *ok = (f == 0);
+  return ILS_OK;
+}
+
+__global__ void dot_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n, double* out) {
+  __shared__ double s[32];
+  double v = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v = fma(a[i], b[i], v);
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    *out = t;
+  }
+}
+
+static int dot_host(Handle& h, const double* a, const double* b, int64_t n, double* res) {
+  double* d = &h.dstat->metric;
+  dot_kernel<<<1, 1024, 0, h.stream>>>(a, b, n, d);
+  ILS_LAUNCHED("dot_kernel");
+  ILS_CU(cudaMemcpyAsync(res, d, sizeof(double), cudaMemcpyDeviceToHost, h.stream));
+  ILS_CU(cudaStreamSynchronize(h.stream));
+  return ILS_OK;
+}
+
+static void free_handle_impl(Handle* h) {
+  if (!h) return;
+  cudaStream_t s = h->stream;
+  double* bufs[] = {h->Arm, h->A1T, h->b, h->N, h->a1tb1, h->ajb, h->G, h->L, h->Z, h->P,
+                    h->part, h->wsA, h->vec, h->red, h->Ab, h->bb};
+  for (double* p : bufs)
+    if (p) cudaFreeAsync(p, s);
+  if (h->S) cudaFreeAsync(h->S, s);
+  if (h->dstat) cudaFreeAsync(h->dstat, s);
+  cudaStreamSynchronize(s);
+  if (h->hstat) cudaFreeHost(h->hstat);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->evk0) cudaEventDestroy(h->evk0);
+  if (h->evk1) cudaEventDestroy(h->evk1);
+}
+
+static float elapsed(Handle& h) {
+  float ms = 0.f;
+  cudaEventSynchronize(h.ev1);
+  cudaEventElapsedTime(&ms, h.ev0, h.ev1);
+  return ms;
+}
+
+}  // namespace ils
+
+using namespace ils;
+
+struct ils_handle_s : public ils::Handle {};
+
+static void free_handle(ils_handle_s* h) {
+  if (!h) return;
+  free_handle_impl(h);
+  delete h;
+}
+
+extern "C" {
+
+void ils_default_opts(ils_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->stop = ILS_STOP_XREF;
+  o->x_ref = nullptr;
+  o->inner_tol = 1e-12;
+  o->max_inner = 100000;
+  o->check_every = 0;
+  o->seed = 0;
+  o->alpha_mode = ILS_ALPHA_UNIFORM;
+  o->alpha_k = 1;
+  o->weighted = 0;
+  o->sp_form = 0;
+}
+
+const char* ils_status_string(int s) {
+  switch (s) {
+    case ILS_OK: return "ok";
+    case ILS_NOT_CONVERGED: return "not converged (iteration cap reached)";
+    case ILS_ERR_ARG: return "invalid argument";
+    case ILS_ERR_SHAPE: return "invalid shape";
+    case ILS_ERR_ZERO_COLUMN: return "A1 has a zero column";
+    case ILS_ERR_NOT_SPD: return "matrix not SPD (condition 1.3 violated)";
+    case ILS_ERR_CUDA: return "CUDA error";
+    case ILS_ERR_NOMEM: return "out of device memory";
+    case ILS_ERR_UNSUPPORTED: return "unsupported option or size";
+    default: return "unknown status";
+  }
+}
+
+const char* ils_last_error(void) { return g_err.c_str(); }
+
+int64_t ils_kernel_launch_count(void) { return launches_now(); }
+
+int ils_create(ils_handle* out, const double* A, const double* b, int64_t p, int64_t q, int64_t n,
+               const ils_ext* ext) {
+  if (!out || !A || !b) {
+    set_error("ils_create: NULL argument");
+    return ILS_ERR_ARG;
+  }
+  *out = nullptr;
+  const int64_t lda = (ext && ext->lda) ? ext->lda : n;
+  const int64_t batch = (ext && ext->batch > 0) ? ext->batch : 1;
+  if (p < 1 || q < 0 || n < 1 || p < n || lda < n) {
+    set_error("ils_create: need p >= 1, q >= 0, n >= 1, p >= n, lda >= n");
+    return ILS_ERR_SHAPE;
+  }
+  if (ext && ext->format != ILS_FORMAT_DENSE) {
+    set_error("ils_create: CSR input is not implemented in this release");
+    return ILS_ERR_UNSUPPORTED;
+  }
+  ils_handle_s* h = new ils_handle_s();
+  h->p = p;
+  h->q = q;
+  h->n = n;
+  h->m = p + q;
+  h->batch = batch;
+  h->stream = ext ? static_cast<cudaStream_t>(ext->stream) : nullptr;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  int rc = ILS_OK;
+  auto fail = [&](int code) {
+    free_handle(h);
+    return code;
+  };
+#define CK(call)                              \
+  do {                                        \
+    rc = (call);                              \
+    if (rc != ILS_OK) return fail(rc);        \
+  } while (0)
+#define CKC(call) CK(((call) == cudaSuccess) ? ILS_OK : cuda_fail(cudaGetLastError(), #call))
+  const cudaStream_t st = h->stream;
+  CKC(cudaMallocAsync(&h->dstat, sizeof(DevStatus), st));
+  CKC(cudaMemsetAsync(h->dstat, 0, sizeof(DevStatus), st));
+  CKC(cudaMallocHost(&h->hstat, sizeof(DevStatus)));
+  CKC(cudaEventCreate(&h->ev0));
+  CKC(cudaEventCreate(&h->ev1));
+  CKC(cudaEventCreate(&h->evk0));
+  CKC(cudaEventCreate(&h->evk1));
+  const int64_t m = h->m;
+  bool ok = true;
+  if (batch > 1) {
+    const size_t abytes = (size_t)batch * m * n * sizeof(double);
+    CKC(cudaMallocAsync(&h->Ab, abytes, st));
+    CKC(cudaMallocAsync(&h->bb, (size_t)batch * m * sizeof(double), st));
+    CKC(cudaMemcpy2DAsync(h->Ab, n * sizeof(double), A, lda * sizeof(double), n * sizeof(double),
+                          (size_t)batch * m, cudaMemcpyDefault, st));
+    CKC(cudaMemcpyAsync(h->bb, b, (size_t)batch * m * sizeof(double), cudaMemcpyDefault, st));
+    CK(check_finite(*h, h->Ab, batch * m, n, n, &ok));
+    if (ok) CK(check_finite(*h, h->bb, batch, m, m, &ok));
+    if (!ok) {
+      set_error("ils_create: non-finite entry in A or b");
+      return fail(ILS_ERR_ARG);
+    }
+    *out = h;
+    return ILS_OK;
+  }
+  h->npad = roundup(n, kPad);
+  h->ppad = roundup(p, kPad);
+  const int64_t np = h->npad;
+  CKC(cudaMallocAsync(&h->Arm, (size_t)(m + 64) * np * sizeof(double), st));
+  CKC(cudaMemsetAsync(h->Arm, 0, (size_t)(m + 64) * np * sizeof(double), st));
+  CKC(cudaMemcpy2DAsync(h->Arm, np * sizeof(double), A, lda * sizeof(double), n * sizeof(double), m,
+                        cudaMemcpyDefault, st));
+  CKC(cudaMallocAsync(&h->b, (size_t)(m + 64) * sizeof(double), st));
+  CKC(cudaMemsetAsync(h->b, 0, (size_t)(m + 64) * sizeof(double), st));
+  CKC(cudaMemcpyAsync(h->b, b, m * sizeof(double), cudaMemcpyDefault, st));
+  CK(check_finite(*h, h->Arm, m, n, np, &ok));
+  if (ok) CK(check_finite(*h, h->b, 1, m, m, &ok));
+  if (!ok) {
+    set_error("ils_create: non-finite entry in A or b");
+    return fail(ILS_ERR_ARG);
+  }
+  CKC(cudaMallocAsync(&h->A1T, (size_t)np * h->ppad * sizeof(double), st));
+  CKC(cudaMemsetAsync(h->A1T, 0, (size_t)np * h->ppad * sizeof(double), st));
+  CK(launch_transpose_a1(*h));
+  CKC(cudaMallocAsync(&h->N, (size_t)n * sizeof(double), st));
+  CKC(cudaMallocAsync(&h->S, (size_t)n * sizeof(uint64_t), st));
+  CK(launch_colnorms(*h));
+  CKC(cudaMemsetAsync(&h->dstat->flag_err, 0, sizeof(int32_t), st));
+  CK(launch_weights(*h, &h->dstat->flag_err));
+  CKC(cudaMallocAsync(&h->a1tb1, (size_t)np * sizeof(double), st));
+  CK(launch_gemv_rows(h->A1T, h->ppad, np, p, h->b, h->a1tb1, 1.0, nullptr, st));
+  h->part_rows = h->num_sms > 16 ? h->num_sms : 16;
+  CKC(cudaMallocAsync(&h->part, (size_t)h->part_rows * np * sizeof(double), st));
+  CKC(cudaMallocAsync(&h->red, (size_t)h->part_rows * 4 * sizeof(double), st));
+  CKC(cudaMallocAsync(&h->vec, (size_t)8 * np * sizeof(double), st));
+  CKC(cudaMemsetAsync(h->vec, 0, (size_t)8 * np * sizeof(double), st));
+  int32_t zf = 0;
+  CKC(cudaMemcpyAsync(&zf, &h->dstat->flag_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CKC(cudaStreamSynchronize(st));
+  if (zf) {
+    set_error("ils_create: A1 has a zero column");
+    return fail(ILS_ERR_ZERO_COLUMN);
+  }
+#undef CK
+#undef CKC
+  *out = h;
+  return ILS_OK;
+}
+
+void ils_destroy(ils_handle h) { free_handle(h); }
+
+// method: 0 SP, 1 SP-RK-RGS, 2 SP-SCD/RCD
+static int solve_common(ils_handle h, int method, const double* x0, double* x, double tol, int64_t max_iter,
+                        const ils_opts* opts_in, ils_report* rep) {
+  if (!h || !x) {
+    set_error("solve: NULL handle or x");
+    return ILS_ERR_ARG;
+  }
+  ils_opts o;
+  if (opts_in) o = *opts_in; else ils_default_opts(&o);
+  if (max_iter < 0 || o.max_inner < 0 || o.inner_tol < 0 || !(tol >= 0)) {
+    set_error("solve: negative cap or tolerance");
+    return ILS_ERR_ARG;
+  }
+  if (o.stop == ILS_STOP_XREF && !o.x_ref) {
+    set_error("solve: ILS_STOP_XREF needs opts->x_ref");
+    return ILS_ERR_ARG;
+  }
+  if (o.stop < 0 || o.stop > 2 || (o.alpha_mode == ILS_ALPHA_FIXED && o.alpha_k < 1)) {
+    set_error("solve: bad option");
+    return ILS_ERR_ARG;
+  }
+  Handle& H = *h;
+  const cudaStream_t st = H.stream;
+  const int64_t n = H.n, B = H.batch;
+  const int64_t l0 = launches_now();
+  for (int c = 0; c < 4; ++c) {
+    H.hot_ms[c] = 0.0;
+    H.hot_work[c] = 0.0;
+    H.hot_n[c] = 0;
+  }
+  int rc = ILS_OK;
+  if (rep) {
+    int64_t* ii = rep->inst_iters;
+    int32_t* is = rep->inst_status;
+    std::memset(rep, 0, sizeof(*rep));
+    rep->inst_iters = ii;
+    rep->inst_status = is;
+  }
+  Staged sx0, sx, sxr;
+  if ((rc = sx0.in(x0, (size_t)B * n * sizeof(double), st))) return rc;
+  if ((rc = sx.out(x, (size_t)B * n * sizeof(double), st))) return rc;
+  if ((rc = sxr.in(o.x_ref, (size_t)B * n * sizeof(double), st))) return rc;
+
+  if (B > 1) {
+    if (o.stop == ILS_STOP_RR) {
+      set_error("batched: ILS_STOP_RR not supported");
+      return ILS_ERR_UNSUPPORTED;
+    }
+    ils_opts od = o;
+    od.x_ref = sxr.d();
+    int64_t* it_dev = nullptr;
+    int32_t* st_dev = nullptr;
+    ILS_CU(cudaMallocAsync(&it_dev, B * sizeof(int64_t), st));
+    ILS_CU(cudaMallocAsync(&st_dev, B * sizeof(int32_t), st));
+    ILS_CU(cudaMemsetAsync(H.dstat, 0, sizeof(DevStatus), st));
+    ILS_CU(cudaEventRecord(H.ev0, st));
+    rc = batched_solve(H, method, sx0.d(), sx.d(), tol, max_iter, od, it_dev, st_dev);
+    ILS_CU(cudaEventRecord(H.ev1, st));
+    if (rc) return rc;
+    std::vector<int64_t> its(B);
+    std::vector<int32_t> sts(B);
+    ILS_CU(cudaMemcpyAsync(its.data(), it_dev, B * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    ILS_CU(cudaMemcpyAsync(sts.data(), st_dev, B * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    ILS_CU(cudaMemcpyAsync(H.hstat, H.dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+    if ((rc = sx.writeback((size_t)B * n * sizeof(double)))) return rc;
+    ILS_CU(cudaStreamSynchronize(st));
+    cudaFreeAsync(it_dev, st);
+    cudaFreeAsync(st_dev, st);
+    int64_t mx = 0;
+    bool all = true;
+    for (int64_t i = 0; i < B; ++i) {
+      mx = its[i] > mx ? its[i] : mx;
+      all = all && sts[i];
+    }
+    if (rep) {
+      rep->outer_iters = mx;
+      rep->inner_iters_total = H.hstat->inner_steps;
+      rep->converged = all ? 1 : 0;
+      rep->solve_ms = elapsed(H);
+      rep->kernel_launches = launches_now() - l0;
+      if (rep->inst_iters) std::memcpy(rep->inst_iters, its.data(), B * sizeof(int64_t));
+      if (rep->inst_status) std::memcpy(rep->inst_status, sts.data(), B * sizeof(int32_t));
+      const double m = (double)H.m;
+      rep->bytes_touched = (double)B * mx * 8.0 * (double)H.q * (n + 1);
+      (void)m;
+    }
+    return all ? ILS_OK : ILS_NOT_CONVERGED;
+  }
+
+  const int64_t np = H.npad;
+  // ---- setup (timed separately)
+  ILS_CU(cudaMemsetAsync(&H.dstat->flag_err, 0, sizeof(int32_t), st));
+  const bool gram_new = !H.have_gram && method != 1, inv_new = !H.have_P && method == 0;
+  ILS_CU(cudaEventRecord(H.ev0, st));
+  if (method == 0) rc = build_inverse(H);
+  else if (method == 2) rc = build_gram(H);
+  ILS_CU(cudaEventRecord(H.ev1, st));
+  if (rc) return rc;
+  const float setup_ms = elapsed(H);
+  if (gram_new || inv_new) {
+    const double nd = (double)H.n, pd = (double)H.p;
+    H.hot_ms[3] += setup_ms;
+    H.hot_work[3] += (gram_new ? 2.0 * pd * nd * nd : 0.0) + (inv_new ? nd * nd * nd : 0.0);
+    H.hot_n[3] += 1;
+  }
+  {
+    int32_t f = 0;
+    ILS_CU(cudaMemcpy(&f, &H.dstat->flag_err, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (f) {
+      set_error("Cholesky of A1^T A1 broke down");
+      return ILS_ERR_NOT_SPD;
+    }
+  }
+  // RR denominator ||A^T J b||^2
+  double ajb2 = 0.0;
+  double* g = H.vec + 5 * np;
+  if (o.stop == ILS_STOP_RR) {
+    double* zero = H.vec + 4 * np;
+    ILS_CU(cudaMemsetAsync(zero, 0, np * sizeof(double), st));
+    if ((rc = full_residual(H, zero, g))) return rc;
+    if ((rc = dot_host(H, g, g, n, &ajb2))) return rc;
+    if (ajb2 == 0.0) {
+      set_error("A^T J b = 0: RR undefined");
+      return ILS_ERR_ARG;
+    }
+  }
+  Staged shist;
+  const size_t hist_bytes = (size_t)max_iter * n * sizeof(double);
+  if (o.x_hist && (rc = shist.out(o.x_hist, hist_bytes, st))) return rc;
+
+  ILS_CU(cudaEventRecord(H.ev0, st));
+  int64_t outer = 0, inner_total = 0;
+  double metric = NAN;
+  int conv = 0;
+  double* xk = H.vec + 6 * np;   // current iterate (device, npad)
+  double* bhat = H.vec + 3 * np;
+  double* xnew = H.vec + 7 * np;
+  ILS_CU(cudaMemsetAsync(xk, 0, np * sizeof(double), st));
+  if (sx0.d()) ILS_CU(cudaMemcpyAsync(xk, sx0.d(), n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  std::vector<int64_t> inner_hist;
+
+  if (method == 0 && o.stop != ILS_STOP_RR) {
+    // whole SP loop in one persistent cooperative launch
+    const int stop = (o.stop == ILS_STOP_XREF) ? ILS_STOP_XREF : ILS_STOP_NONE;
+    if (max_iter > 0) {
+      if ((rc = sp_run(H, xk, xnew, tol, max_iter, stop, sxr.d(), o.sp_form, shist.d(), false, nullptr, &outer,
+                       &metric, &conv)))
+        return rc;
+      ILS_CU(cudaMemcpyAsync(xk, xnew, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+  } else {
+    for (int64_t k = 0; k < max_iter; ++k) {
+      int64_t steps = 0;
+      if (method == 0) {   // SP under the RR rule: one persistent step at a time
+        int64_t one = 0;
+        double mm;
+        int cc;
+        if ((rc = sp_run(H, xk, xnew, 0.0, 1, ILS_STOP_NONE, nullptr, o.sp_form, nullptr, false, nullptr, &one,
+                         &mm, &cc)))
+          return rc;
+      } else {
+        // b_hat = A2bar x_k + A^T J b (K1 stream, rhs_only)
+        if ((rc = sp_run(H, xk, nullptr, 0.0, 1, ILS_STOP_NONE, nullptr, 0, nullptr, true, bhat, nullptr, nullptr,
+                         nullptr)))
+          return rc;
+        if (method == 1)
+          rc = rk_rgs_inner(H, bhat, xnew, o.seed, k, o.max_inner, o.check_every, o.inner_tol, &steps);
+        else
+          rc = scd_inner(H, bhat, xnew, o.seed, k, o.max_inner, o.check_every, o.inner_tol, o.alpha_mode, o.alpha_k,
+                         o.weighted, &steps);
+        if (rc) return rc;
+      }
+      ILS_CU(cudaMemcpyAsync(xk, xnew, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      if (shist.d())
+        ILS_CU(cudaMemcpyAsync(shist.d() + k * n, xk, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      inner_total += steps;
+      inner_hist.push_back(steps);
+      outer = k + 1;
+      bool done = false;
+      if (o.stop == ILS_STOP_XREF) {
+        if ((rc = stop_metric(H, xk, sxr.d(), &H.dstat->metric))) return rc;
+        ILS_CU(cudaMemcpyAsync(&metric, &H.dstat->metric, sizeof(double), cudaMemcpyDeviceToHost, st));
+        ILS_CU(cudaStreamSynchronize(st));
+        done = metric <= tol;
+      } else if (o.stop == ILS_STOP_RR) {
+        if ((rc = full_residual(H, xk, g))) return rc;
+        double gg = 0.0;
+        if ((rc = dot_host(H, g, g, n, &gg))) return rc;
+        metric = gg / ajb2;
+        done = metric < tol;
+      }
+      if (done) {
+        conv = 1;
+        break;
+      }
+    }
+  }
+  ILS_CU(cudaEventRecord(H.ev1, st));
+  const float solve_ms = elapsed(H);
+  ILS_CU(cudaMemcpyAsync(sx.d(), xk, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if ((rc = sx.writeback(n * sizeof(double)))) return rc;
+  if (shist.d() && (rc = shist.writeback((size_t)outer * n * sizeof(double)))) return rc;
+  ILS_CU(cudaStreamSynchronize(st));
+  if (o.inner_hist)
+    for (size_t i = 0; i < inner_hist.size(); ++i) o.inner_hist[i] = inner_hist[i];
+  if (rep) {
+    rep->outer_iters = outer;
+    rep->inner_iters_total = inner_total;
+    rep->converged = conv;
+    rep->final_metric = metric;
+    rep->setup_ms = setup_ms;
+    rep->solve_ms = solve_ms;
+    const double q = (double)H.q, p = (double)H.p, nd = (double)n;
+    if (method == 0)
+      rep->bytes_touched = outer * (8.0 * q * (nd + 1) + 8.0 * nd * nd);
+    else if (method == 1)
+      rep->bytes_touched = outer * 8.0 * q * (nd + 1) + inner_total * 16.0 * p;
+    else
+      rep->bytes_touched = outer * 8.0 * q * (nd + 1) + inner_total * 8.0 * nd;
+    rep->kernel_launches = launches_now() - l0;
+    for (int c = 0; c < 4; ++c) {
+      rep->hot_ms[c] = H.hot_ms[c];
+      rep->hot_work[c] = H.hot_work[c];
+      rep->hot_launches[c] = H.hot_n[c];
+    }
+  }
+  return conv ? ILS_OK : ILS_NOT_CONVERGED;
+}
+
+int ils_sp_solve(ils_handle h, const double* x0, double* x, double tol, int64_t max_iter, const ils_opts* opts,
+                 ils_report* rep) {
+  return solve_common(h, 0, x0, x, tol, max_iter, opts, rep);
+}
+
+int ils_rk_solve(ils_handle h, const double* x0, double* x, double tol, int64_t max_iter, const ils_opts* opts,
+                 ils_report* rep) {
+  return solve_common(h, 1, x0, x, tol, max_iter, opts, rep);
+}
+
+int ils_rgs_solve(ils_handle h, const double* x0, double* x, double tol, int64_t max_iter, const ils_opts* opts,
+                  ils_report* rep) {
+  return solve_common(h, 2, x0, x, tol, max_iter, opts, rep);
+}
+
+int ils_direct_solve(ils_handle h, double* x) {
+  if (!h || !x) return ILS_ERR_ARG;
+  Handle& H = *h;
+  if (H.batch > 1) return ILS_ERR_UNSUPPORTED;
+  const cudaStream_t st = H.stream;
+  const int64_t np = H.npad, n = H.n;
+  int rc = build_gram(H);
+  if (rc) return rc;
+  const size_t bytes = (size_t)np * np * sizeof(double);
+  double *M = nullptr, *Zm = nullptr;
+  ILS_CU(cudaMallocAsync(&M, bytes, st));
+  ILS_CU(cudaMallocAsync(&Zm, bytes, st));
+  ILS_CU(cudaMemcpyAsync(M, H.G, bytes, cudaMemcpyDeviceToDevice, st));
+  // M -= A2^T A2 : opA(i,k) = A2[k][i] (M-contiguous), opB(j,k) = A2[k][j] (N-contiguous)
+  const int64_t kq = roundup(H.q, 32);
+  if (H.q > 0) {
+    rc = gemm_dmma(H, true, true, np, np, kq, -1.0, H.Arm + H.p * np, np, H.Arm + H.p * np, np, 1.0, M, np, true, 1);
+    if (!rc) rc = mirror_lower(H, M, np, np, n);
+  }
+  ILS_CU(cudaMemsetAsync(&H.dstat->flag_err, 0, sizeof(int32_t), st));
+  if (!rc) rc = cholesky_inverse(H, M, Zm, np);
+  // rhs = A^T J b = A1^T b1 - A2^T b2 ; x = Z^T (Z rhs)
+  double* rhs = H.vec + 4 * np;
+  double* y = H.vec + 5 * np;
+  double* xd = H.vec + 6 * np;
+  if (!rc) rc = launch_gemv_cols(H.Arm + H.p * np, np, H.q, np, H.b + H.p, rhs, -1.0, H.a1tb1, st);
+  if (!rc) rc = launch_gemv_rows(Zm, np, np, np, rhs, y, 1.0, nullptr, st);
+  if (!rc) rc = launch_gemv_cols(Zm, np, np, np, y, xd, 1.0, nullptr, st);
+  int32_t f = 0;
+  if (!rc) {
+    Staged sx;
+    if ((rc = sx.out(x, n * sizeof(double), st)) == ILS_OK) {
+      ILS_CU(cudaMemcpyAsync(sx.d(), xd, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      rc = sx.writeback(n * sizeof(double));
+      ILS_CU(cudaMemcpyAsync(&f, &H.dstat->flag_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      ILS_CU(cudaStreamSynchronize(st));
+    }
+  }
+  cudaFreeAsync(M, st);
+  cudaFreeAsync(Zm, st);
+  cudaStreamSynchronize(st);
+  if (rc) return rc;
+  if (f) {
+    set_error("A^T J A is not SPD (condition 1.3)");
+    return ILS_ERR_NOT_SPD;
+  }
+  return ILS_OK;
+}
+
+int ils_relative_residual(ils_handle h, const double* x, double* rr) {
+  if (!h || !x || !rr) return ILS_ERR_ARG;
+  Handle& H = *h;
+  if (H.batch > 1) return ILS_ERR_UNSUPPORTED;
+  const cudaStream_t st = H.stream;
+  const int64_t np = H.npad, n = H.n;
+  Staged sx;
+  int rc = sx.in(x, n * sizeof(double), st);
+  if (rc) return rc;
+  double* xz = H.vec + 4 * np;
+  double* g = H.vec + 5 * np;
+  ILS_CU(cudaMemsetAsync(xz, 0, np * sizeof(double), st));
+  if ((rc = full_residual(H, xz, g))) return rc;
+  double den = 0.0, num = 0.0;
+  if ((rc = dot_host(H, g, g, n, &den))) return rc;
+  if (den == 0.0) {
+    set_error("A^T J b = 0: RR undefined");
+    return ILS_ERR_ARG;
+  }
+  ILS_CU(cudaMemcpyAsync(xz, sx.d(), n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if ((rc = full_residual(H, xz, g))) return rc;
+  if ((rc = dot_host(H, g, g, n, &num))) return rc;
+  *rr = num / den;
+  return ILS_OK;
+}
+
+int ils_get_sampling_tables(ils_handle h, double* N, uint64_t* S) {
+  if (!h) return ILS_ERR_ARG;
+  Handle& H = *h;
+  if (H.batch > 1) return ILS_ERR_UNSUPPORTED;
+  if (N) ILS_CU(cudaMemcpyAsync(N, H.N, H.n * sizeof(double), cudaMemcpyDefault, H.stream));
+  if (S) ILS_CU(cudaMemcpyAsync(S, H.S, H.n * sizeof(uint64_t), cudaMemcpyDefault, H.stream));
+  ILS_CU(cudaStreamSynchronize(H.stream));
+  return ILS_OK;
+}
+
+int ils_rk_indices(ils_handle h, uint64_t seed, int64_t k, int64_t t0, int64_t count, int32_t* j1, int32_t* j2) {
+  if (!h || !j1 || !j2 || count < 0) return ILS_ERR_ARG;
+  Handle& H = *h;
+  if (H.batch > 1) return ILS_ERR_UNSUPPORTED;
+  Staged s1, s2;
+  int rc;
+  if ((rc = s1.out(j1, count * sizeof(int32_t), H.stream))) return rc;
+  if ((rc = s2.out(j2, count * sizeof(int32_t), H.stream))) return rc;
+  if (count > 0 && (rc = rk_indices(H, seed, k, t0, count, static_cast<int32_t*>(s1.dev), static_cast<int32_t*>(s2.dev))))
+    return rc;
+  if ((rc = s1.writeback(count * sizeof(int32_t)))) return rc;
+  if ((rc = s2.writeback(count * sizeof(int32_t)))) return rc;
+  ILS_CU(cudaStreamSynchronize(H.stream));
+  return ILS_OK;
+}
+
+int ils_scd_subset(int64_t n, uint64_t seed, int64_t k, int64_t t, int32_t alpha_mode, int32_t alpha_k,
+                   int32_t* alpha, uint8_t* mask) {
+  if (n < 1 || !alpha || !mask) return ILS_ERR_ARG;
+  cudaStream_t st = nullptr;
+  Staged sa, sm;
+  int rc;
+  if ((rc = sa.out(alpha, sizeof(int32_t), st))) return rc;
+  if ((rc = sm.out(mask, n, st))) return rc;
+  if ((rc = scd_subset_mask(n, seed, k, t, alpha_mode, alpha_k, static_cast<int32_t*>(sa.dev),
+                            static_cast<uint8_t*>(sm.dev), st)))
+    return rc;
+  if ((rc = sa.writeback(sizeof(int32_t)))) return rc;
+  if ((rc = sm.writeback(n))) return rc;
+  ILS_CU(cudaStreamSynchronize(st));
+  return ILS_OK;
+}
+
+}  // extern "C"

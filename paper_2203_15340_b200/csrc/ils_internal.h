@@ -1,0 +1,139 @@
+// ils_internal.h -- host-side internals of libils (handle layout, launchers).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/ils.h"
+
+namespace ils {
+
+constexpr int kPad = 64;  // all dense dimensions padded to multiples of 64
+
+inline int64_t roundup(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// Device-side scalars written by kernels and read back once per call.
+struct DevStatus {
+  int32_t flag_stop;       // outer stop decided
+  int32_t flag_err;        // Cholesky breakdown etc.
+  int64_t iters;           // outer iterations done
+  double metric;           // last stop metric
+  int64_t inner_steps;     // inner steps of the last inner solve
+  int32_t inner_conv;      // inner solve met its tolerance
+  int32_t pad_;
+};
+
+struct Handle {
+  int64_t p = 0, q = 0, n = 0, m = 0, batch = 1;
+  int64_t npad = 0, ppad = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+
+  // dense single-instance layouts
+  double* Arm = nullptr;    // (m + 64) x npad row-major, zero padded  [A1; A2]
+  double* A1T = nullptr;    // npad x ppad: row j = column j of A1 (column-major A1)
+  double* b = nullptr;      // m (+64 zero tail)
+  double* N = nullptr;      // n column norms ||A1_(j)||^2 (sequential order)
+  uint64_t* S = nullptr;    // n weight prefix sums
+  double* a1tb1 = nullptr;  // npad  A1^T b1
+  double* ajb = nullptr;    // npad  A^T J b (lazy)
+
+  // lazy SP / SCD precompute
+  double* G = nullptr;      // npad x npad  A1^T A1 (full symmetric, identity padding)
+  double* L = nullptr;      // npad x npad  Cholesky workspace
+  double* Z = nullptr;      // npad x npad  L^{-1} (lower, zero upper)
+  double* P = nullptr;      // npad x npad  (A1^T A1)^{-1}
+  bool have_gram = false, have_P = false;
+
+  // workspace
+  double* part = nullptr;   // partial sums [grid][npad]
+  int64_t part_rows = 0;
+  double* wsA = nullptr;    // GEMM split-K workspace
+  size_t wsA_bytes = 0;
+  double* vec = nullptr;    // 8 x npad scratch vectors
+  double* red = nullptr;    // reduction scratch [grid * 4]
+  DevStatus* dstat = nullptr;
+  DevStatus* hstat = nullptr;  // pinned host mirror
+
+  // batched layout
+  double* Ab = nullptr;     // [batch][m][n]
+  double* bb = nullptr;     // [batch][m]
+
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t evk0 = nullptr, evk1 = nullptr;   // per-launch timing of the hot kernels
+  double hot_ms[4] = {0, 0, 0, 0};
+  double hot_work[4] = {0, 0, 0, 0};
+  int64_t hot_n[4] = {0, 0, 0, 0};
+};
+
+// Accumulate the device time between h.evk0 and h.evk1 (already recorded) into class c.
+void hot_account(Handle& h, int c, double work);
+
+// error plumbing
+void set_error(const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+void count_launch(int64_t k = 1);
+int64_t launches_now();
+
+#define ILS_CU(call)                                       \
+  do {                                                     \
+    cudaError_t e_ = (call);                               \
+    if (e_ != cudaSuccess) return ::ils::cuda_fail(e_, #call); \
+  } while (0)
+
+#define ILS_LAUNCHED(what)                                         \
+  do {                                                             \
+    ::ils::count_launch();                                         \
+    cudaError_t e_ = cudaGetLastError();                           \
+    if (e_ != cudaSuccess) return ::ils::cuda_fail(e_, what);      \
+  } while (0)
+
+// ---- launchers (each returns ILS_OK or a negative status) ----
+// ingest.cu
+int launch_transpose_a1(Handle& h);
+int launch_colnorms(Handle& h);
+int launch_weights(Handle& h, int32_t* d_zero_flag);
+int launch_gemv_rows(const double* X, int64_t ldx, int64_t rows, int64_t cols, const double* v,
+                     double* y, double alpha, const double* yadd, cudaStream_t st);
+int launch_gemv_cols(const double* X, int64_t ldx, int64_t rows, int64_t cols, const double* v,
+                     double* y, double alpha, const double* yadd, cudaStream_t st);
+
+// dla.cu (dense linear algebra on DMMA)
+// C[MxN] = alpha * sum_k opA(i,k) opB(j,k) + beta*C ; opA(i,k)=A[i*lda+k] (a_mc=0) or A[k*lda+i] (a_mc=1)
+//                                                    opB(j,k)=B[j*ldb+k] (b_nc=0) or B[k*ldb+j] (b_nc=1)
+int gemm_dmma(Handle& h, bool a_mc, bool b_nc, int64_t M, int64_t N, int64_t K, double alpha,
+              const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+              int64_t ldc, bool lower_only, int splits);
+int mirror_lower(Handle& h, double* C, int64_t ld, int64_t n, int64_t n_real);
+// Cholesky of the lower triangle of L (npad x npad) in place, Z = L^{-1}. flag_err set on breakdown.
+int cholesky_inverse(Handle& h, double* L, double* Z, int64_t npad);
+int build_gram(Handle& h);      // G = A1^T A1
+int build_inverse(Handle& h);   // L, Z, P from G
+
+// sp.cu
+int sp_run(Handle& h, const double* x0_dev, double* x_dev, double tol, int64_t max_iter, int stop,
+           const double* xref_dev, int sp_form, double* x_hist_dev, bool rhs_only, double* rhs_out,
+           int64_t* iters_out, double* metric_out, int* conv_out);
+int full_residual(Handle& h, const double* x_dev, double* g_out);  // g = A^T J (b - A x)
+
+// rk_rgs.cu
+int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_t k, int64_t max_inner,
+                 int64_t check_every, double inner_tol, int64_t* steps_out);
+int rk_indices(Handle& h, uint64_t seed, int64_t k, int64_t t0, int64_t count, int32_t* j1, int32_t* j2);
+
+// scd.cu
+int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_t k, int64_t max_inner,
+              int64_t check_every, double inner_tol, int alpha_mode, int alpha_k, int weighted,
+              int64_t* steps_out);
+int scd_subset_mask(int64_t n, uint64_t seed, int64_t k, int64_t t, int alpha_mode, int alpha_k,
+                    int32_t* alpha_dev, uint8_t* mask_dev, cudaStream_t st);
+
+// small vector kernels (sp.cu)
+int stop_metric(Handle& h, const double* x, const double* xref, double* out_dev);
+
+// batched.cu
+int batched_solve(Handle& h, int method, const double* x0, double* x, double tol, int64_t max_iter,
+                  const ils_opts& o, int64_t* inst_iters_dev, int32_t* inst_status_dev);
+
+}  // namespace ils

@@ -1,0 +1,173 @@
+// ingest.cu -- K0: layout and sampling tables built once per handle (ils_create).
+//
+//   A1T  = column-major copy of A1 (RK/RGS read columns of A1)
+//   N_j  = ||A1_(j)||_2^2 summed sequentially in i (include/ils.h "Index stream")
+//   S_j  = prefix sums of W_j = max(1, floor(N_j / N_max * 2^32)) (PAPER.md:297 probabilities)
+//   A1^T b1 (Alg. 2 step 3 / Alg. 5 step 2)
+#include "common.cuh"
+#include "ils_internal.h"
+
+namespace ils {
+
+// A1T[j][i] = Arm[i][j], tile 32x32 through shared memory (coalesced both sides).
+__global__ void transpose_a1_kernel(const double* __restrict__ Arm, int64_t npad, int64_t p,
+                                    double* __restrict__ A1T, int64_t ppad) {
+  __shared__ double tile[32][33];
+  const int64_t j0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t i = i0 + r, j = j0 + threadIdx.x;
+    tile[r][threadIdx.x] = (i < p) ? Arm[i * npad + j] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t j = j0 + r, i = i0 + threadIdx.x;
+    if (i < ppad) A1T[j * ppad + i] = tile[threadIdx.x][r];
+  }
+}
+
+int launch_transpose_a1(Handle& h) {
+  dim3 grid((unsigned)(h.npad / 32), (unsigned)((h.ppad + 31) / 32));
+  transpose_a1_kernel<<<grid, dim3(32, 8), 0, h.stream>>>(h.Arm, h.npad, h.p, h.A1T, h.ppad);
+  ILS_LAUNCHED("transpose_a1_kernel");
+  return ILS_OK;
+}
+
+// N_j = (((0 + a_0j^2) + a_1j^2) + ...) with every square rounded (no FMA contraction).
+__global__ void colnorms_kernel(const double* __restrict__ Arm, int64_t npad, int64_t p, int64_t n,
+                                double* __restrict__ N) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double s = 0.0;
+  int64_t i = 0;
+  for (; i + 8 <= p; i += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(Arm + (i + u) * npad + j);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = __dadd_rn(s, __dmul_rn(v[u], v[u]));
+  }
+  for (; i < p; ++i) {
+    const double v = __ldg(Arm + i * npad + j);
+    s = __dadd_rn(s, __dmul_rn(v, v));
+  }
+  N[j] = s;
+}
+
+int launch_colnorms(Handle& h) {
+  const int bs = 128;
+  colnorms_kernel<<<(unsigned)((h.n + bs - 1) / bs), bs, 0, h.stream>>>(h.Arm, h.npad, h.p, h.n, h.N);
+  ILS_LAUNCHED("colnorms_kernel");
+  return ILS_OK;
+}
+
+// One block: N_max, W_j, zero-column flag, inclusive uint64 scan S.
+__global__ void __launch_bounds__(1024) weights_kernel(const double* __restrict__ N, int n,
+                                                       uint64_t* __restrict__ S, int32_t* zero_flag) {
+  __shared__ double smax[32];
+  __shared__ uint64_t ssum[32];
+  __shared__ uint64_t sbase[1024];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double mx = 0.0;
+  int bad = 0;
+  for (int j = tid; j < n; j += nt) {
+    const double v = N[j];
+    mx = fmax(mx, v);
+    bad |= (v <= 0.0);
+  }
+  bad = __syncthreads_or(bad);
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((tid & 31) == 0) smax[tid >> 5] = mx;
+  __syncthreads();
+  if (tid < 32) {
+    double v = (tid < (nt >> 5)) ? smax[tid] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (tid == 0) smax[0] = v;
+  }
+  __syncthreads();
+  const double nmax = smax[0];
+  if (bad) {
+    if (tid == 0) *zero_flag = 1;
+    return;
+  }
+  // contiguous chunk per thread
+  const int per = (n + nt - 1) / nt;
+  const int j0 = tid * per, j1 = min(n, j0 + per);
+  uint64_t local = 0;
+  for (int j = j0; j < j1; ++j) {
+    const double r = __ddiv_rn(N[j], nmax);
+    uint64_t w = (uint64_t)floor(scalbn(r, 32));
+    local += (w < 1 ? 1 : w);
+  }
+  sbase[tid] = local;
+  __syncthreads();
+  // exclusive scan of sbase (simple Hillis-Steele over 1024 entries, integer exact)
+  for (int off = 1; off < nt; off <<= 1) {
+    const uint64_t add = (tid >= off) ? sbase[tid - off] : 0;
+    __syncthreads();
+    sbase[tid] += add;
+    __syncthreads();
+  }
+  uint64_t run = sbase[tid] - local;
+  for (int j = j0; j < j1; ++j) {
+    const double r = __ddiv_rn(N[j], nmax);
+    uint64_t w = (uint64_t)floor(scalbn(r, 32));
+    run += (w < 1 ? 1 : w);
+    S[j] = run;
+  }
+  (void)ssum;
+}
+
+int launch_weights(Handle& h, int32_t* d_zero_flag) {
+  weights_kernel<<<1, 1024, 0, h.stream>>>(h.N, (int)h.n, h.S, d_zero_flag);
+  ILS_LAUNCHED("weights_kernel");
+  return ILS_OK;
+}
+
+// y[i] = alpha * sum_j X[i*ldx + j] v[j] (+ yadd[i]); one warp per row, fixed-order reduction.
+__global__ void gemv_rows_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows, int64_t cols,
+                                 const double* __restrict__ v, double* __restrict__ y, double alpha,
+                                 const double* __restrict__ yadd) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < rows; i += nw) {
+    const double* xr = X + i * ldx;
+    double s = 0.0;
+    for (int64_t j = lane; j < cols; j += 32) s = fma(xr[j], v[j], s);
+    s = warp_sum(s);
+    if (lane == 0) y[i] = alpha * s + (yadd ? yadd[i] : 0.0);
+  }
+}
+
+int launch_gemv_rows(const double* X, int64_t ldx, int64_t rows, int64_t cols, const double* v, double* y,
+                     double alpha, const double* yadd, cudaStream_t st) {
+  if (rows <= 0) return ILS_OK;
+  const int bs = 256;
+  int64_t blocks = (rows * 32 + bs - 1) / bs;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  gemv_rows_kernel<<<(unsigned)blocks, bs, 0, st>>>(X, ldx, rows, cols, v, y, alpha, yadd);
+  ILS_LAUNCHED("gemv_rows_kernel");
+  return ILS_OK;
+}
+
+// y[j] = alpha * sum_i X[i*ldx + j] v[i] (+ yadd[j]); thread per column, sequential in i.
+__global__ void gemv_cols_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows, int64_t cols,
+                                 const double* __restrict__ v, double* __restrict__ y, double alpha,
+                                 const double* __restrict__ yadd) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  double s = 0.0;
+  for (int64_t i = 0; i < rows; ++i) s = fma(X[i * ldx + j], v[i], s);
+  y[j] = alpha * s + (yadd ? yadd[j] : 0.0);
+}
+
+int launch_gemv_cols(const double* X, int64_t ldx, int64_t rows, int64_t cols, const double* v, double* y,
+                     double alpha, const double* yadd, cudaStream_t st) {
+  if (cols <= 0) return ILS_OK;
+  const int bs = 128;
+  gemv_cols_kernel<<<(unsigned)((cols + bs - 1) / bs), bs, 0, st>>>(X, ldx, rows, cols, v, y, alpha, yadd);
+  ILS_LAUNCHED("gemv_cols_kernel");
+  return ILS_OK;
+}
+
+}  // namespace ils

@@ -1,0 +1,360 @@
+// sp.cu -- K1 (fused outer right-hand-side stream) and the persistent SP solver (Alg. 1).
+//
+// One cooperative launch runs the whole SP iteration (Eq. Sec23 :126):
+//   phase A  K1: each CTA streams its share of rows a_i of A2 (paper form) or of all of A
+//            (correction form / residual) from HBM through a TMA bulk-copy ring in shared
+//            memory; the row is staged ONCE and used twice: d_i = a_i^T x - b_i (block
+//            reduction) then acc += sigma_i d_i a_i (register accumulators).
+//   phase B  c = base + sum_cta partial_cta   (fixed CTA order: deterministic)
+//            paper form: c_k = A1^T b1 + A2^T (A2 x_k - b2) = A2bar x_k + A^T J b (Alg. 2 step 5)
+//   phase C  x_{k+1} = P c_k (paper form) or x_k + P g_k (correction form, reading R14)
+//   phase D  stop test ||x_{k+1} - x_ref|| <= tol ||x_ref|| evaluated redundantly by every CTA.
+// rhs_only: phases A+B for one x (b_hat for SP-RK-RGS / SP-SCD, or g = A^T J (b - A x) for RR).
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "ils_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace ils {
+
+constexpr int SP_THREADS = 512;
+constexpr int SP_WARPS = SP_THREADS / 32;
+constexpr int SP_RMAX = 16;                 // rows per ring stage (max)
+constexpr int SP_STAGE_TARGET = 32768;      // bytes per ring stage (target)
+
+struct SpParams {
+  const double* Arm;
+  const double* b;
+  int64_t npad, n;
+  int64_t row_begin, row_end, p;
+  const double* base;     // added in phase B (A1^T b1) or nullptr
+  const double* P;
+  double* xa;
+  double* xb;
+  const double* xref;
+  double* part;           // [grid][npad]
+  double* cvec;           // [npad]
+  double* red;            // [grid][2]
+  double* x_hist;         // [max_iter][n] or nullptr
+  double tol;
+  int64_t max_iter;
+  int stop, sp_form, rhs_only;
+  int rows_per_stage, nstages;
+  DevStatus* st;
+};
+
+template <int NPAIR>
+__global__ void __launch_bounds__(SP_THREADS, 1) sp_persistent_kernel(SpParams prm) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = gridDim.x, bid = blockIdx.x;
+  const int64_t npad = prm.npad, np2 = npad / 2;
+  const int R = prm.rows_per_stage, NS = prm.nstages;
+  const int64_t stage_dbl = (int64_t)R * npad;
+  double* ring = reinterpret_cast<double*>(smem_raw);
+  double* reds = ring + NS * stage_dbl;                       // [2][SP_WARPS][SP_RMAX]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reds + 2 * SP_WARPS * SP_RMAX);
+  __shared__ double cta_red[SP_WARPS][2];
+
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // this CTA's rows
+  const int64_t rows = prm.row_end - prm.row_begin;
+  const int64_t per = (rows + G - 1) / G;
+  const int64_t r0 = prm.row_begin + (int64_t)bid * per;
+  const int64_t r1 = (r0 + per < prm.row_end) ? r0 + per : prm.row_end;
+  const int64_t myrows = (r1 > r0) ? r1 - r0 : 0;
+  const int64_t nst = (myrows + R - 1) / R;
+  int64_t gstage = 0;   // running stage counter (mbarrier parity bookkeeping)
+
+  double* xcur = prm.xa;
+  double* xnext = prm.xb;
+  const int64_t iters = prm.rhs_only ? 1 : prm.max_iter;
+  for (int64_t k = 0; k < iters; ++k) {
+    // ---------------- phase A: fused row stream
+    double2 xr[NPAIR], acc[NPAIR];
+#pragma unroll
+    for (int u = 0; u < NPAIR; ++u) {
+      const int64_t c = tid + (int64_t)u * SP_THREADS;
+      xr[u] = (c < np2) ? reinterpret_cast<const double2*>(xcur)[c] : make_double2(0.0, 0.0);
+      acc[u] = make_double2(0.0, 0.0);
+    }
+    auto issue = [&](int64_t s) {   // stage s of this iteration -> slot (gstage + s) % NS
+      const int64_t g = gstage + s;
+      const int slot = (int)(g % NS);
+      const int64_t rs = r0 + s * R;
+      const int64_t nr = (rs + R <= r1) ? R : (r1 - rs);
+      const uint32_t bytes = (uint32_t)(nr * npad * sizeof(double));
+      mbar_arrive_expect_tx(&bars[slot], bytes);
+      bulk_g2s(ring + slot * stage_dbl, prm.Arm + rs * npad, bytes, &bars[slot]);
+    };
+    if (tid == 0) {
+      fence_proxy_async();   // order earlier generic smem accesses (cs) before async-proxy writes
+      for (int64_t s = 0; s < nst && s < NS; ++s) issue(s);
+    }
+    for (int64_t s = 0; s < nst; ++s) {
+      const int64_t g = gstage + s;
+      const int slot = (int)(g % NS);
+      const int64_t rs = r0 + s * R;
+      const int nr = (int)((rs + R <= r1) ? R : (r1 - rs));
+      mbar_wait(&bars[slot], (uint32_t)((g / NS) & 1));
+      const double* st = ring + slot * stage_dbl;
+      double* red = reds + (g & 1) * SP_WARPS * SP_RMAX;
+      for (int rr = 0; rr < nr; ++rr) {
+        const double2* row = reinterpret_cast<const double2*>(st + rr * npad);
+        double d = 0.0;
+#pragma unroll
+        for (int u = 0; u < NPAIR; ++u) {
+          const int64_t c = tid + (int64_t)u * SP_THREADS;
+          if (c < np2) {
+            const double2 v = row[c];
+            d = fma(v.x, xr[u].x, d);
+            d = fma(v.y, xr[u].y, d);
+          }
+        }
+        d = warp_sum(d);
+        if (lane == 0) red[warp * SP_RMAX + rr] = d;
+      }
+      __syncthreads();   // B1: stage s partials visible; every thread finished stage s-1
+      if (tid == 0 && s >= 1 && (s - 1) + NS < nst) issue(s - 1 + NS);
+      for (int rr = 0; rr < nr; ++rr) {
+        double d = 0.0;
+#pragma unroll
+        for (int w = 0; w < SP_WARPS; ++w) d += red[w * SP_RMAX + rr];
+        const int64_t i = rs + rr;
+        d -= prm.b[i];
+        if (i < prm.p) d = -d;          // sigma_i = -1 on A1 rows (correction form only)
+        const double2* row = reinterpret_cast<const double2*>(st + rr * npad);
+#pragma unroll
+        for (int u = 0; u < NPAIR; ++u) {
+          const int64_t c = tid + (int64_t)u * SP_THREADS;
+          if (c < np2) {
+            const double2 v = row[c];
+            acc[u].x = fma(d, v.x, acc[u].x);
+            acc[u].y = fma(d, v.y, acc[u].y);
+          }
+        }
+      }
+    }
+    gstage += nst;
+    {
+      double2* pp = reinterpret_cast<double2*>(prm.part + (int64_t)bid * npad);
+#pragma unroll
+      for (int u = 0; u < NPAIR; ++u) {
+        const int64_t c = tid + (int64_t)u * SP_THREADS;
+        if (c < np2) pp[c] = acc[u];
+      }
+    }
+    grid.sync();
+    // ---------------- phase B: c = base + sum_cta part (fixed order)
+    for (int64_t j = (int64_t)bid * SP_THREADS + tid; j < npad; j += (int64_t)G * SP_THREADS) {
+      double s = prm.base ? prm.base[j] : 0.0;
+      for (int c = 0; c < G; ++c) s += prm.part[(int64_t)c * npad + j];
+      prm.cvec[j] = s;
+    }
+    if (prm.rhs_only) break;
+    grid.sync();
+    // ---------------- phase C: x_{k+1} = P c (+ x_k), stop partials
+    double* cs = ring;   // ring is idle here
+    for (int64_t j = tid; j < npad; j += SP_THREADS) cs[j] = prm.cvec[j];
+    __syncthreads();
+    double e2 = 0.0, r2 = 0.0;
+    for (int64_t i = (int64_t)bid * SP_WARPS + warp; i < npad; i += (int64_t)G * SP_WARPS) {
+      const double2* pr = reinterpret_cast<const double2*>(prm.P + i * npad);
+      double s = 0.0;
+      for (int64_t c = lane; c < np2; c += 32) {
+        const double2 v = pr[c];
+        s = fma(v.x, cs[2 * c], s);
+        s = fma(v.y, cs[2 * c + 1], s);
+      }
+      s = warp_sum(s);
+      if (i >= prm.n) s = 0.0;
+      const double xn = prm.sp_form ? xcur[i] + s : s;
+      if (lane == 0) {
+        xnext[i] = xn;
+        if (i < prm.n) {
+          if (prm.x_hist) prm.x_hist[k * prm.n + i] = xn;
+          if (prm.xref) {
+            const double e = xn - prm.xref[i];
+            e2 = fma(e, e, e2);
+            r2 = fma(prm.xref[i], prm.xref[i], r2);
+          }
+        }
+      }
+    }
+    if (lane == 0) {
+      cta_red[warp][0] = e2;
+      cta_red[warp][1] = r2;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double a = 0.0, b = 0.0;
+      for (int w = 0; w < SP_WARPS; ++w) {
+        a += cta_red[w][0];
+        b += cta_red[w][1];
+      }
+      prm.red[2 * bid] = a;
+      prm.red[2 * bid + 1] = b;
+    }
+    grid.sync();
+    // ---------------- phase D: stop decision (identical in every CTA)
+    double E = 0.0, Rr = 0.0;
+    for (int c = 0; c < G; ++c) {
+      E += prm.red[2 * c];
+      Rr += prm.red[2 * c + 1];
+    }
+    const double metric = (prm.xref && Rr > 0.0) ? sqrt(E) / sqrt(Rr) : __longlong_as_double(0x7ff8000000000000LL);
+    const bool done = (prm.stop == ILS_STOP_XREF) && prm.xref && (metric <= prm.tol);
+    if (bid == 0 && tid == 0) {
+      prm.st->iters = k + 1;
+      prm.st->metric = metric;
+      prm.st->flag_stop = done ? 1 : 0;
+    }
+    double* t = xcur;
+    xcur = xnext;
+    xnext = t;
+    if (done) break;
+    __syncthreads();   // cs (ring) reads done before the next phase-A TMA overwrites it
+  }
+}
+
+// ||x - xref|| / ||xref|| (single block, fixed order) -> st->metric
+__global__ void stop_metric_kernel(const double* __restrict__ x, const double* __restrict__ xref, int64_t n,
+                                   double* out) {
+  __shared__ double s1[32], s2[32];
+  double a = 0.0, b = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double e = x[i] - xref[i];
+    a = fma(e, e, a);
+    b = fma(xref[i], xref[i], b);
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if ((threadIdx.x & 31) == 0) {
+    s1[threadIdx.x >> 5] = a;
+    s2[threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double A = 0.0, B = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      A += s1[w];
+      B += s2[w];
+    }
+    *out = sqrt(A) / sqrt(B);
+  }
+}
+
+int stop_metric(Handle& h, const double* x, const double* xref, double* out_dev) {
+  stop_metric_kernel<<<1, 1024, 0, h.stream>>>(x, xref, h.n, out_dev);
+  ILS_LAUNCHED("stop_metric_kernel");
+  return ILS_OK;
+}
+
+template <int NPAIR>
+static int launch_sp(Handle& h, SpParams& prm, size_t smem) {
+  ILS_CU(cudaFuncSetAttribute(sp_persistent_kernel<NPAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem));
+  void* args[] = {&prm};
+  ILS_CU(cudaLaunchCooperativeKernel((void*)sp_persistent_kernel<NPAIR>, dim3(h.num_sms),
+                                     dim3(SP_THREADS), args, smem, h.stream));
+  ILS_LAUNCHED("sp_persistent_kernel");
+  return ILS_OK;
+}
+
+int sp_run(Handle& h, const double* x0_dev, double* x_dev, double tol, int64_t max_iter, int stop,
+           const double* xref_dev, int sp_form, double* x_hist_dev, bool rhs_only, double* rhs_out,
+           int64_t* iters_out, double* metric_out, int* conv_out) {
+  const int64_t npad = h.npad;
+  if (npad > 8192) {
+    set_error("dense n > 8192 is not supported by the SP stream kernel in this release");
+    return ILS_ERR_UNSUPPORTED;
+  }
+  if (!rhs_only) {
+    int r = build_inverse(h);
+    if (r) return r;
+  }
+  double* xa = h.vec;
+  double* xb = h.vec + npad;
+  double* cvec = h.vec + 2 * npad;
+  ILS_CU(cudaMemsetAsync(xa, 0, 2 * npad * sizeof(double), h.stream));
+  if (x0_dev) ILS_CU(cudaMemcpyAsync(xa, x0_dev, h.n * sizeof(double), cudaMemcpyDeviceToDevice, h.stream));
+
+  SpParams prm{};
+  prm.Arm = h.Arm;
+  prm.b = h.b;
+  prm.npad = npad;
+  prm.n = h.n;
+  const bool full = (sp_form == 1);
+  prm.row_begin = full ? 0 : h.p;
+  prm.row_end = h.m;
+  prm.p = full ? h.p : 0;          // sigma = -1 only on A1 rows of the full stream
+  prm.base = full ? nullptr : h.a1tb1;
+  prm.P = h.P;
+  prm.xa = xa;
+  prm.xb = xb;
+  prm.xref = xref_dev;
+  prm.part = h.part;
+  prm.cvec = cvec;
+  prm.red = h.red;
+  prm.x_hist = x_hist_dev;
+  prm.tol = tol;
+  prm.max_iter = max_iter;
+  prm.stop = stop;
+  prm.sp_form = sp_form;
+  prm.rhs_only = rhs_only ? 1 : 0;
+  const int64_t rowbytes = npad * (int64_t)sizeof(double);
+  int R = (int)(SP_STAGE_TARGET / rowbytes);
+  if (R < 1) R = 1;
+  if (R > SP_RMAX) R = SP_RMAX;
+  const int64_t stage_bytes = R * rowbytes;
+  int NS = (int)((200 * 1024) / stage_bytes);
+  if (NS > 4) NS = 4;
+  if (NS < 2) NS = 2;
+  prm.rows_per_stage = R;
+  prm.nstages = NS;
+  prm.st = h.dstat;
+  size_t smem = (size_t)NS * stage_bytes + 2 * SP_WARPS * SP_RMAX * sizeof(double) + NS * sizeof(uint64_t);
+  if ((size_t)npad * sizeof(double) > (size_t)NS * stage_bytes) return ILS_ERR_UNSUPPORTED;
+  ILS_CU(cudaMemsetAsync(h.dstat, 0, sizeof(DevStatus), h.stream));
+  const int64_t np2 = npad / 2;
+  int r;
+  ILS_CU(cudaEventRecord(h.evk0, h.stream));
+  if (np2 <= SP_THREADS) r = launch_sp<1>(h, prm, smem);
+  else if (np2 <= 2 * SP_THREADS) r = launch_sp<2>(h, prm, smem);
+  else if (np2 <= 4 * SP_THREADS) r = launch_sp<4>(h, prm, smem);
+  else r = launch_sp<8>(h, prm, smem);
+  if (r) return r;
+  ILS_CU(cudaEventRecord(h.evk1, h.stream));
+  const double rows = (double)(prm.row_end - prm.row_begin), nd = (double)h.n;
+  if (rhs_only) {
+    hot_account(h, 0, 8.0 * rows * (nd + 1.0));
+    if (rhs_out) ILS_CU(cudaMemcpyAsync(rhs_out, cvec, npad * sizeof(double), cudaMemcpyDeviceToDevice, h.stream));
+    return ILS_OK;
+  }
+  ILS_CU(cudaMemcpyAsync(h.hstat, h.dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, h.stream));
+  ILS_CU(cudaStreamSynchronize(h.stream));
+  const int64_t it = h.hstat->iters;
+  hot_account(h, 0, (double)it * (8.0 * rows * (nd + 1.0) + 8.0 * nd * nd));
+  const double* xfin = (it % 2 == 1) ? xb : xa;
+  if (x_dev) ILS_CU(cudaMemcpyAsync(x_dev, xfin, h.n * sizeof(double), cudaMemcpyDeviceToDevice, h.stream));
+  if (iters_out) *iters_out = it;
+  if (metric_out) *metric_out = h.hstat->metric;
+  if (conv_out) *conv_out = h.hstat->flag_stop;
+  return ILS_OK;
+}
+
+// g = A^T J (b - A x) over all m rows (sigma = -1 on A1 rows): correction-form residual.
+int full_residual(Handle& h, const double* x_dev, double* g_out) {
+  return sp_run(h, x_dev, nullptr, 0.0, 1, ILS_STOP_NONE, nullptr, 1, nullptr, true, g_out, nullptr,
+                nullptr, nullptr);
+}
+
+}  // namespace ils

@@ -1,0 +1,201 @@
+"""Thin ctypes binding of libils.so (include/ils.h). Argument marshalling only: every step of
+the method runs in the CUDA kernels of libils. Arrays may be numpy arrays (host memory) or
+torch tensors (host or CUDA); their data pointers are passed straight through.
+
+The binding fails loudly if the library is missing: there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libils.so")
+
+ILS_OK, ILS_NOT_CONVERGED = 0, 1
+ILS_ERR_ARG, ILS_ERR_SHAPE, ILS_ERR_ZERO_COLUMN, ILS_ERR_NOT_SPD = -1, -2, -3, -4
+ILS_ERR_CUDA, ILS_ERR_NOMEM, ILS_ERR_UNSUPPORTED = -5, -6, -7
+ILS_STOP_XREF, ILS_STOP_RR, ILS_STOP_NONE = 0, 1, 2
+ILS_FORMAT_DENSE, ILS_FORMAT_CSR = 0, 1
+ILS_ALPHA_UNIFORM, ILS_ALPHA_FIXED = 0, 1
+
+EXPORTED = [
+    "ils_default_opts", "ils_status_string", "ils_last_error", "ils_create", "ils_sp_solve",
+    "ils_rk_solve", "ils_rgs_solve", "ils_destroy", "ils_direct_solve", "ils_relative_residual",
+    "ils_get_sampling_tables", "ils_rk_indices", "ils_scd_subset", "ils_kernel_launch_count",
+]
+
+
+class IlsExt(C.Structure):
+    _fields_ = [("format", C.c_int32), ("batch", C.c_int64), ("lda", C.c_int64), ("stream", C.c_void_p)]
+
+
+class IlsOpts(C.Structure):
+    _fields_ = [("stop", C.c_int32), ("x_ref", C.c_void_p), ("inner_tol", C.c_double),
+                ("max_inner", C.c_int64), ("check_every", C.c_int64), ("seed", C.c_uint64),
+                ("alpha_mode", C.c_int32), ("alpha_k", C.c_int32), ("weighted", C.c_int32),
+                ("sp_form", C.c_int32), ("x_hist", C.c_void_p), ("inner_hist", C.c_void_p)]
+
+
+class IlsReport(C.Structure):
+    _fields_ = [("outer_iters", C.c_int64), ("inner_iters_total", C.c_int64), ("converged", C.c_int32),
+                ("final_metric", C.c_double), ("setup_ms", C.c_double), ("solve_ms", C.c_double),
+                ("bytes_touched", C.c_double), ("kernel_launches", C.c_int64),
+                ("hot_ms", C.c_double * 4), ("hot_work", C.c_double * 4), ("hot_launches", C.c_int64 * 4),
+                ("inst_iters", C.c_void_p), ("inst_status", C.c_void_p)]
+
+    def as_dict(self):
+        d = {}
+        for k, _ in self._fields_:
+            if k in ("inst_iters", "inst_status"):
+                continue
+            v = getattr(self, k)
+            d[k] = list(v) if k.startswith("hot_") else v
+        return d
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libils.so. Raises (loudly) if it is missing -- there is no fallback path."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libils.so not built ({path}); run python -m paper_2203_15340_b200.build "
+                          "or __graft_entry__.build()")
+    lib = C.CDLL(path)
+    vp, i64, i32, dbl, u64 = C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_uint64
+    sig = {
+        "ils_default_opts": (None, [C.POINTER(IlsOpts)]),
+        "ils_status_string": (C.c_char_p, [C.c_int]),
+        "ils_last_error": (C.c_char_p, []),
+        "ils_create": (C.c_int, [C.POINTER(vp), vp, vp, i64, i64, i64, C.POINTER(IlsExt)]),
+        "ils_sp_solve": (C.c_int, [vp, vp, vp, dbl, i64, C.POINTER(IlsOpts), C.POINTER(IlsReport)]),
+        "ils_rk_solve": (C.c_int, [vp, vp, vp, dbl, i64, C.POINTER(IlsOpts), C.POINTER(IlsReport)]),
+        "ils_rgs_solve": (C.c_int, [vp, vp, vp, dbl, i64, C.POINTER(IlsOpts), C.POINTER(IlsReport)]),
+        "ils_destroy": (None, [vp]),
+        "ils_direct_solve": (C.c_int, [vp, vp]),
+        "ils_relative_residual": (C.c_int, [vp, vp, C.POINTER(C.c_double)]),
+        "ils_get_sampling_tables": (C.c_int, [vp, vp, vp]),
+        "ils_rk_indices": (C.c_int, [vp, u64, i64, i64, i64, vp, vp]),
+        "ils_scd_subset": (C.c_int, [i64, u64, i64, i64, i32, i32, vp, vp]),
+        "ils_kernel_launch_count": (C.c_int64, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _ptr(a):
+    """Raw data pointer of a numpy array or torch tensor (None -> NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("arrays must be C-contiguous")
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensors must be contiguous")
+        return a.data_ptr()
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+class IlsError(RuntimeError):
+    def __init__(self, status, where):
+        lib = load_library()
+        msg = lib.ils_status_string(status).decode()
+        detail = lib.ils_last_error().decode()
+        super().__init__(f"{where}: {msg} ({status}) {detail}")
+        self.status = status
+
+
+def _check(status, where):
+    if status < 0:
+        raise IlsError(status, where)
+    return status
+
+
+def ils_default_opts(**kw) -> IlsOpts:
+    o = IlsOpts()
+    load_library().ils_default_opts(C.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def ils_create(A, b, p: int, q: int, n: int, batch: int = 1, lda: int = 0, stream=None):
+    """ils_create(A, b, p, q, n, ext): A row-major (m x n) or [batch][m][n] fp64, b (m) or [batch][m]."""
+    lib = load_library()
+    h = C.c_void_p()
+    ext = IlsExt(ILS_FORMAT_DENSE, batch, lda, stream)
+    _check(lib.ils_create(C.byref(h), _ptr(A), _ptr(b), p, q, n, C.byref(ext)), "ils_create")
+    return h
+
+
+def ils_destroy(h):
+    load_library().ils_destroy(h)
+
+
+def _solve(fn, name, h, x0, x, tol, max_iter, opts, inst_iters=None, inst_status=None):
+    rep = IlsReport()
+    rep.inst_iters = _ptr(inst_iters)
+    rep.inst_status = _ptr(inst_status)
+    o = opts if opts is not None else ils_default_opts()
+    st = _check(fn(h, _ptr(x0), _ptr(x), float(tol), int(max_iter), C.byref(o), C.byref(rep)), name)
+    return st, rep
+
+
+def ils_sp_solve(h, x0, x, tol, max_iter, opts=None, **kw):
+    return _solve(load_library().ils_sp_solve, "ils_sp_solve", h, x0, x, tol, max_iter, opts, **kw)
+
+
+def ils_rk_solve(h, x0, x, tol, max_iter, opts=None, **kw):
+    return _solve(load_library().ils_rk_solve, "ils_rk_solve", h, x0, x, tol, max_iter, opts, **kw)
+
+
+def ils_rgs_solve(h, x0, x, tol, max_iter, opts=None, **kw):
+    return _solve(load_library().ils_rgs_solve, "ils_rgs_solve", h, x0, x, tol, max_iter, opts, **kw)
+
+
+def ils_direct_solve(h, x):
+    return _check(load_library().ils_direct_solve(h, _ptr(x)), "ils_direct_solve")
+
+
+def ils_relative_residual(h, x) -> float:
+    rr = C.c_double()
+    _check(load_library().ils_relative_residual(h, _ptr(x), C.byref(rr)), "ils_relative_residual")
+    return rr.value
+
+
+def ils_get_sampling_tables(h, n: int):
+    N = np.zeros(n)
+    S = np.zeros(n, dtype=np.uint64)
+    _check(load_library().ils_get_sampling_tables(h, _ptr(N), _ptr(S)), "ils_get_sampling_tables")
+    return N, S
+
+
+def ils_rk_indices(h, seed: int, k: int, t0: int, count: int):
+    j1 = np.zeros(count, dtype=np.int32)
+    j2 = np.zeros(count, dtype=np.int32)
+    _check(load_library().ils_rk_indices(h, seed, k, t0, count, _ptr(j1), _ptr(j2)), "ils_rk_indices")
+    return j1, j2
+
+
+def ils_scd_subset(n: int, seed: int, k: int, t: int, alpha_mode: int = 0, alpha_k: int = 1):
+    alpha = np.zeros(1, dtype=np.int32)
+    mask = np.zeros(n, dtype=np.uint8)
+    _check(load_library().ils_scd_subset(n, seed, k, t, alpha_mode, alpha_k, _ptr(alpha), _ptr(mask)),
+           "ils_scd_subset")
+    return int(alpha[0]), mask
+
+
+def ils_kernel_launch_count() -> int:
+    return int(load_library().ils_kernel_launch_count())
