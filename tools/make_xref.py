@@ -1,0 +1,44 @@
+"""Write the reference solutions x_ref of the inconsistent workloads (c1) with the ORACLE.
+
+x_ref solves A^T J A x = A^T J b (Eq. Sec12) by the oracle's fp64 Cholesky of
+M = A1^T A1 - A2^T A2 (BASELINE.json configs[1]: "reference solution from the oracle's fp64
+Cholesky of A^T J A"). Calls only oracle/ and workloads/. Output: workloads/xref/<cfg>_seed<s>.npy
+plus a .json with the data fingerprint, so bench.py (GPU leg) can use x_ref without running the
+oracle itself.
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from oracle import ils_oracle as O  # noqa: E402
+from workloads import fingerprint, make_problem  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--seed", type=int, default=0)
+    a = ap.parse_args()
+    pr = make_problem(a.config, seed=a.seed)
+    x = O.direct_solve(pr.A1, pr.A2, pr.b1, pr.b2)
+    out = os.path.join(ROOT, "workloads", "xref")
+    os.makedirs(out, exist_ok=True)
+    base = os.path.join(out, f"{a.config}_seed{a.seed}")
+    np.save(base + ".npy", x)
+    meta = {"config": a.config, "seed": a.seed, "n": int(pr.n), "fingerprint": fingerprint(pr.A, pr.b),
+            "rho": O.spectral_radius_sp(pr.A1, pr.A2),
+            "err_xstar": float(np.linalg.norm(x - pr.xstar) / np.linalg.norm(pr.xstar)),
+            "writer": "tools/make_xref.py (oracle.ils_oracle.direct_solve)"}
+    with open(base + ".json", "w") as f:
+        json.dump(meta, f, indent=1)
+    print(meta)
+
+
+if __name__ == "__main__":
+    main()

@@ -11,4 +11,5 @@ from .configs import (  # noqa: F401
     make_batched,
     make_dense,
     make_ill_conditioned,
+    fingerprint,
 )

@@ -10,6 +10,7 @@ and the problem dimensions only.
 """
 from __future__ import annotations
 
+import hashlib
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -178,3 +179,13 @@ def make_problem(name: str, seed: int = 0, **overrides):
         return make_batched(cfg["batch"], cfg["p"], cfg["q"], cfg["n"], cfg["a2_scale"],
                             base_seed=seed, tol=cfg["tol"])
     raise NotImplementedError(f"workload kind {kind!r} not generated yet")
+
+
+def fingerprint(A: np.ndarray, b: np.ndarray) -> str:
+    """SHA-256 over the first/last 64 rows of A and the head of b: ties a stored x_ref file
+    (workloads/xref/, written by tools/make_xref.py from the oracle) to the generated data."""
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(A[:64]).tobytes())
+    h.update(np.ascontiguousarray(A[-64:]).tobytes())
+    h.update(np.ascontiguousarray(b[:64]).tobytes())
+    return h.hexdigest()
