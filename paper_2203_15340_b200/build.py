@@ -23,17 +23,22 @@ def build(verbose: bool = False, force: bool = False) -> str:
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(d) <= t for d in deps):
             return LIB
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(s):
+        o = os.path.join(LIB_DIR, os.path.basename(s).replace(".cu", ".o"))
+        r = subprocess.run([NVCC, *FLAGS, "-c", s, "-o", o], capture_output=True, text=True)
+        return s, o, r
+
     objs = []
     logs = []
-    for s in srcs:
-        o = os.path.join(LIB_DIR, os.path.basename(s).replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-dc" if False else "-c", s, "-o", o]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        logs.append(r.stdout + r.stderr)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError(f"nvcc failed on {s}")
-        objs.append(o)
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 1)) as ex:
+        for s, o, r in ex.map(compile_one, srcs):
+            logs.append(r.stdout + r.stderr)
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"nvcc failed on {s}")
+            objs.append(o)
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
            "-Xcompiler", "-fPIC", *objs, "-o", LIB]
     r = subprocess.run(cmd, capture_output=True, text=True)

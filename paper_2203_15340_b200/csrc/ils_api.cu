@@ -138,7 +138,7 @@ static void free_handle_impl(Handle* h) {
   if (!h) return;
   cudaStream_t s = h->stream;
   double* bufs[] = {h->Arm, h->A1T, h->b, h->N, h->a1tb1, h->ajb, h->G, h->L, h->Z, h->P,
-                    h->part, h->wsA, h->vec, h->red, h->Ab, h->bb};
+                    h->part, h->wsA, h->vec, h->red, h->Ab, h->bb, h->rk_state};
   for (double* p : bufs)
     if (p) cudaFreeAsync(p, s);
   if (h->S) cudaFreeAsync(h->S, s);

@@ -52,6 +52,7 @@ struct Handle {
   double* wsA = nullptr;    // GEMM split-K workspace
   size_t wsA_bytes = 0;
   double* vec = nullptr;    // 8 x npad scratch vectors
+  double* rk_state = nullptr;  // SP-RK-RGS chunk state: w, r, az [ppad] each, z [npad]
   double* red = nullptr;    // reduction scratch [grid * 4]
   DevStatus* dstat = nullptr;
   DevStatus* hstat = nullptr;  // pinned host mirror
@@ -116,6 +117,9 @@ int sp_run(Handle& h, const double* x0_dev, double* x_dev, double tol, int64_t m
            const double* xref_dev, int sp_form, double* x_hist_dev, bool rhs_only, double* rhs_out,
            int64_t* iters_out, double* metric_out, int* conv_out);
 int full_residual(Handle& h, const double* x_dev, double* g_out);  // g = A^T J (b - A x)
+// SP-RK-RGS inner check (full grid): az = A1 z, g = A1^T az - b_hat, stop flag / r = w - az
+int rk_check(Handle& h, const double* z, const double* bhat, const double* w, double* r, double* az,
+             double inner_tol, int64_t t_now);
 
 // rk_rgs.cu
 int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_t k, int64_t max_inner,

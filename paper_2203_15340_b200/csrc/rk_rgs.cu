@@ -6,47 +6,52 @@
 //   s2 = <a_j2, r> / N_j2                          RGS on A1 z = w       (step 11)
 //      = (<a_j2, r_old> + s1 <a_j2, a_j1>) / N_j2  -> the three dots share ONE reduction
 //   z_j2 += s2 ; r -= s2 a_j2
-// The p-vectors w, r live in registers, split over a thread-block cluster of C CTAs (row
-// slices); the two column slices per step are TMA-prefetched NS steps ahead (the index stream
-// is data-independent), the per-step reduction is warp shuffles + one CTA barrier + a DSMEM
-// all-to-all of 3 doubles + one cluster barrier. z is replicated in every CTA's shared memory.
-// Every check_every steps the inner stop rule of include/ils.h runs in-kernel.
+// rk_rgs_kernel runs the steps [t0, t1) between two inner checks: the p-vectors w, r live in
+// registers, split over a thread-block cluster of C CTAs (row slices); the two column slices per
+// step are TMA-prefetched NS steps ahead (the index stream is data-independent). Per step: warp
+// shuffles, one named barrier, then a one-hop DSMEM all-to-all (st.async + mbarrier complete_tx,
+// no cluster-wide barrier) of the CTA partials; every CTA sums the C partials in the same fixed
+// order. z is replicated in every CTA's smem. The inner stop check (include/ils.h) runs between
+// chunks as a full-GPU fused row stream (rk_check in sp.cu: az = A1 z, g = A1^T az - b_hat, reset
+// r = w - az); w, r, z pass through HBM between chunks.
 #include "common.cuh"
 #include "ils_internal.h"
 
 namespace ils {
 
-constexpr int RK_THREADS = 256;
-constexpr int RK_WARPS = RK_THREADS / 32;
-constexpr int RK_RING = 128;   // index ring entries
+constexpr int RK_MAXW = 16;      // warps per CTA (max)
+constexpr int RK_RING = 128;     // index ring entries
+constexpr int RK_AHEAD = 64;     // ring fill distance (steps)
 constexpr int RK_MAXC = 16;
 
 struct RkIdx {
   int32_t j1, j2;
-  double bh1, n1, n2;
+  double bh1, rn1, rn2;          // b_hat_{j1}, 1/N_{j1}, 1/N_{j2}
 };
 
 struct RkParams {
-  const double* A1T;
+  const double* A1T;   // npad x ppad (column j of A1 contiguous)
   int64_t ppad, npad;
   int n;
   const double* N;
   const uint64_t* S;
   const double* bhat;
-  double* z_out;
+  double* W;           // [ppad] state w (in/out)
+  double* Rv;          // [ppad] state r = w - A1 z (in/out)
+  double* Z;           // [npad] state z (in/out)
   uint64_t seed;
   uint32_t k;
-  int64_t max_inner, check_every;
-  double inner_tol;
-  double* gpart;       // [C][npad]
+  int64_t t0, t1, max_inner;
   DevStatus* st;
-  int C, slice, nslots;
+  int C, slice, slicepad, nslots;
 };
 
+// Ring entries for steps t0 .. t0+31 (one per lane): Philox draw, two weighted inverse-CDF
+// samples on the shared prefix sums, and the scalars the step needs (off the critical path).
 __device__ __forceinline__ void rk_fill_indices(const RkParams& p, const uint64_t* Ss, RkIdx* ring,
                                                 int64_t t0, int lane) {
   const int64_t t = t0 + lane;
-  if (t < p.max_inner) {
+  if (t < p.t1) {
     const U4 x = draw(p.seed, p.k, (uint64_t)t, kTagRkRgs);
     const int j1 = sample_weighted(((uint64_t)x.y << 32) | x.x, Ss, p.n);
     const int j2 = sample_weighted(((uint64_t)x.w << 32) | x.z, Ss, p.n);
@@ -54,247 +59,229 @@ __device__ __forceinline__ void rk_fill_indices(const RkParams& p, const uint64_
     e.j1 = j1;
     e.j2 = j2;
     e.bh1 = p.bhat[j1];
-    e.n1 = p.N[j1];
-    e.n2 = p.N[j2];
+    e.rn1 = 1.0 / p.N[j1];
+    e.rn2 = 1.0 / p.N[j2];
     ring[t & (RK_RING - 1)] = e;
   }
 }
 
-template <int U, bool CLUSTER>
-__global__ void __launch_bounds__(RK_THREADS, 1) rk_rgs_kernel(RkParams p) {
+// CC = cluster size (1: single CTA), U = rows per thread. blockDim.x = 32 * NW threads; thread
+// tid owns rows tid + u * blockDim.x (u < U) of this CTA's row slice. Slot columns are padded to
+// slicepad = U * blockDim.x doubles (zero tail written once), so the row loops carry no bounds.
+template <int CC, int U>
+__global__ void __launch_bounds__(512, 1) rk_rgs_kernel(RkParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int C = p.C;
-  const int rank = CLUSTER ? (int)cluster_ctarank() : 0;
+  const int NT = blockDim.x, NW = NT >> 5;
+  const int rank = (CC > 1) ? (int)cluster_ctarank() : 0;
   const int64_t i0 = (int64_t)rank * p.slice;
   const int own = (int)((i0 + p.slice <= p.ppad) ? p.slice : (p.ppad > i0 ? p.ppad - i0 : 0));
-  const int NS = p.nslots;
+  const int NS = p.nslots, SP = p.slicepad;
+  // every CTA reads the stop flag before any CTA of this launch can change it (cluster sync below)
+  const bool stopped = *(volatile int32_t*)&p.st->inner_conv != 0;
 
   // shared memory carve-up
-  double* slots = reinterpret_cast<double*>(smem_raw);                 // [NS][2][slice]
-  double* zs = slots + (size_t)NS * 2 * p.slice;                       // [npad]
-  double* azs = zs + p.npad;                                           // [slice]
-  uint64_t* Ss = reinterpret_cast<uint64_t*>(azs + p.slice);           // [n]
+  double* slots = reinterpret_cast<double*>(smem_raw);                 // [NS][2][slicepad]
+  double* zs = slots + (size_t)NS * 2 * SP;                            // [npad]
+  uint64_t* Ss = reinterpret_cast<uint64_t*>(zs + p.npad);             // [n]
   RkIdx* ring = reinterpret_cast<RkIdx*>(Ss + ((p.n + 1) & ~1));       // [RK_RING]
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + RK_RING);        // [NS]
-  __shared__ double wred[2][RK_WARPS][3];
-  __shared__ double clred[2][RK_MAXC][3];
-  __shared__ double chk[RK_MAXC][2];
+  __shared__ __align__(16) double wred[2][RK_MAXW][4];
+  __shared__ __align__(16) double recv[2][RK_MAXC][4];                 // per-rank partials (DSMEM target)
+  __shared__ __align__(8) uint64_t redbar[2];
+  __shared__ double chkw[RK_MAXW];
   __shared__ double bnorm_s;
+  if (stopped) return;
 
-  for (int64_t j = tid; j < p.npad; j += RK_THREADS) zs[j] = 0.0;
-  for (int j = tid; j < p.n; j += RK_THREADS) Ss[j] = p.S[j];
+  for (int64_t j = tid; j < p.npad; j += NT) zs[j] = p.Z[j];
+  for (int j = tid; j < p.n; j += NT) Ss[j] = p.S[j];
+  for (int64_t e = tid; e < (int64_t)NS * 2 * SP; e += NT) slots[e] = 0.0;   // zero tails
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    if (CC > 1) {
+      mbar_init(&redbar[0], 1);
+      mbar_init(&redbar[1], 1);
+    }
     fence_mbar_init();
+    if (CC > 1) {   // arm phase 0 of both reduction barriers: CC partial triples (32 B each)
+      mbar_arrive_expect_tx(&redbar[0], CC * 32);
+      mbar_arrive_expect_tx(&redbar[1], CC * 32);
+    }
   }
-  // ||b_hat|| (same fixed order in every CTA)
-  {
+  double bnorm = 1.0;
+  if (p.t0 == 0) {   // ||b_hat|| (same fixed order in every CTA); b_hat = 0 -> z = 0 after 0 steps
     double v = 0.0;
-    for (int j = tid; j < p.n; j += RK_THREADS) v = fma(p.bhat[j], p.bhat[j], v);
+    for (int j = tid; j < p.n; j += NT) v = fma(p.bhat[j], p.bhat[j], v);
     v = warp_sum(v);
-    if (lane == 0) wred[0][warp][0] = v;
+    if (lane == 0) chkw[warp] = v;
     __syncthreads();
     if (tid == 0) {
       double s = 0.0;
-      for (int w = 0; w < RK_WARPS; ++w) s += wred[0][w][0];
+      for (int w = 0; w < NW; ++w) s += chkw[w];
       bnorm_s = sqrt(s);
     }
+    __syncthreads();
+    bnorm = bnorm_s;
   }
   __syncthreads();
-  const double bnorm = bnorm_s;
-  if (CLUSTER) cluster_sync_all();   // peers' smem initialised before any DSMEM store
-  if (bnorm == 0.0) {                // b_hat = 0: z = 0 after 0 steps
-    if (rank == 0) {
-      for (int64_t j = tid; j < p.npad; j += RK_THREADS) p.z_out[j] = 0.0;
-      if (tid == 0) {
-        p.st->inner_steps = 0;
-        p.st->inner_conv = 1;
-      }
+  if (CC > 1) cluster_sync_all();   // peers' barriers initialised before any DSMEM traffic
+  if (bnorm == 0.0) {
+    if (rank == 0 && tid == 0) {
+      p.st->inner_steps = 0;
+      p.st->inner_conv = 1;
     }
-    return;
+    return;   // Z is still the zero initial state
   }
 
-  // index ring: steps [0, 64); step t (t % 32 == 0) fills [t+64, t+96), overwriting entries of
-  // steps t-64..t-33 that every thread has finished with
-  if (warp == 0) {
-    for (int b = 0; b < 2; ++b) rk_fill_indices(p, Ss, ring, 32 * b, lane);
-  }
+  // index ring: steps [t0, t0+64); at step t ((t - t0) % 32 == 0) warp NW-1 fills [t+64, t+96),
+  // overwriting entries of steps t-64..t-33 that every thread has finished with
+  if (warp == 0) rk_fill_indices(p, Ss, ring, p.t0, lane);
+  if (warp == NW - 1) rk_fill_indices(p, Ss, ring, p.t0 + 32, lane);
   __syncthreads();
 
   const uint32_t slice_bytes = (uint32_t)own * sizeof(double);
-  auto issue = [&](int64_t t) {
-    const int slot = (int)(t % NS);
+  const int issuer = NT - 1;
+  auto issue = [&](int64_t t, int slot) {
     const RkIdx e = ring[t & (RK_RING - 1)];
-    double* dst = slots + (size_t)slot * 2 * p.slice;
+    double* dst = slots + (size_t)slot * 2 * SP;
     mbar_arrive_expect_tx(&bars[slot], 2 * slice_bytes);
     bulk_g2s(dst, p.A1T + (int64_t)e.j1 * p.ppad + i0, slice_bytes, &bars[slot]);
-    bulk_g2s(dst + p.slice, p.A1T + (int64_t)e.j2 * p.ppad + i0, slice_bytes, &bars[slot]);
+    bulk_g2s(dst + SP, p.A1T + (int64_t)e.j2 * p.ppad + i0, slice_bytes, &bars[slot]);
   };
-  if (tid == 0 && own > 0) {
-    for (int64_t t = 0; t < NS && t < p.max_inner; ++t) issue(t);
+  // steps [t0, issued) have been requested; after step t, issued = min(t + NS, t1)
+  int64_t issued = (p.t0 + NS < p.t1) ? p.t0 + NS : p.t1;
+  if (tid == issuer && own > 0) {
+    fence_proxy_async();
+    for (int64_t u = p.t0; u < issued; ++u) issue(u, (int)(u - p.t0));
   }
 
   double w[U], r[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u) w[u] = r[u] = 0.0;
+  for (int u = 0; u < U; ++u) {
+    const int64_t i = i0 + tid + u * NT;
+    const bool in = (tid + u * NT < own);
+    w[u] = in ? p.W[i] : 0.0;
+    r[u] = in ? p.Rv[i] : 0.0;
+  }
 
-  int64_t t = 0;
-  int conv = 0;
-  for (; t < p.max_inner; ++t) {
-    if (warp == 0 && (t & 31) == 0 && t + 64 < p.max_inner) rk_fill_indices(p, Ss, ring, t + 64, lane);
-    const int slot = (int)(t % NS);
-    const double* a1 = slots + (size_t)slot * 2 * p.slice;
-    const double* a2 = a1 + p.slice;
+  int slot = 0;
+  uint32_t ph = 0;
+  for (int64_t t = p.t0; t < p.t1; ++t) {
+    const int pb = (int)(t & 1);
+    const double* a1 = slots + (size_t)slot * 2 * SP;
+    const double* a2 = a1 + SP;
     double d1 = 0.0, d2 = 0.0, d3 = 0.0;
-    if (own > 0) mbar_wait(&bars[slot], (uint32_t)((t / NS) & 1));
+    if (own > 0) mbar_wait(&bars[slot], ph);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int e = tid + u * RK_THREADS;
-      if (e < own) {
-        const double x1 = a1[e], x2 = a2[e];
-        d1 = fma(x1, w[u], d1);
-        d2 = fma(x2, r[u], d2);
-        d3 = fma(x2, x1, d3);
-      }
+      const double x1 = a1[tid + u * NT], x2 = a2[tid + u * NT];
+      d1 = fma(x1, w[u], d1);
+      d2 = fma(x2, r[u], d2);
+      d3 = fma(x2, x1, d3);
     }
     d1 = warp_sum(d1);
     d2 = warp_sum(d2);
     d3 = warp_sum(d3);
-    const int pb = (int)(t & 1);
-    if (lane == 0) {
-      wred[pb][warp][0] = d1;
-      wred[pb][warp][1] = d2;
-      wred[pb][warp][2] = d3;
+    if (NW > 1) {
+      if (lane == 0) {
+        wred[pb][warp][0] = d1;
+        wred[pb][warp][1] = d2;
+        wred[pb][warp][2] = d3;
+      }
+      named_bar_sync(1, NT);   // all warps finished step t-1 and deposited step t partials
     }
-    __syncthreads();
-    if (tid == 0 && own > 0 && t >= 1 && t - 1 + NS < p.max_inner) issue(t - 1 + NS);
-    double D1 = 0.0, D2 = 0.0, D3 = 0.0;
-    if (CLUSTER) {
-      if (warp == 0 && lane < C) {
-        double v0 = 0.0, v1 = 0.0, v2 = 0.0;
-#pragma unroll
-        for (int w8 = 0; w8 < RK_WARPS; ++w8) {
-          v0 += wred[pb][w8][0];
-          v1 += wred[pb][w8][1];
-          v2 += wred[pb][w8][2];
+    // refill the slot step t-1 used (every thread is past step t-1 here)
+    if (t > p.t0 && issued < p.t1) {
+      if (tid == issuer && own > 0) issue(issued, slot == 0 ? NS - 1 : slot - 1);
+      ++issued;
+    }
+    double D1, D2, D3;
+    if (CC > 1) {
+      if (warp == 0 && lane < CC) {
+        double v0 = d1, v1 = d2, v2 = d3;
+        if (NW > 1) {
+          v0 = v1 = v2 = 0.0;
+          for (int w8 = 0; w8 < NW; ++w8) {
+            v0 += wred[pb][w8][0];
+            v1 += wred[pb][w8][1];
+            v2 += wred[pb][w8][2];
+          }
         }
-        const uint32_t base = map_shared_rank(smem_u32(&clred[pb][rank][0]), (uint32_t)lane);
-        st_cluster_f64(base, v0);
-        st_cluster_f64(base + 8, v1);
-        st_cluster_f64(base + 16, v2);
+        const uint32_t raddr = map_shared_rank(smem_u32(&recv[pb][rank][0]), (uint32_t)lane);
+        const uint32_t rbar = map_shared_rank(smem_u32(&redbar[pb]), (uint32_t)lane);
+        st_async_v2f64(raddr, v0, v1, rbar);
+        st_async_v2f64(raddr + 16, v2, 0.0, rbar);
       }
-      cluster_sync_all();
-      for (int c = 0; c < C; ++c) {
-        D1 += clred[pb][c][0];
-        D2 += clred[pb][c][1];
-        D3 += clred[pb][c][2];
-      }
-    } else {
+      if (warp == NW - 1 && ((t - p.t0) & 31) == 0 && t + RK_AHEAD < p.t1)
+        rk_fill_indices(p, Ss, ring, t + RK_AHEAD, lane);
+      mbar_wait(&redbar[pb], (uint32_t)(((t - p.t0) >> 1) & 1));
+      double a0[CC], a1v[CC], a2v[CC];
 #pragma unroll
-      for (int w8 = 0; w8 < RK_WARPS; ++w8) {
-        D1 += wred[pb][w8][0];
-        D2 += wred[pb][w8][1];
-        D3 += wred[pb][w8][2];
+      for (int c = 0; c < CC; ++c) {
+        const double2 v = *reinterpret_cast<const double2*>(&recv[pb][c][0]);
+        a0[c] = v.x;
+        a1v[c] = v.y;
+        a2v[c] = recv[pb][c][2];
+      }
+#pragma unroll
+      for (int s = 1; s < CC; s *= 2)
+#pragma unroll
+        for (int c = 0; c + s < CC; c += 2 * s) {
+          a0[c] += a0[c + s];
+          a1v[c] += a1v[c + s];
+          a2v[c] += a2v[c + s];
+        }
+      D1 = a0[0];
+      D2 = a1v[0];
+      D3 = a2v[0];
+      // re-arm for step t+2: its complete_tx cannot arrive before this CTA sends step t+1,
+      // which happens after every thread here has passed this wait
+      if (tid == 0) mbar_arrive_expect_tx(&redbar[pb], CC * 32);
+    } else {
+      if (((t - p.t0) & 31) == 0 && t + RK_AHEAD < p.t1 && warp == NW - 1)
+        rk_fill_indices(p, Ss, ring, t + RK_AHEAD, lane);
+      if (NW > 1) {
+        D1 = D2 = D3 = 0.0;
+        for (int w8 = 0; w8 < NW; ++w8) {
+          D1 += wred[pb][w8][0];
+          D2 += wred[pb][w8][1];
+          D3 += wred[pb][w8][2];
+        }
+      } else {
+        D1 = d1;
+        D2 = d2;
+        D3 = d3;
       }
     }
     const RkIdx ix = ring[t & (RK_RING - 1)];
-    const double s1 = (ix.bh1 - D1) / ix.n1;
-    const double s2 = (D2 + s1 * D3) / ix.n2;
+    const double s1 = (ix.bh1 - D1) * ix.rn1;
+    const double s2 = (D2 + s1 * D3) * ix.rn2;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int e = tid + u * RK_THREADS;
-      if (e < own) {
-        const double x1 = a1[e], x2 = a2[e];
-        w[u] = fma(s1, x1, w[u]);
-        r[u] = fma(s1, x1, r[u]);
-        r[u] = fma(-s2, x2, r[u]);
-      }
+      const double x1 = a1[tid + u * NT], x2 = a2[tid + u * NT];
+      w[u] = fma(s1, x1, w[u]);
+      r[u] = fma(s1, x1, r[u]);
+      r[u] = fma(-s2, x2, r[u]);
     }
     if (tid == 0) zs[ix.j2] += s2;
-
-    if ((t + 1) % p.check_every == 0) {
-      // ---- inner stop rule: az = A1 z (own rows), g = A1^T az - b_hat, reset r = w - az
-      __syncthreads();   // z complete
-      double az[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) az[u] = 0.0;
-      for (int j = 0; j < p.n; ++j) {
-        const double zj = zs[j];
-        const double* col = p.A1T + (int64_t)j * p.ppad + i0;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int e = tid + u * RK_THREADS;
-          if (e < own) az[u] = fma(__ldg(col + e), zj, az[u]);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = tid + u * RK_THREADS;
-        if (e < own) {
-          azs[e] = az[u];
-          r[u] = w[u] - az[u];
-        }
-      }
-      __syncthreads();
-      for (int j = warp; j < p.n; j += RK_WARPS) {
-        const double* col = p.A1T + (int64_t)j * p.ppad + i0;
-        double s = 0.0;
-        for (int e = lane; e < own; e += 32) s = fma(__ldg(col + e), azs[e], s);
-        s = warp_sum(s);
-        if (lane == 0) p.gpart[(int64_t)rank * p.npad + j] = s;
-      }
-      if (CLUSTER) cluster_sync_all(); else __syncthreads();
-      // this CTA's share of ||g||^2
-      const int jper = (p.n + C - 1) / C;
-      const int ja = rank * jper, jb = (ja + jper < p.n) ? ja + jper : p.n;
-      double g2 = 0.0;
-      for (int j = ja + tid; j < jb; j += RK_THREADS) {
-        double g = 0.0;
-        for (int c = 0; c < C; ++c) g += __ldcg(p.gpart + (int64_t)c * p.npad + j);
-        g -= p.bhat[j];
-        g2 = fma(g, g, g2);
-      }
-      g2 = warp_sum(g2);
-      if (lane == 0) wred[0][warp][0] = g2;
-      __syncthreads();
-      if (tid == 0) {
-        double s = 0.0;
-        for (int w8 = 0; w8 < RK_WARPS; ++w8) s += wred[0][w8][0];
-        if (CLUSTER) {
-          for (int c = 0; c < C; ++c) {
-            const uint32_t a = map_shared_rank(smem_u32(&chk[rank][0]), (uint32_t)c);
-            st_cluster_f64(a, s);
-          }
-        } else {
-          chk[0][0] = s;
-        }
-      }
-      if (CLUSTER) cluster_sync_all(); else __syncthreads();
-      double G2 = 0.0;
-      for (int c = 0; c < C; ++c) G2 += chk[c][0];
-      if (sqrt(G2) <= p.inner_tol * bnorm) {
-        conv = 1;
-        ++t;
-        break;
-      }
-      __syncthreads();   // wred[0] reuse / chk reads done before the next check writes
+    if (++slot == NS) {
+      slot = 0;
+      ph ^= 1u;
     }
   }
-  // drain: wait for prefetched-but-unused slots so no TMA is in flight at exit
-  if (own > 0) {
-    const int64_t issued = (t - 1 + NS < p.max_inner) ? (t - 1 + NS) : p.max_inner;
-    for (int64_t u = t; u < issued; ++u) mbar_wait(&bars[u % NS], (uint32_t)((u / NS) & 1));
+  // save the state (no TMA is in flight: every issued step was consumed)
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (tid + u * NT < own) {
+      const int64_t i = i0 + tid + u * NT;
+      p.W[i] = w[u];
+      p.Rv[i] = r[u];
+    }
   }
   __syncthreads();
-  if (rank == 0) {
-    for (int64_t j = tid; j < p.npad; j += RK_THREADS) p.z_out[j] = zs[j];
-    if (tid == 0) {
-      p.st->inner_steps = t;
-      p.st->inner_conv = conv;
-    }
-  }
-  if (CLUSTER) cluster_sync_all();   // no CTA exits while peers may still store into its smem
+  if (rank == 0)
+    for (int64_t j = tid; j < p.npad; j += NT) p.Z[j] = zs[j];
+  if (CC > 1) cluster_sync_all();   // no CTA exits while peers may still access its smem
 }
 
 __global__ void rk_indices_kernel(RkParams p, int64_t t0, int64_t count, int32_t* j1, int32_t* j2) {
@@ -322,45 +309,45 @@ int rk_indices(Handle& h, uint64_t seed, int64_t k, int64_t t0, int64_t count, i
   return ILS_OK;
 }
 
-template <int U, bool CL>
-static int launch_rk(Handle& h, RkParams& p, size_t smem) {
-  ILS_CU(cudaFuncSetAttribute(rk_rgs_kernel<U, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+template <int CC, int U>
+static int launch_rk(Handle& h, RkParams& p, int nt, size_t smem) {
+  auto kern = rk_rgs_kernel<CC, U>;
+  ILS_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.C);
-  cfg.blockDim = dim3(RK_THREADS);
+  cfg.gridDim = dim3(CC);
+  cfg.blockDim = dim3(nt);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = h.stream;
   cudaLaunchAttribute attr[1];
   int na = 0;
-  if (CL) {
-    ILS_CU(cudaFuncSetAttribute(rk_rgs_kernel<U, CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  if (CC > 1) {
+    ILS_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = p.C;
+    attr[0].val.clusterDim.x = CC;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     na = 1;
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  ILS_CU(cudaLaunchKernelEx(&cfg, rk_rgs_kernel<U, CL>, p));
+  ILS_CU(cudaLaunchKernelEx(&cfg, kern, p));
   ILS_LAUNCHED("rk_rgs_kernel");
   return ILS_OK;
 }
 
-template <bool CL>
-static int dispatch_rk(Handle& h, RkParams& p, size_t smem, int U) {
-  switch (U) {
-    case 1: return launch_rk<1, CL>(h, p, smem);
-    case 2: return launch_rk<2, CL>(h, p, smem);
-    case 4: return launch_rk<4, CL>(h, p, smem);
-    case 8: return launch_rk<8, CL>(h, p, smem);
-    case 16: return launch_rk<16, CL>(h, p, smem);
-    default: return launch_rk<32, CL>(h, p, smem);
+template <int U>
+static int dispatch_rk_c(Handle& h, RkParams& p, int nt, size_t smem) {
+  switch (p.C) {
+    case 1: return launch_rk<1, U>(h, p, nt, smem);
+    case 2: return launch_rk<2, U>(h, p, nt, smem);
+    case 4: return launch_rk<4, U>(h, p, nt, smem);
+    case 8: return launch_rk<8, U>(h, p, nt, smem);
+    default: return launch_rk<16, U>(h, p, nt, smem);
   }
 }
 
 static int rk_cluster_size(Handle& h) {
-  // one CTA up to 2048 rows; otherwise a cluster (16 non-portable, fall back to 8)
+  // one CTA up to 2048 rows; otherwise a cluster of up to 16 CTAs (non-portable size)
   if (h.ppad <= 2048) return 1;
   int c = (int)((h.ppad + 511) / 512);
   return c >= 16 ? 16 : (c >= 8 ? 8 : (c >= 4 ? 4 : 2));
@@ -368,6 +355,19 @@ static int rk_cluster_size(Handle& h) {
 
 int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_t k, int64_t max_inner,
                  int64_t check_every, double inner_tol, int64_t* steps_out) {
+  const int64_t ce = check_every > 0 ? check_every : h.n;
+  const cudaStream_t st = h.stream;
+  if (!h.rk_state) {
+    ILS_CU(cudaMallocAsync(&h.rk_state, (size_t)(3 * h.ppad + h.npad) * sizeof(double), st));
+  }
+  double* W = h.rk_state;
+  double* Rv = W + h.ppad;
+  double* AZ = Rv + h.ppad;
+  double* Z = AZ + h.ppad;
+  ILS_CU(cudaMemsetAsync(h.rk_state, 0, (size_t)(3 * h.ppad + h.npad) * sizeof(double), st));
+  ILS_CU(cudaMemsetAsync(&h.dstat->inner_conv, 0, sizeof(int32_t), st));
+  ILS_CU(cudaMemsetAsync(&h.dstat->inner_steps, 0, sizeof(int64_t), st));
+
   RkParams p{};
   p.A1T = h.A1T;
   p.ppad = h.ppad;
@@ -376,47 +376,46 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
   p.N = h.N;
   p.S = h.S;
   p.bhat = bhat;
-  p.z_out = z;
+  p.W = W;
+  p.Rv = Rv;
+  p.Z = Z;
   p.seed = seed;
   p.k = (uint32_t)k;
   p.max_inner = max_inner;
-  p.check_every = check_every > 0 ? check_every : h.n;
-  p.inner_tol = inner_tol;
   p.st = h.dstat;
+  // launch geometry (fixed for the whole solve)
   int C = rk_cluster_size(h);
+  int U = 8, nt = 32;
+  size_t smem = 0;
   for (;;) {
     p.C = C;
     p.slice = (int)(((h.ppad + C - 1) / C + 1) / 2 * 2);
-    const int per = (p.slice + RK_THREADS - 1) / RK_THREADS;
-    int U = 1;
-    while (U < per) U *= 2;
-    if (U > 32) {
-      set_error("RK-RGS: row slice too long for the register-resident kernel");
+    // rows per thread: one warp with U = 8 for slices <= 256, U = 4 up to 2048, else U = 8
+    U = (p.slice <= 256) ? 8 : (p.slice <= 2048 ? 4 : 8);
+    const int nw = (p.slice + 32 * U - 1) / (32 * U);
+    if (nw > RK_MAXW) {
+      set_error("RK-RGS: row slice too long for the register-resident kernel (p > 65536)");
       return ILS_ERR_UNSUPPORTED;
     }
-    const size_t fixed = (size_t)(h.npad + p.slice) * 8 + (size_t)((h.n + 1) & ~1) * 8 +
-                         RK_RING * sizeof(RkIdx) + 16 * 8 + 256;
-    const size_t slot_bytes = (size_t)2 * p.slice * 8;
-    const size_t budget = 225 * 1024;
-    int NS = (int)((budget - fixed) / slot_bytes);
-    if (NS > 8) NS = 8;
+    nt = 32 * nw;
+    p.slicepad = U * nt;
+    const size_t fixed = (size_t)h.npad * 8 + (size_t)((h.n + 1) & ~1) * 8 + RK_RING * sizeof(RkIdx) + 16 * 8 + 256;
+    const size_t slot_bytes = (size_t)2 * p.slicepad * 8;
+    const size_t budget = 200 * 1024;
     if (fixed + 2 * slot_bytes > budget) {
       set_error("RK-RGS: shared memory too small for this problem size");
       return ILS_ERR_UNSUPPORTED;
     }
+    int NS = (int)((budget - fixed) / slot_bytes);
+    if (NS > 8) NS = 8;
     p.nslots = NS;
-    const size_t smem = fixed + (size_t)NS * slot_bytes;
-    if (!h.part || h.part_rows < C) return ILS_ERR_ARG;
-    p.gpart = h.part;
-    int r;
-    ILS_CU(cudaEventRecord(h.evk0, h.stream));
-    if (C == 1) {
-      r = dispatch_rk<false>(h, p, smem, U);
-    } else {
+    smem = fixed + (size_t)NS * slot_bytes;
+    // probe that a cluster of this size can be scheduled
+    if (C > 1) {
       int ncl = 0;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(C);
-      cfg.blockDim = dim3(RK_THREADS);
+      cfg.blockDim = dim3(nt);
       cfg.dynamicSmemBytes = smem;
       cudaLaunchAttribute a;
       a.id = cudaLaunchAttributeClusterDimension;
@@ -425,9 +424,10 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
       a.val.clusterDim.z = 1;
       cfg.attrs = &a;
       cfg.numAttrs = 1;
-      cudaFuncSetAttribute(rk_rgs_kernel<16, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaFuncSetAttribute(rk_rgs_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (cudaOccupancyMaxActiveClusters(&ncl, rk_rgs_kernel<16, true>, &cfg) != cudaSuccess || ncl < 1) {
+      auto kern = (U == 4) ? (void*)rk_rgs_kernel<16, 4> : (void*)rk_rgs_kernel<16, 8>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess || ncl < 1) {
         cudaGetLastError();
         if (C > 2) {
           C /= 2;
@@ -436,18 +436,49 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
         set_error("RK-RGS: no cluster configuration fits");
         return ILS_ERR_UNSUPPORTED;
       }
-      r = dispatch_rk<true>(h, p, smem, U);
     }
-    if (r) return r;
-    ILS_CU(cudaEventRecord(h.evk1, h.stream));
-    ILS_CU(cudaMemcpyAsync(h.hstat, h.dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, h.stream));
-    ILS_CU(cudaStreamSynchronize(h.stream));
-    const int64_t steps = h.hstat->inner_steps;
-    if (steps_out) *steps_out = steps;
-    const double pd = (double)h.p, nd = (double)h.n;
-    hot_account(h, 1, (double)steps * 16.0 * pd + (double)(steps / p.check_every) * 16.0 * pd * nd);
-    return ILS_OK;
+    break;
   }
+
+  // chunks of check_every steps, each followed by the full-GPU inner check; launches are queued
+  // ahead (kernels of a stopped solve return at once) and the stop flag is read every kBatch checks
+  constexpr int kBatch = 8;
+  ILS_CU(cudaEventRecord(h.evk0, st));
+  int64_t t = 0, nchecks = 0;
+  int pending = 0;
+  bool conv = false;
+  while (t < max_inner) {
+    const int64_t t1 = (t + ce < max_inner) ? t + ce : max_inner;
+    p.t0 = t;
+    p.t1 = t1;
+    const int r = (U == 4) ? dispatch_rk_c<4>(h, p, nt, smem) : dispatch_rk_c<8>(h, p, nt, smem);
+    if (r) return r;
+    t = t1;
+    if (t % ce == 0) {
+      const int rc = rk_check(h, Z, bhat, W, Rv, AZ, inner_tol, t);
+      if (rc) return rc;
+      ++nchecks;
+    }
+    if (++pending == kBatch || t >= max_inner) {
+      ILS_CU(cudaMemcpyAsync(h.hstat, h.dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+      ILS_CU(cudaStreamSynchronize(st));
+      pending = 0;
+      if (h.hstat->inner_conv) {
+        conv = true;
+        break;
+      }
+    }
+  }
+  ILS_CU(cudaEventRecord(h.evk1, st));
+  ILS_CU(cudaMemcpyAsync(z, Z, h.npad * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  ILS_CU(cudaMemcpyAsync(h.hstat, h.dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+  ILS_CU(cudaStreamSynchronize(st));
+  const int64_t steps = h.hstat->inner_conv ? h.hstat->inner_steps : max_inner;
+  (void)conv;
+  if (steps_out) *steps_out = steps;
+  const double pd = (double)h.p, nd = (double)h.n;
+  hot_account(h, 1, (double)steps * 16.0 * pd + (double)(steps / ce) * 8.0 * pd * nd);
+  return ILS_OK;
 }
 
 }  // namespace ils

@@ -15,9 +15,10 @@
 
 namespace ils {
 
-constexpr int SCD_THREADS = 1024;
-constexpr int SCD_WARPS = SCD_THREADS / 32;
+constexpr int SCD_MAXT = 256;    // threads per CTA (max)
+constexpr int SCD_MAXW = SCD_MAXT / 32;
 constexpr int SCD_RING = 128;
+constexpr int SCD_AHEAD = 64;
 
 struct ScdKey {
   uint32_t alpha;
@@ -63,42 +64,64 @@ __device__ __forceinline__ void scd_make_key(uint64_t seed, uint32_t k, uint64_t
   e.key[11] = d.x;
 }
 
-template <int U>
-__global__ void __launch_bounds__(SCD_THREADS, 1) scd_kernel(ScdParams p) {
+// Membership bits of this thread's coordinates s = tid + v*NT in tau_t: pi^{-1}(s) < alpha_t.
+template <int V>
+__device__ __forceinline__ uint32_t scd_members(const ScdKey& e, int tid, int NT, int n, uint32_t h,
+                                                uint32_t mask) {
+  uint32_t key[kFeistelRounds];
+#pragma unroll
+  for (int q = 0; q < kFeistelRounds; ++q) key[q] = e.key[q];
+  const uint32_t alpha = e.alpha;
+  uint32_t bits = 0;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int s = tid + v * NT;
+    if (s < n && feistel_inverse((uint32_t)s, key, h, mask, (uint32_t)n) < alpha) bits |= 1u << v;
+  }
+  return bits;
+}
+
+// One CTA of NT <= 256 threads; thread tid owns coordinates s = tid + v*NT (v < V) of r and beta
+// in registers. Per step (software-pipelined): argmax over tau_t (thread -> warp shuffles -> one
+// barrier -> redundant per-warp reduction of the warp winners), then the A1bar row j is loaded
+// from L2 while the membership bits of step t+1 are computed (pure integer work, data-independent).
+template <int V>
+__global__ void __launch_bounds__(SCD_MAXT, 1) scd_kernel(ScdParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* bs = reinterpret_cast<double*>(smem_raw);          // [npad] beta (for checks)
-  double* Ns = bs + p.npad;                                  // [n]
-  uint64_t* Ss = reinterpret_cast<uint64_t*>(Ns + ((p.n + 1) & ~1));
+  double* rNs = bs + p.npad;                                 // [n] 1 / A1bar_jj
+  uint64_t* Ss = reinterpret_cast<uint64_t*>(rNs + ((p.n + 1) & ~1));
   ScdKey* ring = reinterpret_cast<ScdKey*>(Ss + ((p.n + 1) & ~1));
-  __shared__ double wv[2][SCD_WARPS], wp[2][SCD_WARPS];
-  __shared__ int wi[2][SCD_WARPS];
-  __shared__ double red[SCD_WARPS];
+  __shared__ double wv[2][SCD_MAXW], wr[2][SCD_MAXW];
+  __shared__ int wi[2][SCD_MAXW];
+  __shared__ double red[SCD_MAXW];
   __shared__ double rj_s[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NT = blockDim.x, NW = NT >> 5;
   const int n = p.n;
   const uint32_t h = feistel_half_bits((uint32_t)n), mask = (1u << h) - 1u;
 
-  for (int j = tid; j < n; j += SCD_THREADS) {
-    Ns[j] = p.N[j];
+  for (int j = tid; j < n; j += NT) {
+    rNs[j] = 1.0 / p.N[j];
     Ss[j] = p.S[j];
   }
-  double r[U], beta[U];
+  double r[V], beta[V];
   double nb2 = 0.0;
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int s = tid + u * SCD_THREADS;
-    r[u] = (s < n) ? p.bhat[s] : 0.0;
-    beta[u] = 0.0;
-    nb2 = fma(r[u], r[u], nb2);
+  for (int v = 0; v < V; ++v) {
+    const int s = tid + v * NT;
+    r[v] = (s < n) ? p.bhat[s] : 0.0;
+    beta[v] = 0.0;
+    nb2 = fma(r[v], r[v], nb2);
   }
   nb2 = warp_sum(nb2);
   if (lane == 0) red[warp] = nb2;
   __syncthreads();
   double B2 = 0.0;
-  for (int w = 0; w < SCD_WARPS; ++w) B2 += red[w];
+  for (int w = 0; w < NW; ++w) B2 += red[w];
   const double bnorm = sqrt(B2);
   if (bnorm == 0.0) {
-    for (int64_t j = tid; j < p.npad; j += SCD_THREADS) p.beta_out[j] = 0.0;
+    for (int64_t j = tid; j < p.npad; j += NT) p.beta_out[j] = 0.0;
     if (tid == 0) {
       p.st->inner_steps = 0;
       p.st->inner_conv = 1;
@@ -115,101 +138,119 @@ __global__ void __launch_bounds__(SCD_THREADS, 1) scd_kernel(ScdParams p) {
   }
   __syncthreads();
 
+  uint32_t inmask = p.weighted ? 0u : scd_members<V>(ring[0], tid, NT, n, h, mask);
   int64_t t = 0;
   int conv = 0;
+  int64_t next_check = p.check_every;
   for (; t < p.max_inner; ++t) {
-    if (warp == 0 && (t & 31) == 0 && t + 64 + lane < p.max_inner) {
-      const int64_t tt = t + 64 + lane;
-      scd_make_key(p.seed, p.k, (uint64_t)tt, n, p.alpha_mode, p.alpha_k, p.weighted, Ss,
-                   ring[tt & (SCD_RING - 1)]);
-    }
-    const ScdKey& e = ring[t & (SCD_RING - 1)];
     const int pb = (int)(t & 1);
     int j;
     double rj;
     if (p.weighted) {
-      j = e.j;
+      j = ring[t & (SCD_RING - 1)].j;
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (tid + u * SCD_THREADS == j) rj_s[pb] = r[u];
+      for (int v = 0; v < V; ++v)
+        if (tid + v * NT == j) rj_s[pb] = r[v];
       __syncthreads();
       rj = rj_s[pb];
     } else {
-      uint32_t key[kFeistelRounds];
+      // thread-local argmax (coordinates ascend with v: strict > keeps the smallest index)
+      double bv = -1.0, br = 0.0;
+      int bi = INT_MAX;
 #pragma unroll
-      for (int q = 0; q < kFeistelRounds; ++q) key[q] = e.key[q];
-      const uint32_t alpha = e.alpha;
-      ArgMax best{-1.0, INT_MAX, 0.0};
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int s = tid + u * SCD_THREADS;
-        if (s < n) {
-          const uint32_t m = feistel_inverse((uint32_t)s, key, h, mask, (uint32_t)n);
-          if (m < alpha) {
-            const double v = r[u] * r[u];
-            if (argmax_better(v, s, best.val, best.idx)) {
-              best.val = v;
-              best.idx = s;
-              best.pay = r[u];
-            }
-          }
+      for (int v = 0; v < V; ++v) {
+        const double q = r[v] * r[v];
+        if (((inmask >> v) & 1u) && q > bv) {
+          bv = q;
+          bi = tid + v * NT;
+          br = r[v];
         }
       }
-      best = warp_argmax(best);
-      if (lane == 0) {
-        wv[pb][warp] = best.val;
-        wi[pb][warp] = best.idx;
-        wp[pb][warp] = best.pay;
+      // warp argmax (value, index); ties to the smallest index
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (argmax_better(ov, oi, bv, bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      // the winning lane publishes (value, index, r)
+      if (bi != INT_MAX && (bi % NT) == tid) {
+        wv[pb][warp] = bv;
+        wi[pb][warp] = bi;
+        wr[pb][warp] = br;
+      } else if (lane == 0 && bi == INT_MAX) {
+        wv[pb][warp] = -1.0;
+        wi[pb][warp] = INT_MAX;
       }
       __syncthreads();
-      ArgMax b{-1.0, INT_MAX, 0.0};
-      for (int w = 0; w < SCD_WARPS; ++w) {
-        if (argmax_better(wv[pb][w], wi[pb][w], b.val, b.idx)) {
-          b.val = wv[pb][w];
-          b.idx = wi[pb][w];
-          b.pay = wp[pb][w];
+      // every warp reduces the NW warp winners (same fixed tree in every warp)
+      double cv = (lane < NW) ? wv[pb][lane] : -1.0;
+      int ci = (lane < NW) ? wi[pb][lane] : INT_MAX;
+#pragma unroll
+      for (int o = SCD_MAXW / 2; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, cv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, ci, o);
+        if (argmax_better(ov, oi, cv, ci)) {
+          cv = ov;
+          ci = oi;
         }
       }
-      j = b.idx;
-      rj = b.pay;
+      j = __shfl_sync(0xffffffffu, ci, 0);   // lanes >= NW reduced only invalid entries
+      rj = wr[pb][(j % NT) >> 5];
     }
-    const double sc = rj / Ns[j];
+    const double sc = rj * rNs[j];
+    // A1bar row j (L2): issue the loads, then overlap their latency with step t+1's membership
     const double* grow = p.G + (int64_t)j * p.npad;
+    double g[V];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int s = tid + u * SCD_THREADS;
-      if (s < n) {
-        r[u] = fma(-sc, grow[s], r[u]);
-        if (s == j) beta[u] += sc;
-      }
+    for (int v = 0; v < V; ++v) {
+      const int s = tid + v * NT;
+      g[v] = (s < n) ? __ldcg(grow + s) : 0.0;
     }
-    if ((t + 1) % p.check_every == 0) {
+    if (warp == NW - 1 && (t & 31) == 0 && t + SCD_AHEAD + lane < p.max_inner) {
+      const int64_t tt = t + SCD_AHEAD + lane;
+      scd_make_key(p.seed, p.k, (uint64_t)tt, n, p.alpha_mode, p.alpha_k, p.weighted, Ss,
+                   ring[tt & (SCD_RING - 1)]);
+    }
+    if (!p.weighted && t + 1 < p.max_inner)
+      inmask = scd_members<V>(ring[(t + 1) & (SCD_RING - 1)], tid, NT, n, h, mask);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int s = tid + v * NT;
+      r[v] = fma(-sc, g[v], r[v]);
+      if (s == j) beta[v] += sc;
+    }
+    if (t + 1 == next_check) {
+      next_check += p.check_every;
       // r = b_hat - A1bar beta (column access of the symmetric A1bar: coalesced), stop test
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int s = tid + u * SCD_THREADS;
-        if (s < p.npad) bs[s] = beta[u];
+      for (int v = 0; v < V; ++v) {
+        const int s = tid + v * NT;
+        if (s < p.npad) bs[s] = beta[v];
       }
       __syncthreads();
-      double acc[U];
+      double acc[V];
 #pragma unroll
-      for (int u = 0; u < U; ++u) acc[u] = 0.0;
+      for (int v = 0; v < V; ++v) acc[v] = 0.0;
       for (int jj = 0; jj < n; ++jj) {
         const double bj = bs[jj];
-        const double* g = p.G + (int64_t)jj * p.npad;
+        const double* gr = p.G + (int64_t)jj * p.npad;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int s = tid + u * SCD_THREADS;
-          if (s < n) acc[u] = fma(g[s], bj, acc[u]);
+        for (int v = 0; v < V; ++v) {
+          const int s = tid + v * NT;
+          if (s < n) acc[v] = fma(__ldcg(gr + s), bj, acc[v]);
         }
       }
       double r2 = 0.0;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int s = tid + u * SCD_THREADS;
+      for (int v = 0; v < V; ++v) {
+        const int s = tid + v * NT;
         if (s < n) {
-          r[u] = p.bhat[s] - acc[u];
-          r2 = fma(r[u], r[u], r2);
+          r[v] = p.bhat[s] - acc[v];
+          r2 = fma(r[v], r[v], r2);
         }
       }
       r2 = warp_sum(r2);
@@ -217,7 +258,7 @@ __global__ void __launch_bounds__(SCD_THREADS, 1) scd_kernel(ScdParams p) {
       if (lane == 0) red[warp] = r2;
       __syncthreads();
       double R2 = 0.0;
-      for (int w = 0; w < SCD_WARPS; ++w) R2 += red[w];
+      for (int w = 0; w < NW; ++w) R2 += red[w];
       if (sqrt(R2) <= p.inner_tol * bnorm) {
         conv = 1;
         ++t;
@@ -226,9 +267,9 @@ __global__ void __launch_bounds__(SCD_THREADS, 1) scd_kernel(ScdParams p) {
     }
   }
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int s = tid + u * SCD_THREADS;
-    if (s < p.npad) p.beta_out[s] = (s < n) ? beta[u] : 0.0;
+  for (int v = 0; v < V; ++v) {
+    const int s = tid + v * NT;
+    if (s < p.npad) p.beta_out[s] = (s < n) ? beta[v] : 0.0;
   }
   if (tid == 0) {
     p.st->inner_steps = t;
@@ -239,7 +280,7 @@ __global__ void __launch_bounds__(SCD_THREADS, 1) scd_kernel(ScdParams p) {
 int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_t k, int64_t max_inner,
               int64_t check_every, double inner_tol, int alpha_mode, int alpha_k, int weighted,
               int64_t* steps_out) {
-  if (h.npad > 8 * SCD_THREADS) {
+  if (h.npad > 32 * SCD_MAXT) {
     set_error("SP-SCD: n > 8192 not supported by the single-CTA kernel in this release");
     return ILS_ERR_UNSUPPORTED;
   }
@@ -263,21 +304,26 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
   p.weighted = weighted;
   p.st = h.dstat;
   const size_t smem = (size_t)h.npad * 8 + 2 * (size_t)((h.n + 1) & ~1) * 8 + SCD_RING * sizeof(ScdKey);
-  const int per = (int)((h.npad + SCD_THREADS - 1) / SCD_THREADS);
-  int U = 1;
-  while (U < per) U *= 2;
+  // threads: one coordinate per thread up to 256 coordinates, then V coordinates per thread
+  int nt = (int)((h.n + 31) / 32 * 32);
+  if (nt > SCD_MAXT) nt = SCD_MAXT;
+  const int per = (int)((h.n + nt - 1) / nt);
+  int V = 1;
+  while (V < per) V *= 2;
   ILS_CU(cudaEventRecord(h.evk0, h.stream));
-#define SCD_LAUNCH(UU)                                                                              \
+#define SCD_LAUNCH(VV)                                                                              \
   do {                                                                                              \
-    ILS_CU(cudaFuncSetAttribute(scd_kernel<UU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    scd_kernel<UU><<<1, SCD_THREADS, smem, h.stream>>>(p);                                          \
+    ILS_CU(cudaFuncSetAttribute(scd_kernel<VV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    scd_kernel<VV><<<1, nt, smem, h.stream>>>(p);                                                   \
     ILS_LAUNCHED("scd_kernel");                                                                     \
   } while (0)
-  switch (U) {
+  switch (V) {
     case 1: SCD_LAUNCH(1); break;
     case 2: SCD_LAUNCH(2); break;
     case 4: SCD_LAUNCH(4); break;
-    default: SCD_LAUNCH(8); break;
+    case 8: SCD_LAUNCH(8); break;
+    case 16: SCD_LAUNCH(16); break;
+    default: SCD_LAUNCH(32); break;
   }
 #undef SCD_LAUNCH
   ILS_CU(cudaEventRecord(h.evk1, h.stream));

@@ -43,6 +43,17 @@ struct SpParams {
   int stop, sp_form, rhs_only;
   int rows_per_stage, nstages;
   DevStatus* st;
+  // SP-RK-RGS inner check mode (rhs_only = 1, b = nullptr, base = nullptr, x = z): rows [0, p) of
+  // A1 give az_i = <A1[i,:], z> (stored to az_out) and c = A1^T az; then g = c - b_hat,
+  // stop if ||g|| <= inner_tol ||b_hat|| (inner_steps = t_now), else reset r = w - az.
+  int check;
+  double* az_out;
+  const double* bhat;
+  const double* wst;
+  double* rst;
+  int64_t rows_r;          // rows of the r reset (ppad)
+  double inner_tol;
+  int64_t t_now;
 };
 
 template <int NPAIR>
@@ -59,6 +70,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sp_persistent_kernel(SpParams p
   uint64_t* bars = reinterpret_cast<uint64_t*>(reds + 2 * SP_WARPS * SP_RMAX);
   __shared__ double cta_red[SP_WARPS][2];
 
+  if (prm.check && *(volatile int32_t*)&prm.st->inner_conv) return;   // inner solve already stopped
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -129,7 +141,8 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sp_persistent_kernel(SpParams p
 #pragma unroll
         for (int w = 0; w < SP_WARPS; ++w) d += red[w * SP_RMAX + rr];
         const int64_t i = rs + rr;
-        d -= prm.b[i];
+        if (prm.az_out && tid == 0) prm.az_out[i] = d;
+        if (prm.b) d -= prm.b[i];
         if (i < prm.p) d = -d;          // sigma_i = -1 on A1 rows (correction form only)
         const double2* row = reinterpret_cast<const double2*>(st + rr * npad);
 #pragma unroll
@@ -158,6 +171,52 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sp_persistent_kernel(SpParams p
       double s = prm.base ? prm.base[j] : 0.0;
       for (int c = 0; c < G; ++c) s += prm.part[(int64_t)c * npad + j];
       prm.cvec[j] = s;
+    }
+    if (prm.check) {
+      // ||g||^2 and ||b_hat||^2 partials over this CTA's j range (fixed order everywhere)
+      double g2 = 0.0, b2 = 0.0;
+      const int64_t jper = (prm.n + G - 1) / G;
+      const int64_t ja = (int64_t)bid * jper, jb = (ja + jper < prm.n) ? ja + jper : prm.n;
+      for (int64_t j = ja + tid; j < jb; j += SP_THREADS) {
+        double s = (prm.base ? prm.base[j] : 0.0);
+        for (int c = 0; c < G; ++c) s += prm.part[(int64_t)c * npad + j];
+        const double g = s - prm.bhat[j];
+        g2 = fma(g, g, g2);
+        b2 = fma(prm.bhat[j], prm.bhat[j], b2);
+      }
+      g2 = warp_sum(g2);
+      b2 = warp_sum(b2);
+      if (lane == 0) {
+        cta_red[warp][0] = g2;
+        cta_red[warp][1] = b2;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < SP_WARPS; ++w) {
+          a += cta_red[w][0];
+          b += cta_red[w][1];
+        }
+        prm.red[2 * bid] = a;
+        prm.red[2 * bid + 1] = b;
+      }
+      grid.sync();
+      double Gs = 0.0, Bs = 0.0;
+      for (int c = 0; c < G; ++c) {
+        Gs += prm.red[2 * c];
+        Bs += prm.red[2 * c + 1];
+      }
+      const bool conv = sqrt(Gs) <= prm.inner_tol * sqrt(Bs);
+      if (conv) {
+        if (bid == 0 && tid == 0) {
+          prm.st->inner_steps = prm.t_now;
+          prm.st->inner_conv = 1;
+        }
+      } else {
+        for (int64_t i = (int64_t)bid * SP_THREADS + tid; i < prm.rows_r; i += (int64_t)G * SP_THREADS)
+          prm.rst[i] = prm.wst[i] - (i < prm.row_end ? prm.az_out[i] : 0.0);
+      }
+      break;
     }
     if (prm.rhs_only) break;
     grid.sync();
@@ -349,6 +408,58 @@ int sp_run(Handle& h, const double* x0_dev, double* x_dev, double tol, int64_t m
   if (metric_out) *metric_out = h.hstat->metric;
   if (conv_out) *conv_out = h.hstat->flag_stop;
   return ILS_OK;
+}
+
+// SP-RK-RGS inner stop check (include/ils.h "Inner stopping rule"), full grid: az = A1 z,
+// g = A1^T az - b_hat, stop if ||g|| <= inner_tol ||b_hat|| (sets st->inner_conv, inner_steps = t_now),
+// else r = w - az. No-op if st->inner_conv is already set.
+int rk_check(Handle& h, const double* z, const double* bhat, const double* w, double* r, double* az,
+             double inner_tol, int64_t t_now) {
+  SpParams prm{};
+  prm.Arm = h.Arm;
+  prm.b = nullptr;
+  prm.npad = h.npad;
+  prm.n = h.n;
+  prm.row_begin = 0;
+  prm.row_end = h.p;
+  prm.p = 0;
+  prm.base = nullptr;
+  prm.P = nullptr;
+  prm.xa = const_cast<double*>(z);
+  prm.xb = nullptr;
+  prm.xref = nullptr;
+  prm.part = h.part;
+  prm.cvec = h.vec + 2 * h.npad;
+  prm.red = h.red;
+  prm.x_hist = nullptr;
+  prm.max_iter = 1;
+  prm.stop = ILS_STOP_NONE;
+  prm.rhs_only = 1;
+  prm.st = h.dstat;
+  prm.check = 1;
+  prm.az_out = az;
+  prm.bhat = bhat;
+  prm.wst = w;
+  prm.rst = r;
+  prm.rows_r = h.ppad;
+  prm.inner_tol = inner_tol;
+  prm.t_now = t_now;
+  const int64_t rowbytes = h.npad * (int64_t)sizeof(double);
+  int R = (int)(SP_STAGE_TARGET / rowbytes);
+  if (R < 1) R = 1;
+  if (R > SP_RMAX) R = SP_RMAX;
+  const int64_t stage_bytes = R * rowbytes;
+  int NS = (int)((200 * 1024) / stage_bytes);
+  if (NS > 4) NS = 4;
+  if (NS < 2) NS = 2;
+  prm.rows_per_stage = R;
+  prm.nstages = NS;
+  const size_t smem = (size_t)NS * stage_bytes + 2 * SP_WARPS * SP_RMAX * sizeof(double) + NS * sizeof(uint64_t);
+  const int64_t np2 = h.npad / 2;
+  if (np2 <= SP_THREADS) return launch_sp<1>(h, prm, smem);
+  if (np2 <= 2 * SP_THREADS) return launch_sp<2>(h, prm, smem);
+  if (np2 <= 4 * SP_THREADS) return launch_sp<4>(h, prm, smem);
+  return launch_sp<8>(h, prm, smem);
 }
 
 // g = A^T J (b - A x) over all m rows (sigma = -1 on A1 rows): correction-form residual.

@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--max-inner", type=int, default=1_000_000)
     ap.add_argument("--max-iter", type=int, default=200)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--fixed", type=int, default=0, help="fixed horizon: 1 outer x FIXED inner steps, no stopping")
+    ap.add_argument("--check-every", type=int, default=0)
     a = ap.parse_args()
     t0 = time.time()
     pr = make_problem(a.config)
@@ -48,18 +50,22 @@ def main():
     for m in a.methods.split(","):
         for rep in range(a.reps):
             x = torch.zeros(B * n, dtype=torch.float64, device=dev)
-            o = ils.ils_default_opts(x_ref=xr.data_ptr(), inner_tol=itol, max_inner=a.max_inner)
+            o = ils.ils_default_opts(x_ref=xr.data_ptr(), inner_tol=itol, max_inner=a.max_inner,
+                                     check_every=a.check_every)
+            max_iter = a.max_iter
+            if a.fixed:
+                o.stop, o.inner_tol, o.max_inner, max_iter = ils.ILS_STOP_NONE, 0.0, a.fixed, 1
             fn = {"sp": ils.ils_sp_solve, "rk": ils.ils_rk_solve, "rgs": ils.ils_rgs_solve,
                   "rcd": ils.ils_rgs_solve}[m]
             if m == "rcd":
                 o.weighted = 1
             torch.cuda.synchronize()
             t1 = time.perf_counter()
-            st, r = fn(h, None, x, pr.tol, a.max_iter, o)
+            st, r = fn(h, None, x, pr.tol, max_iter, o)
             torch.cuda.synchronize()
             wall = (time.perf_counter() - t1) * 1e3
             d = r.as_dict()
-            d.update(method=m, rep=rep, status=st, wall_ms=wall)
+            d.update(method=m, rep=rep, status=st, wall_ms=wall, check_every=a.check_every, fixed=a.fixed)
             if B == 1:
                 d["err"] = float(torch.linalg.norm(x - xr) / torch.linalg.norm(xr))
             print(json.dumps(d), flush=True)
