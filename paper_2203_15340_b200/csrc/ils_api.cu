@@ -1,6 +1,7 @@
 // ils_api.cu -- the C ABI of libils (include/ils.h): validation, handle, host<->device staging,
 // outer loops and reports. All arithmetic runs in the kernels of this library.
 #include <atomic>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -142,6 +143,7 @@ static void free_handle_impl(Handle* h) {
   for (double* p : bufs)
     if (p) cudaFreeAsync(p, s);
   if (h->S) cudaFreeAsync(h->S, s);
+  if (h->scd_ws) cudaFreeAsync(h->scd_ws, s);
   if (h->dstat) cudaFreeAsync(h->dstat, s);
   cudaStreamSynchronize(s);
   if (h->hstat) cudaFreeHost(h->hstat);
@@ -233,6 +235,10 @@ int ils_create(ils_handle* out, const double* A, const double* b, int64_t p, int
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  {
+    const char* e = getenv("ILS_RK_SINGLE_STEP");
+    h->rk_single_step = (e && e[0] == '1');
+  }
   int rc = ILS_OK;
   auto fail = [&](int code) {
     free_handle(h);

@@ -53,6 +53,9 @@ struct Handle {
   size_t wsA_bytes = 0;
   double* vec = nullptr;    // 8 x npad scratch vectors
   double* rk_state = nullptr;  // SP-RK-RGS chunk state: w, r, az [ppad] each, z [npad]
+  void* scd_ws = nullptr;      // SP-SCD chunk state r, beta, r_tmp [npad], reductions, membership masks
+  size_t scd_ws_bytes = 0;
+  bool rk_single_step = false; // ILS_RK_SINGLE_STEP env: force the one-step-per-reduction RK-RGS kernel
   double* red = nullptr;    // reduction scratch [grid * 4]
   DevStatus* dstat = nullptr;
   DevStatus* hstat = nullptr;  // pinned host mirror

@@ -14,6 +14,9 @@
 // order. z is replicated in every CTA's smem. The inner stop check (include/ils.h) runs between
 // chunks as a full-GPU fused row stream (rk_check in sp.cu: az = A1 z, g = A1^T az - b_hat, reset
 // r = w - az); w, r, z pass through HBM between chunks.
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ils_internal.h"
 
@@ -44,23 +47,39 @@ struct RkParams {
   int64_t t0, t1, max_inner;
   DevStatus* st;
   int C, slice, slicepad, nslots;
+  long long* prof;     // optional per-phase cycle counters (rank 0, thread 0), see ILS_RK_PROF
 };
 
 // Ring entries for steps t0 .. t0+31 (one per lane): Philox draw, two weighted inverse-CDF
 // samples on the shared prefix sums, and the scalars the step needs (off the critical path).
 __device__ __forceinline__ void rk_fill_indices(const RkParams& p, const uint64_t* Ss, RkIdx* ring,
-                                                int64_t t0, int lane) {
+                                                int64_t t0, int lane, const double* bh_tab = nullptr,
+                                                const double* rn_tab = nullptr) {
   const int64_t t = t0 + lane;
-  if (t < p.t1) {
+  if (t >= p.t1) {   // masked step (tail of the last block of a chunk): s1 = s2 = 0
+    RkIdx e;
+    e.j1 = 0;
+    e.j2 = 0;
+    e.bh1 = 0.0;
+    e.rn1 = 0.0;
+    e.rn2 = 0.0;
+    ring[t & (RK_RING - 1)] = e;
+  } else {
     const U4 x = draw(p.seed, p.k, (uint64_t)t, kTagRkRgs);
     const int j1 = sample_weighted(((uint64_t)x.y << 32) | x.x, Ss, p.n);
     const int j2 = sample_weighted(((uint64_t)x.w << 32) | x.z, Ss, p.n);
     RkIdx e;
     e.j1 = j1;
     e.j2 = j2;
-    e.bh1 = p.bhat[j1];
-    e.rn1 = 1.0 / p.N[j1];
-    e.rn2 = 1.0 / p.N[j2];
+    if (bh_tab) {   // shared-memory tables: no dependent global loads on the fill path
+      e.bh1 = bh_tab[j1];
+      e.rn1 = rn_tab[j1];
+      e.rn2 = rn_tab[j2];
+    } else {
+      e.bh1 = p.bhat[j1];
+      e.rn1 = 1.0 / p.N[j1];
+      e.rn2 = 1.0 / p.N[j2];
+    }
     ring[t & (RK_RING - 1)] = e;
   }
 }
@@ -284,6 +303,335 @@ __global__ void __launch_bounds__(512, 1) rk_rgs_kernel(RkParams p) {
   if (CC > 1) cluster_sync_all();   // no CTA exits while peers may still access its smem
 }
 
+// ---------------------------------------------------------------------------------------------
+// Blocked variant: B consecutive steps per cluster reduction. The indices of steps t..t+B-1 are
+// known in advance, so every inner product the B steps need can be written in terms of the state
+// (w, r) at the start of the block and the Gram entries of the 2B columns involved:
+//   <a_i, w_i>        = <a_i, w> + sum_{k<i} s1_k <a_i, a_k>
+//   <b_i, r_i + s1_i a_i> = <b_i, r> + sum_{k<i} (s1_k <b_i, a_k> - s2_k <b_i, b_k>) + s1_i <b_i, a_i>
+// (a_i = A1_(j1_i), b_i = A1_(j2_i)). One reduction of NV = (3B^2 + 3B)/2 values replaces B
+// reductions of 3; the scalar recurrence for s1_i, s2_i runs redundantly in every thread, then
+// w += sum s1_i a_i, r += sum (s1_i a_i - s2_i b_i). Identical to B single steps in exact
+// arithmetic (Alg. 2 steps 9 and 11); only the rounding differs.
+template <int B>
+struct RkBlk {
+  static constexpr int NV = (3 * B * B + 3 * B) / 2;
+  __host__ __device__ static constexpr int P(int i) { return i; }
+  __host__ __device__ static constexpr int Q(int i) { return B + i; }
+  __host__ __device__ static constexpr int AA(int i, int k) { return 2 * B + i * (i - 1) / 2 + k; }
+  __host__ __device__ static constexpr int BA(int i, int k) { return 2 * B + B * (B - 1) / 2 + i * (i + 1) / 2 + k; }
+  __host__ __device__ static constexpr int BB(int i, int k) {
+    return 2 * B + B * (B - 1) / 2 + B * (B + 1) / 2 + i * (i - 1) / 2 + k;
+  }
+};
+
+// butterfly reduce-scatter of NVP (power of two <= 32) values over the warp: on return lane l
+// holds the warp sum of value l & (NVP - 1) (NVP - 1 + log2(32 / NVP) shuffles of doubles)
+template <int NVP>
+__device__ __forceinline__ double warp_reduce_scatter(double (&x)[NVP], int lane) {
+#pragma unroll
+  for (int half = NVP / 2; half >= 1; half /= 2) {
+    const bool hi = (lane & half) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double lo_v = x[i], hi_v = x[i + half];
+      const double send = hi ? lo_v : hi_v;
+      const double keep = hi ? hi_v : lo_v;
+      x[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+    }
+  }
+  double v = x[0];
+#pragma unroll
+  for (int o = NVP; o < 32; o *= 2) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int CC, int U, int B>
+__global__ void __launch_bounds__(256, 1) rk_rgs_block_kernel(RkParams p) {
+  using K = RkBlk<B>;
+  static_assert(K::NV <= 32, "block too large for one warp reduce-scatter");
+  constexpr int NVP = K::NV <= 4 ? 4 : (K::NV <= 8 ? 8 : (K::NV <= 16 ? 16 : 32));
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NT = blockDim.x, NW = NT >> 5;
+  const int rank = (CC > 1) ? (int)cluster_ctarank() : 0;
+  const int64_t i0 = (int64_t)rank * p.slice;
+  const int own = (int)((i0 + p.slice <= p.ppad) ? p.slice : (p.ppad > i0 ? p.ppad - i0 : 0));
+  const int NS = p.nslots, SP = p.slicepad;
+  const bool stopped = *(volatile int32_t*)&p.st->inner_conv != 0;
+
+  double* slots = reinterpret_cast<double*>(smem_raw);                 // [NS][2B][slicepad]
+  double* zs = slots + (size_t)NS * 2 * B * SP;                        // [npad]
+  uint64_t* Ss = reinterpret_cast<uint64_t*>(zs + p.npad);             // [n]
+  RkIdx* ring = reinterpret_cast<RkIdx*>(Ss + ((p.n + 1) & ~1));       // [RK_RING]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + RK_RING);        // [NS]
+  double* bh_tab = reinterpret_cast<double*>(bars + 8);                 // [n] b_hat
+  double* rn_tab = bh_tab + ((p.n + 1) & ~1);                          // [n] 1 / N
+  __shared__ __align__(16) double wred[2][8][32];
+  __shared__ __align__(16) double recv1[2][RK_MAXC][32];   // [source rank][value]
+  __shared__ __align__(8) uint64_t bar1[2];
+  __shared__ double chkw[8];
+  __shared__ __align__(16) double tots[8][32];
+  __shared__ double bnorm_s;
+  if (stopped) return;
+
+  for (int64_t j = tid; j < p.npad; j += NT) zs[j] = p.Z[j];
+  for (int j = tid; j < p.n; j += NT) {
+    Ss[j] = p.S[j];
+    bh_tab[j] = p.bhat[j];
+    rn_tab[j] = 1.0 / p.N[j];
+  }
+  for (int64_t e = tid; e < (int64_t)NS * 2 * B * SP; e += NT) slots[e] = 0.0;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    if (CC > 1) {
+      mbar_init(&bar1[0], 1);
+      mbar_init(&bar1[1], 1);
+    }
+    fence_mbar_init();
+    if (CC > 1) {   // CC sources x 32 values x 8 B
+      mbar_arrive_expect_tx(&bar1[0], CC * NVP * 8);
+      mbar_arrive_expect_tx(&bar1[1], CC * NVP * 8);
+    }
+  }
+  double bnorm = 1.0;
+  if (p.t0 == 0) {
+    double v = 0.0;
+    for (int j = tid; j < p.n; j += NT) v = fma(p.bhat[j], p.bhat[j], v);
+    v = warp_sum(v);
+    if (lane == 0) chkw[warp] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < NW; ++w) s += chkw[w];
+      bnorm_s = sqrt(s);
+    }
+    __syncthreads();
+    bnorm = bnorm_s;
+  }
+  __syncthreads();
+  if (CC > 1) cluster_sync_all();
+  if (bnorm == 0.0) {
+    if (rank == 0 && tid == 0) {
+      p.st->inner_steps = 0;
+      p.st->inner_conv = 1;
+    }
+    return;
+  }
+  if (warp == 0) rk_fill_indices(p, Ss, ring, p.t0, lane, bh_tab, rn_tab);
+  if (warp == NW - 1) rk_fill_indices(p, Ss, ring, p.t0 + 32, lane, bh_tab, rn_tab);
+  __syncthreads();
+
+  const uint32_t slice_bytes = (uint32_t)own * sizeof(double);
+  const int issuer = NT - 1;
+  const int64_t nblk = (p.t1 - p.t0 + B - 1) / B;
+  auto issue = [&](int64_t blk, int slot) {   // 2B column slices of block blk
+    double* dst = slots + (size_t)slot * 2 * B * SP;
+    mbar_arrive_expect_tx(&bars[slot], 2 * B * slice_bytes);
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      const RkIdx e = ring[(p.t0 + blk * B + i) & (RK_RING - 1)];
+      bulk_g2s(dst + (2 * i) * SP, p.A1T + (int64_t)e.j1 * p.ppad + i0, slice_bytes, &bars[slot]);
+      bulk_g2s(dst + (2 * i + 1) * SP, p.A1T + (int64_t)e.j2 * p.ppad + i0, slice_bytes, &bars[slot]);
+    }
+  };
+  int64_t issued = (NS < nblk) ? NS : nblk;   // blocks requested
+  if (tid == issuer && own > 0) {
+    fence_proxy_async();
+    for (int64_t b = 0; b < issued; ++b) issue(b, (int)b);
+  }
+
+  double w[U], r[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t i = i0 + tid + u * NT;
+    const bool in = (tid + u * NT < own);
+    w[u] = in ? p.W[i] : 0.0;
+    r[u] = in ? p.Rv[i] : 0.0;
+  }
+
+  int slot = 0;
+  uint32_t ph = 0;
+  double zprev[B];
+#pragma unroll
+  for (int i = 0; i < B; ++i) zprev[i] = 0.0;
+  const bool prof = p.prof && tid == 0;
+  long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tc = clock64();
+#define RKP(i)                         \
+  if (prof) {                          \
+    const long long c_ = clock64();    \
+    pc[i] += c_ - tc;                  \
+    tc = c_;                           \
+  }
+  for (int64_t blk = 0; blk < nblk; ++blk) {
+    const int64_t t = p.t0 + blk * B;
+    const int pb = (int)(blk & 1);
+    const double* cols = slots + (size_t)slot * 2 * B * SP;
+    if (own > 0) mbar_wait(&bars[slot], ph);
+    RKP(0)
+    double acc[NVP];
+#pragma unroll
+    for (int v = 0; v < NVP; ++v) acc[v] = 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = tid + u * NT;
+      double xa[B], xb[B];
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+        xa[i] = cols[(2 * i) * SP + e];
+        xb[i] = cols[(2 * i + 1) * SP + e];
+      }
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+        acc[K::P(i)] = fma(xa[i], w[u], acc[K::P(i)]);
+        acc[K::Q(i)] = fma(xb[i], r[u], acc[K::Q(i)]);
+#pragma unroll
+        for (int k = 0; k < i; ++k) {
+          acc[K::AA(i, k)] = fma(xa[i], xa[k], acc[K::AA(i, k)]);
+          acc[K::BB(i, k)] = fma(xb[i], xb[k], acc[K::BB(i, k)]);
+        }
+#pragma unroll
+        for (int k = 0; k <= i; ++k) acc[K::BA(i, k)] = fma(xb[i], xa[k], acc[K::BA(i, k)]);
+      }
+    }
+    RKP(1)
+    double mine = warp_reduce_scatter<NVP>(acc, lane);   // lane l: warp total of value l % NVP
+    RKP(2)
+    if (NW > 1) {
+      wred[pb][warp][lane] = mine;
+      named_bar_sync(1, NT);
+    }
+    RKP(3)
+    if (blk >= 1 && issued < nblk) {
+      if (tid == issuer && own > 0) issue(issued, slot == 0 ? NS - 1 : slot - 1);
+      ++issued;
+    }
+    double tot;
+    if (CC > 1) {
+      // one-hop cluster all-to-all of the NVP values: warp 0 forms the CTA totals (lane l ->
+      // value l) and sends them to every rank; each st.async instruction targets ONE destination
+      // CTA with NVP contiguous doubles (destination-uniform instructions are ~2x faster than
+      // lane-scattered ones, and one sending warp beat sends spread over warps: tools/dsmem_bench.cu).
+      if (warp == 0) {
+        double v = mine;
+        if (NW > 1) {
+          v = 0.0;
+          for (int w8 = 0; w8 < NW; ++w8) v += wred[pb][w8][lane];
+        }
+        // lane l < NVP/2 carries values 2l, 2l+1 as one 16-byte st.async (half the instructions)
+        const double v0 = __shfl_sync(0xffffffffu, v, (2 * lane) & 31);
+        const double v1 = __shfl_sync(0xffffffffu, v, (2 * lane + 1) & 31);
+        const uint32_t la = smem_u32(&recv1[pb][rank][2 * (lane & (NVP / 2 - 1))]);
+        const uint32_t lb = smem_u32(&bar1[pb]);
+        if (lane < NVP / 2)
+          for (int c = 0; c < CC; ++c) st_async_v2f64(map_shared_rank(la, (uint32_t)c), v0, v1, map_shared_rank(lb, (uint32_t)c));
+      }
+      // deferred z updates of the previous block (sequential order), hidden in the reduction wait
+      if (warp == NW - 1 && lane == 0 && blk > 0) {
+#pragma unroll
+        for (int i = 0; i < B; ++i) zs[ring[(t - B + i) & (RK_RING - 1)].j2] += zprev[i];
+      }
+      if (warp == NW - 1 && ((t - p.t0) & 31) == 0 && t + RK_AHEAD < p.t1 + 64)
+        rk_fill_indices(p, Ss, ring, t + RK_AHEAD, lane, bh_tab, rn_tab);
+      RKP(4)
+      mbar_wait(&bar1[pb], (uint32_t)((blk >> 1) & 1));
+      RKP(5)
+      {
+        double a[CC];
+#pragma unroll
+        for (int c = 0; c < CC; ++c) a[c] = recv1[pb][c][lane & (NVP - 1)];
+#pragma unroll
+        for (int s = 1; s < CC; s *= 2)
+#pragma unroll
+          for (int c = 0; c + s < CC; c += 2 * s) a[c] += a[c + s];
+        tot = a[0];
+      }
+      // re-arm for block blk+2: its data cannot arrive before this CTA sends block blk+1,
+      // which happens after every thread here has passed this wait
+      if (tid == 0) mbar_arrive_expect_tx(&bar1[pb], CC * NVP * 8);
+    } else {
+      if (((t - p.t0) & 31) == 0 && t + RK_AHEAD < p.t1 + 64 && warp == NW - 1)
+        rk_fill_indices(p, Ss, ring, t + RK_AHEAD, lane, bh_tab, rn_tab);
+      if (NW > 1) {
+        tot = 0.0;
+        for (int w8 = 0; w8 < NW; ++w8) tot += wred[pb][w8][lane];
+      } else {
+        tot = mine;
+      }
+    }
+    RKP(6)
+    // every thread gets all NV totals, then runs the B-step scalar recurrence
+    double T[K::NV];
+    tots[warp][lane] = tot;
+    __syncwarp();
+#pragma unroll
+    for (int v = 0; v < K::NV; ++v) T[v] = tots[warp][v];
+    double s1[B], s2[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      const RkIdx ix = ring[(t + i) & (RK_RING - 1)];
+      double dw = T[K::P(i)];
+#pragma unroll
+      for (int k = 0; k < i; ++k) dw = fma(s1[k], T[K::AA(i, k)], dw);
+      s1[i] = (ix.bh1 - dw) * ix.rn1;
+      double dr = T[K::Q(i)];
+#pragma unroll
+      for (int k = 0; k < i; ++k) {
+        dr = fma(s1[k], T[K::BA(i, k)], dr);
+        dr = fma(-s2[k], T[K::BB(i, k)], dr);
+      }
+      dr = fma(s1[i], T[K::BA(i, i)], dr);
+      s2[i] = dr * ix.rn2;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = tid + u * NT;
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+        const double xa = cols[(2 * i) * SP + e], xb = cols[(2 * i + 1) * SP + e];
+        w[u] = fma(s1[i], xa, w[u]);
+        r[u] = fma(s1[i], xa, r[u]);
+        r[u] = fma(-s2[i], xb, r[u]);
+      }
+    }
+    if (warp == NW - 1 && lane == 0) {
+      if (CC > 1) {
+#pragma unroll
+        for (int i = 0; i < B; ++i) zprev[i] = s2[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < B; ++i) zs[ring[(t + i) & (RK_RING - 1)].j2] += s2[i];
+      }
+    }
+    if (++slot == NS) {
+      slot = 0;
+      ph ^= 1u;
+    }
+    RKP(7)
+  }
+#undef RKP
+  if (CC > 1 && warp == NW - 1 && lane == 0 && nblk > 0) {
+    const int64_t tl = p.t0 + (nblk - 1) * B;
+#pragma unroll
+    for (int i = 0; i < B; ++i) zs[ring[(tl + i) & (RK_RING - 1)].j2] += zprev[i];
+  }
+  if (prof)
+    for (int i = 0; i < 8; ++i) p.prof[rank * 8 + i] += pc[i];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (tid + u * NT < own) {
+      const int64_t i = i0 + tid + u * NT;
+      p.W[i] = w[u];
+      p.Rv[i] = r[u];
+    }
+  }
+  __syncthreads();
+  if (rank == 0)
+    for (int64_t j = tid; j < p.npad; j += NT) p.Z[j] = zs[j];
+  if (CC > 1) cluster_sync_all();
+}
+
 __global__ void rk_indices_kernel(RkParams p, int64_t t0, int64_t count, int32_t* j1, int32_t* j2) {
   extern __shared__ __align__(16) uint64_t Ssm[];
   for (int j = threadIdx.x; j < p.n; j += blockDim.x) Ssm[j] = p.S[j];
@@ -346,6 +694,48 @@ static int dispatch_rk_c(Handle& h, RkParams& p, int nt, size_t smem) {
   }
 }
 
+template <int CC, int U, int B>
+static int launch_rkb(Handle& h, RkParams& p, int nt, size_t smem) {
+  auto kern = rk_rgs_block_kernel<CC, U, B>;
+  ILS_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CC);
+  cfg.blockDim = dim3(nt);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = h.stream;
+  cudaLaunchAttribute attr[1];
+  int na = 0;
+  if (CC > 1) {
+    ILS_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CC;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    na = 1;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  ILS_CU(cudaLaunchKernelEx(&cfg, kern, p));
+  ILS_LAUNCHED("rk_rgs_block_kernel");
+  return ILS_OK;
+}
+
+template <int U, int B>
+static int dispatch_rkb_c(Handle& h, RkParams& p, int nt, size_t smem) {
+  switch (p.C) {
+    case 1: return launch_rkb<1, U, B>(h, p, nt, smem);
+    case 2: return launch_rkb<2, U, B>(h, p, nt, smem);
+    case 4: return launch_rkb<4, U, B>(h, p, nt, smem);
+    case 8: return launch_rkb<8, U, B>(h, p, nt, smem);
+    default: return launch_rkb<16, U, B>(h, p, nt, smem);
+  }
+}
+
+static int dispatch_rkb(Handle& h, RkParams& p, int U, int B, int nt, size_t smem) {
+  if (B == 2) return (U == 4) ? dispatch_rkb_c<4, 2>(h, p, nt, smem) : dispatch_rkb_c<8, 2>(h, p, nt, smem);
+  return (U == 4) ? dispatch_rkb_c<4, 4>(h, p, nt, smem) : dispatch_rkb_c<8, 4>(h, p, nt, smem);
+}
+
 static int rk_cluster_size(Handle& h) {
   // one CTA up to 2048 rows; otherwise a cluster of up to 16 CTAs (non-portable size)
   if (h.ppad <= 2048) return 1;
@@ -383,9 +773,20 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
   p.k = (uint32_t)k;
   p.max_inner = max_inner;
   p.st = h.dstat;
-  // launch geometry (fixed for the whole solve)
+  // launch geometry (fixed for the whole solve). Blocked kernel (4 steps per reduction) when the
+  // CTA has <= 256 threads and >= 2 slots of 8 column slices fit; else the single-step kernel.
   int C = rk_cluster_size(h);
+  {
+    const char* e = getenv("ILS_RK_CLUSTER");   // experiment override: cluster size 1..16 (power of 2)
+    if (e && atoi(e) >= 1) C = atoi(e);
+  }
+  int Bk = 4;
+  {
+    const char* e = getenv("ILS_RK_BLOCK");     // experiment override: steps per reduction 1, 2, 4
+    if (e && (atoi(e) == 1 || atoi(e) == 2 || atoi(e) == 4)) Bk = atoi(e);
+  }
   int U = 8, nt = 32;
+  bool blocked = false;
   size_t smem = 0;
   for (;;) {
     p.C = C;
@@ -400,16 +801,20 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
     nt = 32 * nw;
     p.slicepad = U * nt;
     const size_t fixed = (size_t)h.npad * 8 + (size_t)((h.n + 1) & ~1) * 8 + RK_RING * sizeof(RkIdx) + 16 * 8 + 256;
-    const size_t slot_bytes = (size_t)2 * p.slicepad * 8;
     const size_t budget = 200 * 1024;
-    if (fixed + 2 * slot_bytes > budget) {
+    const size_t slot1 = (size_t)2 * p.slicepad * 8, slot4 = (size_t)Bk * slot1;
+    const size_t fixed4 = fixed + 64 + (size_t)2 * ((h.n + 1) & ~1) * 8;   // + b_hat, 1/N tables
+    blocked = !h.rk_single_step && Bk > 1 && nt <= 256 && fixed4 + 2 * slot4 <= budget;
+    const size_t slot_bytes = blocked ? slot4 : slot1;
+    const size_t fixed_used = blocked ? fixed4 : fixed;
+    if (fixed_used + 2 * slot_bytes > budget) {
       set_error("RK-RGS: shared memory too small for this problem size");
       return ILS_ERR_UNSUPPORTED;
     }
-    int NS = (int)((budget - fixed) / slot_bytes);
+    int NS = (int)((budget - fixed_used) / slot_bytes);
     if (NS > 8) NS = 8;
     p.nslots = NS;
-    smem = fixed + (size_t)NS * slot_bytes;
+    smem = fixed_used + (size_t)NS * slot_bytes;
     // probe that a cluster of this size can be scheduled
     if (C > 1) {
       int ncl = 0;
@@ -424,7 +829,8 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
       a.val.clusterDim.z = 1;
       cfg.attrs = &a;
       cfg.numAttrs = 1;
-      auto kern = (U == 4) ? (void*)rk_rgs_kernel<16, 4> : (void*)rk_rgs_kernel<16, 8>;
+      void* kern = blocked ? ((U == 4) ? (void*)rk_rgs_block_kernel<16, 4, 4> : (void*)rk_rgs_block_kernel<16, 8, 4>)
+                           : ((U == 4) ? (void*)rk_rgs_kernel<16, 4> : (void*)rk_rgs_kernel<16, 8>);
       cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess || ncl < 1) {
@@ -443,6 +849,15 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
   // chunks of check_every steps, each followed by the full-GPU inner check; launches are queued
   // ahead (kernels of a stopped solve return at once) and the stop flag is read every kBatch checks
   constexpr int kBatch = 8;
+  long long* prof = nullptr;
+  {
+    const char* e = getenv("ILS_RK_PROF");
+    if (e && e[0] == '1' && blocked) {
+      ILS_CU(cudaMallocAsync(&prof, 16 * 8 * sizeof(long long), st));
+      ILS_CU(cudaMemsetAsync(prof, 0, 16 * 8 * sizeof(long long), st));
+    }
+  }
+  p.prof = prof;
   ILS_CU(cudaEventRecord(h.evk0, st));
   int64_t t = 0, nchecks = 0;
   int pending = 0;
@@ -451,7 +866,8 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
     const int64_t t1 = (t + ce < max_inner) ? t + ce : max_inner;
     p.t0 = t;
     p.t1 = t1;
-    const int r = (U == 4) ? dispatch_rk_c<4>(h, p, nt, smem) : dispatch_rk_c<8>(h, p, nt, smem);
+    const int r = blocked ? dispatch_rkb(h, p, U, Bk, nt, smem)
+                          : ((U == 4) ? dispatch_rk_c<4>(h, p, nt, smem) : dispatch_rk_c<8>(h, p, nt, smem));
     if (r) return r;
     t = t1;
     if (t % ce == 0) {
@@ -475,6 +891,17 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
   ILS_CU(cudaStreamSynchronize(st));
   const int64_t steps = h.hstat->inner_conv ? h.hstat->inner_steps : max_inner;
   (void)conv;
+  if (prof) {
+    long long hp[16 * 8];
+    ILS_CU(cudaMemcpy(hp, prof, sizeof(hp), cudaMemcpyDeviceToHost));
+    cudaFree(prof);
+    const double nb = (double)((steps + Bk - 1) / Bk);
+    for (int rk = 0; rk < p.C; ++rk) {
+      const long long* q = hp + rk * 8;
+      fprintf(stderr, "ILS_RK_PROF k=%lld rank=%d blocks=%.0f cycles/block: wait %.0f local %.0f rscatter %.0f bar %.0f send %.0f recv %.0f sum %.0f rest %.0f\n",
+              (long long)k, rk, nb, q[0] / nb, q[1] / nb, q[2] / nb, q[3] / nb, q[4] / nb, q[5] / nb, q[6] / nb, q[7] / nb);
+    }
+  }
   if (steps_out) *steps_out = steps;
   const double pd = (double)h.p, nd = (double)h.n;
   hot_account(h, 1, (double)steps * 16.0 * pd + (double)(steps / ce) * 8.0 * pd * nd);

@@ -1,17 +1,27 @@
 // scd.cu -- K2b: persistent SP-SCD / SP-RCD inner solver (Alg. 5 steps 5-12).
 //
 // Step t:  alpha_t, tau_t from the index stream (steps 7-8; include/ils.h):
-//          s in tau_t  <=>  pi^{-1}(s) < alpha_t   (every thread tests the indices it owns)
+//          s in tau_t  <=>  pi^{-1}(s) < alpha_t
 //          j_t = argmax_{s in tau_t} r_s^2, ties to the smallest s     (step 9)
 //          sc = r_j / A1bar_jj ; beta_j += sc ; r -= sc A1bar_(j)       (steps 10-11, :697-698)
 // SP-RCD (weighted): j_t drawn from the column-norm weights (Remark 4.1).
-// One CTA of 1024 threads; thread s owns coordinates s, s+1024, ... of r and beta (registers);
-// the Ab_1 row is read from L2/HBM each step. Every check_every steps r = b_hat - A1bar beta
-// is recomputed and the inner stop rule of include/ils.h is applied.
+//
+// The subsets do not depend on the data, so the integer-heavy membership test (a 12-round
+// Feistel inverse per coordinate and step) is taken off the sequential path: before each chunk
+// of check_every steps, scd_masks_kernel evaluates it for the whole chunk on the full GPU and
+// stores, per (step, thread), the bit mask of that thread's coordinates. scd_chunk_kernel (one
+// CTA, r and beta in registers) then only does the data-dependent part per step: masked local
+// argmax -> warp shuffles -> one barrier -> redundant per-warp reduction of the warp winners ->
+// A1bar row j from L2 -> update. The inner check r = b_hat - A1bar beta (include/ils.h) runs
+// between chunks as a full-GPU kernel (scd_check_kernel); r, beta pass through HBM between chunks.
 #include <climits>
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "ils_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace ils {
 
@@ -34,11 +44,12 @@ struct ScdParams {
   const double* N;
   const uint64_t* S;
   const double* bhat;
-  double* beta_out;
+  double* Rv;        // [npad] state r (in/out)
+  double* Bv;        // [npad] state beta (in/out)
+  const uint32_t* masks;   // [t1 - t0][NT] membership bits (SCD mode)
   uint64_t seed;
   uint32_t k;
-  int64_t max_inner, check_every;
-  double inner_tol;
+  int64_t t0, t1;
   int alpha_mode, alpha_k, weighted;
   DevStatus* st;
 };
@@ -64,32 +75,35 @@ __device__ __forceinline__ void scd_make_key(uint64_t seed, uint32_t k, uint64_t
   e.key[11] = d.x;
 }
 
-// Membership bits of this thread's coordinates s = tid + v*NT in tau_t: pi^{-1}(s) < alpha_t.
-template <int V>
-__device__ __forceinline__ uint32_t scd_members(const ScdKey& e, int tid, int NT, int n, uint32_t h,
-                                                uint32_t mask) {
+// masks[(u - t0) * NT + tid] bit v  <=>  coordinate tid + v*NT is in tau_u. One CTA per step.
+__global__ void __launch_bounds__(256) scd_masks_kernel(uint64_t seed, uint32_t k, int64_t t0, int64_t t1, int n,
+                                                        int alpha_mode, int alpha_k, int NT, int V,
+                                                        uint32_t* __restrict__ masks) {
+  __shared__ ScdKey e;
+  const int64_t u = t0 + blockIdx.x;
+  if (u >= t1) return;
+  if (threadIdx.x == 0) scd_make_key(seed, k, (uint64_t)u, n, alpha_mode, alpha_k, 0, nullptr, e);
+  __syncthreads();
   uint32_t key[kFeistelRounds];
 #pragma unroll
   for (int q = 0; q < kFeistelRounds; ++q) key[q] = e.key[q];
-  const uint32_t alpha = e.alpha;
-  uint32_t bits = 0;
-#pragma unroll
-  for (int v = 0; v < V; ++v) {
-    const int s = tid + v * NT;
-    if (s < n && feistel_inverse((uint32_t)s, key, h, mask, (uint32_t)n) < alpha) bits |= 1u << v;
+  const uint32_t h = feistel_half_bits((uint32_t)n), msk = (1u << h) - 1u;
+  for (int th = threadIdx.x; th < NT; th += blockDim.x) {
+    uint32_t bits = 0;
+    for (int v = 0; v < V; ++v) {
+      const int s = th + v * NT;
+      if (s < n && feistel_inverse((uint32_t)s, key, h, msk, (uint32_t)n) < e.alpha) bits |= 1u << v;
+    }
+    masks[(int64_t)blockIdx.x * NT + th] = bits;
   }
-  return bits;
 }
 
-// One CTA of NT <= 256 threads; thread tid owns coordinates s = tid + v*NT (v < V) of r and beta
-// in registers. Per step (software-pipelined): argmax over tau_t (thread -> warp shuffles -> one
-// barrier -> redundant per-warp reduction of the warp winners), then the A1bar row j is loaded
-// from L2 while the membership bits of step t+1 are computed (pure integer work, data-independent).
+// One CTA of NT <= 256 threads runs steps [t0, t1); thread tid owns coordinates s = tid + v*NT
+// (v < V) of r and beta in registers.
 template <int V>
-__global__ void __launch_bounds__(SCD_MAXT, 1) scd_kernel(ScdParams p) {
+__global__ void __launch_bounds__(SCD_MAXT, 1) scd_chunk_kernel(ScdParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* bs = reinterpret_cast<double*>(smem_raw);          // [npad] beta (for checks)
-  double* rNs = bs + p.npad;                                 // [n] 1 / A1bar_jj
+  double* rNs = reinterpret_cast<double*>(smem_raw);         // [n] 1 / A1bar_jj
   uint64_t* Ss = reinterpret_cast<uint64_t*>(rNs + ((p.n + 1) & ~1));
   ScdKey* ring = reinterpret_cast<ScdKey*>(Ss + ((p.n + 1) & ~1));
   __shared__ double wv[2][SCD_MAXW], wr[2][SCD_MAXW];
@@ -99,50 +113,55 @@ __global__ void __launch_bounds__(SCD_MAXT, 1) scd_kernel(ScdParams p) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NT = blockDim.x, NW = NT >> 5;
   const int n = p.n;
-  const uint32_t h = feistel_half_bits((uint32_t)n), mask = (1u << h) - 1u;
+  if (*(volatile int32_t*)&p.st->inner_conv) return;   // inner solve already stopped
 
   for (int j = tid; j < n; j += NT) {
     rNs[j] = 1.0 / p.N[j];
-    Ss[j] = p.S[j];
+    if (p.weighted) Ss[j] = p.S[j];
   }
   double r[V], beta[V];
   double nb2 = 0.0;
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const int s = tid + v * NT;
-    r[v] = (s < n) ? p.bhat[s] : 0.0;
-    beta[v] = 0.0;
-    nb2 = fma(r[v], r[v], nb2);
+    r[v] = (s < n) ? p.Rv[s] : 0.0;
+    beta[v] = (s < n) ? p.Bv[s] : 0.0;
+    if (s < n) nb2 = fma(p.bhat[s], p.bhat[s], nb2);
   }
-  nb2 = warp_sum(nb2);
-  if (lane == 0) red[warp] = nb2;
-  __syncthreads();
-  double B2 = 0.0;
-  for (int w = 0; w < NW; ++w) B2 += red[w];
-  const double bnorm = sqrt(B2);
-  if (bnorm == 0.0) {
-    for (int64_t j = tid; j < p.npad; j += NT) p.beta_out[j] = 0.0;
-    if (tid == 0) {
-      p.st->inner_steps = 0;
-      p.st->inner_conv = 1;
+  if (p.t0 == 0) {   // b_hat = 0: beta = 0 after 0 steps
+    nb2 = warp_sum(nb2);
+    if (lane == 0) red[warp] = nb2;
+    __syncthreads();
+    double B2 = 0.0;
+    for (int w = 0; w < NW; ++w) B2 += red[w];
+    if (B2 == 0.0) {
+      if (tid == 0) {
+        p.st->inner_steps = 0;
+        p.st->inner_conv = 1;
+      }
+      return;
     }
-    return;
   }
-  if (warp == 0) {
+  if (p.weighted && warp == 0) {
     for (int b = 0; b < 2; ++b) {
-      const int64_t t = 32 * b + lane;
-      if (t < p.max_inner)
-        scd_make_key(p.seed, p.k, (uint64_t)t, n, p.alpha_mode, p.alpha_k, p.weighted, Ss,
-                     ring[t & (SCD_RING - 1)]);
+      const int64_t t = p.t0 + 32 * b + lane;
+      if (t < p.t1)
+        scd_make_key(p.seed, p.k, (uint64_t)t, n, p.alpha_mode, p.alpha_k, 1, Ss, ring[t & (SCD_RING - 1)]);
     }
   }
   __syncthreads();
 
-  uint32_t inmask = p.weighted ? 0u : scd_members<V>(ring[0], tid, NT, n, h, mask);
-  int64_t t = 0;
-  int conv = 0;
-  int64_t next_check = p.check_every;
-  for (; t < p.max_inner; ++t) {
+  // membership masks of steps t..t+3 (prefetch queue; the loads of t+4 overlap 4 steps)
+  const uint32_t* mk = p.masks + tid;
+  const int64_t L = p.t1 - p.t0;
+  uint32_t q0 = 0, q1 = 0, q2 = 0, q3 = 0;
+  if (!p.weighted) {
+    q0 = (0 < L) ? __ldcg(mk) : 0u;
+    q1 = (1 < L) ? __ldcg(mk + NT) : 0u;
+    q2 = (2 < L) ? __ldcg(mk + 2 * NT) : 0u;
+    q3 = (3 < L) ? __ldcg(mk + 3 * NT) : 0u;
+  }
+  for (int64_t t = p.t0; t < p.t1; ++t) {
     const int pb = (int)(t & 1);
     int j;
     double rj;
@@ -151,9 +170,19 @@ __global__ void __launch_bounds__(SCD_MAXT, 1) scd_kernel(ScdParams p) {
 #pragma unroll
       for (int v = 0; v < V; ++v)
         if (tid + v * NT == j) rj_s[pb] = r[v];
+      if (warp == NW - 1 && ((t - p.t0) & 31) == 0 && t + SCD_AHEAD + lane < p.t1) {
+        const int64_t tt = t + SCD_AHEAD + lane;
+        scd_make_key(p.seed, p.k, (uint64_t)tt, n, p.alpha_mode, p.alpha_k, 1, Ss, ring[tt & (SCD_RING - 1)]);
+      }
       __syncthreads();
       rj = rj_s[pb];
     } else {
+      const uint32_t inmask = q0;
+      q0 = q1;
+      q1 = q2;
+      q2 = q3;
+      const int64_t ahead = t - p.t0 + 4;
+      q3 = (ahead < L) ? __ldcg(mk + ahead * NT) : 0u;
       // thread-local argmax (coordinates ascend with v: strict > keeps the smallest index)
       double bv = -1.0, br = 0.0;
       int bi = INT_MAX;
@@ -202,78 +231,82 @@ __global__ void __launch_bounds__(SCD_MAXT, 1) scd_kernel(ScdParams p) {
       rj = wr[pb][(j % NT) >> 5];
     }
     const double sc = rj * rNs[j];
-    // A1bar row j (L2): issue the loads, then overlap their latency with step t+1's membership
     const double* grow = p.G + (int64_t)j * p.npad;
-    double g[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int s = tid + v * NT;
-      g[v] = (s < n) ? __ldcg(grow + s) : 0.0;
-    }
-    if (warp == NW - 1 && (t & 31) == 0 && t + SCD_AHEAD + lane < p.max_inner) {
-      const int64_t tt = t + SCD_AHEAD + lane;
-      scd_make_key(p.seed, p.k, (uint64_t)tt, n, p.alpha_mode, p.alpha_k, p.weighted, Ss,
-                   ring[tt & (SCD_RING - 1)]);
-    }
-    if (!p.weighted && t + 1 < p.max_inner)
-      inmask = scd_members<V>(ring[(t + 1) & (SCD_RING - 1)], tid, NT, n, h, mask);
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int s = tid + v * NT;
-      r[v] = fma(-sc, g[v], r[v]);
-      if (s == j) beta[v] += sc;
-    }
-    if (t + 1 == next_check) {
-      next_check += p.check_every;
-      // r = b_hat - A1bar beta (column access of the symmetric A1bar: coalesced), stop test
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const int s = tid + v * NT;
-        if (s < p.npad) bs[s] = beta[v];
-      }
-      __syncthreads();
-      double acc[V];
-#pragma unroll
-      for (int v = 0; v < V; ++v) acc[v] = 0.0;
-      for (int jj = 0; jj < n; ++jj) {
-        const double bj = bs[jj];
-        const double* gr = p.G + (int64_t)jj * p.npad;
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          const int s = tid + v * NT;
-          if (s < n) acc[v] = fma(__ldcg(gr + s), bj, acc[v]);
-        }
-      }
-      double r2 = 0.0;
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const int s = tid + v * NT;
-        if (s < n) {
-          r[v] = p.bhat[s] - acc[v];
-          r2 = fma(r[v], r[v], r2);
-        }
-      }
-      r2 = warp_sum(r2);
-      __syncthreads();
-      if (lane == 0) red[warp] = r2;
-      __syncthreads();
-      double R2 = 0.0;
-      for (int w = 0; w < NW; ++w) R2 += red[w];
-      if (sqrt(R2) <= p.inner_tol * bnorm) {
-        conv = 1;
-        ++t;
-        break;
+      if (s < n) {
+        r[v] = fma(-sc, __ldcg(grow + s), r[v]);
+        if (s == j) beta[v] += sc;
       }
     }
   }
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const int s = tid + v * NT;
-    if (s < p.npad) p.beta_out[s] = (s < n) ? beta[v] : 0.0;
+    if (s < n) {
+      p.Rv[s] = r[v];
+      p.Bv[s] = beta[v];
+    }
   }
-  if (tid == 0) {
-    p.st->inner_steps = t;
-    p.st->inner_conv = conv;
+}
+
+// Inner check (include/ils.h): r = b_hat - A1bar beta, stop if ||r|| <= inner_tol ||b_hat||
+// (sets st->inner_conv, inner_steps = t_now), else the recomputed r replaces the state.
+// Cooperative full grid; warp per row of A1bar; fixed-order reductions.
+__global__ void __launch_bounds__(256) scd_check_kernel(const double* __restrict__ G, int64_t npad, int n,
+                                                        const double* __restrict__ bhat, const double* __restrict__ Bv,
+                                                        double* __restrict__ Rv, double* __restrict__ rtmp,
+                                                        double* __restrict__ red, double inner_tol, int64_t t_now,
+                                                        DevStatus* st) {
+  cg::grid_group grid = cg::this_grid();
+  if (*(volatile int32_t*)&st->inner_conv) return;
+  __shared__ double sr[8][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwg = gridDim.x * 8;
+  double a = 0.0, b = 0.0;
+  for (int j = blockIdx.x * 8 + warp; j < n; j += nwg) {
+    const double2* row = reinterpret_cast<const double2*>(G + (int64_t)j * npad);
+    const double2* bv = reinterpret_cast<const double2*>(Bv);
+    double s = 0.0;
+    for (int c = lane; c < (int)(npad / 2); c += 32) {
+      const double2 g = __ldcg(row + c), x = __ldcg(bv + c);
+      s = fma(g.x, x.x, s);
+      s = fma(g.y, x.y, s);
+    }
+    s = warp_sum(s);
+    const double rj = bhat[j] - s;
+    if (lane == 0) rtmp[j] = rj;
+    a = fma(rj, rj, a);
+    b = fma(bhat[j], bhat[j], b);
+  }
+  if (lane == 0) {
+    sr[warp][0] = a;
+    sr[warp][1] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double A = 0.0, B = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      A += sr[w][0];
+      B += sr[w][1];
+    }
+    red[2 * blockIdx.x] = A;
+    red[2 * blockIdx.x + 1] = B;
+  }
+  grid.sync();
+  double A = 0.0, B = 0.0;
+  for (int c = 0; c < (int)gridDim.x; ++c) {
+    A += red[2 * c];
+    B += red[2 * c + 1];
+  }
+  if (sqrt(A) <= inner_tol * sqrt(B)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->inner_steps = t_now;
+      st->inner_conv = 1;
+    }
+  } else {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) Rv[j] = rtmp[j];
   }
 }
 
@@ -284,8 +317,37 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
     set_error("SP-SCD: n > 8192 not supported by the single-CTA kernel in this release");
     return ILS_ERR_UNSUPPORTED;
   }
-  int r = build_gram(h);
-  if (r) return r;
+  int rc = build_gram(h);
+  if (rc) return rc;
+  const cudaStream_t st = h.stream;
+  const int64_t ce = check_every > 0 ? check_every : h.n;
+  // threads: one coordinate per thread up to 256 coordinates, then V coordinates per thread
+  int nt = (int)((h.n + 31) / 32 * 32);
+  if (nt > SCD_MAXT) nt = SCD_MAXT;
+  const int per = (int)((h.n + nt - 1) / nt);
+  int V = 1;
+  while (V < per) V *= 2;
+  const int64_t chunk_cap = (max_inner < ce) ? max_inner : ce;
+  const size_t state_dbl = (size_t)3 * h.npad + 2 * (size_t)h.num_sms;
+  const size_t mask_bytes = weighted ? 0 : (size_t)chunk_cap * nt * sizeof(uint32_t);
+  const size_t need = state_dbl * sizeof(double) + mask_bytes;
+  if (h.scd_ws_bytes < need) {
+    if (h.scd_ws) cudaFreeAsync(h.scd_ws, st);
+    h.scd_ws = nullptr;
+    h.scd_ws_bytes = 0;
+    ILS_CU(cudaMallocAsync(&h.scd_ws, need, st));
+    h.scd_ws_bytes = need;
+  }
+  double* Rv = reinterpret_cast<double*>(h.scd_ws);
+  double* Bv = Rv + h.npad;
+  double* rtmp = Bv + h.npad;
+  double* red = rtmp + h.npad;
+  uint32_t* masks = reinterpret_cast<uint32_t*>(red + 2 * h.num_sms);
+  ILS_CU(cudaMemsetAsync(Rv, 0, (size_t)3 * h.npad * sizeof(double), st));
+  ILS_CU(cudaMemcpyAsync(Rv, bhat, h.n * sizeof(double), cudaMemcpyDeviceToDevice, st));   // r_0 = b_hat
+  ILS_CU(cudaMemsetAsync(&h.dstat->inner_conv, 0, sizeof(int32_t), st));
+  ILS_CU(cudaMemsetAsync(&h.dstat->inner_steps, 0, sizeof(int64_t), st));
+
   ScdParams p{};
   p.G = h.G;
   p.npad = h.npad;
@@ -293,46 +355,78 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
   p.N = h.N;
   p.S = h.S;
   p.bhat = bhat;
-  p.beta_out = beta;
+  p.Rv = Rv;
+  p.Bv = Bv;
+  p.masks = masks;
   p.seed = seed;
   p.k = (uint32_t)k;
-  p.max_inner = max_inner;
-  p.check_every = check_every > 0 ? check_every : h.n;
-  p.inner_tol = inner_tol;
   p.alpha_mode = alpha_mode;
   p.alpha_k = alpha_k;
   p.weighted = weighted;
   p.st = h.dstat;
-  const size_t smem = (size_t)h.npad * 8 + 2 * (size_t)((h.n + 1) & ~1) * 8 + SCD_RING * sizeof(ScdKey);
-  // threads: one coordinate per thread up to 256 coordinates, then V coordinates per thread
-  int nt = (int)((h.n + 31) / 32 * 32);
-  if (nt > SCD_MAXT) nt = SCD_MAXT;
-  const int per = (int)((h.n + nt - 1) / nt);
-  int V = 1;
-  while (V < per) V *= 2;
-  ILS_CU(cudaEventRecord(h.evk0, h.stream));
-#define SCD_LAUNCH(VV)                                                                              \
-  do {                                                                                              \
-    ILS_CU(cudaFuncSetAttribute(scd_kernel<VV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    scd_kernel<VV><<<1, nt, smem, h.stream>>>(p);                                                   \
-    ILS_LAUNCHED("scd_kernel");                                                                     \
-  } while (0)
+  const size_t smem = 2 * (size_t)((h.n + 1) & ~1) * 8 + SCD_RING * sizeof(ScdKey);
+  void* kern = nullptr;
   switch (V) {
-    case 1: SCD_LAUNCH(1); break;
-    case 2: SCD_LAUNCH(2); break;
-    case 4: SCD_LAUNCH(4); break;
-    case 8: SCD_LAUNCH(8); break;
-    case 16: SCD_LAUNCH(16); break;
-    default: SCD_LAUNCH(32); break;
+    case 1: kern = (void*)scd_chunk_kernel<1>; break;
+    case 2: kern = (void*)scd_chunk_kernel<2>; break;
+    case 4: kern = (void*)scd_chunk_kernel<4>; break;
+    case 8: kern = (void*)scd_chunk_kernel<8>; break;
+    case 16: kern = (void*)scd_chunk_kernel<16>; break;
+    default: kern = (void*)scd_chunk_kernel<32>; break;
   }
-#undef SCD_LAUNCH
-  ILS_CU(cudaEventRecord(h.evk1, h.stream));
-  ILS_CU(cudaMemcpyAsync(h.hstat, h.dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, h.stream));
-  ILS_CU(cudaStreamSynchronize(h.stream));
-  const int64_t steps = h.hstat->inner_steps;
+  ILS_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int nchk = h.num_sms;
+  {
+    int per_sm = 0;
+    ILS_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scd_check_kernel, 256, 0));
+    if (per_sm < 1) return ILS_ERR_UNSUPPORTED;
+  }
+  const double* Gp = h.G;
+  const int64_t npad = h.npad;
+  const int nn = (int)h.n;
+  DevStatus* dst = h.dstat;
+
+  constexpr int kBatch = 8;
+  ILS_CU(cudaEventRecord(h.evk0, st));
+  int64_t t = 0;
+  int pending = 0;
+  while (t < max_inner) {
+    const int64_t t1 = (t + ce < max_inner) ? t + ce : max_inner;
+    if (!weighted) {
+      scd_masks_kernel<<<(unsigned)(t1 - t), 256, 0, st>>>(seed, (uint32_t)k, t, t1, nn, alpha_mode, alpha_k, nt,
+                                                            V, masks);
+      ILS_LAUNCHED("scd_masks_kernel");
+    }
+    p.t0 = t;
+    p.t1 = t1;
+    void* args[] = {&p};
+    ILS_CU(cudaLaunchKernel(kern, dim3(1), dim3(nt), args, smem, st));
+    ILS_LAUNCHED("scd_chunk_kernel");
+    t = t1;
+    if (t % ce == 0) {
+      double itol = inner_tol;
+      int64_t tn = t;
+      void* cargs[] = {(void*)&Gp, (void*)&npad, (void*)&nn, (void*)&bhat, (void*)&Bv, (void*)&Rv,
+                       (void*)&rtmp, (void*)&red, (void*)&itol, (void*)&tn, (void*)&dst};
+      ILS_CU(cudaLaunchCooperativeKernel((void*)scd_check_kernel, dim3(nchk), dim3(256), cargs, 0, st));
+      ILS_LAUNCHED("scd_check_kernel");
+    }
+    if (++pending == kBatch || t >= max_inner) {
+      ILS_CU(cudaMemcpyAsync(h.hstat, h.dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+      ILS_CU(cudaStreamSynchronize(st));
+      pending = 0;
+      if (h.hstat->inner_conv) break;
+    }
+  }
+  ILS_CU(cudaEventRecord(h.evk1, st));
+  ILS_CU(cudaMemsetAsync(beta, 0, h.npad * sizeof(double), st));
+  ILS_CU(cudaMemcpyAsync(beta, Bv, h.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  ILS_CU(cudaMemcpyAsync(h.hstat, h.dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+  ILS_CU(cudaStreamSynchronize(st));
+  const int64_t steps = h.hstat->inner_conv ? h.hstat->inner_steps : max_inner;
   if (steps_out) *steps_out = steps;
   const double nd = (double)h.n;
-  hot_account(h, 2, (double)steps * 8.0 * nd + (double)(steps / p.check_every) * 8.0 * nd * nd);
+  hot_account(h, 2, (double)steps * 8.0 * nd + (double)(steps / ce) * 8.0 * nd * nd);
   return ILS_OK;
 }
 
