@@ -258,8 +258,12 @@ def roofline(steps, peak_hbm, peak_bf16, traffic_map, cfg):
         ach = per_launch_work / (per_launch_ms * 1e-3) / 1e9
         d = {"bound": "hbm", "unit": "GB/s", "peak_note": "measured hbm_gbs (MEASURED_PEAKS.json)"}
     tr = traffic_map.get(f"{cfg}:{c}") if traffic_map else None
+    tr_note = None
+    if isinstance(tr, dict):
+        tr_note = tr.get("note")
+        tr = tr.get("dram_bytes_per_launch")
     d.update({"kernel": KINDS[c], "achieved": round(ach, 3), "peak": round(peak, 2), "frac": round(ach / peak, 5),
-              "traffic": tr, "launches": n[c], "avg_launch_ms": round(per_launch_ms, 5),
+              "traffic": tr, "traffic_note": tr_note, "launches": n[c], "avg_launch_ms": round(per_launch_ms, 5),
               "algorithmic_per_launch": per_launch_work, "share_of_step": round(ms[c] / step_ms, 4)})
     return d
 

@@ -7,6 +7,7 @@
 // n <= 32: lane j owns coordinate j of x, c, z, beta, r (SCD); every reduction is a warp shuffle;
 // no block, cluster or grid synchronisation. Instance i uses seed + i (include/ils.h).
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "ils_internal.h"
@@ -324,6 +325,363 @@ __global__ void __launch_bounds__(32) batched_kernel(BatchParams P) {
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Specialised batched kernels (one warp per instance, lane j = coordinate j, n <= 32).
+// Shared pieces: per-instance prologue (column norms, A1^T b1, sampling table) and the outer
+// right-hand side c_k = A1^T b1 + A2^T (A2 x_k - b2) (Alg. 2 step 5 / Alg. 5 step 4).
+
+// c_k for the warp's instance: lane j returns c_j (A2 rows read from global / L2).
+__device__ __forceinline__ double batched_rhs(const double* __restrict__ A, const double* __restrict__ b, int p,
+                                              int q, int n, double x, double a1tb1, int lane) {
+  const bool act = lane < n;
+  double c = a1tb1;
+  for (int i0 = 0; i0 < q; i0 += 32) {
+    const int i = i0 + lane;
+    double d = 0.0;
+    const double* ar = A + (int64_t)(p + (i < q ? i : 0)) * n;
+    for (int j = 0; j < n; ++j) d = fma(ar[j], __shfl_sync(0xffffffffu, x, j), d);
+    d = (i < q) ? d - b[p + i] : 0.0;
+    const int cnt = (q - i0 < 32) ? q - i0 : 32;
+    for (int ii = 0; ii < cnt; ++ii) {
+      const double di = __shfl_sync(0xffffffffu, d, ii);
+      if (act) c = fma(A[(int64_t)(p + i0 + ii) * n + lane], di, c);
+    }
+  }
+  return c;
+}
+
+// inclusive prefix sums of the integer column weights W_j = max(1, floor(N_j / N_max * 2^32))
+// (include/ils.h) into S[0..31] (lanes >= n contribute 0)
+__device__ __forceinline__ void batched_weights(double Nj, bool act, int lane, uint64_t* S) {
+  double mx = act ? Nj : 0.0;
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  uint64_t w = 0;
+  if (act) {
+    const uint64_t f = (uint64_t)floor(scalbn(__ddiv_rn(Nj, mx), 32));
+    w = f < 1 ? 1 : f;
+  }
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
+    if (lane >= o) w += y;
+  }
+  S[lane] = w;
+}
+
+// SP-RK-RGS, batched (Alg. 2). A1 is shared-memory resident, column-major with
+// rows padded to 32*RPL (zero rows), so the per-step loops carry no bounds. Per step: indices from
+// a 32-step register window (lane l drew step t0+l: Philox, inverse CDF on S, b_hat_{j1}, 1/N),
+// broadcast by shuffles; three dots over RPL rows per lane; three butterfly warp sums; reciprocal
+// multiplies; axpys from the values still in registers. Inner check every check_every steps.
+template <int RPL>
+__global__ void __launch_bounds__(32) batched_rk_kernel(BatchParams P) {
+  extern __shared__ __align__(16) double sm[];
+  constexpr int PP = 32 * RPL;
+  const int lane = threadIdx.x;
+  const int64_t inst = blockIdx.x;
+  const int p = P.p, q = P.q, n = P.n, m = p + q;
+  const double* A = P.A + inst * (int64_t)m * n;
+  const double* b = P.b + inst * (int64_t)m;
+  const uint64_t seed = P.seed + (uint64_t)inst;
+  double* A1T = sm;                                     // [n][PP]
+  double* azs = A1T + n * PP;                           // [PP]
+  double* cs = azs + PP;                                // [32] c_k (for b_hat_{j1} lookups)
+  double* rns = cs + 32;                                // [32] 1 / N_j
+  uint64_t* S = reinterpret_cast<uint64_t*>(rns + 32);  // [32]
+
+  for (int e = lane; e < n * PP; e += 32) {
+    const int j = e / PP, i = e % PP;
+    A1T[e] = (i < p) ? A[(int64_t)i * n + j] : 0.0;
+  }
+  __syncwarp();
+  const bool act = lane < n;
+  double Nj = 0.0, a1tb1 = 0.0;
+  if (act) {
+    for (int i = 0; i < p; ++i) {   // N_j sequential in i without FMA (include/ils.h)
+      const double v = A1T[lane * PP + i];
+      Nj = __dadd_rn(Nj, __dmul_rn(v, v));
+      a1tb1 = fma(v, b[i], a1tb1);
+    }
+  }
+  batched_weights(Nj, act, lane, S);
+  rns[lane] = act ? 1.0 / Nj : 0.0;
+  double x = (act && P.x0) ? P.x0[inst * n + lane] : 0.0;
+  const double xr = (act && P.xref) ? P.xref[inst * n + lane] : 0.0;
+  const double xr2 = warp_sum(xr * xr);
+  __syncwarp();
+
+  const int64_t ce = P.check_every;
+  int64_t it = 0;
+  int conv = 0;
+  unsigned long long inner_sum = 0;
+  for (; it < P.max_iter; ++it) {
+    const double c = batched_rhs(A, b, p, q, n, x, a1tb1, lane);
+    cs[lane] = act ? c : 0.0;
+    const double cnorm = sqrt(warp_sum(act ? c * c : 0.0));
+    __syncwarp();
+    double z = 0.0;
+    int64_t steps = 0;
+    if (cnorm != 0.0) {
+      double w[RPL], r[RPL];
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) w[u] = r[u] = 0.0;
+      int my1 = 0, my2 = 0;
+      double mybh = 0.0, myr1 = 0.0, myr2 = 0.0;
+      int64_t next_check = ce;
+      for (int64_t t = 0; t < P.max_inner; ++t) {
+        const int kk = (int)(t & 31);
+        if (kk == 0) {   // indices and scalars of steps t..t+31, one per lane
+          const U4 xw = draw(seed, (uint32_t)it, (uint64_t)(t + lane), kTagRkRgs);
+          my1 = sample_weighted(((uint64_t)xw.y << 32) | xw.x, S, n);
+          my2 = sample_weighted(((uint64_t)xw.w << 32) | xw.z, S, n);
+          mybh = cs[my1];
+          myr1 = rns[my1];
+          myr2 = rns[my2];
+        }
+        const int j1 = __shfl_sync(0xffffffffu, my1, kk);
+        const int j2 = __shfl_sync(0xffffffffu, my2, kk);
+        const double bh1 = __shfl_sync(0xffffffffu, mybh, kk);
+        const double rn1 = __shfl_sync(0xffffffffu, myr1, kk);
+        const double rn2 = __shfl_sync(0xffffffffu, myr2, kk);
+        const double* a1 = A1T + j1 * PP + lane;
+        const double* a2 = A1T + j2 * PP + lane;
+        double x1[RPL], x2[RPL];
+        double d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+          x1[u] = a1[32 * u];
+          x2[u] = a2[32 * u];
+          d1 = fma(x1[u], w[u], d1);
+          d2 = fma(x2[u], r[u], d2);
+          d3 = fma(x2[u], x1[u], d3);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+          d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+          d3 += __shfl_xor_sync(0xffffffffu, d3, o);
+        }
+        const double s1 = (bh1 - d1) * rn1;
+        const double s2 = (d2 + s1 * d3) * rn2;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+          w[u] = fma(s1, x1[u], w[u]);
+          r[u] = fma(s1, x1[u], r[u]);
+          r[u] = fma(-s2, x2[u], r[u]);
+        }
+        if (lane == j2) z += s2;
+        steps = t + 1;
+        if (steps == next_check) {   // inner stop rule (include/ils.h): g = A1^T A1 z - b_hat
+          next_check += ce;
+          double az[RPL];
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) az[u] = 0.0;
+          double az2[RPL];   // second accumulator: halves the dependent FMA chain
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) az2[u] = 0.0;
+          int j = 0;
+          for (; j + 1 < n; j += 2) {
+            const double zj = __shfl_sync(0xffffffffu, z, j), zk = __shfl_sync(0xffffffffu, z, j + 1);
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {
+              az[u] = fma(A1T[j * PP + lane + 32 * u], zj, az[u]);
+              az2[u] = fma(A1T[(j + 1) * PP + lane + 32 * u], zk, az2[u]);
+            }
+          }
+          if (j < n) {
+            const double zj = __shfl_sync(0xffffffffu, z, j);
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) az[u] = fma(A1T[j * PP + lane + 32 * u], zj, az[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) az[u] += az2[u];
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) {
+            azs[lane + 32 * u] = az[u];
+            r[u] = w[u] - az[u];
+          }
+          __syncwarp();
+          double g = 0.0;
+          if (act) {   // four accumulators over the (zero-padded) rows
+            double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+            const double* col = A1T + lane * PP;
+            for (int i = 0; i < PP; i += 4) {
+              g0 = fma(col[i], azs[i], g0);
+              g1 = fma(col[i + 1], azs[i + 1], g1);
+              g2 = fma(col[i + 2], azs[i + 2], g2);
+              g3 = fma(col[i + 3], azs[i + 3], g3);
+            }
+            g = ((g0 + g1) + (g2 + g3)) - c;
+          }
+          __syncwarp();
+          const double g2 = warp_sum(act ? g * g : 0.0);
+          if (sqrt(g2) <= P.inner_tol * cnorm) break;
+        }
+      }
+    }
+    inner_sum += (unsigned long long)steps;
+    x = act ? z : 0.0;
+    const double e = act ? x - xr : 0.0;
+    const double e2 = warp_sum(e * e);
+    if (P.stop == ILS_STOP_XREF && P.xref && sqrt(e2) <= P.tol * sqrt(xr2)) {
+      conv = 1;
+      ++it;
+      break;
+    }
+  }
+  if (act) P.x[inst * n + lane] = x;
+  if (lane == 0) {
+    if (P.inst_iters) P.inst_iters[inst] = it;
+    if (P.inst_status) P.inst_status[inst] = conv;
+    atomicAdd(P.inner_total, inner_sum);
+  }
+}
+
+// SP-SCD / SP-RCD, batched (Alg. 5). A1bar (n x n) is shared-memory resident
+// (formed once per instance from A1 rows read through L1/L2), so an instance needs ~10 KB and ~20
+// instances share an SM. Per step: the 12 Feistel round keys and alpha_t come from a 32-step key
+// window in shared memory; lane s tests pi^{-1}(s) < alpha_t; warp argmax of r_s^2 (ties to the
+// smallest s); r -= (r_j / A1bar_jj) A1bar_(j) from shared memory.
+__global__ void __launch_bounds__(32) batched_scd_kernel(BatchParams P) {
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x;
+  const int64_t inst = blockIdx.x;
+  const int p = P.p, q = P.q, n = P.n, m = p + q;
+  const double* A = P.A + inst * (int64_t)m * n;
+  const double* b = P.b + inst * (int64_t)m;
+  const uint64_t seed = P.seed + (uint64_t)inst;
+  double* G = sm;                                       // [32][32] A1bar (row j at G + 32 j)
+  uint64_t* S = reinterpret_cast<uint64_t*>(G + 32 * 32);   // [32]
+  BKey* keys = reinterpret_cast<BKey*>(S + 32);             // [32]
+  const bool act = lane < n;
+  // column j of A1 in registers one row at a time: Gram by rank-1 updates over the p rows
+  double g[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) g[i] = 0.0;
+  double Nj = 0.0, a1tb1 = 0.0;
+  for (int k = 0; k < p; ++k) {
+    const double v = act ? A[(int64_t)k * n + lane] : 0.0;
+    Nj = __dadd_rn(Nj, __dmul_rn(v, v));   // N_j sequential in i without FMA (include/ils.h)
+    a1tb1 = fma(v, b[k], a1tb1);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) g[i] = fma(__shfl_sync(0xffffffffu, v, i), v, g[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) G[i * 32 + lane] = g[i];   // G[i][lane] (symmetric)
+  if (P.weighted) batched_weights(Nj, act, lane, S);
+  const double rn = act ? 1.0 / Nj : 0.0;
+  double x = (act && P.x0) ? P.x0[inst * n + lane] : 0.0;
+  const double xr = (act && P.xref) ? P.xref[inst * n + lane] : 0.0;
+  const double xr2 = warp_sum(xr * xr);
+  const uint32_t hb = feistel_half_bits((uint32_t)n), msk = (1u << hb) - 1u;
+  __syncwarp();
+
+  const int64_t ce = P.check_every;
+  int64_t it = 0;
+  int conv = 0;
+  unsigned long long inner_sum = 0;
+  for (; it < P.max_iter; ++it) {
+    const double c = batched_rhs(A, b, p, q, n, x, a1tb1, lane);
+    const double cnorm = sqrt(warp_sum(act ? c * c : 0.0));
+    double rr = act ? c : 0.0, beta = 0.0;
+    int64_t steps = 0;
+    if (cnorm != 0.0) {
+      int64_t next_check = ce;
+      for (int64_t t = 0; t < P.max_inner; ++t) {
+        const int kk = (int)(t & 31);
+        if (kk == 0) {
+          BKey e;
+          const uint64_t tt = (uint64_t)(t + lane);
+          if (P.weighted) {
+            const U4 xw = draw(seed, (uint32_t)it, tt, kTagRcd);
+            e.j = sample_weighted(((uint64_t)xw.y << 32) | xw.x, S, n);
+            e.alpha = 1;
+          } else {
+            const U4 a = draw(seed, (uint32_t)it, tt, kTagScdA);
+            const U4 bb = draw(seed, (uint32_t)it, tt, kTagScdB);
+            const U4 cc = draw(seed, (uint32_t)it, tt, kTagScdC);
+            const U4 dd = draw(seed, (uint32_t)it, tt, kTagScdD);
+            e.alpha = P.alpha_mode == ILS_ALPHA_UNIFORM ? 1u + mulhi32(a.x, (uint32_t)n)
+                                                        : (uint32_t)(P.alpha_k < n ? P.alpha_k : n);
+            e.j = -1;
+            e.key[0] = a.y; e.key[1] = a.z; e.key[2] = a.w;
+            e.key[3] = bb.x; e.key[4] = bb.y; e.key[5] = bb.z; e.key[6] = bb.w;
+            e.key[7] = cc.x; e.key[8] = cc.y; e.key[9] = cc.z; e.key[10] = cc.w;
+            e.key[11] = dd.x;
+          }
+          __syncwarp();
+          keys[lane] = e;
+          __syncwarp();
+        }
+        int j;
+        if (P.weighted) {
+          j = keys[kk].j;
+        } else {
+          uint32_t key[kFeistelRounds];
+#pragma unroll
+          for (int qq = 0; qq < kFeistelRounds; ++qq) key[qq] = keys[kk].key[qq];
+          const uint32_t alpha = keys[kk].alpha;
+          // pi^{-1}(lane) by cycle walking through a table of one-round-trip decryptions of the
+          // whole domain [0, 4^hb) (<= 64 values: lane v holds D(v) and D(v + 32)); a walk step is
+          // then two shuffles instead of a 12-round decryption (the walk diverges across lanes)
+          const uint32_t dom = 1u << (2 * hb);
+          const uint32_t d0 = (n == 1) ? 0u : feistel_decrypt_once((uint32_t)lane & (dom - 1), key, hb, msk);
+          const uint32_t d1 = (n == 1 || dom <= 32) ? 0u : feistel_decrypt_once((uint32_t)lane + 32u, key, hb, msk);
+          uint32_t y = d0;
+          if (n > 1) {
+            while (__any_sync(0xffffffffu, act && y >= (uint32_t)n)) {
+              const uint32_t t0 = __shfl_sync(0xffffffffu, d0, (int)(y & 31)), t1 = __shfl_sync(0xffffffffu, d1, (int)(y & 31));
+              if (act && y >= (uint32_t)n) y = (y < 32) ? t0 : t1;
+            }
+          }
+          double bv = -1.0;
+          int bi = INT_MAX;
+          if (act && y < alpha) {
+            bv = rr * rr;
+            bi = lane;
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (argmax_better(ov, oi, bv, bi)) {
+              bv = ov;
+              bi = oi;
+            }
+          }
+          j = bi;
+        }
+        const double sc = __shfl_sync(0xffffffffu, rr, j) * __shfl_sync(0xffffffffu, rn, j);
+        if (act) rr = fma(-sc, G[j * 32 + lane], rr);
+        if (lane == j) beta += sc;
+        steps = t + 1;
+        if (steps == next_check) {   // inner stop rule: r = b_hat - A1bar beta
+          next_check += ce;
+          double a = 0.0;
+          for (int jj = 0; jj < n; ++jj) a = fma(G[jj * 32 + lane], __shfl_sync(0xffffffffu, beta, jj), a);
+          rr = act ? c - a : 0.0;
+          const double r2 = warp_sum(rr * rr);
+          if (sqrt(r2) <= P.inner_tol * cnorm) break;
+        }
+      }
+    }
+    inner_sum += (unsigned long long)steps;
+    x = act ? beta : 0.0;
+    const double e = act ? x - xr : 0.0;
+    const double e2 = warp_sum(e * e);
+    if (P.stop == ILS_STOP_XREF && P.xref && sqrt(e2) <= P.tol * sqrt(xr2)) {
+      conv = 1;
+      ++it;
+      break;
+    }
+  }
+  if (act) P.x[inst * n + lane] = x;
+  if (lane == 0) {
+    if (P.inst_iters) P.inst_iters[inst] = it;
+    if (P.inst_status) P.inst_status[inst] = conv;
+    atomicAdd(P.inner_total, inner_sum);
+  }
+}
+
 int batched_solve(Handle& h, int method, const double* x0, double* x, double tol, int64_t max_iter,
                   const ils_opts& o, int64_t* inst_iters_dev, int32_t* inst_status_dev) {
   if (h.n > 32 || h.p > 256 || h.q > 4096) {
@@ -354,6 +712,33 @@ int batched_solve(Handle& h, int method, const double* x0, double* x, double tol
   P.inst_iters = inst_iters_dev;
   P.inst_status = inst_status_dev;
   P.inner_total = reinterpret_cast<unsigned long long*>(&h.dstat->inner_steps);
+  if (method == 1) {   // SP-RK-RGS: A1 resident, rows padded to 32*RPL
+    const int rpl = (int)((h.p + 31) / 32);
+    const int RPL = rpl <= 1 ? 1 : rpl <= 2 ? 2 : rpl <= 3 ? 3 : rpl <= 4 ? 4 : 8;
+    const size_t smem = ((size_t)h.n * 32 * RPL + 32 * RPL + 64) * 8 + 32 * 8;
+#define RKLAUNCH(RR)                                                                                 \
+  do {                                                                                               \
+    ILS_CU(cudaFuncSetAttribute(batched_rk_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    batched_rk_kernel<RR><<<(unsigned)h.batch, 32, smem, h.stream>>>(P);                             \
+    ILS_LAUNCHED("batched_rk_kernel");                                                               \
+  } while (0)
+    switch (RPL) {
+      case 1: RKLAUNCH(1); break;
+      case 2: RKLAUNCH(2); break;
+      case 3: RKLAUNCH(3); break;
+      case 4: RKLAUNCH(4); break;
+      default: RKLAUNCH(8); break;
+    }
+#undef RKLAUNCH
+    return ILS_OK;
+  }
+  if (method == 2) {   // SP-SCD / SP-RCD: A1bar resident
+    const size_t smem = (size_t)32 * 32 * 8 + 32 * 8 + 32 * sizeof(BKey);
+    ILS_CU(cudaFuncSetAttribute(batched_scd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    batched_scd_kernel<<<(unsigned)h.batch, 32, smem, h.stream>>>(P);
+    ILS_LAUNCHED("batched_scd_kernel");
+    return ILS_OK;
+  }
   const size_t smem = (size_t)(h.n * h.p + h.n * h.n + h.p) * 8 + 32 * 8 + 32 * sizeof(BKey);
   const int up = (int)((h.p + 31) / 32);
 #define BLAUNCH(UU)                                                                                   \

@@ -24,13 +24,13 @@ int cuda_fail(cudaError_t e, const char* what) {
 }
 void count_launch(int64_t k) { g_launches += k; }
 
-void hot_account(Handle& h, int c, double work) {
+void hot_account(Handle& h, int c, double work, int64_t launches) {
   float ms = 0.f;
   cudaEventSynchronize(h.evk1);
   cudaEventElapsedTime(&ms, h.evk0, h.evk1);
   h.hot_ms[c] += ms;
   h.hot_work[c] += work;
-  h.hot_n[c] += 1;
+  h.hot_n[c] += launches;
 }
 int64_t launches_now() { return g_launches.load(); }
 
@@ -404,9 +404,19 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
       rep->kernel_launches = launches_now() - l0;
       if (rep->inst_iters) std::memcpy(rep->inst_iters, its.data(), B * sizeof(int64_t));
       if (rep->inst_status) std::memcpy(rep->inst_status, sts.data(), B * sizeof(int32_t));
-      const double m = (double)H.m;
-      rep->bytes_touched = (double)B * mx * 8.0 * (double)H.q * (n + 1);
-      (void)m;
+      // algorithmic bytes: per outer step the A2 stream 8q(n+1) (+ 8n^2 for the P
+      // apply of SP), per inner step 16p (RK-RGS: two columns of A1) or 8n (SCD: one row of A1bar)
+      double outer_sum = 0.0;
+      for (int64_t i = 0; i < B; ++i) outer_sum += (double)its[i];
+      const double nd = (double)n, pd = (double)H.p, qd = (double)H.q;
+      double byt = outer_sum * 8.0 * qd * (nd + 1.0);
+      if (method == 0) byt += outer_sum * 8.0 * nd * nd;
+      else if (method == 1) byt += (double)H.hstat->inner_steps * 16.0 * pd;
+      else byt += (double)H.hstat->inner_steps * 8.0 * nd;
+      rep->bytes_touched = byt;
+      rep->hot_ms[method] = rep->solve_ms;
+      rep->hot_work[method] = byt;
+      rep->hot_launches[method] = 1;
     }
     return all ? ILS_OK : ILS_NOT_CONVERGED;
   }

@@ -72,7 +72,8 @@ struct Handle {
 };
 
 // Accumulate the device time between h.evk0 and h.evk1 (already recorded) into class c.
-void hot_account(Handle& h, int c, double work);
+// launches: hot-kernel launches covered by [evk0, evk1] (RK/SCD: chunk kernels, each with its check)
+void hot_account(Handle& h, int c, double work, int64_t launches = 1);
 
 // error plumbing
 void set_error(const std::string& msg);

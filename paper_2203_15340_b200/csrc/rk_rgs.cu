@@ -904,7 +904,7 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
   }
   if (steps_out) *steps_out = steps;
   const double pd = (double)h.p, nd = (double)h.n;
-  hot_account(h, 1, (double)steps * 16.0 * pd + (double)(steps / ce) * 8.0 * pd * nd);
+  hot_account(h, 1, (double)steps * 16.0 * pd + (double)(steps / ce) * 8.0 * pd * nd, (steps + ce - 1) / ce);
   return ILS_OK;
 }
 

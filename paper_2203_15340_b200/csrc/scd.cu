@@ -426,7 +426,7 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
   const int64_t steps = h.hstat->inner_conv ? h.hstat->inner_steps : max_inner;
   if (steps_out) *steps_out = steps;
   const double nd = (double)h.n;
-  hot_account(h, 2, (double)steps * 8.0 * nd + (double)(steps / ce) * 8.0 * nd * nd);
+  hot_account(h, 2, (double)steps * 8.0 * nd + (double)(steps / ce) * 8.0 * nd * nd, (steps + ce - 1) / ce);
   return ILS_OK;
 }
 
