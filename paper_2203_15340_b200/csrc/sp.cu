@@ -22,7 +22,7 @@ namespace ils {
 constexpr int SP_THREADS = 512;
 constexpr int SP_WARPS = SP_THREADS / 32;
 constexpr int SP_RMAX = 16;                 // rows per ring stage (max)
-constexpr int SP_STAGE_TARGET = 32768;      // bytes per ring stage (target)
+constexpr int SP_STAGE_TARGET = 65536;      // bytes per ring stage (target)
 
 struct SpParams {
   const double* Arm;
@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sp_persistent_kernel(SpParams p
   double* reds = ring + NS * stage_dbl;                       // [2][SP_WARPS][SP_RMAX]
   uint64_t* bars = reinterpret_cast<uint64_t*>(reds + 2 * SP_WARPS * SP_RMAX);
   __shared__ double cta_red[SP_WARPS][2];
+  __shared__ double bsm[2 * SP_RMAX];
 
   if (prm.check && *(volatile int32_t*)&prm.st->inner_conv) return;   // inner solve already stopped
   if (tid == 0) {
@@ -111,14 +112,22 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sp_persistent_kernel(SpParams p
       fence_proxy_async();   // order earlier generic smem accesses (cs) before async-proxy writes
       for (int64_t s = 0; s < nst && s < NS; ++s) issue(s);
     }
+    int slot = (int)(gstage % NS);
+    uint32_t par = (uint32_t)((gstage / NS) & 1);
     for (int64_t s = 0; s < nst; ++s) {
       const int64_t g = gstage + s;
-      const int slot = (int)(g % NS);
       const int64_t rs = r0 + s * R;
       const int nr = (int)((rs + R <= r1) ? R : (r1 - rs));
-      mbar_wait(&bars[slot], (uint32_t)((g / NS) & 1));
+      // b_i of this stage's rows: loaded now, consumed after the barrier (latency off the path)
+      double* bst = bsm + (g & 1) * SP_RMAX;
+      if (tid < nr) bst[tid] = prm.b ? prm.b[rs + tid] : 0.0;
+      mbar_wait(&bars[slot], par);
       const double* st = ring + slot * stage_dbl;
       double* red = reds + (g & 1) * SP_WARPS * SP_RMAX;
+      if (++slot == NS) {
+        slot = 0;
+        par ^= 1u;
+      }
       for (int rr = 0; rr < nr; ++rr) {
         const double2* row = reinterpret_cast<const double2*>(st + rr * npad);
         double d = 0.0;
@@ -142,7 +151,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sp_persistent_kernel(SpParams p
         for (int w = 0; w < SP_WARPS; ++w) d += red[w * SP_RMAX + rr];
         const int64_t i = rs + rr;
         if (prm.az_out && tid == 0) prm.az_out[i] = d;
-        if (prm.b) d -= prm.b[i];
+        d -= bst[rr];
         if (i < prm.p) d = -d;          // sigma_i = -1 on A1 rows (correction form only)
         const double2* row = reinterpret_cast<const double2*>(st + rr * npad);
 #pragma unroll
@@ -227,13 +236,29 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sp_persistent_kernel(SpParams p
     double e2 = 0.0, r2 = 0.0;
     for (int64_t i = (int64_t)bid * SP_WARPS + warp; i < npad; i += (int64_t)G * SP_WARPS) {
       const double2* pr = reinterpret_cast<const double2*>(prm.P + i * npad);
-      double s = 0.0;
-      for (int64_t c = lane; c < np2; c += 32) {
-        const double2 v = pr[c];
-        s = fma(v.x, cs[2 * c], s);
-        s = fma(v.y, cs[2 * c + 1], s);
+      const double2* cs2 = reinterpret_cast<const double2*>(cs);
+      // 8 independent 16-byte loads in flight per lane (a P row is streamed from HBM once)
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int64_t c = lane;
+      for (; c + 7 * 32 < np2; c += 8 * 32) {
+        double2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcs(pr + c + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+          const double2 x0 = cs2[c + 32 * u], x1 = cs2[c + 32 * (u + 1)];
+          s0 = fma(v[u].x, x0.x, s0);
+          s1 = fma(v[u].y, x0.y, s1);
+          s2 = fma(v[u + 1].x, x1.x, s2);
+          s3 = fma(v[u + 1].y, x1.y, s3);
+        }
       }
-      s = warp_sum(s);
+      for (; c < np2; c += 32) {
+        const double2 v = __ldcs(pr + c), x0 = cs2[c];
+        s0 = fma(v.x, x0.x, s0);
+        s1 = fma(v.y, x0.y, s1);
+      }
+      double s = warp_sum((s0 + s1) + (s2 + s3));
       if (i >= prm.n) s = 0.0;
       const double xn = prm.sp_form ? xcur[i] + s : s;
       if (lane == 0) {

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--fixed", type=int, default=0, help="fixed horizon: 1 outer x FIXED inner steps, no stopping")
     ap.add_argument("--check-every", type=int, default=0)
+    ap.add_argument("--sp-form", type=int, default=0)
     a = ap.parse_args()
     t0 = time.time()
     pr = make_problem(a.config)
@@ -52,6 +53,7 @@ def main():
             x = torch.zeros(B * n, dtype=torch.float64, device=dev)
             o = ils.ils_default_opts(x_ref=xr.data_ptr(), inner_tol=itol, max_inner=a.max_inner,
                                      check_every=a.check_every)
+            o.sp_form = a.sp_form
             max_iter = a.max_iter
             if a.fixed:
                 o.stop, o.inner_tol, o.max_inner, max_iter = ils.ILS_STOP_NONE, 0.0, a.fixed, 1
