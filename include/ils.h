@@ -96,10 +96,14 @@ enum { ILS_ALPHA_UNIFORM = 0, ILS_ALPHA_FIXED = 1 };
 
 /* Optional creation extras; NULL = dense, batch 1, lda = n, default stream. */
 typedef struct {
-  int32_t format;            /* ILS_FORMAT_DENSE (CSR: ILS_ERR_UNSUPPORTED in this release) */
+  int32_t format;            /* ILS_FORMAT_DENSE or ILS_FORMAT_CSR (BASELINE.json configs[3]) */
   int64_t batch;             /* >= 1. batch > 1: A is [batch][m][lda], b is [batch][m]; one CTA per instance */
   int64_t lda;               /* row stride of A in elements (0 = n) */
   void* stream;              /* cudaStream_t */
+  /* ILS_FORMAT_CSR (batch 1): A points to the nnz values; rows 0..p-1 are A1, p..m-1 are A2. */
+  const int64_t* row_ptr;    /* [m + 1], row_ptr[0] = 0, non-decreasing, row_ptr[m] = nnz */
+  const int32_t* col_idx;    /* [nnz], 0 <= col < n, strictly increasing within each row */
+  int64_t nnz;
 } ils_ext;
 
 /* Solver options; ils_default_opts() fills the defaults given in brackets. */
@@ -146,7 +150,12 @@ ILS_API const char* ils_last_error(void);
 /* Ingest A (m x n, row-major, stride ext->lda) and b (m). Builds the handle's device copies:
  * row-major [A1; A2] padded to a multiple of 64 columns, column-major A1 (for RK/RGS
  * columns), the column norms N_j, the weight prefix sums S_j, and A1^T b1
- * (Alg. 2 step 3 / Alg. 5 step 2). */
+ * (Alg. 2 step 3 / Alg. 5 step 2).
+ * CSR input (ext->format = ILS_FORMAT_CSR): the CSR arrays are validated (ILS_ERR_ARG on an
+ * out-of-range / unsorted / duplicated column, a bad row pointer or a non-finite value) and
+ * converted to CSC for A1 and A2 (columns sorted by row). SP forms A1^T A1 densely (n <= 29000);
+ * SP-SCD uses it compacted to CSR; sp_form = 1 and the weighted SP-RCD mode return
+ * ILS_ERR_UNSUPPORTED for CSR input in this release. */
 ILS_API int ils_create(ils_handle* h, const double* A, const double* b,
                int64_t p, int64_t q, int64_t n, const ils_ext* ext);
 

@@ -27,6 +27,12 @@ from . import index_stream as ix
 # ----------------------------------------------------------------------------
 
 
+def _dense(M) -> np.ndarray:
+    """A scipy.sparse result (sparse CSR inputs, config c3) as a dense ndarray; identity otherwise.
+    Densifying changes no value: it only lets a dense library routine (Cholesky) take the step."""
+    return M.toarray() if hasattr(M, "toarray") else np.asarray(M)
+
+
 def apply_J(p: int, v: np.ndarray) -> np.ndarray:
     """J v with J = diag(I_p, -I_q)."""
     w = np.array(v, dtype=np.float64, copy=True)
@@ -36,7 +42,7 @@ def apply_J(p: int, v: np.ndarray) -> np.ndarray:
 
 def normal_matrix(A1: np.ndarray, A2: np.ndarray) -> np.ndarray:
     """M = A^T J A = A1^T A1 - A2^T A2, symmetrised (M + M^T)/2."""
-    M = A1.T @ A1 - A2.T @ A2
+    M = _dense(A1.T @ A1 - A2.T @ A2)
     return 0.5 * (M + M.T)
 
 
@@ -144,7 +150,7 @@ def sp_solve(A1, A2, b1, b2, x0=None, tol=1e-8, max_iter=20000, stop=STOP_XREF,
     (SPEC reading, DESIGN.md R12). sp_form 0: x_{k+1} = P c_k with c_k = sp_rhs(x_k);
     sp_form 1 (correction form, identical in exact arithmetic): x_{k+1} = x_k + P A^T J (b - A x_k)."""
     n = A1.shape[1]
-    L = np.linalg.cholesky(A1.T @ A1)
+    L = np.linalg.cholesky(_dense(A1.T @ A1))
 
     def apply_P(v):
         return sla.solve_triangular(L.T, sla.solve_triangular(L, v, lower=True), lower=False)

@@ -365,6 +365,12 @@ int build_gram(Handle& h) {
   if (h.have_gram) return ILS_OK;
   const int64_t np = h.npad;
   if (!h.G) ILS_CU(cudaMallocAsync(&h.G, (size_t)np * np * sizeof(double), h.stream));
+  if (h.sparse) {
+    int r = sparse_gram(h, h.G, false);
+    if (r) return r;
+    h.have_gram = true;
+    return ILS_OK;
+  }
   const int64_t tiles = (np / 64) * (np / 64 + 1) / 2;
   const int sp = pick_splits(h, tiles, h.ppad);
   int r = gemm_launch<false, false>(h, np, np, h.ppad, 1.0, h.A1T, h.ppad, h.A1T, h.ppad, 0.0, h.G, np,

@@ -144,6 +144,12 @@ static void free_handle_impl(Handle* h) {
     if (p) cudaFreeAsync(p, s);
   if (h->S) cudaFreeAsync(h->S, s);
   if (h->scd_ws) cudaFreeAsync(h->scd_ws, s);
+  {
+    void* sb[] = {h->rp, h->ci, h->va, h->cp1, h->cr1, h->cv1, h->cp2, h->cr2, h->cv2, h->sp_y, h->gcsr_ptr,
+                  h->gcsr_col, h->gcsr_val};
+    for (void* q : sb)
+      if (q) cudaFreeAsync(q, s);
+  }
   if (h->dstat) cudaFreeAsync(h->dstat, s);
   cudaStreamSynchronize(s);
   if (h->hstat) cudaFreeHost(h->hstat);
@@ -221,9 +227,14 @@ int ils_create(ils_handle* out, const double* A, const double* b, int64_t p, int
     set_error("ils_create: need p >= 1, q >= 0, n >= 1, p >= n, lda >= n");
     return ILS_ERR_SHAPE;
   }
-  if (ext && ext->format != ILS_FORMAT_DENSE) {
-    set_error("ils_create: CSR input is not implemented in this release");
-    return ILS_ERR_UNSUPPORTED;
+  const bool csr = ext && ext->format == ILS_FORMAT_CSR;
+  if (ext && ext->format != ILS_FORMAT_DENSE && !csr) {
+    set_error("ils_create: unknown format");
+    return ILS_ERR_ARG;
+  }
+  if (csr && (batch != 1 || !ext->row_ptr || !ext->col_idx || ext->nnz < 0)) {
+    set_error("ils_create: CSR input needs batch 1, row_ptr, col_idx and nnz >= 0");
+    return ILS_ERR_ARG;
   }
   ils_handle_s* h = new ils_handle_s();
   h->p = p;
@@ -279,6 +290,62 @@ int ils_create(ils_handle* out, const double* A, const double* b, int64_t p, int
   h->npad = roundup(n, kPad);
   h->ppad = roundup(p, kPad);
   const int64_t np = h->npad;
+  if (csr) {   // ---- CSR input (sparse.cu)
+    const int64_t nnz = ext->nnz;
+    h->sparse = true;
+    h->nnz = nnz;
+    CKC(cudaMallocAsync(&h->rp, (size_t)(m + 1) * sizeof(int64_t), st));
+    CKC(cudaMallocAsync(&h->ci, (size_t)(nnz > 0 ? nnz : 1) * sizeof(int32_t), st));
+    CKC(cudaMallocAsync(&h->va, (size_t)(nnz > 0 ? nnz : 1) * sizeof(double), st));
+    CKC(cudaMemcpyAsync(h->rp, ext->row_ptr, (size_t)(m + 1) * sizeof(int64_t), cudaMemcpyDefault, st));
+    if (nnz > 0) {
+      CKC(cudaMemcpyAsync(h->ci, ext->col_idx, (size_t)nnz * sizeof(int32_t), cudaMemcpyDefault, st));
+      CKC(cudaMemcpyAsync(h->va, A, (size_t)nnz * sizeof(double), cudaMemcpyDefault, st));
+    }
+    CKC(cudaMallocAsync(&h->b, (size_t)(m + 64) * sizeof(double), st));
+    CKC(cudaMemsetAsync(h->b, 0, (size_t)(m + 64) * sizeof(double), st));
+    CKC(cudaMemcpyAsync(h->b, b, m * sizeof(double), cudaMemcpyDefault, st));
+    {
+      int64_t ends[2] = {0, 0};
+      CKC(cudaMemcpyAsync(&ends[0], h->rp, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      CKC(cudaMemcpyAsync(&ends[1], h->rp + m, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      CKC(cudaMemcpyAsync(&h->nnz1, h->rp + p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      CKC(cudaStreamSynchronize(st));
+      if (ends[0] != 0 || ends[1] != nnz) {
+        set_error("ils_create: CSR row_ptr[0] must be 0 and row_ptr[m] = nnz");
+        return fail(ILS_ERR_ARG);
+      }
+    }
+    CK(check_finite(*h, h->b, 1, m, m, &ok));
+    if (!ok) {
+      set_error("ils_create: non-finite entry in b");
+      return fail(ILS_ERR_ARG);
+    }
+    CKC(cudaMallocAsync(&h->N, (size_t)n * sizeof(double), st));
+    CKC(cudaMallocAsync(&h->S, (size_t)n * sizeof(uint64_t), st));
+    CKC(cudaMallocAsync(&h->a1tb1, (size_t)np * sizeof(double), st));
+    CK(sparse_ingest(*h, &h->dstat->flag_err, &ok));
+    if (!ok) {
+      set_error("ils_create: invalid CSR structure (row_ptr, column order/range) or non-finite value");
+      return fail(ILS_ERR_ARG);
+    }
+    CKC(cudaMemsetAsync(&h->dstat->flag_err, 0, sizeof(int32_t), st));
+    CK(launch_weights(*h, &h->dstat->flag_err));
+    h->part_rows = h->num_sms > 16 ? h->num_sms : 16;
+    CKC(cudaMallocAsync(&h->part, (size_t)h->part_rows * np * sizeof(double), st));
+    CKC(cudaMallocAsync(&h->red, (size_t)h->part_rows * 4 * sizeof(double), st));
+    CKC(cudaMallocAsync(&h->vec, (size_t)8 * np * sizeof(double), st));
+    CKC(cudaMemsetAsync(h->vec, 0, (size_t)8 * np * sizeof(double), st));
+    int32_t zf = 0;
+    CKC(cudaMemcpyAsync(&zf, &h->dstat->flag_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CKC(cudaStreamSynchronize(st));
+    if (zf) {
+      set_error("ils_create: A1 has a zero column");
+      return fail(ILS_ERR_ZERO_COLUMN);
+    }
+    *out = h;
+    return ILS_OK;
+  }
   CKC(cudaMallocAsync(&h->Arm, (size_t)(m + 64) * np * sizeof(double), st));
   CKC(cudaMemsetAsync(h->Arm, 0, (size_t)(m + 64) * np * sizeof(double), st));
   CKC(cudaMemcpy2DAsync(h->Arm, np * sizeof(double), A, lda * sizeof(double), n * sizeof(double), m,
@@ -422,6 +489,14 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
   }
 
   const int64_t np = H.npad;
+  if (H.sparse && (o.sp_form == 1 || (method == 2 && o.weighted))) {
+    set_error("CSR input: sp_form = 1 and weighted SP-RCD are not implemented in this release");
+    return ILS_ERR_UNSUPPORTED;
+  }
+  // full residual g = A^T J (b - A x): dense stream kernel or the sparse row/column passes
+  auto full_res = [&](const double* xv, double* gv) -> int {
+    return H.sparse ? sparse_rhs(H, xv, gv, 1) : full_residual(H, xv, gv);
+  };
   // ---- setup (timed separately)
   ILS_CU(cudaMemsetAsync(&H.dstat->flag_err, 0, sizeof(int32_t), st));
   const bool gram_new = !H.have_gram && method != 1, inv_new = !H.have_P && method == 0;
@@ -451,7 +526,7 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
   if (o.stop == ILS_STOP_RR) {
     double* zero = H.vec + 4 * np;
     ILS_CU(cudaMemsetAsync(zero, 0, np * sizeof(double), st));
-    if ((rc = full_residual(H, zero, g))) return rc;
+    if ((rc = full_res(zero, g))) return rc;
     if ((rc = dot_host(H, g, g, n, &ajb2))) return rc;
     if (ajb2 == 0.0) {
       set_error("A^T J b = 0: RR undefined");
@@ -473,7 +548,7 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
   if (sx0.d()) ILS_CU(cudaMemcpyAsync(xk, sx0.d(), n * sizeof(double), cudaMemcpyDeviceToDevice, st));
   std::vector<int64_t> inner_hist;
 
-  if (method == 0 && o.stop != ILS_STOP_RR) {
+  if (method == 0 && o.stop != ILS_STOP_RR && !H.sparse) {
     // whole SP loop in one persistent cooperative launch
     const int stop = (o.stop == ILS_STOP_XREF) ? ILS_STOP_XREF : ILS_STOP_NONE;
     if (max_iter > 0) {
@@ -485,7 +560,13 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
   } else {
     for (int64_t k = 0; k < max_iter; ++k) {
       int64_t steps = 0;
-      if (method == 0) {   // SP under the RR rule: one persistent step at a time
+      if (method == 0 && H.sparse) {   // sparse SP: c_k by the row/column passes, x = P c_k
+        ILS_CU(cudaEventRecord(H.evk0, st));
+        if ((rc = sparse_rhs(H, xk, bhat, 0))) return rc;
+        if ((rc = gemv_p(H, bhat, xnew))) return rc;
+        ILS_CU(cudaEventRecord(H.evk1, st));
+        hot_account(H, 0, 12.0 * (double)(H.nnz - H.nnz1) + 16.0 * (double)H.q + 8.0 * (double)np * (double)np);
+      } else if (method == 0) {   // SP under the RR rule: one persistent step at a time
         int64_t one = 0;
         double mm;
         int cc;
@@ -494,14 +575,20 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
           return rc;
       } else {
         // b_hat = A2bar x_k + A^T J b (K1 stream, rhs_only)
-        if ((rc = sp_run(H, xk, nullptr, 0.0, 1, ILS_STOP_NONE, nullptr, 0, nullptr, true, bhat, nullptr, nullptr,
-                         nullptr)))
+        if (H.sparse) {
+          if ((rc = sparse_rhs(H, xk, bhat, 0))) return rc;
+        } else if ((rc = sp_run(H, xk, nullptr, 0.0, 1, ILS_STOP_NONE, nullptr, 0, nullptr, true, bhat, nullptr,
+                                nullptr, nullptr))) {
           return rc;
+        }
         if (method == 1)
-          rc = rk_rgs_inner(H, bhat, xnew, o.seed, k, o.max_inner, o.check_every, o.inner_tol, &steps);
+          rc = H.sparse ? sparse_rk_inner(H, bhat, xnew, o.seed, k, o.max_inner, o.check_every, o.inner_tol, &steps)
+                        : rk_rgs_inner(H, bhat, xnew, o.seed, k, o.max_inner, o.check_every, o.inner_tol, &steps);
         else
-          rc = scd_inner(H, bhat, xnew, o.seed, k, o.max_inner, o.check_every, o.inner_tol, o.alpha_mode, o.alpha_k,
-                         o.weighted, &steps);
+          rc = H.sparse ? sparse_scd_inner(H, bhat, xnew, o.seed, k, o.max_inner, o.check_every, o.inner_tol,
+                                           o.alpha_mode, o.alpha_k, &steps)
+                        : scd_inner(H, bhat, xnew, o.seed, k, o.max_inner, o.check_every, o.inner_tol, o.alpha_mode,
+                                    o.alpha_k, o.weighted, &steps);
         if (rc) return rc;
       }
       ILS_CU(cudaMemcpyAsync(xk, xnew, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -517,7 +604,7 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
         ILS_CU(cudaStreamSynchronize(st));
         done = metric <= tol;
       } else if (o.stop == ILS_STOP_RR) {
-        if ((rc = full_residual(H, xk, g))) return rc;
+        if ((rc = full_res(xk, g))) return rc;
         double gg = 0.0;
         if ((rc = dot_host(H, g, g, n, &gg))) return rc;
         metric = gg / ajb2;
@@ -545,7 +632,13 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
     rep->setup_ms = setup_ms;
     rep->solve_ms = solve_ms;
     const double q = (double)H.q, p = (double)H.p, nd = (double)n;
-    if (method == 0)
+    if (H.sparse) {   // algorithmic bytes of the sparse path (12 B per CSR/CSC entry)
+      const double a2 = 12.0 * (double)(H.nnz - H.nnz1) * 2.0 + 16.0 * q;
+      const double rk_step = 2.0 * ((double)H.nnz1 / nd) * 28.0;
+      const double scd_step = 12.0 * ((double)H.gnnz / nd);
+      rep->bytes_touched = outer * a2 + (method == 0 ? outer * 8.0 * (double)np * (double)np
+                                                     : inner_total * (method == 1 ? rk_step : scd_step));
+    } else if (method == 0)
       rep->bytes_touched = outer * (8.0 * q * (nd + 1) + 8.0 * nd * nd);
     else if (method == 1)
       rep->bytes_touched = outer * 8.0 * q * (nd + 1) + inner_total * 16.0 * p;
@@ -591,7 +684,9 @@ int ils_direct_solve(ils_handle h, double* x) {
   ILS_CU(cudaMemcpyAsync(M, H.G, bytes, cudaMemcpyDeviceToDevice, st));
   // M -= A2^T A2 : opA(i,k) = A2[k][i] (M-contiguous), opB(j,k) = A2[k][j] (N-contiguous)
   const int64_t kq = roundup(H.q, 32);
-  if (H.q > 0) {
+  if (H.sparse) {
+    if (H.q > 0) rc = sparse_gram(H, M, true);
+  } else if (H.q > 0) {
     rc = gemm_dmma(H, true, true, np, np, kq, -1.0, H.Arm + H.p * np, np, H.Arm + H.p * np, np, 1.0, M, np, true, 1);
     if (!rc) rc = mirror_lower(H, M, np, np, n);
   }
@@ -601,7 +696,14 @@ int ils_direct_solve(ils_handle h, double* x) {
   double* rhs = H.vec + 4 * np;
   double* y = H.vec + 5 * np;
   double* xd = H.vec + 6 * np;
-  if (!rc) rc = launch_gemv_cols(H.Arm + H.p * np, np, H.q, np, H.b + H.p, rhs, -1.0, H.a1tb1, st);
+  if (!rc) {
+    if (H.sparse) {   // A^T J (b - A 0) by the sparse passes
+      ILS_CU(cudaMemsetAsync(xd, 0, np * sizeof(double), st));
+      rc = sparse_rhs(H, xd, rhs, 1);
+    } else {
+      rc = launch_gemv_cols(H.Arm + H.p * np, np, H.q, np, H.b + H.p, rhs, -1.0, H.a1tb1, st);
+    }
+  }
   if (!rc) rc = launch_gemv_rows(Zm, np, np, np, rhs, y, 1.0, nullptr, st);
   if (!rc) rc = launch_gemv_cols(Zm, np, np, np, y, xd, 1.0, nullptr, st);
   int32_t f = 0;
@@ -636,8 +738,9 @@ int ils_relative_residual(ils_handle h, const double* x, double* rr) {
   if (rc) return rc;
   double* xz = H.vec + 4 * np;
   double* g = H.vec + 5 * np;
+  auto fres = [&](const double* xv, double* gv) { return H.sparse ? sparse_rhs(H, xv, gv, 1) : full_residual(H, xv, gv); };
   ILS_CU(cudaMemsetAsync(xz, 0, np * sizeof(double), st));
-  if ((rc = full_residual(H, xz, g))) return rc;
+  if ((rc = fres(xz, g))) return rc;
   double den = 0.0, num = 0.0;
   if ((rc = dot_host(H, g, g, n, &den))) return rc;
   if (den == 0.0) {
@@ -645,7 +748,7 @@ int ils_relative_residual(ils_handle h, const double* x, double* rr) {
     return ILS_ERR_ARG;
   }
   ILS_CU(cudaMemcpyAsync(xz, sx.d(), n * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  if ((rc = full_residual(H, xz, g))) return rc;
+  if ((rc = fres(xz, g))) return rc;
   if ((rc = dot_host(H, g, g, n, &num))) return rc;
   *rr = num / den;
   return ILS_OK;

@@ -60,6 +60,25 @@ struct Handle {
   DevStatus* dstat = nullptr;
   DevStatus* hstat = nullptr;  // pinned host mirror
 
+  // CSR input (BASELINE.json configs[3])
+  bool sparse = false;
+  int64_t nnz = 0, nnz1 = 0;
+  int64_t* rp = nullptr;    // [m+1]
+  int32_t* ci = nullptr;    // [nnz]
+  double* va = nullptr;     // [nnz]
+  int64_t* cp1 = nullptr;   // CSC of A1: [n+1], rows sorted
+  int32_t* cr1 = nullptr;
+  double* cv1 = nullptr;
+  int64_t* cp2 = nullptr;   // CSC of A2 (row indices relative to p)
+  int32_t* cr2 = nullptr;
+  double* cv2 = nullptr;
+  double* sp_y = nullptr;   // [m] row-pass scratch
+  int64_t* gcsr_ptr = nullptr;   // A1bar compacted to CSR (SP-SCD)
+  int32_t* gcsr_col = nullptr;
+  double* gcsr_val = nullptr;
+  int64_t gnnz = 0;
+  size_t rk_state_words = 0;
+
   // batched layout
   double* Ab = nullptr;     // [batch][m][n]
   double* bb = nullptr;     // [batch][m]
@@ -139,6 +158,19 @@ int scd_subset_mask(int64_t n, uint64_t seed, int64_t k, int64_t t, int alpha_mo
 
 // small vector kernels (sp.cu)
 int stop_metric(Handle& h, const double* x, const double* xref, double* out_dev);
+
+// sparse.cu (CSR input)
+int sparse_ingest(Handle& h, int32_t* d_flag, bool* ok);
+int sparse_gram(Handle& h, double* G, bool subtract_a2);
+int sparse_rhs(Handle& h, const double* x, double* c, int full);
+int gemv_p(Handle& h, const double* c, double* x);
+int sparse_rk_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_t k, int64_t max_inner,
+                    int64_t check_every, double inner_tol, int64_t* steps_out);
+int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_t k, int64_t max_inner,
+                     int64_t check_every, double inner_tol, int alpha_mode, int alpha_k, int64_t* steps_out);
+// scd.cu: membership masks of steps [t0, t1) for NT threads x V coordinates
+int scd_masks(Handle& h, uint64_t seed, int64_t k, int64_t t0, int64_t t1, int alpha_mode, int alpha_k, int NT, int V,
+              uint32_t* masks);
 
 // batched.cu
 int batched_solve(Handle& h, int method, const double* x0, double* x, double tol, int64_t max_iter,

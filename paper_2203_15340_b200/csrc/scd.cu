@@ -310,6 +310,15 @@ __global__ void __launch_bounds__(256) scd_check_kernel(const double* __restrict
   }
 }
 
+int scd_masks(Handle& h, uint64_t seed, int64_t k, int64_t t0, int64_t t1, int alpha_mode, int alpha_k, int NT, int V,
+              uint32_t* masks) {
+  if (t1 <= t0) return ILS_OK;
+  scd_masks_kernel<<<(unsigned)(t1 - t0), 256, 0, h.stream>>>(seed, (uint32_t)k, t0, t1, (int)h.n, alpha_mode, alpha_k,
+                                                               NT, V, masks);
+  ILS_LAUNCHED("scd_masks_kernel");
+  return ILS_OK;
+}
+
 int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_t k, int64_t max_inner,
               int64_t check_every, double inner_tol, int alpha_mode, int alpha_k, int weighted,
               int64_t* steps_out) {

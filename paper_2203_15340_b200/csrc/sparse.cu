@@ -1,0 +1,954 @@
+// sparse.cu -- K5: the CSR input path (BASELINE.json configs[3]).
+//
+// Ingest: validation, CSR -> CSC of A1 and of A2 (count, scan, scatter, per-column rank sort by
+//         row: a deterministic layout), column norms N_j (sequential in i, no FMA: include/ils.h)
+//         and A1^T b1 from the CSC of A1.
+// Gram:   A1bar = A1^T A1 formed densely for the exact-inverse SP baseline and the
+//         SP-SCD row table: one CTA per column j accumulates row j of A1bar in shared memory from
+//         the column's entries (i, v) and the CSR row i (fixed order: deterministic), then writes it.
+// Stream: c_k = A1^T b1 + A2^T (A2 x_k - b2) (Alg. 2 step 5) as a CSR row pass (y = A2 x - b2)
+//         and a CSC column pass (fixed order per column, no atomics). The "full" variant gives
+//         g = A^T J (b - A x) for the RR stop and the correction form.
+// SP-RK-RGS: persistent single-CTA chunk kernel; w, r (p-vectors, L2-resident) are gathered /
+//         scattered at the ~250 rows of the two sampled columns; <a_j2, a_j1> comes from the dense
+//         A1bar (prefetched with the index ring). Check: A1 z (CSR) and A1^T (A1 z) (CSC).
+// SP-SCD: A1bar compacted to CSR (~11% dense at c3); one CTA keeps r (n <= 26000) in shared
+//         memory; membership masks precomputed per chunk (scd.cu); check r = b_hat - A1bar beta.
+#include <climits>
+
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "ils_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace ils {
+
+// ---------------------------------------------------------------------------------------------
+// ingest
+__global__ void csr_validate_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                    const double* __restrict__ va, int64_t m, int64_t n, int64_t nnz,
+                                    int32_t* flag) {
+  int bad = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = rp[i], b = rp[i + 1];
+    if (a > b || a < 0 || b > nnz) {
+      bad = 1;
+      continue;
+    }
+    int prev = -1;
+    for (int64_t e = a; e < b; ++e) {
+      const int c = ci[e];
+      if (c <= prev || c >= n) bad = 1;   // in range, strictly increasing (no duplicates)
+      if (!isfinite(va[e])) bad = 1;
+      prev = c;
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(flag, 1);
+}
+
+__global__ void csc_count_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int64_t r0,
+                                 int64_t r1, int32_t* __restrict__ cnt) {
+  for (int64_t i = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < r1; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e) atomicAdd(&cnt[ci[e]], 1);
+}
+
+// exclusive scan of int32 counts into int64 pointers (one CTA of 1024 threads, chunked)
+__global__ void __launch_bounds__(1024) scan_counts_kernel(const int32_t* __restrict__ cnt, int64_t n,
+                                                           int64_t* __restrict__ ptr) {
+  __shared__ int64_t part[1024];
+  const int tid = threadIdx.x;
+  const int64_t per = (n + 1023) / 1024;
+  const int64_t a = tid * per, b = (a + per < n) ? a + per : n;
+  int64_t s = 0;
+  for (int64_t j = a; j < b; ++j) s += cnt[j];
+  part[tid] = s;
+  __syncthreads();
+  if (tid == 0) {
+    int64_t acc = 0;
+    for (int t = 0; t < 1024; ++t) {
+      const int64_t v = part[t];
+      part[t] = acc;
+      acc += v;
+    }
+    ptr[n] = acc;
+  }
+  __syncthreads();
+  int64_t acc = part[tid];
+  for (int64_t j = a; j < b; ++j) {
+    ptr[j] = acc;
+    acc += cnt[j];
+  }
+}
+
+__global__ void csc_scatter_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                   const double* __restrict__ va, int64_t r0, int64_t r1,
+                                   const int64_t* __restrict__ cptr, int32_t* __restrict__ cursor,
+                                   int32_t* __restrict__ crow, double* __restrict__ cval) {
+  for (int64_t i = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < r1; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
+      const int c = ci[e];
+      const int64_t pos = cptr[c] + atomicAdd(&cursor[c], 1);
+      crow[pos] = (int32_t)(i - r0);
+      cval[pos] = va[e];
+    }
+}
+
+// rank sort of each column by row (rows in a column are distinct): a warp per column
+constexpr int SORT_CAP = 1024;
+__global__ void __launch_bounds__(128) csc_sort_kernel(const int64_t* __restrict__ cptr, int32_t* __restrict__ crow,
+                                                       double* __restrict__ cval, int64_t n) {
+  __shared__ int32_t srow[4][SORT_CAP];
+  __shared__ double sval[4][SORT_CAP];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t j = (int64_t)blockIdx.x * 4 + warp; j < n; j += (int64_t)gridDim.x * 4) {
+    const int64_t a = cptr[j];
+    const int k = (int)(cptr[j + 1] - a);
+    if (k <= 1) continue;
+    if (k <= SORT_CAP) {
+      for (int e = lane; e < k; e += 32) {
+        srow[warp][e] = crow[a + e];
+        sval[warp][e] = cval[a + e];
+      }
+      __syncwarp();
+      for (int e = lane; e < k; e += 32) {
+        const int r = srow[warp][e];
+        int rank = 0;
+        for (int f = 0; f < k; ++f) rank += (srow[warp][f] < r);
+        crow[a + rank] = r;
+        cval[a + rank] = sval[warp][e];
+      }
+      __syncwarp();
+    } else if (lane == 0) {   // long column: insertion sort in place
+      for (int e = 1; e < k; ++e) {
+        const int r = crow[a + e];
+        const double v = cval[a + e];
+        int f = e - 1;
+        while (f >= 0 && crow[a + f] > r) {
+          crow[a + f + 1] = crow[a + f];
+          cval[a + f + 1] = cval[a + f];
+          --f;
+        }
+        crow[a + f + 1] = r;
+        cval[a + f + 1] = v;
+      }
+    }
+  }
+}
+
+// N_j = sum_i A1[i,j]^2 in increasing i without FMA (include/ils.h); t_j = sum_i A1[i,j] b_i
+__global__ void csc_colnorms_kernel(const int64_t* __restrict__ cptr, const int32_t* __restrict__ crow,
+                                    const double* __restrict__ cval, const double* __restrict__ b, int64_t n,
+                                    double* __restrict__ N, double* __restrict__ atb) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0, t = 0.0;
+    for (int64_t e = cptr[j]; e < cptr[j + 1]; ++e) {
+      const double v = cval[e];
+      s = __dadd_rn(s, __dmul_rn(v, v));
+      t = fma(v, b[crow[e]], t);
+    }
+    N[j] = s;
+    atb[j] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// dense Gram rows from the sparse A (rows [r0, r1)): G[j][:] (+)= alpha * sum_{(i,v) in col j} v A[i,:]
+// One CTA per column j (row j of G lives in shared memory); padded rows j >= n get the identity.
+__global__ void __launch_bounds__(256) sparse_gram_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                          const double* __restrict__ va, int64_t r0,
+                                                          const int64_t* __restrict__ cptr,
+                                                          const int32_t* __restrict__ crow,
+                                                          const double* __restrict__ cval, int64_t n, int64_t npad,
+                                                          double alpha, int accumulate, double* __restrict__ G) {
+  extern __shared__ __align__(16) double gs[];
+  const int64_t j = blockIdx.x;
+  double* grow = G + j * npad;
+  if (j >= n) {   // padding: identity row (accumulate mode leaves it untouched)
+    if (!accumulate)
+      for (int64_t k = threadIdx.x; k < npad; k += blockDim.x) grow[k] = (k == j) ? 1.0 : 0.0;
+    return;
+  }
+  for (int64_t k = threadIdx.x; k < npad; k += blockDim.x) gs[k] = accumulate ? grow[k] : 0.0;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    for (int64_t e = cptr[j]; e < cptr[j + 1]; ++e) {
+      const int64_t i = r0 + crow[e];
+      const double v = alpha * cval[e];
+      for (int64_t f = rp[i] + lane; f < rp[i + 1]; f += 32) gs[ci[f]] = fma(v, va[f], gs[ci[f]]);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int64_t k = threadIdx.x; k < npad; k += blockDim.x) grow[k] = gs[k];
+}
+
+// ---------------------------------------------------------------------------------------------
+// right-hand-side stream
+// y[i - r0] = sigma_i (A_i x - b_i), sigma = -1 for i < psig (A1 rows of the full residual)
+__global__ void spmv_rows_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                 const double* __restrict__ va, const double* __restrict__ b,
+                                 const double* __restrict__ x, int64_t r0, int64_t r1, int64_t psig,
+                                 double* __restrict__ y) {
+  for (int64_t i = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < r1; i += (int64_t)gridDim.x * blockDim.x) {
+    double d = 0.0;
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e) d = fma(va[e], x[ci[e]], d);
+    d = b ? d - b[i] : d;
+    y[i - r0] = (i < psig) ? -d : d;
+  }
+}
+
+// c_j = (base_j or c_j if accumulate) + sum over the CSC entries (i, v) of column j of v y_i
+__global__ void spmv_cols_kernel(const int64_t* __restrict__ cptr, const int32_t* __restrict__ crow,
+                                 const double* __restrict__ cval, const double* __restrict__ y,
+                                 const double* __restrict__ base, int64_t n, int64_t npad, int accumulate,
+                                 double* __restrict__ c) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < npad; j += (int64_t)gridDim.x * blockDim.x) {
+    if (j >= n) {
+      if (!accumulate) c[j] = 0.0;
+      continue;
+    }
+    double s = accumulate ? c[j] : (base ? base[j] : 0.0);
+    for (int64_t e = cptr[j]; e < cptr[j + 1]; ++e) s = fma(cval[e], y[crow[e]], s);
+    c[j] = s;
+  }
+}
+
+static int grid_for(int64_t work, int bs) {
+  int64_t g = (work + bs - 1) / bs;
+  if (g > 148 * 32) g = 148 * 32;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// c = A1^T b1 + A2^T (A2 x - b2) (full = 0) or g = A^T J (b - A x) (full = 1); c has npad entries
+int sparse_rhs(Handle& h, const double* x, double* c, int full) {
+  const cudaStream_t st = h.stream;
+  double* y = h.sp_y;
+  if (!full) {
+    spmv_rows_kernel<<<grid_for(h.q, 256), 256, 0, st>>>(h.rp, h.ci, h.va, h.b, x, h.p, h.m, 0, y);
+    ILS_LAUNCHED("spmv_rows_kernel");
+    spmv_cols_kernel<<<grid_for(h.npad, 256), 256, 0, st>>>(h.cp2, h.cr2, h.cv2, y, h.a1tb1, h.n, h.npad, 0, c);
+    ILS_LAUNCHED("spmv_cols_kernel");
+    return ILS_OK;
+  }
+  spmv_rows_kernel<<<grid_for(h.m, 256), 256, 0, st>>>(h.rp, h.ci, h.va, h.b, x, 0, h.m, h.p, y);
+  ILS_LAUNCHED("spmv_rows_kernel");
+  spmv_cols_kernel<<<grid_for(h.npad, 256), 256, 0, st>>>(h.cp1, h.cr1, h.cv1, y, nullptr, h.n, h.npad, 0, c);
+  ILS_LAUNCHED("spmv_cols_kernel");
+  spmv_cols_kernel<<<grid_for(h.npad, 256), 256, 0, st>>>(h.cp2, h.cr2, h.cv2, y + h.p, nullptr, h.n, h.npad, 1, c);
+  ILS_LAUNCHED("spmv_cols_kernel");
+  return ILS_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// create-time ingest for CSR input (device arrays already copied into the handle)
+static int build_csc(Handle& h, int64_t r0, int64_t r1, int64_t** cptr, int32_t** crow, double** cval,
+                     int32_t* cnt) {
+  const cudaStream_t st = h.stream;
+  const int64_t n = h.n;
+  const int64_t nnz = 0;
+  (void)nnz;
+  ILS_CU(cudaMemsetAsync(cnt, 0, (size_t)n * sizeof(int32_t), st));
+  csc_count_kernel<<<grid_for(r1 - r0, 256), 256, 0, st>>>(h.rp, h.ci, r0, r1, cnt);
+  ILS_LAUNCHED("csc_count_kernel");
+  ILS_CU(cudaMallocAsync(cptr, (size_t)(n + 1) * sizeof(int64_t), st));
+  scan_counts_kernel<<<1, 1024, 0, st>>>(cnt, n, *cptr);
+  ILS_LAUNCHED("scan_counts_kernel");
+  int64_t total = 0;
+  ILS_CU(cudaMemcpyAsync(&total, *cptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  ILS_CU(cudaStreamSynchronize(st));
+  ILS_CU(cudaMallocAsync(crow, (size_t)(total > 0 ? total : 1) * sizeof(int32_t), st));
+  ILS_CU(cudaMallocAsync(cval, (size_t)(total > 0 ? total : 1) * sizeof(double), st));
+  ILS_CU(cudaMemsetAsync(cnt, 0, (size_t)n * sizeof(int32_t), st));
+  csc_scatter_kernel<<<grid_for(r1 - r0, 256), 256, 0, st>>>(h.rp, h.ci, h.va, r0, r1, *cptr, cnt, *crow, *cval);
+  ILS_LAUNCHED("csc_scatter_kernel");
+  csc_sort_kernel<<<grid_for(n * 32, 128), 128, 0, st>>>(*cptr, *crow, *cval, n);
+  ILS_LAUNCHED("csc_sort_kernel");
+  return ILS_OK;
+}
+
+int sparse_ingest(Handle& h, int32_t* d_flag, bool* ok) {
+  const cudaStream_t st = h.stream;
+  ILS_CU(cudaMemsetAsync(d_flag, 0, sizeof(int32_t), st));
+  csr_validate_kernel<<<grid_for(h.m, 256), 256, 0, st>>>(h.rp, h.ci, h.va, h.m, h.n, h.nnz, d_flag);
+  ILS_LAUNCHED("csr_validate_kernel");
+  int32_t f = 0;
+  ILS_CU(cudaMemcpyAsync(&f, d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  ILS_CU(cudaStreamSynchronize(st));
+  *ok = (f == 0);
+  if (!*ok) return ILS_OK;
+  int32_t* cnt = nullptr;
+  ILS_CU(cudaMallocAsync(&cnt, (size_t)h.n * sizeof(int32_t), st));
+  int rc = build_csc(h, 0, h.p, &h.cp1, &h.cr1, &h.cv1, cnt);
+  if (!rc) rc = build_csc(h, h.p, h.m, &h.cp2, &h.cr2, &h.cv2, cnt);
+  cudaFreeAsync(cnt, st);
+  if (rc) return rc;
+  csc_colnorms_kernel<<<grid_for(h.n, 256), 256, 0, st>>>(h.cp1, h.cr1, h.cv1, h.b, h.n, h.N, h.a1tb1);
+  ILS_LAUNCHED("csc_colnorms_kernel");
+  ILS_CU(cudaMemsetAsync(h.a1tb1 + h.n, 0, (h.npad - h.n) * sizeof(double), st));
+  ILS_CU(cudaMallocAsync(&h.sp_y, (size_t)(h.m + 64) * sizeof(double), st));
+  return ILS_OK;
+}
+
+// dense A1bar (alpha = 1) or M = A1bar - A2^T A2 (into a caller buffer) from the CSR/CSC arrays
+int sparse_gram(Handle& h, double* G, bool subtract_a2) {
+  const cudaStream_t st = h.stream;
+  const size_t smem = (size_t)h.npad * sizeof(double);
+  if (smem > 227 * 1024) {
+    set_error("sparse path: n > 29000 does not fit the shared-memory Gram row");
+    return ILS_ERR_UNSUPPORTED;
+  }
+  ILS_CU(cudaFuncSetAttribute(sparse_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (!subtract_a2) {
+    sparse_gram_kernel<<<(unsigned)h.npad, 256, smem, st>>>(h.rp, h.ci, h.va, 0, h.cp1, h.cr1, h.cv1, h.n, h.npad, 1.0,
+                                                            0, G);
+    ILS_LAUNCHED("sparse_gram_kernel");
+  } else {
+    sparse_gram_kernel<<<(unsigned)h.npad, 256, smem, st>>>(h.rp, h.ci, h.va, h.p, h.cp2, h.cr2, h.cv2, h.n, h.npad,
+                                                            -1.0, 1, G);
+    ILS_LAUNCHED("sparse_gram_kernel");
+  }
+  return ILS_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// x = P c (dense, npad x npad): warp per row, 8 outstanding 16-byte loads per lane
+__global__ void __launch_bounds__(256) gemv_p_kernel(const double* __restrict__ P, const double* __restrict__ c,
+                                                     int64_t npad, int64_t n, double* __restrict__ x) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t np2 = npad / 2;
+  const double2* c2 = reinterpret_cast<const double2*>(c);
+  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < npad; i += (int64_t)gridDim.x * 8) {
+    const double2* pr = reinterpret_cast<const double2*>(P + i * npad);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int64_t k = lane;
+    for (; k + 7 * 32 < np2; k += 8 * 32) {
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcs(pr + k + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) {
+        const double2 a = __ldg(c2 + k + 32 * u), b = __ldg(c2 + k + 32 * (u + 1));
+        s0 = fma(v[u].x, a.x, s0);
+        s1 = fma(v[u].y, a.y, s1);
+        s2 = fma(v[u + 1].x, b.x, s2);
+        s3 = fma(v[u + 1].y, b.y, s3);
+      }
+    }
+    for (; k < np2; k += 32) {
+      const double2 v = __ldcs(pr + k), a = __ldg(c2 + k);
+      s0 = fma(v.x, a.x, s0);
+      s1 = fma(v.y, a.y, s1);
+    }
+    const double s = warp_sum((s0 + s1) + (s2 + s3));
+    if (lane == 0) x[i] = (i < n) ? s : 0.0;
+  }
+}
+
+int gemv_p(Handle& h, const double* c, double* x) {
+  gemv_p_kernel<<<(unsigned)(h.num_sms * 8), 256, 0, h.stream>>>(h.P, c, h.npad, h.n, x);
+  ILS_LAUNCHED("gemv_p_kernel");
+  return ILS_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// SP-RK-RGS on CSR input: one CTA; steps [t0, t1) of one inner solve; w, r, z in global memory.
+struct SpRkParams {
+  const int64_t* cp;    // CSC of A1
+  const int32_t* cr;
+  const double* cv;
+  const double* G;      // dense A1bar (npad x npad): <a_j2, a_j1>
+  int64_t npad;
+  int n;
+  const double* N;
+  const uint64_t* S;
+  const double* bhat;
+  double* W;
+  double* Rv;
+  double* Z;
+  uint64_t seed;
+  uint32_t k;
+  int64_t t0, t1;
+  DevStatus* st;
+};
+
+struct SpRkIdx {
+  int32_t j1, j2;
+  double bh1, rn1, rn2, g21;
+};
+
+constexpr int SRK_RING = 128;
+constexpr int SRK_T = 256;
+
+__device__ __forceinline__ void srk_fill(const SpRkParams& p, const uint64_t* Ss, SpRkIdx* ring, int64_t t0, int lane) {
+  const int64_t t = t0 + lane;
+  if (t < p.t1) {
+    const U4 x = draw(p.seed, p.k, (uint64_t)t, kTagRkRgs);
+    const int j1 = sample_weighted(((uint64_t)x.y << 32) | x.x, Ss, p.n);
+    const int j2 = sample_weighted(((uint64_t)x.w << 32) | x.z, Ss, p.n);
+    SpRkIdx e;
+    e.j1 = j1;
+    e.j2 = j2;
+    e.bh1 = p.bhat[j1];
+    e.rn1 = 1.0 / p.N[j1];
+    e.rn2 = 1.0 / p.N[j2];
+    e.g21 = p.G[(int64_t)j2 * p.npad + j1];
+    ring[t & (SRK_RING - 1)] = e;
+  }
+}
+
+__global__ void __launch_bounds__(SRK_T) sparse_rk_kernel(SpRkParams p) {
+  extern __shared__ __align__(16) uint64_t Ssm[];             // [n]
+  __shared__ SpRkIdx ring[SRK_RING];
+  __shared__ double red[2][SRK_T / 32][2];
+  __shared__ double bn_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (*(volatile int32_t*)&p.st->inner_conv) return;
+  for (int j = tid; j < p.n; j += SRK_T) Ssm[j] = p.S[j];
+  if (p.t0 == 0) {   // b_hat = 0: z = 0 after 0 steps
+    double v = 0.0;
+    for (int j = tid; j < p.n; j += SRK_T) v = fma(p.bhat[j], p.bhat[j], v);
+    v = warp_sum(v);
+    if (lane == 0) red[0][warp][0] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < SRK_T / 32; ++w) s += red[0][w][0];
+      bn_s = s;
+    }
+    __syncthreads();
+    if (bn_s == 0.0) {
+      if (tid == 0) {
+        p.st->inner_steps = 0;
+        p.st->inner_conv = 1;
+      }
+      return;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) srk_fill(p, Ssm, ring, p.t0, lane);
+  if (warp == 1) srk_fill(p, Ssm, ring, p.t0 + 32, lane);
+  __syncthreads();
+  for (int64_t t = p.t0; t < p.t1; ++t) {
+    const int pb = (int)(t & 1);
+    if (warp == 7 && ((t - p.t0) & 31) == 0 && t + 64 < p.t1) srk_fill(p, Ssm, ring, t + 64, lane);
+    const SpRkIdx ix = ring[t & (SRK_RING - 1)];
+    const int64_t a1 = p.cp[ix.j1], e1 = p.cp[ix.j1 + 1];
+    const int64_t a2 = p.cp[ix.j2], e2 = p.cp[ix.j2 + 1];
+    double d1 = 0.0, d2 = 0.0;
+    for (int64_t e = a1 + tid; e < e1; e += SRK_T) d1 = fma(p.cv[e], p.W[p.cr[e]], d1);
+    for (int64_t e = a2 + tid; e < e2; e += SRK_T) d2 = fma(p.cv[e], p.Rv[p.cr[e]], d2);
+    d1 = warp_sum(d1);
+    d2 = warp_sum(d2);
+    if (lane == 0) {
+      red[pb][warp][0] = d1;
+      red[pb][warp][1] = d2;
+    }
+    __syncthreads();
+    double D1 = 0.0, D2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < SRK_T / 32; ++w) {
+      D1 += red[pb][w][0];
+      D2 += red[pb][w][1];
+    }
+    const double s1 = (ix.bh1 - D1) * ix.rn1;
+    const double s2 = (D2 + s1 * ix.g21) * ix.rn2;
+    // w += s1 a_j1 ; r += s1 a_j1 (rows of a column are distinct: no conflicts)
+    for (int64_t e = a1 + tid; e < e1; e += SRK_T) {
+      const int i = p.cr[e];
+      const double v = p.cv[e];
+      p.W[i] = fma(s1, v, p.W[i]);
+      p.Rv[i] = fma(s1, v, p.Rv[i]);
+    }
+    __syncthreads();   // r += s1 a_j1 complete before r -= s2 a_j2 (rows may coincide)
+    for (int64_t e = a2 + tid; e < e2; e += SRK_T) {
+      const int i = p.cr[e];
+      p.Rv[i] = fma(-s2, p.cv[e], p.Rv[i]);
+    }
+    if (tid == 0) p.Z[ix.j2] += s2;
+    __syncthreads();   // next step's gathers see this step's updates
+  }
+}
+
+// inner check: az = A1 z (rows, CSR), g = A1^T az - b_hat (CSC), stop / r = w - az (cooperative)
+__global__ void __launch_bounds__(256) sparse_rk_check_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                              const double* __restrict__ va, int64_t p_rows,
+                                                              const int64_t* __restrict__ cp,
+                                                              const int32_t* __restrict__ cr,
+                                                              const double* __restrict__ cv, int64_t n,
+                                                              const double* __restrict__ bhat,
+                                                              const double* __restrict__ Z, const double* __restrict__ W,
+                                                              double* __restrict__ Rv, double* __restrict__ az,
+                                                              double* __restrict__ red, double inner_tol, int64_t t_now,
+                                                              DevStatus* st) {
+  cg::grid_group grid = cg::this_grid();
+  if (*(volatile int32_t*)&st->inner_conv) return;
+  __shared__ double sr[8][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gsz = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = gtid; i < p_rows; i += gsz) {
+    double d = 0.0;
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e) d = fma(va[e], Z[ci[e]], d);
+    az[i] = d;
+  }
+  grid.sync();
+  double a = 0.0, b = 0.0;
+  for (int64_t j = gtid; j < n; j += gsz) {
+    double s = 0.0;
+    for (int64_t e = cp[j]; e < cp[j + 1]; ++e) s = fma(cv[e], az[cr[e]], s);
+    const double g = s - bhat[j];
+    a = fma(g, g, a);
+    b = fma(bhat[j], bhat[j], b);
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if (lane == 0) {
+    sr[warp][0] = a;
+    sr[warp][1] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double A = 0.0, B = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      A += sr[w][0];
+      B += sr[w][1];
+    }
+    red[2 * blockIdx.x] = A;
+    red[2 * blockIdx.x + 1] = B;
+  }
+  grid.sync();
+  double A = 0.0, B = 0.0;
+  for (int c = 0; c < (int)gridDim.x; ++c) {
+    A += red[2 * c];
+    B += red[2 * c + 1];
+  }
+  if (sqrt(A) <= inner_tol * sqrt(B)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->inner_steps = t_now;
+      st->inner_conv = 1;
+    }
+  } else {
+    for (int64_t i = gtid; i < p_rows; i += gsz) Rv[i] = W[i] - az[i];
+  }
+}
+
+int sparse_rk_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_t k, int64_t max_inner,
+                    int64_t check_every, double inner_tol, int64_t* steps_out) {
+  int rc = build_gram(h);   // <a_j2, a_j1> lookups
+  if (rc) return rc;
+  const cudaStream_t st = h.stream;
+  const int64_t ce = check_every > 0 ? check_every : h.n;
+  const size_t words = (size_t)2 * h.ppad + h.ppad + h.npad + 2 * h.num_sms;
+  if (!h.rk_state || h.rk_state_words < words) {
+    if (h.rk_state) cudaFreeAsync(h.rk_state, st);
+    ILS_CU(cudaMallocAsync(&h.rk_state, words * sizeof(double), st));
+    h.rk_state_words = words;
+  }
+  double* W = h.rk_state;
+  double* Rv = W + h.ppad;
+  double* AZ = Rv + h.ppad;
+  double* Z = AZ + h.ppad;
+  double* red = Z + h.npad;
+  ILS_CU(cudaMemsetAsync(h.rk_state, 0, (size_t)(3 * h.ppad + h.npad) * sizeof(double), st));
+  ILS_CU(cudaMemsetAsync(&h.dstat->inner_conv, 0, sizeof(int32_t), st));
+  ILS_CU(cudaMemsetAsync(&h.dstat->inner_steps, 0, sizeof(int64_t), st));
+  SpRkParams prm{};
+  prm.cp = h.cp1;
+  prm.cr = h.cr1;
+  prm.cv = h.cv1;
+  prm.G = h.G;
+  prm.npad = h.npad;
+  prm.n = (int)h.n;
+  prm.N = h.N;
+  prm.S = h.S;
+  prm.bhat = bhat;
+  prm.W = W;
+  prm.Rv = Rv;
+  prm.Z = Z;
+  prm.seed = seed;
+  prm.k = (uint32_t)k;
+  prm.st = h.dstat;
+  const size_t smem = (size_t)h.n * sizeof(uint64_t);
+  ILS_CU(cudaFuncSetAttribute(sparse_rk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t prow = h.p, nn = h.n;
+  const int64_t* rp = h.rp;
+  const int32_t* ci = h.ci;
+  const double* va = h.va;
+  const int64_t* cp = h.cp1;
+  const int32_t* cr = h.cr1;
+  const double* cv = h.cv1;
+  DevStatus* dst = h.dstat;
+  constexpr int kBatch = 8;
+  ILS_CU(cudaEventRecord(h.evk0, st));
+  int64_t t = 0;
+  int pending = 0;
+  while (t < max_inner) {
+    const int64_t t1 = (t + ce < max_inner) ? t + ce : max_inner;
+    prm.t0 = t;
+    prm.t1 = t1;
+    sparse_rk_kernel<<<1, SRK_T, smem, st>>>(prm);
+    ILS_LAUNCHED("sparse_rk_kernel");
+    t = t1;
+    if (t % ce == 0) {
+      double itol = inner_tol;
+      int64_t tn = t;
+      void* args[] = {(void*)&rp, (void*)&ci, (void*)&va, (void*)&prow, (void*)&cp, (void*)&cr, (void*)&cv,
+                      (void*)&nn, (void*)&bhat, (void*)&Z, (void*)&W, (void*)&Rv, (void*)&AZ, (void*)&red,
+                      (void*)&itol, (void*)&tn, (void*)&dst};
+      ILS_CU(cudaLaunchCooperativeKernel((void*)sparse_rk_check_kernel, dim3(h.num_sms), dim3(256), args, 0, st));
+      ILS_LAUNCHED("sparse_rk_check_kernel");
+    }
+    if (++pending == kBatch || t >= max_inner) {
+      ILS_CU(cudaMemcpyAsync(h.hstat, h.dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+      ILS_CU(cudaStreamSynchronize(st));
+      pending = 0;
+      if (h.hstat->inner_conv) break;
+    }
+  }
+  ILS_CU(cudaEventRecord(h.evk1, st));
+  ILS_CU(cudaMemcpyAsync(z, Z, h.npad * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  ILS_CU(cudaMemcpyAsync(h.hstat, h.dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+  ILS_CU(cudaStreamSynchronize(st));
+  const int64_t steps = h.hstat->inner_conv ? h.hstat->inner_steps : max_inner;
+  if (steps_out) *steps_out = steps;
+  const double nnz1 = (double)h.nnz1;
+  // bytes per step: the two sampled columns (12 B per entry) and the w / r entries they touch
+  hot_account(h, 1, (double)steps * 2.0 * (nnz1 / (double)h.n) * 28.0 + (double)(steps / ce) * 24.0 * nnz1,
+              (steps + ce - 1) / ce);
+  return ILS_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// SP-SCD on CSR input: A1bar compacted to CSR; one CTA with r in shared memory.
+__global__ void gram_count_kernel(const double* __restrict__ G, int64_t npad, int64_t n, int64_t* __restrict__ cnt) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; j < n; j += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    int64_t c = 0;
+    for (int64_t k = lane; k < n; k += 32) c += (G[j * npad + k] != 0.0);
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) cnt[j] = c;
+  }
+}
+
+__global__ void __launch_bounds__(1024) scan64_kernel(int64_t* __restrict__ a, int64_t n) {   // exclusive, in place, a[n] = total
+  __shared__ int64_t part[1024];
+  const int tid = threadIdx.x;
+  const int64_t per = (n + 1023) / 1024;
+  const int64_t s0 = tid * per, s1 = (s0 + per < n) ? s0 + per : n;
+  int64_t s = 0;
+  for (int64_t j = s0; j < s1; ++j) s += a[j];
+  part[tid] = s;
+  __syncthreads();
+  if (tid == 0) {
+    int64_t acc = 0;
+    for (int t = 0; t < 1024; ++t) {
+      const int64_t v = part[t];
+      part[t] = acc;
+      acc += v;
+    }
+    a[n] = acc;
+  }
+  __syncthreads();
+  int64_t acc = part[tid];
+  for (int64_t j = s0; j < s1; ++j) {
+    const int64_t v = a[j];
+    a[j] = acc;
+    acc += v;
+  }
+}
+
+// ordered compaction of row j of G (ballot within the warp keeps the column order)
+__global__ void gram_compact_kernel(const double* __restrict__ G, int64_t npad, int64_t n, const int64_t* __restrict__ ptr,
+                                    int32_t* __restrict__ col, double* __restrict__ val) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; j < n; j += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    int64_t pos = ptr[j];
+    for (int64_t k0 = 0; k0 < n; k0 += 32) {
+      const int64_t k = k0 + lane;
+      const double v = (k < n) ? G[j * npad + k] : 0.0;
+      const unsigned m = __ballot_sync(0xffffffffu, v != 0.0);
+      if (v != 0.0) {
+        const int64_t at = pos + __popc(m & ((1u << lane) - 1u));
+        col[at] = (int32_t)k;
+        val[at] = v;
+      }
+      pos += __popc(m);
+    }
+  }
+}
+
+int sparse_gram_csr(Handle& h) {
+  if (h.gcsr_ptr) return ILS_OK;
+  int rc = build_gram(h);
+  if (rc) return rc;
+  const cudaStream_t st = h.stream;
+  ILS_CU(cudaMallocAsync(&h.gcsr_ptr, (size_t)(h.n + 1) * sizeof(int64_t), st));
+  gram_count_kernel<<<grid_for(h.n * 32, 256), 256, 0, st>>>(h.G, h.npad, h.n, h.gcsr_ptr);
+  ILS_LAUNCHED("gram_count_kernel");
+  scan64_kernel<<<1, 1024, 0, st>>>(h.gcsr_ptr, h.n);
+  ILS_LAUNCHED("scan64_kernel");
+  int64_t total = 0;
+  ILS_CU(cudaMemcpyAsync(&total, h.gcsr_ptr + h.n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  ILS_CU(cudaStreamSynchronize(st));
+  h.gnnz = total;
+  ILS_CU(cudaMallocAsync(&h.gcsr_col, (size_t)(total > 0 ? total : 1) * sizeof(int32_t), st));
+  ILS_CU(cudaMallocAsync(&h.gcsr_val, (size_t)(total > 0 ? total : 1) * sizeof(double), st));
+  gram_compact_kernel<<<grid_for(h.n * 32, 256), 256, 0, st>>>(h.G, h.npad, h.n, h.gcsr_ptr, h.gcsr_col, h.gcsr_val);
+  ILS_LAUNCHED("gram_compact_kernel");
+  return ILS_OK;
+}
+
+struct SpScdParams {
+  const int64_t* gp;
+  const int32_t* gc;
+  const double* gv;
+  int n;
+  int64_t npad;
+  const double* N;
+  const double* bhat;
+  double* Rv;     // [npad] state r (in/out)
+  double* Bv;     // [npad] state beta (in/out)
+  const uint32_t* masks;   // [t1 - t0][NT] (V coordinates per thread, s = tid + v*NT)
+  int V;
+  int64_t t0, t1;
+  DevStatus* st;
+};
+
+constexpr int SSCD_T = 1024;
+
+__global__ void __launch_bounds__(SSCD_T, 1) sparse_scd_kernel(SpScdParams p) {
+  extern __shared__ __align__(16) double rs[];     // [npad] r
+  __shared__ double wv[2][32], wr[2][32];
+  __shared__ int wi[2][32];
+  __shared__ double red[32];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n = p.n, V = p.V;
+  if (*(volatile int32_t*)&p.st->inner_conv) return;
+  double nb2 = 0.0;
+  for (int s = tid; s < p.npad; s += SSCD_T) {
+    rs[s] = (s < n) ? p.Rv[s] : 0.0;
+    if (s < n) nb2 = fma(p.bhat[s], p.bhat[s], nb2);
+  }
+  if (p.t0 == 0) {
+    nb2 = warp_sum(nb2);
+    if (lane == 0) red[warp] = nb2;
+    __syncthreads();
+    double B2 = 0.0;
+    for (int w = 0; w < 32; ++w) B2 += red[w];
+    if (B2 == 0.0) {
+      if (tid == 0) {
+        p.st->inner_steps = 0;
+        p.st->inner_conv = 1;
+      }
+      return;
+    }
+  }
+  __syncthreads();
+  const uint32_t* mk = p.masks + tid;
+  uint32_t q0 = __ldcg(mk), q1 = (p.t1 - p.t0 > 1) ? __ldcg(mk + SSCD_T) : 0u;
+  for (int64_t t = p.t0; t < p.t1; ++t) {
+    const int pb = (int)(t & 1);
+    const uint32_t inmask = q0;
+    q0 = q1;
+    const int64_t ahead = t - p.t0 + 2;
+    q1 = (ahead < p.t1 - p.t0) ? __ldcg(mk + ahead * SSCD_T) : 0u;
+    double bv = -1.0, br = 0.0;
+    int bi = INT_MAX;
+    for (int v = 0; v < V; ++v) {
+      if ((inmask >> v) & 1u) {
+        const int s = tid + v * SSCD_T;
+        const double r = rs[s];
+        const double q = r * r;
+        if (q > bv) {
+          bv = q;
+          bi = s;
+          br = r;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (argmax_better(ov, oi, bv, bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (bi != INT_MAX && (bi % SSCD_T) == tid) {
+      wv[pb][warp] = bv;
+      wi[pb][warp] = bi;
+      wr[pb][warp] = br;
+    } else if (lane == 0 && bi == INT_MAX) {
+      wv[pb][warp] = -1.0;
+      wi[pb][warp] = INT_MAX;
+    }
+    __syncthreads();
+    double cv = wv[pb][lane];
+    int cix = wi[pb][lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, cv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, cix, o);
+      if (argmax_better(ov, oi, cv, cix)) {
+        cv = ov;
+        cix = oi;
+      }
+    }
+    const int j = cix;
+    const double sc = wr[pb][(j % SSCD_T) >> 5] / p.N[j];
+    // r -= sc A1bar_(j): the row's columns are distinct
+    for (int64_t e = p.gp[j] + tid; e < p.gp[j + 1]; e += SSCD_T) {
+      const int c = p.gc[e];
+      rs[c] = fma(-sc, p.gv[e], rs[c]);
+    }
+    if (tid == 0) p.Bv[j] += sc;
+    __syncthreads();
+  }
+  for (int s = tid; s < n; s += SSCD_T) p.Rv[s] = rs[s];
+}
+
+__global__ void __launch_bounds__(256) sparse_scd_check_kernel(const int64_t* __restrict__ gp, const int32_t* __restrict__ gc,
+                                                               const double* __restrict__ gv, int64_t n,
+                                                               const double* __restrict__ bhat,
+                                                               const double* __restrict__ Bv, double* __restrict__ Rv,
+                                                               double* __restrict__ rtmp, double* __restrict__ red,
+                                                               double inner_tol, int64_t t_now, DevStatus* st) {
+  cg::grid_group grid = cg::this_grid();
+  if (*(volatile int32_t*)&st->inner_conv) return;
+  __shared__ double sr[8][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double a = 0.0, b = 0.0;
+  for (int64_t j = (int64_t)blockIdx.x * 8 + warp; j < n; j += (int64_t)gridDim.x * 8) {
+    double s = 0.0;
+    for (int64_t e = gp[j] + lane; e < gp[j + 1]; e += 32) s = fma(gv[e], Bv[gc[e]], s);
+    s = warp_sum(s);
+    const double rj = bhat[j] - s;
+    if (lane == 0) rtmp[j] = rj;
+    a = fma(rj, rj, a);
+    b = fma(bhat[j], bhat[j], b);
+  }
+  if (lane == 0) {
+    sr[warp][0] = a;
+    sr[warp][1] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double A = 0.0, B = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      A += sr[w][0];
+      B += sr[w][1];
+    }
+    red[2 * blockIdx.x] = A;
+    red[2 * blockIdx.x + 1] = B;
+  }
+  grid.sync();
+  double A = 0.0, B = 0.0;
+  for (int c = 0; c < (int)gridDim.x; ++c) {
+    A += red[2 * c];
+    B += red[2 * c + 1];
+  }
+  if (sqrt(A) <= inner_tol * sqrt(B)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->inner_steps = t_now;
+      st->inner_conv = 1;
+    }
+  } else {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+      Rv[j] = rtmp[j];
+  }
+}
+
+int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_t k, int64_t max_inner,
+                     int64_t check_every, double inner_tol, int alpha_mode, int alpha_k, int64_t* steps_out) {
+  int rc = sparse_gram_csr(h);
+  if (rc) return rc;
+  const cudaStream_t st = h.stream;
+  const int64_t ce = check_every > 0 ? check_every : h.n;
+  const int V = (int)((h.n + SSCD_T - 1) / SSCD_T);
+  if (V > 32 || (size_t)h.npad * 8 > 227 * 1024) {
+    set_error("sparse SP-SCD: n too large for the shared-memory residual");
+    return ILS_ERR_UNSUPPORTED;
+  }
+  const int64_t chunk_cap = (max_inner < ce) ? max_inner : ce;
+  const size_t need = ((size_t)3 * h.npad + 2 * (size_t)h.num_sms) * sizeof(double) +
+                      (size_t)chunk_cap * SSCD_T * sizeof(uint32_t);
+  if (h.scd_ws_bytes < need) {
+    if (h.scd_ws) cudaFreeAsync(h.scd_ws, st);
+    h.scd_ws = nullptr;
+    h.scd_ws_bytes = 0;
+    ILS_CU(cudaMallocAsync(&h.scd_ws, need, st));
+    h.scd_ws_bytes = need;
+  }
+  double* Rv = reinterpret_cast<double*>(h.scd_ws);
+  double* Bv = Rv + h.npad;
+  double* rtmp = Bv + h.npad;
+  double* red = rtmp + h.npad;
+  uint32_t* masks = reinterpret_cast<uint32_t*>(red + 2 * h.num_sms);
+  ILS_CU(cudaMemsetAsync(Rv, 0, (size_t)3 * h.npad * sizeof(double), st));
+  ILS_CU(cudaMemcpyAsync(Rv, bhat, h.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  ILS_CU(cudaMemsetAsync(&h.dstat->inner_conv, 0, sizeof(int32_t), st));
+  ILS_CU(cudaMemsetAsync(&h.dstat->inner_steps, 0, sizeof(int64_t), st));
+  SpScdParams prm{};
+  prm.gp = h.gcsr_ptr;
+  prm.gc = h.gcsr_col;
+  prm.gv = h.gcsr_val;
+  prm.n = (int)h.n;
+  prm.npad = h.npad;
+  prm.N = h.N;
+  prm.bhat = bhat;
+  prm.Rv = Rv;
+  prm.Bv = Bv;
+  prm.masks = masks;
+  prm.V = V;
+  prm.st = h.dstat;
+  const size_t smem = (size_t)h.npad * sizeof(double);
+  ILS_CU(cudaFuncSetAttribute(sparse_scd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t* gp = h.gcsr_ptr;
+  const int32_t* gc = h.gcsr_col;
+  const double* gv = h.gcsr_val;
+  const int64_t nn = h.n;
+  DevStatus* dst = h.dstat;
+  constexpr int kBatch = 8;
+  ILS_CU(cudaEventRecord(h.evk0, st));
+  int64_t t = 0;
+  int pending = 0;
+  while (t < max_inner) {
+    const int64_t t1 = (t + ce < max_inner) ? t + ce : max_inner;
+    if ((rc = scd_masks(h, seed, k, t, t1, alpha_mode, alpha_k, SSCD_T, V, masks))) return rc;
+    prm.t0 = t;
+    prm.t1 = t1;
+    sparse_scd_kernel<<<1, SSCD_T, smem, st>>>(prm);
+    ILS_LAUNCHED("sparse_scd_kernel");
+    t = t1;
+    if (t % ce == 0) {
+      double itol = inner_tol;
+      int64_t tn = t;
+      void* args[] = {(void*)&gp, (void*)&gc, (void*)&gv, (void*)&nn, (void*)&bhat, (void*)&Bv, (void*)&Rv,
+                      (void*)&rtmp, (void*)&red, (void*)&itol, (void*)&tn, (void*)&dst};
+      ILS_CU(cudaLaunchCooperativeKernel((void*)sparse_scd_check_kernel, dim3(h.num_sms), dim3(256), args, 0, st));
+      ILS_LAUNCHED("sparse_scd_check_kernel");
+    }
+    if (++pending == kBatch || t >= max_inner) {
+      ILS_CU(cudaMemcpyAsync(h.hstat, h.dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+      ILS_CU(cudaStreamSynchronize(st));
+      pending = 0;
+      if (h.hstat->inner_conv) break;
+    }
+  }
+  ILS_CU(cudaEventRecord(h.evk1, st));
+  ILS_CU(cudaMemsetAsync(beta, 0, h.npad * sizeof(double), st));
+  ILS_CU(cudaMemcpyAsync(beta, Bv, h.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  ILS_CU(cudaMemcpyAsync(h.hstat, h.dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+  ILS_CU(cudaStreamSynchronize(st));
+  const int64_t steps = h.hstat->inner_conv ? h.hstat->inner_steps : max_inner;
+  if (steps_out) *steps_out = steps;
+  const double row = (double)h.gnnz / (double)h.n;
+  hot_account(h, 2, (double)steps * 12.0 * row + (double)(steps / ce) * 12.0 * (double)h.gnnz, (steps + ce - 1) / ce);
+  return ILS_OK;
+}
+
+}  // namespace ils

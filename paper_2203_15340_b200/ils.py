@@ -29,7 +29,8 @@ EXPORTED = [
 
 
 class IlsExt(C.Structure):
-    _fields_ = [("format", C.c_int32), ("batch", C.c_int64), ("lda", C.c_int64), ("stream", C.c_void_p)]
+    _fields_ = [("format", C.c_int32), ("batch", C.c_int64), ("lda", C.c_int64), ("stream", C.c_void_p),
+                ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("nnz", C.c_int64)]
 
 
 class IlsOpts(C.Structure):
@@ -131,11 +132,17 @@ def ils_default_opts(**kw) -> IlsOpts:
     return o
 
 
-def ils_create(A, b, p: int, q: int, n: int, batch: int = 1, lda: int = 0, stream=None):
-    """ils_create(A, b, p, q, n, ext): A row-major (m x n) or [batch][m][n] fp64, b (m) or [batch][m]."""
+def ils_create(A, b, p: int, q: int, n: int, batch: int = 1, lda: int = 0, stream=None, row_ptr=None,
+               col_idx=None):
+    """ils_create(A, b, p, q, n, ext): A row-major (m x n) or [batch][m][n] fp64, b (m) or [batch][m].
+    CSR input: A = values [nnz], row_ptr int64 [m+1], col_idx int32 [nnz] (ILS_FORMAT_CSR)."""
     lib = load_library()
     h = C.c_void_p()
-    ext = IlsExt(ILS_FORMAT_DENSE, batch, lda, stream)
+    if row_ptr is not None:
+        nnz = int(A.numel() if hasattr(A, "numel") else A.size)
+        ext = IlsExt(ILS_FORMAT_CSR, 1, 0, stream, _ptr(row_ptr), _ptr(col_idx), nnz)
+    else:
+        ext = IlsExt(ILS_FORMAT_DENSE, batch, lda, stream, None, None, 0)
     _check(lib.ils_create(C.byref(h), _ptr(A), _ptr(b), p, q, n, C.byref(ext)), "ils_create")
     return h
 

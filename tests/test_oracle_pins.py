@@ -402,6 +402,27 @@ def test_methods_converge_on_c0():
     assert O.spectral_radius_sp(pr.A1, pr.A2) < 1.0 and O.is_spd(O.normal_matrix(pr.A1, pr.A2))
 
 
+def test_sparse_inputs_match_the_pinned_dense_oracle():
+    """The oracle on scipy.sparse CSR inputs (configs[3]) equals the pinned dense oracle on the
+    same matrix: only the storage differs (PAPER.md:43-46 direct solve, Alg. 1 SP iterates)."""
+    from workloads import make_sparse
+    pr = make_sparse(400, 80, 30, 5, seed=3)
+    S = pr.scipy()
+    A = pr.dense()
+    sp_args = (S[:pr.p], S[pr.p:], pr.b[:pr.p], pr.b[pr.p:])
+    de_args = (A[:pr.p], A[pr.p:], pr.b[:pr.p], pr.b[pr.p:])
+    xs, xd = O.direct_solve(*sp_args), O.direct_solve(*de_args)
+    assert np.linalg.norm(xs - xd) <= 1e-12 * np.linalg.norm(xd)
+    rs = O.sp_solve(*sp_args, max_iter=4, stop=O.STOP_NONE)
+    rd = O.sp_solve(*de_args, max_iter=4, stop=O.STOP_NONE)
+    for a, b in zip(rs.x_hist, rd.x_hist):
+        assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(b)
+    assert abs(O.relative_residual(*sp_args, xs) - O.relative_residual(*de_args, xd)) <= 1e-20
+    # the generator's CSR layout: sorted distinct columns, row_ptr consistent
+    assert np.all(np.diff(pr.row_ptr) == 5)
+    assert all(np.all(np.diff(pr.col_idx[pr.row_ptr[i]:pr.row_ptr[i + 1]]) > 0) for i in range(pr.m))
+
+
 def test_oracle_not_imported_by_product():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     pkg = os.path.join(root, "paper_2203_15340_b200")

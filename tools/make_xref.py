@@ -25,14 +25,26 @@ def main():
     ap.add_argument("--config", default="c1")
     ap.add_argument("--seed", type=int, default=0)
     a = ap.parse_args()
-    pr = make_problem(a.config, seed=a.seed)
-    x = O.direct_solve(pr.A1, pr.A2, pr.b1, pr.b2)
+    seed = a.seed
+    while True:   # configs[3]: "regenerate with seed+1 if the oracle's Cholesky of A^T J A fails"
+        pr = make_problem(a.config, seed=seed)
+        if hasattr(pr, "scipy"):
+            S = pr.scipy()
+            A1, A2, b1, b2 = S[:pr.p], S[pr.p:], pr.b[:pr.p], pr.b[pr.p:]
+        else:
+            A1, A2, b1, b2 = pr.A1, pr.A2, pr.b1, pr.b2
+        try:
+            x = O.direct_solve(A1, A2, b1, b2)
+            break
+        except np.linalg.LinAlgError:
+            seed += 1
     out = os.path.join(ROOT, "workloads", "xref")
     os.makedirs(out, exist_ok=True)
     base = os.path.join(out, f"{a.config}_seed{a.seed}")
     np.save(base + ".npy", x)
-    meta = {"config": a.config, "seed": a.seed, "n": int(pr.n), "fingerprint": fingerprint(pr.A, pr.b),
-            "rho": O.spectral_radius_sp(pr.A1, pr.A2),
+    meta = {"config": a.config, "seed": a.seed, "data_seed": seed, "n": int(pr.n),
+            "fingerprint": fingerprint(pr if hasattr(pr, "scipy") else pr.A, pr.b),
+            "rho": O.spectral_radius_sp(A1, A2) if not hasattr(pr, "scipy") else None,
             "err_xstar": float(np.linalg.norm(x - pr.xstar) / np.linalg.norm(pr.xstar)),
             "writer": "tools/make_xref.py (oracle.ils_oracle.direct_solve)"}
     with open(base + ".json", "w") as f:

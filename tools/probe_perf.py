@@ -31,7 +31,12 @@ def main():
     pr = make_problem(a.config)
     print(f"gen {a.config}: {time.time() - t0:.1f}s", flush=True)
     dev = "cuda:0"
-    if a.config == "c4":
+    if a.config == "c3":
+        t = {k: torch.from_numpy(getattr(pr, k)).to(dev) for k in ("vals", "b", "row_ptr", "col_idx")}
+        h = ils.ils_create(t["vals"], t["b"], pr.p, pr.q, pr.n, row_ptr=t["row_ptr"], col_idx=t["col_idx"])
+        n, B = pr.n, 1
+        xr = torch.from_numpy(np.load(os.path.join(ROOT, "workloads", "xref", "c3_seed0.npy"))).to(dev)
+    elif a.config == "c4":
         A = torch.from_numpy(pr.A).to(dev)
         b = torch.from_numpy(pr.b).to(dev)
         xr = torch.from_numpy(pr.xstar).to(dev)

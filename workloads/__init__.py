@@ -11,5 +11,7 @@ from .configs import (  # noqa: F401
     make_batched,
     make_dense,
     make_ill_conditioned,
+    make_sparse,
+    SparseIls,
     fingerprint,
 )

@@ -115,6 +115,71 @@ def make_ill_conditioned(p: int = 40000, q: int = 10000, n: int = 4000, seed: in
 
 
 @dataclass
+class SparseIls:
+    """BASELINE.json configs[3]: A = [A1; A2] in CSR (row_ptr int64, col_idx int32 sorted within
+    each row, vals float64), b = A x* + noise."""
+
+    name: str
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    vals: np.ndarray
+    b: np.ndarray
+    p: int
+    q: int
+    n: int
+    xstar: np.ndarray
+    tol: float
+    meta: dict = field(default_factory=dict)
+
+    consistent = False
+
+    @property
+    def m(self) -> int:
+        return self.p + self.q
+
+    @property
+    def nnz(self) -> int:
+        return int(self.vals.size)
+
+    def scipy(self):
+        """The same matrix as a scipy.sparse CSR matrix (test/oracle convenience)."""
+        import scipy.sparse as sp
+        return sp.csr_matrix((self.vals, self.col_idx, self.row_ptr), shape=(self.m, self.n))
+
+    def dense(self) -> np.ndarray:
+        return self.scipy().toarray()
+
+
+def make_sparse(p: int = 500000, q: int = 100000, n: int = 20000, nnz_per_row: int = 10,
+                a2_scale: float = 0.3, noise: float = 1e-3, seed: int = 0, tol: float = 1e-8,
+                name: str = "c3") -> SparseIls:
+    """BASELINE.json configs[3]: every row has nnz_per_row nonzeros at distinct uniform-random
+    columns (sorted), values N(0,1) in A1 and a2_scale*N(0,1) in A2; x* ~ N(0,1);
+    b = A x* + noise*N(0,1) on all m rows. Draw order: columns, values, x*, noise."""
+    rng = _rng(seed)
+    m = p + q
+    k = min(nnz_per_row, n)
+    cols = rng.integers(0, n, size=(m, k), dtype=np.int64)
+    while True:   # redraw duplicated columns within a row until all k are distinct
+        srt = np.sort(cols, axis=1)
+        dup_rows = np.flatnonzero(np.any(srt[:, 1:] == srt[:, :-1], axis=1))
+        if dup_rows.size == 0:
+            break
+        cols[dup_rows] = rng.integers(0, n, size=(dup_rows.size, k), dtype=np.int64)
+    cols = np.sort(cols, axis=1)
+    vals = rng.standard_normal((m, k))
+    vals[p:] *= a2_scale
+    xstar = rng.standard_normal(n)
+    row_ptr = np.arange(0, (m + 1) * k, k, dtype=np.int64)
+    col_idx = cols.reshape(-1).astype(np.int32)
+    v = vals.reshape(-1)
+    Ax = (vals * xstar[cols]).sum(axis=1)
+    b = Ax + noise * rng.standard_normal(m) if noise > 0 else Ax
+    return SparseIls(name=name, row_ptr=row_ptr, col_idx=col_idx, vals=np.ascontiguousarray(v), b=b, p=p, q=q,
+                     n=n, xstar=xstar, tol=tol, meta=dict(seed=seed, nnz_per_row=k, a2_scale=a2_scale, noise=noise))
+
+
+@dataclass
 class BatchedIls:
     """BASELINE.json configs[4]: independent instances, instance i seeded base+i."""
 
@@ -175,17 +240,26 @@ def make_problem(name: str, seed: int = 0, **overrides):
     if kind == "illcond":
         return make_ill_conditioned(cfg["p"], cfg["q"], cfg["n"], seed=seed,
                                     tol=cfg["tol"], name=name)
+    if kind == "sparse":
+        return make_sparse(cfg["p"], cfg["q"], cfg["n"], cfg["nnz_per_row"], cfg["a2_scale"], cfg["noise"],
+                           seed=seed, tol=cfg["tol"], name=name)
     if kind == "batched":
         return make_batched(cfg["batch"], cfg["p"], cfg["q"], cfg["n"], cfg["a2_scale"],
                             base_seed=seed, tol=cfg["tol"])
     raise NotImplementedError(f"workload kind {kind!r} not generated yet")
 
 
-def fingerprint(A: np.ndarray, b: np.ndarray) -> str:
-    """SHA-256 over the first/last 64 rows of A and the head of b: ties a stored x_ref file
-    (workloads/xref/, written by tools/make_xref.py from the oracle) to the generated data."""
+def fingerprint(A, b: np.ndarray) -> str:
+    """SHA-256 over the first/last 64 rows of A (dense) or its CSR arrays' heads and tails (sparse)
+    and the head of b: ties a stored x_ref file (workloads/xref/, written by tools/make_xref.py
+    from the oracle) to the generated data."""
     h = hashlib.sha256()
-    h.update(np.ascontiguousarray(A[:64]).tobytes())
-    h.update(np.ascontiguousarray(A[-64:]).tobytes())
+    if isinstance(A, np.ndarray):
+        h.update(np.ascontiguousarray(A[:64]).tobytes())
+        h.update(np.ascontiguousarray(A[-64:]).tobytes())
+    else:
+        for arr in (A.row_ptr, A.col_idx, A.vals):
+            h.update(np.ascontiguousarray(arr[:640]).tobytes())
+            h.update(np.ascontiguousarray(arr[-640:]).tobytes())
     h.update(np.ascontiguousarray(b[:64]).tobytes())
     return h.hexdigest()
