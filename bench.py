@@ -51,6 +51,7 @@ def workload_desc(cfg: str) -> str:
         "c0": "c0 tiny dense p=200 q=100 n=50, A2 0.3N(0,1), b=Ax*, tol 1e-10",
         "c1": "c1 medium dense p=8000 q=2000 n=1000, A2 0.5N(0,1), b=Ax*+0.01N(0,1), tol 1e-8 vs oracle Cholesky x_ref",
         "c2": "c2 ill-conditioned dense p=40000 q=10000 n=4000, s log-spaced 1..1e3, b=Ax*, tol 1e-8",
+        "c3": "c3 sparse CSR p=500000 q=100000 n=20000, 10 nnz/row, A2 0.3N(0,1), b=Ax*+1e-3N(0,1), tol 1e-8 vs oracle Cholesky x_ref",
         "c4": "c4 batched 4096 x (p=96 q=32 n=32), tol 1e-10 per instance",
     }[cfg]
 
@@ -69,18 +70,24 @@ def inner_tol_for(tol: float) -> float:
     return 1e-12 if tol <= 1e-10 else 1e-10
 
 
+# RK / RGS on c2 and c3 need ~1e10 / ~1e6-1e7 latency-bound inner steps per outer iteration
+# (DESIGN.md §8): the bench times SP there; tools/probe_perf.py reports capped runs.
+DEFAULT_METHODS = {"c0": "sp,rk,rgs", "c1": "sp,rk,rgs", "c2": "sp", "c3": "sp", "c4": "sp,rk,rgs"}
+
+
 def load_problem(cfg: str):
     """Seeded synthetic workload (workloads/) and its x_ref: x* for consistent configs, else the
     oracle-written file workloads/xref/<cfg>_seed0.npy (tools/make_xref.py)."""
-    from workloads import make_problem
-    pr = make_problem(cfg)
+    from workloads import fingerprint, make_problem
+    base = os.path.join(ROOT, "workloads", "xref", f"{cfg}_seed0")
+    meta = None
+    if os.path.exists(base + ".json"):
+        with open(base + ".json") as f:
+            meta = json.load(f)
+    pr = make_problem(cfg, seed=(meta or {}).get("data_seed", 0))
     if cfg == "c4" or pr.consistent:
         return pr, pr.xstar
-    base = os.path.join(ROOT, "workloads", "xref", f"{cfg}_seed0")
-    with open(base + ".json") as f:
-        meta = json.load(f)
-    from workloads import fingerprint
-    if meta["fingerprint"] != fingerprint(pr.A, pr.b):
+    if meta is None or meta["fingerprint"] != fingerprint(pr if hasattr(pr, "scipy") else pr.A, pr.b):
         raise RuntimeError(f"x_ref file {base}.npy does not match the generated {cfg} data; rerun tools/make_xref.py")
     return pr, np.load(base + ".npy")
 
@@ -143,24 +150,35 @@ class Runner:
         self.ils, self.torch, self.dev, self.cfg, self.pr = ils, torch, dev, cfg, pr
         self.methods = methods
         self.batched = cfg == "c4"
+        self.sparse = hasattr(pr, "scipy")
         self.B = pr.batch if self.batched else 1
         self.n = pr.n
         self.tol = pr.tol
         self.itol = inner_tol_for(pr.tol)
         self.host = host
         t = torch
+        if self.sparse:
+            src = {k: np.ascontiguousarray(getattr(pr, k)) for k in ("vals", "row_ptr", "col_idx")}
+            if host:
+                self.A, self.rp, self.ci = (t.from_numpy(src[k]).pin_memory() for k in ("vals", "row_ptr", "col_idx"))
+            else:
+                self.A, self.rp, self.ci = (t.from_numpy(src[k]).to(dev) for k in ("vals", "row_ptr", "col_idx"))
         if host:   # pinned host buffers: the library stages them to HBM inside the call
-            self.A = t.from_numpy(np.ascontiguousarray(pr.A)).pin_memory()
+            if not self.sparse:
+                self.A = t.from_numpy(np.ascontiguousarray(pr.A)).pin_memory()
             self.b = t.from_numpy(np.ascontiguousarray(pr.b)).pin_memory()
             self.xref = t.from_numpy(np.ascontiguousarray(xref, dtype=np.float64).reshape(-1)).pin_memory()
             self.x = {m: t.zeros(self.B * self.n, dtype=t.float64).pin_memory() for m in methods}
         else:
-            self.A = t.from_numpy(np.ascontiguousarray(pr.A)).to(dev)
+            if not self.sparse:
+                self.A = t.from_numpy(np.ascontiguousarray(pr.A)).to(dev)
             self.b = t.from_numpy(np.ascontiguousarray(pr.b)).to(dev)
             self.xref = t.from_numpy(np.ascontiguousarray(xref, dtype=np.float64).reshape(-1)).to(dev)
             self.x = {m: t.zeros(self.B * self.n, dtype=t.float64, device=dev) for m in methods}
         self.xref_host = np.ascontiguousarray(xref, dtype=np.float64).reshape(self.B, self.n)
         self.h2d = self.A.numel() * 8 + self.b.numel() * 8 + len(methods) * self.xref.numel() * 8
+        if self.sparse:
+            self.h2d += self.rp.numel() * 8 + self.ci.numel() * 4
         self.d2h = len(methods) * self.B * self.n * 8
 
     def step(self):
@@ -168,7 +186,10 @@ class Runner:
         stream = t.cuda.current_stream().cuda_stream
         evs = [t.cuda.Event(enable_timing=True) for _ in range(len(self.methods) + 2)]
         evs[0].record()
-        if self.batched:
+        if self.sparse:
+            h = ils.ils_create(self.A, self.b, self.pr.p, self.pr.q, self.n, stream=stream, row_ptr=self.rp,
+                               col_idx=self.ci)
+        elif self.batched:
             h = ils.ils_create(self.A, self.b, self.pr.p, self.pr.q, self.n, batch=self.B, stream=stream)
         else:
             h = ils.ils_create(self.A, self.b, self.pr.p, self.pr.q, self.n, stream=stream)
@@ -280,7 +301,12 @@ def oracle_sample(cfg, pr, xref, counts, methods, budget_s=20.0):
         cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
         cores = os.cpu_count() or 1
-    A1, A2, b1, b2 = pr.A1, pr.A2, pr.b1, pr.b2
+    if hasattr(pr, "scipy"):
+        S = pr.scipy()
+        A1, A2, b1, b2 = S[:pr.p], S[pr.p:], pr.b[:pr.p], pr.b[pr.p:]
+        methods = [m for m in methods if m == "sp"]
+    else:
+        A1, A2, b1, b2 = pr.A1, pr.A2, pr.b1, pr.b2
     n = pr.n
     itol = inner_tol_for(pr.tol)
     per = {}
@@ -366,11 +392,13 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c1", choices=["c0", "c1", "c2", "c4"])
-    ap.add_argument("--methods", default="sp,rk,rgs")
+    ap.add_argument("--config", default="c1", choices=["c0", "c1", "c2", "c3", "c4"])
+    ap.add_argument("--methods", default=None, help="default: per config (DEFAULT_METHODS)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     a = ap.parse_args()
+    if a.methods is None:
+        a.methods = DEFAULT_METHODS[a.config]
     if a.warmup < 3:
         a.warmup = 3   # contract: W >= 3 warm-up steps
     rank = int(os.environ.get("RANK", "0"))

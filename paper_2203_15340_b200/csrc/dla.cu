@@ -256,6 +256,15 @@ int mirror_lower(Handle& h, double* C, int64_t ld, int64_t n, int64_t n_real) {
   return ILS_OK;
 }
 
+// B[j][i] = A[i][j] (n x n, n multiple of 32)
+__global__ void transpose_kernel(const double* __restrict__ A, double* __restrict__ B, int64_t n) {
+  __shared__ double tile[32][33];
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;
+  for (int r = threadIdx.y; r < 32; r += 8) tile[r][threadIdx.x] = A[(bi * 32 + r) * n + bj * 32 + threadIdx.x];
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) B[(bj * 32 + r) * n + bi * 32 + threadIdx.x] = tile[threadIdx.x][r];
+}
+
 // ---------------------------------------------------------------- 64x64 base: potf2 + trtri
 // Lower-triangle Cholesky of the 64x64 block at (s,s) of L, and its inverse into Z.
 __global__ void __launch_bounds__(256) potf2_trtri_kernel(double* __restrict__ L, double* __restrict__ Z,
@@ -394,6 +403,16 @@ int build_inverse(Handle& h) {
   ILS_CU(cudaMemcpyAsync(h.L, h.G, bytes, cudaMemcpyDeviceToDevice, h.stream));
   r = cholesky_inverse(h, h.L, h.Z, np);
   if (r) return r;
+  if (h.sparse && np >= 8192) {
+    // large n: apply P = Z^T Z as two triangular GEMVs (Z and its transpose, each half read per
+    // step: the same 8n^2 bytes as a P GEMV) instead of paying the n^3 GEMM for P; P holds Z^T
+    dim3 grid((unsigned)(np / 32), (unsigned)(np / 32));
+    transpose_kernel<<<grid, dim3(32, 8), 0, h.stream>>>(h.Z, h.P, np);
+    ILS_LAUNCHED("transpose_kernel");
+    h.use_zt = true;
+    h.have_P = true;
+    return ILS_OK;
+  }
   // P = Z^T Z: opA(i,k) = Z[k][i] (M-contiguous), opB(j,k) = Z[k][j] (N-contiguous); K from max(i,j)
   const int64_t tiles = (np / 64) * (np / 64 + 1) / 2;
   const int sp = pick_splits(h, tiles, np / 2);

@@ -245,6 +245,15 @@ int ils_create(ils_handle* out, const double* A, const double* b, int64_t p, int
   h->stream = ext ? static_cast<cudaStream_t>(ext->stream) : nullptr;
   int dev = 0;
   cudaGetDevice(&dev);
+  {   // keep freed stream-ordered allocations cached in the pool: handles of the same size reuse
+      // them instead of returning GBs to the OS at every synchronisation
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+  }
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev);
   {
     const char* e = getenv("ILS_RK_SINGLE_STEP");

@@ -45,6 +45,7 @@ struct Handle {
   double* Z = nullptr;      // npad x npad  L^{-1} (lower, zero upper)
   double* P = nullptr;      // npad x npad  (A1^T A1)^{-1}
   bool have_gram = false, have_P = false;
+  bool use_zt = false;      // P applied as Z^T (Z c): P buffer holds Z^T (large sparse n)
 
   // workspace
   double* part = nullptr;   // partial sums [grid][npad]
