@@ -330,6 +330,17 @@ int ils_create(ils_handle* out, const double* A, const double* b, int64_t p, int
       set_error("ils_create: non-finite entry in b");
       return fail(ILS_ERR_ARG);
     }
+    {   // sum of squared row lengths of A1 (Gram flop count)
+      std::vector<int64_t> rph((size_t)p + 1);
+      CKC(cudaMemcpyAsync(rph.data(), h->rp, (size_t)(p + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      CKC(cudaStreamSynchronize(st));
+      double sq = 0.0;
+      for (int64_t i = 0; i < p; ++i) {
+        const double l = (double)(rph[i + 1] - rph[i]);
+        sq += l * l;
+      }
+      h->a1_row_sq = sq;
+    }
     CKC(cudaMallocAsync(&h->N, (size_t)n * sizeof(double), st));
     CKC(cudaMallocAsync(&h->S, (size_t)n * sizeof(uint64_t), st));
     CKC(cudaMallocAsync(&h->a1tb1, (size_t)np * sizeof(double), st));
@@ -518,7 +529,10 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
   if (gram_new || inv_new) {
     const double nd = (double)H.n, pd = (double)H.p;
     H.hot_ms[3] += setup_ms;
-    H.hot_work[3] += (gram_new ? 2.0 * pd * nd * nd : 0.0) + (inv_new ? nd * nd * nd : 0.0);
+    // algorithmic flops (LAPACK counts): SYRK p n (n+1) (sparse: 2 sum_i nnz_i^2 over A1 rows),
+    // Cholesky n^3/3 + triangular inverse n^3/3 (+ P = Z^T Z n^3/3 when formed)
+    const double gram = H.sparse ? 2.0 * H.a1_row_sq : pd * nd * (nd + 1.0);
+    H.hot_work[3] += (gram_new ? gram : 0.0) + (inv_new ? (H.use_zt ? 2.0 : 3.0) * nd * nd * nd / 3.0 : 0.0);
     H.hot_n[3] += 1;
   }
   {

@@ -64,6 +64,7 @@ struct Handle {
   // CSR input (BASELINE.json configs[3])
   bool sparse = false;
   int64_t nnz = 0, nnz1 = 0;
+  double a1_row_sq = 0.0;   // sum over A1 rows of nnz_i^2
   int64_t* rp = nullptr;    // [m+1]
   int32_t* ci = nullptr;    // [nnz]
   double* va = nullptr;     // [nnz]
