@@ -682,6 +682,240 @@ __global__ void __launch_bounds__(32) batched_scd_kernel(BatchParams P) {
   }
 }
 
+// SP-RK-RGS, batched, blocked: 4 steps per warp reduction (the identity of rk_rgs.cu's blocked
+// kernel, Alg. 2 steps 9 and 11). Every Gram entry the 4-step recurrence needs (<a_i, a_k>,
+// <b_i, a_k>, <b_i, b_k>) is looked up in the instance's A1bar (32 x 33, shared memory, formed once
+// per solve), so a block reduces only the 8 state products <a_i, w>, <b_i, r> (butterfly
+// reduce-scatter + broadcast: 16 shuffles per step-block instead of 30 per step).
+template <int NVP>
+__device__ __forceinline__ double bw_reduce_scatter(double (&x)[NVP], int lane) {
+#pragma unroll
+  for (int half = NVP / 2; half >= 1; half /= 2) {
+    const bool hi = (lane & half) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double lo_v = x[i], hi_v = x[i + half];
+      const double send = hi ? lo_v : hi_v;
+      const double keep = hi ? hi_v : lo_v;
+      x[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+    }
+  }
+  double v = x[0];
+#pragma unroll
+  for (int o = NVP; o < 32; o *= 2) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int RPL>
+__global__ void __launch_bounds__(32) batched_rkb_kernel(BatchParams P) {
+  constexpr int B = 4;
+  extern __shared__ __align__(16) double sm[];
+  constexpr int PP = 32 * RPL;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x;
+  const int64_t inst = blockIdx.x;
+  const int p = P.p, q = P.q, n = P.n, m = p + q;
+  const double* A = P.A + inst * (int64_t)m * n;
+  const double* b = P.b + inst * (int64_t)m;
+  const uint64_t seed = P.seed + (uint64_t)inst;
+  double* A1T = sm;                                     // [n][PP]
+  double* G = A1T + n * PP;                             // [32][33] A1bar
+  double* azs = G + 32 * 33;                            // [PP]
+  double* cs = azs + PP;                                // [32]
+  double* rns = cs + 32;                                // [32]
+  uint64_t* S = reinterpret_cast<uint64_t*>(rns + 32);  // [32]
+
+  for (int e = lane; e < n * PP; e += 32) {
+    const int j = e / PP, i = e % PP;
+    A1T[e] = (i < p) ? A[(int64_t)i * n + j] : 0.0;
+  }
+  __syncwarp();
+  const bool act = lane < n;
+  double Nj = 0.0, a1tb1 = 0.0;
+  if (act) {
+    for (int i = 0; i < p; ++i) {   // N_j sequential in i without FMA (include/ils.h)
+      const double v = A1T[lane * PP + i];
+      Nj = __dadd_rn(Nj, __dmul_rn(v, v));
+      a1tb1 = fma(v, b[i], a1tb1);
+    }
+  }
+  // A1bar[i][lane] (rows rotated by lane: conflict-free shared-memory reads)
+  for (int i = 0; i < n; ++i) {
+    double s = 0.0;
+    if (act)
+      for (int kk = 0, k = lane % p; kk < p; ++kk, k = (k + 1 == p) ? 0 : k + 1)
+        s = fma(A1T[i * PP + k], A1T[lane * PP + k], s);
+    G[i * 33 + lane] = act ? s : 0.0;
+  }
+  batched_weights(Nj, act, lane, S);
+  rns[lane] = act ? 1.0 / Nj : 0.0;
+  double x = (act && P.x0) ? P.x0[inst * n + lane] : 0.0;
+  const double xr = (act && P.xref) ? P.xref[inst * n + lane] : 0.0;
+  const double xr2 = warp_sum(xr * xr);
+  __syncwarp();
+
+  const int64_t ce = P.check_every;
+  int64_t it = 0;
+  int conv = 0;
+  unsigned long long inner_sum = 0;
+  for (; it < P.max_iter; ++it) {
+    const double c = batched_rhs(A, b, p, q, n, x, a1tb1, lane);
+    cs[lane] = act ? c : 0.0;
+    const double cnorm = sqrt(warp_sum(act ? c * c : 0.0));
+    __syncwarp();
+    double z = 0.0;
+    int64_t steps = 0;
+    if (cnorm != 0.0) {
+      double w[RPL], r[RPL];
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) w[u] = r[u] = 0.0;
+      int my1 = 0, my2 = 0;
+      double mybh = 0.0, myr1 = 0.0, myr2 = 0.0;
+      int64_t next_check = ce;
+      for (int64_t t = 0; t < P.max_inner; t += B) {
+        const int kk = (int)(t & 31);
+        if (kk == 0) {   // indices and scalars of steps t..t+31, one per lane
+          const U4 xw = draw(seed, (uint32_t)it, (uint64_t)(t + lane), kTagRkRgs);
+          my1 = sample_weighted(((uint64_t)xw.y << 32) | xw.x, S, n);
+          my2 = sample_weighted(((uint64_t)xw.w << 32) | xw.z, S, n);
+          mybh = cs[my1];
+          myr1 = rns[my1];
+          myr2 = rns[my2];
+        }
+        int j1[B], j2[B];
+        double bh[B], rn1[B], rn2[B];
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+          j1[i] = __shfl_sync(FULL, my1, kk + i);
+          j2[i] = __shfl_sync(FULL, my2, kk + i);
+          bh[i] = __shfl_sync(FULL, mybh, kk + i);
+          const bool live = t + i < P.max_inner;   // steps past max_inner are masked: s1 = s2 = 0
+          rn1[i] = live ? __shfl_sync(FULL, myr1, kk + i) : 0.0;
+          rn2[i] = live ? __shfl_sync(FULL, myr2, kk + i) : 0.0;
+        }
+        double x1[B][RPL], x2[B][RPL];
+        double acc[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acc[v] = 0.0;
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+          const double* a1 = A1T + j1[i] * PP + lane;
+          const double* a2 = A1T + j2[i] * PP + lane;
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) {
+            x1[i][u] = a1[32 * u];
+            x2[i][u] = a2[32 * u];
+            acc[i] = fma(x1[i][u], w[u], acc[i]);
+            acc[B + i] = fma(x2[i][u], r[u], acc[B + i]);
+          }
+        }
+        // Gram entries of the block (broadcast shared-memory reads, independent of the reduction)
+        double AA[B][B], BA[B][B], BB[B][B];
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+#pragma unroll
+          for (int k = 0; k < B; ++k) {
+            AA[i][k] = (k < i) ? G[j1[i] * 33 + j1[k]] : 0.0;
+            BA[i][k] = (k <= i) ? G[j2[i] * 33 + j1[k]] : 0.0;
+            BB[i][k] = (k < i) ? G[j2[i] * 33 + j2[k]] : 0.0;
+          }
+        const double mine = bw_reduce_scatter<8>(acc, lane);   // lane l: total of value l & 7
+        double T[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) T[v] = __shfl_sync(FULL, mine, v);
+        double s1[B], s2[B];
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+          double dw = T[i];
+#pragma unroll
+          for (int k = 0; k < i; ++k) dw = fma(s1[k], AA[i][k], dw);
+          s1[i] = (bh[i] - dw) * rn1[i];
+          double dr = T[B + i];
+#pragma unroll
+          for (int k = 0; k < i; ++k) {
+            dr = fma(s1[k], BA[i][k], dr);
+            dr = fma(-s2[k], BB[i][k], dr);
+          }
+          dr = fma(s1[i], BA[i][i], dr);
+          s2[i] = dr * rn2[i];
+        }
+#pragma unroll
+        for (int u = 0; u < RPL; ++u)
+#pragma unroll
+          for (int i = 0; i < B; ++i) {
+            w[u] = fma(s1[i], x1[i][u], w[u]);
+            r[u] = fma(s1[i], x1[i][u], r[u]);
+            r[u] = fma(-s2[i], x2[i][u], r[u]);
+          }
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+          if (lane == j2[i]) z += s2[i];
+        steps = (t + B < P.max_inner) ? t + B : P.max_inner;
+        if (t + B == next_check) {   // inner stop rule (include/ils.h): g = A1^T A1 z - b_hat
+          next_check += ce;
+          double az[RPL], az2[RPL];
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) az[u] = az2[u] = 0.0;
+          int j = 0;
+          for (; j + 1 < n; j += 2) {
+            const double zj = __shfl_sync(FULL, z, j), zk = __shfl_sync(FULL, z, j + 1);
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {
+              az[u] = fma(A1T[j * PP + lane + 32 * u], zj, az[u]);
+              az2[u] = fma(A1T[(j + 1) * PP + lane + 32 * u], zk, az2[u]);
+            }
+          }
+          if (j < n) {
+            const double zj = __shfl_sync(FULL, z, j);
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) az[u] = fma(A1T[j * PP + lane + 32 * u], zj, az[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) {
+            az[u] += az2[u];
+            azs[lane + 32 * u] = az[u];
+            r[u] = w[u] - az[u];
+          }
+          __syncwarp();
+          double g = 0.0;
+          if (act) {   // rows rotated by lane: conflict-free; two accumulators
+            double g0 = 0.0, g1 = 0.0;
+            const double* col = A1T + lane * PP;
+            int i0 = lane % p;   // rotated start, wrapped incrementally (no modulo in the loop)
+            int ii = 0;
+            for (; ii + 1 < p; ii += 2) {
+              const int i1 = (i0 + 1 == p) ? 0 : i0 + 1;
+              g0 = fma(col[i0], azs[i0], g0);
+              g1 = fma(col[i1], azs[i1], g1);
+              i0 = (i1 + 1 == p) ? 0 : i1 + 1;
+            }
+            if (ii < p) g0 = fma(col[i0], azs[i0], g0);
+            g = (g0 + g1) - c;
+          }
+          __syncwarp();
+          const double gg = warp_sum(g * g);
+          if (sqrt(gg) <= P.inner_tol * cnorm) break;
+        }
+      }
+    }
+    inner_sum += (unsigned long long)steps;
+    x = act ? z : 0.0;
+    const double e = act ? x - xr : 0.0;
+    const double e2 = warp_sum(e * e);
+    if (P.stop == ILS_STOP_XREF && P.xref && sqrt(e2) <= P.tol * sqrt(xr2)) {
+      conv = 1;
+      ++it;
+      break;
+    }
+  }
+  if (act) P.x[inst * n + lane] = x;
+  if (lane == 0) {
+    if (P.inst_iters) P.inst_iters[inst] = it;
+    if (P.inst_status) P.inst_status[inst] = conv;
+    atomicAdd(P.inner_total, inner_sum);
+  }
+}
+
 int batched_solve(Handle& h, int method, const double* x0, double* x, double tol, int64_t max_iter,
                   const ils_opts& o, int64_t* inst_iters_dev, int32_t* inst_status_dev) {
   if (h.n > 32 || h.p > 256 || h.q > 4096) {
@@ -712,6 +946,26 @@ int batched_solve(Handle& h, int method, const double* x0, double* x, double tol
   P.inst_iters = inst_iters_dev;
   P.inst_status = inst_status_dev;
   P.inner_total = reinterpret_cast<unsigned long long*>(&h.dstat->inner_steps);
+  if (method == 1 && P.check_every % 4 == 0 && !getenv("ILS_BATCHED_RK_SINGLE")) {   // blocked, 4 steps/reduction
+    const int rpl = (int)((h.p + 31) / 32);
+    const int RPL = rpl <= 1 ? 1 : rpl <= 2 ? 2 : rpl <= 3 ? 3 : rpl <= 4 ? 4 : 8;
+    const size_t smem = ((size_t)h.n * 32 * RPL + 32 * 33 + 32 * RPL + 64) * 8 + 32 * 8;
+#define RKBLAUNCH(RR)                                                                                \
+  do {                                                                                               \
+    ILS_CU(cudaFuncSetAttribute(batched_rkb_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    batched_rkb_kernel<RR><<<(unsigned)h.batch, 32, smem, h.stream>>>(P);                            \
+    ILS_LAUNCHED("batched_rkb_kernel");                                                              \
+  } while (0)
+    switch (RPL) {
+      case 1: RKBLAUNCH(1); break;
+      case 2: RKBLAUNCH(2); break;
+      case 3: RKBLAUNCH(3); break;
+      case 4: RKBLAUNCH(4); break;
+      default: RKBLAUNCH(8); break;
+    }
+#undef RKBLAUNCH
+    return ILS_OK;
+  }
   if (method == 1) {   // SP-RK-RGS: A1 resident, rows padded to 32*RPL
     const int rpl = (int)((h.p + 31) / 32);
     const int RPL = rpl <= 1 ? 1 : rpl <= 2 ? 2 : rpl <= 3 ? 3 : rpl <= 4 ? 4 : 8;
