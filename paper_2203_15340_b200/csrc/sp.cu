@@ -175,20 +175,33 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sp_persistent_kernel(SpParams p
       }
     }
     grid.sync();
-    // ---------------- phase B: c = base + sum_cta part (fixed order)
-    for (int64_t j = (int64_t)bid * SP_THREADS + tid; j < npad; j += (int64_t)G * SP_THREADS) {
-      double s = prm.base ? prm.base[j] : 0.0;
-      for (int c = 0; c < G; ++c) s += prm.part[(int64_t)c * npad + j];
-      prm.cvec[j] = s;
+    // ---------------- phase B: c = base + sum_cta part (fixed order). Every CTA owns a contiguous
+    // slice [jb0, jb1) of c; its 16 warps each sum every 16th partial row for 32 consecutive j
+    // (coalesced, ~G/16 independent loads per thread), then one warp adds the 16 chunk sums.
+    const int64_t jb0 = (int64_t)bid * npad / G, jb1 = (int64_t)(bid + 1) * npad / G;
+    {
+      double* chs = ring;   // [16][32] chunk sums (the ring is idle between phases)
+      for (int64_t j0 = jb0; j0 < jb1; j0 += 32) {
+        const int64_t j = j0 + lane;
+        double sacc = 0.0;
+        if (j < jb1)
+          for (int c = warp; c < G; c += SP_WARPS) sacc += prm.part[(int64_t)c * npad + j];
+        chs[warp * 32 + lane] = sacc;
+        __syncthreads();
+        if (warp == 0 && j < jb1) {
+          double t = prm.base ? prm.base[j] : 0.0;
+          for (int w = 0; w < SP_WARPS; ++w) t += chs[w * 32 + lane];
+          prm.cvec[j] = t;
+        }
+        __syncthreads();
+      }
     }
     if (prm.check) {
       // ||g||^2 and ||b_hat||^2 partials over this CTA's j range (fixed order everywhere)
       double g2 = 0.0, b2 = 0.0;
-      const int64_t jper = (prm.n + G - 1) / G;
-      const int64_t ja = (int64_t)bid * jper, jb = (ja + jper < prm.n) ? ja + jper : prm.n;
-      for (int64_t j = ja + tid; j < jb; j += SP_THREADS) {
-        double s = (prm.base ? prm.base[j] : 0.0);
-        for (int c = 0; c < G; ++c) s += prm.part[(int64_t)c * npad + j];
+      const int64_t jb = (jb1 < prm.n) ? jb1 : prm.n;
+      for (int64_t j = jb0 + tid; j < jb; j += SP_THREADS) {
+        const double s = prm.cvec[j];   // this CTA's slice, written above
         const double g = s - prm.bhat[j];
         g2 = fma(g, g, g2);
         b2 = fma(prm.bhat[j], prm.bhat[j], b2);
