@@ -415,9 +415,11 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
     if (t % ce == 0) {
       double itol = inner_tol;
       int64_t tn = t;
+      // small n: one CTA (no grid barrier); else the cooperative full-GPU check
+      const unsigned grid = (h.n <= 512) ? 1u : (unsigned)nchk;
       void* cargs[] = {(void*)&Gp, (void*)&npad, (void*)&nn, (void*)&bhat, (void*)&Bv, (void*)&Rv,
                        (void*)&rtmp, (void*)&red, (void*)&itol, (void*)&tn, (void*)&dst};
-      ILS_CU(cudaLaunchCooperativeKernel((void*)scd_check_kernel, dim3(nchk), dim3(256), cargs, 0, st));
+      ILS_CU(cudaLaunchCooperativeKernel((void*)scd_check_kernel, dim3(grid), dim3(256), cargs, 0, st));
       ILS_LAUNCHED("scd_check_kernel");
     }
     if (++pending == kBatch || t >= max_inner) {

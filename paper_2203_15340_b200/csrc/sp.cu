@@ -451,8 +451,67 @@ int sp_run(Handle& h, const double* x0_dev, double* x_dev, double tol, int64_t m
 // SP-RK-RGS inner stop check (include/ils.h "Inner stopping rule"), full grid: az = A1 z,
 // g = A1^T az - b_hat, stop if ||g|| <= inner_tol ||b_hat|| (sets st->inner_conv, inner_steps = t_now),
 // else r = w - az. No-op if st->inner_conv is already set.
+// Small problems (p x n <= 2^20): the same check in ONE CTA (no grid barrier, no 148-CTA launch):
+// az = A1 z (thread per row, A1 rows of the row-major copy), g = A1^T az (warp per column),
+// ||g|| vs inner_tol ||b_hat||, r = w - az. Fixed-order reductions.
+__global__ void __launch_bounds__(1024) rk_check_small_kernel(const double* __restrict__ Arm, int64_t npad, int64_t p,
+                                                              int64_t n, int64_t ppad, const double* __restrict__ z,
+                                                              const double* __restrict__ bhat,
+                                                              const double* __restrict__ w, double* __restrict__ r,
+                                                              double* __restrict__ az, double inner_tol, int64_t t_now,
+                                                              DevStatus* st) {
+  __shared__ double red[32][2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (*(volatile int32_t*)&st->inner_conv) return;
+  for (int64_t i = tid; i < p; i += 1024) {
+    const double* row = Arm + i * npad;
+    double d0 = 0.0, d1 = 0.0;
+    int64_t j = 0;
+    for (; j + 1 < n; j += 2) {
+      d0 = fma(row[j], z[j], d0);
+      d1 = fma(row[j + 1], z[j + 1], d1);
+    }
+    if (j < n) d0 = fma(row[j], z[j], d0);
+    az[i] = d0 + d1;
+  }
+  __syncthreads();
+  double g2 = 0.0, b2 = 0.0;
+  for (int64_t j = warp; j < n; j += 32) {
+    double s = 0.0;
+    for (int64_t i = lane; i < p; i += 32) s = fma(Arm[i * npad + j], az[i], s);
+    s = warp_sum(s);
+    const double g = s - bhat[j];
+    g2 = fma(g, g, g2);
+    b2 = fma(bhat[j], bhat[j], b2);
+  }
+  if (lane == 0) {
+    red[warp][0] = g2;
+    red[warp][1] = b2;
+  }
+  __syncthreads();
+  double G2 = 0.0, B2 = 0.0;
+  for (int q = 0; q < 32; ++q) {
+    G2 += red[q][0];
+    B2 += red[q][1];
+  }
+  if (sqrt(G2) <= inner_tol * sqrt(B2)) {
+    if (tid == 0) {
+      st->inner_steps = t_now;
+      st->inner_conv = 1;
+    }
+  } else {
+    for (int64_t i = tid; i < ppad; i += 1024) r[i] = w[i] - (i < p ? az[i] : 0.0);
+  }
+}
+
 int rk_check(Handle& h, const double* z, const double* bhat, const double* w, double* r, double* az,
              double inner_tol, int64_t t_now) {
+  if (h.ppad * h.npad <= (int64_t)1 << 20) {
+    rk_check_small_kernel<<<1, 1024, 0, h.stream>>>(h.Arm, h.npad, h.p, h.n, h.ppad, z, bhat, w, r, az, inner_tol,
+                                                     t_now, h.dstat);
+    ILS_LAUNCHED("rk_check_small_kernel");
+    return ILS_OK;
+  }
   SpParams prm{};
   prm.Arm = h.Arm;
   prm.b = nullptr;
