@@ -223,6 +223,18 @@ class Runner:
         return res
 
 
+def max_over_ranks(value: float, device) -> float:
+    """Whole-job time = the slowest rank (contract: max over ranks). One all-reduce (MAX) of a
+    scalar; a no-op for a single process. Works for nccl (cuda device) and gloo (cpu)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def flush_l2(buf):
     buf.add_(1)   # 256 MiB read+write > 126 MB L2
 
@@ -446,10 +458,7 @@ def main():
     clocks = clk.summary()
     errs = run.errors()
     step_ms = statistics.mean(s[0] for s in steps)
-    tmax = torch.tensor([step_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    value = float(tmax.item())
+    value = max_over_ranks(step_ms, dev)
 
     e2e = None
     if not a.no_e2e:
@@ -462,10 +471,8 @@ def main():
             torch.cuda.synchronize()
             es.append(hrun.step()[0])
         barrier()
-        ev = torch.tensor([statistics.mean(es)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(ev, op=dist.ReduceOp.MAX)
-        e2e = {"value": round(float(ev.item()), 4), "unit": "ms", "h2d_bytes_per_step": hrun.h2d,
+        ev = max_over_ranks(statistics.mean(es), dev)
+        e2e = {"value": round(ev, 4), "unit": "ms", "h2d_bytes_per_step": hrun.h2d,
                "d2h_bytes_per_step": hrun.d2h}
         del hrun
 
