@@ -419,6 +419,8 @@ struct SpRkParams {
 struct SpRkIdx {
   int32_t j1, j2;
   double bh1, rn1, rn2, g21;
+  int64_t a1, a2;    // CSC starts of the two columns
+  int32_t k1, k2;    // their lengths
 };
 
 constexpr int SRK_RING = 128;
@@ -437,12 +439,45 @@ __device__ __forceinline__ void srk_fill(const SpRkParams& p, const uint64_t* Ss
     e.rn1 = 1.0 / p.N[j1];
     e.rn2 = 1.0 / p.N[j2];
     e.g21 = p.G[(int64_t)j2 * p.npad + j1];
+    e.a1 = p.cp[j1];
+    e.a2 = p.cp[j2];
+    e.k1 = (int32_t)(p.cp[j1 + 1] - e.a1);
+    e.k2 = (int32_t)(p.cp[j2 + 1] - e.a2);
     ring[t & (SRK_RING - 1)] = e;
   }
 }
 
+constexpr int SRK_D = 4;        // column prefetch depth (steps)
+constexpr int SRK_MAXK = 512;   // column entries staged per column (longer columns read from global)
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+
+// first index f in sorted rows[0, k) with rows[f] == r, else -1
+__device__ __forceinline__ int find_row(const int32_t* rows, int k, int r) {
+  int lo = 0, hi = k;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (rows[mid] < r) lo = mid + 1; else hi = mid;
+  }
+  return (lo < k && rows[lo] == r) ? lo : -1;
+}
+
+// One step needs the entries (i, v) of columns j1 and j2 (CSC, sorted by row). They are staged in
+// shared memory SRK_D steps ahead (cp.async; the index stream is data-independent). Per step ONE
+// round of independent gathers (w at rows of j1, r at rows of j1 and of j2), one block reduction,
+// then plain stores: a row present in both columns is written once, by its j2 entry, as
+// (r + s1 a_j1) - s2 a_j2 (the sequential order of Alg. 2 steps 9 and 11); the match is a binary
+// search in the other column's staged rows.
 __global__ void __launch_bounds__(SRK_T) sparse_rk_kernel(SpRkParams p) {
-  extern __shared__ __align__(16) uint64_t Ssm[];             // [n]
+  extern __shared__ __align__(16) unsigned char srk_smem[];
+  double (*cvs)[2][SRK_MAXK] = reinterpret_cast<double (*)[2][SRK_MAXK]>(srk_smem);              // [D][2][MAXK]
+  int32_t (*crs)[2][SRK_MAXK] = reinterpret_cast<int32_t (*)[2][SRK_MAXK]>(srk_smem + SRK_D * 2 * SRK_MAXK * 8);
+  uint64_t* Ssm = reinterpret_cast<uint64_t*>(srk_smem + SRK_D * 2 * SRK_MAXK * 12);           // [n]
   __shared__ SpRkIdx ring[SRK_RING];
   __shared__ double red[2][SRK_T / 32][2];
   __shared__ double bn_s;
@@ -473,15 +508,67 @@ __global__ void __launch_bounds__(SRK_T) sparse_rk_kernel(SpRkParams p) {
   if (warp == 0) srk_fill(p, Ssm, ring, p.t0, lane);
   if (warp == 1) srk_fill(p, Ssm, ring, p.t0 + 32, lane);
   __syncthreads();
+  auto stage = [&](int64_t t) {   // cp.async the two columns of step t into slot t % D
+    if (t < p.t1) {
+      const SpRkIdx ix = ring[t & (SRK_RING - 1)];
+      const int sl = (int)(t % SRK_D);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int64_t a = c ? ix.a2 : ix.a1;
+        const int k = min(SRK_MAXK, c ? ix.k2 : ix.k1);
+        for (int e = tid; e < k; e += SRK_T) {
+          cp_async4(&crs[sl][c][e], p.cr + a + e);
+          cp_async8(&cvs[sl][c][e], p.cv + a + e);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  for (int64_t t = p.t0; t < p.t0 + SRK_D; ++t) stage(t);
   for (int64_t t = p.t0; t < p.t1; ++t) {
     const int pb = (int)(t & 1);
+    const int sl = (int)(t % SRK_D);
     if (warp == 7 && ((t - p.t0) & 31) == 0 && t + 64 < p.t1) srk_fill(p, Ssm, ring, t + 64, lane);
+    cp_async_wait<SRK_D - 1>();
+    __syncthreads();   // slot sl staged by every thread
     const SpRkIdx ix = ring[t & (SRK_RING - 1)];
-    const int64_t a1 = p.cp[ix.j1], e1 = p.cp[ix.j1 + 1];
-    const int64_t a2 = p.cp[ix.j2], e2 = p.cp[ix.j2 + 1];
+    const int64_t a1 = ix.a1, a2 = ix.a2;
+    const int k1 = ix.k1, k2 = ix.k2;
+    // z_{j2}: its load rides with the gathers; the store below follows the previous step's store
+    // to the same address in program order of thread 0
+    const double zold = (tid == 0) ? p.Z[ix.j2] : 0.0;
+    const int32_t* R1 = crs[sl][0];
+    const int32_t* R2 = crs[sl][1];
+    const bool st1 = k1 <= SRK_MAXK, st2 = k2 <= SRK_MAXK;
+    // gathers (one round of independent loads)
+    constexpr int EPT = (SRK_MAXK + SRK_T - 1) / SRK_T;
+    int i1[EPT], i2[EPT];
+    double v1[EPT], v2[EPT], w1[EPT], q1[EPT], q2[EPT];
     double d1 = 0.0, d2 = 0.0;
-    for (int64_t e = a1 + tid; e < e1; e += SRK_T) d1 = fma(p.cv[e], p.W[p.cr[e]], d1);
-    for (int64_t e = a2 + tid; e < e2; e += SRK_T) d2 = fma(p.cv[e], p.Rv[p.cr[e]], d2);
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) {
+      const int e = tid + u * SRK_T;
+      i1[u] = -1;
+      i2[u] = -1;
+      if (e < k1) {
+        i1[u] = st1 ? R1[e] : p.cr[a1 + e];
+        v1[u] = st1 ? cvs[sl][0][e] : p.cv[a1 + e];
+        w1[u] = p.W[i1[u]];
+        q1[u] = p.Rv[i1[u]];
+      }
+      if (e < k2) {
+        i2[u] = st2 ? R2[e] : p.cr[a2 + e];
+        v2[u] = st2 ? cvs[sl][1][e] : p.cv[a2 + e];
+        q2[u] = p.Rv[i2[u]];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) {
+      if (i1[u] >= 0) d1 = fma(v1[u], w1[u], d1);
+      if (i2[u] >= 0) d2 = fma(v2[u], q2[u], d2);
+    }
+    for (int e = tid + EPT * SRK_T; e < k1; e += SRK_T) d1 = fma(p.cv[a1 + e], p.W[p.cr[a1 + e]], d1);
+    for (int e = tid + EPT * SRK_T; e < k2; e += SRK_T) d2 = fma(p.cv[a2 + e], p.Rv[p.cr[a2 + e]], d2);
     d1 = warp_sum(d1);
     d2 = warp_sum(d2);
     if (lane == 0) {
@@ -497,21 +584,38 @@ __global__ void __launch_bounds__(SRK_T) sparse_rk_kernel(SpRkParams p) {
     }
     const double s1 = (ix.bh1 - D1) * ix.rn1;
     const double s2 = (D2 + s1 * ix.g21) * ix.rn2;
-    // w += s1 a_j1 ; r += s1 a_j1 (rows of a column are distinct: no conflicts)
-    for (int64_t e = a1 + tid; e < e1; e += SRK_T) {
-      const int i = p.cr[e];
-      const double v = p.cv[e];
-      p.W[i] = fma(s1, v, p.W[i]);
-      p.Rv[i] = fma(s1, v, p.Rv[i]);
+    const bool fast = st1 && st2 && k1 <= EPT * SRK_T && k2 <= EPT * SRK_T;
+    if (fast) {
+#pragma unroll
+      for (int u = 0; u < EPT; ++u) {
+        if (i1[u] >= 0) {
+          p.W[i1[u]] = fma(s1, v1[u], w1[u]);
+          if (find_row(R2, k2, i1[u]) < 0) p.Rv[i1[u]] = fma(s1, v1[u], q1[u]);
+        }
+        if (i2[u] >= 0) {
+          const int f = find_row(R1, k1, i2[u]);
+          const double base = (f >= 0) ? fma(s1, cvs[sl][0][f], q2[u]) : q2[u];
+          p.Rv[i2[u]] = fma(-s2, v2[u], base);
+        }
+      }
+    } else {   // long columns: the two-phase read-modify-write form
+      for (int e = tid; e < k1; e += SRK_T) {
+        const int i = p.cr[a1 + e];
+        const double v = p.cv[a1 + e];
+        p.W[i] = fma(s1, v, p.W[i]);
+        p.Rv[i] = fma(s1, v, p.Rv[i]);
+      }
+      __syncthreads();
+      for (int e = tid; e < k2; e += SRK_T) {
+        const int i = p.cr[a2 + e];
+        p.Rv[i] = fma(-s2, p.cv[a2 + e], p.Rv[i]);
+      }
     }
-    __syncthreads();   // r += s1 a_j1 complete before r -= s2 a_j2 (rows may coincide)
-    for (int64_t e = a2 + tid; e < e2; e += SRK_T) {
-      const int i = p.cr[e];
-      p.Rv[i] = fma(-s2, p.cv[e], p.Rv[i]);
-    }
-    if (tid == 0) p.Z[ix.j2] += s2;
-    __syncthreads();   // next step's gathers see this step's updates
+    if (tid == 0) p.Z[ix.j2] = zold + s2;
+    __syncthreads();   // next step's gathers see these stores; slot sl is free
+    stage(t + SRK_D);
   }
+  cp_async_wait<0>();
 }
 
 // inner check: az = A1 z (rows, CSR), g = A1^T az - b_hat (CSC), stop / r = w - az (cooperative)
@@ -612,7 +716,11 @@ int sparse_rk_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int
   prm.seed = seed;
   prm.k = (uint32_t)k;
   prm.st = h.dstat;
-  const size_t smem = (size_t)h.n * sizeof(uint64_t);
+  const size_t smem = (size_t)SRK_D * 2 * SRK_MAXK * 12 + (size_t)h.n * sizeof(uint64_t);
+  if (smem > 227 * 1024) {
+    set_error("sparse SP-RK-RGS: n too large for the shared-memory sampling table");
+    return ILS_ERR_UNSUPPORTED;
+  }
   ILS_CU(cudaFuncSetAttribute(sparse_rk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t prow = h.p, nn = h.n;
   const int64_t* rp = h.rp;
