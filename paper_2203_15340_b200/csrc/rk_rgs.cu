@@ -733,6 +733,7 @@ static int dispatch_rkb_c(Handle& h, RkParams& p, int nt, size_t smem) {
 
 static int dispatch_rkb(Handle& h, RkParams& p, int U, int B, int nt, size_t smem) {
   if (B == 2) return (U == 4) ? dispatch_rkb_c<4, 2>(h, p, nt, smem) : dispatch_rkb_c<8, 2>(h, p, nt, smem);
+  if (U == 2) return dispatch_rkb_c<2, 4>(h, p, nt, smem);
   return (U == 4) ? dispatch_rkb_c<4, 4>(h, p, nt, smem) : dispatch_rkb_c<8, 4>(h, p, nt, smem);
 }
 
@@ -793,6 +794,10 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
     p.slice = (int)(((h.ppad + C - 1) / C + 1) / 2 * 2);
     // rows per thread: one warp with U = 8 for slices <= 256, U = 4 up to 2048, else U = 8
     U = (p.slice <= 256) ? 8 : (p.slice <= 2048 ? 4 : 8);
+    {
+      const char* e = getenv("ILS_RK_U");   // experiment override of rows per thread (2, 4, 8)
+      if (e && (atoi(e) == 2 || atoi(e) == 4 || atoi(e) == 8)) U = atoi(e);
+    }
     const int nw = (p.slice + 32 * U - 1) / (32 * U);
     if (nw > RK_MAXW) {
       set_error("RK-RGS: row slice too long for the register-resident kernel (p > 65536)");
@@ -829,7 +834,8 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
       a.val.clusterDim.z = 1;
       cfg.attrs = &a;
       cfg.numAttrs = 1;
-      void* kern = blocked ? ((U == 4) ? (void*)rk_rgs_block_kernel<16, 4, 4> : (void*)rk_rgs_block_kernel<16, 8, 4>)
+      void* kern = blocked ? ((U == 2) ? (void*)rk_rgs_block_kernel<16, 2, 4>
+                              : (U == 4) ? (void*)rk_rgs_block_kernel<16, 4, 4> : (void*)rk_rgs_block_kernel<16, 8, 4>)
                            : ((U == 4) ? (void*)rk_rgs_kernel<16, 4> : (void*)rk_rgs_kernel<16, 8>);
       cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -867,7 +873,7 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
     p.t0 = t;
     p.t1 = t1;
     const int r = blocked ? dispatch_rkb(h, p, U, Bk, nt, smem)
-                          : ((U == 4) ? dispatch_rk_c<4>(h, p, nt, smem) : dispatch_rk_c<8>(h, p, nt, smem));
+                          : ((U == 8) ? dispatch_rk_c<8>(h, p, nt, smem) : dispatch_rk_c<4>(h, p, nt, smem));
     if (r) return r;
     t = t1;
     if (t % ce == 0) {
