@@ -302,3 +302,25 @@ def test_batched_converges_c4_subset():
         assert st == ils.ILS_OK and sts.all()
         err = np.linalg.norm(x - bt.xstar, axis=1) / np.linalg.norm(bt.xstar, axis=1)
         assert err.max() <= 1e-10
+
+
+# ------------------------------------------------------------------ full-size configs
+def test_c2_full_size_sp_iterates_and_convergence():
+    """configs[2] at full size (p=40000, q=10000, n=4000, ill-conditioned) in the bench's launch
+    configuration: the first two SP iterates match the oracle's (1e-9, the paper-form floor is
+    ~1e-10, SURVEY Appendix A probe 3) and SP reaches 1e-8 against x* (consistent b = A x*)."""
+    pr = make_problem("c2")
+    K = 2
+    ref = O.sp_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE)
+    hist = np.zeros((K, pr.n))
+    x = torch.zeros(pr.n, dtype=torch.float64, device=DEV)
+    xs = torch.from_numpy(pr.xstar).to(DEV)
+    with H(pr) as hh:
+        o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, x_hist=hist.ctypes.data)
+        ils.ils_sp_solve(hh.h, None, x, 0.0, K, o)
+        for k in range(K):
+            assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
+        o = ils.ils_default_opts(x_ref=xs.data_ptr())
+        st, rep = ils.ils_sp_solve(hh.h, None, x, pr.tol, 100, o)
+    assert st == ils.ILS_OK and rep.converged
+    assert _rel(x.cpu().numpy(), pr.xstar) <= pr.tol
