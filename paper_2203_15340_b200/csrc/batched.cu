@@ -624,10 +624,11 @@ __global__ void __launch_bounds__(32) batched_scd_kernel(BatchParams P) {
           // whole domain [0, 4^hb) (<= 64 values: lane v holds D(v) and D(v + 32)); a walk step is
           // then two shuffles instead of a 12-round decryption (the walk diverges across lanes)
           const uint32_t dom = 1u << (2 * hb);
-          const uint32_t d0 = (n == 1) ? 0u : feistel_decrypt_once((uint32_t)lane & (dom - 1), key, hb, msk);
-          const uint32_t d1 = (n == 1 || dom <= 32) ? 0u : feistel_decrypt_once((uint32_t)lane + 32u, key, hb, msk);
+          const bool allm = alpha >= (uint32_t)n;   // tau_t = [n] (Motzkin case): no permutation needed
+          const uint32_t d0 = (n == 1 || allm) ? 0u : feistel_decrypt_once((uint32_t)lane & (dom - 1), key, hb, msk);
+          const uint32_t d1 = (n == 1 || allm || dom <= 32) ? 0u : feistel_decrypt_once((uint32_t)lane + 32u, key, hb, msk);
           uint32_t y = d0;
-          if (n > 1) {
+          if (n > 1 && !allm) {
             while (__any_sync(0xffffffffu, act && y >= (uint32_t)n)) {
               const uint32_t t0 = __shfl_sync(0xffffffffu, d0, (int)(y & 31)), t1 = __shfl_sync(0xffffffffu, d1, (int)(y & 31));
               if (act && y >= (uint32_t)n) y = (y < 32) ? t0 : t1;

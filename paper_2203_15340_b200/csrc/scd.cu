@@ -51,6 +51,7 @@ struct ScdParams {
   uint32_t k;
   int64_t t0, t1;
   int alpha_mode, alpha_k, weighted;
+  int all_members;   // alpha_t = n for every step (Remark 4.1 Motzkin case): tau_t = [n], no masks
   DevStatus* st;
 };
 
@@ -155,7 +156,11 @@ __global__ void __launch_bounds__(SCD_MAXT, 1) scd_chunk_kernel(ScdParams p) {
   const uint32_t* mk = p.masks + tid;
   const int64_t L = p.t1 - p.t0;
   uint32_t q0 = 0, q1 = 0, q2 = 0, q3 = 0;
-  if (!p.weighted) {
+  uint32_t allbits = 0;
+#pragma unroll
+  for (int v = 0; v < V; ++v)
+    if (tid + v * NT < n) allbits |= 1u << v;
+  if (!p.weighted && !p.all_members) {
     q0 = (0 < L) ? __ldcg(mk) : 0u;
     q1 = (1 < L) ? __ldcg(mk + NT) : 0u;
     q2 = (2 < L) ? __ldcg(mk + 2 * NT) : 0u;
@@ -177,12 +182,15 @@ __global__ void __launch_bounds__(SCD_MAXT, 1) scd_chunk_kernel(ScdParams p) {
       __syncthreads();
       rj = rj_s[pb];
     } else {
-      const uint32_t inmask = q0;
-      q0 = q1;
-      q1 = q2;
-      q2 = q3;
-      const int64_t ahead = t - p.t0 + 4;
-      q3 = (ahead < L) ? __ldcg(mk + ahead * NT) : 0u;
+      uint32_t inmask = allbits;
+      if (!p.all_members) {
+        inmask = q0;
+        q0 = q1;
+        q1 = q2;
+        q2 = q3;
+        const int64_t ahead = t - p.t0 + 4;
+        q3 = (ahead < L) ? __ldcg(mk + ahead * NT) : 0u;
+      }
       // thread-local argmax (coordinates ascend with v: strict > keeps the smallest index)
       double bv = -1.0, br = 0.0;
       int bi = INT_MAX;
@@ -372,6 +380,7 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
   p.alpha_mode = alpha_mode;
   p.alpha_k = alpha_k;
   p.weighted = weighted;
+  p.all_members = (!weighted && alpha_mode == ILS_ALPHA_FIXED && alpha_k >= h.n) ? 1 : 0;
   p.st = h.dstat;
   const size_t smem = 2 * (size_t)((h.n + 1) & ~1) * 8 + SCD_RING * sizeof(ScdKey);
   void* kern = nullptr;
@@ -401,7 +410,7 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
   int pending = 0;
   while (t < max_inner) {
     const int64_t t1 = (t + ce < max_inner) ? t + ce : max_inner;
-    if (!weighted) {
+    if (!weighted && !p.all_members) {
       scd_masks_kernel<<<(unsigned)(t1 - t), 256, 0, st>>>(seed, (uint32_t)k, t, t1, nn, alpha_mode, alpha_k, nt,
                                                             V, masks);
       ILS_LAUNCHED("scd_masks_kernel");

@@ -862,6 +862,7 @@ struct SpScdParams {
   double* Bv;     // [npad] state beta (in/out)
   const uint32_t* masks;   // [t1 - t0][NT] (V coordinates per thread, s = tid + v*NT)
   int V;
+  int all_members;         // alpha_t = n every step (Motzkin): no masks
   int64_t t0, t1;
   DevStatus* st;
 };
@@ -897,13 +898,23 @@ __global__ void __launch_bounds__(SSCD_T, 1) sparse_scd_kernel(SpScdParams p) {
   }
   __syncthreads();
   const uint32_t* mk = p.masks + tid;
-  uint32_t q0 = __ldcg(mk), q1 = (p.t1 - p.t0 > 1) ? __ldcg(mk + SSCD_T) : 0u;
+  uint32_t allbits = 0;
+  for (int v = 0; v < V; ++v)
+    if (tid + v * SSCD_T < n) allbits |= 1u << v;
+  uint32_t q0 = 0, q1 = 0;
+  if (!p.all_members) {
+    q0 = __ldcg(mk);
+    q1 = (p.t1 - p.t0 > 1) ? __ldcg(mk + SSCD_T) : 0u;
+  }
   for (int64_t t = p.t0; t < p.t1; ++t) {
     const int pb = (int)(t & 1);
-    const uint32_t inmask = q0;
-    q0 = q1;
-    const int64_t ahead = t - p.t0 + 2;
-    q1 = (ahead < p.t1 - p.t0) ? __ldcg(mk + ahead * SSCD_T) : 0u;
+    uint32_t inmask = allbits;
+    if (!p.all_members) {
+      inmask = q0;
+      q0 = q1;
+      const int64_t ahead = t - p.t0 + 2;
+      q1 = (ahead < p.t1 - p.t0) ? __ldcg(mk + ahead * SSCD_T) : 0u;
+    }
     double bv = -1.0, br = 0.0;
     int bi = INT_MAX;
     for (int v = 0; v < V; ++v) {
@@ -1053,6 +1064,7 @@ int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed,
   prm.Bv = Bv;
   prm.masks = masks;
   prm.V = V;
+  prm.all_members = (alpha_mode == ILS_ALPHA_FIXED && alpha_k >= h.n) ? 1 : 0;
   prm.st = h.dstat;
   const size_t smem = (size_t)h.npad * sizeof(double);
   ILS_CU(cudaFuncSetAttribute(sparse_scd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1067,7 +1079,7 @@ int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed,
   int pending = 0;
   while (t < max_inner) {
     const int64_t t1 = (t + ce < max_inner) ? t + ce : max_inner;
-    if ((rc = scd_masks(h, seed, k, t, t1, alpha_mode, alpha_k, SSCD_T, V, masks))) return rc;
+    if (!prm.all_members && (rc = scd_masks(h, seed, k, t, t1, alpha_mode, alpha_k, SSCD_T, V, masks))) return rc;
     prm.t0 = t;
     prm.t1 = t1;
     sparse_scd_kernel<<<1, SSCD_T, smem, st>>>(prm);

@@ -256,7 +256,7 @@ def test_scd_converges_c0():
 
 
 # ------------------------------------------------------------------ batched (K4)
-@pytest.mark.parametrize("method", ["sp", "rk", "rgs", "rcd"])
+@pytest.mark.parametrize("method", ["sp", "rk", "rgs", "rcd", "motzkin"])
 def test_batched_vs_oracle(method):
     from workloads import make_batched
     bt = make_batched(batch=24, p=96, q=32, n=32, base_seed=100)
@@ -267,8 +267,10 @@ def test_batched_vs_oracle(method):
     try:
         o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, max_inner=T, check_every=ce, inner_tol=0.0, seed=100,
                                  weighted=1 if method == "rcd" else 0)
+        if method == "motzkin":   # alpha = n: tau_t = [n], global argmax (Remark 4.1)
+            o.alpha_mode, o.alpha_k = ils.ILS_ALPHA_FIXED, bt.n
         fn = {"sp": ils.ils_sp_solve, "rk": ils.ils_rk_solve, "rgs": ils.ils_rgs_solve,
-              "rcd": ils.ils_rgs_solve}[method]
+              "rcd": ils.ils_rgs_solve, "motzkin": ils.ils_rgs_solve}[method]
         fn(h, None, x, 0.0, K, o)
     finally:
         ils.ils_destroy(h)
@@ -280,6 +282,9 @@ def test_batched_vs_oracle(method):
             ref = O.sp_solve(A1, A2, b1, b2, **kw)
         elif method == "rk":
             ref = O.sp_rk_rgs_solve(A1, A2, b1, b2, seed=100 + i, max_inner=T, check_every=ce, inner_tol=0.0, **kw)
+        elif method == "motzkin":
+            ref = O.sp_scd_solve(A1, A2, b1, b2, seed=100 + i, max_inner=T, check_every=ce, inner_tol=0.0,
+                                 alpha_mode=1, alpha_fixed=bt.n, **kw)
         else:
             ref = O.sp_scd_solve(A1, A2, b1, b2, seed=100 + i, max_inner=T, check_every=ce, inner_tol=0.0,
                                  weighted=(method == "rcd"), **kw)

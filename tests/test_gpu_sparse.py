@@ -131,7 +131,7 @@ def test_sparse_rk_fixed_horizon(T):
     assert list(inner) == list(ref.inner_hist)
 
 
-@pytest.mark.parametrize("mode", [(0, 1), (1, 1), (1, 5)])
+@pytest.mark.parametrize("mode", [(0, 1), (1, 1), (1, 5), (1, 10 ** 6)])
 def test_sparse_scd_fixed_horizon(mode):
     pr = make_sparse(600, 120, 80, 6, seed=16)
     A1, A2, b1, b2 = _dense(pr)
@@ -143,7 +143,7 @@ def test_sparse_scd_fixed_horizon(mode):
     x = np.zeros(pr.n)
     with HS(pr) as hh:
         o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, seed=9, max_inner=T, check_every=ce, inner_tol=0.0,
-                                 alpha_mode=amode, alpha_k=ak, x_hist=hist.ctypes.data)
+                                 alpha_mode=amode, alpha_k=min(ak, 2 ** 31 - 1), x_hist=hist.ctypes.data)
         ils.ils_rgs_solve(hh.h, None, x, 0.0, K, o)
     for kk in range(K):
         assert _rel(hist[kk], ref.x_hist[kk]) <= 1e-9, kk
