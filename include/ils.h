@@ -117,7 +117,10 @@ typedef struct {
   int32_t alpha_mode;        /* [ILS_ALPHA_UNIFORM] SCD alpha policy */
   int32_t alpha_k;           /* [1] alpha for ILS_ALPHA_FIXED */
   int32_t weighted;          /* [0] ils_rgs_solve: 1 = SP-RCD (alpha = 1, column-norm weights) */
-  int32_t sp_form;           /* [0] 0: x = P (A1^T b1 + A2^T (A2 x - b2)) (Sec23); 1: x += P A^T J (b - A x) */
+  int32_t sp_form;           /* [0] 0: x = P (A1^T b1 + A2^T (A2 x - b2)) (Sec23); 1: x += P A^T J (b - A x);
+                                2: the paper's literal layout: SP x = B x + c with B = P A2^T A2, c = P A^T J b
+                                formed once (Alg. 1 steps 2-6); RK/RGS b_hat = A2bar x + A^T J b
+                                with A2bar = A2^T A2 formed once (Alg. 2 steps 2-5, Alg. 5 steps 2-4). Dense only. */
   double* x_hist;            /* [NULL] optional [max_iter][n] record of every outer iterate (batch 1) */
   int64_t* inner_hist;       /* [NULL] optional [max_iter] inner step count per outer iteration */
 } ils_opts;

@@ -98,6 +98,12 @@ def sp_rhs(A1, A2, b1, b2, x) -> np.ndarray:
     return A1.T @ b1 + A2.T @ (A2 @ x - b2)
 
 
+def sp_rhs_literal(A2bar, AJb, x) -> np.ndarray:
+    """b_hat = A2bar x_k + A^T J b with the precomputed A2bar = A2^T A2 (Alg. 2 steps 2, 3, 5,
+    PAPER.md:291-294; Alg. 5 steps 2, 4) -- the paper's literal layout."""
+    return A2bar @ x + AJb
+
+
 def spectral_radius_sp(A1, A2) -> float:
     """rho((A1^T A1)^{-1} A2^T A2) (Theorem 2.1) as
     lambda_max(L^{-1} A2bar L^{-T}) with A1bar = L L^T (a similarity transform)."""
@@ -148,18 +154,26 @@ def sp_solve(A1, A2, b1, b2, x0=None, tol=1e-8, max_iter=20000, stop=STOP_XREF,
     """SP method, Alg. 1: x_{k+1} = (A1^T A1)^{-1} A2^T A2 x_k + (A1^T A1)^{-1} A^T J b
     (Eq. Sec23). P = (A1^T A1)^{-1} is applied by Cholesky solves
     (SPEC reading, DESIGN.md R12). sp_form 0: x_{k+1} = P c_k with c_k = sp_rhs(x_k);
-    sp_form 1 (correction form, identical in exact arithmetic): x_{k+1} = x_k + P A^T J (b - A x_k)."""
+    sp_form 1 (correction form, identical in exact arithmetic): x_{k+1} = x_k + P A^T J (b - A x_k);
+    sp_form 2 (Alg. 1 literal): B = P A2bar and c = P A^T J b formed explicitly
+    (P applied to the columns of A2bar by Cholesky solves), x_{k+1} = B x_k + c."""
     n = A1.shape[1]
     L = np.linalg.cholesky(_dense(A1.T @ A1))
 
     def apply_P(v):
         return sla.solve_triangular(L.T, sla.solve_triangular(L, v, lower=True), lower=False)
 
+    if sp_form == 2:
+        B = apply_P(_dense(A2.T @ A2))          # Alg. 1 step 3: B = (A1^T A1)^{-1} A2^T A2
+        c = apply_P(ajb(A1, A2, b1, b2))        # Alg. 1 step 4: c = (A1^T A1)^{-1} A^T J b
+
     x = np.zeros(n) if x0 is None else np.array(x0, dtype=np.float64)
     rep = Report(x=x)
     for k in range(max_iter):
         if sp_form == 0:
             x = apply_P(sp_rhs(A1, A2, b1, b2, x))
+        elif sp_form == 2:
+            x = B @ x + c                        # Alg. 1 step 6
         else:
             g = A1.T @ (b1 - A1 @ x) - A2.T @ (b2 - A2 @ x)
             x = x + apply_P(g)
@@ -232,7 +246,7 @@ def rk_rgs_inner(A1T, N, S, bhat, seed, k, max_inner, check_every, inner_tol,
 
 def sp_rk_rgs_solve(A1, A2, b1, b2, x0=None, tol=1e-8, max_iter=20000, stop=STOP_XREF,
                     x_ref=None, seed=0, max_inner=100000, check_every=None,
-                    inner_tol=1e-12) -> Report:
+                    inner_tol=1e-12, rhs_literal=False) -> Report:
     """SP-RK-RGS, Alg. 2: outer b_hat = A2bar x_k + A^T J b (step 5),
     inner RK-RGS (steps 6-12), x_{k+1} = z (step 13)."""
     n = A1.shape[1]
@@ -240,10 +254,12 @@ def sp_rk_rgs_solve(A1, A2, b1, b2, x0=None, tol=1e-8, max_iter=20000, stop=STOP
     N = ix.column_norms_sq(A1)
     _, S = ix.weights_prefix(N)
     ce = n if check_every is None else check_every
+    if rhs_literal:   # Alg. 2 steps 2-3
+        A2bar, AJb = _dense(A2.T @ A2), ajb(A1, A2, b1, b2)
     x = np.zeros(n) if x0 is None else np.array(x0, dtype=np.float64)
     rep = Report(x=x)
     for k in range(max_iter):
-        bhat = sp_rhs(A1, A2, b1, b2, x)
+        bhat = sp_rhs_literal(A2bar, AJb, x) if rhs_literal else sp_rhs(A1, A2, b1, b2, x)
         x, steps = rk_rgs_inner(A1T, N, S, bhat, seed, k, max_inner, ce, inner_tol)
         rep.inner_iters_total += steps
         rep.inner_hist.append(steps)
@@ -313,7 +329,7 @@ def scd_inner(G, N, S, bhat, seed, k, max_inner, check_every, inner_tol,
 
 def sp_scd_solve(A1, A2, b1, b2, x0=None, tol=1e-8, max_iter=20000, stop=STOP_XREF,
                  x_ref=None, seed=0, max_inner=100000, check_every=None, inner_tol=1e-12,
-                 alpha_mode=0, alpha_fixed=1, weighted=False) -> Report:
+                 alpha_mode=0, alpha_fixed=1, weighted=False, rhs_literal=False) -> Report:
     """SP-SCD, Alg. 5. A1bar = A1^T A1 formed once (step 2); the outer
     right side b_hat = A2bar x_k + A^T J b (step 4) is formed as sp_rhs(x_k)."""
     n = A1.shape[1]
@@ -321,10 +337,12 @@ def sp_scd_solve(A1, A2, b1, b2, x0=None, tol=1e-8, max_iter=20000, stop=STOP_XR
     N = ix.column_norms_sq(A1)
     _, S = ix.weights_prefix(N)
     ce = n if check_every is None else check_every
+    if rhs_literal:   # Alg. 5 step 2
+        A2bar, AJb = _dense(A2.T @ A2), ajb(A1, A2, b1, b2)
     x = np.zeros(n) if x0 is None else np.array(x0, dtype=np.float64)
     rep = Report(x=x)
     for k in range(max_iter):
-        bhat = sp_rhs(A1, A2, b1, b2, x)
+        bhat = sp_rhs_literal(A2bar, AJb, x) if rhs_literal else sp_rhs(A1, A2, b1, b2, x)
         x, steps = scd_inner(G, N, S, bhat, seed, k, max_inner, ce, inner_tol,
                              alpha_mode, alpha_fixed, weighted)
         rep.inner_iters_total += steps

@@ -481,4 +481,46 @@ int build_inverse(Handle& h) {
   return ILS_OK;
 }
 
+// Paper-literal precompute (Alg. 1 steps 2-4; Alg. 2 steps 2-3, :291-292):
+// A2bar = A2^T A2 (DMMA SYRK over the A2 rows), A^T J b = A1^T b1 - A2^T b2.
+int build_a2bar(Handle& h) {
+  if (h.have_a2bar) return ILS_OK;
+  const int64_t np = h.npad;
+  const size_t bytes = (size_t)np * np * sizeof(double);
+  if (!h.A2bar) ILS_CU(cudaMallocAsync(&h.A2bar, bytes, h.stream));
+  if (!h.lit_vec) ILS_CU(cudaMallocAsync(&h.lit_vec, 2 * (size_t)np * sizeof(double), h.stream));
+  ILS_CU(cudaMemsetAsync(h.A2bar, 0, bytes, h.stream));
+  if (h.q > 0) {
+    const int64_t kq = roundup(h.q, 32);
+    const int64_t tiles = (np / 64) * (np / 64 + 1) / 2;
+    const int sp = pick_splits(h, tiles, kq);
+    int r = gemm_launch<true, true>(h, np, np, kq, 1.0, h.Arm + h.p * np, np, h.Arm + h.p * np, np, 0.0, h.A2bar,
+                                    np, true, false, sp, false);
+    if (r) return r;
+    r = mirror_lower(h, h.A2bar, np, np, np);
+    if (r) return r;
+  }
+  int r = launch_gemv_cols(h.Arm + h.p * np, np, h.q, np, h.b + h.p, h.lit_vec, -1.0, h.a1tb1, h.stream);
+  if (r) return r;
+  h.have_a2bar = true;
+  return ILS_OK;
+}
+
+// B = P A2bar (DMMA GEMM) and c0 = P A^T J b (Alg. 1 steps 3-4)
+int build_explicit_b(Handle& h) {
+  if (h.have_B) return ILS_OK;
+  int r = build_inverse(h);
+  if (!r) r = build_a2bar(h);
+  if (r) return r;
+  const int64_t np = h.npad;
+  if (!h.Bmat) ILS_CU(cudaMallocAsync(&h.Bmat, (size_t)np * np * sizeof(double), h.stream));
+  const int sp = pick_splits(h, (np / 64) * (np / 64), np);
+  r = gemm_launch<false, true>(h, np, np, np, 1.0, h.P, np, h.A2bar, np, 0.0, h.Bmat, np, false, false, sp, sp > 1);
+  if (r) return r;
+  r = launch_gemv_rows(h.P, np, np, np, h.lit_vec, h.lit_vec + np, 1.0, nullptr, h.stream);
+  if (r) return r;
+  h.have_B = true;
+  return ILS_OK;
+}
+
 }  // namespace ils

@@ -139,7 +139,7 @@ static void free_handle_impl(Handle* h) {
   if (!h) return;
   cudaStream_t s = h->stream;
   double* bufs[] = {h->Arm, h->A1T, h->b, h->N, h->a1tb1, h->ajb, h->G, h->L, h->Z, h->P,
-                    h->part, h->wsA, h->vec, h->red, h->Ab, h->bb, h->rk_state};
+                    h->part, h->wsA, h->vec, h->red, h->Ab, h->bb, h->rk_state, h->A2bar, h->Bmat, h->lit_vec};
   for (double* p : bufs)
     if (p) cudaFreeAsync(p, s);
   if (h->S) cudaFreeAsync(h->S, s);
@@ -509,8 +509,12 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
   }
 
   const int64_t np = H.npad;
-  if (H.sparse && (o.sp_form == 1 || (method == 2 && o.weighted))) {
-    set_error("CSR input: sp_form = 1 and weighted SP-RCD are not implemented in this release");
+  if (o.sp_form < 0 || o.sp_form > 2 || (o.sp_form == 1 && method != 0)) {
+    set_error("solve: sp_form must be 0 or 2 (RK/RGS), 0..2 (SP)");
+    return ILS_ERR_ARG;
+  }
+  if (H.sparse && (o.sp_form != 0 || (method == 2 && o.weighted))) {
+    set_error("CSR input: sp_form 1/2 and weighted SP-RCD are not implemented in this release");
     return ILS_ERR_UNSUPPORTED;
   }
   // full residual g = A^T J (b - A x): dense stream kernel or the sparse row/column passes
@@ -520,19 +524,22 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
   // ---- setup (timed separately)
   ILS_CU(cudaMemsetAsync(&H.dstat->flag_err, 0, sizeof(int32_t), st));
   const bool gram_new = !H.have_gram && method != 1, inv_new = !H.have_P && method == 0;
+  const bool lit_new = o.sp_form == 2 && (method == 0 ? !H.have_B : !H.have_a2bar);
   ILS_CU(cudaEventRecord(H.ev0, st));
-  if (method == 0) rc = build_inverse(H);
+  if (method == 0) rc = (o.sp_form == 2) ? build_explicit_b(H) : build_inverse(H);
   else if (method == 2) rc = build_gram(H);
+  if (!rc && method != 0 && o.sp_form == 2) rc = build_a2bar(H);
   ILS_CU(cudaEventRecord(H.ev1, st));
   if (rc) return rc;
   const float setup_ms = elapsed(H);
-  if (gram_new || inv_new) {
+  if (gram_new || inv_new || lit_new) {
     const double nd = (double)H.n, pd = (double)H.p;
     H.hot_ms[3] += setup_ms;
     // algorithmic flops (LAPACK counts): SYRK p n (n+1) (sparse: 2 sum_i nnz_i^2 over A1 rows),
     // Cholesky n^3/3 + triangular inverse n^3/3 (+ P = Z^T Z n^3/3 when formed)
     const double gram = H.sparse ? 2.0 * H.a1_row_sq : pd * nd * (nd + 1.0);
-    H.hot_work[3] += (gram_new ? gram : 0.0) + (inv_new ? (H.use_zt ? 2.0 : 3.0) * nd * nd * nd / 3.0 : 0.0);
+    H.hot_work[3] += (gram_new ? gram : 0.0) + (inv_new ? (H.use_zt ? 2.0 : 3.0) * nd * nd * nd / 3.0 : 0.0) +
+                     (lit_new ? (double)H.q * nd * (nd + 1.0) + (method == 0 ? 2.0 * nd * nd * nd : 0.0) : 0.0);
     H.hot_n[3] += 1;
   }
   {
@@ -571,7 +578,7 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
   if (sx0.d()) ILS_CU(cudaMemcpyAsync(xk, sx0.d(), n * sizeof(double), cudaMemcpyDeviceToDevice, st));
   std::vector<int64_t> inner_hist;
 
-  if (method == 0 && o.stop != ILS_STOP_RR && !H.sparse) {
+  if (method == 0 && o.stop != ILS_STOP_RR && !H.sparse && o.sp_form != 2) {
     // whole SP loop in one persistent cooperative launch
     const int stop = (o.stop == ILS_STOP_XREF) ? ILS_STOP_XREF : ILS_STOP_NONE;
     if (max_iter > 0) {
@@ -583,7 +590,12 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
   } else {
     for (int64_t k = 0; k < max_iter; ++k) {
       int64_t steps = 0;
-      if (method == 0 && H.sparse) {   // sparse SP: c_k by the row/column passes, x = P c_k
+      if (method == 0 && o.sp_form == 2) {   // Alg. 1 literal: x_{k+1} = B x_k + c0 (one n x n GEMV)
+        ILS_CU(cudaEventRecord(H.evk0, st));
+        if ((rc = launch_gemv_rows(H.Bmat, np, np, np, xk, xnew, 1.0, H.lit_vec + np, st))) return rc;
+        ILS_CU(cudaEventRecord(H.evk1, st));
+        hot_account(H, 0, 8.0 * (double)n * (double)n);
+      } else if (method == 0 && H.sparse) {   // sparse SP: c_k by the row/column passes, x = P c_k
         ILS_CU(cudaEventRecord(H.evk0, st));
         if ((rc = sparse_rhs(H, xk, bhat, 0))) return rc;
         if ((rc = gemv_p(H, bhat, xnew))) return rc;
@@ -598,7 +610,9 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
           return rc;
       } else {
         // b_hat = A2bar x_k + A^T J b (K1 stream, rhs_only)
-        if (H.sparse) {
+        if (o.sp_form == 2) {   // b_hat = A2bar x_k + A^T J b (Alg. 2 step 5 / Alg. 5 step 4, literal)
+          if ((rc = launch_gemv_rows(H.A2bar, np, np, np, xk, bhat, 1.0, H.lit_vec, st))) return rc;
+        } else if (H.sparse) {
           if ((rc = sparse_rhs(H, xk, bhat, 0))) return rc;
         } else if ((rc = sp_run(H, xk, nullptr, 0.0, 1, ILS_STOP_NONE, nullptr, 0, nullptr, true, bhat, nullptr,
                                 nullptr, nullptr))) {
@@ -661,6 +675,9 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
       const double scd_step = 12.0 * ((double)H.gnnz / nd);
       rep->bytes_touched = outer * a2 + (method == 0 ? outer * 8.0 * (double)np * (double)np
                                                      : inner_total * (method == 1 ? rk_step : scd_step));
+    } else if (o.sp_form == 2) {   // literal forms: one n x n GEMV per outer step
+      const double inner_b = (method == 1) ? inner_total * 16.0 * p : (method == 2 ? inner_total * 8.0 * nd : 0.0);
+      rep->bytes_touched = outer * 8.0 * nd * nd + inner_b;
     } else if (method == 0)
       rep->bytes_touched = outer * (8.0 * q * (nd + 1) + 8.0 * nd * nd);
     else if (method == 1)

@@ -46,6 +46,11 @@ struct Handle {
   double* P = nullptr;      // npad x npad  (A1^T A1)^{-1}
   bool have_gram = false, have_P = false;
   bool use_zt = false;      // P applied as Z^T (Z c): P buffer holds Z^T (large sparse n)
+  // paper-literal precompute (sp_form = 2): A2bar = A2^T A2, B = P A2bar, c0 = P A^T J b
+  double* A2bar = nullptr;
+  double* Bmat = nullptr;
+  double* lit_vec = nullptr;   // [2][npad]: A^T J b, c0
+  bool have_a2bar = false, have_B = false;
 
   // workspace
   double* part = nullptr;   // partial sums [grid][npad]
@@ -136,6 +141,8 @@ int mirror_lower(Handle& h, double* C, int64_t ld, int64_t n, int64_t n_real);
 int cholesky_inverse(Handle& h, double* L, double* Z, int64_t npad);
 int build_gram(Handle& h);      // G = A1^T A1
 int build_inverse(Handle& h);   // L, Z, P from G
+int build_a2bar(Handle& h);     // A2bar = A2^T A2 and A^T J b (dense)
+int build_explicit_b(Handle& h);   // B = P A2bar, c0 = P A^T J b (dense)
 
 // sp.cu
 int sp_run(Handle& h, const double* x0_dev, double* x_dev, double tol, int64_t max_iter, int stop,

@@ -329,3 +329,30 @@ def test_c2_full_size_sp_iterates_and_convergence():
         st, rep = ils.ils_sp_solve(hh.h, None, x, pr.tol, 100, o)
     assert st == ils.ILS_OK and rep.converged
     assert _rel(x.cpu().numpy(), pr.xstar) <= pr.tol
+
+
+# ------------------------------------------------------------------ paper-literal precompute (sp_form 2)
+@pytest.mark.parametrize("method", ["sp", "rk", "rgs"])
+def test_literal_precompute_forms(method):
+    """Alg. 1 literal (B = P A2bar, c = P A^T J b) and the precomputed-A2bar right-hand side of
+    Alg. 2 / Alg. 5 (sp_form = 2) against the oracle's literal forms at a fixed horizon."""
+    pr = make_dense(180, 60, 40, 0.3, noise=0.05, seed=21)
+    K = 4
+    kw = dict(max_iter=K, stop=O.STOP_NONE)
+    if method == "sp":
+        ref = O.sp_solve(pr.A1, pr.A2, pr.b1, pr.b2, sp_form=2, **kw)
+    elif method == "rk":
+        ref = O.sp_rk_rgs_solve(pr.A1, pr.A2, pr.b1, pr.b2, seed=4, max_inner=200, check_every=40, inner_tol=0.0,
+                                rhs_literal=True, **kw)
+    else:
+        ref = O.sp_scd_solve(pr.A1, pr.A2, pr.b1, pr.b2, seed=4, max_inner=200, check_every=40, inner_tol=0.0,
+                             rhs_literal=True, **kw)
+    hist = np.zeros((K, pr.n))
+    x = np.zeros(pr.n)
+    with H(pr) as hh:
+        o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, sp_form=2, seed=4, max_inner=200, check_every=40,
+                                 inner_tol=0.0, x_hist=hist.ctypes.data)
+        fn = {"sp": ils.ils_sp_solve, "rk": ils.ils_rk_solve, "rgs": ils.ils_rgs_solve}[method]
+        fn(hh.h, None, x, 0.0, K, o)
+    for k in range(K):
+        assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k

@@ -402,6 +402,27 @@ def test_methods_converge_on_c0():
     assert O.spectral_radius_sp(pr.A1, pr.A2) < 1.0 and O.is_spd(O.normal_matrix(pr.A1, pr.A2))
 
 
+def test_paper_literal_forms_match_the_pinned_forms():
+    """Alg. 1 literal (explicit B = P A2bar, c = P A^T J b; sp_form 2) and the precomputed-A2bar
+    right-hand side of Alg. 2 / Alg. 5 equal the pinned streaming forms (the same iteration in
+    exact arithmetic, PAPER.md:126 vs :134-139; P1 closed form on the 2x2 example)."""
+    g = _load("sp_2x2.json")
+    A1, A2, b1, b2 = _np(g, "A1"), _np(g, "A2"), _np(g, "b1"), _np(g, "b2")
+    rep = O.sp_solve(A1, A2, b1, b2, max_iter=4, stop=O.STOP_NONE, sp_form=2)
+    for k, xk in enumerate(_np(g, "sp_iterates")):
+        assert np.allclose(rep.x_hist[k], xk, atol=1e-15), k
+    pr = make_dense(150, 40, 30, 0.3, noise=0.1, seed=2)
+    args = (pr.A1, pr.A2, pr.b1, pr.b2)
+    r0 = O.sp_solve(*args, max_iter=5, stop=O.STOP_NONE)
+    r2 = O.sp_solve(*args, max_iter=5, stop=O.STOP_NONE, sp_form=2)
+    for a, b in zip(r2.x_hist, r0.x_hist):
+        assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(b)
+    for fn, kw in ((O.sp_rk_rgs_solve, dict(max_inner=300)), (O.sp_scd_solve, dict(max_inner=300))):
+        ra = fn(*args, max_iter=3, stop=O.STOP_NONE, inner_tol=0.0, check_every=50, **kw)
+        rb = fn(*args, max_iter=3, stop=O.STOP_NONE, inner_tol=0.0, check_every=50, rhs_literal=True, **kw)
+        assert np.linalg.norm(ra.x - rb.x) <= 1e-10 * np.linalg.norm(ra.x)
+
+
 def test_sparse_inputs_match_the_pinned_dense_oracle():
     """The oracle on scipy.sparse CSR inputs (configs[3]) equals the pinned dense oracle on the
     same matrix: only the storage differs (PAPER.md:43-46 direct solve, Alg. 1 SP iterates)."""
