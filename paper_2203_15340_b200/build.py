@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIB_DIR, "libils.so")
-SOURCES = ["ils_api.cu", "ingest.cu", "dla.cu", "sp.cu", "rk_rgs.cu", "scd.cu", "batched.cu", "sparse.cu"]
+SOURCES = ["ils_api.cu", "ingest.cu", "dla.cu", "sp.cu", "rk_rgs.cu", "scd.cu", "batched.cu", "sparse.cu", "large.cu"]
 NVCC = os.environ.get("NVCC", "nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",

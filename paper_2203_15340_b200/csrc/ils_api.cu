@@ -297,6 +297,10 @@ int ils_create(ils_handle* out, const double* A, const double* b, int64_t p, int
     return ILS_OK;
   }
   h->npad = roundup(n, kPad);
+  {
+    const char* e = getenv("ILS_FORCE_LARGE");   // test hook: take the n > 8192 dense paths at any n
+    h->large = !csr && (h->npad > 8192 || (e && e[0] == '1'));
+  }
   h->ppad = roundup(p, kPad);
   const int64_t np = h->npad;
   if (csr) {   // ---- CSR input (sparse.cu)
@@ -578,7 +582,8 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
   if (sx0.d()) ILS_CU(cudaMemcpyAsync(xk, sx0.d(), n * sizeof(double), cudaMemcpyDeviceToDevice, st));
   std::vector<int64_t> inner_hist;
 
-  if (method == 0 && o.stop != ILS_STOP_RR && !H.sparse && o.sp_form != 2) {
+  const bool big = !H.sparse && H.large;   // dense n > 8192: host-looped two-pass SP (large.cu)
+  if (method == 0 && o.stop != ILS_STOP_RR && !H.sparse && o.sp_form != 2 && !big) {
     // whole SP loop in one persistent cooperative launch
     const int stop = (o.stop == ILS_STOP_XREF) ? ILS_STOP_XREF : ILS_STOP_NONE;
     if (max_iter > 0) {
@@ -595,12 +600,21 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
         if ((rc = launch_gemv_rows(H.Bmat, np, np, np, xk, xnew, 1.0, H.lit_vec + np, st))) return rc;
         ILS_CU(cudaEventRecord(H.evk1, st));
         hot_account(H, 0, 8.0 * (double)n * (double)n);
-      } else if (method == 0 && H.sparse) {   // sparse SP: c_k by the row/column passes, x = P c_k
+      } else if (method == 0 && (H.sparse || big)) {   // c_k by row/column passes, x = P c_k (+ x_k)
         ILS_CU(cudaEventRecord(H.evk0, st));
-        if ((rc = sparse_rhs(H, xk, bhat, 0))) return rc;
+        if (H.sparse) {
+          if ((rc = sparse_rhs(H, xk, bhat, 0))) return rc;
+        } else if ((rc = dense_rhs_twopass(H, xk, bhat, o.sp_form == 1))) {
+          return rc;
+        }
         if ((rc = gemv_p(H, bhat, xnew))) return rc;
+        if (big && o.sp_form == 1 && (rc = vec_add(H, xnew, xk, n))) return rc;
         ILS_CU(cudaEventRecord(H.evk1, st));
-        hot_account(H, 0, 12.0 * (double)(H.nnz - H.nnz1) + 16.0 * (double)H.q + 8.0 * (double)np * (double)np);
+        if (H.sparse)
+          hot_account(H, 0, 12.0 * (double)(H.nnz - H.nnz1) + 16.0 * (double)H.q + 8.0 * (double)np * (double)np, 2);
+        else   // two passes over A2 (or all of A under the correction form) + the P sweep
+          hot_account(H, 0, 16.0 * (double)(o.sp_form == 1 ? H.m : H.q) * (double)n + 8.0 * (double)np * (double)np,
+                      o.sp_form == 1 ? 5 : 3);
       } else if (method == 0) {   // SP under the RR rule: one persistent step at a time
         int64_t one = 0;
         double mm;

@@ -61,6 +61,7 @@ struct Handle {
   double* rk_state = nullptr;  // SP-RK-RGS chunk state: w, r, az [ppad] each, z [npad]
   void* scd_ws = nullptr;      // SP-SCD chunk state r, beta, r_tmp [npad], reductions, membership masks
   size_t scd_ws_bytes = 0;
+  bool large = false;          // dense n > 8192 (or ILS_FORCE_LARGE=1): two-pass SP RHS/check, global-z RK, smem-r SCD
   bool rk_single_step = false; // ILS_RK_SINGLE_STEP env: force the one-step-per-reduction RK-RGS kernel
   double* red = nullptr;    // reduction scratch [grid * 4]
   DevStatus* dstat = nullptr;
@@ -180,6 +181,12 @@ int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed,
 // scd.cu: membership masks of steps [t0, t1) for NT threads x V coordinates
 int scd_masks(Handle& h, uint64_t seed, int64_t k, int64_t t0, int64_t t1, int alpha_mode, int alpha_k, int NT, int V,
               uint32_t* masks);
+
+// large.cu (dense n > 8192)
+int dense_rhs_twopass(Handle& h, const double* x, double* c, int full);
+int rk_check_twopass(Handle& h, const double* z, const double* bhat, const double* w, double* r, double* az,
+                     double inner_tol, int64_t t_now);
+int vec_add(Handle& h, double* x, const double* y, int64_t n);
 
 // batched.cu
 int batched_solve(Handle& h, int method, const double* x0, double* x, double tol, int64_t max_iter,

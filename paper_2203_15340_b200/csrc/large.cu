@@ -1,0 +1,154 @@
+// large.cu -- dense inputs with n > 8192 (the paper's own Tables 2-5 sizes): rows of A
+// no longer fit a shared-memory ring next to register accumulators, so the outer right-hand side
+// runs as two passes (y = A2 x - b2 row pass, c = A1^T b1 + A2^T y column pass), x = P c uses the
+// generic P GEMV, and the SP-RK-RGS inner check is a row pass + column pass + a one-CTA decision.
+#include "common.cuh"
+#include "ils_internal.h"
+
+namespace ils {
+
+// y[i] = sum_j X[i][j] v[j] - b[i] over rows [0, rows), warp per row, two accumulators
+__global__ void rows_minus_b_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows, int64_t cols,
+                                    const double* __restrict__ v, const double* __restrict__ b,
+                                    double* __restrict__ y) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < rows; i += nw) {
+    const double* xr = X + i * ldx;
+    double s0 = 0.0, s1 = 0.0;
+    int64_t j = lane;
+    for (; j + 32 < cols; j += 64) {
+      s0 = fma(xr[j], v[j], s0);
+      s1 = fma(xr[j + 32], v[j + 32], s1);
+    }
+    if (j < cols) s0 = fma(xr[j], v[j], s0);
+    const double s = warp_sum(s0 + s1);
+    if (lane == 0) y[i] = b ? s - b[i] : s;
+  }
+}
+
+// c[j] = (base[j]) + alpha * sum_i X[i][j] y[i]: columns split over CTAs, rows over warps of a CTA
+// (fixed-order combine in shared memory), coalesced row segments
+__global__ void __launch_bounds__(256) cols_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows,
+                                                   int64_t cols, const double* __restrict__ y, double alpha,
+                                                   const double* base, double* c) {
+  __shared__ double part[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t j0 = (int64_t)blockIdx.x * 32; j0 < cols; j0 += (int64_t)gridDim.x * 32) {
+    const int64_t j = j0 + lane;
+    double s = 0.0;
+    if (j < cols)
+      for (int64_t i = warp; i < rows; i += 8) s = fma(X[i * ldx + j], y[i], s);
+    part[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && j < cols) {
+      double t = 0.0;
+      for (int w = 0; w < 8; ++w) t += part[w][lane];
+      c[j] = (base ? base[j] : 0.0) + alpha * t;
+    }
+    __syncthreads();
+  }
+}
+
+static int grid_cols(int64_t cols) {
+  int64_t g = (cols + 31) / 32;
+  return (int)(g > 148 * 8 ? 148 * 8 : (g < 1 ? 1 : g));
+}
+
+static int ensure_y(Handle& h) {
+  if (!h.sp_y) ILS_CU(cudaMallocAsync(&h.sp_y, (size_t)(h.m + 64 + h.npad) * sizeof(double), h.stream));
+  return ILS_OK;
+}
+
+// c = A1^T b1 + A2^T (A2 x - b2) (full = 0) or g = A^T J (b - A x) (full = 1), npad entries
+int dense_rhs_twopass(Handle& h, const double* x, double* c, int full) {
+  int rc = ensure_y(h);
+  if (rc) return rc;
+  const cudaStream_t st = h.stream;
+  const int64_t np = h.npad;
+  ILS_CU(cudaMemsetAsync(c, 0, np * sizeof(double), st));
+  if (!full) {
+    rows_minus_b_kernel<<<148 * 16, 256, 0, st>>>(h.Arm + h.p * np, np, h.q, h.n, x, h.b + h.p, h.sp_y);
+    ILS_LAUNCHED("rows_minus_b_kernel");
+    cols_kernel<<<grid_cols(h.n), 256, 0, st>>>(h.Arm + h.p * np, np, h.q, h.n, h.sp_y, 1.0, h.a1tb1, c);
+    ILS_LAUNCHED("cols_kernel");
+    return ILS_OK;
+  }
+  // g = A1^T (b1 - A1 x) - A2^T (b2 - A2 x) = -A1^T y1 + A2^T y2 with y = A x - b
+  rows_minus_b_kernel<<<148 * 16, 256, 0, st>>>(h.Arm, np, h.m, h.n, x, h.b, h.sp_y);
+  ILS_LAUNCHED("rows_minus_b_kernel");
+  cols_kernel<<<grid_cols(h.n), 256, 0, st>>>(h.Arm + h.p * np, np, h.q, h.n, h.sp_y + h.p, 1.0, nullptr, c);
+  ILS_LAUNCHED("cols_kernel");
+  cols_kernel<<<grid_cols(h.n), 256, 0, st>>>(h.Arm, np, h.p, h.n, h.sp_y, -1.0, c, c);   // in place per column
+  ILS_LAUNCHED("cols_kernel");
+  return ILS_OK;
+}
+
+// stop decision of the SP-RK-RGS inner check from g (already A1^T A1 z), one CTA, fixed order
+__global__ void __launch_bounds__(1024) check_finish_kernel(const double* __restrict__ g, const double* __restrict__ bhat,
+                                                            int64_t n, const double* __restrict__ az,
+                                                            const double* __restrict__ w, double* __restrict__ r,
+                                                            int64_t p, int64_t ppad, double inner_tol, int64_t t_now,
+                                                            DevStatus* st) {
+  __shared__ double red[32][2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (*(volatile int32_t*)&st->inner_conv) return;
+  double a = 0.0, b = 0.0;
+  for (int64_t j = tid; j < n; j += 1024) {
+    const double d = g[j] - bhat[j];
+    a = fma(d, d, a);
+    b = fma(bhat[j], bhat[j], b);
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if (lane == 0) {
+    red[warp][0] = a;
+    red[warp][1] = b;
+  }
+  __syncthreads();
+  double A = 0.0, B = 0.0;
+  for (int q = 0; q < 32; ++q) {
+    A += red[q][0];
+    B += red[q][1];
+  }
+  if (sqrt(A) <= inner_tol * sqrt(B)) {
+    if (tid == 0) {
+      st->inner_steps = t_now;
+      st->inner_conv = 1;
+    }
+  } else {
+    for (int64_t i = tid; i < ppad; i += 1024) r[i] = w[i] - (i < p ? az[i] : 0.0);
+  }
+}
+
+// the SP-RK-RGS inner check (include/ils.h) for large n: az = A1 z, g = A1^T az, decide, r = w - az
+int rk_check_twopass(Handle& h, const double* z, const double* bhat, const double* w, double* r, double* az,
+                     double inner_tol, int64_t t_now) {
+  int rc = ensure_y(h);
+  if (rc) return rc;
+  const cudaStream_t st = h.stream;
+  const int64_t np = h.npad;
+  rows_minus_b_kernel<<<148 * 16, 256, 0, st>>>(h.Arm, np, h.p, h.n, z, nullptr, az);
+  ILS_LAUNCHED("rows_minus_b_kernel");
+  double* g = h.sp_y + h.m + 64;
+  cols_kernel<<<grid_cols(h.n), 256, 0, st>>>(h.Arm, np, h.p, h.n, az, 1.0, nullptr, g);
+  ILS_LAUNCHED("cols_kernel");
+  check_finish_kernel<<<1, 1024, 0, st>>>(g, bhat, h.n, az, w, r, h.p, h.ppad, inner_tol, t_now, h.dstat);
+  ILS_LAUNCHED("check_finish_kernel");
+  return ILS_OK;
+}
+
+__global__ void add_kernel(double* __restrict__ x, const double* __restrict__ y, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] += y[i];
+}
+
+// x += y over n entries (the correction form x_{k+1} = x_k + P g_k on the two-pass path)
+int vec_add(Handle& h, double* x, const double* y, int64_t n) {
+  add_kernel<<<148, 256, 0, h.stream>>>(x, y, n);
+  ILS_LAUNCHED("add_kernel");
+  return ILS_OK;
+}
+
+}  // namespace ils

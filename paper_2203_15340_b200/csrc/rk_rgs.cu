@@ -48,6 +48,7 @@ struct RkParams {
   DevStatus* st;
   int C, slice, slicepad, nslots;
   long long* prof;     // optional per-phase cycle counters (rank 0, thread 0), see ILS_RK_PROF
+  int gmode;           // 1: z and the sampling table stay in global memory (large n, single-step kernel)
 };
 
 // Ring entries for steps t0 .. t0+31 (one per lane): Philox draw, two weighted inverse-CDF
@@ -100,10 +101,15 @@ __global__ void __launch_bounds__(512, 1) rk_rgs_kernel(RkParams p) {
   const bool stopped = *(volatile int32_t*)&p.st->inner_conv != 0;
 
   // shared memory carve-up
+  // gmode (large n): z lives in global memory (rank 0 updates it) and the sampler searches the
+  // global prefix sums; otherwise both are replicated in every CTA's shared memory
+  const bool gm = p.gmode != 0;
   double* slots = reinterpret_cast<double*>(smem_raw);                 // [NS][2][slicepad]
-  double* zs = slots + (size_t)NS * 2 * SP;                            // [npad]
-  uint64_t* Ss = reinterpret_cast<uint64_t*>(zs + p.npad);             // [n]
-  RkIdx* ring = reinterpret_cast<RkIdx*>(Ss + ((p.n + 1) & ~1));       // [RK_RING]
+  double* zsm = slots + (size_t)NS * 2 * SP;                           // [npad] (smem mode)
+  uint64_t* Ssm = reinterpret_cast<uint64_t*>(gm ? (double*)zsm : zsm + p.npad);   // [n] (smem mode)
+  RkIdx* ring = reinterpret_cast<RkIdx*>(gm ? (uint64_t*)zsm : Ssm + ((p.n + 1) & ~1));   // [RK_RING]
+  double* zs = gm ? p.Z : zsm;
+  const uint64_t* Ss = gm ? p.S : Ssm;
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + RK_RING);        // [NS]
   __shared__ __align__(16) double wred[2][RK_MAXW][4];
   __shared__ __align__(16) double recv[2][RK_MAXC][4];                 // per-rank partials (DSMEM target)
@@ -112,8 +118,10 @@ __global__ void __launch_bounds__(512, 1) rk_rgs_kernel(RkParams p) {
   __shared__ double bnorm_s;
   if (stopped) return;
 
-  for (int64_t j = tid; j < p.npad; j += NT) zs[j] = p.Z[j];
-  for (int j = tid; j < p.n; j += NT) Ss[j] = p.S[j];
+  if (!gm) {
+    for (int64_t j = tid; j < p.npad; j += NT) zsm[j] = p.Z[j];
+    for (int j = tid; j < p.n; j += NT) Ssm[j] = p.S[j];
+  }
   for (int64_t e = tid; e < (int64_t)NS * 2 * SP; e += NT) slots[e] = 0.0;   // zero tails
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
@@ -190,6 +198,9 @@ __global__ void __launch_bounds__(512, 1) rk_rgs_kernel(RkParams p) {
     const double* a1 = slots + (size_t)slot * 2 * SP;
     const double* a2 = a1 + SP;
     double d1 = 0.0, d2 = 0.0, d3 = 0.0;
+    // gmode: the global RMW of z_{j2} overlaps this step (the previous store to the same address
+    // precedes this load in thread 0's program order)
+    const double zold = (gm && rank == 0 && tid == 0) ? p.Z[ring[t & (RK_RING - 1)].j2] : 0.0;
     if (own > 0) mbar_wait(&bars[slot], ph);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -275,6 +286,7 @@ __global__ void __launch_bounds__(512, 1) rk_rgs_kernel(RkParams p) {
     const RkIdx ix = ring[t & (RK_RING - 1)];
     const double s1 = (ix.bh1 - D1) * ix.rn1;
     const double s2 = (D2 + s1 * D3) * ix.rn2;
+    // gmode: z_{j2} was loaded by rank 0 / thread 0 at the top of this step (zold below)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const double x1 = a1[tid + u * NT], x2 = a2[tid + u * NT];
@@ -282,7 +294,11 @@ __global__ void __launch_bounds__(512, 1) rk_rgs_kernel(RkParams p) {
       r[u] = fma(s1, x1, r[u]);
       r[u] = fma(-s2, x2, r[u]);
     }
-    if (tid == 0) zs[ix.j2] += s2;
+    if (!gm) {
+      if (tid == 0) zs[ix.j2] += s2;
+    } else if (rank == 0 && tid == 0) {
+      zs[ix.j2] = zold + s2;
+    }
     if (++slot == NS) {
       slot = 0;
       ph ^= 1u;
@@ -298,7 +314,7 @@ __global__ void __launch_bounds__(512, 1) rk_rgs_kernel(RkParams p) {
     }
   }
   __syncthreads();
-  if (rank == 0)
+  if (rank == 0 && !gm)
     for (int64_t j = tid; j < p.npad; j += NT) p.Z[j] = zs[j];
   if (CC > 1) cluster_sync_all();   // no CTA exits while peers may still access its smem
 }
@@ -809,9 +825,12 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
     const size_t budget = 200 * 1024;
     const size_t slot1 = (size_t)2 * p.slicepad * 8, slot4 = (size_t)Bk * slot1;
     const size_t fixed4 = fixed + 64 + (size_t)2 * ((h.n + 1) & ~1) * 8;   // + b_hat, 1/N tables
-    blocked = !h.rk_single_step && Bk > 1 && nt <= 256 && fixed4 + 2 * slot4 <= budget;
+    blocked = !h.rk_single_step && !h.large && Bk > 1 && nt <= 256 && fixed4 + 2 * slot4 <= budget;
+    // large n: z and the prefix sums do not fit next to two slots -> keep them in global memory
+    p.gmode = (!blocked && (h.large || fixed + 2 * slot1 > budget)) ? 1 : 0;
+    const size_t fixed_g = (size_t)RK_RING * sizeof(RkIdx) + 16 * 8 + 256;
     const size_t slot_bytes = blocked ? slot4 : slot1;
-    const size_t fixed_used = blocked ? fixed4 : fixed;
+    const size_t fixed_used = blocked ? fixed4 : (p.gmode ? fixed_g : fixed);
     if (fixed_used + 2 * slot_bytes > budget) {
       set_error("RK-RGS: shared memory too small for this problem size");
       return ILS_ERR_UNSUPPORTED;

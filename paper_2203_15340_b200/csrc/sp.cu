@@ -370,8 +370,12 @@ int sp_run(Handle& h, const double* x0_dev, double* x_dev, double tol, int64_t m
            const double* xref_dev, int sp_form, double* x_hist_dev, bool rhs_only, double* rhs_out,
            int64_t* iters_out, double* metric_out, int* conv_out) {
   const int64_t npad = h.npad;
-  if (npad > 8192) {
-    set_error("dense n > 8192 is not supported by the SP stream kernel in this release");
+  if (h.large) {   // large n: two-pass right-hand side (large.cu); the caller loops for SP
+    if (rhs_only) {
+      const int full = (sp_form == 1);
+      return dense_rhs_twopass(h, x0_dev, rhs_out ? rhs_out : h.vec + 2 * npad, full);
+    }
+    set_error("internal: the persistent SP kernel needs n <= 8192");
     return ILS_ERR_UNSUPPORTED;
   }
   if (!rhs_only) {
@@ -506,6 +510,7 @@ __global__ void __launch_bounds__(1024) rk_check_small_kernel(const double* __re
 
 int rk_check(Handle& h, const double* z, const double* bhat, const double* w, double* r, double* az,
              double inner_tol, int64_t t_now) {
+  if (h.large) return rk_check_twopass(h, z, bhat, w, r, az, inner_tol, t_now);
   if (h.ppad * h.npad <= (int64_t)1 << 20) {
     rk_check_small_kernel<<<1, 1024, 0, h.stream>>>(h.Arm, h.npad, h.p, h.n, h.ppad, z, bhat, w, r, az, inner_tol,
                                                      t_now, h.dstat);

@@ -851,6 +851,7 @@ int sparse_gram_csr(Handle& h) {
 }
 
 struct SpScdParams {
+  const double* Gd;        // dense A1bar rows (npad stride) for dense input with large n, else null
   const int64_t* gp;
   const int32_t* gc;
   const double* gv;
@@ -961,9 +962,14 @@ __global__ void __launch_bounds__(SSCD_T, 1) sparse_scd_kernel(SpScdParams p) {
     const int j = cix;
     const double sc = wr[pb][(j % SSCD_T) >> 5] / p.N[j];
     // r -= sc A1bar_(j): the row's columns are distinct
-    for (int64_t e = p.gp[j] + tid; e < p.gp[j + 1]; e += SSCD_T) {
-      const int c = p.gc[e];
-      rs[c] = fma(-sc, p.gv[e], rs[c]);
+    if (p.Gd) {
+      const double* grow = p.Gd + (int64_t)j * p.npad;
+      for (int c = tid; c < n; c += SSCD_T) rs[c] = fma(-sc, __ldcg(grow + c), rs[c]);
+    } else {
+      for (int64_t e = p.gp[j] + tid; e < p.gp[j + 1]; e += SSCD_T) {
+        const int c = p.gc[e];
+        rs[c] = fma(-sc, p.gv[e], rs[c]);
+      }
     }
     if (tid == 0) p.Bv[j] += sc;
     __syncthreads();
@@ -971,7 +977,8 @@ __global__ void __launch_bounds__(SSCD_T, 1) sparse_scd_kernel(SpScdParams p) {
   for (int s = tid; s < n; s += SSCD_T) p.Rv[s] = rs[s];
 }
 
-__global__ void __launch_bounds__(256) sparse_scd_check_kernel(const int64_t* __restrict__ gp, const int32_t* __restrict__ gc,
+__global__ void __launch_bounds__(256) sparse_scd_check_kernel(const double* __restrict__ Gd, int64_t npad,
+                                                               const int64_t* __restrict__ gp, const int32_t* __restrict__ gc,
                                                                const double* __restrict__ gv, int64_t n,
                                                                const double* __restrict__ bhat,
                                                                const double* __restrict__ Bv, double* __restrict__ Rv,
@@ -984,7 +991,11 @@ __global__ void __launch_bounds__(256) sparse_scd_check_kernel(const int64_t* __
   double a = 0.0, b = 0.0;
   for (int64_t j = (int64_t)blockIdx.x * 8 + warp; j < n; j += (int64_t)gridDim.x * 8) {
     double s = 0.0;
-    for (int64_t e = gp[j] + lane; e < gp[j + 1]; e += 32) s = fma(gv[e], Bv[gc[e]], s);
+    if (Gd) {
+      for (int64_t c = lane; c < n; c += 32) s = fma(Gd[j * npad + c], Bv[c], s);
+    } else {
+      for (int64_t e = gp[j] + lane; e < gp[j + 1]; e += 32) s = fma(gv[e], Bv[gc[e]], s);
+    }
     s = warp_sum(s);
     const double rj = bhat[j] - s;
     if (lane == 0) rtmp[j] = rj;
@@ -1024,7 +1035,8 @@ __global__ void __launch_bounds__(256) sparse_scd_check_kernel(const int64_t* __
 
 int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_t k, int64_t max_inner,
                      int64_t check_every, double inner_tol, int alpha_mode, int alpha_k, int64_t* steps_out) {
-  int rc = sparse_gram_csr(h);
+  // CSR input: A1bar compacted to CSR; dense input with large n: the dense A1bar rows
+  int rc = h.sparse ? sparse_gram_csr(h) : build_gram(h);
   if (rc) return rc;
   const cudaStream_t st = h.stream;
   const int64_t ce = check_every > 0 ? check_every : h.n;
@@ -1053,6 +1065,7 @@ int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed,
   ILS_CU(cudaMemsetAsync(&h.dstat->inner_conv, 0, sizeof(int32_t), st));
   ILS_CU(cudaMemsetAsync(&h.dstat->inner_steps, 0, sizeof(int64_t), st));
   SpScdParams prm{};
+  prm.Gd = h.sparse ? nullptr : h.G;
   prm.gp = h.gcsr_ptr;
   prm.gc = h.gcsr_col;
   prm.gv = h.gcsr_val;
@@ -1071,6 +1084,8 @@ int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed,
   const int64_t* gp = h.gcsr_ptr;
   const int32_t* gc = h.gcsr_col;
   const double* gv = h.gcsr_val;
+  const double* Gd = prm.Gd;
+  const int64_t npd = h.npad;
   const int64_t nn = h.n;
   DevStatus* dst = h.dstat;
   constexpr int kBatch = 8;
@@ -1088,8 +1103,8 @@ int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed,
     if (t % ce == 0) {
       double itol = inner_tol;
       int64_t tn = t;
-      void* args[] = {(void*)&gp, (void*)&gc, (void*)&gv, (void*)&nn, (void*)&bhat, (void*)&Bv, (void*)&Rv,
-                      (void*)&rtmp, (void*)&red, (void*)&itol, (void*)&tn, (void*)&dst};
+      void* args[] = {(void*)&Gd, (void*)&npd, (void*)&gp, (void*)&gc, (void*)&gv, (void*)&nn, (void*)&bhat,
+                      (void*)&Bv, (void*)&Rv, (void*)&rtmp, (void*)&red, (void*)&itol, (void*)&tn, (void*)&dst};
       ILS_CU(cudaLaunchCooperativeKernel((void*)sparse_scd_check_kernel, dim3(h.num_sms), dim3(256), args, 0, st));
       ILS_LAUNCHED("sparse_scd_check_kernel");
     }
@@ -1107,8 +1122,8 @@ int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed,
   ILS_CU(cudaStreamSynchronize(st));
   const int64_t steps = h.hstat->inner_conv ? h.hstat->inner_steps : max_inner;
   if (steps_out) *steps_out = steps;
-  const double row = (double)h.gnnz / (double)h.n;
-  hot_account(h, 2, (double)steps * 12.0 * row + (double)(steps / ce) * 12.0 * (double)h.gnnz, (steps + ce - 1) / ce);
+  const double row = h.sparse ? 12.0 * (double)h.gnnz / (double)h.n : 8.0 * (double)h.n;
+  hot_account(h, 2, (double)steps * row + (double)(steps / ce) * row * (double)h.n, (steps + ce - 1) / ce);
   return ILS_OK;
 }
 
