@@ -149,3 +149,34 @@ def test_large_real_n_above_8192(monkeypatch):
             fn(hh.h, None, x, 0.0, K, o)
             for k in range(K):
                 assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, (fn, kw, k)
+
+
+@pytest.mark.parametrize("shape", [(3000, 200, 200), (2500, 1, 300), (1500, 1, 70)])
+def test_paper_family_parity(shape):
+    """The paper's own families (§5.2, q = n; §5.3 Minkowski, q = 1)
+    at reduced sizes on the default routing: all three methods at fixed horizons against the oracle."""
+    from workloads import make_paper
+    p, q, n = shape
+    pr = make_paper(p, q, n, seed=37)
+    K = 3
+    refs = [
+        (ils.ils_sp_solve, O.sp_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE), {}),
+        (ils.ils_rk_solve, O.sp_rk_rgs_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE, seed=4,
+                                             max_inner=500, check_every=100, inner_tol=1e-6),
+         dict(max_inner=500, check_every=100, inner_tol=1e-6)),
+        (ils.ils_rgs_solve, O.sp_scd_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE, seed=4,
+                                           max_inner=300, check_every=60, inner_tol=1e-6, alpha_mode=0),
+         dict(max_inner=300, check_every=60, inner_tol=1e-6, alpha_mode=0)),
+    ]
+    with Big(pr, force=False) as hh:
+        for fn, ref, kw in refs:
+            hist = np.zeros((K, n))
+            inner = np.zeros(K, dtype=np.int64)
+            x = np.zeros(n)
+            o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, seed=4, x_hist=hist.ctypes.data,
+                                     inner_hist=inner.ctypes.data, **kw)
+            fn(hh.h, None, x, 0.0, K, o)
+            if fn is not ils.ils_sp_solve:
+                assert list(inner) == list(ref.inner_hist), fn
+            for k in range(K):
+                assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, (fn, k)

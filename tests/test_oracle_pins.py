@@ -16,7 +16,7 @@ import scipy.linalg as sla
 
 from oracle import ils_oracle as O
 from oracle import index_stream as ix
-from workloads import make_dense, make_problem
+from workloads import PAPER_TABLES, make_dense, make_paper, make_problem
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
@@ -442,6 +442,61 @@ def test_sparse_inputs_match_the_pinned_dense_oracle():
     # the generator's CSR layout: sorted distinct columns, row_ptr consistent
     assert np.all(np.diff(pr.row_ptr) == 5)
     assert all(np.all(np.diff(pr.col_idx[pr.row_ptr[i]:pr.row_ptr[i + 1]]) > 0) for i in range(pr.m))
+
+
+# ---------------------------------------------------------------- P19 the paper's own families
+def test_p19_paper_family_structure():
+    """§5.2 / §5.3 generator: A1, b in [0,1), A2 = 7*eye(q,n)."""
+    pr = make_paper(400, 30, 30, seed=3)
+    assert np.array_equal(pr.A2, 7.0 * np.eye(30))
+    assert pr.A1.min() >= 0.0 and pr.A1.max() < 1.0 and pr.b.min() >= 0.0 and pr.b.max() < 1.0
+    assert abs(pr.A1.mean() - 0.5) < 0.01 and abs(pr.A1.var() - 1.0 / 12.0) < 0.005
+    mk = make_paper(300, 1, 40, seed=4)
+    assert mk.q == 1 and np.array_equal(mk.A2[0], 7.0 * np.eye(1, 40)[0])
+    with pytest.raises(ValueError):
+        make_paper(10, 5, 4)
+    assert [len(v) for v in PAPER_TABLES.values()] == [3, 3, 3, 3]
+    assert PAPER_TABLES["t2"][0] == (30000, 13000, 13000) and PAPER_TABLES["t5"][2] == (60000, 1, 15000)
+
+
+def test_p19_song_family_spectral_radius_closed_form():
+    """q = n, A2 = 7I: B = (A1^T A1)^{-1} A2^T A2 = 49 (A1^T A1)^{-1}, so rho(B) = 49 / lambda_min(A1^T A1)
+    (Theorem 2.1); SP converges iff lambda_min > 49 (condition Sec13)."""
+    pr = make_paper(2500, 60, 60, seed=5)
+    lam = np.linalg.eigvalsh(pr.A1.T @ pr.A1).min()
+    rho = O.spectral_radius_sp(pr.A1, pr.A2)
+    assert abs(rho - 49.0 / lam) <= 1e-12 * max(rho, 1.0)
+    assert rho < 1.0 and O.is_spd(O.normal_matrix(pr.A1, pr.A2))
+    rep = O.sp_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=200, stop=O.STOP_NONE)
+    xs = O.direct_solve(pr.A1, pr.A2, pr.b1, pr.b2)
+    G = pr.A1.T @ pr.A1
+    errs = [np.sqrt((x - xs) @ G @ (x - xs)) for x in rep.x_hist[:6]]
+    for k in range(5):   # energy-norm contraction by rho per outer step (Theorem 2.1)
+        assert errs[k + 1] <= rho * errs[k] * (1 + 1e-9) + 1e-13
+
+
+def test_p19_minkowski_sherman_morrison():
+    """Minkowski space q = 1: A^T J A = A1^T A1 - 49 e1 e1^T, a rank-one
+    downdate. rho(B) = 49 [(A1^T A1)^{-1}]_11 and the SP / SP-RK-RGS limit equals the
+    Sherman-Morrison solution built from solves with A1^T A1 only."""
+    pr = make_paper(2000, 1, 30, seed=6)
+    G = pr.A1.T @ pr.A1
+    e = np.zeros(30)
+    e[0] = 1.0
+    Gi_e = np.linalg.solve(G, e)
+    assert abs(O.spectral_radius_sp(pr.A1, pr.A2) - 49.0 * Gi_e[0]) <= 1e-12
+    rhs = pr.A1.T @ pr.b1 - 7.0 * pr.b2[0] * e
+    y = np.linalg.solve(G, rhs)
+    x_sm = y + 49.0 * Gi_e * y[0] / (1.0 - 49.0 * Gi_e[0])
+    for rep in (O.sp_solve(pr.A1, pr.A2, pr.b1, pr.b2, tol=1e-14, stop=O.STOP_RR, max_iter=500),
+                O.sp_rk_rgs_solve(pr.A1, pr.A2, pr.b1, pr.b2, tol=1e-14, stop=O.STOP_RR, max_iter=500, seed=1,
+                                  max_inner=200000, inner_tol=1e-10)):
+        assert rep.converged
+        # ||x - x*|| <= ||M^{-1}||_2 ||A^T J (b - A x)||_2 with M = A^T J A = G - 49 e1 e1^T
+        g = pr.A1.T @ (pr.b1 - pr.A1 @ rep.x) - pr.A2.T @ (pr.b2 - pr.A2 @ rep.x)
+        bound = np.linalg.norm(g) / np.linalg.eigvalsh(G - 49.0 * np.outer(e, e)).min()
+        assert np.linalg.norm(rep.x - x_sm) <= bound * (1 + 1e-6) + 1e-14
+        assert np.linalg.norm(rep.x - x_sm) <= 1e-4 * np.linalg.norm(x_sm)
 
 
 def test_oracle_not_imported_by_product():

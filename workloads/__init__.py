@@ -12,6 +12,8 @@ from .configs import (  # noqa: F401
     make_dense,
     make_ill_conditioned,
     make_sparse,
+    make_paper,
+    PAPER_TABLES,
     SparseIls,
     fingerprint,
 )

@@ -228,6 +228,41 @@ CONFIGS = {
 }
 
 
+def make_paper(p: int, q: int, n: int, seed: int = 0, tol: float = 1e-6, name: str = "paper") -> IlsProblem:
+    """The paper's own synthetic family.
+
+    §5.2 (from Song's USSOR examples): A1 = rand(p,n), A2 = 7*eye(q,n),
+    b1 = rand(p,1), b2 = rand(q,1); Tables 2-3 use p in {30000, 40000}, q = n in
+    {13000, 14000, 15000}. §5.3 Minkowski: the same with q = 1 and
+    p in {50000, 60000} (Tables 4-5). MATLAB's rand is uniform on (0,1); here numpy's
+    Generator(Philox(seed)).random draws uniform [0,1) in the order A1, b1, b2 -- the same
+    distribution, not MATLAB's stream. The problem is not consistent (b is random): there is no
+    generating x*, so xstar is NaN and x_ref comes from a direct solve. tol is the paper's RR
+    threshold 1e-6.
+    """
+    if q > n:
+        raise ValueError("7*eye(q,n) with q > n has zero rows; the paper uses q = n or q = 1")
+    rng = _rng(seed)
+    m = p + q
+    A = np.zeros((m, n))
+    A[:p] = rng.random((p, n))
+    A[p + np.arange(q), np.arange(q)] = 7.0
+    b = np.empty(m)
+    b[:p] = rng.random(p)
+    b[p:] = rng.random(q)
+    return IlsProblem(name=name, A=A, b=b, p=p, q=q, xstar=np.full(n, np.nan), consistent=False, tol=tol,
+                      meta=dict(family="minkowski" if q == 1 else "song-ussor", seed=seed))
+
+
+# Tables 2-5 of the paper (PAPER.md:715-877): (table, p, q, n); q = "n" means q = n.
+PAPER_TABLES = {
+    "t2": [(30000, n, n) for n in (13000, 14000, 15000)],   # PAPER.md:713-750
+    "t3": [(40000, n, n) for n in (13000, 14000, 15000)],   # PAPER.md:755-787
+    "t4": [(50000, 1, n) for n in (13000, 14000, 15000)],   # PAPER.md:807-841
+    "t5": [(60000, 1, n) for n in (13000, 14000, 15000)],   # PAPER.md:843-877
+}
+
+
 def make_problem(name: str, seed: int = 0, **overrides):
     """Build config `name` (c0..c4) with optional shape overrides (tests use
     reduced shapes with the same recipe)."""
