@@ -15,6 +15,7 @@
 // A1bar row j from L2 -> update. The inner check r = b_hat - A1bar beta (include/ils.h) runs
 // between chunks as a full-GPU kernel (scd_check_kernel); r, beta pass through HBM between chunks.
 #include <climits>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -25,7 +26,8 @@ namespace cg = cooperative_groups;
 
 namespace ils {
 
-constexpr int SCD_MAXT = 256;    // threads per CTA (max)
+constexpr int SCD_MAXT = 256;    // threads per CTA (max; 512 and 1024 measured slower at n = 384-1000)
+constexpr int SCD_DEFT = SCD_MAXT;
 constexpr int SCD_MAXW = SCD_MAXT / 32;
 constexpr int SCD_RING = 128;
 constexpr int SCD_AHEAD = 64;
@@ -97,6 +99,104 @@ __global__ void __launch_bounds__(256) scd_masks_kernel(uint64_t seed, uint32_t 
     }
     masks[(int64_t)blockIdx.x * NT + th] = bits;
   }
+}
+
+// Single-warp SP-SCD for n <= 256 (non-weighted): lane l owns coordinates l + 32 v (v < V) of r
+// and beta in registers. Per step: masked local argmax -> 5 butterfly shuffles (every lane ends
+// with the winner, no barrier) -> r_j from the owner lane -> A1bar row j from L2 (V independent
+// coalesced loads per lane) -> update. No shared-memory round trip or CTA barrier on the
+// sequential path.
+template <int V>
+__global__ void __launch_bounds__(32, 1) scd_warp_kernel(ScdParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* rNs = reinterpret_cast<double*>(smem_raw);   // [n] 1 / A1bar_jj
+  double* bs = rNs + ((p.n + 1) & ~1);                  // [n] beta (off the sequential path)
+  const int lane = threadIdx.x;
+  const int n = p.n;
+  if (*(volatile int32_t*)&p.st->inner_conv) return;
+  for (int j = lane; j < n; j += 32) {
+    rNs[j] = 1.0 / p.N[j];
+    bs[j] = p.Bv[j];
+  }
+  double r[V];
+  double nb2 = 0.0;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int s = lane + 32 * v;
+    r[v] = (s < n) ? p.Rv[s] : 0.0;
+    if (s < n) nb2 = fma(p.bhat[s], p.bhat[s], nb2);
+  }
+  if (p.t0 == 0 && warp_sum(nb2) == 0.0) {   // b_hat = 0: beta = 0 after 0 steps
+    if (lane == 0) {
+      p.st->inner_steps = 0;
+      p.st->inner_conv = 1;
+    }
+    return;
+  }
+  __syncwarp();
+  uint32_t allbits = 0;
+#pragma unroll
+  for (int v = 0; v < V; ++v)
+    if (lane + 32 * v < n) allbits |= 1u << v;
+  const uint32_t* mk = p.masks + lane;
+  const int64_t L = p.t1 - p.t0;
+  uint32_t q0 = 0, q1 = 0, q2 = 0, q3 = 0;
+  if (!p.all_members) {
+    q0 = (0 < L) ? __ldcg(mk) : 0u;
+    q1 = (1 < L) ? __ldcg(mk + 32) : 0u;
+    q2 = (2 < L) ? __ldcg(mk + 64) : 0u;
+    q3 = (3 < L) ? __ldcg(mk + 96) : 0u;
+  }
+  for (int64_t t = p.t0; t < p.t1; ++t) {
+    uint32_t inmask = allbits;
+    if (!p.all_members) {
+      inmask = q0;
+      q0 = q1;
+      q1 = q2;
+      q2 = q3;
+      const int64_t ahead = t - p.t0 + 4;
+      q3 = (ahead < L) ? __ldcg(mk + ahead * 32) : 0u;
+    }
+    // lane-local argmax (coordinates ascend with v: strict > keeps the smallest index)
+    double bv = -1.0, br = 0.0;
+    int bi = INT_MAX;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const double q = r[v] * r[v];
+      if (((inmask >> v) & 1u) && q > bv) {
+        bv = q;
+        bi = lane + 32 * v;
+        br = r[v];
+      }
+    }
+    // butterfly argmax across lanes: every lane ends with the winner
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (argmax_better(ov, oi, bv, bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    const int j = bi;
+    const double rj = __shfl_sync(0xffffffffu, br, j & 31);   // the owner lane's local best is j
+    const double sc = rj * rNs[j];
+    const double* grow = p.G + (int64_t)j * p.npad + lane;
+    double g[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) g[v] = (lane + 32 * v < n) ? __ldcg(grow + 32 * v) : 0.0;
+    if (lane == (j & 31)) bs[j] += sc;
+#pragma unroll
+    for (int v = 0; v < V; ++v) r[v] = fma(-sc, g[v], r[v]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int s = lane + 32 * v;
+    if (s < n) p.Rv[s] = r[v];
+  }
+  for (int j = lane; j < n; j += 32) p.Bv[j] = bs[j];
 }
 
 // One CTA of NT <= 256 threads runs steps [t0, t1); thread tid owns coordinates s = tid + v*NT
@@ -203,40 +303,42 @@ __global__ void __launch_bounds__(SCD_MAXT, 1) scd_chunk_kernel(ScdParams p) {
           br = r[v];
         }
       }
-      // warp argmax (value, index); ties to the smallest index
+      // warp argmax (value, index, r) by butterfly: every lane ends with the warp winner; ties to
+      // the smallest index
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        const double orr = __shfl_xor_sync(0xffffffffu, br, o);
         if (argmax_better(ov, oi, bv, bi)) {
           bv = ov;
           bi = oi;
+          br = orr;
         }
       }
-      // the winning lane publishes (value, index, r)
-      if (bi != INT_MAX && (bi % NT) == tid) {
+      if (lane == 0) {
         wv[pb][warp] = bv;
         wi[pb][warp] = bi;
         wr[pb][warp] = br;
-      } else if (lane == 0 && bi == INT_MAX) {
-        wv[pb][warp] = -1.0;
-        wi[pb][warp] = INT_MAX;
       }
       __syncthreads();
       // every warp reduces the NW warp winners (same fixed tree in every warp)
       double cv = (lane < NW) ? wv[pb][lane] : -1.0;
       int ci = (lane < NW) ? wi[pb][lane] : INT_MAX;
+      double cr = (lane < NW) ? wr[pb][lane] : 0.0;
 #pragma unroll
       for (int o = SCD_MAXW / 2; o > 0; o >>= 1) {
         const double ov = __shfl_xor_sync(0xffffffffu, cv, o);
         const int oi = __shfl_xor_sync(0xffffffffu, ci, o);
+        const double orr = __shfl_xor_sync(0xffffffffu, cr, o);
         if (argmax_better(ov, oi, cv, ci)) {
           cv = ov;
           ci = oi;
+          cr = orr;
         }
       }
       j = __shfl_sync(0xffffffffu, ci, 0);   // lanes >= NW reduced only invalid entries
-      rj = wr[pb][(j % NT) >> 5];
+      rj = __shfl_sync(0xffffffffu, cr, 0);
     }
     const double sc = rj * rNs[j];
     const double* grow = p.G + (int64_t)j * p.npad;
@@ -330,7 +432,7 @@ int scd_masks(Handle& h, uint64_t seed, int64_t k, int64_t t0, int64_t t1, int a
 int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_t k, int64_t max_inner,
               int64_t check_every, double inner_tol, int alpha_mode, int alpha_k, int weighted,
               int64_t* steps_out) {
-  if (h.large || h.npad > 32 * SCD_MAXT) {   // large n: r in shared memory, dense A1bar rows (sparse.cu kernel)
+  if (h.large || h.npad > 32 * SCD_DEFT) {   // large n: r in shared memory, dense A1bar rows (sparse.cu kernel)
     if (weighted) {
       set_error("SP-RCD: n > 8192 is not implemented in this release");
       return ILS_ERR_UNSUPPORTED;
@@ -341,9 +443,18 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
   if (rc) return rc;
   const cudaStream_t st = h.stream;
   const int64_t ce = check_every > 0 ? check_every : h.n;
-  // threads: one coordinate per thread up to 256 coordinates, then V coordinates per thread
-  int nt = (int)((h.n + 31) / 32 * 32);
-  if (nt > SCD_MAXT) nt = SCD_MAXT;
+  // n <= 256 (non-weighted): one warp, V = n/32 coordinates per lane (scd_warp_kernel: no barrier,
+  // measured 16.6 vs 22.1 ms at c0); larger n: one coordinate per thread up to 256 coordinates, then
+  // V per thread (scd_chunk_kernel: at c1 the single warp's per-step issue of V = 32 loads, squares
+  // and compares made it slower, 220 vs 178 ms)
+  const char* env_cta = getenv("ILS_SCD_CTA");   // experiment override: force the multi-warp kernel
+  const bool warpk = !weighted && h.n <= 256 && !(env_cta && env_cta[0] == '1');
+  int nt = warpk ? 32 : (int)((h.n + 31) / 32 * 32);
+  if (nt > SCD_DEFT) nt = SCD_DEFT;
+  {
+    const char* e = getenv("ILS_SCD_NT");   // experiment override of the CTA size (multi-warp kernel)
+    if (e && !warpk && atoi(e) >= 64 && atoi(e) <= SCD_MAXT && (atoi(e) & 31) == 0) nt = atoi(e);
+  }
   const int per = (int)((h.n + nt - 1) / nt);
   int V = 1;
   while (V < per) V *= 2;
@@ -387,7 +498,14 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
   p.st = h.dstat;
   const size_t smem = 2 * (size_t)((h.n + 1) & ~1) * 8 + SCD_RING * sizeof(ScdKey);
   void* kern = nullptr;
-  switch (V) {
+  if (warpk) {
+    switch (V) {
+      case 1: kern = (void*)scd_warp_kernel<1>; break;
+      case 2: kern = (void*)scd_warp_kernel<2>; break;
+      case 4: kern = (void*)scd_warp_kernel<4>; break;
+      default: kern = (void*)scd_warp_kernel<8>; break;
+    }
+  } else switch (V) {
     case 1: kern = (void*)scd_chunk_kernel<1>; break;
     case 2: kern = (void*)scd_chunk_kernel<2>; break;
     case 4: kern = (void*)scd_chunk_kernel<4>; break;
@@ -422,7 +540,7 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
     p.t1 = t1;
     void* args[] = {&p};
     ILS_CU(cudaLaunchKernel(kern, dim3(1), dim3(nt), args, smem, st));
-    ILS_LAUNCHED("scd_chunk_kernel");
+    ILS_LAUNCHED(warpk ? "scd_warp_kernel" : "scd_chunk_kernel");
     t = t1;
     if (t % ce == 0) {
       double itol = inner_tol;

@@ -453,10 +453,6 @@ constexpr int SRK_MAXK = 512;   // column entries staged per column (longer colu
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-
 // first index f in sorted rows[0, k) with rows[f] == r, else -1
 __device__ __forceinline__ int find_row(const int32_t* rows, int k, int r) {
   int lo = 0, hi = k;
