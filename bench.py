@@ -15,8 +15,10 @@ Inputs are resident in HBM when the timed region starts; L2 is flushed (256 MiB 
 timed steps. e2e repeats the step with pinned HOST buffers (H2D of A, b, x_ref and D2H of x inside
 the timed region). cpu_baseline times the CPU oracle (test infrastructure) on a bounded sample.
 
-Multi-GPU: the single-instance path does not shard:
---gpus N runs N independent replicas (weak scaling), value = max over ranks of ms per step.
+Multi-GPU: the single-instance path does not shard ("replicas only"): --gpus N
+runs N independent replicas (weak scaling), value = max over ranks of ms per step. The batched
+config (c4) partitions instances: rank r solves its own 4096 instances (data seeds r*4096 + i,
+instance_partition()), no data-path collective (weak scaling).
 """
 from __future__ import annotations
 
@@ -75,17 +77,30 @@ def inner_tol_for(tol: float) -> float:
 DEFAULT_METHODS = {"c0": "sp,rk,rgs", "c1": "sp,rk,rgs", "c2": "sp", "c3": "sp", "c4": "sp,rk,rgs"}
 
 
-def load_problem(cfg: str):
+def instance_partition(rank: int, world: int, batch: int) -> tuple:
+    """Batched config under N ranks: rank r owns instances [r*batch, (r+1)*batch) of the global
+    seeded family (instance i has data seed i), so ranks hold disjoint instances and the job solves
+    world*batch instances (weak scaling, no collective on the data path)."""
+    if not 0 <= rank < world:
+        raise ValueError("rank out of range")
+    return rank * batch, (rank + 1) * batch
+
+
+def load_problem(cfg: str, rank: int = 0, world: int = 1):
     """Seeded synthetic workload (workloads/) and its x_ref: x* for consistent configs, else the
     oracle-written file workloads/xref/<cfg>_seed0.npy (tools/make_xref.py)."""
-    from workloads import fingerprint, make_problem
+    from workloads import CONFIGS, fingerprint, make_problem
+    if cfg == "c4":
+        lo, _ = instance_partition(rank, world, CONFIGS["c4"]["batch"])
+        pr = make_problem(cfg, seed=lo)
+        return pr, pr.xstar
     base = os.path.join(ROOT, "workloads", "xref", f"{cfg}_seed0")
     meta = None
     if os.path.exists(base + ".json"):
         with open(base + ".json") as f:
             meta = json.load(f)
     pr = make_problem(cfg, seed=(meta or {}).get("data_seed", 0))
-    if cfg == "c4" or pr.consistent:
+    if pr.consistent:
         return pr, pr.xstar
     if meta is None or meta["fingerprint"] != fingerprint(pr if hasattr(pr, "scipy") else pr.A, pr.b):
         raise RuntimeError(f"x_ref file {base}.npy does not match the generated {cfg} data; rerun tools/make_xref.py")
@@ -433,7 +448,7 @@ def main():
     peak_hbm, peak_bf16, _, peak_src = load_peaks()
     cfg = a.config
     methods = a.methods.split(",")
-    pr, xref = load_problem(cfg)
+    pr, xref = load_problem(cfg, rank, world)
     run = Runner(cfg, pr, xref, methods, torch, dev)
     flushbuf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -488,7 +503,7 @@ def main():
             "warmup": a.warmup, "ms_per_step": round(value, 4), "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "methods": methods,
-                       "parallelism": "replicas" if world > 1 else "single-gpu",
+                       "parallelism": ("instance-partition" if cfg == "c4" else "replicas") if world > 1 else "single-gpu",
                        "l2": "flushed between timed steps (256 MiB write)",
                        "create_ms": round(statistics.mean(s[1] for s in steps), 4)},
             "per_method": per,
