@@ -528,7 +528,7 @@ __global__ void __launch_bounds__(256, 1) rk_rgs_block_kernel(RkParams p) {
       // one-hop cluster all-to-all of the NVP values: warp 0 forms the CTA totals (lane l ->
       // value l) and sends them to every rank; each st.async instruction targets ONE destination
       // CTA with NVP contiguous doubles (destination-uniform instructions are ~2x faster than
-      // lane-scattered ones, and one sending warp beat sends spread over warps: tools/dsmem_bench.cu).
+      // lane-scattered ones, and one sending warp beat sends spread over warps: tools/mb/dsmem_bench.cu).
       if (warp == 0) {
         double v = mine;
         if (NW > 1) {
