@@ -266,106 +266,72 @@ __global__ void transpose_kernel(const double* __restrict__ A, double* __restric
 }
 
 // ---------------------------------------------------------------- 64x64 base: potf2 + trtri
-// One warp: Cholesky of a 32x32 SPD block held row-wise in registers (lane i = row i, r[j] =
-// A[i][j] for j <= i), then the inverse of the factor column-wise (lane c = column c of L^{-1}).
-// All indices are static after unrolling; broadcasts are shuffles. bad = a pivot was <= 0.
-__device__ __forceinline__ void chol32_inv32(double (&r)[32], double (&z)[32], int lane, int& bad) {
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    const double dkk = __shfl_sync(0xffffffffu, r[k], k);
-    if (!(dkk > 0.0) || !isfinite(dkk)) bad = 1;
-    const double s = sqrt(fmax(dkk, 0.0));
-    const double inv = (s > 0.0) ? 1.0 / s : 0.0;
-    if (lane > k) r[k] *= inv;
-    if (lane == k) r[k] = s;
-#pragma unroll
-    for (int j = k + 1; j < 32; ++j) {
-      const double ljk = __shfl_sync(0xffffffffu, r[k], j);
-      if (lane >= j) r[j] = fma(-r[k], ljk, r[j]);
-    }
-  }
-  // z = column `lane` of L^{-1}: Z[i][c] = (delta_ic - sum_{k<i} L[i][k] Z[k][c]) / L[i][i]
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    double s = (i == lane) ? 1.0 : 0.0;
-#pragma unroll
-    for (int k = 0; k < i; ++k) s = fma(-__shfl_sync(0xffffffffu, r[k], i), z[k], s);
-    const double lii = __shfl_sync(0xffffffffu, r[i], i);
-    z[i] = (lane <= i && lii > 0.0) ? s / lii : 0.0;
-  }
-}
-
-// C[32x32] (+)= alpha * X * Y^T-ish products over 32 in shared memory (all threads of the CTA).
-// mode 0: C = A * B^T (C[i][j] = sum_k A[i][k] B[j][k]); mode 1: C = A * B (sum_k A[i][k] B[k][j])
-__device__ __forceinline__ void mm32(double (*C)[65], const double (*A)[65], const double (*B)[65], int mode,
-                                     double alpha, bool accumulate, bool lower_only) {
-  for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
-    const int i = e >> 5, j = e & 31;
-    if (lower_only && j > i) continue;
-    double s = 0.0;
-#pragma unroll 8
-    for (int k = 0; k < 32; ++k) s = fma(A[i][k], mode == 0 ? B[j][k] : B[k][j], s);
-    C[i][j] = accumulate ? fma(alpha, s, C[i][j]) : alpha * s;
-  }
-}
-
-// Lower-triangle Cholesky of the 64x64 block at (s0, s0) of L (in place) and its inverse into Z,
-// as a 2x2 block recursion over 32x32 sub-blocks: chol/inv of A11 (warp 0), L21 = A21 Z11^T,
-// A22 -= L21 L21^T, chol/inv of A22 (warp 0), Z21 = -Z22 (L21 Z11).
+// Cholesky of the 64x64 diagonal block at (s0, s0) of L (lower, in place) and its inverse into Z,
+// in shared memory with loops (no full unrolling: a fully unrolled 32x32 register version was
+// ~54k SASS instructions executed once and instruction-fetch bound, 187 us per block on B200).
+// Right-looking potf2: per column k one pivot, a column scale and a rank-1 update of the trailing
+// lower triangle by a 16x16 thread grid (4x4 elements each). trtri: row by row, Z[i][c] for all
+// c <= i in parallel, 4 threads per column splitting the k-sum (fixed shuffle order).
 __global__ void __launch_bounds__(256) potf2_trtri_kernel(double* __restrict__ L, double* __restrict__ Z,
                                                           int64_t ld, int64_t s0, int32_t* err) {
   extern __shared__ __align__(16) double potf_smem[];
   double (*a)[65] = reinterpret_cast<double (*)[65]>(potf_smem);            // [64][65] A, then L
   double (*zi)[65] = reinterpret_cast<double (*)[65]>(potf_smem + 64 * 65);  // [64][65] Z
-  double (*t)[65] = reinterpret_cast<double (*)[65]>(potf_smem + 128 * 65);  // [32][65] scratch
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ double rdiag[64];   // 1 / L_ii
+  __shared__ int bad_s;
+  const int tid = threadIdx.x;
   double* blk = L + s0 * ld + s0;
   for (int e = tid; e < 64 * 64; e += 256) {
     const int i = e >> 6, j = e & 63;
     a[i][j] = (j <= i) ? blk[i * ld + j] : 0.0;
     zi[i][j] = 0.0;
   }
-  __syncthreads();
-  __shared__ int bad_s;
   if (tid == 0) bad_s = 0;
   __syncthreads();
-  auto factor = [&](int o) {   // chol + inverse of the 32x32 diagonal block at (o, o) by warp 0
-    if (warp == 0) {
-      double r[32], z[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        r[j] = (j <= lane) ? a[o + lane][o + j] : 0.0;
-        z[j] = 0.0;
+  const int ty = tid >> 4, tx = tid & 15;   // 16x16 grid, rows ty + 16 u, columns tx + 16 v
+  for (int k = 0; k < 64; ++k) {
+    // pivot: every row thread takes sqrt(a_kk) itself (no extra barrier); row k stores it
+    if (tid >= k && tid < 64) {
+      const double d = a[k][k];
+      const bool ok = d > 0.0 && isfinite(d);
+      const double rs = ok ? rsqrt(d) : 0.0;   // 1 / L_kk
+      if (tid == k) {
+        if (!ok) bad_s = 1;
+        a[k][k] = d * rs;
+        rdiag[k] = rs;
+      } else {
+        a[tid][k] *= rs;
       }
-      int bad = 0;
-      chol32_inv32(r, z, lane, bad);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        a[o + lane][o + j] = (j <= lane) ? r[j] : 0.0;
-        zi[o + j][o + lane] = z[j];
-      }
-      if (__any_sync(0xffffffffu, bad) && lane == 0) bad_s = 1;
     }
     __syncthreads();
-  };
-  factor(0);
-  // L21 = A21 Z11^T  (a[32..63][0..31])
-  mm32(t, reinterpret_cast<const double (*)[65]>(&a[32][0]), reinterpret_cast<const double (*)[65]>(&zi[0][0]), 0, 1.0,
-       false, false);
-  __syncthreads();
-  for (int e = tid; e < 1024; e += 256) a[32 + (e >> 5)][e & 31] = t[e >> 5][e & 31];
-  __syncthreads();
-  // A22 -= L21 L21^T (lower)
-  mm32(reinterpret_cast<double (*)[65]>(&a[32][32]), reinterpret_cast<const double (*)[65]>(&a[32][0]),
-       reinterpret_cast<const double (*)[65]>(&a[32][0]), 0, -1.0, true, true);
-  __syncthreads();
-  factor(32);
-  // Z21 = -Z22 (L21 Z11): T = L21 Z11, then Z21 = -Z22 T
-  mm32(t, reinterpret_cast<const double (*)[65]>(&a[32][0]), reinterpret_cast<const double (*)[65]>(&zi[0][0]), 1, 1.0,
-       false, false);
-  __syncthreads();
-  mm32(reinterpret_cast<double (*)[65]>(&zi[32][0]), reinterpret_cast<const double (*)[65]>(&zi[32][32]),
-       reinterpret_cast<const double (*)[65]>(&t[0][0]), 1, -1.0, false, false);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = ty + 16 * u;
+      if (i <= k) continue;
+      const double lik = a[i][k];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int j = tx + 16 * v;
+        if (j > k && j <= i) a[i][j] = fma(-lik, a[j][k], a[i][j]);
+      }
+    }
+    __syncthreads();
+  }
+  // Z = L^{-1}: Z[i][c] = (delta_ic - sum_{c <= k < i} L[i][k] Z[k][c]) / L[i][i]. Column c belongs
+  // to one quad of lanes of one warp (4 threads split the k-sum), so the forward substitution
+  // needs only warp-level synchronisation.
+  const int c = tid >> 2, part = tid & 3;
+  for (int i = (tid >> 5) * 8; i < 64; ++i) {   // warp-uniform trip count (the warp's first column)
+    double sum = 0.0;
+    if (i >= c)
+      for (int k = c + part; k < i; k += 4) sum = fma(a[i][k], zi[k][c], sum);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    if (part == 0 && i >= c) {
+      zi[i][c] = (((i == c) ? 1.0 : 0.0) - sum) * rdiag[i];
+    }
+    __syncwarp();
+  }
   __syncthreads();
   double* zb = Z + s0 * ld + s0;
   for (int e = tid; e < 64 * 64; e += 256) {
@@ -379,7 +345,7 @@ __global__ void __launch_bounds__(256) potf2_trtri_kernel(double* __restrict__ L
 // Recursive Cholesky + inverse on blocks [s, e) (units of 64).
 static int chol_rec(Handle& h, double* L, double* Z, int64_t ld, int64_t s, int64_t e, double* tmp) {
   if (e - s == 1) {
-    const int smem = (2 * 64 + 32) * 65 * (int)sizeof(double);
+    const int smem = 2 * 64 * 65 * (int)sizeof(double);
     ILS_CU(cudaFuncSetAttribute(potf2_trtri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     potf2_trtri_kernel<<<1, 256, smem, h.stream>>>(L, Z, ld, s * 64, &h.dstat->flag_err);
     ILS_LAUNCHED("potf2_trtri_kernel");

@@ -33,29 +33,55 @@ int launch_transpose_a1(Handle& h) {
 }
 
 // N_j = (((0 + a_0j^2) + a_1j^2) + ...) with every square rounded (no FMA contraction).
-__global__ void colnorms_kernel(const double* __restrict__ Arm, int64_t npad, int64_t p, int64_t n,
-                                double* __restrict__ N) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
+// N_j = sum_i a_ij^2 in sequential row order, each product and sum rounded (no FMA): the oracle's
+// definition bit for bit (R7). One CTA per 32 columns: 8 warps stream 32-row tiles of
+// the column group into an 8-stage shared-memory ring with 16-byte cp.async (deep memory-level
+// parallelism), warp 0 runs the 32 sequential per-column sums out of shared memory.
+constexpr int CN_TR = 32;        // rows per tile
+constexpr int CN_ST = 8;         // ring stages
+__global__ void __launch_bounds__(256) colnorms_kernel(const double* __restrict__ Arm, int64_t npad, int64_t p,
+                                                       int64_t n, double* __restrict__ N) {
+  extern __shared__ __align__(16) unsigned char cn_smem[];
+  double(*ring)[CN_TR][32] = reinterpret_cast<double(*)[CN_TR][32]>(cn_smem);   // [CN_ST][CN_TR][32]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t j0 = (int64_t)blockIdx.x * 32;
+  const int64_t ntiles = (p + CN_TR - 1) / CN_TR;
+  auto issue = [&](int64_t t) {
+    if (t < ntiles) {
+      double(*dst)[32] = ring[t % CN_ST];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int c = tid + 256 * k;   // 512 16-byte chunks: row c / 16, column pair c % 16
+        const int64_t i = t * CN_TR + (c >> 4);
+        if (i < p) cp_async16(&dst[c >> 4][2 * (c & 15)], Arm + i * npad + j0 + 2 * (c & 15));
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int t = 0; t < CN_ST - 1; ++t) issue(t);
   double s = 0.0;
-  int64_t i = 0;
-  for (; i + 8 <= p; i += 8) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldg(Arm + (i + u) * npad + j);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) s = __dadd_rn(s, __dmul_rn(v[u], v[u]));
+  for (int64_t t = 0; t < ntiles; ++t) {
+    cp_async_wait<CN_ST - 2>();
+    __syncthreads();   // tile t visible to warp 0; every thread is done with tile t - 1
+    issue(t + CN_ST - 1);
+    if (warp == 0) {
+      const double(*tile)[32] = ring[t % CN_ST];
+      const int rows = (int)((p - t * CN_TR) < CN_TR ? (p - t * CN_TR) : CN_TR);
+      for (int r = 0; r < rows; ++r) {
+        const double v = tile[r][lane];
+        s = __dadd_rn(s, __dmul_rn(v, v));
+      }
+    }
   }
-  for (; i < p; ++i) {
-    const double v = __ldg(Arm + i * npad + j);
-    s = __dadd_rn(s, __dmul_rn(v, v));
-  }
-  N[j] = s;
+  cp_async_wait<0>();
+  if (warp == 0 && j0 + lane < n) N[j0 + lane] = s;
 }
 
 int launch_colnorms(Handle& h) {
-  const int bs = 128;
-  colnorms_kernel<<<(unsigned)((h.n + bs - 1) / bs), bs, 0, h.stream>>>(h.Arm, h.npad, h.p, h.n, h.N);
+  const int smem = CN_ST * CN_TR * 32 * (int)sizeof(double);
+  ILS_CU(cudaFuncSetAttribute(colnorms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  colnorms_kernel<<<(unsigned)((h.n + 31) / 32), 256, smem, h.stream>>>(h.Arm, h.npad, h.p, h.n, h.N);
   ILS_LAUNCHED("colnorms_kernel");
   return ILS_OK;
 }
