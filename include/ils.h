@@ -77,6 +77,8 @@ extern "C" {
 #endif
 
 typedef struct ils_handle_s* ils_handle;
+typedef struct ils_comm_s* ils_comm;   /* NCCL communicator for row-sharded handles */
+#define ILS_COMM_ID_BYTES 128
 
 enum {
   ILS_OK = 0,
@@ -104,6 +106,14 @@ typedef struct {
   const int64_t* row_ptr;    /* [m + 1], row_ptr[0] = 0, non-decreasing, row_ptr[m] = nnz */
   const int32_t* col_idx;    /* [nnz], 0 <= col < n, strictly increasing within each row */
   int64_t nnz;
+  /* Row sharding (dense, batch 1): A and b hold THIS rank's row block
+   * [A1_r; A2_r] (p = p_r >= 1 rows of A1, q = q_r >= 0 rows of A2; the global p >= n is the
+   * caller's to guarantee). Row sums (A1^T A1, column norms, c_k, A^T J (b - A x)) are reduced
+   * over comm with NCCL all-reduce; every rank then holds identical iterates. Supported:
+   * ils_sp_solve (sp_form 0/1, all stop rules), ils_rgs_solve (SP-SCD/RCD; the inner solve runs
+   * replicated), ils_relative_residual. ils_rk_solve (needs whole columns of A1), sp_form 2 and
+   * ils_direct_solve return ILS_ERR_UNSUPPORTED. NULL = unsharded. Borrowed until ils_destroy. */
+  ils_comm comm;
 } ils_ext;
 
 /* Solver options; ils_default_opts() fills the defaults given in brackets. */
@@ -198,6 +208,14 @@ ILS_API int ils_rk_indices(ils_handle h, uint64_t seed, int64_t k, int64_t t0, i
  * step t of outer iteration k, by the device code the inner kernel uses. */
 ILS_API int ils_scd_subset(int64_t n, uint64_t seed, int64_t k, int64_t t, int32_t alpha_mode,
                    int32_t alpha_k, int32_t* alpha, uint8_t* mask);
+
+/* Row-sharded handles (ext->comm): one NCCL communicator per process/GPU. Rank 0 calls
+ * ils_comm_unique_id (ILS_COMM_ID_BYTES bytes, host), shares it with the other ranks by any
+ * out-of-band means (e.g. torch.distributed broadcast), then every rank calls ils_comm_create
+ * with its rank on its own device. NCCL is loaded at run time (ILS_ERR_UNSUPPORTED if absent). */
+ILS_API int ils_comm_unique_id(void* id);
+ILS_API int ils_comm_create(const void* id, int nranks, int rank, ils_comm* comm);
+ILS_API void ils_comm_destroy(ils_comm comm);
 
 /* Total kernels launched by this process through libils (for launch accounting). */
 ILS_API int64_t ils_kernel_launch_count(void);

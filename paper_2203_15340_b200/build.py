@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIB_DIR, "libils.so")
-SOURCES = ["ils_api.cu", "ingest.cu", "dla.cu", "sp.cu", "rk_rgs.cu", "scd.cu", "batched.cu", "sparse.cu", "large.cu"]
+SOURCES = ["ils_api.cu", "ingest.cu", "dla.cu", "sp.cu", "rk_rgs.cu", "scd.cu", "batched.cu", "sparse.cu", "large.cu", "comm.cu"]
 NVCC = os.environ.get("NVCC", "nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
@@ -40,7 +40,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
                 raise RuntimeError(f"nvcc failed on {s}")
             objs.append(o)
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
-           "-Xcompiler", "-fPIC", *objs, "-o", LIB]
+           "-Xcompiler", "-fPIC", *objs, "-ldl", "-o", LIB]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -408,6 +408,9 @@ int build_gram(Handle& h) {
   int r = gemm_launch<false, false>(h, np, np, h.ppad, 1.0, h.A1T, h.ppad, h.A1T, h.ppad, 0.0, h.G, np,
                                     true, false, sp, false);
   if (r) return r;
+  // row-sharded handle: sum the ranks' lower triangles before the mirror sets the padded diagonal
+  r = allreduce_sum(h, h.G, np * np);
+  if (r) return r;
   r = mirror_lower(h, h.G, np, np, h.n);
   if (r) return r;
   h.have_gram = true;

@@ -223,11 +223,17 @@ int ils_create(ils_handle* out, const double* A, const double* b, int64_t p, int
   *out = nullptr;
   const int64_t lda = (ext && ext->lda) ? ext->lda : n;
   const int64_t batch = (ext && ext->batch > 0) ? ext->batch : 1;
-  if (p < 1 || q < 0 || n < 1 || p < n || lda < n) {
-    set_error("ils_create: need p >= 1, q >= 0, n >= 1, p >= n, lda >= n");
+  const bool sharded = ext && ext->comm;
+  // a row shard may hold fewer than n rows of A1; the global p >= n is the caller's contract
+  if (p < 1 || q < 0 || n < 1 || (!sharded && p < n) || lda < n) {
+    set_error("ils_create: need p >= 1, q >= 0, n >= 1, p >= n (unsharded), lda >= n");
     return ILS_ERR_SHAPE;
   }
   const bool csr = ext && ext->format == ILS_FORMAT_CSR;
+  if (sharded && (csr || batch != 1)) {
+    set_error("ils_create: row sharding (ext->comm) needs dense input and batch 1");
+    return ILS_ERR_UNSUPPORTED;
+  }
   if (ext && ext->format != ILS_FORMAT_DENSE && !csr) {
     set_error("ils_create: unknown format");
     return ILS_ERR_ARG;
@@ -243,6 +249,7 @@ int ils_create(ils_handle* out, const double* A, const double* b, int64_t p, int
   h->m = p + q;
   h->batch = batch;
   h->stream = ext ? static_cast<cudaStream_t>(ext->stream) : nullptr;
+  h->comm = sharded ? static_cast<ils::ils_comm_impl*>(ext->comm) : nullptr;
   int dev = 0;
   cudaGetDevice(&dev);
   {   // keep freed stream-ordered allocations cached in the pool: handles of the same size reuse
@@ -389,6 +396,7 @@ int ils_create(ils_handle* out, const double* A, const double* b, int64_t p, int
   CKC(cudaMallocAsync(&h->N, (size_t)n * sizeof(double), st));
   CKC(cudaMallocAsync(&h->S, (size_t)n * sizeof(uint64_t), st));
   CK(launch_colnorms(*h));
+  CK(allreduce_sum(*h, h->N, n));   // sharded: N_j = sum over ranks (comm.cu)
   CKC(cudaMemsetAsync(&h->dstat->flag_err, 0, sizeof(int32_t), st));
   CK(launch_weights(*h, &h->dstat->flag_err));
   CKC(cudaMallocAsync(&h->a1tb1, (size_t)np * sizeof(double), st));
@@ -521,9 +529,16 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
     set_error("CSR input: sp_form 1/2 and weighted SP-RCD are not implemented in this release");
     return ILS_ERR_UNSUPPORTED;
   }
+  const bool sharded = H.comm != nullptr;
+  if (sharded && (method == 1 || o.sp_form == 2)) {
+    set_error("row-sharded handle: SP-RK-RGS (needs whole columns of A1) and sp_form 2 are not supported");
+    return ILS_ERR_UNSUPPORTED;
+  }
   // full residual g = A^T J (b - A x): dense stream kernel or the sparse row/column passes
+  // (sharded: local rows, then the sum over ranks)
   auto full_res = [&](const double* xv, double* gv) -> int {
-    return H.sparse ? sparse_rhs(H, xv, gv, 1) : full_residual(H, xv, gv);
+    const int r = H.sparse ? sparse_rhs(H, xv, gv, 1) : full_residual(H, xv, gv);
+    return r ? r : allreduce_sum(H, gv, H.npad);
   };
   // ---- setup (timed separately)
   ILS_CU(cudaMemsetAsync(&H.dstat->flag_err, 0, sizeof(int32_t), st));
@@ -583,7 +598,7 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
   std::vector<int64_t> inner_hist;
 
   const bool big = !H.sparse && H.large;   // dense n > 8192: host-looped two-pass SP (large.cu)
-  if (method == 0 && o.stop != ILS_STOP_RR && !H.sparse && o.sp_form != 2 && !big) {
+  if (method == 0 && o.stop != ILS_STOP_RR && !H.sparse && o.sp_form != 2 && !big && !sharded) {
     // whole SP loop in one persistent cooperative launch
     const int stop = (o.stop == ILS_STOP_XREF) ? ILS_STOP_XREF : ILS_STOP_NONE;
     if (max_iter > 0) {
@@ -600,15 +615,19 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
         if ((rc = launch_gemv_rows(H.Bmat, np, np, np, xk, xnew, 1.0, H.lit_vec + np, st))) return rc;
         ILS_CU(cudaEventRecord(H.evk1, st));
         hot_account(H, 0, 8.0 * (double)n * (double)n);
-      } else if (method == 0 && (H.sparse || big)) {   // c_k by row/column passes, x = P c_k (+ x_k)
+      } else if (method == 0 && (H.sparse || big || sharded)) {   // c_k by row/column passes, x = P c_k (+ x_k)
         ILS_CU(cudaEventRecord(H.evk0, st));
         if (H.sparse) {
           if ((rc = sparse_rhs(H, xk, bhat, 0))) return rc;
-        } else if ((rc = dense_rhs_twopass(H, xk, bhat, o.sp_form == 1))) {
+        } else if (big) {
+          if ((rc = dense_rhs_twopass(H, xk, bhat, o.sp_form == 1))) return rc;
+        } else if ((rc = sp_run(H, xk, nullptr, 0.0, 1, ILS_STOP_NONE, nullptr, o.sp_form, nullptr, true, bhat,
+                                nullptr, nullptr, nullptr))) {
           return rc;
         }
+        if ((rc = allreduce_sum(H, bhat, np))) return rc;   // sharded: sum of the ranks' partial c_k / g_k
         if ((rc = gemv_p(H, bhat, xnew))) return rc;
-        if (big && o.sp_form == 1 && (rc = vec_add(H, xnew, xk, n))) return rc;
+        if ((big || sharded) && o.sp_form == 1 && (rc = vec_add(H, xnew, xk, n))) return rc;
         ILS_CU(cudaEventRecord(H.evk1, st));
         if (H.sparse)
           hot_account(H, 0, 12.0 * (double)(H.nnz - H.nnz1) + 16.0 * (double)H.q + 8.0 * (double)np * (double)np, 2);
@@ -632,6 +651,7 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
                                 nullptr, nullptr))) {
           return rc;
         }
+        if ((rc = allreduce_sum(H, bhat, np))) return rc;   // sharded SP-SCD: global b_hat
         if (method == 1)
           rc = H.sparse ? sparse_rk_inner(H, bhat, xnew, o.seed, k, o.max_inner, o.check_every, o.inner_tol, &steps)
                         : rk_rgs_inner(H, bhat, xnew, o.seed, k, o.max_inner, o.check_every, o.inner_tol, &steps);
@@ -727,6 +747,10 @@ int ils_direct_solve(ils_handle h, double* x) {
   if (!h || !x) return ILS_ERR_ARG;
   Handle& H = *h;
   if (H.batch > 1) return ILS_ERR_UNSUPPORTED;
+  if (H.comm) {
+    set_error("ils_direct_solve: not supported on a row-sharded handle");
+    return ILS_ERR_UNSUPPORTED;
+  }
   const cudaStream_t st = H.stream;
   const int64_t np = H.npad, n = H.n;
   int rc = build_gram(H);
@@ -792,7 +816,10 @@ int ils_relative_residual(ils_handle h, const double* x, double* rr) {
   if (rc) return rc;
   double* xz = H.vec + 4 * np;
   double* g = H.vec + 5 * np;
-  auto fres = [&](const double* xv, double* gv) { return H.sparse ? sparse_rhs(H, xv, gv, 1) : full_residual(H, xv, gv); };
+  auto fres = [&](const double* xv, double* gv) {
+    const int r = H.sparse ? sparse_rhs(H, xv, gv, 1) : full_residual(H, xv, gv);
+    return r ? r : allreduce_sum(H, gv, H.npad);   // sharded: sum over ranks
+  };
   ILS_CU(cudaMemsetAsync(xz, 0, np * sizeof(double), st));
   if ((rc = fres(xz, g))) return rc;
   double den = 0.0, num = 0.0;

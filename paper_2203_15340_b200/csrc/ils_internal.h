@@ -24,6 +24,11 @@ struct DevStatus {
   int32_t pad_;
 };
 
+struct ils_comm_impl {
+  void* nccl = nullptr;   // ncclComm_t
+  int nranks = 1, rank = 0;
+};
+
 struct Handle {
   int64_t p = 0, q = 0, n = 0, m = 0, batch = 1;
   int64_t npad = 0, ppad = 0;
@@ -61,6 +66,7 @@ struct Handle {
   double* rk_state = nullptr;  // SP-RK-RGS chunk state: w, r, az [ppad] each, z [npad]
   void* scd_ws = nullptr;      // SP-SCD chunk state r, beta, r_tmp [npad], reductions, membership masks
   size_t scd_ws_bytes = 0;
+  ils_comm_impl* comm = nullptr;   // row-sharded handle (comm.cu): row sums are all-reduced
   bool large = false;          // dense n > 8192 (or ILS_FORCE_LARGE=1): two-pass SP RHS/check, global-z RK, smem-r SCD
   bool rk_single_step = false; // ILS_RK_SINGLE_STEP env: force the one-step-per-reduction RK-RGS kernel
   double* red = nullptr;    // reduction scratch [grid * 4]
@@ -182,6 +188,9 @@ int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed,
 int scd_masks(Handle& h, uint64_t seed, int64_t k, int64_t t0, int64_t t1, int alpha_mode, int alpha_k, int NT, int V,
               uint32_t* masks);
 
+// comm.cu (row-sharded handles): in-place sum over ranks on h.stream (no-op when unsharded)
+int allreduce_sum(Handle& h, double* buf, int64_t count);
+
 // large.cu (dense n > 8192)
 int dense_rhs_twopass(Handle& h, const double* x, double* c, int full);
 int rk_check_twopass(Handle& h, const double* z, const double* bhat, const double* w, double* r, double* az,
@@ -193,3 +202,7 @@ int batched_solve(Handle& h, int method, const double* x0, double* x, double tol
                   const ils_opts& o, int64_t* inst_iters_dev, int32_t* inst_status_dev);
 
 }  // namespace ils
+
+// the public opaque communicator type (include/ils.h) is the internal one
+struct ils_comm_s : public ils::ils_comm_impl {};
+

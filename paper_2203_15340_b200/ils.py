@@ -25,12 +25,13 @@ EXPORTED = [
     "ils_default_opts", "ils_status_string", "ils_last_error", "ils_create", "ils_sp_solve",
     "ils_rk_solve", "ils_rgs_solve", "ils_destroy", "ils_direct_solve", "ils_relative_residual",
     "ils_get_sampling_tables", "ils_rk_indices", "ils_scd_subset", "ils_kernel_launch_count",
+    "ils_comm_unique_id", "ils_comm_create", "ils_comm_destroy",
 ]
 
 
 class IlsExt(C.Structure):
     _fields_ = [("format", C.c_int32), ("batch", C.c_int64), ("lda", C.c_int64), ("stream", C.c_void_p),
-                ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("nnz", C.c_int64)]
+                ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("nnz", C.c_int64), ("comm", C.c_void_p)]
 
 
 class IlsOpts(C.Structure):
@@ -85,6 +86,9 @@ def load_library(path: str = LIB_PATH):
         "ils_rk_indices": (C.c_int, [vp, u64, i64, i64, i64, vp, vp]),
         "ils_scd_subset": (C.c_int, [i64, u64, i64, i64, i32, i32, vp, vp]),
         "ils_kernel_launch_count": (C.c_int64, []),
+        "ils_comm_unique_id": (C.c_int, [vp]),
+        "ils_comm_create": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(vp)]),
+        "ils_comm_destroy": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -133,16 +137,17 @@ def ils_default_opts(**kw) -> IlsOpts:
 
 
 def ils_create(A, b, p: int, q: int, n: int, batch: int = 1, lda: int = 0, stream=None, row_ptr=None,
-               col_idx=None):
+               col_idx=None, comm=None):
     """ils_create(A, b, p, q, n, ext): A row-major (m x n) or [batch][m][n] fp64, b (m) or [batch][m].
-    CSR input: A = values [nnz], row_ptr int64 [m+1], col_idx int32 [nnz] (ILS_FORMAT_CSR)."""
+    CSR input: A = values [nnz], row_ptr int64 [m+1], col_idx int32 [nnz] (ILS_FORMAT_CSR).
+    comm (ils_comm_create): A, b are this rank's row block, p, q its local row counts."""
     lib = load_library()
     h = C.c_void_p()
     if row_ptr is not None:
         nnz = int(A.numel() if hasattr(A, "numel") else A.size)
-        ext = IlsExt(ILS_FORMAT_CSR, 1, 0, stream, _ptr(row_ptr), _ptr(col_idx), nnz)
+        ext = IlsExt(ILS_FORMAT_CSR, 1, 0, stream, _ptr(row_ptr), _ptr(col_idx), nnz, comm)
     else:
-        ext = IlsExt(ILS_FORMAT_DENSE, batch, lda, stream, None, None, 0)
+        ext = IlsExt(ILS_FORMAT_DENSE, batch, lda, stream, None, None, 0, comm)
     _check(lib.ils_create(C.byref(h), _ptr(A), _ptr(b), p, q, n, C.byref(ext)), "ils_create")
     return h
 
@@ -206,3 +211,51 @@ def ils_scd_subset(n: int, seed: int, k: int, t: int, alpha_mode: int = 0, alpha
 
 def ils_kernel_launch_count() -> int:
     return int(load_library().ils_kernel_launch_count())
+
+
+# ---- row sharding (include/ils.h "Row-sharded handles")
+ILS_COMM_ID_BYTES = 128
+
+
+def ils_comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(ILS_COMM_ID_BYTES)
+    _check(load_library().ils_comm_unique_id(buf), "ils_comm_unique_id")
+    return buf.raw
+
+
+def ils_comm_create(uid: bytes, nranks: int, rank: int):
+    if len(uid) != ILS_COMM_ID_BYTES:
+        raise ValueError("communicator id must be ILS_COMM_ID_BYTES bytes")
+    c = C.c_void_p()
+    buf = C.create_string_buffer(uid, ILS_COMM_ID_BYTES)
+    _check(load_library().ils_comm_create(buf, nranks, rank, C.byref(c)), "ils_comm_create")
+    return c
+
+
+def ils_comm_destroy(c):
+    load_library().ils_comm_destroy(c)
+
+
+def shard_rows(p: int, q: int, world: int, rank: int):
+    """Contiguous row blocks of A1 and A2 for `rank` of `world`: ((p0, p1), (q0, q1)), the first
+    p % world (q % world) ranks taking one extra row. Every rank gets >= 1 row of A1 (needs
+    p >= world); the blocks tile [0, p) and [0, q) exactly."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world / rank")
+    if p < world:
+        raise ValueError("row sharding needs at least one A1 row per rank")
+
+    def block(total):
+        base, extra = divmod(total, world)
+        lo = rank * base + min(rank, extra)
+        return lo, lo + base + (1 if rank < extra else 0)
+
+    return block(p), block(q)
+
+
+def make_comm(rank: int, world: int, broadcast_object):
+    """Create this rank's communicator: rank 0 draws the NCCL id, `broadcast_object(obj) -> obj`
+    (e.g. a torch.distributed.broadcast_object_list wrapper) hands it to every rank."""
+    uid = ils_comm_unique_id() if rank == 0 else None
+    uid = broadcast_object(uid)
+    return ils_comm_create(uid, world, rank)
