@@ -429,7 +429,7 @@ int build_inverse(Handle& h) {
   ILS_CU(cudaMemcpyAsync(h.L, h.G, bytes, cudaMemcpyDeviceToDevice, h.stream));
   r = cholesky_inverse(h, h.L, h.Z, np);
   if (r) return r;
-  if (h.sparse && np >= 8192) {
+  if ((h.sparse || h.large) && np >= 8192) {
     // large n: apply P = Z^T Z as two triangular GEMVs (Z and its transpose, each half read per
     // step: the same 8n^2 bytes as a P GEMV) instead of paying the n^3 GEMM for P; P holds Z^T
     dim3 grid((unsigned)(np / 32), (unsigned)(np / 32));

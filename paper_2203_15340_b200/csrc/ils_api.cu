@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -135,6 +136,29 @@ static int dot_host(Handle& h, const double* a, const double* b, int64_t n, doub
   return ILS_OK;
 }
 
+// Pinned host status blocks are recycled across handles: cudaMallocHost / cudaFreeHost cost
+// milliseconds (and cudaFreeHost synchronises the device), measured at ~1-3 ms per ils_create.
+static std::mutex g_pin_mu;
+static std::vector<DevStatus*> g_pin_free;
+static DevStatus* pinned_status_get() {
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (!g_pin_free.empty()) {
+      DevStatus* s = g_pin_free.back();
+      g_pin_free.pop_back();
+      return s;
+    }
+  }
+  void* p = nullptr;
+  if (cudaMallocHost(&p, sizeof(DevStatus)) != cudaSuccess) return nullptr;
+  return static_cast<DevStatus*>(p);
+}
+static void pinned_status_put(DevStatus* s) {
+  if (!s) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.push_back(s);
+}
+
 static void free_handle_impl(Handle* h) {
   if (!h) return;
   cudaStream_t s = h->stream;
@@ -152,7 +176,7 @@ static void free_handle_impl(Handle* h) {
   }
   if (h->dstat) cudaFreeAsync(h->dstat, s);
   cudaStreamSynchronize(s);
-  if (h->hstat) cudaFreeHost(h->hstat);
+  pinned_status_put(h->hstat);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->evk0) cudaEventDestroy(h->evk0);
@@ -280,7 +304,11 @@ int ils_create(ils_handle* out, const double* A, const double* b, int64_t p, int
   const cudaStream_t st = h->stream;
   CKC(cudaMallocAsync(&h->dstat, sizeof(DevStatus), st));
   CKC(cudaMemsetAsync(h->dstat, 0, sizeof(DevStatus), st));
-  CKC(cudaMallocHost(&h->hstat, sizeof(DevStatus)));
+  h->hstat = pinned_status_get();
+  if (!h->hstat) {
+    set_error("ils_create: pinned host allocation failed");
+    return fail(ILS_ERR_NOMEM);
+  }
   CKC(cudaEventCreate(&h->ev0));
   CKC(cudaEventCreate(&h->ev1));
   CKC(cudaEventCreate(&h->evk0));
@@ -378,21 +406,22 @@ int ils_create(ils_handle* out, const double* A, const double* b, int64_t p, int
     return ILS_OK;
   }
   CKC(cudaMallocAsync(&h->Arm, (size_t)(m + 64) * np * sizeof(double), st));
-  CKC(cudaMemsetAsync(h->Arm, 0, (size_t)(m + 64) * np * sizeof(double), st));
-  CKC(cudaMemcpy2DAsync(h->Arm, np * sizeof(double), A, lda * sizeof(double), n * sizeof(double), m,
-                        cudaMemcpyDefault, st));
   CKC(cudaMallocAsync(&h->b, (size_t)(m + 64) * sizeof(double), st));
   CKC(cudaMemsetAsync(h->b, 0, (size_t)(m + 64) * sizeof(double), st));
   CKC(cudaMemcpyAsync(h->b, b, m * sizeof(double), cudaMemcpyDefault, st));
-  CK(check_finite(*h, h->Arm, m, n, np, &ok));
-  if (ok) CK(check_finite(*h, h->b, 1, m, m, &ok));
-  if (!ok) {
-    set_error("ils_create: non-finite entry in A or b");
-    return fail(ILS_ERR_ARG);
-  }
   CKC(cudaMallocAsync(&h->A1T, (size_t)np * h->ppad * sizeof(double), st));
-  CKC(cudaMemsetAsync(h->A1T, 0, (size_t)np * h->ppad * sizeof(double), st));
-  CK(launch_transpose_a1(*h));
+  CKC(cudaMemsetAsync(&h->dstat->flag_nonfinite, 0, sizeof(int32_t), st));
+  // one fused pass: Arm (padded), A1T, finite check (ingest.cu). Host A is uploaded into Arm
+  // first and then processed in place.
+  const double* Asrc = A;
+  int64_t lsrc = lda;
+  if (!is_device_ptr(A)) {
+    CKC(cudaMemcpy2DAsync(h->Arm, np * sizeof(double), A, lda * sizeof(double), n * sizeof(double), m,
+                          cudaMemcpyHostToDevice, st));
+    Asrc = h->Arm;
+    lsrc = np;
+  }
+  CK(launch_ingest_dense(*h, Asrc, lsrc, h->b, &h->dstat->flag_nonfinite));
   CKC(cudaMallocAsync(&h->N, (size_t)n * sizeof(double), st));
   CKC(cudaMallocAsync(&h->S, (size_t)n * sizeof(uint64_t), st));
   CK(launch_colnorms(*h));
@@ -406,10 +435,13 @@ int ils_create(ils_handle* out, const double* A, const double* b, int64_t p, int
   CKC(cudaMallocAsync(&h->red, (size_t)h->part_rows * 4 * sizeof(double), st));
   CKC(cudaMallocAsync(&h->vec, (size_t)8 * np * sizeof(double), st));
   CKC(cudaMemsetAsync(h->vec, 0, (size_t)8 * np * sizeof(double), st));
-  int32_t zf = 0;
-  CKC(cudaMemcpyAsync(&zf, &h->dstat->flag_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CKC(cudaMemcpyAsync(h->hstat, h->dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
   CKC(cudaStreamSynchronize(st));
-  if (zf) {
+  if (h->hstat->flag_nonfinite) {
+    set_error("ils_create: non-finite entry in A or b");
+    return fail(ILS_ERR_ARG);
+  }
+  if (h->hstat->flag_err) {
     set_error("ils_create: A1 has a zero column");
     return fail(ILS_ERR_ZERO_COLUMN);
   }

@@ -21,7 +21,7 @@ struct DevStatus {
   double metric;           // last stop metric
   int64_t inner_steps;     // inner steps of the last inner solve
   int32_t inner_conv;      // inner solve met its tolerance
-  int32_t pad_;
+  int32_t flag_nonfinite;  // ingest: a non-finite entry in A or b
 };
 
 struct ils_comm_impl {
@@ -130,6 +130,7 @@ int64_t launches_now();
 // ---- launchers (each returns ILS_OK or a negative status) ----
 // ingest.cu
 int launch_transpose_a1(Handle& h);
+int launch_ingest_dense(Handle& h, const double* A, int64_t lda, const double* b, int32_t* flag);
 int launch_colnorms(Handle& h);
 int launch_weights(Handle& h, int32_t* d_zero_flag);
 int launch_gemv_rows(const double* X, int64_t ldx, int64_t rows, int64_t cols, const double* v,

@@ -25,6 +25,47 @@ __global__ void transpose_a1_kernel(const double* __restrict__ Arm, int64_t npad
   }
 }
 
+// Fused dense ingest (one pass over A): 32x32 tiles of the padded [A1; A2] region; each tile is
+// read once from the caller's A (or in place from Arm after a host upload), written row-major
+// into Arm with zero padding (rows >= m, columns >= n), written transposed into A1T for rows < p
+// (zeros for p <= row < ppad), and checked for non-finite values (flag). b is checked by the same
+// grid. Replaces a memset + 2D copy + finite scan + transpose (4 passes) by one.
+__global__ void ingest_dense_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ b,
+                                    int64_t m, int64_t n, int64_t p, int64_t rows_pad, int64_t npad, int64_t ppad,
+                                    double* Arm, double* __restrict__ A1T, int32_t* flag) {
+  __shared__ double tile[32][33];
+  const int64_t j0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
+  bool bad = false;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t i = i0 + r, j = j0 + threadIdx.x;
+    double v = 0.0;
+    if (i < m && j < n) {
+      v = A[i * lda + j];
+      bad |= !isfinite(v);
+    }
+    tile[r][threadIdx.x] = (i < p) ? v : 0.0;
+    if (i < rows_pad) Arm[i * npad + j] = v;
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0)
+    for (int64_t k = threadIdx.y * 32 + threadIdx.x; k < m; k += 256) bad |= !isfinite(b[k]);
+  if (bad) atomicExch(flag, 1);
+  if (i0 >= ppad) return;
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t j = j0 + r, i = i0 + threadIdx.x;
+    if (i < ppad) A1T[j * ppad + i] = tile[threadIdx.x][r];
+  }
+}
+
+int launch_ingest_dense(Handle& h, const double* A, int64_t lda, const double* b, int32_t* flag) {
+  const int64_t rows_pad = h.m + 64;
+  dim3 grid((unsigned)(h.npad / 32), (unsigned)((rows_pad + 31) / 32));
+  ingest_dense_kernel<<<grid, dim3(32, 8), 0, h.stream>>>(A, lda, b, h.m, h.n, h.p, rows_pad, h.npad, h.ppad,
+                                                          h.Arm, h.A1T, flag);
+  ILS_LAUNCHED("ingest_dense_kernel");
+  return ILS_OK;
+}
+
 int launch_transpose_a1(Handle& h) {
   dim3 grid((unsigned)(h.npad / 32), (unsigned)((h.ppad + 31) / 32));
   transpose_a1_kernel<<<grid, dim3(32, 8), 0, h.stream>>>(h.Arm, h.npad, h.p, h.A1T, h.ppad);

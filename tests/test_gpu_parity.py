@@ -115,6 +115,55 @@ def test_not_spd_and_argument_errors():
     assert e.value.status == ils.ILS_ERR_SHAPE
 
 
+@pytest.mark.parametrize("where", ["A1", "A2", "lastcol", "b1", "b2"])
+@pytest.mark.parametrize("dev", [False, True])
+def test_nonfinite_input_rejected(where, dev):
+    """The fused ingest pass (ingest_dense_kernel) flags NaN / Inf anywhere in A or b, host or
+    device input."""
+    pr = make_dense(70, 20, 33, 0.3, seed=21)
+    A, b = pr.A.copy(), pr.b.copy()
+    if where == "A1":
+        A[3, 5] = np.inf
+    elif where == "A2":
+        A[75, 0] = np.nan
+    elif where == "lastcol":
+        A[89, 32] = -np.inf
+    elif where == "b1":
+        b[0] = np.nan
+    else:
+        b[89] = np.inf
+    if dev:
+        A, b = torch.from_numpy(A).to(DEV), torch.from_numpy(b).to(DEV)
+    with pytest.raises(ils.IlsError) as e:
+        ils.ils_create(A, b, 70, 20, 33)
+    assert e.value.status == ils.ILS_ERR_ARG
+
+
+@pytest.mark.parametrize("dev", [False, True])
+def test_strided_input_matches_contiguous(dev):
+    """lda > n (row stride) through the fused ingest: identical tables and SP iterates."""
+    pr = make_dense(130, 37, 67, 0.3, seed=22)
+    lda = 80
+    As = np.zeros((pr.m, lda))
+    As[:, :pr.n] = pr.A
+    As[:, pr.n:] = np.nan   # never read
+    Ain, bin_ = (torch.from_numpy(As).to(DEV), torch.from_numpy(pr.b).to(DEV)) if dev else (As, pr.b)
+    h1 = ils.ils_create(Ain, bin_, pr.p, pr.q, pr.n, lda=lda)
+    h2 = ils.ils_create(pr.A, pr.b, pr.p, pr.q, pr.n)
+    try:
+        N1, S1 = ils.ils_get_sampling_tables(h1, pr.n)
+        N2, S2 = ils.ils_get_sampling_tables(h2, pr.n)
+        assert np.array_equal(N1, N2) and np.array_equal(S1, S2)
+        x1, x2 = np.zeros(pr.n), np.zeros(pr.n)
+        o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE)
+        ils.ils_sp_solve(h1, None, x1, 0.0, 5, o)
+        ils.ils_sp_solve(h2, None, x2, 0.0, 5, o)
+        assert np.array_equal(x1, x2)
+    finally:
+        ils.ils_destroy(h1)
+        ils.ils_destroy(h2)
+
+
 # ------------------------------------------------------------------ SP (Alg. 1)
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("form", [0, 1])
