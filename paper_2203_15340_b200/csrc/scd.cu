@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(32, 1) scd_warp_kernel(ScdParams p) {
     const double* grow = p.G + (int64_t)j * p.npad + lane;
     double g[V];
 #pragma unroll
-    for (int v = 0; v < V; ++v) g[v] = (lane + 32 * v < n) ? __ldcg(grow + 32 * v) : 0.0;
+    for (int v = 0; v < V; ++v) g[v] = (lane + 32 * v < n) ? __ldg(grow + 32 * v) : 0.0;
     if (lane == (j & 31)) bs[j] += sc;
 #pragma unroll
     for (int v = 0; v < V; ++v) r[v] = fma(-sc, g[v], r[v]);
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(SCD_MAXT, 1) scd_chunk_kernel(ScdParams p) {
     for (int v = 0; v < V; ++v) {
       const int s = tid + v * NT;
       if (s < n) {
-        r[v] = fma(-sc, __ldcg(grow + s), r[v]);
+        r[v] = fma(-sc, __ldg(grow + s), r[v]);
         if (s == j) beta[v] += sc;
       }
     }
