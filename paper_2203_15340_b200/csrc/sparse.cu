@@ -18,6 +18,8 @@
 
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ils_internal.h"
 
@@ -967,10 +969,217 @@ __global__ void __launch_bounds__(SSCD_T, 1) sparse_scd_kernel(SpScdParams p) {
         rs[c] = fma(-sc, p.gv[e], rs[c]);
       }
     }
-    if (tid == 0) p.Bv[j] += sc;
+    if (tid == 0) atomicAdd(p.Bv + j, sc);   // fire-and-forget (program-ordered per address)
     __syncthreads();
   }
   for (int s = tid; s < n; s += SSCD_T) p.Rv[s] = rs[s];
+}
+
+// ---------------------------------------------------------------------------------------------
+// SP-SCD for dense input with large n (the paper's n = 13000-15000): a 16-CTA cluster of 256
+// threads, V = 4 coordinates of r per thread for n <= 16384 (V = 8 up to 32768), r in registers.
+// Per step: masked local argmax -> warp butterfly -> CTA winner (barrier + warp reduction) -> the
+// CTA winners (r_j^2, j, r_j, N_j) exchanged through DSMEM (destination-uniform st.async with
+// mbarrier complete_tx, as in rk_rgs.cu) -> every CTA reduces the 16 candidates in the same order
+// (ties to the smallest index) -> each thread updates its coordinates from row j of A1bar (HBM /
+// L2, one coalesced pass over the row spread over 16 SMs instead of one).
+constexpr int SCDC_C = 16;
+constexpr int SCDC_T = 256;   // 8 warps per CTA: the per-step reductions are issue-bound, fewer warps win
+
+struct ScdClParams {
+  const double* G;        // A1bar, npad x npad
+  int64_t npad;
+  int n;
+  const double* N;
+  const double* bhat;
+  double* Rv;             // [npad] state r
+  double* Bv;             // [npad] state beta
+  const uint32_t* masks;  // [t1 - t0][SCDC_C * SCDC_T], bit v <=> coordinate g + v * SCDC_C * SCDC_T
+  int all_members;
+  int64_t t0, t1;
+  DevStatus* st;
+};
+
+template <int V>
+__global__ void __cluster_dims__(SCDC_C, 1, 1) __launch_bounds__(SCDC_T, 1) scd_cluster_kernel(ScdClParams p) {
+  constexpr int NTT = SCDC_C * SCDC_T;
+  __shared__ double wv[2][32], wr[2][32], wn[2][32];
+  __shared__ int wi[2][32];
+  __shared__ __align__(16) double recv[2][SCDC_C][4];   // [source CTA] (r_j^2, r_j, j, N_j)
+  __shared__ __align__(8) uint64_t rbar[2];
+  __shared__ double red[32];
+  __shared__ int win_j[2];
+  __shared__ double win_sc[2];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = (int)cluster_ctarank();
+  const int g = rank * SCDC_T + tid;
+  const int n = p.n;
+  if (*(volatile int32_t*)&p.st->inner_conv) return;
+  if (p.t0 == 0) {   // b_hat = 0: beta = 0 after 0 steps (every CTA takes the same decision)
+    double v = 0.0;
+    for (int s = tid; s < n; s += SCDC_T) v = fma(p.bhat[s], p.bhat[s], v);
+    v = warp_sum(v);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double B2 = 0.0;
+    for (int w = 0; w < SCDC_T / 32; ++w) B2 += red[w];
+    if (B2 == 0.0) {
+      if (rank == 0 && tid == 0) {
+        p.st->inner_steps = 0;
+        p.st->inner_conv = 1;
+      }
+      return;
+    }
+  }
+  double r[V], nj[V], beta[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int s = g + v * NTT;
+    r[v] = (s < n) ? p.Rv[s] : 0.0;
+    nj[v] = (s < n) ? p.N[s] : 1.0;
+    beta[v] = (s < n) ? p.Bv[s] : 0.0;
+  }
+  uint32_t allbits = 0;
+#pragma unroll
+  for (int v = 0; v < V; ++v)
+    if (g + v * NTT < n) allbits |= 1u << v;
+  if (tid == 0) {
+    mbar_init(&rbar[0], 1);
+    mbar_init(&rbar[1], 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(&rbar[0], SCDC_C * 32);
+    mbar_arrive_expect_tx(&rbar[1], SCDC_C * 32);
+  }
+  __syncthreads();
+  cluster_sync_all();
+  const uint32_t* mk = p.masks + g;
+  const int64_t L = p.t1 - p.t0;
+  uint32_t q0 = 0, q1 = 0, q2 = 0, q3 = 0;
+  if (!p.all_members) {
+    q0 = (0 < L) ? __ldcg(mk) : 0u;
+    q1 = (1 < L) ? __ldcg(mk + NTT) : 0u;
+    q2 = (2 < L) ? __ldcg(mk + 2 * NTT) : 0u;
+    q3 = (3 < L) ? __ldcg(mk + 3 * NTT) : 0u;
+  }
+  for (int64_t t = p.t0; t < p.t1; ++t) {
+    const int pb = (int)(t & 1);
+    uint32_t inmask = allbits;
+    if (!p.all_members) {
+      inmask = q0;
+      q0 = q1;
+      q1 = q2;
+      q2 = q3;
+      const int64_t ahead = t - p.t0 + 4;
+      q3 = (ahead < L) ? __ldcg(mk + ahead * NTT) : 0u;
+    }
+    double bv = -1.0, br = 0.0, bn = 1.0;
+    int bi = INT_MAX;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const double q = r[v] * r[v];
+      if (((inmask >> v) & 1u) && q > bv) {
+        bv = q;
+        bi = g + v * NTT;
+        br = r[v];
+        bn = nj[v];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      const double orr = __shfl_xor_sync(0xffffffffu, br, o);
+      const double on = __shfl_xor_sync(0xffffffffu, bn, o);
+      if (argmax_better(ov, oi, bv, bi)) {
+        bv = ov;
+        bi = oi;
+        br = orr;
+        bn = on;
+      }
+    }
+    if (lane == 0) {
+      wv[pb][warp] = bv;
+      wi[pb][warp] = bi;
+      wr[pb][warp] = br;
+      wn[pb][warp] = bn;
+    }
+    __syncthreads();
+    if (warp == 0) {   // CTA winner, one message to every CTA, then the cluster winner
+      double cv = (lane < SCDC_T / 32) ? wv[pb][lane] : -1.0;
+      double cr = (lane < SCDC_T / 32) ? wr[pb][lane] : 0.0;
+      double cn = (lane < SCDC_T / 32) ? wn[pb][lane] : 1.0;
+      int ci = (lane < SCDC_T / 32) ? wi[pb][lane] : INT_MAX;
+#pragma unroll
+      for (int o = SCDC_T / 64; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, cv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, ci, o);
+        const double orr = __shfl_xor_sync(0xffffffffu, cr, o);
+        const double on = __shfl_xor_sync(0xffffffffu, cn, o);
+        if (argmax_better(ov, oi, cv, ci)) {
+          cv = ov;
+          ci = oi;
+          cr = orr;
+          cn = on;
+        }
+      }
+      // lane 0 carries (r_j^2, r_j), lane 1 carries (j, N_j): 32 bytes per destination
+      const int ci0 = __shfl_sync(0xffffffffu, ci, 0);   // all lanes shuffle (no divergent shfl)
+      const double cn0 = __shfl_sync(0xffffffffu, cn, 0);
+      const double m0 = (lane == 0) ? cv : (double)ci0;
+      const double m1 = (lane == 0) ? cr : cn0;
+      const uint32_t la = smem_u32(&recv[pb][rank][2 * (lane & 1)]);
+      const uint32_t lb = smem_u32(&rbar[pb]);
+      if (lane < 2)
+#pragma unroll
+        for (int c = 0; c < SCDC_C; ++c) st_async_v2f64(map_shared_rank(la, (uint32_t)c), m0, m1, map_shared_rank(lb, (uint32_t)c));
+      mbar_wait_cluster(&rbar[pb], (uint32_t)((t - p.t0) >> 1) & 1u);
+      // the 16 CTA winners, lane c holds candidate c; fixed butterfly (ties to the smallest index)
+      double xv = (lane < SCDC_C) ? recv[pb][lane][0] : -1.0;
+      double xr = (lane < SCDC_C) ? recv[pb][lane][1] : 0.0;
+      double xn = (lane < SCDC_C) ? recv[pb][lane][3] : 1.0;
+      int xi = (lane < SCDC_C) ? (int)recv[pb][lane][2] : INT_MAX;
+#pragma unroll
+      for (int o = SCDC_C / 2; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, xv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, xi, o);
+        const double orr = __shfl_xor_sync(0xffffffffu, xr, o);
+        const double on = __shfl_xor_sync(0xffffffffu, xn, o);
+        if (argmax_better(ov, oi, xv, xi)) {
+          xv = ov;
+          xi = oi;
+          xr = orr;
+          xn = on;
+        }
+      }
+      __syncwarp();   // warp 0 has read recv[pb]: re-arm it for step t + 2
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&rbar[pb], SCDC_C * 32);
+        win_j[pb] = xi;
+        win_sc[pb] = xr / xn;
+      }
+    }
+    __syncthreads();
+    const int ci = win_j[pb];
+    const double cr = win_sc[pb], cn = 1.0;
+    const int j = ci;
+    const double sc = cr / cn;   // = r_j / N_j (computed once by warp 0)
+    const double* grow = p.G + (int64_t)j * p.npad;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int s = g + v * NTT;
+      if (s < n) r[v] = fma(-sc, __ldg(grow + s), r[v]);
+      if (s == j) beta[v] += sc;   // registers: no dependent global load on the step chain
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int s = g + v * NTT;
+    if (s < n) {
+      p.Rv[s] = r[v];
+      p.Bv[s] = beta[v];
+    }
+  }
+  cluster_sync_all();   // no CTA exits while a peer may still write into its shared memory
 }
 
 __global__ void __launch_bounds__(256) sparse_scd_check_kernel(const double* __restrict__ Gd, int64_t npad,
@@ -1042,8 +1251,13 @@ int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed,
     return ILS_ERR_UNSUPPORTED;
   }
   const int64_t chunk_cap = (max_inner < ce) ? max_inner : ce;
+  // dense A1bar rows (large n): the 16-CTA cluster kernel (one or two coordinates per thread)
+  const char* ecl = getenv("ILS_SCD_CLUSTER");
+  const bool cl = !h.sparse && h.n <= 8 * SCDC_C * SCDC_T && !(ecl && ecl[0] == '0');
+  const int Vc = (h.n <= 4 * SCDC_C * SCDC_T) ? 4 : 8;
+  const int mask_threads = cl ? SCDC_C * SCDC_T : SSCD_T;
   const size_t need = ((size_t)3 * h.npad + 2 * (size_t)h.num_sms) * sizeof(double) +
-                      (size_t)chunk_cap * SSCD_T * sizeof(uint32_t);
+                      (size_t)chunk_cap * mask_threads * sizeof(uint32_t);
   if (h.scd_ws_bytes < need) {
     if (h.scd_ws) cudaFreeAsync(h.scd_ws, st);
     h.scd_ws = nullptr;
@@ -1090,11 +1304,37 @@ int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed,
   int pending = 0;
   while (t < max_inner) {
     const int64_t t1 = (t + ce < max_inner) ? t + ce : max_inner;
-    if (!prm.all_members && (rc = scd_masks(h, seed, k, t, t1, alpha_mode, alpha_k, SSCD_T, V, masks))) return rc;
+    if (!prm.all_members &&
+        (rc = scd_masks(h, seed, k, t, t1, alpha_mode, alpha_k, mask_threads, cl ? Vc : V, masks)))
+      return rc;
     prm.t0 = t;
     prm.t1 = t1;
-    sparse_scd_kernel<<<1, SSCD_T, smem, st>>>(prm);
-    ILS_LAUNCHED("sparse_scd_kernel");
+    if (cl) {
+      ScdClParams cp{};
+      cp.G = h.G;
+      cp.npad = h.npad;
+      cp.n = (int)h.n;
+      cp.N = h.N;
+      cp.bhat = bhat;
+      cp.Rv = Rv;
+      cp.Bv = Bv;
+      cp.masks = masks;
+      cp.all_members = prm.all_members;
+      cp.t0 = t;
+      cp.t1 = t1;
+      cp.st = h.dstat;
+      if (Vc == 4) {
+        ILS_CU(cudaFuncSetAttribute(scd_cluster_kernel<4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        scd_cluster_kernel<4><<<SCDC_C, SCDC_T, 0, st>>>(cp);
+      } else {
+        ILS_CU(cudaFuncSetAttribute(scd_cluster_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        scd_cluster_kernel<8><<<SCDC_C, SCDC_T, 0, st>>>(cp);
+      }
+      ILS_LAUNCHED("scd_cluster_kernel");
+    } else {
+      sparse_scd_kernel<<<1, SSCD_T, smem, st>>>(prm);
+      ILS_LAUNCHED("sparse_scd_kernel");
+    }
     t = t1;
     if (t % ce == 0) {
       double itol = inner_tol;

@@ -14,3 +14,5 @@ timeout 300 python tools/probe_perf.py --config c1 --methods rk --reps 1 --max-i
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"rk_rgs_block_kernel" -s 2 -c 1 -o gpurun_out/res_prof_c1_rkb python tools/probe_perf.py --config c1 --methods rk --reps 1 --max-iter 1 > gpurun_out/res_ncu_rkb.log 2>&1; echo ncu_rk=$?
 timeout 300 python tools/probe_perf.py --config c1 --methods rgs --reps 1 --max-iter 1 > gpurun_out/res_pr_rgs.log 2>&1 && \
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"scd_chunk_kernel|scd_masks_kernel|scd_check_kernel" -s 3 -c 3 -o gpurun_out/res_prof_c1_scd python tools/probe_perf.py --config c1 --methods rgs --reps 1 --max-iter 1 > gpurun_out/res_ncu_scd.log 2>&1; echo ncu_scd=$?
+timeout 1500 python tools/paper_tables.py --trials 10 --out gpurun_out/res_paper_tables > gpurun_out/res_paper_tables.log 2>&1; echo tables=$?
+timeout 600 python tools/alpha_study.py --config c1 --seeds 3 --out gpurun_out/res_alpha_c1 > gpurun_out/res_alpha.log 2>&1; echo alpha=$?
