@@ -300,7 +300,7 @@ def roofline(steps, peak_hbm, peak_bf16, traffic_map, cfg):
     if c == 3:
         peak = peak_bf16 * FP64_OVER_BF16
         ach = per_launch_work / (per_launch_ms * 1e-3) / 1e12
-        d = {"bound": "tensor", "unit": "TFLOP/s", "peak_note": "fp64 DMMA: measured bf16 burst x 40/2250 (nominal ratio)"}
+        d = {"bound": "tensor", "unit": "TFLOP/s", "peak_note": "fp64 DMMA: measured bf16 burst x 40/2250 (nominal ratio); cuBLAS DGEMM measured 35.4-36.2 TFLOP/s on this pool (tools/mb/dgemm_peak.py)"}
     else:
         peak = peak_hbm
         ach = per_launch_work / (per_launch_ms * 1e-3) / 1e9
