@@ -46,12 +46,15 @@ __device__ __forceinline__ double frag(const double* __restrict__ s, int r, int 
   return MC ? s[k * LDM + r] : s[r * LDK + k];
 }
 
-// grid: (tiles, 1, splits). lower_only: tiles enumerate bm >= bn. tri_k: K starts at max(bm,bn)*64.
+// grid: (tiles, 1, splits). lower_only: tiles enumerate bm >= bn. kmode restricts each tile's K
+// range to where a triangular operand is non-zero (64-aligned blocks): 1 K >= max(row0, col0)
+// (Z^T Z), 2 K < col0 + BN (B lower, C = A B^T), 3 K >= col0 (B lower, C = A B),
+// 4 K < row0 + BM (A lower, C = A B).
 template <bool AMC, bool BNC>
 __global__ void __launch_bounds__(GEMM_THREADS) gemm_dmma_kernel(
     int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
     const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
-    int lower_only, int tri_k, int splits, double* __restrict__ ws) {
+    int lower_only, int kmode, int splits, double* __restrict__ ws) {
   extern __shared__ __align__(128) double smem[];
   const int64_t nt = N / BN;
   int64_t bm, bn;
@@ -66,13 +69,17 @@ __global__ void __launch_bounds__(GEMM_THREADS) gemm_dmma_kernel(
     bn = t % nt;
   }
   const int64_t row0 = bm * BM, col0 = bn * BN;
-  int64_t kbeg = tri_k ? (row0 > col0 ? row0 : col0) : 0;
-  const int64_t klen = K - kbeg;
+  int64_t kbeg = 0, kend = K;
+  if (kmode == 1) kbeg = row0 > col0 ? row0 : col0;
+  else if (kmode == 2) kend = (col0 + BN < K) ? col0 + BN : K;
+  else if (kmode == 3) kbeg = col0;
+  else if (kmode == 4) kend = (row0 + BM < K) ? row0 + BM : K;
+  const int64_t klen = kend > kbeg ? kend - kbeg : 0;
   int64_t kc = (klen + splits - 1) / splits;
   kc = (kc + BK - 1) / BK * BK;
   const int64_t z = blockIdx.z;
   const int64_t ks = kbeg + z * kc;
-  const int64_t ke = (ks + kc < K) ? ks + kc : K;
+  const int64_t ke = (ks + kc < kend) ? ks + kc : kend;
   const int nk = ke > ks ? (int)((ke - ks) / BK) : 0;
 
   double* sA = smem;
@@ -179,7 +186,7 @@ static int ensure_ws(Handle& h, size_t bytes) {
 template <bool AMC, bool BNC>
 static int gemm_launch(Handle& h, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
                        int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
-                       bool lower_only, bool tri_k, int splits, bool force_ws) {
+                       bool lower_only, int kmode, int splits, bool force_ws) {
   static bool attr_set = false;
   if (!attr_set) {
     ILS_CU(cudaFuncSetAttribute(gemm_dmma_kernel<AMC, BNC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -197,7 +204,7 @@ static int gemm_launch(Handle& h, int64_t M, int64_t N, int64_t K, double alpha,
   }
   dim3 grid((unsigned)tiles, 1, (unsigned)splits);
   gemm_dmma_kernel<AMC, BNC><<<grid, GEMM_THREADS, GEMM_SMEM, h.stream>>>(
-      M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower_only ? 1 : 0, tri_k ? 1 : 0, splits, ws);
+      M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower_only ? 1 : 0, kmode, splits, ws);
   ILS_LAUNCHED("gemm_dmma_kernel");
   if (ws) {
     const int64_t total = M * N;
@@ -213,15 +220,15 @@ int gemm_dmma(Handle& h, bool a_mc, bool b_nc, int64_t M, int64_t N, int64_t K, 
               const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
               int64_t ldc, bool lower_only, int splits) {
   if (a_mc && b_nc)
-    return gemm_launch<true, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower_only, false,
+    return gemm_launch<true, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower_only, 0,
                                    splits, false);
   if (a_mc)
-    return gemm_launch<true, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower_only, false,
+    return gemm_launch<true, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower_only, 0,
                                     splits, false);
   if (b_nc)
-    return gemm_launch<false, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower_only, false,
+    return gemm_launch<false, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower_only, 0,
                                     splits, false);
-  return gemm_launch<false, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower_only, false,
+  return gemm_launch<false, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower_only, 0,
                                    splits, false);
 }
 
@@ -362,24 +369,24 @@ static int chol_rec(Handle& h, double* L, double* Z, int64_t ld, int64_t s, int6
   if (r) return r;
   // L21 = A21 Z11^T  (tmp, then copy back: in-place operands)
   const int sp1 = pick_splits(h, (n2 / 64) * (n1 / 64), n1);
-  r = gemm_launch<false, false>(h, n2, n1, n1, 1.0, L21, ld, Z11, ld, 0.0, tmp, n1, false, false, sp1,
+  r = gemm_launch<false, false>(h, n2, n1, n1, 1.0, L21, ld, Z11, ld, 0.0, tmp, n1, false, 2, sp1,
                                 sp1 > 1);
   if (r) return r;
   ILS_CU(cudaMemcpy2DAsync(L21, ld * sizeof(double), tmp, n1 * sizeof(double), n1 * sizeof(double), n2,
                            cudaMemcpyDeviceToDevice, h.stream));
   // A22 -= L21 L21^T (lower tiles)
   const int sp2 = pick_splits(h, (n2 / 64) * (n2 / 64 + 1) / 2, n1);
-  r = gemm_launch<false, false>(h, n2, n2, n1, -1.0, L21, ld, L21, ld, 1.0, L22, ld, true, false, sp2,
+  r = gemm_launch<false, false>(h, n2, n2, n1, -1.0, L21, ld, L21, ld, 1.0, L22, ld, true, 0, sp2,
                                 false);
   if (r) return r;
   r = chol_rec(h, L, Z, ld, hmid, e, tmp);
   if (r) return r;
   // Z21 = -Z22 (L21 Z11): T1 = L21 Z11 -> tmp (opB(j,k) = Z11[k][j], N-contiguous)
-  r = gemm_launch<false, true>(h, n2, n1, n1, 1.0, L21, ld, Z11, ld, 0.0, tmp, n1, false, false, sp1,
+  r = gemm_launch<false, true>(h, n2, n1, n1, 1.0, L21, ld, Z11, ld, 0.0, tmp, n1, false, 3, sp1,
                                sp1 > 1);
   if (r) return r;
   const int sp3 = pick_splits(h, (n2 / 64) * (n1 / 64), n2);
-  r = gemm_launch<false, true>(h, n2, n1, n2, -1.0, Z22, ld, tmp, n1, 0.0, Z21, ld, false, false, sp3,
+  r = gemm_launch<false, true>(h, n2, n1, n2, -1.0, Z22, ld, tmp, n1, 0.0, Z21, ld, false, 4, sp3,
                                false);
   return r;
 }
@@ -406,7 +413,7 @@ int build_gram(Handle& h) {
   const int64_t tiles = (np / 64) * (np / 64 + 1) / 2;
   const int sp = pick_splits(h, tiles, h.ppad);
   int r = gemm_launch<false, false>(h, np, np, h.ppad, 1.0, h.A1T, h.ppad, h.A1T, h.ppad, 0.0, h.G, np,
-                                    true, false, sp, false);
+                                    true, 0, sp, false);
   if (r) return r;
   // row-sharded handle: sum the ranks' lower triangles before the mirror sets the padded diagonal
   r = allreduce_sum(h, h.G, np * np);
@@ -442,7 +449,7 @@ int build_inverse(Handle& h) {
   // P = Z^T Z: opA(i,k) = Z[k][i] (M-contiguous), opB(j,k) = Z[k][j] (N-contiguous); K from max(i,j)
   const int64_t tiles = (np / 64) * (np / 64 + 1) / 2;
   const int sp = pick_splits(h, tiles, np / 2);
-  r = gemm_launch<true, true>(h, np, np, np, 1.0, h.Z, np, h.Z, np, 0.0, h.P, np, true, true, sp, false);
+  r = gemm_launch<true, true>(h, np, np, np, 1.0, h.Z, np, h.Z, np, 0.0, h.P, np, true, 1, sp, false);
   if (r) return r;
   r = mirror_lower(h, h.P, np, np, np);
   if (r) return r;
@@ -484,7 +491,7 @@ int build_explicit_b(Handle& h) {
   const int64_t np = h.npad;
   if (!h.Bmat) ILS_CU(cudaMallocAsync(&h.Bmat, (size_t)np * np * sizeof(double), h.stream));
   const int sp = pick_splits(h, (np / 64) * (np / 64), np);
-  r = gemm_launch<false, true>(h, np, np, np, 1.0, h.P, np, h.A2bar, np, 0.0, h.Bmat, np, false, false, sp, sp > 1);
+  r = gemm_launch<false, true>(h, np, np, np, 1.0, h.P, np, h.A2bar, np, 0.0, h.Bmat, np, false, 0, sp, sp > 1);
   if (r) return r;
   r = launch_gemv_rows(h.P, np, np, np, h.lit_vec, h.lit_vec + np, 1.0, nullptr, h.stream);
   if (r) return r;
