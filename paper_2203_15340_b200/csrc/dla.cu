@@ -350,7 +350,11 @@ __global__ void __launch_bounds__(256) potf2_trtri_kernel(double* __restrict__ L
 }
 
 // Recursive Cholesky + inverse on blocks [s, e) (units of 64).
-static int chol_rec(Handle& h, double* L, double* Z, int64_t ld, int64_t s, int64_t e, double* tmp) {
+// need_z = false (right spine of a top-level call with full_z = false): the caller never uses this
+// block's inverse as a whole, so Z21 = -Z22 L21 Z11 (two GEMMs) is skipped here; zc_apply_spine
+// applies Z through L21 instead. The left child's full inverse is always needed (L21 = A21 Z11^T).
+static int chol_rec(Handle& h, double* L, double* Z, int64_t ld, int64_t s, int64_t e, double* tmp,
+                    bool need_z) {
   if (e - s == 1) {
     const int smem = 2 * 64 * 65 * (int)sizeof(double);
     ILS_CU(cudaFuncSetAttribute(potf2_trtri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -365,7 +369,7 @@ static int chol_rec(Handle& h, double* L, double* Z, int64_t ld, int64_t s, int6
   double* Z11 = Z + s * 64 * ld + s * 64;
   double* Z21 = Z + hmid * 64 * ld + s * 64;
   double* Z22 = Z + hmid * 64 * ld + hmid * 64;
-  int r = chol_rec(h, L, Z, ld, s, hmid, tmp);
+  int r = chol_rec(h, L, Z, ld, s, hmid, tmp, true);
   if (r) return r;
   // L21 = A21 Z11^T  (tmp, then copy back: in-place operands)
   const int sp1 = pick_splits(h, (n2 / 64) * (n1 / 64), n1);
@@ -379,8 +383,19 @@ static int chol_rec(Handle& h, double* L, double* Z, int64_t ld, int64_t s, int6
   r = gemm_launch<false, false>(h, n2, n2, n1, -1.0, L21, ld, L21, ld, 1.0, L22, ld, true, 0, sp2,
                                 false);
   if (r) return r;
-  r = chol_rec(h, L, Z, ld, hmid, e, tmp);
+  if (!need_z) {
+    if (h.nspine >= 24) {
+      set_error("Cholesky: recursion deeper than the spine table");
+      return ILS_ERR_UNSUPPORTED;
+    }
+    h.spine[3 * h.nspine] = s;
+    h.spine[3 * h.nspine + 1] = hmid;
+    h.spine[3 * h.nspine + 2] = e;
+    ++h.nspine;
+  }
+  r = chol_rec(h, L, Z, ld, hmid, e, tmp, need_z);
   if (r) return r;
+  if (!need_z) return ILS_OK;
   // Z21 = -Z22 (L21 Z11): T1 = L21 Z11 -> tmp (opB(j,k) = Z11[k][j], N-contiguous)
   r = gemm_launch<false, true>(h, n2, n1, n1, 1.0, L21, ld, Z11, ld, 0.0, tmp, n1, false, 3, sp1,
                                sp1 > 1);
@@ -391,13 +406,51 @@ static int chol_rec(Handle& h, double* L, double* Z, int64_t ld, int64_t s, int6
   return r;
 }
 
-int cholesky_inverse(Handle& h, double* L, double* Z, int64_t npad) {
+int cholesky_inverse(Handle& h, double* L, double* Z, int64_t npad, bool full_z) {
   ILS_CU(cudaMemsetAsync(Z, 0, (size_t)npad * npad * sizeof(double), h.stream));
   double* tmp = nullptr;
   ILS_CU(cudaMallocAsync(&tmp, (size_t)npad * npad * sizeof(double), h.stream));
-  int r = chol_rec(h, L, Z, npad, 0, npad / 64, tmp);
+  h.nspine = 0;
+  int r = chol_rec(h, L, Z, npad, 0, npad / 64, tmp, full_z);
   cudaFreeAsync(tmp, h.stream);
   return r;
+}
+
+// x = Z^T (Z c) with Z = L^{-1} held only partly: on every right-spine node (s, mid, e) the
+// blocks Z11 = Z[s:mid, s:mid] (complete) and L21 = L[mid:e, s:mid] are used instead of Z21:
+//   Z c:    y1 = Z11 c1 ; c2 <- c2 - L21 y1 ; recurse on [mid, e)      (Z21 = -Z22 L21 Z11)
+//   Z^T y:  x2 = Z22^T y2 (recursively) ; x1 = Z11^T (y1 - L21^T x2)
+// ending in the last leaf block, whose inverse is complete. Two GEMV launches per node and pass.
+int zc_apply_spine(Handle& h, const double* c, double* x) {
+  const int64_t np = h.npad, B = 64;
+  const cudaStream_t st = h.stream;
+  double* w = h.vec + 2 * np;    // working copy of c (updated in place on the spine)
+  double* y = h.vec + 4 * np;    // Z c
+  double* t = h.vec + 5 * np;    // scratch
+  ILS_CU(cudaMemcpyAsync(w, c, np * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  const double* Z = h.Z;
+  const double* L = h.L;
+  int rc;
+  int64_t tail = 0;
+  for (int k = 0; k < h.nspine; ++k) {
+    const int64_t s = h.spine[3 * k] * B, m = h.spine[3 * k + 1] * B, e = h.spine[3 * k + 2] * B;
+    if ((rc = launch_tri_rows(Z + s * np + s, np, m - s, w + s, y + s, st))) return rc;
+    // w[m:e] = w[m:e] - L21 y1 (into t, then back: no aliasing inside the kernel)
+    if ((rc = launch_gemv_rows(L + m * np + s, np, e - m, m - s, y + s, t + m, -1.0, w + m, st))) return rc;
+    ILS_CU(cudaMemcpyAsync(w + m, t + m, (e - m) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    tail = m;
+  }
+  if ((rc = launch_tri_rows(Z + tail * np + tail, np, np - tail, w + tail, y + tail, st))) return rc;
+  // Z^T y, bottom-up: the tail block first, then every spine node's left block
+  if ((rc = launch_cols(Z + tail * np + tail, np, np - tail, np - tail, y + tail, 1.0, nullptr, x + tail, 1, st)))
+    return rc;
+  for (int k = h.nspine - 1; k >= 0; --k) {
+    const int64_t s = h.spine[3 * k] * B, m = h.spine[3 * k + 1] * B, e = h.spine[3 * k + 2] * B;
+    if ((rc = launch_cols(L + m * np + s, np, e - m, m - s, x + m, -1.0, y + s, t + s, 0, st))) return rc;
+    if ((rc = launch_cols(Z + s * np + s, np, m - s, m - s, t + s, 1.0, nullptr, x + s, 1, st))) return rc;
+  }
+  if (h.n < np) ILS_CU(cudaMemsetAsync(x + h.n, 0, (np - h.n) * sizeof(double), st));
+  return ILS_OK;
 }
 
 int build_gram(Handle& h) {
@@ -432,20 +485,19 @@ int build_inverse(Handle& h) {
   const size_t bytes = (size_t)np * np * sizeof(double);
   if (!h.L) ILS_CU(cudaMallocAsync(&h.L, bytes, h.stream));
   if (!h.Z) ILS_CU(cudaMallocAsync(&h.Z, bytes, h.stream));
-  if (!h.P) ILS_CU(cudaMallocAsync(&h.P, bytes, h.stream));
   ILS_CU(cudaMemcpyAsync(h.L, h.G, bytes, cudaMemcpyDeviceToDevice, h.stream));
-  r = cholesky_inverse(h, h.L, h.Z, np);
-  if (r) return r;
   if ((h.sparse || h.large) && np >= 8192) {
-    // large n: apply P = Z^T Z as two triangular GEMVs (Z and its transpose, each half read per
-    // step: the same 8n^2 bytes as a P GEMV) instead of paying the n^3 GEMM for P; P holds Z^T
-    dim3 grid((unsigned)(np / 32), (unsigned)(np / 32));
-    transpose_kernel<<<grid, dim3(32, 8), 0, h.stream>>>(h.Z, h.P, np);
-    ILS_LAUNCHED("transpose_kernel");
+    // large n (few outer steps, setup-dominated): no n^3 GEMM for P and no inverse blocks on the
+    // recursion's right spine; x = Z^T (Z c) is applied through the spine (zc_apply_spine)
+    r = cholesky_inverse(h, h.L, h.Z, np, false);
+    if (r) return r;
     h.use_zt = true;
     h.have_P = true;
     return ILS_OK;
   }
+  if (!h.P) ILS_CU(cudaMallocAsync(&h.P, bytes, h.stream));
+  r = cholesky_inverse(h, h.L, h.Z, np, true);
+  if (r) return r;
   // P = Z^T Z: opA(i,k) = Z[k][i] (M-contiguous), opB(j,k) = Z[k][j] (N-contiguous); K from max(i,j)
   const int64_t tiles = (np / 64) * (np / 64 + 1) / 2;
   const int sp = pick_splits(h, tiles, np / 2);
@@ -485,6 +537,10 @@ int build_a2bar(Handle& h) {
 // B = P A2bar (DMMA GEMM) and c0 = P A^T J b (Alg. 1 steps 3-4)
 int build_explicit_b(Handle& h) {
   if (h.have_B) return ILS_OK;
+  if ((h.sparse || h.large) && h.npad >= 8192) {
+    set_error("sp_form 2 (explicit B = P A2bar) is not supported for n >= 8192 (P is applied implicitly there)");
+    return ILS_ERR_UNSUPPORTED;
+  }
   int r = build_inverse(h);
   if (!r) r = build_a2bar(h);
   if (r) return r;

@@ -801,7 +801,7 @@ int ils_direct_solve(ils_handle h, double* x) {
     if (!rc) rc = mirror_lower(H, M, np, np, n);
   }
   ILS_CU(cudaMemsetAsync(&H.dstat->flag_err, 0, sizeof(int32_t), st));
-  if (!rc) rc = cholesky_inverse(H, M, Zm, np);
+  if (!rc) rc = cholesky_inverse(H, M, Zm, np, true);
   // rhs = A^T J b = A1^T b1 - A2^T b2 ; x = Z^T (Z rhs)
   double* rhs = H.vec + 4 * np;
   double* y = H.vec + 5 * np;

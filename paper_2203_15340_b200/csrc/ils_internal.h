@@ -50,7 +50,10 @@ struct Handle {
   double* Z = nullptr;      // npad x npad  L^{-1} (lower, zero upper)
   double* P = nullptr;      // npad x npad  (A1^T A1)^{-1}
   bool have_gram = false, have_P = false;
-  bool use_zt = false;      // P applied as Z^T (Z c): P buffer holds Z^T (large sparse n)
+  bool use_zt = false;      // P applied as Z^T (Z c) (n >= 8192): Z built without the off-diagonal
+                            // blocks of the recursion's right spine, applied through L (dla.cu)
+  int nspine = 0;           // right-spine nodes (s, mid, e) in 64-blocks, top-down
+  int64_t spine[3 * 24];
   // paper-literal precompute (sp_form = 2): A2bar = A2^T A2, B = P A2bar, c0 = P A^T J b
   double* A2bar = nullptr;
   double* Bmat = nullptr;
@@ -146,7 +149,7 @@ int gemm_dmma(Handle& h, bool a_mc, bool b_nc, int64_t M, int64_t N, int64_t K, 
               int64_t ldc, bool lower_only, int splits);
 int mirror_lower(Handle& h, double* C, int64_t ld, int64_t n, int64_t n_real);
 // Cholesky of the lower triangle of L (npad x npad) in place, Z = L^{-1}. flag_err set on breakdown.
-int cholesky_inverse(Handle& h, double* L, double* Z, int64_t npad);
+int cholesky_inverse(Handle& h, double* L, double* Z, int64_t npad, bool full_z);
 int build_gram(Handle& h);      // G = A1^T A1
 int build_inverse(Handle& h);   // L, Z, P from G
 int build_a2bar(Handle& h);     // A2bar = A2^T A2 and A^T J b (dense)
@@ -197,6 +200,10 @@ int dense_rhs_twopass(Handle& h, const double* x, double* c, int full);
 int rk_check_twopass(Handle& h, const double* z, const double* bhat, const double* w, double* r, double* az,
                      double inner_tol, int64_t t_now);
 int vec_add(Handle& h, double* x, const double* y, int64_t n);
+int launch_cols(const double* X, int64_t ldx, int64_t rows, int64_t cols, const double* y, double alpha,
+                const double* base, double* c, int tri_lower, cudaStream_t st);
+int launch_tri_rows(const double* T, int64_t ld, int64_t m, const double* c, double* y, cudaStream_t st);
+int zc_apply_spine(Handle& h, const double* c, double* x);
 
 // batched.cu
 int batched_solve(Handle& h, int method, const double* x0, double* x, double tol, int64_t max_iter,

@@ -32,14 +32,14 @@ __global__ void rows_minus_b_kernel(const double* __restrict__ X, int64_t ldx, i
 // (fixed-order combine in shared memory), coalesced row segments
 __global__ void __launch_bounds__(256) cols_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows,
                                                    int64_t cols, const double* __restrict__ y, double alpha,
-                                                   const double* base, double* c) {
+                                                   const double* base, double* c, int tri_lower = 0) {
   __shared__ double part[8][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t j0 = (int64_t)blockIdx.x * 32; j0 < cols; j0 += (int64_t)gridDim.x * 32) {
     const int64_t j = j0 + lane;
     double s = 0.0;
-    if (j < cols)
-      for (int64_t i = warp; i < rows; i += 8) s = fma(X[i * ldx + j], y[i], s);
+    if (j < cols)   // tri_lower: X[i][j] = 0 for i < j, so rows start at the tile's first column
+      for (int64_t i = (tri_lower ? j0 : 0) + warp; i < rows; i += 8) s = fma(X[i * ldx + j], y[i], s);
     part[warp][lane] = s;
     __syncthreads();
     if (warp == 0 && j < cols) {
@@ -48,6 +48,33 @@ __global__ void __launch_bounds__(256) cols_kernel(const double* __restrict__ X,
       c[j] = (base ? base[j] : 0.0) + alpha * t;
     }
     __syncthreads();
+  }
+}
+
+// y = T c for the lower-triangular m x m block T (row stride ld, 16-byte aligned rows); warp per row
+__global__ void __launch_bounds__(256) tri_rows_kernel(const double* __restrict__ T, int64_t ld, int64_t m,
+                                                       const double* __restrict__ c, double* __restrict__ y) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double2* c2 = reinterpret_cast<const double2*>(c);
+  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < m; i += (int64_t)gridDim.x * 8) {
+    const double2* tr = reinterpret_cast<const double2*>(T + i * ld);
+    const int64_t k1 = (i >> 1) + 1;   // double2 entries covering columns 0..i (i + 1 is zero if present)
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int64_t k = lane;
+    for (; k + 32 < k1; k += 64) {
+      const double2 v = __ldcs(tr + k), w = __ldcs(tr + k + 32), a = __ldg(c2 + k), b = __ldg(c2 + k + 32);
+      s0 = fma(v.x, a.x, s0);
+      s1 = fma(v.y, a.y, s1);
+      s2 = fma(w.x, b.x, s2);
+      s3 = fma(w.y, b.y, s3);
+    }
+    if (k < k1) {
+      const double2 v = __ldcs(tr + k), a = __ldg(c2 + k);
+      s0 = fma(v.x, a.x, s0);
+      s1 = fma(v.y, a.y, s1);
+    }
+    const double s = warp_sum((s0 + s1) + (s2 + s3));
+    if (lane == 0) y[i] = s;
   }
 }
 
@@ -142,6 +169,24 @@ int rk_check_twopass(Handle& h, const double* z, const double* bhat, const doubl
 __global__ void add_kernel(double* __restrict__ x, const double* __restrict__ y, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] += y[i];
+}
+
+// c = base + alpha * X^T y over `rows` rows (tri_lower: X lower triangular, zero rows skipped)
+int launch_cols(const double* X, int64_t ldx, int64_t rows, int64_t cols, const double* y, double alpha,
+                const double* base, double* c, int tri_lower, cudaStream_t st) {
+  if (cols <= 0) return ILS_OK;
+  cols_kernel<<<grid_cols(cols), 256, 0, st>>>(X, ldx, rows, cols, y, alpha, base, c, tri_lower);
+  ILS_LAUNCHED("cols_kernel");
+  return ILS_OK;
+}
+
+int launch_tri_rows(const double* T, int64_t ld, int64_t m, const double* c, double* y, cudaStream_t st) {
+  if (m <= 0) return ILS_OK;
+  int64_t g = (m + 7) / 8;
+  if (g > 148 * 8) g = 148 * 8;
+  tri_rows_kernel<<<(unsigned)g, 256, 0, st>>>(T, ld, m, c, y);
+  ILS_LAUNCHED("tri_rows_kernel");
+  return ILS_OK;
 }
 
 // x += y over n entries (the correction form x_{k+1} = x_k + P g_k on the two-pass path)

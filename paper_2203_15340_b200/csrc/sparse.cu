@@ -384,14 +384,7 @@ __global__ void __launch_bounds__(256) tri_gemv_kernel(const double* __restrict_
 }
 
 int gemv_p(Handle& h, const double* c, double* x) {
-  if (h.use_zt) {   // x = Z^T (Z c): the P buffer holds Z^T; the entries outside the triangles are zero
-    double* y = h.vec + 2 * h.npad;
-    tri_gemv_kernel<<<(unsigned)(h.num_sms * 8), 256, 0, h.stream>>>(h.Z, c, h.npad, h.npad, 0, y);
-    ILS_LAUNCHED("tri_gemv_kernel");
-    tri_gemv_kernel<<<(unsigned)(h.num_sms * 8), 256, 0, h.stream>>>(h.P, y, h.npad, h.n, 1, x);
-    ILS_LAUNCHED("tri_gemv_kernel");
-    return ILS_OK;
-  }
+  if (h.use_zt) return zc_apply_spine(h, c, x);   // x = Z^T (Z c) through the recursion's spine (dla.cu)
   gemv_p_kernel<<<(unsigned)(h.num_sms * 8), 256, 0, h.stream>>>(h.P, c, h.npad, h.n, x);
   ILS_LAUNCHED("gemv_p_kernel");
   return ILS_OK;
