@@ -175,12 +175,49 @@ __global__ void __launch_bounds__(256) sparse_gram_kernel(const int64_t* __restr
   for (int64_t k = threadIdx.x; k < npad; k += blockDim.x) gs[k] = accumulate ? grow[k] : 0.0;
   __syncthreads();
   if (threadIdx.x < 32) {
+    // One warp applies the column's entries in their stored order (deterministic sums); the
+    // dependent global loads are batched: lane l fetches entry base + l's row, value and row
+    // extent, then the first 32 entries of G_ROWS consecutive rows are loaded before any of them
+    // is applied (G_ROWS rows in flight instead of one).
+    constexpr int G_ROWS = 8;
     const int lane = threadIdx.x;
-    for (int64_t e = cptr[j]; e < cptr[j + 1]; ++e) {
-      const int64_t i = r0 + crow[e];
-      const double v = alpha * cval[e];
-      for (int64_t f = rp[i] + lane; f < rp[i + 1]; f += 32) gs[ci[f]] = fma(v, va[f], gs[ci[f]]);
-      __syncwarp();
+    const int64_t e0 = cptr[j], e1 = cptr[j + 1];
+    for (int64_t base = e0; base < e1; base += 32) {
+      const int64_t e = base + lane;
+      double v = 0.0;
+      int64_t f0 = 0, f1 = 0;
+      if (e < e1) {
+        const int64_t i = r0 + crow[e];
+        v = alpha * cval[e];
+        f0 = rp[i];
+        f1 = rp[i + 1];
+      }
+      const int cnt = (int)((e1 - base) < 32 ? (e1 - base) : 32);
+      for (int q0 = 0; q0 < cnt; q0 += G_ROWS) {
+        int cc[G_ROWS];
+        double aa[G_ROWS];
+#pragma unroll
+        for (int u = 0; u < G_ROWS; ++u) {
+          const int64_t g0 = __shfl_sync(0xffffffffu, f0, (q0 + u) & 31);
+          const int64_t g1 = __shfl_sync(0xffffffffu, f1, (q0 + u) & 31);
+          const bool ok = (q0 + u < cnt) && (g0 + lane < g1);
+          cc[u] = ok ? ci[g0 + lane] : -1;
+          aa[u] = ok ? va[g0 + lane] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < G_ROWS; ++u) {
+          const double vu = __shfl_sync(0xffffffffu, v, (q0 + u) & 31);
+          if (cc[u] >= 0) gs[cc[u]] = fma(vu, aa[u], gs[cc[u]]);
+          // rows longer than 32 entries: the rest in order (rare on the benchmark data)
+          const int64_t g0 = __shfl_sync(0xffffffffu, f0, (q0 + u) & 31);
+          const int64_t g1 = __shfl_sync(0xffffffffu, f1, (q0 + u) & 31);
+          if (q0 + u < cnt && g1 - g0 > 32) {
+            __syncwarp();
+            for (int64_t f = g0 + 32 + lane; f < g1; f += 32) gs[ci[f]] = fma(vu, va[f], gs[ci[f]]);
+          }
+          __syncwarp();
+        }
+      }
     }
   }
   __syncthreads();
