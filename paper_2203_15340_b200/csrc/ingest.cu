@@ -199,9 +199,16 @@ __global__ void gemv_rows_kernel(const double* __restrict__ X, int64_t ldx, int6
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i < rows; i += nw) {
     const double* xr = X + i * ldx;
-    double s = 0.0;
-    for (int64_t j = lane; j < cols; j += 32) s = fma(xr[j], v[j], s);
-    s = warp_sum(s);
+    double s = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;   // four loads in flight per lane
+    int64_t j = lane;
+    for (; j + 96 < cols; j += 128) {
+      s = fma(xr[j], v[j], s);
+      s1 = fma(xr[j + 32], v[j + 32], s1);
+      s2 = fma(xr[j + 64], v[j + 64], s2);
+      s3 = fma(xr[j + 96], v[j + 96], s3);
+    }
+    for (; j < cols; j += 32) s = fma(xr[j], v[j], s);
+    s = warp_sum((s + s1) + (s2 + s3));
     if (lane == 0) y[i] = alpha * s + (yadd ? yadd[i] : 0.0);
   }
 }

@@ -38,8 +38,18 @@ __global__ void __launch_bounds__(256) cols_kernel(const double* __restrict__ X,
   for (int64_t j0 = (int64_t)blockIdx.x * 32; j0 < cols; j0 += (int64_t)gridDim.x * 32) {
     const int64_t j = j0 + lane;
     double s = 0.0;
-    if (j < cols)   // tri_lower: X[i][j] = 0 for i < j, so rows start at the tile's first column
-      for (int64_t i = (tri_lower ? j0 : 0) + warp; i < rows; i += 8) s = fma(X[i * ldx + j], y[i], s);
+    if (j < cols) {   // tri_lower: X[i][j] = 0 for i < j, so rows start at the tile's first column
+      double s1 = 0.0, s2 = 0.0, s3 = 0.0;   // four rows in flight per warp
+      int64_t i = (tri_lower ? j0 : 0) + warp;
+      for (; i + 24 < rows; i += 32) {
+        s = fma(X[i * ldx + j], y[i], s);
+        s1 = fma(X[(i + 8) * ldx + j], y[i + 8], s1);
+        s2 = fma(X[(i + 16) * ldx + j], y[i + 16], s2);
+        s3 = fma(X[(i + 24) * ldx + j], y[i + 24], s3);
+      }
+      for (; i < rows; i += 8) s = fma(X[i * ldx + j], y[i], s);
+      s = (s + s1) + (s2 + s3);
+    }
     part[warp][lane] = s;
     __syncthreads();
     if (warp == 0 && j < cols) {
