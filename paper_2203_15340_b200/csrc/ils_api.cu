@@ -589,7 +589,9 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
     // algorithmic flops (LAPACK counts): SYRK p n (n+1) (sparse: 2 sum_i nnz_i^2 over A1 rows),
     // Cholesky n^3/3 + triangular inverse n^3/3 (+ P = Z^T Z n^3/3 when formed)
     const double gram = H.sparse ? 2.0 * H.a1_row_sq : pd * nd * (nd + 1.0);
-    H.hot_work[3] += (gram_new ? gram : 0.0) + (inv_new ? (H.use_zt ? 2.0 : 3.0) * nd * nd * nd / 3.0 : 0.0) +
+    // use_zt (n >= 8192): only the Cholesky (n^3 / 3) is counted; the partial inverse formed there
+    // replaces triangular solves and is an implementation choice, not algorithmic work
+    H.hot_work[3] += (gram_new ? gram : 0.0) + (inv_new ? (H.use_zt ? 1.0 : 3.0) * nd * nd * nd / 3.0 : 0.0) +
                      (lit_new ? (double)H.q * nd * (nd + 1.0) + (method == 0 ? 2.0 * nd * nd * nd : 0.0) : 0.0);
     H.hot_n[3] += 1;
   }
