@@ -149,6 +149,10 @@ def test_large_real_n_above_8192(monkeypatch):
             fn(hh.h, None, x, 0.0, K, o)
             for k in range(K):
                 assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, (fn, kw, k)
+        # the explicit B = P A2bar of sp_form 2 is not formed at n >= 8192 (P is applied implicitly)
+        with pytest.raises(ils.IlsError) as e:
+            ils.ils_sp_solve(hh.h, None, np.zeros(n), 0.0, 1, ils.ils_default_opts(stop=ils.ILS_STOP_NONE, sp_form=2))
+        assert e.value.status == ils.ILS_ERR_UNSUPPORTED
 
 
 @pytest.mark.parametrize("shape", [(3000, 200, 200), (2500, 1, 300), (1500, 1, 70)])

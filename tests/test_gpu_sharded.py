@@ -124,3 +124,26 @@ def test_sharded_unsupported_modes_and_shapes(comm):
     with pytest.raises(ils.IlsError) as e:   # without a communicator p < n is a shape error
         ils.ils_create(A, b, 30, pr.q, pr.n)
     assert e.value.status == ils.ILS_ERR_SHAPE
+
+
+def test_sharded_with_large_n_routing(comm, monkeypatch):
+    """Sharded handle on the n > 8192 routing (forced at small n): two-pass right-hand side and the
+    cluster SP-SCD kernel, each followed by the NCCL all-reduce."""
+    monkeypatch.setenv("ILS_FORCE_LARGE", "1")
+    pr = make_dense(600, 120, 80, 0.3, seed=46)
+    K = 3
+    ref_sp = O.sp_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE, sp_form=1)
+    ref_scd = O.sp_scd_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE, seed=3, max_inner=200,
+                             check_every=40, inner_tol=1e-9, alpha_mode=0)
+    h, keep = _handle(pr, comm)
+    try:
+        for fn, ref, kw in ((ils.ils_sp_solve, ref_sp, dict(sp_form=1)),
+                            (ils.ils_rgs_solve, ref_scd, dict(seed=3, max_inner=200, check_every=40, inner_tol=1e-9))):
+            hist = np.zeros((K, pr.n))
+            x = np.zeros(pr.n)
+            o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, x_hist=hist.ctypes.data, **kw)
+            fn(h, None, x, 0.0, K, o)
+            for k in range(K):
+                assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, (fn, k)
+    finally:
+        ils.ils_destroy(h)
