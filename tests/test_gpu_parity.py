@@ -405,3 +405,66 @@ def test_literal_precompute_forms(method):
         fn(hh.h, None, x, 0.0, K, o)
     for k in range(K):
         assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
+
+
+# ------------------------------------------------------------------ full-size bench configurations
+def test_c1_full_size_inner_counts_match_oracle():
+    """BASELINE.json configs[1] in the bench's configuration (x_ref stop at 1e-8, inner_tol 1e-10,
+    max_inner 1e6, seed 0): every outer step's inner-step count of SP-RK-RGS and SP-SCD equals the
+    oracle's (profiles/oracle_c1_counts.json, written by tools/oracle_counts.py from oracle/ only),
+    which pins the whole index stream and every inner stop decision at full size."""
+    import json
+    import os
+    ref = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                      "profiles", "oracle_c1_counts.json")))
+    pr = make_problem("c1")
+    xref = np.load(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                "workloads", "xref", "c1_seed0.npy"))
+    xr_t = torch.from_numpy(xref).to(DEV)
+    with H(pr) as hh:
+        for name, fn in (("rk", ils.ils_rk_solve), ("rgs", ils.ils_rgs_solve)):
+            x = torch.zeros(pr.n, dtype=torch.float64, device=DEV)
+            inner = np.zeros(200, dtype=np.int64)
+            o = ils.ils_default_opts(x_ref=xr_t.data_ptr(), inner_tol=ref["inner_tol"], max_inner=ref["max_inner"],
+                                     inner_hist=inner.ctypes.data)
+            st, rep = fn(hh.h, None, x, pr.tol, 200, o)
+            assert st == ils.ILS_OK and rep.converged, name
+            assert rep.outer_iters == ref[name]["outer"], name
+            assert list(inner[:rep.outer_iters]) == ref[name]["inner_hist"], name
+            err = _rel(x.cpu().numpy(), xref)
+            assert err <= pr.tol and abs(err - ref[name]["final_err"]) <= 1e-9 * ref[name]["final_err"] + 1e-12, name
+
+
+def test_scd_c1_fixed_horizon():
+    """c1 size through the CTA SP-SCD kernel (n = 1000, V = 4) against the oracle, 3000 steps."""
+    pr = make_problem("c1")
+    K, T, ce = 1, 3000, 1000
+    ref = O.sp_scd_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE, seed=0, max_inner=T,
+                         check_every=ce, inner_tol=0.0)
+    hist = np.zeros((K, pr.n))
+    x = np.zeros(pr.n)
+    with H(pr) as hh:
+        o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, seed=0, max_inner=T, check_every=ce, inner_tol=0.0,
+                                 x_hist=hist.ctypes.data)
+        ils.ils_rgs_solve(hh.h, None, x, 0.0, K, o)
+    assert _rel(hist[0], ref.x_hist[0]) <= 1e-9
+
+
+def test_c4_full_size_all_instances_converge():
+    """BASELINE.json configs[4]: all 4096 instances, every method, each within 1e-10 of its x*."""
+    pr = make_problem("c4")
+    for fn in (ils.ils_sp_solve, ils.ils_rk_solve, ils.ils_rgs_solve):
+        x = torch.zeros((pr.batch, pr.n), dtype=torch.float64, device=DEV)
+        A = torch.from_numpy(pr.A).to(DEV)
+        b = torch.from_numpy(pr.b).to(DEV)
+        xs = torch.from_numpy(pr.xstar).to(DEV)
+        sts = np.zeros(pr.batch, dtype=np.int32)
+        h = ils.ils_create(A, b, pr.p, pr.q, pr.n, batch=pr.batch)
+        try:
+            o = ils.ils_default_opts(x_ref=xs.data_ptr(), inner_tol=1e-12, max_inner=1_000_000)
+            st, rep = fn(h, None, x, pr.tol, 1000, o, inst_status=sts)
+        finally:
+            ils.ils_destroy(h)
+        assert st == ils.ILS_OK and sts.all(), fn
+        err = (torch.linalg.norm(x - xs, dim=1) / torch.linalg.norm(xs, dim=1)).max().item()
+        assert err <= pr.tol, (fn, err)
