@@ -312,6 +312,12 @@ def roofline(steps, peak_hbm, peak_bf16, traffic_map, cfg):
         peak = peak_hbm
         ach = per_launch_work / (per_launch_ms * 1e-3) / 1e9
         d = {"bound": "hbm", "unit": "GB/s", "peak_note": "measured hbm_gbs (MEASURED_PEAKS.json)"}
+    if c == 1:
+        d["limiter"] = ("latency: one 16-CTA DSMEM all-to-all per 4 inner steps (~1000-1300 cycles floor, "
+                        "tools/mb/dsmem_bench2.cu) plus the step's products; the columns are L2-resident at c1 "
+                        "(DESIGN.md §7)")
+    elif c == 2:
+        d["limiter"] = "latency: one dependent A1bar row load plus a CTA argmax per inner step (DESIGN.md §7)"
     tr = traffic_map.get(f"{cfg}:{c}") if traffic_map else None
     tr_note = None
     if isinstance(tr, dict):
