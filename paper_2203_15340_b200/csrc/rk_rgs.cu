@@ -699,6 +699,206 @@ static int launch_rk(Handle& h, RkParams& p, int nt, size_t smem) {
   return ILS_OK;
 }
 
+// Whole SP-RK-RGS inner solve in ONE CTA launch for small problems (one CTA, A1 staged entirely
+// in shared memory: ppad * npad * 8 <= ~150 KB, e.g. configs[0]): the blocked recurrence of
+// rk_rgs_block_kernel (4 steps per reduction, here over the CTA's warps only) plus the inner stop
+// check (include/ils.h: az = A1 z, g = A1^T az - b_hat, reset r = w - az) done in place every
+// check_every steps, so a solve is one launch instead of two launches per check interval.
+// Blocks restart at every check boundary (steps past it are masked), as the chunked launches do.
+template <int U>
+__global__ void __launch_bounds__(256, 1) rk_rgs_small_kernel(RkParams p, double* __restrict__ zout,
+                                                              int64_t ce, double inner_tol) {
+  constexpr int B = 4;
+  using K = RkBlk<B>;
+  constexpr int NVP = 32;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NT = blockDim.x, NW = NT >> 5;
+  const int64_t PP = p.ppad;
+  const int n = p.n;
+  double* A1s = reinterpret_cast<double*>(smem_raw);            // [npad][ppad], column j contiguous
+  double* zs = A1s + (size_t)p.npad * PP;                        // [npad]
+  double* azs = zs + p.npad;                                     // [ppad]
+  uint64_t* Ss = reinterpret_cast<uint64_t*>(azs + PP);          // [n]
+  double* bh_tab = reinterpret_cast<double*>(Ss + ((n + 1) & ~1));   // [n]
+  double* rn_tab = bh_tab + ((n + 1) & ~1);                     // [n]
+  RkIdx* ring = reinterpret_cast<RkIdx*>(rn_tab + ((n + 1) & ~1));   // [RK_RING]
+  __shared__ __align__(16) double wred[8][32];
+  __shared__ double tots[32];
+  __shared__ double red2[8][2];
+  __shared__ int stop_s;
+
+  for (int64_t e = tid; e < (int64_t)p.npad * PP; e += NT) A1s[e] = p.A1T[e];
+  for (int j = tid; j < p.npad; j += NT) zs[j] = 0.0;
+  for (int j = tid; j < n; j += NT) {
+    Ss[j] = p.S[j];
+    bh_tab[j] = p.bhat[j];
+    rn_tab[j] = 1.0 / p.N[j];
+  }
+  if (tid == 0) stop_s = 0;
+  __syncthreads();
+  // ||b_hat|| (fixed order) and the b_hat = 0 case (beta = 0 after 0 steps)
+  {
+    double v = 0.0;
+    for (int j = tid; j < n; j += NT) v = fma(bh_tab[j], bh_tab[j], v);
+    v = warp_sum(v);
+    if (lane == 0) red2[warp][0] = v;
+  }
+  __syncthreads();
+  double bnorm2 = 0.0;
+  for (int w = 0; w < NW; ++w) bnorm2 += red2[w][0];
+  __syncthreads();
+  if (bnorm2 == 0.0) {
+    if (tid == 0) {
+      p.st->inner_steps = 0;
+      p.st->inner_conv = 1;
+    }
+    for (int j = tid; j < p.npad; j += NT) zout[j] = 0.0;
+    return;
+  }
+  double w[U], r[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) w[u] = r[u] = 0.0;
+  int64_t filled = 0;   // ring holds steps [filled - RK_RING, filled)
+  int64_t t = 0;
+  bool conv = false;
+  while (t < p.max_inner && !conv) {
+    const int64_t cend = (t + ce < p.max_inner) ? t + ce : p.max_inner;   // this check interval
+    for (; t < cend; t += B) {
+      if (t + B > filled) {   // indices of the next 32 steps (one warp, then visible to all)
+        if (warp == 0) rk_fill_indices(p, Ss, ring, filled, lane, bh_tab, rn_tab);
+        filled += 32;
+        __syncthreads();
+      }
+      RkIdx ix[B];
+#pragma unroll
+      for (int i = 0; i < B; ++i) ix[i] = ring[(t + i) & (RK_RING - 1)];
+      double acc[NVP];
+#pragma unroll
+      for (int v = 0; v < NVP; ++v) acc[v] = 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = tid + u * NT;
+        if (e < PP) {
+          double xa[B], xb[B];
+#pragma unroll
+          for (int i = 0; i < B; ++i) {
+            xa[i] = A1s[(int64_t)ix[i].j1 * PP + e];
+            xb[i] = A1s[(int64_t)ix[i].j2 * PP + e];
+          }
+#pragma unroll
+          for (int i = 0; i < B; ++i) {
+            acc[K::P(i)] = fma(xa[i], w[u], acc[K::P(i)]);
+            acc[K::Q(i)] = fma(xb[i], r[u], acc[K::Q(i)]);
+#pragma unroll
+            for (int k = 0; k < i; ++k) {
+              acc[K::AA(i, k)] = fma(xa[i], xa[k], acc[K::AA(i, k)]);
+              acc[K::BB(i, k)] = fma(xb[i], xb[k], acc[K::BB(i, k)]);
+            }
+#pragma unroll
+            for (int k = 0; k <= i; ++k) acc[K::BA(i, k)] = fma(xb[i], xa[k], acc[K::BA(i, k)]);
+          }
+        }
+      }
+      const double mine = warp_reduce_scatter<NVP>(acc, lane);
+      wred[warp][lane] = mine;
+      __syncthreads();
+      if (warp == 0) {
+        double v = 0.0;
+        for (int w8 = 0; w8 < NW; ++w8) v += wred[w8][lane];
+        tots[lane] = v;
+      }
+      __syncthreads();
+      double T[K::NV];
+#pragma unroll
+      for (int v = 0; v < K::NV; ++v) T[v] = tots[v];
+      double s1[B], s2[B];
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+        const bool live = t + i < cend;   // steps past the check boundary (or max_inner) are masked
+        double dw = T[K::P(i)];
+#pragma unroll
+        for (int k = 0; k < i; ++k) dw = fma(s1[k], T[K::AA(i, k)], dw);
+        s1[i] = live ? (ix[i].bh1 - dw) * ix[i].rn1 : 0.0;
+        double dr = T[K::Q(i)];
+#pragma unroll
+        for (int k = 0; k < i; ++k) {
+          dr = fma(s1[k], T[K::BA(i, k)], dr);
+          dr = fma(-s2[k], T[K::BB(i, k)], dr);
+        }
+        dr = fma(s1[i], T[K::BA(i, i)], dr);
+        s2[i] = live ? dr * ix[i].rn2 : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = tid + u * NT;
+        if (e < PP) {
+#pragma unroll
+          for (int i = 0; i < B; ++i) {
+            const double xa = A1s[(int64_t)ix[i].j1 * PP + e], xb = A1s[(int64_t)ix[i].j2 * PP + e];
+            w[u] = fma(s1[i], xa, w[u]);
+            r[u] = fma(s1[i], xa, r[u]);
+            r[u] = fma(-s2[i], xb, r[u]);
+          }
+        }
+      }
+      if (tid == 0)
+#pragma unroll
+        for (int i = 0; i < B; ++i) zs[ix[i].j2] += s2[i];   // program order (j2 may repeat)
+      __syncthreads();   // tots / wred reuse, zs visible
+    }
+    t = cend;
+    if (t % ce != 0) break;   // max_inner reached off the check grid: no check (chunked path rule)
+    // ---- inner stop check at t: az = A1 z (own rows), g = A1^T az - b_hat, r := w - az
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = tid + u * NT;
+      if (e < PP) {
+        double a = 0.0, a2 = 0.0;
+        int j = 0;
+        for (; j + 1 < n; j += 2) {
+          a = fma(A1s[(int64_t)j * PP + e], zs[j], a);
+          a2 = fma(A1s[(int64_t)(j + 1) * PP + e], zs[j + 1], a2);
+        }
+        if (j < n) a = fma(A1s[(int64_t)j * PP + e], zs[j], a);
+        azs[e] = (e < p.slice) ? a + a2 : 0.0;   // rows >= p are zero padding
+      }
+    }
+    __syncthreads();
+    double g2 = 0.0;
+    for (int j = warp; j < n; j += NW) {
+      double sacc = 0.0;
+      for (int64_t i = lane; i < PP; i += 32) sacc = fma(A1s[(int64_t)j * PP + i], azs[i], sacc);
+      sacc = warp_sum(sacc);
+      const double g = sacc - bh_tab[j];
+      g2 = fma(g, g, g2);
+    }
+    if (lane == 0) red2[warp][1] = g2;
+    __syncthreads();
+    if (tid == 0) {
+      double G2 = 0.0;
+      for (int w8 = 0; w8 < NW; ++w8) G2 += red2[w8][1];
+      stop_s = (sqrt(G2) <= inner_tol * sqrt(bnorm2)) ? 1 : 0;
+    }
+    __syncthreads();
+    if (stop_s) {
+      conv = true;
+      if (tid == 0) {
+        p.st->inner_steps = t;
+        p.st->inner_conv = 1;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = tid + u * NT;
+        if (e < PP) r[u] = w[u] - azs[e];
+      }
+    }
+    __syncthreads();
+  }
+  for (int j = tid; j < p.npad; j += NT) zout[j] = zs[j];
+}
+
 template <int U>
 static int dispatch_rk_c(Handle& h, RkParams& p, int nt, size_t smem) {
   switch (p.C) {
@@ -883,6 +1083,38 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
     }
   }
   p.prof = prof;
+  {   // one-CTA problems: the whole inner solve in one launch (rk_rgs_small_kernel)
+    const char* e = getenv("ILS_RK_SMALL");
+    const size_t small_smem = ((size_t)h.npad * h.ppad + h.npad + h.ppad + 3 * (size_t)((h.n + 1) & ~1)) * 8 +
+                              RK_RING * sizeof(RkIdx) + 64;
+    if (C == 1 && !(e && e[0] == '0') && small_smem <= 200 * 1024 && h.ppad <= 2048 && !prof) {
+      // one row per thread up to 256 rows (8 warps share the products and reductions), then U rows
+      const int nts = (int)((h.ppad + 31) / 32 * 32);
+      const int ntc = nts > 256 ? 256 : nts;
+      const int Us = (int)((h.ppad + ntc - 1) / ntc);
+      p.slice = (int)h.p;   // rows >= p are padding (azs)
+      p.t0 = 0;
+      p.t1 = max_inner;
+      ILS_CU(cudaEventRecord(h.evk0, st));
+      void* kern = (Us <= 1) ? (void*)rk_rgs_small_kernel<1>
+                   : (Us <= 2) ? (void*)rk_rgs_small_kernel<2>
+                   : (Us <= 4) ? (void*)rk_rgs_small_kernel<4> : (void*)rk_rgs_small_kernel<8>;
+      ILS_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_smem));
+      double itol = inner_tol;
+      int64_t ce64 = ce;
+      void* args[] = {&p, &z, &ce64, &itol};
+      ILS_CU(cudaLaunchKernel(kern, dim3(1), dim3(ntc), args, small_smem, st));
+      ILS_LAUNCHED("rk_rgs_small_kernel");
+      ILS_CU(cudaEventRecord(h.evk1, st));
+      ILS_CU(cudaMemcpyAsync(h.hstat, h.dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+      ILS_CU(cudaStreamSynchronize(st));
+      const int64_t steps = h.hstat->inner_conv ? h.hstat->inner_steps : max_inner;
+      if (steps_out) *steps_out = steps;
+      const double pd = (double)h.p, nd = (double)h.n;
+      hot_account(h, 1, (double)steps * 16.0 * pd + (double)(steps / ce) * 8.0 * pd * nd, 1);
+      return ILS_OK;
+    }
+  }
   ILS_CU(cudaEventRecord(h.evk0, st));
   int64_t t = 0, nchecks = 0;
   int pending = 0;
