@@ -55,6 +55,8 @@ struct ScdParams {
   int alpha_mode, alpha_k, weighted;
   int all_members;   // alpha_t = n for every step (Remark 4.1 Motzkin case): tau_t = [n], no masks
   DevStatus* st;
+  int64_t ce;        // scd_warp_kernel: inner check every ce steps inside the launch (0: none)
+  double inner_tol;
 };
 
 __device__ __forceinline__ void scd_make_key(uint64_t seed, uint32_t k, uint64_t t, int n, int alpha_mode,
@@ -147,7 +149,41 @@ __global__ void __launch_bounds__(32, 1) scd_warp_kernel(ScdParams p) {
     q2 = (2 < L) ? __ldcg(mk + 64) : 0u;
     q3 = (3 < L) ? __ldcg(mk + 96) : 0u;
   }
+  double bn2 = 0.0;   // ||b_hat||^2 for the in-kernel checks (fixed order)
+  if (p.ce > 0) {
+    double v = 0.0;
+    for (int s = lane; s < n; s += 32) v = fma(p.bhat[s], p.bhat[s], v);
+    bn2 = warp_sum(v);
+  }
   for (int64_t t = p.t0; t < p.t1; ++t) {
+    if (p.ce > 0 && t > p.t0 && t % p.ce == 0) {   // inner check at t (include/ils.h): r = b_hat - A1bar beta
+      __syncwarp();
+      double r2 = 0.0;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int s = lane + 32 * v;
+        if (s < n) {
+          const double* grow2 = p.G + (int64_t)s * p.npad;
+          double a = 0.0, a2 = 0.0;
+          int kk = 0;
+          for (; kk + 1 < n; kk += 2) {
+            a = fma(__ldg(grow2 + kk), bs[kk], a);
+            a2 = fma(__ldg(grow2 + kk + 1), bs[kk + 1], a2);
+          }
+          if (kk < n) a = fma(__ldg(grow2 + kk), bs[kk], a);
+          r[v] = p.bhat[s] - (a + a2);
+          r2 = fma(r[v], r[v], r2);
+        }
+      }
+      r2 = warp_sum(r2);
+      if (sqrt(r2) <= p.inner_tol * sqrt(bn2)) {
+        if (lane == 0) {
+          p.st->inner_steps = t;
+          p.st->inner_conv = 1;
+        }
+        break;
+      }
+    }
     uint32_t inmask = allbits;
     if (!p.all_members) {
       inmask = q0;
@@ -458,7 +494,10 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
   const int per = (int)((h.n + nt - 1) / nt);
   int V = 1;
   while (V < per) V *= 2;
-  const int64_t chunk_cap = (max_inner < ce) ? max_inner : ce;
+  // the single-warp kernel runs kWarpChunks check intervals per launch with its checks in place
+  constexpr int64_t kWarpChunks = 8;
+  const int64_t span = warpk ? kWarpChunks * ce : ce;
+  const int64_t chunk_cap = (max_inner < span) ? max_inner : span;
   const size_t state_dbl = (size_t)3 * h.npad + 2 * (size_t)h.num_sms;
   const size_t mask_bytes = weighted ? 0 : (size_t)chunk_cap * nt * sizeof(uint32_t);
   const size_t need = state_dbl * sizeof(double) + mask_bytes;
@@ -529,8 +568,10 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
   ILS_CU(cudaEventRecord(h.evk0, st));
   int64_t t = 0;
   int pending = 0;
+  p.ce = warpk ? ce : 0;
+  p.inner_tol = inner_tol;
   while (t < max_inner) {
-    const int64_t t1 = (t + ce < max_inner) ? t + ce : max_inner;
+    const int64_t t1 = (t + span < max_inner) ? t + span : max_inner;
     if (!weighted && !p.all_members) {
       scd_masks_kernel<<<(unsigned)(t1 - t), 256, 0, st>>>(seed, (uint32_t)k, t, t1, nn, alpha_mode, alpha_k, nt,
                                                             V, masks);
