@@ -263,15 +263,6 @@ int mirror_lower(Handle& h, double* C, int64_t ld, int64_t n, int64_t n_real) {
   return ILS_OK;
 }
 
-// B[j][i] = A[i][j] (n x n, n multiple of 32)
-__global__ void transpose_kernel(const double* __restrict__ A, double* __restrict__ B, int64_t n) {
-  __shared__ double tile[32][33];
-  const int64_t bi = blockIdx.y, bj = blockIdx.x;
-  for (int r = threadIdx.y; r < 32; r += 8) tile[r][threadIdx.x] = A[(bi * 32 + r) * n + bj * 32 + threadIdx.x];
-  __syncthreads();
-  for (int r = threadIdx.y; r < 32; r += 8) B[(bj * 32 + r) * n + bi * 32 + threadIdx.x] = tile[threadIdx.x][r];
-}
-
 // ---------------------------------------------------------------- 64x64 base: potf2 + trtri
 // Cholesky of the 64x64 diagonal block at (s0, s0) of L (lower, in place) and its inverse into Z,
 // in shared memory with loops (no full unrolling: a fully unrolled 32x32 register version was

@@ -387,39 +387,6 @@ __global__ void __launch_bounds__(256) gemv_p_kernel(const double* __restrict__ 
   }
 }
 
-// y = T c with T triangular (lower: row i reads columns [0, i]; upper: [i, npad)); warp per row
-__global__ void __launch_bounds__(256) tri_gemv_kernel(const double* __restrict__ T, const double* __restrict__ c,
-                                                       int64_t npad, int64_t n, int upper, double* __restrict__ y) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double2* c2 = reinterpret_cast<const double2*>(c);
-  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < npad; i += (int64_t)gridDim.x * 8) {
-    const double2* tr = reinterpret_cast<const double2*>(T + i * npad);
-    const int64_t k0 = upper ? (i >> 1) : 0, k1 = upper ? npad / 2 : (i >> 1) + 1;   // double2 range
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int64_t k = k0 + lane;
-    for (; k + 7 * 32 < k1; k += 8 * 32) {
-      double2 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldcs(tr + k + 32 * u);
-#pragma unroll
-      for (int u = 0; u < 8; u += 2) {
-        const double2 a = __ldg(c2 + k + 32 * u), b = __ldg(c2 + k + 32 * (u + 1));
-        s0 = fma(v[u].x, a.x, s0);
-        s1 = fma(v[u].y, a.y, s1);
-        s2 = fma(v[u + 1].x, b.x, s2);
-        s3 = fma(v[u + 1].y, b.y, s3);
-      }
-    }
-    for (; k < k1; k += 32) {
-      const double2 v = __ldcs(tr + k), a = __ldg(c2 + k);
-      s0 = fma(v.x, a.x, s0);
-      s1 = fma(v.y, a.y, s1);
-    }
-    const double s = warp_sum((s0 + s1) + (s2 + s3));
-    if (lane == 0) y[i] = (i < n) ? s : 0.0;
-  }
-}
-
 int gemv_p(Handle& h, const double* c, double* x) {
   if (h.use_zt) return zc_apply_spine(h, c, x);   // x = Z^T (Z c) through the recursion's spine (dla.cu)
   gemv_p_kernel<<<(unsigned)(h.num_sms * 8), 256, 0, h.stream>>>(h.P, c, h.npad, h.n, x);
