@@ -49,6 +49,7 @@ struct RkParams {
   int C, slice, slicepad, nslots;
   long long* prof;     // optional per-phase cycle counters (rank 0, thread 0), see ILS_RK_PROF
   int gmode;           // 1: z and the sampling table stay in global memory (large n, single-step kernel)
+  const double* G;     // look-ahead kernel: A1bar (npad x npad) for the column inner products
 };
 
 // Ring entries for steps t0 .. t0+31 (one per lane): Philox draw, two weighted inverse-CDF
@@ -899,6 +900,357 @@ __global__ void __launch_bounds__(256, 1) rk_rgs_small_kernel(RkParams p, double
   for (int j = tid; j < p.npad; j += NT) zout[j] = zs[j];
 }
 
+// ---------------------------------------------------------------------------------------------
+// Look-ahead blocked SP-RK-RGS (experiment, ILS_RK_LA=1): the cluster exchange of block i+1 is in
+// flight while block i's recurrence runs. Block i+1's state products are formed on the state
+// S_i (before block i's update) and corrected after the exchange with block i's scalars and the
+// cross inner products between the two blocks' columns, looked up in A1bar (G):
+//   <a1'_k, w_{i+1}> = <a1'_k, w_i> + sum_m s1_m <a1'_k, a1_m>
+//   <a2'_k, r_{i+1}> = <a2'_k, r_i> + sum_m s1_m <a2'_k, a1_m> - sum_m s2_m <a2'_k, a2_m>
+// The 22 in-block column products also come from G, so only 8 values per block are reduced. The
+// last warp of the CTA is a communication warp: it sums the compute warps' partials, sends them
+// to the cluster (destination-uniform st.async), refills the TMA ring and fills the index / Gram
+// ring ahead; the compute warps never issue a send.
+constexpr int LA_NG = 70;   // Gram values per block: 22 in-block (RkBlk<4> order) + 48 cross
+
+// (value v of a block) -> (step of the current block, its column, step of the same / previous block,
+// its column): 22 in-block products in RkBlk<4> order, then X1, X2, X3 (4 x 4 each) with block - 1
+__constant__ int8_t la_map[LA_NG][4] = {
+    {1, 0, 0, 0}, {2, 0, 0, 0}, {2, 0, 1, 0}, {3, 0, 0, 0}, {3, 0, 1, 0}, {3, 0, 2, 0},                       // AA
+    {0, 1, 0, 0}, {1, 1, 0, 0}, {1, 1, 1, 0}, {2, 1, 0, 0}, {2, 1, 1, 0}, {2, 1, 2, 0}, {3, 1, 0, 0},
+    {3, 1, 1, 0}, {3, 1, 2, 0}, {3, 1, 3, 0},                                                               // BA
+    {1, 1, 0, 1}, {2, 1, 0, 1}, {2, 1, 1, 1}, {3, 1, 0, 1}, {3, 1, 1, 1}, {3, 1, 2, 1},                       // BB
+    {0, 0, -4, 0}, {0, 0, -3, 0}, {0, 0, -2, 0}, {0, 0, -1, 0}, {1, 0, -4, 0}, {1, 0, -3, 0}, {1, 0, -2, 0},
+    {1, 0, -1, 0}, {2, 0, -4, 0}, {2, 0, -3, 0}, {2, 0, -2, 0}, {2, 0, -1, 0}, {3, 0, -4, 0}, {3, 0, -3, 0},
+    {3, 0, -2, 0}, {3, 0, -1, 0},                                                                           // X1
+    {0, 1, -4, 0}, {0, 1, -3, 0}, {0, 1, -2, 0}, {0, 1, -1, 0}, {1, 1, -4, 0}, {1, 1, -3, 0}, {1, 1, -2, 0},
+    {1, 1, -1, 0}, {2, 1, -4, 0}, {2, 1, -3, 0}, {2, 1, -2, 0}, {2, 1, -1, 0}, {3, 1, -4, 0}, {3, 1, -3, 0},
+    {3, 1, -2, 0}, {3, 1, -1, 0},                                                                           // X2
+    {0, 1, -4, 1}, {0, 1, -3, 1}, {0, 1, -2, 1}, {0, 1, -1, 1}, {1, 1, -4, 1}, {1, 1, -3, 1}, {1, 1, -2, 1},
+    {1, 1, -1, 1}, {2, 1, -4, 1}, {2, 1, -3, 1}, {2, 1, -2, 1}, {2, 1, -1, 1}, {3, 1, -4, 1}, {3, 1, -3, 1},
+    {3, 1, -2, 1}, {3, 1, -1, 1}};                                                                          // X3
+
+// Gram values of 8 blocks from blk0 (one warp): all loads issued before any store
+__device__ __forceinline__ void la_fill_gram(const RkParams& p, const RkIdx* ring, double (*gring)[LA_NG],
+                                             int64_t blk0, int lane) {
+  __syncwarp();
+  constexpr int PER = (8 * LA_NG + 31) / 32;
+  double val[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int e = lane + 32 * q;
+    val[q] = 0.0;
+    if (e < 8 * LA_NG) {
+      const int bl = e / LA_NG, v = e - bl * LA_NG;
+      const int64_t b = blk0 + bl;
+      const int64_t tb = p.t0 + 4 * b;
+      const int sa = la_map[v][0], ca = la_map[v][1], sb = la_map[v][2], cb = la_map[v][3];
+      if (v < 22 || b > 0) {
+        const RkIdx ea = ring[(tb + sa) & (RK_RING - 1)];
+        const RkIdx ebb = ring[(tb + sb) & (RK_RING - 1)];
+        const int ja = ca ? ea.j2 : ea.j1, jb = cb ? ebb.j2 : ebb.j1;
+        val[q] = __ldg(p.G + (int64_t)ja * p.npad + jb);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int e = lane + 32 * q;
+    if (e < 8 * LA_NG) {
+      const int bl = e / LA_NG, v = e - bl * LA_NG;
+      gring[(blk0 + bl) & 31][v] = val[q];
+    }
+  }
+}
+
+template <int CC, int U>
+__global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
+  constexpr int B = 4, NRV = 8;
+  using K = RkBlk<B>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NT = blockDim.x, NW = NT >> 5, NWc = NW - 2, NTc = NWc * 32;
+  const bool comm = (warp == NWc), feeder = (warp == NWc + 1), helper = comm || feeder;
+  const int rank = (int)cluster_ctarank();
+  const int64_t i0 = (int64_t)rank * p.slice;
+  const int own = (int)((i0 + p.slice <= p.ppad) ? p.slice : (p.ppad > i0 ? p.ppad - i0 : 0));
+  const int NS = p.nslots, SP = p.slicepad;
+  if (*(volatile int32_t*)&p.st->inner_conv != 0) return;
+
+  double* slots = reinterpret_cast<double*>(smem_raw);                 // [NS][2B][slicepad]
+  double* zs = slots + (size_t)NS * 2 * B * SP;                        // [npad]
+  uint64_t* Ss = reinterpret_cast<uint64_t*>(zs + p.npad);             // [n]
+  RkIdx* ring = reinterpret_cast<RkIdx*>(Ss + ((p.n + 1) & ~1));       // [RK_RING]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + RK_RING);        // [NS]
+  double* bh_tab = reinterpret_cast<double*>(bars + 8);                 // [n]
+  double* rn_tab = bh_tab + ((p.n + 1) & ~1);                          // [n]
+  double (*gring)[LA_NG] = reinterpret_cast<double (*)[LA_NG]>(rn_tab + ((p.n + 1) & ~1));   // [32][70]
+  __shared__ __align__(16) double wred[2][8][8];
+  __shared__ __align__(16) double recv[4][RK_MAXC][NRV];
+  __shared__ __align__(8) uint64_t rbar[4];
+  __shared__ double chkw[9];
+  __shared__ double bnorm_s;
+
+  for (int64_t j = tid; j < p.npad; j += NT) zs[j] = p.Z[j];
+  for (int j = tid; j < p.n; j += NT) {
+    Ss[j] = p.S[j];
+    bh_tab[j] = p.bhat[j];
+    rn_tab[j] = 1.0 / p.N[j];
+  }
+  for (int64_t e = tid; e < (int64_t)NS * 2 * B * SP; e += NT) slots[e] = 0.0;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < 4; ++s) mbar_init(&rbar[s], 1);
+    fence_mbar_init();
+    for (int s = 0; s < 4; ++s) mbar_arrive_expect_tx(&rbar[s], CC * NRV * 8);
+  }
+  double bnorm = 1.0;
+  if (p.t0 == 0) {
+    double v = 0.0;
+    for (int j = tid; j < p.n; j += NT) v = fma(p.bhat[j], p.bhat[j], v);
+    v = warp_sum(v);
+    if (lane == 0) chkw[warp] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < NW; ++w) s += chkw[w];
+      bnorm_s = sqrt(s);
+    }
+    __syncthreads();
+    bnorm = bnorm_s;
+  }
+  __syncthreads();
+  cluster_sync_all();
+  if (bnorm == 0.0) {
+    if (rank == 0 && tid == 0) {
+      p.st->inner_steps = 0;
+      p.st->inner_conv = 1;
+    }
+    return;
+  }
+  const int64_t nblk = (p.t1 - p.t0 + B - 1) / B;
+  const uint32_t slice_bytes = (uint32_t)own * sizeof(double);
+  int64_t filled_blk = 0;   // blocks whose ring + Gram entries are written
+  if (feeder) {
+    for (int q = 0; q < 2; ++q) {   // 16 blocks ahead
+      rk_fill_indices(p, Ss, ring, p.t0 + 32 * q, lane, bh_tab, rn_tab);
+      la_fill_gram(p, ring, gring, 8 * q, lane);
+    }
+  }
+  filled_blk = 16;
+  auto issue = [&](int64_t blk, int slot) {   // 2B column slices of block blk (comm lane 0)
+    double* dst = slots + (size_t)slot * 2 * B * SP;
+    mbar_arrive_expect_tx(&bars[slot], 2 * B * slice_bytes);
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      const RkIdx e = ring[(p.t0 + blk * B + i) & (RK_RING - 1)];
+      bulk_g2s(dst + (2 * i) * SP, p.A1T + (int64_t)e.j1 * p.ppad + i0, slice_bytes, &bars[slot]);
+      bulk_g2s(dst + (2 * i + 1) * SP, p.A1T + (int64_t)e.j2 * p.ppad + i0, slice_bytes, &bars[slot]);
+    }
+  };
+  if (feeder && lane == 0 && own > 0) {
+    fence_proxy_async();
+    for (int64_t b = 0; b < NS && b < nblk; ++b) issue(b, (int)b);
+  }
+  __syncthreads();
+
+  double w[U], r[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int e = tid + u * NTc;
+    const bool in = !helper && (e < own);
+    w[u] = in ? p.W[i0 + e] : 0.0;
+    r[u] = in ? p.Rv[i0 + e] : 0.0;
+  }
+  double s1p[B], s2p[B];
+#pragma unroll
+  for (int i = 0; i < B; ++i) s1p[i] = s2p[i] = 0.0;
+
+  const bool prof = p.prof && (tid == 0 || (helper && lane == 0));
+  long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tc = clock64();
+#define LAP(k)                       \
+  if (prof) {                        \
+    const long long c_ = clock64();  \
+    pc[k] += c_ - tc;                \
+    tc = c_;                         \
+  }
+  for (int64_t i = -1; i < nblk; ++i) {
+    const int64_t nb = i + 1;   // block whose partials are formed and sent in this iteration
+    // ---- phase 1 (compute warps): state products of block nb on the current state S_{nb-1}
+    if (!helper && nb < nblk) {
+      const int sl = (int)(nb % NS);
+      if (own > 0) mbar_wait(&bars[sl], (uint32_t)((nb / NS) & 1));
+      const double* cols = slots + (size_t)sl * 2 * B * SP;
+      double acc[NRV];
+#pragma unroll
+      for (int v = 0; v < NRV; ++v) acc[v] = 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = tid + u * NTc;
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+          acc[K::P(k)] = fma(cols[(2 * k) * SP + e], w[u], acc[K::P(k)]);
+          acc[K::Q(k)] = fma(cols[(2 * k + 1) * SP + e], r[u], acc[K::Q(k)]);
+        }
+      }
+      const double mine = warp_reduce_scatter<NRV>(acc, lane);   // lane l: warp total of value l & 7
+      if (lane < NRV) wred[nb & 1][warp][lane] = mine;
+    }
+    LAP(helper ? 7 : 0)
+    named_bar_sync(1, NT);   // B1: partials of nb visible; every compute thread finished block i-1
+    LAP(helper ? 4 : 1)
+    if (comm) {
+      if (nb < nblk) {   // send block nb's CTA totals to every rank (lanes 0..3: values 2l, 2l+1)
+        double v = 0.0;
+        for (int w8 = 0; w8 < NWc; ++w8) v += wred[nb & 1][w8][lane & 7];
+        const double v0 = __shfl_sync(0xffffffffu, v, (2 * lane) & 7);
+        const double v1 = __shfl_sync(0xffffffffu, v, (2 * lane + 1) & 7);
+        const int b4 = (int)(nb & 3);
+        const uint32_t la = smem_u32(&recv[b4][rank][2 * (lane & 3)]);
+        const uint32_t lb = smem_u32(&rbar[b4]);
+        if (lane < NRV / 2)
+          for (int c = 0; c < CC; ++c) st_async_v2f64(map_shared_rank(la, (uint32_t)c), v0, v1, map_shared_rank(lb, (uint32_t)c));
+      }
+      LAP(5)
+      continue;
+    }
+    if (feeder) {
+      // refill the slot of block i-1 (its axpy finished before B1) with block i-1+NS
+      if (i >= 1 && (i - 1) + NS < nblk && lane == 0 && own > 0) issue((i - 1) + NS, (int)((i - 1) % NS));
+      LAP(6)
+      // indices + Gram values ahead (visible to the compute warps after the next B1)
+      if (filled_blk < nblk && filled_blk < i + NS + 10) {
+        rk_fill_indices(p, Ss, ring, p.t0 + 4 * filled_blk, lane, bh_tab, rn_tab);
+        la_fill_gram(p, ring, gring, filled_blk, lane);
+        filled_blk += 8;
+      }
+      LAP(7)
+      continue;
+    }
+    if (i < 0) continue;
+    // ---- phase 2 (compute warps): block i
+    const int b4 = (int)(i & 3);
+    mbar_wait_cluster(&rbar[b4], (uint32_t)((i >> 2) & 1));
+    LAP(2)
+    double tot;
+    {
+      double a[CC];
+#pragma unroll
+      for (int c = 0; c < CC; ++c) a[c] = recv[b4][c][lane & 7];
+#pragma unroll
+      for (int s = 1; s < CC; s *= 2)
+#pragma unroll
+        for (int c = 0; c + s < CC; c += 2 * s) a[c] += a[c + s];
+      tot = a[0];
+    }
+    double T[K::NV];
+#pragma unroll
+    for (int v = 0; v < NRV; ++v) T[v] = __shfl_sync(0xffffffffu, tot, v);
+    const double* gb = gring[i & 31];
+#pragma unroll
+    for (int v = NRV; v < K::NV; ++v) T[v] = gb[v - NRV];
+    if (i > 0) {   // corrections for block i-1's update (its products used S_{i-1})
+#pragma unroll
+      for (int k = 0; k < B; ++k) {
+        double cp = T[K::P(k)], cq = T[K::Q(k)];
+#pragma unroll
+        for (int m = 0; m < B; ++m) {
+          cp = fma(s1p[m], gb[22 + 4 * k + m], cp);
+          cq = fma(s1p[m], gb[38 + 4 * k + m], cq);
+          cq = fma(-s2p[m], gb[54 + 4 * k + m], cq);
+        }
+        T[K::P(k)] = cp;
+        T[K::Q(k)] = cq;
+      }
+    }
+    const int64_t t = p.t0 + i * B;
+    double s1[B], s2[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const RkIdx ix = ring[(t + k) & (RK_RING - 1)];
+      double dw = T[K::P(k)];
+#pragma unroll
+      for (int m = 0; m < k; ++m) dw = fma(s1[m], T[K::AA(k, m)], dw);
+      s1[k] = (ix.bh1 - dw) * ix.rn1;
+      double dr = T[K::Q(k)];
+#pragma unroll
+      for (int m = 0; m < k; ++m) {
+        dr = fma(s1[m], T[K::BA(k, m)], dr);
+        dr = fma(-s2[m], T[K::BB(k, m)], dr);
+      }
+      dr = fma(s1[k], T[K::BA(k, k)], dr);
+      s2[k] = dr * ix.rn2;
+    }
+    const double* cols = slots + (size_t)(i % NS) * 2 * B * SP;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = tid + u * NTc;
+#pragma unroll
+      for (int k = 0; k < B; ++k) {
+        const double xa = cols[(2 * k) * SP + e], xb = cols[(2 * k + 1) * SP + e];
+        w[u] = fma(s1[k], xa, w[u]);
+        r[u] = fma(s1[k], xa, r[u]);
+        r[u] = fma(-s2[k], xb, r[u]);
+      }
+    }
+    if (tid == 0)
+#pragma unroll
+      for (int k = 0; k < B; ++k) zs[ring[(t + k) & (RK_RING - 1)].j2] += s2[k];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      s1p[k] = s1[k];
+      s2p[k] = s2[k];
+    }
+    named_bar_sync(2, NTc);   // every compute thread read recv[b4]
+    if (tid == 0) mbar_arrive_expect_tx(&rbar[b4], CC * NRV * 8);   // for block i + 4
+    LAP(3)
+  }
+#undef LAP
+  if (prof && tid == 0)
+    for (int k = 0; k < 4; ++k) p.prof[rank * 8 + k] += pc[k];
+  if (prof && comm && lane == 0)
+    for (int k = 4; k < 6; ++k) p.prof[rank * 8 + k] += pc[k];
+  if (prof && feeder && lane == 0)
+    for (int k = 6; k < 8; ++k) p.prof[rank * 8 + k] += pc[k];
+  if (!helper) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = tid + u * NTc;
+      if (e < own) {
+        p.W[i0 + e] = w[u];
+        p.Rv[i0 + e] = r[u];
+      }
+    }
+  }
+  __syncthreads();
+  if (rank == 0)
+    for (int64_t j = tid; j < p.npad; j += NT) p.Z[j] = zs[j];
+  cluster_sync_all();
+}
+
+template <int CC, int U>
+static int launch_rkla(Handle& h, RkParams& p, int nt, size_t smem) {
+  auto kern = rk_rgs_la_kernel<CC, U>;
+  ILS_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ILS_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CC);
+  cfg.blockDim = dim3(nt);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = h.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ILS_CU(cudaLaunchKernelEx(&cfg, kern, p));
+  ILS_LAUNCHED("rk_rgs_la_kernel");
+  return ILS_OK;
+}
+
 template <int U>
 static int dispatch_rk_c(Handle& h, RkParams& p, int nt, size_t smem) {
   switch (p.C) {
@@ -1071,13 +1423,29 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
     break;
   }
 
+  // look-ahead variant (ILS_RK_LA=1): one more warp, a 32-block Gram ring in shared memory
+  bool la = false;
+  size_t smem_la = 0;
+  {
+    const char* e = getenv("ILS_RK_LA");
+    if (e && e[0] == '1' && blocked && C == 16 && Bk == 4 && (U == 4 || U == 8) && nt + 64 <= 288 && !h.large &&
+        !h.sparse) {
+      smem_la = smem + (size_t)32 * LA_NG * sizeof(double);
+      if (smem_la <= 227 * 1024) {
+        int rc = build_gram(h);
+        if (rc) return rc;
+        p.G = h.G;
+        la = true;
+      }
+    }
+  }
   // chunks of check_every steps, each followed by the full-GPU inner check; launches are queued
   // ahead (kernels of a stopped solve return at once) and the stop flag is read every kBatch checks
   constexpr int kBatch = 8;
   long long* prof = nullptr;
   {
     const char* e = getenv("ILS_RK_PROF");
-    if (e && e[0] == '1' && blocked) {
+    if (e && e[0] == '1' && blocked) {   // (the look-ahead kernel reports: compute phase1, B1, recv, phase2 | comm B1, send, refill, fill)
       ILS_CU(cudaMallocAsync(&prof, 16 * 8 * sizeof(long long), st));
       ILS_CU(cudaMemsetAsync(prof, 0, 16 * 8 * sizeof(long long), st));
     }
@@ -1123,8 +1491,9 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
     const int64_t t1 = (t + ce < max_inner) ? t + ce : max_inner;
     p.t0 = t;
     p.t1 = t1;
-    const int r = blocked ? dispatch_rkb(h, p, U, Bk, nt, smem)
-                          : ((U == 8) ? dispatch_rk_c<8>(h, p, nt, smem) : dispatch_rk_c<4>(h, p, nt, smem));
+    const int r = la ? ((U == 4) ? launch_rkla<16, 4>(h, p, nt + 64, smem_la) : launch_rkla<16, 8>(h, p, nt + 64, smem_la))
+                  : blocked ? dispatch_rkb(h, p, U, Bk, nt, smem)
+                            : ((U == 8) ? dispatch_rk_c<8>(h, p, nt, smem) : dispatch_rk_c<4>(h, p, nt, smem));
     if (r) return r;
     t = t1;
     if (t % ce == 0) {

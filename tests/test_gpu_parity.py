@@ -260,6 +260,24 @@ def test_rk_cluster_path_c1_horizon():
         assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
 
 
+def test_rk_lookahead_kernel_c1_horizon(monkeypatch):
+    """The look-ahead SP-RK-RGS kernel (opt-in, ILS_RK_LA=1: block i+1's exchange in flight during
+    block i, stale-state products corrected through A1bar) against the oracle at c1 size."""
+    monkeypatch.setenv("ILS_RK_LA", "1")
+    pr = make_problem("c1")
+    K, T, ce = 2, 3000, 1000
+    ref = O.sp_rk_rgs_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE, seed=1,
+                            max_inner=T, check_every=ce, inner_tol=0.0)
+    hist = np.zeros((K, pr.n))
+    x = np.zeros(pr.n)
+    with H(pr) as hh:
+        o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, seed=1, max_inner=T, check_every=ce, inner_tol=0.0,
+                                 x_hist=hist.ctypes.data)
+        ils.ils_rk_solve(hh.h, None, x, 0.0, K, o)
+    for k in range(K):
+        assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
+
+
 def test_rk_converges_c0():
     pr = make_problem("c0")
     ref = O.sp_rk_rgs_solve(pr.A1, pr.A2, pr.b1, pr.b2, tol=1e-10, x_ref=pr.xstar, inner_tol=1e-12,
