@@ -1113,11 +1113,11 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
           for (int c = 0; c < CC; ++c) st_async_v2f64(map_shared_rank(la, (uint32_t)c), v0, v1, map_shared_rank(lb, (uint32_t)c));
       }
       LAP(5)
+      // refill the slot of block i-1 (its axpy finished before B1) with block i-1+NS
+      if (i >= 1 && (i - 1) + NS < nblk && lane == 0 && own > 0) issue((i - 1) + NS, (int)((i - 1) % NS));
       continue;
     }
     if (feeder) {
-      // refill the slot of block i-1 (its axpy finished before B1) with block i-1+NS
-      if (i >= 1 && (i - 1) + NS < nblk && lane == 0 && own > 0) issue((i - 1) + NS, (int)((i - 1) % NS));
       LAP(6)
       // indices + Gram values ahead (visible to the compute warps after the next B1)
       if (filled_blk < nblk && filled_blk < i + NS + 10) {
