@@ -486,3 +486,25 @@ def test_c4_full_size_all_instances_converge():
         assert st == ils.ILS_OK and sts.all(), fn
         err = (torch.linalg.norm(x - xs, dim=1) / torch.linalg.norm(xs, dim=1)).max().item()
         assert err <= pr.tol, (fn, err)
+
+
+# ------------------------------------------------------------------ determinism (include/ils.h)
+@pytest.mark.parametrize("cfg", ["c0", "c1"])
+def test_bitwise_deterministic_runs(cfg):
+    """Same inputs and seed give bitwise-identical iterates and counts (fixed-order reductions, no
+    floating-point atomics on the dense paths): two fresh handles, every method, a short horizon."""
+    pr = make_problem(cfg)
+    outs = []
+    for _ in range(2):
+        res = []
+        with H(pr) as hh:
+            for fn in (ils.ils_sp_solve, ils.ils_rk_solve, ils.ils_rgs_solve):
+                x = np.zeros(pr.n)
+                inner = np.zeros(3, dtype=np.int64)
+                o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, seed=7, max_inner=2500, inner_tol=1e-6,
+                                         inner_hist=inner.ctypes.data)
+                fn(hh.h, None, x, 0.0, 3, o)
+                res.append((x.copy(), inner.copy()))
+        outs.append(res)
+    for (xa, ia), (xb, ib) in zip(outs[0], outs[1]):
+        assert np.array_equal(xa, xb) and np.array_equal(ia, ib)
