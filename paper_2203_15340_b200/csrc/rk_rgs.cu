@@ -963,14 +963,28 @@ __device__ __forceinline__ void la_fill_gram(const RkParams& p, const RkIdx* rin
   }
 }
 
+__device__ __forceinline__ int64_t ld_acquire_cta_s64(const int64_t* a) {
+  int64_t v;
+  asm volatile("ld.acquire.cta.shared::cta.s64 %0, [%1];" : "=l"(v) : "r"(smem_u32(a)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta_s64(int64_t* a, int64_t v) {
+  asm volatile("st.release.cta.shared::cta.s64 [%0], %1;" ::"r"(smem_u32(a)), "l"(v) : "memory");
+}
+
+// Warp roles: NWc compute warps (rows), a communication warp (sends the block partials), a fill
+// warp (index + Gram rings ahead) and a TMA warp (column refills). Only compute + communication
+// warps meet at a named barrier per block; the fill and TMA warps run ahead, throttled by progress
+// counters in shared memory (release / acquire), so their long operations never stall the step.
 template <int CC, int U>
 __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
   constexpr int B = 4, NRV = 8;
   using K = RkBlk<B>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int NT = blockDim.x, NW = NT >> 5, NWc = NW - 2, NTc = NWc * 32;
-  const bool comm = (warp == NWc), feeder = (warp == NWc + 1), helper = comm || feeder;
+  const int NT = blockDim.x, NW = NT >> 5, NWc = NW - 3, NTc = NWc * 32;
+  const bool comm = (warp == NWc), filler = (warp == NWc + 1), tmaw = (warp == NWc + 2);
+  const bool compute = warp < NWc;
   const int rank = (int)cluster_ctarank();
   const int64_t i0 = (int64_t)rank * p.slice;
   const int own = (int)((i0 + p.slice <= p.ppad) ? p.slice : (p.ppad > i0 ? p.ppad - i0 : 0));
@@ -988,8 +1002,10 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
   __shared__ __align__(16) double wred[2][8][8];
   __shared__ __align__(16) double recv[4][RK_MAXC][NRV];
   __shared__ __align__(8) uint64_t rbar[4];
-  __shared__ double chkw[9];
+  __shared__ double chkw[12];
   __shared__ double bnorm_s;
+  __shared__ __align__(8) int64_t filled_s;   // blocks whose index + Gram entries are written
+  __shared__ __align__(8) int64_t done_s;     // blocks whose axpy is complete (compute warps)
 
   for (int64_t j = tid; j < p.npad; j += NT) zs[j] = p.Z[j];
   for (int j = tid; j < p.n; j += NT) {
@@ -1003,6 +1019,7 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
     for (int s = 0; s < 4; ++s) mbar_init(&rbar[s], 1);
     fence_mbar_init();
     for (int s = 0; s < 4; ++s) mbar_arrive_expect_tx(&rbar[s], CC * NRV * 8);
+    done_s = 0;
   }
   double bnorm = 1.0;
   if (p.t0 == 0) {
@@ -1030,15 +1047,14 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
   }
   const int64_t nblk = (p.t1 - p.t0 + B - 1) / B;
   const uint32_t slice_bytes = (uint32_t)own * sizeof(double);
-  int64_t filled_blk = 0;   // blocks whose ring + Gram entries are written
-  if (feeder) {
-    for (int q = 0; q < 2; ++q) {   // 16 blocks ahead
+  if (filler) {
+    for (int q = 0; q < 2; ++q) {   // 16 blocks ahead before the step loop starts
       rk_fill_indices(p, Ss, ring, p.t0 + 32 * q, lane, bh_tab, rn_tab);
       la_fill_gram(p, ring, gring, 8 * q, lane);
     }
+    if (lane == 0) filled_s = 16;
   }
-  filled_blk = 16;
-  auto issue = [&](int64_t blk, int slot) {   // 2B column slices of block blk (comm lane 0)
+  auto issue = [&](int64_t blk, int slot) {   // 2B column slices of block blk (one thread)
     double* dst = slots + (size_t)slot * 2 * B * SP;
     mbar_arrive_expect_tx(&bars[slot], 2 * B * slice_bytes);
 #pragma unroll
@@ -1048,178 +1064,179 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
       bulk_g2s(dst + (2 * i + 1) * SP, p.A1T + (int64_t)e.j2 * p.ppad + i0, slice_bytes, &bars[slot]);
     }
   };
-  if (feeder && lane == 0 && own > 0) {
+  __syncthreads();
+  if (tmaw && lane == 0 && own > 0) {
     fence_proxy_async();
     for (int64_t b = 0; b < NS && b < nblk; ++b) issue(b, (int)b);
   }
-  __syncthreads();
 
-  double w[U], r[U];
+  if (filler) {   // ---- fill warp: index + Gram rings, at most 24 blocks ahead of the consumers
+    int64_t f = 16;
+    while (f < nblk) {
+      while (f + 8 > ld_acquire_cta_s64(&done_s) + 24) {
+      }
+      rk_fill_indices(p, Ss, ring, p.t0 + 4 * f, lane, bh_tab, rn_tab);
+      la_fill_gram(p, ring, gring, f, lane);
+      f += 8;
+      __syncwarp();
+      if (lane == 0) st_release_cta_s64(&filled_s, f);
+    }
+  } else if (tmaw) {   // ---- TMA warp: refill slot (b % NS) once block b - NS is done
+    if (lane == 0 && own > 0) {
+      int slot = 0;
+      for (int64_t b = NS; b < nblk; ++b) {
+        while (ld_acquire_cta_s64(&done_s) < b - NS + 1 || ld_acquire_cta_s64(&filled_s) <= b) {
+        }
+        fence_proxy_async();
+        issue(b, slot);
+        if (++slot == NS) slot = 0;
+      }
+    }
+  } else {   // ---- compute warps and the communication warp
+    double w[U], r[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int e = tid + u * NTc;
-    const bool in = !helper && (e < own);
-    w[u] = in ? p.W[i0 + e] : 0.0;
-    r[u] = in ? p.Rv[i0 + e] : 0.0;
-  }
-  double s1p[B], s2p[B];
+    for (int u = 0; u < U; ++u) {
+      const int e = tid + u * NTc;
+      const bool in = compute && (e < own);
+      w[u] = in ? p.W[i0 + e] : 0.0;
+      r[u] = in ? p.Rv[i0 + e] : 0.0;
+    }
+    double s1p[B], s2p[B];
 #pragma unroll
-  for (int i = 0; i < B; ++i) s1p[i] = s2p[i] = 0.0;
-
-  const bool prof = p.prof && (tid == 0 || (helper && lane == 0));
-  long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long tc = clock64();
-#define LAP(k)                       \
-  if (prof) {                        \
-    const long long c_ = clock64();  \
-    pc[k] += c_ - tc;                \
-    tc = c_;                         \
-  }
-  for (int64_t i = -1; i < nblk; ++i) {
-    const int64_t nb = i + 1;   // block whose partials are formed and sent in this iteration
-    // ---- phase 1 (compute warps): state products of block nb on the current state S_{nb-1}
-    if (!helper && nb < nblk) {
-      const int sl = (int)(nb % NS);
-      if (own > 0) mbar_wait(&bars[sl], (uint32_t)((nb / NS) & 1));
-      const double* cols = slots + (size_t)sl * 2 * B * SP;
-      double acc[NRV];
+    for (int i = 0; i < B; ++i) s1p[i] = s2p[i] = 0.0;
+    int sl_nb = NS - 1, sl_i = NS - 2;
+    uint32_t ph_nb = 1;
+    for (int64_t i = -1; i < nblk; ++i) {
+      const int64_t nb = i + 1;
+      sl_i = sl_nb;
+      if (++sl_nb == NS) {
+        sl_nb = 0;
+        ph_nb ^= 1u;
+      }
+      // ---- phase 1 (compute warps): state products of block nb on S_{nb-1}
+      if (compute && nb < nblk) {
+        while (ld_acquire_cta_s64(&filled_s) <= nb + 1) {   // ring + Gram entries of blocks nb, nb+1
+          if (ld_acquire_cta_s64(&filled_s) >= nblk) break;
+        }
+        if (own > 0) mbar_wait(&bars[sl_nb], ph_nb);
+        const double* cols = slots + (size_t)sl_nb * 2 * B * SP;
+        double acc[NRV];
 #pragma unroll
-      for (int v = 0; v < NRV; ++v) acc[v] = 0.0;
+        for (int v = 0; v < NRV; ++v) acc[v] = 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = tid + u * NTc;
+#pragma unroll
+          for (int k = 0; k < B; ++k) {
+            acc[K::P(k)] = fma(cols[(2 * k) * SP + e], w[u], acc[K::P(k)]);
+            acc[K::Q(k)] = fma(cols[(2 * k + 1) * SP + e], r[u], acc[K::Q(k)]);
+          }
+        }
+        const double mine = warp_reduce_scatter<NRV>(acc, lane);
+        if (lane < NRV) wred[nb & 1][warp][lane] = mine;
+      }
+      named_bar_sync(1, NTc + 32);   // B1: compute warps + communication warp
+      if (comm) {
+        if (nb < nblk) {
+          double v = 0.0;
+          for (int w8 = 0; w8 < NWc; ++w8) v += wred[nb & 1][w8][lane & 7];
+          const double v0 = __shfl_sync(0xffffffffu, v, (2 * lane) & 7);
+          const double v1 = __shfl_sync(0xffffffffu, v, (2 * lane + 1) & 7);
+          const int b4 = (int)(nb & 3);
+          const uint32_t la = smem_u32(&recv[b4][rank][2 * (lane & 3)]);
+          const uint32_t lb = smem_u32(&rbar[b4]);
+          if (lane < NRV / 2)
+            for (int c = 0; c < CC; ++c) st_async_v2f64(map_shared_rank(la, (uint32_t)c), v0, v1, map_shared_rank(lb, (uint32_t)c));
+        }
+        continue;
+      }
+      if (i < 0) continue;
+      // ---- phase 2 (compute warps): block i
+      const int b4 = (int)(i & 3);
+      mbar_wait(&rbar[b4], (uint32_t)((i >> 2) & 1));
+      double tot;
+      {
+        double a[CC];
+#pragma unroll
+        for (int c = 0; c < CC; ++c) a[c] = recv[b4][c][lane & 7];
+#pragma unroll
+        for (int s = 1; s < CC; s *= 2)
+#pragma unroll
+          for (int c = 0; c + s < CC; c += 2 * s) a[c] += a[c + s];
+        tot = a[0];
+      }
+      double T[K::NV];
+#pragma unroll
+      for (int v = 0; v < NRV; ++v) T[v] = __shfl_sync(0xffffffffu, tot, v);
+      const double* gb = gring[i & 31];
+#pragma unroll
+      for (int v = NRV; v < K::NV; ++v) T[v] = gb[v - NRV];
+      if (i > 0) {
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+          double cp = T[K::P(k)], cq = T[K::Q(k)];
+#pragma unroll
+          for (int m = 0; m < B; ++m) {
+            cp = fma(s1p[m], gb[22 + 4 * k + m], cp);
+            cq = fma(s1p[m], gb[38 + 4 * k + m], cq);
+            cq = fma(-s2p[m], gb[54 + 4 * k + m], cq);
+          }
+          T[K::P(k)] = cp;
+          T[K::Q(k)] = cq;
+        }
+      }
+      const int64_t t = p.t0 + i * B;
+      double s1[B], s2[B];
+#pragma unroll
+      for (int k = 0; k < B; ++k) {
+        const RkIdx ix = ring[(t + k) & (RK_RING - 1)];
+        double dw = T[K::P(k)];
+#pragma unroll
+        for (int m = 0; m < k; ++m) dw = fma(s1[m], T[K::AA(k, m)], dw);
+        s1[k] = (ix.bh1 - dw) * ix.rn1;
+        double dr = T[K::Q(k)];
+#pragma unroll
+        for (int m = 0; m < k; ++m) {
+          dr = fma(s1[m], T[K::BA(k, m)], dr);
+          dr = fma(-s2[m], T[K::BB(k, m)], dr);
+        }
+        dr = fma(s1[k], T[K::BA(k, k)], dr);
+        s2[k] = dr * ix.rn2;
+      }
+      const double* cols = slots + (size_t)sl_i * 2 * B * SP;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int e = tid + u * NTc;
 #pragma unroll
         for (int k = 0; k < B; ++k) {
-          acc[K::P(k)] = fma(cols[(2 * k) * SP + e], w[u], acc[K::P(k)]);
-          acc[K::Q(k)] = fma(cols[(2 * k + 1) * SP + e], r[u], acc[K::Q(k)]);
+          const double xa = cols[(2 * k) * SP + e], xb = cols[(2 * k + 1) * SP + e];
+          w[u] = fma(s1[k], xa, w[u]);
+          r[u] = fma(s1[k], xa, r[u]);
+          r[u] = fma(-s2[k], xb, r[u]);
         }
       }
-      const double mine = warp_reduce_scatter<NRV>(acc, lane);   // lane l: warp total of value l & 7
-      if (lane < NRV) wred[nb & 1][warp][lane] = mine;
-    }
-    LAP(helper ? 7 : 0)
-    named_bar_sync(1, NT);   // B1: partials of nb visible; every compute thread finished block i-1
-    LAP(helper ? 4 : 1)
-    if (comm) {
-      if (nb < nblk) {   // send block nb's CTA totals to every rank (lanes 0..3: values 2l, 2l+1)
-        double v = 0.0;
-        for (int w8 = 0; w8 < NWc; ++w8) v += wred[nb & 1][w8][lane & 7];
-        const double v0 = __shfl_sync(0xffffffffu, v, (2 * lane) & 7);
-        const double v1 = __shfl_sync(0xffffffffu, v, (2 * lane + 1) & 7);
-        const int b4 = (int)(nb & 3);
-        const uint32_t la = smem_u32(&recv[b4][rank][2 * (lane & 3)]);
-        const uint32_t lb = smem_u32(&rbar[b4]);
-        if (lane < NRV / 2)
-          for (int c = 0; c < CC; ++c) st_async_v2f64(map_shared_rank(la, (uint32_t)c), v0, v1, map_shared_rank(lb, (uint32_t)c));
-      }
-      LAP(5)
-      // refill the slot of block i-1 (its axpy finished before B1) with block i-1+NS
-      if (i >= 1 && (i - 1) + NS < nblk && lane == 0 && own > 0) issue((i - 1) + NS, (int)((i - 1) % NS));
-      continue;
-    }
-    if (feeder) {
-      LAP(6)
-      // indices + Gram values ahead (visible to the compute warps after the next B1)
-      if (filled_blk < nblk && filled_blk < i + NS + 10) {
-        rk_fill_indices(p, Ss, ring, p.t0 + 4 * filled_blk, lane, bh_tab, rn_tab);
-        la_fill_gram(p, ring, gring, filled_blk, lane);
-        filled_blk += 8;
-      }
-      LAP(7)
-      continue;
-    }
-    if (i < 0) continue;
-    // ---- phase 2 (compute warps): block i
-    const int b4 = (int)(i & 3);
-    mbar_wait_cluster(&rbar[b4], (uint32_t)((i >> 2) & 1));
-    LAP(2)
-    double tot;
-    {
-      double a[CC];
+      if (tid == 0)
 #pragma unroll
-      for (int c = 0; c < CC; ++c) a[c] = recv[b4][c][lane & 7];
-#pragma unroll
-      for (int s = 1; s < CC; s *= 2)
-#pragma unroll
-        for (int c = 0; c + s < CC; c += 2 * s) a[c] += a[c + s];
-      tot = a[0];
-    }
-    double T[K::NV];
-#pragma unroll
-    for (int v = 0; v < NRV; ++v) T[v] = __shfl_sync(0xffffffffu, tot, v);
-    const double* gb = gring[i & 31];
-#pragma unroll
-    for (int v = NRV; v < K::NV; ++v) T[v] = gb[v - NRV];
-    if (i > 0) {   // corrections for block i-1's update (its products used S_{i-1})
+        for (int k = 0; k < B; ++k) zs[ring[(t + k) & (RK_RING - 1)].j2] += s2[k];
 #pragma unroll
       for (int k = 0; k < B; ++k) {
-        double cp = T[K::P(k)], cq = T[K::Q(k)];
+        s1p[k] = s1[k];
+        s2p[k] = s2[k];
+      }
+      named_bar_sync(2, NTc);   // every compute thread read recv[b4] and finished block i's axpy
+      if (tid == 0) {
+        mbar_arrive_expect_tx(&rbar[b4], CC * NRV * 8);   // for block i + 4
+        st_release_cta_s64(&done_s, i + 1);
+      }
+    }
+    if (compute) {
 #pragma unroll
-        for (int m = 0; m < B; ++m) {
-          cp = fma(s1p[m], gb[22 + 4 * k + m], cp);
-          cq = fma(s1p[m], gb[38 + 4 * k + m], cq);
-          cq = fma(-s2p[m], gb[54 + 4 * k + m], cq);
+      for (int u = 0; u < U; ++u) {
+        const int e = tid + u * NTc;
+        if (e < own) {
+          p.W[i0 + e] = w[u];
+          p.Rv[i0 + e] = r[u];
         }
-        T[K::P(k)] = cp;
-        T[K::Q(k)] = cq;
-      }
-    }
-    const int64_t t = p.t0 + i * B;
-    double s1[B], s2[B];
-#pragma unroll
-    for (int k = 0; k < B; ++k) {
-      const RkIdx ix = ring[(t + k) & (RK_RING - 1)];
-      double dw = T[K::P(k)];
-#pragma unroll
-      for (int m = 0; m < k; ++m) dw = fma(s1[m], T[K::AA(k, m)], dw);
-      s1[k] = (ix.bh1 - dw) * ix.rn1;
-      double dr = T[K::Q(k)];
-#pragma unroll
-      for (int m = 0; m < k; ++m) {
-        dr = fma(s1[m], T[K::BA(k, m)], dr);
-        dr = fma(-s2[m], T[K::BB(k, m)], dr);
-      }
-      dr = fma(s1[k], T[K::BA(k, k)], dr);
-      s2[k] = dr * ix.rn2;
-    }
-    const double* cols = slots + (size_t)(i % NS) * 2 * B * SP;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = tid + u * NTc;
-#pragma unroll
-      for (int k = 0; k < B; ++k) {
-        const double xa = cols[(2 * k) * SP + e], xb = cols[(2 * k + 1) * SP + e];
-        w[u] = fma(s1[k], xa, w[u]);
-        r[u] = fma(s1[k], xa, r[u]);
-        r[u] = fma(-s2[k], xb, r[u]);
-      }
-    }
-    if (tid == 0)
-#pragma unroll
-      for (int k = 0; k < B; ++k) zs[ring[(t + k) & (RK_RING - 1)].j2] += s2[k];
-#pragma unroll
-    for (int k = 0; k < B; ++k) {
-      s1p[k] = s1[k];
-      s2p[k] = s2[k];
-    }
-    named_bar_sync(2, NTc);   // every compute thread read recv[b4]
-    if (tid == 0) mbar_arrive_expect_tx(&rbar[b4], CC * NRV * 8);   // for block i + 4
-    LAP(3)
-  }
-#undef LAP
-  if (prof && tid == 0)
-    for (int k = 0; k < 4; ++k) p.prof[rank * 8 + k] += pc[k];
-  if (prof && comm && lane == 0)
-    for (int k = 4; k < 6; ++k) p.prof[rank * 8 + k] += pc[k];
-  if (prof && feeder && lane == 0)
-    for (int k = 6; k < 8; ++k) p.prof[rank * 8 + k] += pc[k];
-  if (!helper) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = tid + u * NTc;
-      if (e < own) {
-        p.W[i0 + e] = w[u];
-        p.Rv[i0 + e] = r[u];
       }
     }
   }
@@ -1428,7 +1445,7 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
   size_t smem_la = 0;
   {
     const char* e = getenv("ILS_RK_LA");
-    if (e && e[0] == '1' && blocked && C == 16 && Bk == 4 && (U == 4 || U == 8) && nt + 64 <= 288 && !h.large &&
+    if (e && e[0] == '1' && blocked && C == 16 && Bk == 4 && (U == 4 || U == 8) && nt + 96 <= 288 && !h.large &&
         !h.sparse) {
       smem_la = smem + (size_t)32 * LA_NG * sizeof(double);
       if (smem_la <= 227 * 1024) {
@@ -1491,7 +1508,7 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
     const int64_t t1 = (t + ce < max_inner) ? t + ce : max_inner;
     p.t0 = t;
     p.t1 = t1;
-    const int r = la ? ((U == 4) ? launch_rkla<16, 4>(h, p, nt + 64, smem_la) : launch_rkla<16, 8>(h, p, nt + 64, smem_la))
+    const int r = la ? ((U == 4) ? launch_rkla<16, 4>(h, p, nt + 96, smem_la) : launch_rkla<16, 8>(h, p, nt + 96, smem_la))
                   : blocked ? dispatch_rkb(h, p, U, Bk, nt, smem)
                             : ((U == 8) ? dispatch_rk_c<8>(h, p, nt, smem) : dispatch_rk_c<4>(h, p, nt, smem));
     if (r) return r;
