@@ -1006,6 +1006,7 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
   __shared__ double bnorm_s;
   __shared__ __align__(8) int64_t filled_s;   // blocks whose index + Gram entries are written
   __shared__ __align__(8) int64_t done_s;     // blocks whose axpy is complete (compute warps)
+  __shared__ double zmail[2][4];              // s2 of the last block, applied to z by the comm warp
 
   for (int64_t j = tid; j < p.npad; j += NT) zs[j] = p.Z[j];
   for (int j = tid; j < p.n; j += NT) {
@@ -1104,8 +1105,25 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
     double s1p[B], s2p[B];
 #pragma unroll
     for (int i = 0; i < B; ++i) s1p[i] = s2p[i] = 0.0;
+    int64_t known_filled = 0;
+    // for the next block: its in-block Gram values and the corrections of its stale-state products,
+    // formed at the end of the previous block (off the path between the exchange and the recurrence)
+    double gin[22], corr[2 * B];
+#pragma unroll
+    for (int v = 0; v < 22; ++v) gin[v] = gring[0][v];
+#pragma unroll
+    for (int v = 0; v < 2 * B; ++v) corr[v] = 0.0;
     int sl_nb = NS - 1, sl_i = NS - 2;
     uint32_t ph_nb = 1;
+    const bool prof = p.prof && tid == 0;
+    long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tc = clock64();
+#define LAP(k)                       \
+  if (prof) {                        \
+    const long long c_ = clock64();  \
+    pc[k] += c_ - tc;                \
+    tc = c_;                         \
+  }
     for (int64_t i = -1; i < nblk; ++i) {
       const int64_t nb = i + 1;
       sl_i = sl_nb;
@@ -1115,10 +1133,14 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
       }
       // ---- phase 1 (compute warps): state products of block nb on S_{nb-1}
       if (compute && nb < nblk) {
-        while (ld_acquire_cta_s64(&filled_s) <= nb + 1) {   // ring + Gram entries of blocks nb, nb+1
-          if (ld_acquire_cta_s64(&filled_s) >= nblk) break;
+        if (known_filled <= nb + 1 && known_filled < nblk) {   // ring + Gram entries of blocks nb, nb+1
+          do {
+            known_filled = ld_acquire_cta_s64(&filled_s);
+          } while (known_filled <= nb + 1 && known_filled < nblk);
         }
+        LAP(7)
         if (own > 0) mbar_wait(&bars[sl_nb], ph_nb);
+        LAP(6)
         const double* cols = slots + (size_t)sl_nb * 2 * B * SP;
         double acc[NRV];
 #pragma unroll
@@ -1135,7 +1157,9 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
         const double mine = warp_reduce_scatter<NRV>(acc, lane);
         if (lane < NRV) wred[nb & 1][warp][lane] = mine;
       }
+      LAP(0)
       named_bar_sync(1, NTc + 32);   // B1: compute warps + communication warp
+      LAP(1)
       if (comm) {
         if (nb < nblk) {
           double v = 0.0;
@@ -1148,12 +1172,18 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
           if (lane < NRV / 2)
             for (int c = 0; c < CC; ++c) st_async_v2f64(map_shared_rank(la, (uint32_t)c), v0, v1, map_shared_rank(lb, (uint32_t)c));
         }
+        if (i >= 1 && lane == 0) {   // z updates of block i - 1 (posted before B1), sequential order
+          const int64_t tp = p.t0 + (i - 1) * B;
+#pragma unroll
+          for (int k = 0; k < B; ++k) zs[ring[(tp + k) & (RK_RING - 1)].j2] += zmail[(i - 1) & 1][k];
+        }
         continue;
       }
       if (i < 0) continue;
       // ---- phase 2 (compute warps): block i
       const int b4 = (int)(i & 3);
       mbar_wait(&rbar[b4], (uint32_t)((i >> 2) & 1));
+      LAP(2)
       double tot;
       {
         double a[CC];
@@ -1167,24 +1197,10 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
       }
       double T[K::NV];
 #pragma unroll
-      for (int v = 0; v < NRV; ++v) T[v] = __shfl_sync(0xffffffffu, tot, v);
-      const double* gb = gring[i & 31];
+      for (int v = 0; v < NRV; ++v) T[v] = __shfl_sync(0xffffffffu, tot, v) + corr[v];
 #pragma unroll
-      for (int v = NRV; v < K::NV; ++v) T[v] = gb[v - NRV];
-      if (i > 0) {
-#pragma unroll
-        for (int k = 0; k < B; ++k) {
-          double cp = T[K::P(k)], cq = T[K::Q(k)];
-#pragma unroll
-          for (int m = 0; m < B; ++m) {
-            cp = fma(s1p[m], gb[22 + 4 * k + m], cp);
-            cq = fma(s1p[m], gb[38 + 4 * k + m], cq);
-            cq = fma(-s2p[m], gb[54 + 4 * k + m], cq);
-          }
-          T[K::P(k)] = cp;
-          T[K::Q(k)] = cq;
-        }
-      }
+      for (int v = NRV; v < K::NV; ++v) T[v] = gin[v - NRV];
+      LAP(3)
       const int64_t t = p.t0 + i * B;
       double s1[B], s2[B];
 #pragma unroll
@@ -1203,6 +1219,29 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
         dr = fma(s1[k], T[K::BA(k, k)], dr);
         s2[k] = dr * ix.rn2;
       }
+      LAP(4)
+      if (i + 1 < nblk) {   // block i+1: corrections with this block's scalars, in-block Gram values
+        if (known_filled <= i + 1 && known_filled < nblk) {
+          do {
+            known_filled = ld_acquire_cta_s64(&filled_s);
+          } while (known_filled <= i + 1 && known_filled < nblk);
+        }
+        const double* gn = gring[(i + 1) & 31];
+#pragma unroll
+        for (int v = 0; v < 22; ++v) gin[v] = gn[v];
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+          double cp = 0.0, cq = 0.0;
+#pragma unroll
+          for (int m = 0; m < B; ++m) {
+            cp = fma(s1[m], gn[22 + 4 * k + m], cp);
+            cq = fma(s1[m], gn[38 + 4 * k + m], cq);
+            cq = fma(-s2[m], gn[54 + 4 * k + m], cq);
+          }
+          corr[K::P(k)] = cp;
+          corr[K::Q(k)] = cq;
+        }
+      }
       const double* cols = slots + (size_t)sl_i * 2 * B * SP;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -1215,9 +1254,10 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
           r[u] = fma(-s2[k], xb, r[u]);
         }
       }
+      LAP(5)
       if (tid == 0)
 #pragma unroll
-        for (int k = 0; k < B; ++k) zs[ring[(t + k) & (RK_RING - 1)].j2] += s2[k];
+        for (int k = 0; k < B; ++k) zmail[i & 1][k] = s2[k];   // the comm warp applies them
 #pragma unroll
       for (int k = 0; k < B; ++k) {
         s1p[k] = s1[k];
@@ -1228,7 +1268,11 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
         mbar_arrive_expect_tx(&rbar[b4], CC * NRV * 8);   // for block i + 4
         st_release_cta_s64(&done_s, i + 1);
       }
+      LAP(5)
     }
+#undef LAP
+    if (prof)
+      for (int k = 0; k < 8; ++k) p.prof[rank * 8 + k] += pc[k];
     if (compute) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -1239,6 +1283,12 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
         }
       }
     }
+  }
+  __syncthreads();
+  if (comm && lane == 0 && nblk >= 1) {   // the last block's z updates
+    const int64_t tp = p.t0 + (nblk - 1) * B;
+#pragma unroll
+    for (int k = 0; k < B; ++k) zs[ring[(tp + k) & (RK_RING - 1)].j2] += zmail[(nblk - 1) & 1][k];
   }
   __syncthreads();
   if (rank == 0)
