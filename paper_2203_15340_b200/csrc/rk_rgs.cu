@@ -901,7 +901,8 @@ __global__ void __launch_bounds__(256, 1) rk_rgs_small_kernel(RkParams p, double
 }
 
 // ---------------------------------------------------------------------------------------------
-// Look-ahead blocked SP-RK-RGS (experiment, ILS_RK_LA=1): the cluster exchange of block i+1 is in
+// Look-ahead blocked SP-RK-RGS (default for 16-CTA clusters; ILS_RK_LA=0 selects rk_rgs_block_kernel):
+// the cluster exchange of block i+1 is in
 // flight while block i's recurrence runs. Block i+1's state products are formed on the state
 // S_i (before block i's update) and corrected after the exchange with block i's scalars and the
 // cross inner products between the two blocks' columns, looked up in A1bar (G):
@@ -1490,12 +1491,13 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
     break;
   }
 
-  // look-ahead variant (ILS_RK_LA=1): one more warp, a 32-block Gram ring in shared memory
+  // look-ahead variant (default for the 16-CTA blocked geometry; ILS_RK_LA=0 disables): three
+  // helper warps and a 32-block Gram ring in shared memory, A1bar built once per handle
   bool la = false;
   size_t smem_la = 0;
   {
     const char* e = getenv("ILS_RK_LA");
-    if (e && e[0] == '1' && blocked && C == 16 && Bk == 4 && (U == 4 || U == 8) && nt + 96 <= 288 && !h.large &&
+    if (!(e && e[0] == '0') && blocked && C == 16 && Bk == 4 && (U == 4 || U == 8) && nt + 96 <= 288 && !h.large &&
         !h.sparse) {
       smem_la = smem + (size_t)32 * LA_NG * sizeof(double);
       if (smem_la <= 227 * 1024) {

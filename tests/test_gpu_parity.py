@@ -244,8 +244,10 @@ def test_rk_fixed_horizon(shape, T):
         assert g == o_ or (n <= 3 and g % ce == 0 and g < o_)
 
 
-def test_rk_cluster_path_c1_horizon():
-    """c1 rows (p = 8000) exercise the 16-CTA cluster/DSMEM kernel with in-kernel checks."""
+def test_rk_cluster_path_c1_horizon(monkeypatch):
+    """c1 rows (p = 8000) exercise the 16-CTA cluster/DSMEM blocked kernel without look-ahead
+    (ILS_RK_LA=0; the look-ahead default is covered by test_rk_lookahead_kernel_c1_horizon)."""
+    monkeypatch.setenv("ILS_RK_LA", "0")
     pr = make_problem("c1")
     K, T, ce = 2, 3000, 1000
     ref = O.sp_rk_rgs_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE, seed=0,
@@ -272,6 +274,24 @@ def test_rk_lookahead_kernel_c1_horizon(monkeypatch):
     x = np.zeros(pr.n)
     with H(pr) as hh:
         o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, seed=1, max_inner=T, check_every=ce, inner_tol=0.0,
+                                 x_hist=hist.ctypes.data)
+        ils.ils_rk_solve(hh.h, None, x, 0.0, K, o)
+    for k in range(K):
+        assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
+
+
+@pytest.mark.parametrize("T,ce", [(1, 1000), (5, 3), (7, 4), (130, 64)])
+def test_rk_cluster_short_horizons(T, ce):
+    """16-CTA cluster path (p = 8000) at short / ragged horizons and check intervals: partial last
+    blocks, a horizon shorter than the TMA ring, checks inside a block of 4 steps."""
+    pr = make_dense(8000, 400, 300, 0.5, seed=47)
+    K = 2
+    ref = O.sp_rk_rgs_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE, seed=2, max_inner=T,
+                            check_every=ce, inner_tol=0.0)
+    hist = np.zeros((K, pr.n))
+    x = np.zeros(pr.n)
+    with H(pr) as hh:
+        o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, seed=2, max_inner=T, check_every=ce, inner_tol=0.0,
                                  x_hist=hist.ctypes.data)
         ils.ils_rk_solve(hh.h, None, x, 0.0, K, o)
     for k in range(K):
