@@ -167,7 +167,7 @@ ILS_API const char* ils_last_error(void);
  * CSR input (ext->format = ILS_FORMAT_CSR): the CSR arrays are validated (ILS_ERR_ARG on an
  * out-of-range / unsorted / duplicated column, a bad row pointer or a non-finite value) and
  * converted to CSC for A1 and A2 (columns sorted by row). SP forms A1^T A1 densely (n <= 29000);
- * SP-SCD uses it compacted to CSR; sp_form = 1 and the weighted SP-RCD mode return
+ * SP-SCD/RCD use it compacted to CSR; sp_form = 2 (explicit B = P A2bar) returns
  * ILS_ERR_UNSUPPORTED for CSR input in this release. */
 ILS_API int ils_create(ils_handle* h, const double* A, const double* b,
                int64_t p, int64_t q, int64_t n, const ils_ext* ext);

@@ -557,8 +557,8 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
     set_error("solve: sp_form must be 0 or 2 (RK/RGS), 0..2 (SP)");
     return ILS_ERR_ARG;
   }
-  if (H.sparse && (o.sp_form != 0 || (method == 2 && o.weighted))) {
-    set_error("CSR input: sp_form 1/2 and weighted SP-RCD are not implemented in this release");
+  if (H.sparse && o.sp_form == 2) {
+    set_error("CSR input: sp_form 2 (explicit B = P A2bar) is not implemented in this release");
     return ILS_ERR_UNSUPPORTED;
   }
   const bool sharded = H.comm != nullptr;
@@ -651,8 +651,8 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
         hot_account(H, 0, 8.0 * (double)n * (double)n);
       } else if (method == 0 && (H.sparse || big || sharded)) {   // c_k by row/column passes, x = P c_k (+ x_k)
         ILS_CU(cudaEventRecord(H.evk0, st));
-        if (H.sparse) {
-          if ((rc = sparse_rhs(H, xk, bhat, 0))) return rc;
+        if (H.sparse) {   // paper form c_k, or the correction form's g_k = A^T J (b - A x_k)
+          if ((rc = sparse_rhs(H, xk, bhat, o.sp_form == 1))) return rc;
         } else if (big) {
           if ((rc = dense_rhs_twopass(H, xk, bhat, o.sp_form == 1))) return rc;
         } else if ((rc = sp_run(H, xk, nullptr, 0.0, 1, ILS_STOP_NONE, nullptr, o.sp_form, nullptr, true, bhat,
@@ -661,10 +661,13 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
         }
         if ((rc = allreduce_sum(H, bhat, np))) return rc;   // sharded: sum of the ranks' partial c_k / g_k
         if ((rc = gemv_p(H, bhat, xnew))) return rc;
-        if ((big || sharded) && o.sp_form == 1 && (rc = vec_add(H, xnew, xk, n))) return rc;
+        if ((big || sharded || H.sparse) && o.sp_form == 1 && (rc = vec_add(H, xnew, xk, n))) return rc;
         ILS_CU(cudaEventRecord(H.evk1, st));
-        if (H.sparse)
-          hot_account(H, 0, 12.0 * (double)(H.nnz - H.nnz1) + 16.0 * (double)H.q + 8.0 * (double)np * (double)np, 2);
+        if (H.sparse)   // row pass + column pass over A2 (all of A, twice, under the correction form) + P
+          hot_account(H, 0, (o.sp_form == 1 ? 24.0 * (double)H.nnz + 16.0 * (double)H.m
+                                            : 24.0 * (double)(H.nnz - H.nnz1) + 16.0 * (double)H.q) +
+                                8.0 * (double)np * (double)np,
+                      o.sp_form == 1 ? 5 : 2);
         else   // two passes over A2 (or all of A under the correction form) + the P sweep
           hot_account(H, 0, 16.0 * (double)(o.sp_form == 1 ? H.m : H.q) * (double)n + 8.0 * (double)np * (double)np,
                       o.sp_form == 1 ? 5 : 3);
@@ -691,7 +694,7 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
                         : rk_rgs_inner(H, bhat, xnew, o.seed, k, o.max_inner, o.check_every, o.inner_tol, &steps);
         else
           rc = H.sparse ? sparse_scd_inner(H, bhat, xnew, o.seed, k, o.max_inner, o.check_every, o.inner_tol,
-                                           o.alpha_mode, o.alpha_k, &steps)
+                                           o.alpha_mode, o.alpha_k, o.weighted, &steps)
                         : scd_inner(H, bhat, xnew, o.seed, k, o.max_inner, o.check_every, o.inner_tol, o.alpha_mode,
                                     o.alpha_k, o.weighted, &steps);
         if (rc) return rc;
@@ -738,7 +741,8 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
     rep->solve_ms = solve_ms;
     const double q = (double)H.q, p = (double)H.p, nd = (double)n;
     if (H.sparse) {   // algorithmic bytes of the sparse path (12 B per CSR/CSC entry)
-      const double a2 = 12.0 * (double)(H.nnz - H.nnz1) * 2.0 + 16.0 * q;
+      const double a2 = (method == 0 && o.sp_form == 1) ? 24.0 * (double)H.nnz + 16.0 * (double)H.m
+                                                        : 12.0 * (double)(H.nnz - H.nnz1) * 2.0 + 16.0 * q;
       const double rk_step = 2.0 * ((double)H.nnz1 / nd) * 28.0;
       const double scd_step = 12.0 * ((double)H.gnnz / nd);
       rep->bytes_touched = outer * a2 + (method == 0 ? outer * 8.0 * (double)np * (double)np

@@ -187,7 +187,7 @@ int gemv_p(Handle& h, const double* c, double* x);
 int sparse_rk_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_t k, int64_t max_inner,
                     int64_t check_every, double inner_tol, int64_t* steps_out);
 int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_t k, int64_t max_inner,
-                     int64_t check_every, double inner_tol, int alpha_mode, int alpha_k, int64_t* steps_out);
+                     int64_t check_every, double inner_tol, int alpha_mode, int alpha_k, int weighted, int64_t* steps_out);
 // scd.cu: membership masks of steps [t0, t1) for NT threads x V coordinates
 int scd_masks(Handle& h, uint64_t seed, int64_t k, int64_t t0, int64_t t1, int alpha_mode, int alpha_k, int NT, int V,
               uint32_t* masks);

@@ -469,11 +469,8 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
               int64_t check_every, double inner_tol, int alpha_mode, int alpha_k, int weighted,
               int64_t* steps_out) {
   if (h.large || h.npad > 32 * SCD_DEFT) {   // large n: r in shared memory, dense A1bar rows (sparse.cu kernel)
-    if (weighted) {
-      set_error("SP-RCD: n > 8192 is not implemented in this release");
-      return ILS_ERR_UNSUPPORTED;
-    }
-    return sparse_scd_inner(h, bhat, beta, seed, k, max_inner, check_every, inner_tol, alpha_mode, alpha_k, steps_out);
+    return sparse_scd_inner(h, bhat, beta, seed, k, max_inner, check_every, inner_tol, alpha_mode, alpha_k, weighted,
+                            steps_out);
   }
   int rc = build_gram(h);
   if (rc) return rc;

@@ -859,11 +859,22 @@ struct SpScdParams {
   const uint32_t* masks;   // [t1 - t0][NT] (V coordinates per thread, s = tid + v*NT)
   int V;
   int all_members;         // alpha_t = n every step (Motzkin): no masks
+  const int32_t* jw;       // weighted SP-RCD: j_t for t in [t0, t1) (rcd_index_kernel), else null
   int64_t t0, t1;
   DevStatus* st;
 };
 
 constexpr int SSCD_T = 1024;
+
+// SP-RCD: j_t drawn from the column-norm weights, one thread per step of the
+// chunk, the same draw (tag kTagRcd) and integer inverse-CDF as the one-CTA kernel (scd.cu)
+__global__ void rcd_index_kernel(uint64_t seed, uint32_t k, int64_t t0, int64_t t1, int n,
+                                 const uint64_t* __restrict__ S, int32_t* __restrict__ J) {
+  const int64_t u = t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= t1) return;
+  const U4 x = draw(seed, k, (uint64_t)u, kTagRcd);
+  J[u - t0] = sample_weighted(((uint64_t)x.y << 32) | x.x, S, n);
+}
 
 __global__ void __launch_bounds__(SSCD_T, 1) sparse_scd_kernel(SpScdParams p) {
   extern __shared__ __align__(16) double rs[];     // [npad] r
@@ -893,6 +904,32 @@ __global__ void __launch_bounds__(SSCD_T, 1) sparse_scd_kernel(SpScdParams p) {
     }
   }
   __syncthreads();
+  if (p.jw) {   // weighted: j_t is data-independent, r_j read from the shared residual, no argmax
+    const int64_t L = p.t1 - p.t0;
+    int j0 = __ldcg(p.jw), j1 = (L > 1) ? __ldcg(p.jw + 1) : 0;
+    double n0 = p.N[j0];
+    for (int64_t u = 0; u < L; ++u) {
+      const int j = j0;
+      const double sc = rs[j] / n0;
+      j0 = j1;
+      n0 = p.N[j0];
+      j1 = (u + 2 < L) ? __ldcg(p.jw + u + 2) : 0;
+      __syncthreads();   // every thread has read r_j before any update of it
+      if (p.Gd) {
+        const double* grow = p.Gd + (int64_t)j * p.npad;
+        for (int c = tid; c < n; c += SSCD_T) rs[c] = fma(-sc, __ldcg(grow + c), rs[c]);
+      } else {
+        for (int64_t e = p.gp[j] + tid; e < p.gp[j + 1]; e += SSCD_T) {
+          const int c = p.gc[e];
+          rs[c] = fma(-sc, p.gv[e], rs[c]);
+        }
+      }
+      if (tid == 0) atomicAdd(p.Bv + j, sc);
+      __syncthreads();
+    }
+    for (int s2 = tid; s2 < n; s2 += SSCD_T) p.Rv[s2] = rs[s2];
+    return;
+  }
   const uint32_t* mk = p.masks + tid;
   uint32_t allbits = 0;
   for (int v = 0; v < V; ++v)
@@ -1236,7 +1273,8 @@ __global__ void __launch_bounds__(256) sparse_scd_check_kernel(const double* __r
 }
 
 int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_t k, int64_t max_inner,
-                     int64_t check_every, double inner_tol, int alpha_mode, int alpha_k, int64_t* steps_out) {
+                     int64_t check_every, double inner_tol, int alpha_mode, int alpha_k, int weighted,
+                     int64_t* steps_out) {
   // CSR input: A1bar compacted to CSR; dense input with large n: the dense A1bar rows
   int rc = h.sparse ? sparse_gram_csr(h) : build_gram(h);
   if (rc) return rc;
@@ -1250,7 +1288,7 @@ int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed,
   const int64_t chunk_cap = (max_inner < ce) ? max_inner : ce;
   // dense A1bar rows (large n): the 16-CTA cluster kernel (one or two coordinates per thread)
   const char* ecl = getenv("ILS_SCD_CLUSTER");
-  const bool cl = !h.sparse && h.n <= 8 * SCDC_C * SCDC_T && !(ecl && ecl[0] == '0');
+  const bool cl = !weighted && !h.sparse && h.n <= 8 * SCDC_C * SCDC_T && !(ecl && ecl[0] == '0');
   const int Vc = (h.n <= 4 * SCDC_C * SCDC_T) ? 4 : 8;
   const int mask_threads = cl ? SCDC_C * SCDC_T : SSCD_T;
   const size_t need = ((size_t)3 * h.npad + 2 * (size_t)h.num_sms) * sizeof(double) +
@@ -1285,6 +1323,7 @@ int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed,
   prm.masks = masks;
   prm.V = V;
   prm.all_members = (alpha_mode == ILS_ALPHA_FIXED && alpha_k >= h.n) ? 1 : 0;
+  prm.jw = weighted ? reinterpret_cast<const int32_t*>(masks) : nullptr;   // chunk_cap <= the mask space
   prm.st = h.dstat;
   const size_t smem = (size_t)h.npad * sizeof(double);
   ILS_CU(cudaFuncSetAttribute(sparse_scd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1301,9 +1340,14 @@ int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed,
   int pending = 0;
   while (t < max_inner) {
     const int64_t t1 = (t + ce < max_inner) ? t + ce : max_inner;
-    if (!prm.all_members &&
-        (rc = scd_masks(h, seed, k, t, t1, alpha_mode, alpha_k, mask_threads, cl ? Vc : V, masks)))
+    if (weighted) {
+      rcd_index_kernel<<<(unsigned)((t1 - t + 255) / 256), 256, 0, st>>>(seed, (uint32_t)k, t, t1, (int)h.n, h.S,
+                                                                           reinterpret_cast<int32_t*>(masks));
+      ILS_LAUNCHED("rcd_index_kernel");
+    } else if (!prm.all_members &&
+               (rc = scd_masks(h, seed, k, t, t1, alpha_mode, alpha_k, mask_threads, cl ? Vc : V, masks))) {
       return rc;
+    }
     prm.t0 = t;
     prm.t1 = t1;
     if (cl) {

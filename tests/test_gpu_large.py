@@ -94,20 +94,21 @@ def test_large_rk_fixed_horizon(shape, T, ce, itol, monkeypatch):
 
 
 @pytest.mark.parametrize("shape", SHAPES)
-@pytest.mark.parametrize("mode", [(0, 1), (1, 1), (1, 5), (1, 10 ** 6)])
+@pytest.mark.parametrize("mode", [(0, 1, 0), (1, 1, 0), (1, 5, 0), (1, 10 ** 6, 0), (1, 1, 1)])
 def test_large_scd_fixed_horizon(shape, mode, monkeypatch):
+    """(alpha_mode, alpha_k, weighted): weighted = 1 is SP-RCD (PAPER.md:460-475)."""
     p, q, n, s = shape
     pr = make_dense(p, q, n, s, seed=34)
-    amode, ak = mode
+    amode, ak, wt = mode
     K, T, ce = 3, 300, 40
     ref = O.sp_scd_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE, seed=9, max_inner=T,
-                         check_every=ce, inner_tol=1e-9, alpha_mode=amode, alpha_fixed=ak)
+                         check_every=ce, inner_tol=1e-9, alpha_mode=amode, alpha_fixed=ak, weighted=bool(wt))
     hist = np.zeros((K, n))
     inner = np.zeros(K, dtype=np.int64)
     x = np.zeros(n)
     with Big(pr, monkeypatch) as hh:
         o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, seed=9, max_inner=T, check_every=ce, inner_tol=1e-9,
-                                 alpha_mode=amode, alpha_k=min(ak, 2 ** 31 - 1), x_hist=hist.ctypes.data,
+                                 alpha_mode=amode, alpha_k=min(ak, 2 ** 31 - 1), weighted=wt, x_hist=hist.ctypes.data,
                                  inner_hist=inner.ctypes.data)
         ils.ils_rgs_solve(hh.h, None, x, 0.0, K, o)
     assert list(inner) == list(ref.inner_hist)
@@ -128,7 +129,7 @@ def test_large_methods_converge(monkeypatch):
 
 def test_large_real_n_above_8192(monkeypatch):
     """A dense problem with n = 8300 (> 8192, npad 8320) on the default routing: SP (both forms),
-    SP-RK-RGS and SP-SCD at short fixed horizons against the oracle."""
+    SP-RK-RGS, SP-SCD and SP-RCD at short fixed horizons against the oracle."""
     p, q, n = 8700, 300, 8300
     pr = make_dense(p, q, n, 0.3, seed=36)
     monkeypatch.delenv("ILS_FORCE_LARGE", raising=False)
@@ -138,11 +139,14 @@ def test_large_real_n_above_8192(monkeypatch):
                                check_every=100, inner_tol=0.0)
     ref_scd = O.sp_scd_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE, seed=2, max_inner=400,
                              check_every=100, inner_tol=0.0, alpha_mode=1, alpha_fixed=64)
+    ref_rcd = O.sp_scd_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE, seed=2, max_inner=400,
+                             check_every=100, inner_tol=0.0, weighted=True)
     with Big(pr) as hh:
         for fn, ref, kw in ((ils.ils_sp_solve, ref_sp, {}), (ils.ils_sp_solve, ref_sp, {"sp_form": 1}),
                             (ils.ils_rk_solve, ref_rk, {"max_inner": 400, "check_every": 100}),
                             (ils.ils_rgs_solve, ref_scd, {"max_inner": 400, "check_every": 100, "alpha_mode": 1,
-                                                          "alpha_k": 64})):
+                                                          "alpha_k": 64}),
+                            (ils.ils_rgs_solve, ref_rcd, {"max_inner": 400, "check_every": 100, "weighted": 1})):
             hist = np.zeros((K, n))
             x = np.zeros(n)
             o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, seed=2, inner_tol=0.0, x_hist=hist.ctypes.data, **kw)

@@ -81,16 +81,19 @@ def test_sparse_direct_solve_and_rr(shape):
 
 
 @pytest.mark.parametrize("shape", SHAPES)
-def test_sparse_sp_fixed_horizon(shape):
+@pytest.mark.parametrize("form", [0, 1])
+def test_sparse_sp_fixed_horizon(shape, form):
+    """form 0: the paper's x_{k+1} = P (A1^T b1 + A2^T (A2 x_k - b2)); form 1: the correction form
+    x_{k+1} = x_k + P A^T J (b - A x_k) (DESIGN.md readings)."""
     p, q, n, k = shape
     pr = make_sparse(p, q, n, k, seed=13)
     A1, A2, b1, b2 = _dense(pr)
     K = 6
-    ref = O.sp_solve(A1, A2, b1, b2, max_iter=K, stop=O.STOP_NONE)
+    ref = O.sp_solve(A1, A2, b1, b2, max_iter=K, stop=O.STOP_NONE, sp_form=form)
     hist = np.zeros((K, n))
     x = np.zeros(n)
     with HS(pr) as hh:
-        o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, x_hist=hist.ctypes.data)
+        o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, sp_form=form, x_hist=hist.ctypes.data)
         st, rep = ils.ils_sp_solve(hh.h, None, x, 0.0, K, o)
     assert rep.outer_iters == K
     for kk in range(K):
@@ -108,7 +111,7 @@ def test_sparse_sp_rr_stop_and_unsupported_modes():
         assert rep.converged and rep.final_metric < 1e-12
         assert abs(rep.outer_iters - ref.outer_iters) <= 1
         with pytest.raises(ils.IlsError) as e:
-            ils.ils_sp_solve(hh.h, None, x, 1e-12, 5, ils.ils_default_opts(stop=ils.ILS_STOP_NONE, sp_form=1))
+            ils.ils_sp_solve(hh.h, None, x, 1e-12, 5, ils.ils_default_opts(stop=ils.ILS_STOP_NONE, sp_form=2))
         assert e.value.status == ils.ILS_ERR_UNSUPPORTED
 
 
@@ -131,22 +134,36 @@ def test_sparse_rk_fixed_horizon(T):
     assert list(inner) == list(ref.inner_hist)
 
 
-@pytest.mark.parametrize("mode", [(0, 1), (1, 1), (1, 5), (1, 10 ** 6)])
+@pytest.mark.parametrize("mode", [(0, 1, 0), (1, 1, 0), (1, 5, 0), (1, 10 ** 6, 0), (1, 1, 1)])
 def test_sparse_scd_fixed_horizon(mode):
+    """(alpha_mode, alpha_k, weighted): weighted = 1 is SP-RCD (PAPER.md:460-475)."""
     pr = make_sparse(600, 120, 80, 6, seed=16)
     A1, A2, b1, b2 = _dense(pr)
-    amode, ak = mode
+    amode, ak, wt = mode
     K, T, ce = 3, 300, 40
     ref = O.sp_scd_solve(A1, A2, b1, b2, max_iter=K, stop=O.STOP_NONE, seed=9, max_inner=T, check_every=ce,
-                         inner_tol=0.0, alpha_mode=amode, alpha_fixed=ak)
+                         inner_tol=0.0, alpha_mode=amode, alpha_fixed=ak, weighted=bool(wt))
     hist = np.zeros((K, pr.n))
+    inner = np.zeros(K, dtype=np.int64)
     x = np.zeros(pr.n)
     with HS(pr) as hh:
         o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, seed=9, max_inner=T, check_every=ce, inner_tol=0.0,
-                                 alpha_mode=amode, alpha_k=min(ak, 2 ** 31 - 1), x_hist=hist.ctypes.data)
+                                 alpha_mode=amode, alpha_k=min(ak, 2 ** 31 - 1), weighted=wt,
+                                 x_hist=hist.ctypes.data, inner_hist=inner.ctypes.data)
         ils.ils_rgs_solve(hh.h, None, x, 0.0, K, o)
+    assert list(inner) == list(ref.inner_hist)
     for kk in range(K):
         assert _rel(hist[kk], ref.x_hist[kk]) <= 1e-9, kk
+
+
+def test_sparse_rcd_converges():
+    """Weighted SP-RCD on CSR input reaches the planted solution (consistent system)."""
+    pr = make_sparse(800, 160, 60, 6, seed=19, noise=0.0)
+    x = np.zeros(pr.n)
+    with HS(pr) as hh:
+        o = ils.ils_default_opts(x_ref=pr.xstar.ctypes.data, inner_tol=1e-12, max_inner=400000, weighted=1)
+        st, rep = ils.ils_rgs_solve(hh.h, None, x, 1e-10, 200, o)
+    assert st == ils.ILS_OK and _rel(x, pr.xstar) <= 1e-10
 
 
 def test_sparse_methods_converge():
