@@ -908,32 +908,43 @@ __global__ void __launch_bounds__(256, 1) rk_rgs_small_kernel(RkParams p, double
 // cross inner products between the two blocks' columns, looked up in A1bar (G):
 //   <a1'_k, w_{i+1}> = <a1'_k, w_i> + sum_m s1_m <a1'_k, a1_m>
 //   <a2'_k, r_{i+1}> = <a2'_k, r_i> + sum_m s1_m <a2'_k, a1_m> - sum_m s2_m <a2'_k, a2_m>
-// The 22 in-block column products also come from G, so only 8 values per block are reduced. The
-// last warp of the CTA is a communication warp: it sums the compute warps' partials, sends them
-// to the cluster (destination-uniform st.async), refills the TMA ring and fills the index / Gram
-// ring ahead; the compute warps never issue a send.
-constexpr int LA_NG = 70;   // Gram values per block: 22 in-block (RkBlk<4> order) + 48 cross
+// The 22 in-block column products also come from G, so only 8 values per block are reduced. A
+// communication warp sums the compute warps' partials and sends them to the cluster
+// (destination-uniform st.async) as soon as they are deposited; a reduce warp sums the 16
+// received partials of block i, adds the corrections with block i-1's scalars (mailed by the
+// compute warps) and hands the 8 finished products to the compute warps through an mbarrier, so
+// the compute warps' own path per block is products -> recurrence -> axpy. A fill warp and a TMA
+// warp run ahead (index / Gram rings, column refills); the compute warps never issue a send.
+constexpr int LA_GR = 16;    // blocks in the Gram ring (the fill warp runs at most LA_GR blocks ahead)
+constexpr int LA_NG = 118;   // Gram values per block: 22 in-block (RkBlk<4> order) + 48 with block - 1 + 48 with block - 2
 
-// (value v of a block) -> (step of the current block, its column, step of the same / previous block,
-// its column): 22 in-block products in RkBlk<4> order, then X1, X2, X3 (4 x 4 each) with block - 1
-__constant__ int8_t la_map[LA_NG][4] = {
+// (value v of a block) -> (step of the current block, its column, step relative to the block start
+// (negative: an earlier block), its column): 22 in-block products in RkBlk<4> order, then X1, X2,
+// X3 (4 x 4 each) with block - 1 and the same three with block - 2
+__constant__ __align__(4) int8_t la_map[LA_NG][4] = {
     {1, 0, 0, 0}, {2, 0, 0, 0}, {2, 0, 1, 0}, {3, 0, 0, 0}, {3, 0, 1, 0}, {3, 0, 2, 0},                       // AA
     {0, 1, 0, 0}, {1, 1, 0, 0}, {1, 1, 1, 0}, {2, 1, 0, 0}, {2, 1, 1, 0}, {2, 1, 2, 0}, {3, 1, 0, 0},
     {3, 1, 1, 0}, {3, 1, 2, 0}, {3, 1, 3, 0},                                                               // BA
     {1, 1, 0, 1}, {2, 1, 0, 1}, {2, 1, 1, 1}, {3, 1, 0, 1}, {3, 1, 1, 1}, {3, 1, 2, 1},                       // BB
-    {0, 0, -4, 0}, {0, 0, -3, 0}, {0, 0, -2, 0}, {0, 0, -1, 0}, {1, 0, -4, 0}, {1, 0, -3, 0}, {1, 0, -2, 0},
-    {1, 0, -1, 0}, {2, 0, -4, 0}, {2, 0, -3, 0}, {2, 0, -2, 0}, {2, 0, -1, 0}, {3, 0, -4, 0}, {3, 0, -3, 0},
-    {3, 0, -2, 0}, {3, 0, -1, 0},                                                                           // X1
-    {0, 1, -4, 0}, {0, 1, -3, 0}, {0, 1, -2, 0}, {0, 1, -1, 0}, {1, 1, -4, 0}, {1, 1, -3, 0}, {1, 1, -2, 0},
-    {1, 1, -1, 0}, {2, 1, -4, 0}, {2, 1, -3, 0}, {2, 1, -2, 0}, {2, 1, -1, 0}, {3, 1, -4, 0}, {3, 1, -3, 0},
-    {3, 1, -2, 0}, {3, 1, -1, 0},                                                                           // X2
-    {0, 1, -4, 1}, {0, 1, -3, 1}, {0, 1, -2, 1}, {0, 1, -1, 1}, {1, 1, -4, 1}, {1, 1, -3, 1}, {1, 1, -2, 1},
-    {1, 1, -1, 1}, {2, 1, -4, 1}, {2, 1, -3, 1}, {2, 1, -2, 1}, {2, 1, -1, 1}, {3, 1, -4, 1}, {3, 1, -3, 1},
-    {3, 1, -2, 1}, {3, 1, -1, 1}};                                                                          // X3
+    {0, 0, -4, 0}, {0, 0, -3, 0}, {0, 0, -2, 0}, {0, 0, -1, 0}, {1, 0, -4, 0}, {1, 0, -3, 0}, {1, 0, -2, 0}, {1, 0, -1, 0},
+    {2, 0, -4, 0}, {2, 0, -3, 0}, {2, 0, -2, 0}, {2, 0, -1, 0}, {3, 0, -4, 0}, {3, 0, -3, 0}, {3, 0, -2, 0}, {3, 0, -1, 0},   // X1 (block - 1)
+    {0, 1, -4, 0}, {0, 1, -3, 0}, {0, 1, -2, 0}, {0, 1, -1, 0}, {1, 1, -4, 0}, {1, 1, -3, 0}, {1, 1, -2, 0}, {1, 1, -1, 0},
+    {2, 1, -4, 0}, {2, 1, -3, 0}, {2, 1, -2, 0}, {2, 1, -1, 0}, {3, 1, -4, 0}, {3, 1, -3, 0}, {3, 1, -2, 0}, {3, 1, -1, 0},   // X2 (block - 1)
+    {0, 1, -4, 1}, {0, 1, -3, 1}, {0, 1, -2, 1}, {0, 1, -1, 1}, {1, 1, -4, 1}, {1, 1, -3, 1}, {1, 1, -2, 1}, {1, 1, -1, 1},
+    {2, 1, -4, 1}, {2, 1, -3, 1}, {2, 1, -2, 1}, {2, 1, -1, 1}, {3, 1, -4, 1}, {3, 1, -3, 1}, {3, 1, -2, 1}, {3, 1, -1, 1},   // X3 (block - 1)
+    {0, 0, -8, 0}, {0, 0, -7, 0}, {0, 0, -6, 0}, {0, 0, -5, 0}, {1, 0, -8, 0}, {1, 0, -7, 0}, {1, 0, -6, 0}, {1, 0, -5, 0},
+    {2, 0, -8, 0}, {2, 0, -7, 0}, {2, 0, -6, 0}, {2, 0, -5, 0}, {3, 0, -8, 0}, {3, 0, -7, 0}, {3, 0, -6, 0}, {3, 0, -5, 0},   // X1' (block - 2)
+    {0, 1, -8, 0}, {0, 1, -7, 0}, {0, 1, -6, 0}, {0, 1, -5, 0}, {1, 1, -8, 0}, {1, 1, -7, 0}, {1, 1, -6, 0}, {1, 1, -5, 0},
+    {2, 1, -8, 0}, {2, 1, -7, 0}, {2, 1, -6, 0}, {2, 1, -5, 0}, {3, 1, -8, 0}, {3, 1, -7, 0}, {3, 1, -6, 0}, {3, 1, -5, 0},   // X2' (block - 2)
+    {0, 1, -8, 1}, {0, 1, -7, 1}, {0, 1, -6, 1}, {0, 1, -5, 1}, {1, 1, -8, 1}, {1, 1, -7, 1}, {1, 1, -6, 1}, {1, 1, -5, 1},
+    {2, 1, -8, 1}, {2, 1, -7, 1}, {2, 1, -6, 1}, {2, 1, -5, 1}, {3, 1, -8, 1}, {3, 1, -7, 1}, {3, 1, -6, 1}, {3, 1, -5, 1}    // X3' (block - 2)
+};
 
 // Gram values of 8 blocks from blk0 (one warp): all loads issued before any store
+// (map: la_map copied to shared memory -- lanes read different rows, which the constant cache
+// would serialise)
 __device__ __forceinline__ void la_fill_gram(const RkParams& p, const RkIdx* ring, double (*gring)[LA_NG],
-                                             int64_t blk0, int lane) {
+                                             const int8_t (*map)[4], int64_t blk0, int lane) {
   __syncwarp();
   constexpr int PER = (8 * LA_NG + 31) / 32;
   double val[PER];
@@ -945,8 +956,8 @@ __device__ __forceinline__ void la_fill_gram(const RkParams& p, const RkIdx* rin
       const int bl = e / LA_NG, v = e - bl * LA_NG;
       const int64_t b = blk0 + bl;
       const int64_t tb = p.t0 + 4 * b;
-      const int sa = la_map[v][0], ca = la_map[v][1], sb = la_map[v][2], cb = la_map[v][3];
-      if (v < 22 || b > 0) {
+      const int sa = map[v][0], ca = map[v][1], sb = map[v][2], cb = map[v][3];
+      if (v < 22 || 4 * b + sb >= 0) {   // the earlier block exists in this launch
         const RkIdx ea = ring[(tb + sa) & (RK_RING - 1)];
         const RkIdx ebb = ring[(tb + sb) & (RK_RING - 1)];
         const int ja = ca ? ea.j2 : ea.j1, jb = cb ? ebb.j2 : ebb.j1;
@@ -959,7 +970,7 @@ __device__ __forceinline__ void la_fill_gram(const RkParams& p, const RkIdx* rin
     const int e = lane + 32 * q;
     if (e < 8 * LA_NG) {
       const int bl = e / LA_NG, v = e - bl * LA_NG;
-      gring[(blk0 + bl) & 31][v] = val[q];
+      gring[(blk0 + bl) & (LA_GR - 1)][v] = val[q];
     }
   }
 }
@@ -973,18 +984,20 @@ __device__ __forceinline__ void st_release_cta_s64(int64_t* a, int64_t v) {
   asm volatile("st.release.cta.shared::cta.s64 [%0], %1;" ::"r"(smem_u32(a)), "l"(v) : "memory");
 }
 
-// Warp roles: NWc compute warps (rows), a communication warp (sends the block partials), a fill
-// warp (index + Gram rings ahead) and a TMA warp (column refills). Only compute + communication
-// warps meet at a named barrier per block; the fill and TMA warps run ahead, throttled by progress
-// counters in shared memory (release / acquire), so their long operations never stall the step.
+// Warp roles: NWc compute warps (rows), a communication warp (sends the block partials), a reduce
+// warp (cluster sum + corrections -> finished products), a fill warp (index + Gram rings ahead)
+// and a TMA warp (column refills). Compute, communication and reduce warps meet at a named barrier
+// per block; the fill and TMA warps run ahead, throttled by progress counters in shared memory
+// (release / acquire), so their long operations never stall the step.
 template <int CC, int U>
-__global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
+__global__ void __launch_bounds__(320, 1) rk_rgs_la_kernel(RkParams p) {
   constexpr int B = 4, NRV = 8;
+  static_assert(CC == 16, "the communication warp's cluster sum is written for 16 sources");
   using K = RkBlk<B>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int NT = blockDim.x, NW = NT >> 5, NWc = NW - 3, NTc = NWc * 32;
-  const bool comm = (warp == NWc), filler = (warp == NWc + 1), tmaw = (warp == NWc + 2);
+  const int NT = blockDim.x, NW = NT >> 5, NWc = NW - 4, NTc = NWc * 32;
+  const bool comm = (warp == NWc), reducer = (warp == NWc + 1), filler = (warp == NWc + 2), tmaw = (warp == NWc + 3);
   const bool compute = warp < NWc;
   const int rank = (int)cluster_ctarank();
   const int64_t i0 = (int64_t)rank * p.slice;
@@ -999,15 +1012,20 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + RK_RING);        // [NS]
   double* bh_tab = reinterpret_cast<double*>(bars + 8);                 // [n]
   double* rn_tab = bh_tab + ((p.n + 1) & ~1);                          // [n]
-  double (*gring)[LA_NG] = reinterpret_cast<double (*)[LA_NG]>(rn_tab + ((p.n + 1) & ~1));   // [32][70]
+  double (*gring)[LA_NG] = reinterpret_cast<double (*)[LA_NG]>(rn_tab + ((p.n + 1) & ~1));   // [LA_GR][LA_NG]
   __shared__ __align__(16) double wred[2][8][8];
-  __shared__ __align__(16) double recv[4][RK_MAXC][NRV];
-  __shared__ __align__(8) uint64_t rbar[4];
+  __shared__ __align__(16) double recv[8][RK_MAXC][NRV];   // block b in buffer b & 7 (sent two blocks ahead)
+  __shared__ __align__(8) uint64_t rbar[8];
   __shared__ double chkw[12];
   __shared__ double bnorm_s;
   __shared__ __align__(8) int64_t filled_s;   // blocks whose index + Gram entries are written
   __shared__ __align__(8) int64_t done_s;     // blocks whose axpy is complete (compute warps)
-  __shared__ double zmail[2][4];              // s2 of the last block, applied to z by the comm warp
+  __shared__ double smail[4][8];              // s1 (0..3), s2 (4..7) of block i, slot i & 3 (compute -> comm, reduce)
+  __shared__ double tsm[2][8];                // finished state products of block i, slot i & 1 (comm -> compute)
+  __shared__ __align__(8) uint64_t tbar[2];   // tsm[s] written (one arrival by the reduce warp)
+  __shared__ __align__(8) uint64_t sbar[2];   // smail of block b posted (one arrival by compute thread 0), slot b & 1
+  __shared__ __align__(4) int8_t lam[LA_NG][4];
+  if (tid < LA_NG) *reinterpret_cast<int32_t*>(lam[tid]) = *reinterpret_cast<const int32_t*>(la_map[tid]);
 
   for (int64_t j = tid; j < p.npad; j += NT) zs[j] = p.Z[j];
   for (int j = tid; j < p.n; j += NT) {
@@ -1018,9 +1036,11 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
   for (int64_t e = tid; e < (int64_t)NS * 2 * B * SP; e += NT) slots[e] = 0.0;
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
-    for (int s = 0; s < 4; ++s) mbar_init(&rbar[s], 1);
+    for (int s = 0; s < 8; ++s) mbar_init(&rbar[s], 1);
+    for (int s = 0; s < 2; ++s) mbar_init(&tbar[s], 1);
+    for (int s = 0; s < 2; ++s) mbar_init(&sbar[s], 1);
     fence_mbar_init();
-    for (int s = 0; s < 4; ++s) mbar_arrive_expect_tx(&rbar[s], CC * NRV * 8);
+    for (int s = 0; s < 8; ++s) mbar_arrive_expect_tx(&rbar[s], CC * NRV * 8);
     done_s = 0;
   }
   double bnorm = 1.0;
@@ -1052,7 +1072,7 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
   if (filler) {
     for (int q = 0; q < 2; ++q) {   // 16 blocks ahead before the step loop starts
       rk_fill_indices(p, Ss, ring, p.t0 + 32 * q, lane, bh_tab, rn_tab);
-      la_fill_gram(p, ring, gring, 8 * q, lane);
+      la_fill_gram(p, ring, gring, lam, 8 * q, lane);
     }
     if (lane == 0) filled_s = 16;
   }
@@ -1075,10 +1095,10 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
   if (filler) {   // ---- fill warp: index + Gram rings, at most 24 blocks ahead of the consumers
     int64_t f = 16;
     while (f < nblk) {
-      while (f + 8 > ld_acquire_cta_s64(&done_s) + 24) {
+      while (f + 8 > ld_acquire_cta_s64(&done_s) + LA_GR) {   // slot of block done must stay
       }
       rk_fill_indices(p, Ss, ring, p.t0 + 4 * f, lane, bh_tab, rn_tab);
-      la_fill_gram(p, ring, gring, f, lane);
+      la_fill_gram(p, ring, gring, lam, f, lane);
       f += 8;
       __syncwarp();
       if (lane == 0) st_release_cta_s64(&filled_s, f);
@@ -1094,6 +1114,51 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
         if (++slot == NS) slot = 0;
       }
     }
+  } else if (reducer) {   // ---- reduce warp: finished products of block i once s(i-1) is posted
+    const bool rprof = p.prof && lane == 0;
+    long long hr[2] = {0, 0};
+    for (int64_t i = 0; i < nblk; ++i) {
+      if (i >= 1) mbar_wait(&sbar[(i - 1) & 1], (uint32_t)(((i - 1) >> 1) & 1));
+      long long rc0 = rprof ? clock64() : 0;
+      const int b4 = (int)(i & 7);
+      mbar_wait(&rbar[b4], (uint32_t)((i >> 3) & 1));
+      if (rprof) {
+        const long long c_ = clock64();
+        hr[0] += c_ - rc0;
+        rc0 = c_;
+      }
+      // lane (v, g): sources 4g .. 4g+3 of value v (cluster sum in a fixed tree) plus the
+      // correction terms of step m = g of blocks i-1 and i-2 (missing from the stale state S_{i-2}),
+      // then a butterfly over the four lane groups
+      const int v = lane & 7, g = lane >> 3, k = v & 3;
+      const bool isq = v >= B;
+      const double* gn = gring[i & (LA_GR - 1)];
+      double tot = (recv[b4][4 * g][v] + recv[b4][4 * g + 1][v]) + (recv[b4][4 * g + 2][v] + recv[b4][4 * g + 3][v]);
+#pragma unroll
+      for (int d = 1; d <= 2; ++d) {
+        if (i >= d) {
+          const double* sm = smail[(i - d) & 3];
+          const int o = 22 + 48 * (d - 1) + 4 * k + g;
+          const double ga = gn[o + (isq ? 16 : 0)];
+          const double gb = isq ? gn[o + 32] : 0.0;
+          tot = fma(sm[g], ga, tot);
+          tot = fma(-sm[B + g], gb, tot);
+        }
+      }
+      tot += __shfl_xor_sync(0xffffffffu, tot, 8);
+      tot += __shfl_xor_sync(0xffffffffu, tot, 16);
+      if (lane < NRV) tsm[i & 1][lane] = tot;
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&tbar[i & 1]);
+        mbar_arrive_expect_tx(&rbar[b4], CC * NRV * 8);   // for block i + 8
+      }
+      if (rprof) hr[1] += clock64() - rc0;
+    }
+    if (rprof) {
+      p.prof[128 + rank * 8 + 0] += hr[0];
+      p.prof[128 + rank * 8 + 1] += hr[1];
+    }
   } else {   // ---- compute warps and the communication warp
     double w[U], r[U];
 #pragma unroll
@@ -1103,21 +1168,12 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
       w[u] = in ? p.W[i0 + e] : 0.0;
       r[u] = in ? p.Rv[i0 + e] : 0.0;
     }
-    double s1p[B], s2p[B];
-#pragma unroll
-    for (int i = 0; i < B; ++i) s1p[i] = s2p[i] = 0.0;
     int64_t known_filled = 0;
-    // for the next block: its in-block Gram values and the corrections of its stale-state products,
-    // formed at the end of the previous block (off the path between the exchange and the recurrence)
-    double gin[22], corr[2 * B];
-#pragma unroll
-    for (int v = 0; v < 22; ++v) gin[v] = gring[0][v];
-#pragma unroll
-    for (int v = 0; v < 2 * B; ++v) corr[v] = 0.0;
-    int sl_nb = NS - 1, sl_i = NS - 2;
+    int sl_nb = NS - 1, sl_i = 0;
     uint32_t ph_nb = 1;
     const bool prof = p.prof && tid == 0;
     long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long hx[5] = {0, 0, 0, 0, 0};   // helper-warp timers (lane 0 of the reduce / comm warp)
     long long tc = clock64();
 #define LAP(k)                       \
   if (prof) {                        \
@@ -1125,14 +1181,14 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
     pc[k] += c_ - tc;                \
     tc = c_;                         \
   }
-    for (int64_t i = -1; i < nblk; ++i) {
-      const int64_t nb = i + 1;
-      sl_i = sl_nb;
+    for (int64_t i = -2; i < nblk; ++i) {
+      const int64_t nb = i + 2;
       if (++sl_nb == NS) {
         sl_nb = 0;
         ph_nb ^= 1u;
       }
-      // ---- phase 1 (compute warps): state products of block nb on S_{nb-1}
+      sl_i = sl_nb - 2 < 0 ? sl_nb - 2 + NS : sl_nb - 2;   // slot of block i (NS >= 3)
+      // ---- phase 1 (compute warps): state products of block nb = i + 2 on S_i (blocks i, i+1 not applied)
       if (compute && nb < nblk) {
         if (known_filled <= nb + 1 && known_filled < nblk) {   // ring + Gram entries of blocks nb, nb+1
           do {
@@ -1162,45 +1218,44 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
       named_bar_sync(1, NTc + 32);   // B1: compute warps + communication warp
       LAP(1)
       if (comm) {
+        const bool cprof = p.prof && lane == 0;
+        long long cc0 = cprof ? clock64() : 0;
         if (nb < nblk) {
           double v = 0.0;
           for (int w8 = 0; w8 < NWc; ++w8) v += wred[nb & 1][w8][lane & 7];
           const double v0 = __shfl_sync(0xffffffffu, v, (2 * lane) & 7);
           const double v1 = __shfl_sync(0xffffffffu, v, (2 * lane + 1) & 7);
-          const int b4 = (int)(nb & 3);
+          const int b4 = (int)(nb & 7);
           const uint32_t la = smem_u32(&recv[b4][rank][2 * (lane & 3)]);
           const uint32_t lb = smem_u32(&rbar[b4]);
           if (lane < NRV / 2)
             for (int c = 0; c < CC; ++c) st_async_v2f64(map_shared_rank(la, (uint32_t)c), v0, v1, map_shared_rank(lb, (uint32_t)c));
+          __syncwarp();
+          if (cprof) {
+            const long long c_ = clock64();
+            hx[3] += c_ - cc0;
+            cc0 = c_;
+          }
         }
-        if (i >= 1 && lane == 0) {   // z updates of block i - 1 (posted before B1), sequential order
+        if (i >= 1 && lane == 0) {   // z updates of block i - 1, sequential order
           const int64_t tp = p.t0 + (i - 1) * B;
 #pragma unroll
-          for (int k = 0; k < B; ++k) zs[ring[(tp + k) & (RK_RING - 1)].j2] += zmail[(i - 1) & 1][k];
+          for (int k = 0; k < B; ++k) zs[ring[(tp + k) & (RK_RING - 1)].j2] += smail[(i - 1) & 3][B + k];
         }
         continue;
       }
       if (i < 0) continue;
       // ---- phase 2 (compute warps): block i
-      const int b4 = (int)(i & 3);
-      mbar_wait(&rbar[b4], (uint32_t)((i >> 2) & 1));
-      LAP(2)
-      double tot;
-      {
-        double a[CC];
-#pragma unroll
-        for (int c = 0; c < CC; ++c) a[c] = recv[b4][c][lane & 7];
-#pragma unroll
-        for (int s = 1; s < CC; s *= 2)
-#pragma unroll
-          for (int c = 0; c + s < CC; c += 2 * s) a[c] += a[c + s];
-        tot = a[0];
-      }
       double T[K::NV];
+      {
+        const double* gi = gring[i & (LA_GR - 1)];   // in-block Gram values (filled: see phase 1)
 #pragma unroll
-      for (int v = 0; v < NRV; ++v) T[v] = __shfl_sync(0xffffffffu, tot, v) + corr[v];
+        for (int v = NRV; v < K::NV; ++v) T[v] = gi[v - NRV];
+      }
+      mbar_wait(&tbar[i & 1], (uint32_t)((i >> 1) & 1));
+      LAP(2)
 #pragma unroll
-      for (int v = NRV; v < K::NV; ++v) T[v] = gin[v - NRV];
+      for (int v = 0; v < NRV; ++v) T[v] = tsm[i & 1][v];
       LAP(3)
       const int64_t t = p.t0 + i * B;
       double s1[B], s2[B];
@@ -1221,27 +1276,13 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
         s2[k] = dr * ix.rn2;
       }
       LAP(4)
-      if (i + 1 < nblk) {   // block i+1: corrections with this block's scalars, in-block Gram values
-        if (known_filled <= i + 1 && known_filled < nblk) {
-          do {
-            known_filled = ld_acquire_cta_s64(&filled_s);
-          } while (known_filled <= i + 1 && known_filled < nblk);
-        }
-        const double* gn = gring[(i + 1) & 31];
-#pragma unroll
-        for (int v = 0; v < 22; ++v) gin[v] = gn[v];
+      if (tid == 0) {   // the reduce warp forms block i+1's products (and the comm warp z) with them
 #pragma unroll
         for (int k = 0; k < B; ++k) {
-          double cp = 0.0, cq = 0.0;
-#pragma unroll
-          for (int m = 0; m < B; ++m) {
-            cp = fma(s1[m], gn[22 + 4 * k + m], cp);
-            cq = fma(s1[m], gn[38 + 4 * k + m], cq);
-            cq = fma(-s2[m], gn[54 + 4 * k + m], cq);
-          }
-          corr[K::P(k)] = cp;
-          corr[K::Q(k)] = cq;
+          smail[i & 3][k] = s1[k];
+          smail[i & 3][B + k] = s2[k];
         }
+        mbar_arrive(&sbar[i & 1]);
       }
       const double* cols = slots + (size_t)sl_i * 2 * B * SP;
 #pragma unroll
@@ -1256,24 +1297,16 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
         }
       }
       LAP(5)
-      if (tid == 0)
-#pragma unroll
-        for (int k = 0; k < B; ++k) zmail[i & 1][k] = s2[k];   // the comm warp applies them
-#pragma unroll
-      for (int k = 0; k < B; ++k) {
-        s1p[k] = s1[k];
-        s2p[k] = s2[k];
-      }
-      named_bar_sync(2, NTc);   // every compute thread read recv[b4] and finished block i's axpy
-      if (tid == 0) {
-        mbar_arrive_expect_tx(&rbar[b4], CC * NRV * 8);   // for block i + 4
-        st_release_cta_s64(&done_s, i + 1);
-      }
+      named_bar_sync(2, NTc);   // every compute thread finished block i's axpy (slot sl_i reusable)
+      if (tid == 0) st_release_cta_s64(&done_s, i + 1);
       LAP(5)
     }
 #undef LAP
     if (prof)
       for (int k = 0; k < 8; ++k) p.prof[rank * 8 + k] += pc[k];
+    if (p.prof && lane == 0 && comm)
+      for (int k = 0; k < 5; ++k)
+        if (hx[k]) p.prof[128 + rank * 8 + k] += hx[k];
     if (compute) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -1289,7 +1322,7 @@ __global__ void __launch_bounds__(288, 1) rk_rgs_la_kernel(RkParams p) {
   if (comm && lane == 0 && nblk >= 1) {   // the last block's z updates
     const int64_t tp = p.t0 + (nblk - 1) * B;
 #pragma unroll
-    for (int k = 0; k < B; ++k) zs[ring[(tp + k) & (RK_RING - 1)].j2] += zmail[(nblk - 1) & 1][k];
+    for (int k = 0; k < B; ++k) zs[ring[(tp + k) & (RK_RING - 1)].j2] += smail[(nblk - 1) & 3][B + k];
   }
   __syncthreads();
   if (rank == 0)
@@ -1497,10 +1530,17 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
   size_t smem_la = 0;
   {
     const char* e = getenv("ILS_RK_LA");
-    if (!(e && e[0] == '0') && blocked && C == 16 && Bk == 4 && (U == 4 || U == 8) && nt + 96 <= 288 && !h.large &&
+    if (!(e && e[0] == '0') && blocked && C == 16 && Bk == 4 && (U == 4 || U == 8) && nt + 128 <= 320 && !h.large &&
         !h.sparse) {
-      smem_la = smem + (size_t)32 * LA_NG * sizeof(double);
-      if (smem_la <= 227 * 1024) {
+      // the Gram ring replaces one column slot when both do not fit (>= 3 slots: blocks i .. i+2 live)
+      const size_t ring_bytes = (size_t)LA_GR * LA_NG * sizeof(double), slot_la = (size_t)2 * Bk * p.slicepad * 8;
+      smem_la = smem + ring_bytes;
+      const size_t cap = 227 * 1024 - 10 * 1024;   // the kernel's static shared memory (~9.6 KB) counts too
+      while (smem_la > cap && p.nslots > 4) {
+        p.nslots -= 1;
+        smem_la -= slot_la;
+      }
+      if (smem_la <= cap) {
         int rc = build_gram(h);
         if (rc) return rc;
         p.G = h.G;
@@ -1515,8 +1555,8 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
   {
     const char* e = getenv("ILS_RK_PROF");
     if (e && e[0] == '1' && blocked) {   // (the look-ahead kernel reports: compute phase1, B1, recv, phase2 | comm B1, send, refill, fill)
-      ILS_CU(cudaMallocAsync(&prof, 16 * 8 * sizeof(long long), st));
-      ILS_CU(cudaMemsetAsync(prof, 0, 16 * 8 * sizeof(long long), st));
+      ILS_CU(cudaMallocAsync(&prof, 16 * 16 * sizeof(long long), st));
+      ILS_CU(cudaMemsetAsync(prof, 0, 16 * 16 * sizeof(long long), st));
     }
   }
   p.prof = prof;
@@ -1560,7 +1600,7 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
     const int64_t t1 = (t + ce < max_inner) ? t + ce : max_inner;
     p.t0 = t;
     p.t1 = t1;
-    const int r = la ? ((U == 4) ? launch_rkla<16, 4>(h, p, nt + 96, smem_la) : launch_rkla<16, 8>(h, p, nt + 96, smem_la))
+    const int r = la ? ((U == 4) ? launch_rkla<16, 4>(h, p, nt + 128, smem_la) : launch_rkla<16, 8>(h, p, nt + 128, smem_la))
                   : blocked ? dispatch_rkb(h, p, U, Bk, nt, smem)
                             : ((U == 8) ? dispatch_rk_c<8>(h, p, nt, smem) : dispatch_rk_c<4>(h, p, nt, smem));
     if (r) return r;
@@ -1587,7 +1627,7 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
   const int64_t steps = h.hstat->inner_conv ? h.hstat->inner_steps : max_inner;
   (void)conv;
   if (prof) {
-    long long hp[16 * 8];
+    long long hp[16 * 16];
     ILS_CU(cudaMemcpy(hp, prof, sizeof(hp), cudaMemcpyDeviceToHost));
     cudaFree(prof);
     const double nb = (double)((steps + Bk - 1) / Bk);
@@ -1595,6 +1635,11 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
       const long long* q = hp + rk * 8;
       fprintf(stderr, "ILS_RK_PROF k=%lld rank=%d blocks=%.0f cycles/block: wait %.0f local %.0f rscatter %.0f bar %.0f send %.0f recv %.0f sum %.0f rest %.0f\n",
               (long long)k, rk, nb, q[0] / nb, q[1] / nb, q[2] / nb, q[3] / nb, q[4] / nb, q[5] / nb, q[6] / nb, q[7] / nb);
+      if (la) {   // look-ahead helper warps: reduce warp (B1 -> data, data -> T posted), comm warp (send issue)
+        const long long* r2 = hp + 128 + rk * 8;
+        fprintf(stderr, "ILS_RK_PROF_LA rank=%d reduce: data wait %.0f T %.0f rest %.0f | comm: send %.0f z %.0f\n", rk,
+                r2[0] / nb, r2[1] / nb, r2[2] / nb, r2[3] / nb, r2[4] / nb);
+      }
     }
   }
   if (steps_out) *steps_out = steps;
