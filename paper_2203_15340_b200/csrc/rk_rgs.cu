@@ -990,7 +990,7 @@ __device__ __forceinline__ void st_release_cta_s64(int64_t* a, int64_t v) {
 // per block; the fill and TMA warps run ahead, throttled by progress counters in shared memory
 // (release / acquire), so their long operations never stall the step.
 template <int CC, int U>
-__global__ void __launch_bounds__(320, 1) rk_rgs_la_kernel(RkParams p) {
+__global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
   constexpr int B = 4, NRV = 8;
   static_assert(CC == 16, "the communication warp's cluster sum is written for 16 sources");
   using K = RkBlk<B>;
@@ -1530,7 +1530,7 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
   size_t smem_la = 0;
   {
     const char* e = getenv("ILS_RK_LA");
-    if (!(e && e[0] == '0') && blocked && C == 16 && Bk == 4 && (U == 4 || U == 8) && nt + 128 <= 320 && !h.large &&
+    if (!(e && e[0] == '0') && blocked && C == 16 && Bk == 4 && (U == 2 || U == 4 || U == 8) && nt + 128 <= 384 && !h.large &&
         !h.sparse) {
       // the Gram ring replaces one column slot when both do not fit (>= 3 slots: blocks i .. i+2 live)
       const size_t ring_bytes = (size_t)LA_GR * LA_NG * sizeof(double), slot_la = (size_t)2 * Bk * p.slicepad * 8;
@@ -1600,7 +1600,9 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
     const int64_t t1 = (t + ce < max_inner) ? t + ce : max_inner;
     p.t0 = t;
     p.t1 = t1;
-    const int r = la ? ((U == 4) ? launch_rkla<16, 4>(h, p, nt + 128, smem_la) : launch_rkla<16, 8>(h, p, nt + 128, smem_la))
+    const int r = la ? ((U == 2)   ? launch_rkla<16, 2>(h, p, nt + 128, smem_la)
+                        : (U == 4) ? launch_rkla<16, 4>(h, p, nt + 128, smem_la)
+                                   : launch_rkla<16, 8>(h, p, nt + 128, smem_la))
                   : blocked ? dispatch_rkb(h, p, U, Bk, nt, smem)
                             : ((U == 8) ? dispatch_rk_c<8>(h, p, nt, smem) : dispatch_rk_c<4>(h, p, nt, smem));
     if (r) return r;
