@@ -298,6 +298,31 @@ def test_rk_cluster_short_horizons(T, ce):
         assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
 
 
+@pytest.mark.parametrize("shape", [(10000, 500, 700), (7900, 300, 1500)])
+@pytest.mark.parametrize("T,ce", [(6, 5), (2003, 250)])
+@pytest.mark.parametrize("la", ["1", "0"])
+def test_rk_cluster_geometries(shape, T, ce, la, monkeypatch):
+    """Other 16-CTA geometries: 5 compute warps (p = 10000) and n = 1500 (four column slots next to
+    the Gram ring), with the look-ahead kernel (default) and without (ILS_RK_LA=0); iterates and
+    inner counts against the oracle."""
+    monkeypatch.setenv("ILS_RK_LA", la)
+    p, q, n = shape
+    pr = make_dense(p, q, n, 0.5, seed=48)
+    K = 2
+    ref = O.sp_rk_rgs_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE, seed=6, max_inner=T,
+                            check_every=ce, inner_tol=1e-6)
+    hist = np.zeros((K, pr.n))
+    inner = np.zeros(K, dtype=np.int64)
+    x = np.zeros(pr.n)
+    with H(pr) as hh:
+        o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, seed=6, max_inner=T, check_every=ce, inner_tol=1e-6,
+                                 x_hist=hist.ctypes.data, inner_hist=inner.ctypes.data)
+        ils.ils_rk_solve(hh.h, None, x, 0.0, K, o)
+    assert list(inner) == list(ref.inner_hist)
+    for k in range(K):
+        assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
+
+
 def test_rk_converges_c0():
     pr = make_problem("c0")
     ref = O.sp_rk_rgs_solve(pr.A1, pr.A2, pr.b1, pr.b2, tol=1e-10, x_ref=pr.xstar, inner_tol=1e-12,
