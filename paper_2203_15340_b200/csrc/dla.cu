@@ -265,70 +265,121 @@ int mirror_lower(Handle& h, double* C, int64_t ld, int64_t n, int64_t n_real) {
 
 // ---------------------------------------------------------------- 64x64 base: potf2 + trtri
 // Cholesky of the 64x64 diagonal block at (s0, s0) of L (lower, in place) and its inverse into Z,
-// in shared memory with loops (no full unrolling: a fully unrolled 32x32 register version was
-// ~54k SASS instructions executed once and instruction-fetch bound, 187 us per block on B200).
-// Right-looking potf2: per column k one pivot, a column scale and a rank-1 update of the trailing
-// lower triangle by a 16x16 thread grid (4x4 elements each). trtri: row by row, Z[i][c] for all
-// c <= i in parallel, 4 threads per column splitting the k-sum (fixed shuffle order).
+// fused in one right-looking sweep with both trailing matrices in registers. A 16x16 thread grid
+// holds 4x4 elements each (rows ty + 16 u, columns tx + 16 v) of A (-> L) and of W, the working
+// right-hand side of L Z = I. Iteration k: the owners of column k of A publish it and the diagonal
+// owner publishes 1 / sqrt(a_kk); the owners of row k-1 of W publish Z[k-1][:] = W[k-1][:] / L_{k-1,k-1};
+// one barrier; then every thread applies a_ij -= l_ik l_jk (l = published * rs, the arithmetic of a
+// textbook potf2) and W_ic -= L[i][k-1] Z[k-1][c]. One barrier per column for both factorisations
+// (the shared-memory loop version with a separate trtri pass took ~75 us per block, mostly barrier
+// and issue stalls; a fully unrolled 32x32 register version was instruction-fetch bound).
 __global__ void __launch_bounds__(256) potf2_trtri_kernel(double* __restrict__ L, double* __restrict__ Z,
                                                           int64_t ld, int64_t s0, int32_t* err) {
   extern __shared__ __align__(16) double potf_smem[];
-  double (*a)[65] = reinterpret_cast<double (*)[65]>(potf_smem);            // [64][65] A, then L
-  double (*zi)[65] = reinterpret_cast<double (*)[65]>(potf_smem + 64 * 65);  // [64][65] Z
-  __shared__ double rdiag[64];   // 1 / L_ii
+  double (*a)[65] = reinterpret_cast<double (*)[65]>(potf_smem);            // [64][65] L (lower)
+  double (*zi)[65] = reinterpret_cast<double (*)[65]>(potf_smem + 64 * 65);  // [64][65] Z (lower)
+  __shared__ double colv[3][64];   // raw column k of the trailing A (rows >= k), buffer k % 3
+  __shared__ double rsv[3];        // 1 / L_kk, buffer k % 3
+  __shared__ double zrow[2][64];   // row k-1 of Z (columns <= k-1), buffer (k-1) & 1
   __shared__ int bad_s;
   const int tid = threadIdx.x;
   double* blk = L + s0 * ld + s0;
-  for (int e = tid; e < 64 * 64; e += 256) {
-    const int i = e >> 6, j = e & 63;
-    a[i][j] = (j <= i) ? blk[i * ld + j] : 0.0;
-    zi[i][j] = 0.0;
-  }
+  const int ty = tid >> 4, tx = tid & 15;
+  double t[4][4], w[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int i = ty + 16 * u, j = tx + 16 * v;
+      t[u][v] = (j <= i) ? blk[i * ld + j] : 0.0;
+      w[u][v] = (j == i) ? 1.0 : 0.0;
+    }
   if (tid == 0) bad_s = 0;
-  __syncthreads();
-  const int ty = tid >> 4, tx = tid & 15;   // 16x16 grid, rows ty + 16 u, columns tx + 16 v
-  for (int k = 0; k < 64; ++k) {
-    // pivot: every row thread takes sqrt(a_kk) itself (no extra barrier); row k stores it
-    if (tid >= k && tid < 64) {
-      const double d = a[k][k];
-      const bool ok = d > 0.0 && isfinite(d);
-      const double rs = ok ? rsqrt(d) : 0.0;   // 1 / L_kk
-      if (tid == k) {
-        if (!ok) bad_s = 1;
-        a[k][k] = d * rs;
-        rdiag[k] = rs;
-      } else {
-        a[tid][k] *= rs;
+  int b3 = 0, bm3 = 2;   // k % 3, (k - 1) % 3
+  for (int k = 0; k <= 64; ++k) {
+    const int m = k - 1;
+    // ---- publish
+    if (k < 64 && tx == (k & 15)) {   // column k of A (rows >= k); the diagonal owner adds 1 / L_kk
+      const int kv = k >> 4;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = ty + 16 * u;
+        double val = 0.0;
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          if (v == kv) val = t[u][v];
+        if (i >= k) colv[b3][i] = val;
+        if (i == k) {
+          const bool ok = val > 0.0 && isfinite(val);
+          rsv[b3] = ok ? rsqrt(val) : 0.0;
+          if (!ok) bad_s = 1;
+        }
+      }
+    }
+    if (m >= 0 && ty == (m & 15)) {   // row m of Z = row m of W scaled by 1 / L_mm
+      const int mu = m >> 4;
+      const double rm = rsv[bm3];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (u != mu) continue;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int c = tx + 16 * v;
+          if (c <= m) {
+            const double z = w[u][v] * rm;
+            zrow[m & 1][c] = z;
+            zi[m][c] = z;
+          }
+        }
       }
     }
     __syncthreads();
+    // ---- update
+    if (k < 64) {
+      const double rs = rsv[b3];
+      double lik[4], ljk[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = ty + 16 * u;
-      if (i <= k) continue;
-      const double lik = a[i][k];
+      for (int u = 0; u < 4; ++u) lik[u] = colv[b3][(ty + 16 * u) & 63] * rs;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int j = tx + 16 * v;
-        if (j > k && j <= i) a[i][j] = fma(-lik, a[j][k], a[i][j]);
+      for (int v = 0; v < 4; ++v) ljk[v] = colv[b3][(tx + 16 * v) & 63] * rs;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = ty + 16 * u;
+        if (i <= k) continue;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int j = tx + 16 * v;
+          if (j > k && j <= i) t[u][v] = fma(-lik[u], ljk[v], t[u][v]);
+        }
+      }
+      if (tx == (k & 15)) {   // the finished column k of L
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = ty + 16 * u;
+          if (i > k) a[i][k] = lik[u];
+          if (i == k) a[k][k] = colv[b3][k] * rs;
+        }
       }
     }
-    __syncthreads();
-  }
-  // Z = L^{-1}: Z[i][c] = (delta_ic - sum_{c <= k < i} L[i][k] Z[k][c]) / L[i][i]. Column c belongs
-  // to one quad of lanes of one warp (4 threads split the k-sum), so the forward substitution
-  // needs only warp-level synchronisation.
-  const int c = tid >> 2, part = tid & 3;
-  for (int i = (tid >> 5) * 8; i < 64; ++i) {   // warp-uniform trip count (the warp's first column)
-    double sum = 0.0;
-    if (i >= c)
-      for (int k = c + part; k < i; k += 4) sum = fma(a[i][k], zi[k][c], sum);
-    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-    if (part == 0 && i >= c) {
-      zi[i][c] = (((i == c) ? 1.0 : 0.0) - sum) * rdiag[i];
+    if (m >= 0) {   // W_ic -= L[i][m] Z[m][c] for i > m, c <= m
+      const double rm = rsv[bm3];
+      double zmc[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) zmc[v] = zrow[m & 1][tx + 16 * v];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = ty + 16 * u;
+        if (i <= m) continue;
+        const double lim = colv[bm3][i] * rm;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int c = tx + 16 * v;
+          if (c <= m) w[u][v] = fma(-lim, zmc[v], w[u][v]);
+        }
+      }
     }
-    __syncwarp();
+    bm3 = b3;
+    b3 = (b3 == 2) ? 0 : b3 + 1;
   }
   __syncthreads();
   double* zb = Z + s0 * ld + s0;
