@@ -124,6 +124,20 @@ __device__ __forceinline__ bool argmax_better(double v1, int i1, double v2, int 
   return (v1 > v2) || (v1 == v2 && i1 < i2);
 }
 
+// Warp argmax of a non-negative double key with ties to the smallest index, by integer warp
+// reductions (redux.sync): the bit pattern of a double >= 0 orders like the value, so the max is
+// taken on the high word, then on the low word among the lanes that hold the high max, then the
+// min index among the lanes that hold both. Lanes without a candidate pass key 0 and idx INT_MAX
+// (a valid key 0 then wins by its index). Returns the winning index in every lane (INT_MAX: none).
+__device__ __forceinline__ int warp_argmax_redux(double key, int idx) {
+  const unsigned long long kb = (unsigned long long)__double_as_longlong(key);
+  const unsigned hi = (unsigned)(kb >> 32), lo = (unsigned)kb;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  const unsigned cand = (hi == mhi && lo == mlo) ? (unsigned)idx : 0xffffffffu;
+  return (int)min(__reduce_min_sync(0xffffffffu, cand), (unsigned)INT_MAX);
+}
+
 __device__ __forceinline__ ArgMax warp_argmax(ArgMax a) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

@@ -205,17 +205,9 @@ __global__ void __launch_bounds__(32, 1) scd_warp_kernel(ScdParams p) {
         br = r[v];
       }
     }
-    // butterfly argmax across lanes: every lane ends with the winner
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (argmax_better(ov, oi, bv, bi)) {
-        bv = ov;
-        bi = oi;
-      }
-    }
-    const int j = bi;
+    // argmax across lanes by integer warp reductions (common.cuh): every lane gets the winner
+    if (bi == INT_MAX) bv = 0.0;
+    const int j = warp_argmax_redux(bv, bi);
     const double rj = __shfl_sync(0xffffffffu, br, j & 31);   // the owner lane's local best is j
     const double sc = rj * rNs[j];
     const double* grow = p.G + (int64_t)j * p.npad + lane;
@@ -339,42 +331,21 @@ __global__ void __launch_bounds__(SCD_MAXT, 1) scd_chunk_kernel(ScdParams p) {
           br = r[v];
         }
       }
-      // warp argmax (value, index, r) by butterfly: every lane ends with the warp winner; ties to
-      // the smallest index
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        const double orr = __shfl_xor_sync(0xffffffffu, br, o);
-        if (argmax_better(ov, oi, bv, bi)) {
-          bv = ov;
-          bi = oi;
-          br = orr;
-        }
-      }
-      if (lane == 0) {
+      // warp argmax (ties to the smallest index) by integer warp reductions on the key bits; the
+      // winner's lane is its index mod 32 (coordinates tid + v NT, NT a multiple of 32)
+      if (bi == INT_MAX) bv = 0.0;
+      const int wj = warp_argmax_redux(bv, bi);
+      if (wj == INT_MAX ? lane == 0 : bi == wj) {   // the winning lane (or lane 0: no candidate) records it
         wv[pb][warp] = bv;
-        wi[pb][warp] = bi;
+        wi[pb][warp] = wj;
         wr[pb][warp] = br;
       }
       __syncthreads();
-      // every warp reduces the NW warp winners (same fixed tree in every warp)
-      double cv = (lane < NW) ? wv[pb][lane] : -1.0;
-      int ci = (lane < NW) ? wi[pb][lane] : INT_MAX;
-      double cr = (lane < NW) ? wr[pb][lane] : 0.0;
-#pragma unroll
-      for (int o = SCD_MAXW / 2; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, cv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, ci, o);
-        const double orr = __shfl_xor_sync(0xffffffffu, cr, o);
-        if (argmax_better(ov, oi, cv, ci)) {
-          cv = ov;
-          ci = oi;
-          cr = orr;
-        }
-      }
-      j = __shfl_sync(0xffffffffu, ci, 0);   // lanes >= NW reduced only invalid entries
-      rj = __shfl_sync(0xffffffffu, cr, 0);
+      // every warp reduces the NW warp winners the same way
+      const double cv = (lane < NW) ? wv[pb][lane] : 0.0;
+      const int ci = (lane < NW) ? wi[pb][lane] : INT_MAX;
+      j = warp_argmax_redux(cv, ci);
+      rj = wr[pb][(j % NT) >> 5];   // the winning warp's entry
     }
     const double sc = rj * rNs[j];
     const double* grow = p.G + (int64_t)j * p.npad;

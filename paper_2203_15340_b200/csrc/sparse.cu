@@ -962,36 +962,16 @@ __global__ void __launch_bounds__(SSCD_T, 1) sparse_scd_kernel(SpScdParams p) {
         }
       }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (argmax_better(ov, oi, bv, bi)) {
-        bv = ov;
-        bi = oi;
-      }
-    }
-    if (bi != INT_MAX && (bi % SSCD_T) == tid) {
+    // warp argmax by integer warp reductions (common.cuh); the winning thread records it
+    if (bi == INT_MAX) bv = 0.0;
+    const int wj = warp_argmax_redux(bv, bi);
+    if (wj == INT_MAX ? lane == 0 : bi == wj) {
       wv[pb][warp] = bv;
-      wi[pb][warp] = bi;
+      wi[pb][warp] = wj;
       wr[pb][warp] = br;
-    } else if (lane == 0 && bi == INT_MAX) {
-      wv[pb][warp] = -1.0;
-      wi[pb][warp] = INT_MAX;
     }
     __syncthreads();
-    double cv = wv[pb][lane];
-    int cix = wi[pb][lane];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, cv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, cix, o);
-      if (argmax_better(ov, oi, cv, cix)) {
-        cv = ov;
-        cix = oi;
-      }
-    }
-    const int j = cix;
+    const int j = warp_argmax_redux(wv[pb][lane], wi[pb][lane]);   // 32 warps: one entry per lane
     const double sc = wr[pb][(j % SSCD_T) >> 5] / p.N[j];
     // r -= sc A1bar_(j): the row's columns are distinct
     if (p.Gd) {
@@ -1118,47 +1098,23 @@ __global__ void __cluster_dims__(SCDC_C, 1, 1) __launch_bounds__(SCDC_T, 1) scd_
         bn = nj[v];
       }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      const double orr = __shfl_xor_sync(0xffffffffu, br, o);
-      const double on = __shfl_xor_sync(0xffffffffu, bn, o);
-      if (argmax_better(ov, oi, bv, bi)) {
-        bv = ov;
-        bi = oi;
-        br = orr;
-        bn = on;
-      }
-    }
-    if (lane == 0) {
+    // warp argmax by integer warp reductions (common.cuh); the winning thread records it
+    if (bi == INT_MAX) bv = 0.0;
+    const int wj = warp_argmax_redux(bv, bi);
+    if (wj == INT_MAX ? lane == 0 : bi == wj) {
       wv[pb][warp] = bv;
-      wi[pb][warp] = bi;
+      wi[pb][warp] = wj;
       wr[pb][warp] = br;
       wn[pb][warp] = bn;
     }
     __syncthreads();
     if (warp == 0) {   // CTA winner, one message to every CTA, then the cluster winner
-      double cv = (lane < SCDC_T / 32) ? wv[pb][lane] : -1.0;
-      double cr = (lane < SCDC_T / 32) ? wr[pb][lane] : 0.0;
-      double cn = (lane < SCDC_T / 32) ? wn[pb][lane] : 1.0;
-      int ci = (lane < SCDC_T / 32) ? wi[pb][lane] : INT_MAX;
-#pragma unroll
-      for (int o = SCDC_T / 64; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, cv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, ci, o);
-        const double orr = __shfl_xor_sync(0xffffffffu, cr, o);
-        const double on = __shfl_xor_sync(0xffffffffu, cn, o);
-        if (argmax_better(ov, oi, cv, ci)) {
-          cv = ov;
-          ci = oi;
-          cr = orr;
-          cn = on;
-        }
-      }
+      const double cv0 = (lane < SCDC_T / 32) ? wv[pb][lane] : 0.0;
+      const int ci0 = warp_argmax_redux(cv0, (lane < SCDC_T / 32) ? wi[pb][lane] : INT_MAX);
+      const int ww = (ci0 == INT_MAX) ? 0 : (((ci0 % NTT) - rank * SCDC_T) >> 5);   // its warp
+      const double cv = (ci0 == INT_MAX) ? 0.0 : wv[pb][ww];
+      const double cr = wr[pb][ww], cn0 = (ci0 == INT_MAX) ? 1.0 : wn[pb][ww];
       // lane 0 carries (r_j^2, r_j), lane 1 carries (j, N_j): 32 bytes per destination
-      const int ci0 = __shfl_sync(0xffffffffu, ci, 0);   // all lanes shuffle (no divergent shfl)
-      const double cn0 = __shfl_sync(0xffffffffu, cn, 0);
       const double m0 = (lane == 0) ? cv : (double)ci0;
       const double m1 = (lane == 0) ? cr : cn0;
       const uint32_t la = smem_u32(&recv[pb][rank][2 * (lane & 1)]);
@@ -1167,24 +1123,11 @@ __global__ void __cluster_dims__(SCDC_C, 1, 1) __launch_bounds__(SCDC_T, 1) scd_
 #pragma unroll
         for (int c = 0; c < SCDC_C; ++c) st_async_v2f64(map_shared_rank(la, (uint32_t)c), m0, m1, map_shared_rank(lb, (uint32_t)c));
       mbar_wait_cluster(&rbar[pb], (uint32_t)((t - p.t0) >> 1) & 1u);
-      // the 16 CTA winners, lane c holds candidate c; fixed butterfly (ties to the smallest index)
-      double xv = (lane < SCDC_C) ? recv[pb][lane][0] : -1.0;
-      double xr = (lane < SCDC_C) ? recv[pb][lane][1] : 0.0;
-      double xn = (lane < SCDC_C) ? recv[pb][lane][3] : 1.0;
-      int xi = (lane < SCDC_C) ? (int)recv[pb][lane][2] : INT_MAX;
-#pragma unroll
-      for (int o = SCDC_C / 2; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, xv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, xi, o);
-        const double orr = __shfl_xor_sync(0xffffffffu, xr, o);
-        const double on = __shfl_xor_sync(0xffffffffu, xn, o);
-        if (argmax_better(ov, oi, xv, xi)) {
-          xv = ov;
-          xi = oi;
-          xr = orr;
-          xn = on;
-        }
-      }
+      // the 16 CTA winners, lane c holds candidate c (ties to the smallest index)
+      const double xv = (lane < SCDC_C) ? recv[pb][lane][0] : 0.0;
+      const int xi = warp_argmax_redux(xv, (lane < SCDC_C) ? (int)recv[pb][lane][2] : INT_MAX);
+      const int wc = (xi % NTT) / SCDC_T;   // the CTA that owns coordinate xi
+      const double xr = recv[pb][wc][1], xn = recv[pb][wc][3];
       __syncwarp();   // warp 0 has read recv[pb]: re-arm it for step t + 2
       if (lane == 0) {
         mbar_arrive_expect_tx(&rbar[pb], SCDC_C * 32);
