@@ -634,22 +634,13 @@ __global__ void __launch_bounds__(32) batched_scd_kernel(BatchParams P) {
               if (act && y >= (uint32_t)n) y = (y < 32) ? t0 : t1;
             }
           }
-          double bv = -1.0;
+          double bv = 0.0;
           int bi = INT_MAX;
           if (act && y < alpha) {
             bv = rr * rr;
             bi = lane;
           }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (argmax_better(ov, oi, bv, bi)) {
-              bv = ov;
-              bi = oi;
-            }
-          }
-          j = bi;
+          j = warp_argmax_redux(bv, bi);   // integer warp reductions, ties to the smallest index
         }
         const double sc = __shfl_sync(0xffffffffu, rr, j) * __shfl_sync(0xffffffffu, rn, j);
         if (act) rr = fma(-sc, G[j * 32 + lane], rr);
