@@ -344,6 +344,24 @@ struct RkBlk {
 
 // butterfly reduce-scatter of NVP (power of two <= 32) values over the warp: on return lane l
 // holds the warp sum of value l & (NVP - 1) (NVP - 1 + log2(32 / NVP) shuffles of doubles)
+// the butterfly levels of warp_reduce_scatter only: lane l holds value l & (NVP - 1) summed over its
+// NVP-lane group (the cross-group sum is left to the consumer)
+template <int NVP>
+__device__ __forceinline__ double warp_reduce_scatter_groups(double (&x)[NVP], int lane) {
+#pragma unroll
+  for (int half = NVP / 2; half >= 1; half /= 2) {
+    const bool hi = (lane & half) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double lo_v = x[i], hi_v = x[i + half];
+      const double send = hi ? lo_v : hi_v;
+      const double keep = hi ? hi_v : lo_v;
+      x[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+    }
+  }
+  return x[0];
+}
+
 template <int NVP>
 __device__ __forceinline__ double warp_reduce_scatter(double (&x)[NVP], int lane) {
 #pragma unroll
@@ -1013,7 +1031,7 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
   double* bh_tab = reinterpret_cast<double*>(bars + 8);                 // [n]
   double* rn_tab = bh_tab + ((p.n + 1) & ~1);                          // [n]
   double (*gring)[LA_NG] = reinterpret_cast<double (*)[LA_NG]>(rn_tab + ((p.n + 1) & ~1));   // [LA_GR][LA_NG]
-  __shared__ __align__(16) double wred[2][8][8];
+  __shared__ __align__(16) double wred[2][8][32];   // per warp: value lane & 7 over lane group lane >> 3
   __shared__ __align__(16) double recv[8][RK_MAXC][NRV];   // block b in buffer b & 7 (sent two blocks ahead)
   __shared__ __align__(8) uint64_t rbar[8];
   __shared__ double chkw[12];
@@ -1211,8 +1229,7 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
             acc[K::Q(k)] = fma(cols[(2 * k + 1) * SP + e], r[u], acc[K::Q(k)]);
           }
         }
-        const double mine = warp_reduce_scatter<NRV>(acc, lane);
-        if (lane < NRV) wred[nb & 1][warp][lane] = mine;
+        wred[nb & 1][warp][lane] = warp_reduce_scatter_groups<NRV>(acc, lane);   // groups summed by the comm warp
       }
       LAP(0)
       named_bar_sync(1, NTc + 32);   // B1: compute warps + communication warp
@@ -1222,7 +1239,9 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
         long long cc0 = cprof ? clock64() : 0;
         if (nb < nblk) {
           double v = 0.0;
-          for (int w8 = 0; w8 < NWc; ++w8) v += wred[nb & 1][w8][lane & 7];
+          for (int w8 = 0; w8 < NWc; ++w8) v += wred[nb & 1][w8][lane];
+          v += __shfl_xor_sync(0xffffffffu, v, 8);
+          v += __shfl_xor_sync(0xffffffffu, v, 16);
           const double v0 = __shfl_sync(0xffffffffu, v, (2 * lane) & 7);
           const double v1 = __shfl_sync(0xffffffffu, v, (2 * lane + 1) & 7);
           const int b4 = (int)(nb & 7);
@@ -1535,7 +1554,7 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
       // the Gram ring replaces one column slot when both do not fit (>= 3 slots: blocks i .. i+2 live)
       const size_t ring_bytes = (size_t)LA_GR * LA_NG * sizeof(double), slot_la = (size_t)2 * Bk * p.slicepad * 8;
       smem_la = smem + ring_bytes;
-      const size_t cap = 227 * 1024 - 10 * 1024;   // the kernel's static shared memory (~9.6 KB) counts too
+      const size_t cap = 227 * 1024 - 14 * 1024;   // the kernel's static shared memory (~12.7 KB) counts too
       while (smem_la > cap && p.nslots > 4) {
         p.nslots -= 1;
         smem_la -= slot_la;
