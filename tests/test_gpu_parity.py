@@ -337,6 +337,37 @@ def test_rk_converges_c0():
 
 
 # ------------------------------------------------------------------ SP-SCD / SP-RCD (Alg. 5)
+@pytest.mark.parametrize("n,force_large", [(40, False), (1000, False), (1000, True)])
+@pytest.mark.parametrize("mode", [(0, 1), (1, 10 ** 6)])
+def test_scd_argmax_ties(n, force_large, mode, monkeypatch):
+    """Exact ties in the Alg. 5 step 8 argmax: A1 = 2 I, A2 = I / 2 (q = n),
+    b = (+-1, ...): r_j^2 is the same for every coordinate until it is zeroed, so every step is a
+    tie that must go to the smallest index of tau_t (reading of argmax). Covers the
+    one-warp (n = 40), one-CTA (n = 1000) and 16-CTA cluster (forced large) kernels; inner counts
+    and iterates against the oracle."""
+    from workloads.configs import IlsProblem
+    monkeypatch.setenv("ILS_FORCE_LARGE", "1" if force_large else "0")
+    A = np.vstack([2.0 * np.eye(n), 0.5 * np.eye(n)])
+    b = np.where(np.arange(2 * n) % 3 == 0, -1.0, 1.0)
+    pr = IlsProblem(name="ties", A=np.ascontiguousarray(A), b=b, p=n, q=n, xstar=np.zeros(n), consistent=False,
+                    tol=1e-8)
+    amode, ak = mode
+    K, T, ce = 2, 3 * n // 2, n // 4
+    ref = O.sp_scd_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE, seed=12, max_inner=T,
+                         check_every=ce, inner_tol=0.0, alpha_mode=amode, alpha_fixed=ak)
+    hist = np.zeros((K, n))
+    inner = np.zeros(K, dtype=np.int64)
+    x = np.zeros(n)
+    with H(pr) as hh:
+        o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, seed=12, max_inner=T, check_every=ce, inner_tol=0.0,
+                                 alpha_mode=amode, alpha_k=min(ak, 2 ** 31 - 1), x_hist=hist.ctypes.data,
+                                 inner_hist=inner.ctypes.data)
+        ils.ils_rgs_solve(hh.h, None, x, 0.0, K, o)
+    assert list(inner) == list(ref.inner_hist)
+    for k in range(K):
+        assert _rel(hist[k], ref.x_hist[k]) <= 1e-12, k
+
+
 @pytest.mark.parametrize("shape", [(200, 100, 50, 0.3), (130, 37, 67, 0.3), (257, 40, 3, 0.3)])
 @pytest.mark.parametrize("mode", [(0, 1, 0), (1, 1, 0), (1, 5, 0), (1, 10 ** 6, 0), (0, 1, 1)])
 def test_scd_fixed_horizon(shape, mode):
