@@ -1569,7 +1569,11 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
   }
   // chunks of check_every steps, each followed by the full-GPU inner check; launches are queued
   // ahead (kernels of a stopped solve return at once) and the stop flag is read every kBatch checks
-  constexpr int kBatch = 8;
+  int kBatch = 8;   // chunks queued between reads of the stop flag
+  {
+    const char* e = getenv("ILS_RK_KBATCH");   // experiment override
+    if (e && atoi(e) >= 1 && atoi(e) <= 256) kBatch = atoi(e);
+  }
   long long* prof = nullptr;
   {
     const char* e = getenv("ILS_RK_PROF");
