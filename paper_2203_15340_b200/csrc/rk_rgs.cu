@@ -1658,8 +1658,12 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
     const double nb = (double)((steps + Bk - 1) / Bk);
     for (int rk = 0; rk < p.C; ++rk) {
       const long long* q = hp + rk * 8;
-      fprintf(stderr, "ILS_RK_PROF k=%lld rank=%d blocks=%.0f cycles/block: wait %.0f local %.0f rscatter %.0f bar %.0f send %.0f recv %.0f sum %.0f rest %.0f\n",
-              (long long)k, rk, nb, q[0] / nb, q[1] / nb, q[2] / nb, q[3] / nb, q[4] / nb, q[5] / nb, q[6] / nb, q[7] / nb);
+      if (la)   // look-ahead kernel phases on compute thread 0 (LAP indices in rk_rgs_la_kernel)
+        fprintf(stderr, "ILS_RK_PROF k=%lld rank=%d blocks=%.0f cycles/block: products %.0f B1 %.0f T-wait %.0f T-read %.0f recurrence %.0f axpy %.0f TMA-wait %.0f fill-wait %.0f\n",
+                (long long)k, rk, nb, q[0] / nb, q[1] / nb, q[2] / nb, q[3] / nb, q[4] / nb, q[5] / nb, q[6] / nb, q[7] / nb);
+      else
+        fprintf(stderr, "ILS_RK_PROF k=%lld rank=%d blocks=%.0f cycles/block: wait %.0f local %.0f rscatter %.0f bar %.0f send %.0f recv %.0f sum %.0f rest %.0f\n",
+                (long long)k, rk, nb, q[0] / nb, q[1] / nb, q[2] / nb, q[3] / nb, q[4] / nb, q[5] / nb, q[6] / nb, q[7] / nb);
       if (la) {   // look-ahead helper warps: reduce warp (B1 -> data, data -> T posted), comm warp (send issue)
         const long long* r2 = hp + 128 + rk * 8;
         fprintf(stderr, "ILS_RK_PROF_LA rank=%d reduce: data wait %.0f T %.0f rest %.0f | comm: send %.0f z %.0f\n", rk,
