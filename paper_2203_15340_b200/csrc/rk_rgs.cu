@@ -1087,13 +1087,12 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
   }
   const int64_t nblk = (p.t1 - p.t0 + B - 1) / B;
   const uint32_t slice_bytes = (uint32_t)own * sizeof(double);
-  if (filler) {
-    for (int q = 0; q < 2; ++q) {   // 16 blocks ahead before the step loop starts
-      rk_fill_indices(p, Ss, ring, p.t0 + 32 * q, lane, bh_tab, rn_tab);
-      la_fill_gram(p, ring, gring, lam, 8 * q, lane);
-    }
-    if (lane == 0) filled_s = 16;
-  }
+  // 16 blocks ahead before the step loop starts, split over the fill and TMA warps (indices of both
+  // halves first: the Gram values of a block read the indices of the two blocks before it)
+  if (filler || tmaw) rk_fill_indices(p, Ss, ring, p.t0 + (tmaw ? 32 : 0), lane, bh_tab, rn_tab);
+  __syncthreads();
+  if (filler || tmaw) la_fill_gram(p, ring, gring, lam, tmaw ? 8 : 0, lane);
+  if (filler && lane == 0) filled_s = 16;
   auto issue = [&](int64_t blk, int slot) {   // 2B column slices of block blk (one thread)
     double* dst = slots + (size_t)slot * 2 * B * SP;
     mbar_arrive_expect_tx(&bars[slot], 2 * B * slice_bytes);
