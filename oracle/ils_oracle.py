@@ -244,14 +244,66 @@ def rk_rgs_inner(A1T, N, S, bhat, seed, k, max_inner, check_every, inner_tol,
     return z, t
 
 
+def _issparse(M) -> bool:
+    return hasattr(M, "tocsc")
+
+
+def _csc_sorted(M):
+    """A scipy.sparse matrix in CSC with ascending row indices in every column (canonical)."""
+    C = M.tocsc(copy=True)
+    C.sort_indices()
+    return C
+
+
+def rk_rgs_inner_sparse(A1c, N, S, bhat, seed, k, max_inner, check_every, inner_tol):
+    """rk_rgs_inner (Alg. 2 steps 6-12) for A1 stored by columns (scipy CSC,
+    configs[3]): the same steps in the same order, each column A1_(j) touched only on its stored
+    rows. The dense step's remaining entries are exact zeros, which add nothing to the dots and
+    leave w_i and (A1 z)_i unchanged, so this is the dense loop with the zero terms skipped
+    (pinned against rk_rgs_inner in tests/test_oracle_pins.py). Returns (z, steps)."""
+    p, n = A1c.shape
+    ip, ri, va = A1c.indptr, A1c.indices, A1c.data
+    w = np.zeros(p)
+    z = np.zeros(n)
+    az = np.zeros(p)
+    nb = float(np.linalg.norm(bhat))
+    if nb == 0.0:
+        return z, 0
+    t = 0
+    CH = 4096
+    while t < max_inner:
+        cnt = min(CH, max_inner - t)
+        J1, J2 = ix.rk_rgs_indices(seed, k, t, cnt, S)
+        for c in range(cnt):
+            j1, j2 = int(J1[c]), int(J2[c])
+            r1, v1 = ri[ip[j1]:ip[j1 + 1]], va[ip[j1]:ip[j1 + 1]]
+            s1 = (bhat[j1] - v1 @ w[r1]) / N[j1]           # step 9 (RK on A1^T w = b_hat)
+            w[r1] += s1 * v1
+            r2, v2 = ri[ip[j2]:ip[j2 + 1]], va[ip[j2]:ip[j2 + 1]]
+            s2 = (v2 @ (w[r2] - az[r2])) / N[j2]          # step 11 (RGS on A1 z = w)
+            z[j2] += s2
+            az[r2] += s2 * v2
+            t += 1
+            if t % check_every == 0:                      # reading R2
+                az = A1c @ z
+                g = A1c.T @ az - bhat
+                if float(np.linalg.norm(g)) <= inner_tol * nb:
+                    return z, t
+    return z, t
+
+
 def sp_rk_rgs_solve(A1, A2, b1, b2, x0=None, tol=1e-8, max_iter=20000, stop=STOP_XREF,
                     x_ref=None, seed=0, max_inner=100000, check_every=None,
                     inner_tol=1e-12, rhs_literal=False) -> Report:
     """SP-RK-RGS, Alg. 2: outer b_hat = A2bar x_k + A^T J b (step 5),
     inner RK-RGS (steps 6-12), x_{k+1} = z (step 13)."""
     n = A1.shape[1]
-    A1T = np.ascontiguousarray(A1.T)
-    N = ix.column_norms_sq(A1)
+    if _issparse(A1):   # CSR/CSC input (configs[3]): the column-wise path, same steps
+        A1c = _csc_sorted(A1)
+        N = ix.column_norms_sq_csc(A1c.indptr, A1c.data, n)
+    else:
+        A1T = np.ascontiguousarray(A1.T)
+        N = ix.column_norms_sq(A1)
     _, S = ix.weights_prefix(N)
     ce = n if check_every is None else check_every
     if rhs_literal:   # Alg. 2 steps 2-3 (PAPER.md:291-292)
@@ -260,7 +312,10 @@ def sp_rk_rgs_solve(A1, A2, b1, b2, x0=None, tol=1e-8, max_iter=20000, stop=STOP
     rep = Report(x=x)
     for k in range(max_iter):
         bhat = sp_rhs_literal(A2bar, AJb, x) if rhs_literal else sp_rhs(A1, A2, b1, b2, x)
-        x, steps = rk_rgs_inner(A1T, N, S, bhat, seed, k, max_inner, ce, inner_tol)
+        if _issparse(A1):
+            x, steps = rk_rgs_inner_sparse(A1c, N, S, bhat, seed, k, max_inner, ce, inner_tol)
+        else:
+            x, steps = rk_rgs_inner(A1T, N, S, bhat, seed, k, max_inner, ce, inner_tol)
         rep.inner_iters_total += steps
         rep.inner_hist.append(steps)
         rep.outer_iters = k + 1
@@ -327,14 +382,53 @@ def scd_inner(G, N, S, bhat, seed, k, max_inner, check_every, inner_tol,
     return beta, t
 
 
+def scd_inner_sparse(Gc, N, S, bhat, seed, k, max_inner, check_every, inner_tol,
+                     alpha_mode=0, alpha_fixed=1, weighted=False):
+    """scd_inner (Alg. 5 steps 5-11) with A1bar = A1^T A1 stored sparse (scipy
+    CSR, configs[3]): step 11's update r -= s A1bar_(j) touches only the stored entries of row j;
+    the skipped entries are exact zeros (r_i - s*0 = r_i). Pinned against scd_inner in
+    tests/test_oracle_pins.py. Returns (beta, steps)."""
+    n = Gc.shape[0]
+    ip, ci, va = Gc.indptr, Gc.indices, Gc.data
+    beta = np.zeros(n)
+    r = bhat.copy()
+    nb = float(np.linalg.norm(bhat))
+    if nb == 0.0:
+        return beta, 0
+    t = 0
+    while t < max_inner:
+        if weighted:
+            j = int(ix.rcd_indices(seed, k, t, 1, S)[0])
+        else:
+            _, tau = ix.scd_subset(seed, k, t, n, alpha_mode, alpha_fixed)
+            j = scd_select(r, tau)
+        s = r[j] / N[j]                                   # step 10 (A1bar_jj = N_j, R13)
+        beta[j] += s
+        cols = ci[ip[j]:ip[j + 1]]
+        r[cols] -= s * va[ip[j]:ip[j + 1]]                # step 11
+        t += 1
+        if t % check_every == 0:
+            r = bhat - Gc @ beta
+            if float(np.linalg.norm(r)) <= inner_tol * nb:
+                return beta, t
+    return beta, t
+
+
 def sp_scd_solve(A1, A2, b1, b2, x0=None, tol=1e-8, max_iter=20000, stop=STOP_XREF,
                  x_ref=None, seed=0, max_inner=100000, check_every=None, inner_tol=1e-12,
                  alpha_mode=0, alpha_fixed=1, weighted=False, rhs_literal=False) -> Report:
     """SP-SCD, Alg. 5. A1bar = A1^T A1 formed once (step 2); the outer
     right side b_hat = A2bar x_k + A^T J b (step 4) is formed as sp_rhs(x_k)."""
     n = A1.shape[1]
-    G = A1.T @ A1
-    N = ix.column_norms_sq(A1)
+    sparse = _issparse(A1)
+    if sparse:   # CSR/CSC input (configs[3]): A1bar kept sparse, same steps
+        A1c = _csc_sorted(A1)
+        G = (A1c.T @ A1c).tocsr()
+        G.sort_indices()
+        N = ix.column_norms_sq_csc(A1c.indptr, A1c.data, n)
+    else:
+        G = A1.T @ A1
+        N = ix.column_norms_sq(A1)
     _, S = ix.weights_prefix(N)
     ce = n if check_every is None else check_every
     if rhs_literal:   # Alg. 5 step 2 (PAPER.md:689)
@@ -343,8 +437,8 @@ def sp_scd_solve(A1, A2, b1, b2, x0=None, tol=1e-8, max_iter=20000, stop=STOP_XR
     rep = Report(x=x)
     for k in range(max_iter):
         bhat = sp_rhs_literal(A2bar, AJb, x) if rhs_literal else sp_rhs(A1, A2, b1, b2, x)
-        x, steps = scd_inner(G, N, S, bhat, seed, k, max_inner, ce, inner_tol,
-                             alpha_mode, alpha_fixed, weighted)
+        inner = scd_inner_sparse if sparse else scd_inner
+        x, steps = inner(G, N, S, bhat, seed, k, max_inner, ce, inner_tol, alpha_mode, alpha_fixed, weighted)
         rep.inner_iters_total += steps
         rep.inner_hist.append(steps)
         rep.outer_iters = k + 1

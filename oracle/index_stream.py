@@ -76,6 +76,22 @@ def column_norms_sq(A1: np.ndarray) -> np.ndarray:
     return N
 
 
+def column_norms_sq_csc(indptr: np.ndarray, data: np.ndarray, n: int) -> np.ndarray:
+    """The same N_j for A1 stored by columns (CSC with ascending row indices per column, e.g.
+    configs[3]): the stored entries of column j are added in ascending row order, each square
+    rounded before the add. The structural zeros the dense loop also adds leave every partial sum
+    unchanged (s + 0.0 = s exactly), so this equals column_norms_sq on the densified matrix bit for
+    bit (pinned in tests/test_oracle_pins.py). Rank r of every column is added in pass r."""
+    indptr = np.asarray(indptr, dtype=np.int64)
+    cnt = np.diff(indptr)
+    N = np.zeros(n)
+    for r in range(int(cnt.max()) if n else 0):
+        cols = np.flatnonzero(cnt > r)
+        v = data[indptr[cols] + r]
+        N[cols] = N[cols] + v * v
+    return N
+
+
 def weights_prefix(N: np.ndarray):
     """Integer weights W_j = max(1, floor(N_j / N_max * 2^32)) and inclusive prefix sums
     S_j = sum_{i<=j} W_i (Python ints, exact)."""

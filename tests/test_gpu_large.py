@@ -25,6 +25,15 @@ def _rel(a, b):
     return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
 
 
+def _par(a, b):
+    """Parity distance of two iterates: the larger of the norm-wise relative difference (the
+    north_star bar) and the element-wise max |a_i - b_i| / max |b_i|, so that a wrong small
+    coordinate cannot hide inside the norm."""
+    a, b = np.asarray(a), np.asarray(b)
+    d = np.abs(a - b)
+    return max(_rel(a, b), float(d.max() / max(np.abs(b).max(), 1e-300)) if d.size else 0.0)
+
+
 class Big:
     def __init__(self, pr, monkeypatch=None, force=True):
         if monkeypatch is not None:
@@ -57,7 +66,7 @@ def test_large_sp_fixed_horizon(shape, form, monkeypatch):
         st, rep = ils.ils_sp_solve(hh.h, None, x, 0.0, K, o)
     assert rep.outer_iters == K
     for k in range(K):
-        assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
+        assert _par(hist[k], ref.x_hist[k]) <= 1e-9, k
 
 
 def test_large_sp_rr_stop_and_relative_residual(monkeypatch):
@@ -90,7 +99,7 @@ def test_large_rk_fixed_horizon(shape, T, ce, itol, monkeypatch):
         ils.ils_rk_solve(hh.h, None, x, 0.0, K, o)
     assert list(inner) == list(ref.inner_hist)
     for k in range(K):
-        assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
+        assert _par(hist[k], ref.x_hist[k]) <= 1e-9, k
 
 
 @pytest.mark.parametrize("shape", SHAPES)
@@ -113,7 +122,7 @@ def test_large_scd_fixed_horizon(shape, mode, monkeypatch):
         ils.ils_rgs_solve(hh.h, None, x, 0.0, K, o)
     assert list(inner) == list(ref.inner_hist)
     for k in range(K):
-        assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
+        assert _par(hist[k], ref.x_hist[k]) <= 1e-9, k
 
 
 def test_large_methods_converge(monkeypatch):
@@ -152,7 +161,7 @@ def test_large_real_n_above_8192(monkeypatch):
             o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, seed=2, inner_tol=0.0, x_hist=hist.ctypes.data, **kw)
             fn(hh.h, None, x, 0.0, K, o)
             for k in range(K):
-                assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, (fn, kw, k)
+                assert _par(hist[k], ref.x_hist[k]) <= 1e-9, (fn, kw, k)
         # the explicit B = P A2bar of sp_form 2 is not formed at n >= 8192 (P is applied implicitly)
         with pytest.raises(ils.IlsError) as e:
             ils.ils_sp_solve(hh.h, None, np.zeros(n), 0.0, 1, ils.ils_default_opts(stop=ils.ILS_STOP_NONE, sp_form=2))
@@ -187,4 +196,4 @@ def test_paper_family_parity(shape):
             if fn is not ils.ils_sp_solve:
                 assert list(inner) == list(ref.inner_hist), fn
             for k in range(K):
-                assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, (fn, k)
+                assert _par(hist[k], ref.x_hist[k]) <= 1e-9, (fn, k)

@@ -22,6 +22,15 @@ def _rel(a, b):
     return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
 
 
+def _par(a, b):
+    """Parity distance of two iterates: the larger of the norm-wise relative difference (the
+    north_star bar) and the element-wise max |a_i - b_i| / max |b_i|, so that a wrong small
+    coordinate cannot hide inside the norm."""
+    a, b = np.asarray(a), np.asarray(b)
+    d = np.abs(a - b)
+    return max(_rel(a, b), float(d.max() / max(np.abs(b).max(), 1e-300)) if d.size else 0.0)
+
+
 class H:
     """Handle on a problem; A, b passed as device tensors (or host arrays if host=True)."""
 
@@ -88,7 +97,7 @@ def test_direct_solve(shape):
     with H(pr, host=True) as hh:
         ils.ils_direct_solve(hh.h, x)
         rr = ils.ils_relative_residual(hh.h, x)
-    assert _rel(x, xo) <= 1e-10
+    assert _par(x, xo) <= 1e-10
     assert rr <= 1e-20 and abs(rr - O.relative_residual(pr.A1, pr.A2, pr.b1, pr.b2, x)) <= 1e-18
 
 
@@ -179,8 +188,8 @@ def test_sp_fixed_horizon(shape, form):
         st, rep = ils.ils_sp_solve(hh.h, None, x, 0.0, K, o)
     assert rep.outer_iters == K
     for k in range(K):
-        assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
-    assert _rel(x, ref.x) <= 1e-9
+        assert _par(hist[k], ref.x_hist[k]) <= 1e-9, k
+    assert _par(x, ref.x) <= 1e-9
 
 
 @pytest.mark.parametrize("cfg", ["c0", "c1"])
@@ -205,7 +214,7 @@ def test_sp_q0_one_step():
     with H(pr) as hh:
         o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE)
         ils.ils_sp_solve(hh.h, None, x, 0.0, 1, o)
-    assert _rel(x, xls) <= 1e-11
+    assert _par(x, xls) <= 1e-11
 
 
 def test_sp_rr_stop():
@@ -237,7 +246,7 @@ def test_rk_fixed_horizon(shape, T):
                                  x_hist=hist.ctypes.data, inner_hist=inner.ctypes.data)
         st, rep = ils.ils_rk_solve(hh.h, None, x, 0.0, K, o)
     for k in range(K):
-        assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
+        assert _par(hist[k], ref.x_hist[k]) <= 1e-9, k
     # inner_tol = 0 stops only on an exactly zero gradient; with tiny n the iteration can reach
     # that at a check on one side and not the other (a stop decision at a threshold, R25)
     for g, o_ in zip(inner, ref.inner_hist):
@@ -259,7 +268,7 @@ def test_rk_cluster_path_c1_horizon(monkeypatch):
                                  x_hist=hist.ctypes.data)
         ils.ils_rk_solve(hh.h, None, x, 0.0, K, o)
     for k in range(K):
-        assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
+        assert _par(hist[k], ref.x_hist[k]) <= 1e-9, k
 
 
 def test_rk_lookahead_kernel_c1_horizon(monkeypatch):
@@ -277,7 +286,7 @@ def test_rk_lookahead_kernel_c1_horizon(monkeypatch):
                                  x_hist=hist.ctypes.data)
         ils.ils_rk_solve(hh.h, None, x, 0.0, K, o)
     for k in range(K):
-        assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
+        assert _par(hist[k], ref.x_hist[k]) <= 1e-9, k
 
 
 @pytest.mark.parametrize("T,ce", [(1, 1000), (5, 3), (7, 4), (130, 64)])
@@ -295,7 +304,7 @@ def test_rk_cluster_short_horizons(T, ce):
                                  x_hist=hist.ctypes.data)
         ils.ils_rk_solve(hh.h, None, x, 0.0, K, o)
     for k in range(K):
-        assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
+        assert _par(hist[k], ref.x_hist[k]) <= 1e-9, k
 
 
 @pytest.mark.parametrize("shape", [(10000, 500, 700), (7900, 300, 1500)])
@@ -320,7 +329,7 @@ def test_rk_cluster_geometries(shape, T, ce, la, monkeypatch):
         ils.ils_rk_solve(hh.h, None, x, 0.0, K, o)
     assert list(inner) == list(ref.inner_hist)
     for k in range(K):
-        assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
+        assert _par(hist[k], ref.x_hist[k]) <= 1e-9, k
 
 
 def test_rk_converges_c0():
@@ -365,7 +374,7 @@ def test_scd_argmax_ties(n, force_large, mode, monkeypatch):
         ils.ils_rgs_solve(hh.h, None, x, 0.0, K, o)
     assert list(inner) == list(ref.inner_hist)
     for k in range(K):
-        assert _rel(hist[k], ref.x_hist[k]) <= 1e-12, k
+        assert _par(hist[k], ref.x_hist[k]) <= 1e-12, k
 
 
 @pytest.mark.parametrize("shape", [(200, 100, 50, 0.3), (130, 37, 67, 0.3), (257, 40, 3, 0.3)])
@@ -386,7 +395,7 @@ def test_scd_fixed_horizon(shape, mode):
                                  x_hist=hist.ctypes.data)
         ils.ils_rgs_solve(hh.h, None, x, 0.0, K, o)
     for k in range(K):
-        assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
+        assert _par(hist[k], ref.x_hist[k]) <= 1e-9, k
 
 
 def test_scd_converges_c0():
@@ -431,7 +440,7 @@ def test_batched_vs_oracle(method):
         else:
             ref = O.sp_scd_solve(A1, A2, b1, b2, seed=100 + i, max_inner=T, check_every=ce, inner_tol=0.0,
                                  weighted=(method == "rcd"), **kw)
-        assert _rel(x[i], ref.x) <= 1e-9, (method, i)
+        assert _par(x[i], ref.x) <= 1e-9, (method, i)
 
 
 def test_batched_converges_c4_subset():
@@ -450,28 +459,6 @@ def test_batched_converges_c4_subset():
         assert st == ils.ILS_OK and sts.all()
         err = np.linalg.norm(x - bt.xstar, axis=1) / np.linalg.norm(bt.xstar, axis=1)
         assert err.max() <= 1e-10
-
-
-# ------------------------------------------------------------------ full-size configs
-def test_c2_full_size_sp_iterates_and_convergence():
-    """configs[2] at full size (p=40000, q=10000, n=4000, ill-conditioned) in the bench's launch
-    configuration: the first two SP iterates match the oracle's (1e-9, the paper-form floor is
-    ~1e-10, SURVEY Appendix A probe 3) and SP reaches 1e-8 against x* (consistent b = A x*)."""
-    pr = make_problem("c2")
-    K = 2
-    ref = O.sp_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE)
-    hist = np.zeros((K, pr.n))
-    x = torch.zeros(pr.n, dtype=torch.float64, device=DEV)
-    xs = torch.from_numpy(pr.xstar).to(DEV)
-    with H(pr) as hh:
-        o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, x_hist=hist.ctypes.data)
-        ils.ils_sp_solve(hh.h, None, x, 0.0, K, o)
-        for k in range(K):
-            assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
-        o = ils.ils_default_opts(x_ref=xs.data_ptr())
-        st, rep = ils.ils_sp_solve(hh.h, None, x, pr.tol, 100, o)
-    assert st == ils.ILS_OK and rep.converged
-    assert _rel(x.cpu().numpy(), pr.xstar) <= pr.tol
 
 
 # ------------------------------------------------------------------ paper-literal precompute (sp_form 2)
@@ -498,7 +485,7 @@ def test_literal_precompute_forms(method):
         fn = {"sp": ils.ils_sp_solve, "rk": ils.ils_rk_solve, "rgs": ils.ils_rgs_solve}[method]
         fn(hh.h, None, x, 0.0, K, o)
     for k in range(K):
-        assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
+        assert _par(hist[k], ref.x_hist[k]) <= 1e-9, k
 
 
 # ------------------------------------------------------------------ full-size bench configurations
@@ -541,7 +528,7 @@ def test_scd_c1_fixed_horizon():
         o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, seed=0, max_inner=T, check_every=ce, inner_tol=0.0,
                                  x_hist=hist.ctypes.data)
         ils.ils_rgs_solve(hh.h, None, x, 0.0, K, o)
-    assert _rel(hist[0], ref.x_hist[0]) <= 1e-9
+    assert _par(hist[0], ref.x_hist[0]) <= 1e-9
 
 
 def test_c4_full_size_all_instances_converge():

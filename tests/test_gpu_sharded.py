@@ -21,6 +21,15 @@ def _rel(a, b):
     return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
 
 
+def _par(a, b):
+    """Parity distance of two iterates: the larger of the norm-wise relative difference (the
+    north_star bar) and the element-wise max |a_i - b_i| / max |b_i|, so that a wrong small
+    coordinate cannot hide inside the norm."""
+    a, b = np.asarray(a), np.asarray(b)
+    d = np.abs(a - b)
+    return max(_rel(a, b), float(d.max() / max(np.abs(b).max(), 1e-300)) if d.size else 0.0)
+
+
 @pytest.fixture(scope="module")
 def comm():
     c = ils.ils_comm_create(ils.ils_comm_unique_id(), 1, 0)
@@ -51,7 +60,7 @@ def test_sharded_sp_fixed_horizon(comm, shape, form):
         ils.ils_destroy(h)
     assert rep.outer_iters == K
     for k in range(K):
-        assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
+        assert _par(hist[k], ref.x_hist[k]) <= 1e-9, k
 
 
 def test_sharded_sp_stops_and_residual(comm):
@@ -93,7 +102,7 @@ def test_sharded_scd_fixed_horizon(comm, mode):
         ils.ils_destroy(h)
     assert list(inner) == list(ref.inner_hist)
     for k in range(K):
-        assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, k
+        assert _par(hist[k], ref.x_hist[k]) <= 1e-9, k
 
 
 def test_sharded_unsupported_modes_and_shapes(comm):
@@ -144,6 +153,6 @@ def test_sharded_with_large_n_routing(comm, monkeypatch):
             o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, x_hist=hist.ctypes.data, **kw)
             fn(h, None, x, 0.0, K, o)
             for k in range(K):
-                assert _rel(hist[k], ref.x_hist[k]) <= 1e-9, (fn, k)
+                assert _par(hist[k], ref.x_hist[k]) <= 1e-9, (fn, k)
     finally:
         ils.ils_destroy(h)

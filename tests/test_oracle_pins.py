@@ -47,6 +47,8 @@ def test_p1_two_by_two_closed_form():
     assert abs(O.spectral_radius_sp(A1, A2) - g["rho"]) < 1e-15
     assert O.relative_residual(A1, A2, b1, b2, np.zeros(2)) == g["rr_at_zero"]
     assert O.relative_residual(A1, A2, b1, b2, _np(g, "x_star")) == g["rr_at_xstar"]
+    # the squared reading of RR (R15): 9/160 at x_1, where the unsquared ratio would be 0.237
+    assert O.relative_residual(A1, A2, b1, b2, _np(g, "sp_iterates")[0]) == g["rr_at_x1"]
 
 
 # ---------------------------------------------------------------- P2: single steps
@@ -442,6 +444,36 @@ def test_sparse_inputs_match_the_pinned_dense_oracle():
     # the generator's CSR layout: sorted distinct columns, row_ptr consistent
     assert np.all(np.diff(pr.row_ptr) == 5)
     assert all(np.all(np.diff(pr.col_idx[pr.row_ptr[i]:pr.row_ptr[i + 1]]) > 0) for i in range(pr.m))
+
+
+@pytest.mark.parametrize("shape", [(400, 80, 30, 5), (3000, 200, 12, 2), (150, 40, 60, 7)])
+def test_sparse_column_path_matches_the_pinned_dense_oracle(shape):
+    """P18b: the oracle's column-wise CSC path (rk_rgs_inner_sparse, scd_inner_sparse,
+    column_norms_sq_csc -- what it runs on configs[3] at full size) equals the pinned dense path on
+    the densified matrix: column norms bit for bit, identical inner counts (stop decisions) and
+    iterates to rounding, for SP-RK-RGS, SP-SCD (uniform alpha, Motzkin) and weighted SP-RCD.
+    Shape (3000, 200, 12, 2) gives ~500 stored entries per column."""
+    from workloads import make_sparse
+    p, q, n, k = shape
+    pr = make_sparse(p, q, n, k, seed=31)
+    S = pr.scipy()
+    A = pr.dense()
+    A1c = S[:p].tocsc()
+    A1c.sort_indices()
+    Nd = ix.column_norms_sq(A[:p])
+    Ns = ix.column_norms_sq_csc(A1c.indptr, A1c.data, n)
+    assert np.array_equal(Nd.view(np.uint64), Ns.view(np.uint64))
+    sp_args = (S[:p], S[p:], pr.b[:p], pr.b[p:])
+    de_args = (A[:p], A[p:], pr.b[:p], pr.b[p:])
+    kw = dict(max_iter=3, stop=O.STOP_NONE, seed=4, max_inner=700, check_every=50, inner_tol=1e-7)
+    cases = [(O.sp_rk_rgs_solve, {}), (O.sp_scd_solve, {}), (O.sp_scd_solve, dict(alpha_mode=1, alpha_fixed=n)),
+             (O.sp_scd_solve, dict(weighted=True))]
+    for fn, extra in cases:
+        rs = fn(*sp_args, **kw, **extra)
+        rd = fn(*de_args, **kw, **extra)
+        assert rs.inner_hist == rd.inner_hist, (fn.__name__, extra)
+        for a, b in zip(rs.x_hist, rd.x_hist):
+            assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(b), (fn.__name__, extra)
 
 
 # ---------------------------------------------------------------- P19 the paper's own families
