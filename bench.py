@@ -58,6 +58,13 @@ def workload_desc(cfg: str) -> str:
     }[cfg]
 
 
+def config_dict(cfg: str, methods, world: int) -> dict:
+    """The line's `config` (identical for the GPU arm and the reference arm)."""
+    return {"workload": workload_desc(cfg), "methods": list(methods),
+            "parallelism": ("instance-partition" if cfg == "c4" else "replicas") if world > 1 else "single-gpu",
+            "l2": "flushed between timed steps (256 MiB write)"}
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -329,6 +336,76 @@ def roofline(steps, peak_hbm, peak_bf16, traffic_map, cfg):
     return d
 
 
+def validity(steps, errs, tol):
+    """(valid, reason): every timed step of every method returned ILS_OK and the final iterates are
+    within the config tolerance of x_ref; a capped (ILS_NOT_CONVERGED) run is not a time-to-tolerance."""
+    bad = []
+    for m in steps[0][2]:
+        sts = sorted({int(s[2][m]["status"]) for s in steps})
+        if sts != [0]:
+            bad.append(f"{m}: status {sts}")
+        if not (errs[m] <= tol):
+            bad.append(f"{m}: rel err {errs[m]:.3e} > tol {tol:g}")
+    return (not bad), "; ".join(bad) or None
+
+
+def config_block(cfgs, torch, dev, peak_hbm, flushbuf, steps=3, warmup=2):
+    """Compact results of the other BASELINE.json configs in the same run (same timing rules: inputs
+    resident in HBM, L2 flushed between steps, CUDA events on the launching stream). For c2 the
+    K1 + P stream of SP (`sp_persistent_kernel`, one launch for all outer steps) is reported against
+    the measured HBM peak with the algorithmic bytes 8q(n+1) + 8n^2 per outer step (SURVEY.md §8(d));
+    for c4 the batched methods' effective GB/s of A touched (on-chip served, not an HBM claim)."""
+    out = {}
+    for cfg in cfgs:
+        t_gen = time.perf_counter()
+        pr, xref = load_problem(cfg)
+        gen_s = time.perf_counter() - t_gen
+        methods = DEFAULT_METHODS[cfg].split(",")
+        run = Runner(cfg, pr, xref, methods, torch, dev)
+        for _ in range(warmup):
+            flush_l2(flushbuf)
+            run.step()
+        sts = []
+        for _ in range(steps):
+            flush_l2(flushbuf)
+            torch.cuda.synchronize()
+            sts.append(run.step())
+        errs = run.errors()
+        per = summarise_methods(sts, cfg, pr, peak_hbm)
+        ok, why = validity(sts, errs, pr.tol)
+        blk = {"workload": workload_desc(cfg), "steps": steps, "ms": round(statistics.mean(x[0] for x in sts), 4),
+               "valid": ok, "invalid_reason": why, "generate_s": round(gen_s, 1), "per_method": {}}
+        for m, d in per.items():
+            keep = {k: d[k] for k in ("ms", "setup_ms", "solve_ms", "outer", "inner", "converged",
+                                      "algorithmic_GBps", "frac_of_measured_hbm") if k in d}
+            keep["max_rel_err_vs_xref"] = errs[m]
+            blk["per_method"][m] = keep
+        if cfg == "c2" and "sp" in methods:
+            ms = sum(x[2]["sp"]["hot_ms"][0] for x in sts)
+            work = sum(x[2]["sp"]["hot_work"][0] for x in sts)
+            if ms > 0:
+                gbs = work / (ms * 1e-3) / 1e9
+                o = sts[-1][2]["sp"]["outer_iters"]
+                blk["k1p_stream"] = {
+                    "kernel": "sp_persistent_kernel (K1 fused A2 stream + P apply, all outer steps in one launch)",
+                    "GBps": round(gbs, 1), "frac_of_measured_hbm": round(gbs / peak_hbm, 4),
+                    "frac_of_8TBps": round(gbs / HBM_NOMINAL_GBS, 4), "peak_hbm_gbs": peak_hbm,
+                    "bytes_per_outer": 8.0 * pr.q * (pr.n + 1) + 8.0 * pr.n * pr.n, "outer": o,
+                    "kernel_ms_per_solve": round(ms / len(sts), 4),
+                    "note": "algorithmic bytes 8q(n+1) (A2 rows + b2) + 8n^2 (P) per outer step / kernel time "
+                            "(CUDA events around the launch on the handle's stream); A2 + P = 450 MB per step, "
+                            "far above the 126 MB L2"}
+            try:
+                with open(os.path.join(ROOT, "profiles", "c2_rho.json")) as f:
+                    blk["rho_sp"] = json.load(f)
+            except OSError:
+                pass
+        out[cfg] = blk
+        del run
+        torch.cuda.empty_cache()
+    return out
+
+
 # ------------------------------------------------------------------------------------------ oracle
 def oracle_sample(cfg, pr, xref, counts, methods, budget_s=20.0):
     """CPU oracle (test infrastructure) on a bounded sample of the workload, extrapolated to the
@@ -336,11 +413,13 @@ def oracle_sample(cfg, pr, xref, counts, methods, budget_s=20.0):
     Returns (total_ms, per_method_ms, sample description, cores)."""
     from oracle import ils_oracle as O
     from oracle import index_stream as ix
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    except Exception:
-        cores = os.cpu_count() or 1
+    from threadpoolctl import threadpool_limits
+    cores = 1   # the oracle is timed single-threaded (BLAS pinned to one thread, north_star)
+    with threadpool_limits(limits=1):
+        return _oracle_sample(O, ix, cfg, pr, xref, counts, methods, budget_s, cores)
+
+
+def _oracle_sample(O, ix, cfg, pr, xref, counts, methods, budget_s, cores):
     if hasattr(pr, "scipy"):
         S = pr.scipy()
         A1, A2, b1, b2 = S[:pr.p], S[pr.p:], pr.b[:pr.p], pr.b[pr.p:]
@@ -418,7 +497,7 @@ def run_reference(a, rank, world):
     line = {"metric": METRIC, "value": round(v, 3), "unit": "ms", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": round(v, 3), "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload_desc(cfg), "methods": methods},
+            "config": config_dict(cfg, methods, world),
             "per_method_ms": {m: round(x, 2) for m, x in per.items()},
             "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": cores, "kind": "oracle",
                              "sample": note + f"; wall per sample step {statistics.mean(walls):.0f} ms"},
@@ -436,6 +515,8 @@ def main():
     ap.add_argument("--methods", default=None, help="default: per config (DEFAULT_METHODS)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--extra-configs", default="c0,c2,c3,c4",
+                    help="other configs measured in the same run (compact block); '' to skip")
     a = ap.parse_args()
     if a.methods is None:
         a.methods = DEFAULT_METHODS[a.config]
@@ -512,14 +593,21 @@ def main():
     per = summarise_methods(steps, cfg, pr, peak_hbm)
     for m in per:
         per[m]["max_rel_err_vs_xref"] = errs[m]
+    valid, why = validity(steps, errs, pr.tol)
+    extra = None
+    if rank == 0 and world == 1 and a.extra_configs:
+        del run
+        torch.cuda.empty_cache()
+        extra = config_block([c for c in a.extra_configs.split(",") if c and c != cfg], torch, dev, peak_hbm,
+                             flushbuf)
     line = {"metric": METRIC, "value": round(value, 4), "unit": "ms", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": round(value, 4), "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_desc(cfg), "methods": methods,
-                       "parallelism": ("instance-partition" if cfg == "c4" else "replicas") if world > 1 else "single-gpu",
-                       "l2": "flushed between timed steps (256 MiB write)",
-                       "create_ms": round(statistics.mean(s[1] for s in steps), 4)},
+            "config": config_dict(cfg, methods, world),
+            "create_ms": round(statistics.mean(s[1] for s in steps), 4),
+            "valid": valid, "invalid_reason": why,
             "per_method": per,
+            "configs": extra,
             "roofline": roofline(steps, peak_hbm, peak_bf16, traffic_map, cfg),
             "peaks_source": peak_src,
             "gpu_launches": launches, "clocks": clocks, "e2e": e2e}

@@ -7,7 +7,9 @@
 //            reduction) then acc += sigma_i d_i a_i (register accumulators).
 //   phase B  c = base + sum_cta partial_cta   (fixed CTA order: deterministic)
 //            paper form: c_k = A1^T b1 + A2^T (A2 x_k - b2) = A2bar x_k + A^T J b (Alg. 2 step 5)
-//   phase C  x_{k+1} = P c_k (paper form) or x_k + P g_k (correction form, reading R14)
+//   phase C  x_{k+1} = P c_k (paper form) or x_k + P g_k (correction form, reading R14), the rows
+//            of P streamed through the same TMA ring as A2 (one row stream per CTA across phases
+//            and outer steps, so HBM stays busy through the grid barriers)
 //   phase D  stop test ||x_{k+1} - x_ref|| <= tol ||x_ref|| evaluated redundantly by every CTA.
 // rhs_only: phases A+B for one x (b_hat for SP-RK-RGS / SP-SCD, or g = A^T J (b - A x) for RR).
 #include <cooperative_groups.h>
@@ -19,9 +21,11 @@ namespace cg = cooperative_groups;
 
 namespace ils {
 
-constexpr int SP_THREADS = 512;
-constexpr int SP_WARPS = SP_THREADS / 32;
+constexpr int SPW = 16;                     // consumer warps
+constexpr int SP_CONS = SPW * 32;           // consumer threads (own the column pairs of x, c, acc)
+constexpr int SP_THREADS = SP_CONS;
 constexpr int SP_RMAX = 16;                 // rows per ring stage (max)
+constexpr int SP_NRED = 8;                  // partial-dot buffers (>= ring stages: reuse safety)
 constexpr int SP_STAGE_TARGET = 65536;      // bytes per ring stage (target)
 
 struct SpParams {
@@ -56,9 +60,58 @@ struct SpParams {
   int64_t t_now;
 };
 
+// Software grid barrier (one arrival per CTA, generation counter in DevStatus); the TMA ring keeps
+// filling while the CTA waits. Co-residency is guaranteed by the cooperative launch.
+__device__ __forceinline__ void sp_grid_barrier(DevStatus* st, int tid) {
+  named_bar_sync(1, SP_CONS);
+  if (tid == 0) {
+    volatile uint32_t* gen = &st->gbar_gen;
+    const uint32_t g0 = *gen;
+    __threadfence();
+    if (atomicAdd(&st->gbar_count, 1u) == gridDim.x - 1) {
+      st->gbar_count = 0;
+      __threadfence();
+      atomicAdd(&st->gbar_gen, 1u);
+    } else {
+      while (*gen == g0) {
+      }
+    }
+    __threadfence();
+  }
+  named_bar_sync(1, SP_CONS);
+}
+
+// Sum of v[c] over c in [0, G) in one fixed order, computed by warp 0 (lane l adds c = l, l+32, ...,
+// then a butterfly), result broadcast through shared memory to all consumer threads.
+__device__ __forceinline__ void sp_sum2_over_ctas(const double* red, int G, int tid, double* bc, double& a,
+                                                  double& b) {
+  if (tid < 32) {
+    double x = 0.0, y = 0.0;
+    for (int c = tid; c < G; c += 32) {
+      x += red[2 * c];
+      y += red[2 * c + 1];
+    }
+    x = warp_sum(x);
+    y = warp_sum(y);
+    if (tid == 0) {
+      bc[0] = x;
+      bc[1] = y;
+    }
+  }
+  named_bar_sync(1, SP_CONS);
+  a = bc[0];
+  b = bc[1];
+  named_bar_sync(1, SP_CONS);
+}
+
+// Row stream per CTA: the CTA walks its stages (A2 rows of every outer step, then its rows of P)
+// through a ring of TMA bulk copies; the 16th warp to release a slot refills it at once. The warps
+// never meet at a CTA barrier inside a phase: a stage's per-warp partial dots are posted to a
+// split-phase mbarrier (rfull) and the stage is finished -- 16-way sum, axpy from the same smem
+// copy, slot release -- only after the NEXT stage's dots are issued, so the cross-warp reduction
+// latency hides behind independent work.
 template <int NPAIR>
 __global__ void __launch_bounds__(SP_THREADS, 1) sp_persistent_kernel(SpParams prm) {
-  cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = gridDim.x, bid = blockIdx.x;
@@ -66,97 +119,171 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sp_persistent_kernel(SpParams p
   const int R = prm.rows_per_stage, NS = prm.nstages;
   const int64_t stage_dbl = (int64_t)R * npad;
   double* ring = reinterpret_cast<double*>(smem_raw);
-  double* reds = ring + NS * stage_dbl;                       // [2][SP_WARPS][SP_RMAX]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reds + 2 * SP_WARPS * SP_RMAX);
-  __shared__ double cta_red[SP_WARPS][2];
-  __shared__ double bsm[2 * SP_RMAX];
+  double* reds = ring + NS * stage_dbl;                       // [SP_NRED][SPW][R]
+  uint64_t* fullb = reinterpret_cast<uint64_t*>(reds + SP_NRED * SPW * R);
+  uint64_t* rfull = fullb + NS;
+  __shared__ double chs[SPW * 32];
+  __shared__ double wred[SPW][2];
+  __shared__ double bc[2];
+  __shared__ uint32_t relcnt[SP_NRED];
 
   if (prm.check && *(volatile int32_t*)&prm.st->inner_conv) return;   // inner solve already stopped
   if (tid == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&fullb[s], 1);
+      relcnt[s] = 0;
+    }
+    for (int s = 0; s < SP_NRED; ++s) mbar_init(&rfull[s], SPW);
     fence_mbar_init();
   }
   __syncthreads();
 
-  // this CTA's rows
   const int64_t rows = prm.row_end - prm.row_begin;
   const int64_t per = (rows + G - 1) / G;
   const int64_t r0 = prm.row_begin + (int64_t)bid * per;
   const int64_t r1 = (r0 + per < prm.row_end) ? r0 + per : prm.row_end;
-  const int64_t myrows = (r1 > r0) ? r1 - r0 : 0;
-  const int64_t nst = (myrows + R - 1) / R;
-  int64_t gstage = 0;   // running stage counter (mbarrier parity bookkeeping)
+  const int64_t nstA = (r1 > r0) ? (r1 - r0 + R - 1) / R : 0;
+  const bool has_c = !prm.rhs_only;
+  const int64_t pper = has_c ? (prm.n + G - 1) / G : 0;
+  const int64_t q0 = (int64_t)bid * pper;
+  const int64_t q1 = (q0 + pper < prm.n) ? q0 + pper : prm.n;
+  const int64_t nstP = (has_c && q1 > q0) ? (q1 - q0 + R - 1) / R : 0;
+  const int64_t spi = nstA + nstP;
+  const int64_t iters = prm.rhs_only ? 1 : prm.max_iter;
 
+  const int64_t total = iters * spi;
+  // stage gi of this CTA's row stream -> its ring slot (one TMA bulk copy, completion on fullb)
+  auto issue = [&](int64_t gi, int slot) {   // slot = gi mod NS
+    if (gi >= total) return;
+    const int64_t s = gi % spi;
+    const double* src;
+    int64_t nr;
+    if (s < nstA) {
+      const int64_t rs = r0 + s * R;
+      nr = (rs + R <= r1) ? R : (r1 - rs);
+      src = prm.Arm + rs * npad;
+    } else {
+      const int64_t rs = q0 + (s - nstA) * R;
+      nr = (rs + R <= q1) ? R : (q1 - rs);
+      src = prm.P + rs * npad;
+    }
+    const uint32_t bytes = (uint32_t)(nr * npad * sizeof(double));
+    mbar_arrive_expect_tx(&fullb[slot], bytes);
+    bulk_g2s(ring + slot * stage_dbl, src, bytes, &fullb[slot]);
+  };
+  // every warp releases a stage after its last read of the slot; the 16th release refills the slot
+  // with stage gg + NS (no producer warp, no CTA barrier)
+  auto release = [&](int64_t gg, int slot) {
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      const uint32_t old = atomicAdd(&relcnt[slot], 1u);
+      if (old % SPW == SPW - 1) {
+        __threadfence_block();
+        fence_proxy_async();
+        issue(gg + NS, slot);
+      }
+    }
+  };
+  if (tid == 0) {
+    fence_proxy_async();
+    for (int gi = 0; gi < NS; ++gi) issue(gi, gi);
+  }
+
+  // ---------------- consumer warps (512 threads)
+  int64_t g = 0;   // next stage to consume
+  int cslot = 0;        // its ring slot (g mod NS) and phase parity (g / NS mod 2), kept incrementally
+  uint32_t cpar = 0;
+  auto advance = [&]() {
+    ++g;
+    if (++cslot == NS) {
+      cslot = 0;
+      cpar ^= 1u;
+    }
+  };
   double* xcur = prm.xa;
   double* xnext = prm.xb;
-  const int64_t iters = prm.rhs_only ? 1 : prm.max_iter;
   for (int64_t k = 0; k < iters; ++k) {
-    // ---------------- phase A: fused row stream
-    double2 xr[NPAIR], acc[NPAIR];
+    // ---------------- phase A: fused row stream over this CTA's A2 rows
+    double2 vr[NPAIR], acc[NPAIR];
 #pragma unroll
     for (int u = 0; u < NPAIR; ++u) {
-      const int64_t c = tid + (int64_t)u * SP_THREADS;
-      xr[u] = (c < np2) ? reinterpret_cast<const double2*>(xcur)[c] : make_double2(0.0, 0.0);
+      const int64_t c = tid + (int64_t)u * SP_CONS;
+      vr[u] = (c < np2) ? reinterpret_cast<const double2*>(xcur)[c] : make_double2(0.0, 0.0);
       acc[u] = make_double2(0.0, 0.0);
     }
-    auto issue = [&](int64_t s) {   // stage s of this iteration -> slot (gstage + s) % NS
-      const int64_t g = gstage + s;
-      const int slot = (int)(g % NS);
-      const int64_t rs = r0 + s * R;
-      const int64_t nr = (rs + R <= r1) ? R : (r1 - rs);
-      const uint32_t bytes = (uint32_t)(nr * npad * sizeof(double));
-      mbar_arrive_expect_tx(&bars[slot], bytes);
-      bulk_g2s(ring + slot * stage_dbl, prm.Arm + rs * npad, bytes, &bars[slot]);
-    };
-    if (tid == 0) {
-      fence_proxy_async();   // order earlier generic smem accesses (cs) before async-proxy writes
-      for (int64_t s = 0; s < nst && s < NS; ++s) issue(s);
-    }
-    int slot = (int)(gstage % NS);
-    uint32_t par = (uint32_t)((gstage / NS) & 1);
-    for (int64_t s = 0; s < nst; ++s) {
-      const int64_t g = gstage + s;
-      const int64_t rs = r0 + s * R;
-      const int nr = (int)((rs + R <= r1) ? R : (r1 - rs));
-      // b_i of this stage's rows: loaded now, consumed after the barrier (latency off the path)
-      double* bst = bsm + (g & 1) * SP_RMAX;
-      if (tid < nr) bst[tid] = prm.b ? prm.b[rs + tid] : 0.0;
-      mbar_wait(&bars[slot], par);
+    double bprev = 0.0;
+    auto dots = [&](int64_t gg, int slot, uint32_t par, int nr) {   // partial dots of stage gg -> reds, post rfull
+      mbar_wait(&fullb[slot], par);
       const double* st = ring + slot * stage_dbl;
-      double* red = reds + (g & 1) * SP_WARPS * SP_RMAX;
-      if (++slot == NS) {
-        slot = 0;
-        par ^= 1u;
-      }
-      for (int rr = 0; rr < nr; ++rr) {
-        const double2* row = reinterpret_cast<const double2*>(st + rr * npad);
-        double d = 0.0;
+      double* red = reds + (gg & (SP_NRED - 1)) * SPW * R;
+      int rr = 0;
+      for (; rr + 1 < nr; rr += 2) {
+        const double2* row0 = reinterpret_cast<const double2*>(st + rr * npad);
+        const double2* row1 = reinterpret_cast<const double2*>(st + (rr + 1) * npad);
+        double d0 = 0.0, d1 = 0.0;
 #pragma unroll
         for (int u = 0; u < NPAIR; ++u) {
-          const int64_t c = tid + (int64_t)u * SP_THREADS;
+          const int64_t c = tid + (int64_t)u * SP_CONS;
           if (c < np2) {
-            const double2 v = row[c];
-            d = fma(v.x, xr[u].x, d);
-            d = fma(v.y, xr[u].y, d);
+            const double2 v0 = row0[c], v1 = row1[c];
+            d0 = fma(v0.x, vr[u].x, d0);
+            d1 = fma(v1.x, vr[u].x, d1);
+            d0 = fma(v0.y, vr[u].y, d0);
+            d1 = fma(v1.y, vr[u].y, d1);
           }
         }
-        d = warp_sum(d);
-        if (lane == 0) red[warp * SP_RMAX + rr] = d;
-      }
-      __syncthreads();   // B1: stage s partials visible; every thread finished stage s-1
-      if (tid == 0 && s >= 1 && (s - 1) + NS < nst) issue(s - 1 + NS);
-      for (int rr = 0; rr < nr; ++rr) {
-        double d = 0.0;
 #pragma unroll
-        for (int w = 0; w < SP_WARPS; ++w) d += red[w * SP_RMAX + rr];
+        for (int o = 16; o > 0; o >>= 1) {
+          d0 += __shfl_xor_sync(0xffffffffu, d0, o);
+          d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+        }
+        if (lane == 0) {
+          red[warp * R + rr] = d0;
+          red[warp * R + rr + 1] = d1;
+        }
+      }
+      if (rr < nr) {
+        const double2* row0 = reinterpret_cast<const double2*>(st + rr * npad);
+        double d0 = 0.0;
+#pragma unroll
+        for (int u = 0; u < NPAIR; ++u) {
+          const int64_t c = tid + (int64_t)u * SP_CONS;
+          if (c < np2) {
+            const double2 v0 = row0[c];
+            d0 = fma(v0.x, vr[u].x, d0);
+            d0 = fma(v0.y, vr[u].y, d0);
+          }
+        }
+        d0 = warp_sum(d0);
+        if (lane == 0) red[warp * R + rr] = d0;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&rfull[gg & (SP_NRED - 1)]);
+    };
+    // 16-way sum of row rr of stage gg (same fixed order in every warp): lane l adds warp l & 15
+    auto rowsum = [&](const double* red, int rr) {
+      double t = red[(lane & 15) * R + rr];
+      t += __shfl_xor_sync(0xffffffffu, t, 8);
+      t += __shfl_xor_sync(0xffffffffu, t, 4);
+      t += __shfl_xor_sync(0xffffffffu, t, 2);
+      t += __shfl_xor_sync(0xffffffffu, t, 1);
+      return t;
+    };
+    auto finish = [&](int64_t gg, int slot, int64_t rs, int nr, double bv) {   // sum, axpy, release slot
+      mbar_wait(&rfull[gg & (SP_NRED - 1)], (uint32_t)((gg / SP_NRED) & 1));
+      const double* st = ring + slot * stage_dbl;
+      const double* red = reds + (gg & (SP_NRED - 1)) * SPW * R;
+      for (int rr = 0; rr < nr; ++rr) {
+        double d = rowsum(red, rr);
         const int64_t i = rs + rr;
         if (prm.az_out && tid == 0) prm.az_out[i] = d;
-        d -= bst[rr];
+        d -= __shfl_sync(0xffffffffu, bv, rr);
         if (i < prm.p) d = -d;          // sigma_i = -1 on A1 rows (correction form only)
         const double2* row = reinterpret_cast<const double2*>(st + rr * npad);
 #pragma unroll
         for (int u = 0; u < NPAIR; ++u) {
-          const int64_t c = tid + (int64_t)u * SP_THREADS;
+          const int64_t c = tid + (int64_t)u * SP_CONS;
           if (c < np2) {
             const double2 v = row[c];
             acc[u].x = fma(d, v.x, acc[u].x);
@@ -164,70 +291,90 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sp_persistent_kernel(SpParams p
           }
         }
       }
+      release(gg, slot);
+    };
+    int pslot = 0;
+    for (int64_t s = 0; s < nstA; ++s) {
+      const int64_t rs = r0 + s * R;
+      const int nr = (int)((rs + R <= r1) ? R : (r1 - rs));
+      // b_i of this stage's rows (lane rr holds row rr), consumed in finish()
+      const double bcur = (prm.b && lane < nr) ? __ldg(prm.b + rs + lane) : 0.0;
+      dots(g, cslot, cpar, nr);
+      if (s > 0) finish(g - 1, pslot, rs - R, R, bprev);
+      bprev = bcur;
+      pslot = cslot;
+      advance();
     }
-    gstage += nst;
+    if (nstA > 0) {
+      const int64_t rs = r0 + (nstA - 1) * R;
+      finish(g - 1, pslot, rs, (int)((rs + R <= r1) ? R : (r1 - rs)), bprev);
+    }
     {
       double2* pp = reinterpret_cast<double2*>(prm.part + (int64_t)bid * npad);
 #pragma unroll
       for (int u = 0; u < NPAIR; ++u) {
-        const int64_t c = tid + (int64_t)u * SP_THREADS;
+        const int64_t c = tid + (int64_t)u * SP_CONS;
         if (c < np2) pp[c] = acc[u];
       }
     }
-    grid.sync();
+    sp_grid_barrier(prm.st, tid);
     // ---------------- phase B: c = base + sum_cta part (fixed order). Every CTA owns a contiguous
-    // slice [jb0, jb1) of c; its 16 warps each sum every 16th partial row for 32 consecutive j
-    // (coalesced, ~G/16 independent loads per thread), then one warp adds the 16 chunk sums.
+    // slice [jb0, jb1) of c; warp w adds partial rows w, w+16, ... (ten loads in flight per thread)
+    // for 32 consecutive j, then warp 0 adds the 16 chunk sums.
     const int64_t jb0 = (int64_t)bid * npad / G, jb1 = (int64_t)(bid + 1) * npad / G;
-    {
-      double* chs = ring;   // [16][32] chunk sums (the ring is idle between phases)
-      for (int64_t j0 = jb0; j0 < jb1; j0 += 32) {
-        const int64_t j = j0 + lane;
-        double sacc = 0.0;
-        if (j < jb1)
-          for (int c = warp; c < G; c += SP_WARPS) sacc += prm.part[(int64_t)c * npad + j];
-        chs[warp * 32 + lane] = sacc;
-        __syncthreads();
-        if (warp == 0 && j < jb1) {
-          double t = prm.base ? prm.base[j] : 0.0;
-          for (int w = 0; w < SP_WARPS; ++w) t += chs[w * 32 + lane];
-          prm.cvec[j] = t;
+    for (int64_t j0 = jb0; j0 < jb1; j0 += 32) {
+      const int64_t j = j0 + lane;
+      double sacc = 0.0;
+      if (j < jb1) {
+        for (int c0 = warp; c0 < G; c0 += 10 * SPW) {
+          double v[10];
+#pragma unroll
+          for (int i = 0; i < 10; ++i) {
+            const int c = c0 + i * SPW;
+            v[i] = (c < G) ? prm.part[(int64_t)c * npad + j] : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < 10; ++i) sacc += v[i];
         }
-        __syncthreads();
       }
+      chs[warp * 32 + lane] = sacc;
+      named_bar_sync(1, SP_CONS);
+      if (warp == 0 && j < jb1) {
+        double t = prm.base ? prm.base[j] : 0.0;
+        for (int w = 0; w < SPW; ++w) t += chs[w * 32 + lane];
+        prm.cvec[j] = t;
+      }
+      named_bar_sync(1, SP_CONS);
     }
     if (prm.check) {
       // ||g||^2 and ||b_hat||^2 partials over this CTA's j range (fixed order everywhere)
       double g2 = 0.0, b2 = 0.0;
       const int64_t jb = (jb1 < prm.n) ? jb1 : prm.n;
-      for (int64_t j = jb0 + tid; j < jb; j += SP_THREADS) {
+      for (int64_t j = jb0 + tid; j < jb; j += SP_CONS) {
         const double s = prm.cvec[j];   // this CTA's slice, written above
-        const double g = s - prm.bhat[j];
-        g2 = fma(g, g, g2);
+        const double gg = s - prm.bhat[j];
+        g2 = fma(gg, gg, g2);
         b2 = fma(prm.bhat[j], prm.bhat[j], b2);
       }
       g2 = warp_sum(g2);
       b2 = warp_sum(b2);
       if (lane == 0) {
-        cta_red[warp][0] = g2;
-        cta_red[warp][1] = b2;
+        wred[warp][0] = g2;
+        wred[warp][1] = b2;
       }
-      __syncthreads();
+      named_bar_sync(1, SP_CONS);
       if (tid == 0) {
         double a = 0.0, b = 0.0;
-        for (int w = 0; w < SP_WARPS; ++w) {
-          a += cta_red[w][0];
-          b += cta_red[w][1];
+        for (int w = 0; w < SPW; ++w) {
+          a += wred[w][0];
+          b += wred[w][1];
         }
         prm.red[2 * bid] = a;
         prm.red[2 * bid + 1] = b;
       }
-      grid.sync();
-      double Gs = 0.0, Bs = 0.0;
-      for (int c = 0; c < G; ++c) {
-        Gs += prm.red[2 * c];
-        Bs += prm.red[2 * c + 1];
-      }
+      sp_grid_barrier(prm.st, tid);
+      double Gs, Bs;
+      sp_sum2_over_ctas(prm.red, G, tid, bc, Gs, Bs);
       const bool conv = sqrt(Gs) <= prm.inner_tol * sqrt(Bs);
       if (conv) {
         if (bid == 0 && tid == 0) {
@@ -235,78 +382,65 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sp_persistent_kernel(SpParams p
           prm.st->inner_conv = 1;
         }
       } else {
-        for (int64_t i = (int64_t)bid * SP_THREADS + tid; i < prm.rows_r; i += (int64_t)G * SP_THREADS)
+        for (int64_t i = (int64_t)bid * SP_CONS + tid; i < prm.rows_r; i += (int64_t)G * SP_CONS)
           prm.rst[i] = prm.wst[i] - (i < prm.row_end ? prm.az_out[i] : 0.0);
       }
       break;
     }
     if (prm.rhs_only) break;
-    grid.sync();
-    // ---------------- phase C: x_{k+1} = P c (+ x_k), stop partials
-    double* cs = ring;   // ring is idle here
-    for (int64_t j = tid; j < npad; j += SP_THREADS) cs[j] = prm.cvec[j];
-    __syncthreads();
+    sp_grid_barrier(prm.st, tid);
+    // ---------------- phase C: x_{k+1} = P c (+ x_k) over this CTA's rows [q0, q1) of P, streamed
+    // through the same ring (already in flight); c in registers in the x layout of phase A. The
+    // stage's x entries are finished by warp (stage mod 16) once all 16 warps posted their dots.
+#pragma unroll
+    for (int u = 0; u < NPAIR; ++u) {
+      const int64_t c = tid + (int64_t)u * SP_CONS;
+      vr[u] = (c < np2) ? reinterpret_cast<const double2*>(prm.cvec)[c] : make_double2(0.0, 0.0);
+    }
     double e2 = 0.0, r2 = 0.0;
-    for (int64_t i = (int64_t)bid * SP_WARPS + warp; i < npad; i += (int64_t)G * SP_WARPS) {
-      const double2* pr = reinterpret_cast<const double2*>(prm.P + i * npad);
-      const double2* cs2 = reinterpret_cast<const double2*>(cs);
-      // 8 independent 16-byte loads in flight per lane (a P row is streamed from HBM once)
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int64_t c = lane;
-      for (; c + 7 * 32 < np2; c += 8 * 32) {
-        double2 v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldcs(pr + c + 32 * u);
-#pragma unroll
-        for (int u = 0; u < 8; u += 2) {
-          const double2 x0 = cs2[c + 32 * u], x1 = cs2[c + 32 * (u + 1)];
-          s0 = fma(v[u].x, x0.x, s0);
-          s1 = fma(v[u].y, x0.y, s1);
-          s2 = fma(v[u + 1].x, x1.x, s2);
-          s3 = fma(v[u + 1].y, x1.y, s3);
-        }
-      }
-      for (; c < np2; c += 32) {
-        const double2 v = __ldcs(pr + c), x0 = cs2[c];
-        s0 = fma(v.x, x0.x, s0);
-        s1 = fma(v.y, x0.y, s1);
-      }
-      double s = warp_sum((s0 + s1) + (s2 + s3));
-      if (i >= prm.n) s = 0.0;
-      const double xn = prm.sp_form ? xcur[i] + s : s;
-      if (lane == 0) {
-        xnext[i] = xn;
-        if (i < prm.n) {
-          if (prm.x_hist) prm.x_hist[k * prm.n + i] = xn;
-          if (prm.xref) {
-            const double e = xn - prm.xref[i];
-            e2 = fma(e, e, e2);
-            r2 = fma(prm.xref[i], prm.xref[i], r2);
+    for (int64_t s = 0; s < nstP; ++s) {
+      const int64_t rs = q0 + s * R;
+      const int nr = (int)((rs + R <= q1) ? R : (q1 - rs));
+      dots(g, cslot, cpar, nr);
+      if (warp == (int)(g & (SPW - 1))) {
+        mbar_wait(&rfull[g & (SP_NRED - 1)], (uint32_t)((g / SP_NRED) & 1));
+        const double* red = reds + (g & (SP_NRED - 1)) * SPW * R;
+        for (int rr = 0; rr < nr; ++rr) {
+          const double sum = rowsum(red, rr);
+          if (lane == 0) {
+            const int64_t i = rs + rr;
+            const double xn = prm.sp_form ? xcur[i] + sum : sum;
+            xnext[i] = xn;
+            if (prm.x_hist) prm.x_hist[k * prm.n + i] = xn;
+            if (prm.xref) {
+              const double e = xn - prm.xref[i];
+              e2 = fma(e, e, e2);
+              r2 = fma(prm.xref[i], prm.xref[i], r2);
+            }
           }
         }
       }
+      release(g, cslot);
+      advance();
     }
     if (lane == 0) {
-      cta_red[warp][0] = e2;
-      cta_red[warp][1] = r2;
+      wred[warp][0] = e2;
+      wred[warp][1] = r2;
     }
-    __syncthreads();
+    named_bar_sync(1, SP_CONS);
     if (tid == 0) {
       double a = 0.0, b = 0.0;
-      for (int w = 0; w < SP_WARPS; ++w) {
-        a += cta_red[w][0];
-        b += cta_red[w][1];
+      for (int w = 0; w < SPW; ++w) {
+        a += wred[w][0];
+        b += wred[w][1];
       }
       prm.red[2 * bid] = a;
       prm.red[2 * bid + 1] = b;
     }
-    grid.sync();
+    sp_grid_barrier(prm.st, tid);
     // ---------------- phase D: stop decision (identical in every CTA)
-    double E = 0.0, Rr = 0.0;
-    for (int c = 0; c < G; ++c) {
-      E += prm.red[2 * c];
-      Rr += prm.red[2 * c + 1];
-    }
+    double E, Rr;
+    sp_sum2_over_ctas(prm.red, G, tid, bc, E, Rr);
     const double metric = (prm.xref && Rr > 0.0) ? sqrt(E) / sqrt(Rr) : __longlong_as_double(0x7ff8000000000000LL);
     const bool done = (prm.stop == ILS_STOP_XREF) && prm.xref && (metric <= prm.tol);
     if (bid == 0 && tid == 0) {
@@ -318,8 +452,16 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sp_persistent_kernel(SpParams p
     xcur = xnext;
     xnext = t;
     if (done) break;
-    __syncthreads();   // cs (ring) reads done before the next phase-A TMA overwrites it
   }
+  // drain: copies already issued into this CTA's ring (stages g .. g+NS-1) land before it exits
+  if (tid == 0)
+    for (int64_t d = g; d < g + NS && d < total; ++d) {
+      mbar_wait(&fullb[cslot], cpar);
+      if (++cslot == NS) {
+        cslot = 0;
+        cpar ^= 1u;
+      }
+    }
 }
 
 // ||x - xref|| / ||xref|| (single block, fixed order) -> st->metric
@@ -355,10 +497,42 @@ int stop_metric(Handle& h, const double* x, const double* xref, double* out_dev)
   return ILS_OK;
 }
 
+// TMA ring geometry of the row stream: R whole rows per stage (~SP_STAGE_TARGET bytes), NS stages in
+// ~200 KB of shared memory. ILS_SP_STAGE / ILS_SP_NS: experiment overrides (stage bytes, stage cap).
+static void sp_ring_geometry(int64_t npad, int& R, int& NS) {
+  const int64_t rowbytes = npad * (int64_t)sizeof(double);
+  int64_t target = SP_STAGE_TARGET;
+  int nscap = 6;
+  if (const char* e = getenv("ILS_SP_STAGE")) target = atoll(e) > 0 ? atoll(e) : target;
+  if (const char* e = getenv("ILS_SP_NS")) nscap = atoi(e) >= 2 ? atoi(e) : nscap;
+  R = (int)(target / rowbytes);
+  if (R < 1) R = 1;
+  if (R > SP_RMAX) R = SP_RMAX;
+  const int64_t stage_bytes = R * rowbytes;
+  NS = (int)((200 * 1024) / stage_bytes);
+  if (NS > nscap) NS = nscap;
+  if (NS > SP_NRED) NS = SP_NRED;
+  if (NS < 2) NS = 2;
+}
+
+// dynamic shared memory of the row-stream kernel: ring + partial-dot buffers + mbarriers
+static size_t sp_smem_bytes(int64_t stage_bytes, int R, int NS) {
+  return (size_t)NS * stage_bytes + (size_t)SP_NRED * SPW * R * sizeof(double) +
+         (size_t)(NS + SP_NRED) * sizeof(uint64_t);
+}
+
 template <int NPAIR>
 static int launch_sp(Handle& h, SpParams& prm, size_t smem) {
   ILS_CU(cudaFuncSetAttribute(sp_persistent_kernel<NPAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)smem));
+  if (getenv("ILS_DEBUG_OCC")) {
+    int nb = -1;
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, sp_persistent_kernel<NPAIR>);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sp_persistent_kernel<NPAIR>, SP_THREADS, smem);
+    fprintf(stderr, "ILS_DEBUG_OCC NPAIR=%d smem=%zu occ=%d (%s) regs=%d maxthr=%d static=%zu maxdyn=%d\n", NPAIR, smem, nb,
+            cudaGetErrorString(e), fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes);
+  }
   void* args[] = {&prm};
   ILS_CU(cudaLaunchCooperativeKernel((void*)sp_persistent_kernel<NPAIR>, dim3(h.num_sms),
                                      dim3(SP_THREADS), args, smem, h.stream));
@@ -411,26 +585,21 @@ int sp_run(Handle& h, const double* x0_dev, double* x_dev, double tol, int64_t m
   prm.stop = stop;
   prm.sp_form = sp_form;
   prm.rhs_only = rhs_only ? 1 : 0;
-  const int64_t rowbytes = npad * (int64_t)sizeof(double);
-  int R = (int)(SP_STAGE_TARGET / rowbytes);
-  if (R < 1) R = 1;
-  if (R > SP_RMAX) R = SP_RMAX;
-  const int64_t stage_bytes = R * rowbytes;
-  int NS = (int)((200 * 1024) / stage_bytes);
-  if (NS > 4) NS = 4;
-  if (NS < 2) NS = 2;
+  int R, NS;
+  sp_ring_geometry(npad, R, NS);
+  const int64_t stage_bytes = R * npad * (int64_t)sizeof(double);
   prm.rows_per_stage = R;
   prm.nstages = NS;
   prm.st = h.dstat;
-  size_t smem = (size_t)NS * stage_bytes + 2 * SP_WARPS * SP_RMAX * sizeof(double) + NS * sizeof(uint64_t);
+  size_t smem = sp_smem_bytes(stage_bytes, R, NS);
   if ((size_t)npad * sizeof(double) > (size_t)NS * stage_bytes) return ILS_ERR_UNSUPPORTED;
   ILS_CU(cudaMemsetAsync(h.dstat, 0, sizeof(DevStatus), h.stream));
   const int64_t np2 = npad / 2;
   int r;
   ILS_CU(cudaEventRecord(h.evk0, h.stream));
-  if (np2 <= SP_THREADS) r = launch_sp<1>(h, prm, smem);
-  else if (np2 <= 2 * SP_THREADS) r = launch_sp<2>(h, prm, smem);
-  else if (np2 <= 4 * SP_THREADS) r = launch_sp<4>(h, prm, smem);
+  if (np2 <= SP_CONS) r = launch_sp<1>(h, prm, smem);
+  else if (np2 <= 2 * SP_CONS) r = launch_sp<2>(h, prm, smem);
+  else if (np2 <= 4 * SP_CONS) r = launch_sp<4>(h, prm, smem);
   else r = launch_sp<8>(h, prm, smem);
   if (r) return r;
   ILS_CU(cudaEventRecord(h.evk1, h.stream));
@@ -546,21 +715,16 @@ int rk_check(Handle& h, const double* z, const double* bhat, const double* w, do
   prm.rows_r = h.ppad;
   prm.inner_tol = inner_tol;
   prm.t_now = t_now;
-  const int64_t rowbytes = h.npad * (int64_t)sizeof(double);
-  int R = (int)(SP_STAGE_TARGET / rowbytes);
-  if (R < 1) R = 1;
-  if (R > SP_RMAX) R = SP_RMAX;
-  const int64_t stage_bytes = R * rowbytes;
-  int NS = (int)((200 * 1024) / stage_bytes);
-  if (NS > 4) NS = 4;
-  if (NS < 2) NS = 2;
+  int R, NS;
+  sp_ring_geometry(h.npad, R, NS);
+  const int64_t stage_bytes = R * h.npad * (int64_t)sizeof(double);
   prm.rows_per_stage = R;
   prm.nstages = NS;
-  const size_t smem = (size_t)NS * stage_bytes + 2 * SP_WARPS * SP_RMAX * sizeof(double) + NS * sizeof(uint64_t);
+  const size_t smem = sp_smem_bytes(stage_bytes, R, NS);
   const int64_t np2 = h.npad / 2;
-  if (np2 <= SP_THREADS) return launch_sp<1>(h, prm, smem);
-  if (np2 <= 2 * SP_THREADS) return launch_sp<2>(h, prm, smem);
-  if (np2 <= 4 * SP_THREADS) return launch_sp<4>(h, prm, smem);
+  if (np2 <= SP_CONS) return launch_sp<1>(h, prm, smem);
+  if (np2 <= 2 * SP_CONS) return launch_sp<2>(h, prm, smem);
+  if (np2 <= 4 * SP_CONS) return launch_sp<4>(h, prm, smem);
   return launch_sp<8>(h, prm, smem);
 }
 
