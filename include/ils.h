@@ -53,10 +53,12 @@
  *
  * Inner stopping rule (the paper says "until convergence"; R2):
  *   the inner solve of outer iteration k starts from zero. If ||b_hat|| = 0
- *   it returns 0 after 0 steps. After every check_every steps: SP-RK-RGS recomputes
- *   az = A1 z, g = A1^T az - b_hat, stops if ||g||_2 <= inner_tol ||b_hat||_2 and otherwise
- *   continues with the residual reset r = w - az; SP-SCD recomputes r = b_hat - A1bar beta and
- *   stops if ||r||_2 <= inner_tol ||b_hat||_2. The solve also stops after max_inner steps.
+ *   it returns 0 after 0 steps. After every check_every steps: SP-RK-RGS evaluates
+ *   g = A1^T A1 z - b_hat (as A1bar z - b_hat where A1bar = A1^T A1 is resident, else as
+ *   A1^T (A1 z) - b_hat: the same vector up to rounding) and stops if ||g||_2 <= inner_tol
+ *   ||b_hat||_2; the check reads z only -- the residual r = w - A1 z is maintained by the steps
+ *   and never recomputed. SP-SCD recomputes r = b_hat - A1bar beta and stops if
+ *   ||r||_2 <= inner_tol ||b_hat||_2. The solve also stops after max_inner steps.
  * Outer stopping rule: after forming x_{k+1}: STOP_XREF ||x_{k+1} - x_ref||_2 <= tol ||x_ref||_2
  *   (BASELINE.json), STOP_RR RR(x_{k+1}) < tol with RR = ||A^T J (A x - b)||^2 / ||A^T J b||^2
  *   (PAPER.md:651-653), STOP_NONE never (fixed horizon). outer_iters counts completed updates.

@@ -215,8 +215,9 @@ def rk_rgs_inner(A1T, N, S, bhat, seed, k, max_inner, check_every, inner_tol,
     z_0 = w_0 = 0 (step 6). For t = 0,1,...: (j1, j2) from the index stream
     (steps 8, 10); RK step on A1^T w = bhat (step 9); RGS step on A1 z = w (step 11).
     "until convergence" (step 7, silent -- reading R2): after every check_every steps
-    recompute az = A1 z, g = A1^T az - bhat, stop if ||g|| <= inner_tol ||bhat||, and
-    continue from az (drift reset). Stops at max_inner steps. Returns (z, steps)."""
+    g = A1^T (A1 z) - bhat, stop if ||g|| <= inner_tol ||bhat||. The check reads z only: the
+    incrementally maintained A1 z (reading R21) is never recomputed, as in Alg. 2 itself.
+    Stops at max_inner steps. Returns (z, steps)."""
     p, n = A1T.shape[1], A1T.shape[0]
     w = np.zeros(p)
     z = np.zeros(n)
@@ -237,8 +238,7 @@ def rk_rgs_inner(A1T, N, S, bhat, seed, k, max_inner, check_every, inner_tol,
             if step_hook is not None:
                 step_hook(t, j1, j2, w, z, az)
             if t % check_every == 0:
-                az = A1T.T @ z
-                g = A1T @ az - bhat
+                g = A1T @ (A1T.T @ z) - bhat
                 if float(np.linalg.norm(g)) <= inner_tol * nb:
                     return z, t
     return z, t
@@ -284,9 +284,8 @@ def rk_rgs_inner_sparse(A1c, N, S, bhat, seed, k, max_inner, check_every, inner_
             z[j2] += s2
             az[r2] += s2 * v2
             t += 1
-            if t % check_every == 0:                      # reading R2
-                az = A1c @ z
-                g = A1c.T @ az - bhat
+            if t % check_every == 0:                      # reading R2 (no recomputation of A1 z)
+                g = A1c.T @ (A1c @ z) - bhat
                 if float(np.linalg.norm(g)) <= inner_tol * nb:
                     return z, t
     return z, t

@@ -226,10 +226,7 @@ __global__ void __launch_bounds__(32) batched_kernel(BatchParams P) {
                 const double zj = shfl(z, j);
                 if (i < p) a = fma(A1T[j * p + i], zj, a);
               }
-              if (i < p) {
-                az[i] = a;
-                r[u] = w[u] - a;
-              }
+              if (i < p) az[i] = a;
             }
             __syncwarp();
             double g = 0.0;
@@ -497,7 +494,6 @@ __global__ void __launch_bounds__(32) batched_rk_kernel(BatchParams P) {
 #pragma unroll
           for (int u = 0; u < RPL; ++u) {
             azs[lane + 32 * u] = az[u];
-            r[u] = w[u] - az[u];
           }
           __syncwarp();
           double g = 0.0;

@@ -154,12 +154,10 @@ __global__ void __launch_bounds__(1024) check_finish_kernel(const double* __rest
       st->inner_steps = t_now;
       st->inner_conv = 1;
     }
-  } else {
-    for (int64_t i = tid; i < ppad; i += 1024) r[i] = w[i] - (i < p ? az[i] : 0.0);
   }
 }
 
-// the SP-RK-RGS inner check (include/ils.h) for large n: az = A1 z, g = A1^T az, decide, r = w - az
+// the SP-RK-RGS inner check (include/ils.h) for large n: az = A1 z, g = A1^T az, decide (reads z only)
 int rk_check_twopass(Handle& h, const double* z, const double* bhat, const double* w, double* r, double* az,
                      double inner_tol, int64_t t_now) {
   int rc = ensure_y(h);

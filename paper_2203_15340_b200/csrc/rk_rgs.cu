@@ -50,6 +50,11 @@ struct RkParams {
   long long* prof;     // optional per-phase cycle counters (rank 0, thread 0), see ILS_RK_PROF
   int gmode;           // 1: z and the sampling table stay in global memory (large n, single-step kernel)
   const double* G;     // look-ahead kernel: A1bar (npad x npad) for the column inner products
+  // look-ahead kernel, whole inner solve in one launch: the inner check every ce steps runs in the
+  // kernel (g = A1bar z - b_hat on a snapshot of z, Zsnap = [C][npad] global scratch)
+  int64_t ce;
+  double inner_tol;
+  double* Zsnap;
 };
 
 // Ring entries for steps t0 .. t0+31 (one per lane): Philox draw, two weighted inverse-CDF
@@ -868,7 +873,7 @@ __global__ void __launch_bounds__(256, 1) rk_rgs_small_kernel(RkParams p, double
     }
     t = cend;
     if (t % ce != 0) break;   // max_inner reached off the check grid: no check (chunked path rule)
-    // ---- inner stop check at t: az = A1 z (own rows), g = A1^T az - b_hat, r := w - az
+    // ---- inner stop check at t: az = A1 z (own rows), g = A1^T az - b_hat (reads z only)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int e = tid + u * NT;
@@ -905,12 +910,6 @@ __global__ void __launch_bounds__(256, 1) rk_rgs_small_kernel(RkParams p, double
       if (tid == 0) {
         p.st->inner_steps = t;
         p.st->inner_conv = 1;
-      }
-    } else {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = tid + u * NT;
-        if (e < PP) r[u] = w[u] - azs[e];
       }
     }
     __syncthreads();
@@ -993,6 +992,12 @@ __device__ __forceinline__ void la_fill_gram(const RkParams& p, const RkIdx* rin
   }
 }
 
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double a, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr), "d"(a),
+               "r"(rbar)
+               : "memory");
+}
+
 __device__ __forceinline__ int64_t ld_acquire_cta_s64(const int64_t* a) {
   int64_t v;
   asm volatile("ld.acquire.cta.shared::cta.s64 %0, [%1];" : "=l"(v) : "r"(smem_u32(a)) : "memory");
@@ -1003,10 +1008,18 @@ __device__ __forceinline__ void st_release_cta_s64(int64_t* a, int64_t v) {
 }
 
 // Warp roles: NWc compute warps (rows), a communication warp (sends the block partials), a reduce
-// warp (cluster sum + corrections -> finished products), a fill warp (index + Gram rings ahead)
-// and a TMA warp (column refills). Compute, communication and reduce warps meet at a named barrier
-// per block; the fill and TMA warps run ahead, throttled by progress counters in shared memory
-// (release / acquire), so their long operations never stall the step.
+// warp (cluster sum + corrections -> finished products), a fill warp (index + Gram rings ahead),
+// a TMA warp (column refills) and a check warp. Compute, communication and reduce warps meet at a
+// named barrier per block; the fill and TMA warps run ahead, throttled by progress counters in
+// shared memory (release / acquire), so their long operations never stall the step.
+// One launch runs the whole inner solve [t0, t1). The inner check (include/ils.h) reads z only, so
+// it runs beside the steps: at every check step t_c the communication warp copies z (after exactly
+// t_c steps) to a snapshot, the check warp forms its rows of g = A1bar z - b_hat, the 16 partial
+// ||g||^2 are exchanged (st.async) and summed in one fixed order in every CTA. On a stop, every
+// CTA's communication warp flags its next block message; the first block f whose messages carry a
+// flag is the same in every CTA (same messages), and every CTA ends after block f + 2 -- the last
+// block any CTA can have sent -- so no message is left in flight. The output is the snapshot z and
+// the step count t_c, exactly as if the steps had stopped at t_c.
 template <int CC, int U>
 __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
   constexpr int B = 4, NRV = 8;
@@ -1014,8 +1027,9 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
   using K = RkBlk<B>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int NT = blockDim.x, NW = NT >> 5, NWc = NW - 4, NTc = NWc * 32;
+  const int NT = blockDim.x, NW = NT >> 5, NWc = NW - 5, NTc = NWc * 32;
   const bool comm = (warp == NWc), reducer = (warp == NWc + 1), filler = (warp == NWc + 2), tmaw = (warp == NWc + 3);
+  const bool checker = (warp == NWc + 4);
   const bool compute = warp < NWc;
   const int rank = (int)cluster_ctarank();
   const int64_t i0 = (int64_t)rank * p.slice;
@@ -1032,7 +1046,16 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
   double* rn_tab = bh_tab + ((p.n + 1) & ~1);                          // [n]
   double (*gring)[LA_NG] = reinterpret_cast<double (*)[LA_NG]>(rn_tab + ((p.n + 1) & ~1));   // [LA_GR][LA_NG]
   __shared__ __align__(16) double wred[2][8][32];   // per warp: value lane & 7 over lane group lane >> 3
-  __shared__ __align__(16) double recv[8][RK_MAXC][NRV];   // block b in buffer b & 7 (sent two blocks ahead)
+  constexpr int NMSG = NRV + 2;                          // 8 products + stop flag + pad
+  __shared__ __align__(16) double recv[8][RK_MAXC][NMSG];  // block b in buffer b & 7 (sent two blocks ahead)
+  __shared__ __align__(8) double crecv[2][RK_MAXC];       // check m partials in buffer m & 1
+  __shared__ __align__(8) uint64_t cbar[2];
+  __shared__ __align__(8) int64_t lim_s;      // blocks to run (lowered once on a stop)
+  __shared__ __align__(8) int64_t snap_s;     // z snapshots taken (comm warp)
+  __shared__ __align__(8) int64_t chkd_s;     // checks decided (check warp)
+  __shared__ __align__(8) int64_t stop_t_s;   // step of the check that stopped the solve, -1: none
+  __shared__ int stop_req_s;                  // flag the next block messages
+  __shared__ int zdone_s;                     // the communication warp's last z update is done
   __shared__ __align__(8) uint64_t rbar[8];
   __shared__ double chkw[12];
   __shared__ double bnorm_s;
@@ -1058,8 +1081,16 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
     for (int s = 0; s < 2; ++s) mbar_init(&tbar[s], 1);
     for (int s = 0; s < 2; ++s) mbar_init(&sbar[s], 1);
     fence_mbar_init();
-    for (int s = 0; s < 8; ++s) mbar_arrive_expect_tx(&rbar[s], CC * NRV * 8);
+    for (int s = 0; s < 2; ++s) mbar_init(&cbar[s], 1);
+    fence_mbar_init();
+    for (int s = 0; s < 8; ++s) mbar_arrive_expect_tx(&rbar[s], CC * NMSG * 8);
+    for (int s = 0; s < 2; ++s) mbar_arrive_expect_tx(&cbar[s], CC * 8);
     done_s = 0;
+    snap_s = 0;
+    chkd_s = 0;
+    stop_t_s = -1;
+    stop_req_s = 0;
+    zdone_s = 0;
   }
   double bnorm = 1.0;
   if (p.t0 == 0) {
@@ -1086,6 +1117,7 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
     return;
   }
   const int64_t nblk = (p.t1 - p.t0 + B - 1) / B;
+  if (tid == 0) lim_s = nblk;
   const uint32_t slice_bytes = (uint32_t)own * sizeof(double);
   // 16 blocks ahead before the step loop starts, split over the fill and TMA warps (indices of both
   // halves first: the Gram values of a block read the indices of the two blocks before it)
@@ -1111,9 +1143,15 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
 
   if (filler) {   // ---- fill warp: index + Gram rings, at most 24 blocks ahead of the consumers
     int64_t f = 16;
-    while (f < nblk) {
+    bool quit = false;
+    while (f < nblk && !quit) {
       while (f + 8 > ld_acquire_cta_s64(&done_s) + LA_GR) {   // slot of block done must stay
+        if (f >= ld_acquire_cta_s64(&lim_s) + 8) {            // stopped: nothing further is needed
+          quit = true;
+          break;
+        }
       }
+      if (quit) break;
       rk_fill_indices(p, Ss, ring, p.t0 + 4 * f, lane, bh_tab, rn_tab);
       la_fill_gram(p, ring, gring, lam, f, lane);
       f += 8;
@@ -1123,18 +1161,77 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
   } else if (tmaw) {   // ---- TMA warp: refill slot (b % NS) once block b - NS is done
     if (lane == 0 && own > 0) {
       int slot = 0;
-      for (int64_t b = NS; b < nblk; ++b) {
+      int64_t b = NS;
+      for (; b < nblk; ++b) {
+        bool quit = false;
         while (ld_acquire_cta_s64(&done_s) < b - NS + 1 || ld_acquire_cta_s64(&filled_s) <= b) {
+          if (b >= ld_acquire_cta_s64(&lim_s)) {
+            quit = true;
+            break;
+          }
         }
+        if (quit) break;
         fence_proxy_async();
         issue(b, slot);
         if (++slot == NS) slot = 0;
       }
+      // drain: blocks issued at or past the final limit were never consumed -- their copies must
+      // land before the CTA exits (every block below it was waited for by the compute warps)
+      const int64_t issued = (b < nblk) ? b : nblk;
+      const int64_t lim_end = ld_acquire_cta_s64(&done_s);
+      for (int64_t d = lim_end; d < issued; ++d) mbar_wait(&bars[d % NS], (uint32_t)((d / NS) & 1));
+    }
+  } else if (checker) {   // ---- check warp: g = A1bar z - b_hat on each snapshot, cluster sum, decide
+    const int64_t per = (p.n + CC - 1) / CC;
+    const int64_t j0 = (int64_t)rank * per, j1 = (j0 + per < p.n) ? j0 + per : p.n;
+    const double* zsn = p.Zsnap + (int64_t)rank * p.npad;
+    int64_t m = 0;
+    for (int64_t tc = (p.t0 / p.ce + 1) * p.ce; tc < p.t1; tc += p.ce, ++m) {
+      bool gone = false;   // the solve ended before this snapshot was taken
+      while (ld_acquire_cta_s64(&snap_s) <= m) {
+        if (*(volatile int*)&zdone_s) {
+          __threadfence_block();
+          gone = ld_acquire_cta_s64(&snap_s) <= m;
+          break;
+        }
+      }
+      if (gone) break;
+      double part = 0.0;
+      for (int64_t j = j0; j < j1; ++j) {   // rows in order, each a warp dot product
+        const double* gr = p.G + j * p.npad;
+        double a0 = 0.0, a1 = 0.0;
+        int64_t c = lane;
+        for (; c + 32 < p.npad; c += 64) {
+          a0 = fma(gr[c], zsn[c], a0);
+          a1 = fma(gr[c + 32], zsn[c + 32], a1);
+        }
+        if (c < p.npad) a0 = fma(gr[c], zsn[c], a0);
+        const double gj = warp_sum(a0 + a1) - bh_tab[j];
+        part = fma(gj, gj, part);
+      }
+      const int bsel = (int)(m & 1);
+      if (lane < CC)
+        st_async_f64(map_shared_rank(smem_u32(&crecv[bsel][rank]), (uint32_t)lane), part,
+                     map_shared_rank(smem_u32(&cbar[bsel]), (uint32_t)lane));
+      mbar_wait_cluster(&cbar[bsel], (uint32_t)((m >> 1) & 1));
+      double g2 = 0.0;
+      for (int c = 0; c < CC; ++c) g2 += crecv[bsel][c];
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(&cbar[bsel], CC * 8);   // for check m + 2
+      const bool stop = sqrt(g2) <= p.inner_tol * bnorm;
+      if (lane == 0) {
+        if (stop) {
+          stop_t_s = tc;
+          stop_req_s = 1;
+        }
+        st_release_cta_s64(&chkd_s, m + 1);
+      }
+      if (stop) break;
     }
   } else if (reducer) {   // ---- reduce warp: finished products of block i once s(i-1) is posted
     const bool rprof = p.prof && lane == 0;
     long long hr[2] = {0, 0};
-    for (int64_t i = 0; i < nblk; ++i) {
+    for (int64_t i = 0; i < *(volatile int64_t*)&lim_s; ++i) {
       if (i >= 1) mbar_wait(&sbar[(i - 1) & 1], (uint32_t)(((i - 1) >> 1) & 1));
       long long rc0 = rprof ? clock64() : 0;
       const int b4 = (int)(i & 7);
@@ -1165,10 +1262,13 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
       tot += __shfl_xor_sync(0xffffffffu, tot, 8);
       tot += __shfl_xor_sync(0xffffffffu, tot, 16);
       if (lane < NRV) tsm[i & 1][lane] = tot;
+      // stop flags of block i (identical messages in every CTA): end after block i + 2
+      const bool flag = __any_sync(0xffffffffu, lane < CC && recv[b4][lane][NRV] != 0.0);
+      if (flag && lane == 0 && lim_s > i + 3) lim_s = i + 3;
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&tbar[i & 1]);
-        mbar_arrive_expect_tx(&rbar[b4], CC * NRV * 8);   // for block i + 8
+        mbar_arrive_expect_tx(&rbar[b4], CC * NMSG * 8);   // for block i + 8
       }
       if (rprof) hr[1] += clock64() - rc0;
     }
@@ -1198,15 +1298,46 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
     pc[k] += c_ - tc;                \
     tc = c_;                         \
   }
-    for (int64_t i = -2; i < nblk; ++i) {
+    int64_t next_tc = (p.t0 / p.ce + 1) * p.ce;   // next check step (communication warp)
+    int64_t msnap = 0;                            // snapshots taken
+    // z updates of block blk in step order (communication warp), with the z snapshot of every check
+    // step inside the block taken after exactly that many steps
+    auto zupd = [&](int64_t blk) {
+      const int64_t tp = p.t0 + blk * B;
+      const double* sm = smail[blk & 3];
+      int kdone = 0;
+      while (next_tc > tp && next_tc <= tp + B && next_tc < p.t1) {
+        const int kk = (int)(next_tc - tp);
+        if (lane == 0)
+          for (int k = kdone; k < kk; ++k) zs[ring[(tp + k) & (RK_RING - 1)].j2] += sm[B + k];
+        kdone = kk;
+        while (ld_acquire_cta_s64(&chkd_s) < msnap) {   // the previous snapshot is still being read
+        }
+        if (*(volatile int64_t*)&stop_t_s < 0) {
+          __syncwarp();
+          double* dst = p.Zsnap + (int64_t)rank * p.npad;
+          for (int64_t j = lane; j < p.npad; j += 32) dst[j] = zs[j];
+          __threadfence_block();
+          __syncwarp();
+          if (lane == 0) st_release_cta_s64(&snap_s, msnap + 1);
+          ++msnap;
+        }
+        next_tc += p.ce;
+      }
+      if (lane == 0)
+        for (int k = kdone; k < B; ++k) zs[ring[(tp + k) & (RK_RING - 1)].j2] += sm[B + k];
+      __syncwarp();
+    };
+    for (int64_t i = -2; i < *(volatile int64_t*)&lim_s; ++i) {
       const int64_t nb = i + 2;
+      const int64_t lim = *(volatile int64_t*)&lim_s;
       if (++sl_nb == NS) {
         sl_nb = 0;
         ph_nb ^= 1u;
       }
       sl_i = sl_nb - 2 < 0 ? sl_nb - 2 + NS : sl_nb - 2;   // slot of block i (NS >= 3)
       // ---- phase 1 (compute warps): state products of block nb = i + 2 on S_i (blocks i, i+1 not applied)
-      if (compute && nb < nblk) {
+      if (compute && nb < lim) {
         if (known_filled <= nb + 1 && known_filled < nblk) {   // ring + Gram entries of blocks nb, nb+1
           do {
             known_filled = ld_acquire_cta_s64(&filled_s);
@@ -1236,7 +1367,7 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
       if (comm) {
         const bool cprof = p.prof && lane == 0;
         long long cc0 = cprof ? clock64() : 0;
-        if (nb < nblk) {
+        if (nb < *(volatile int64_t*)&lim_s) {
           double v = 0.0;
           for (int w8 = 0; w8 < NWc; ++w8) v += wred[nb & 1][w8][lane];
           v += __shfl_xor_sync(0xffffffffu, v, 8);
@@ -1246,8 +1377,12 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
           const int b4 = (int)(nb & 7);
           const uint32_t la = smem_u32(&recv[b4][rank][2 * (lane & 3)]);
           const uint32_t lb = smem_u32(&rbar[b4]);
-          if (lane < NRV / 2)
-            for (int c = 0; c < CC; ++c) st_async_v2f64(map_shared_rank(la, (uint32_t)c), v0, v1, map_shared_rank(lb, (uint32_t)c));
+          const double fl = *(volatile int*)&stop_req_s ? 1.0 : 0.0;   // stop flag (lane NRV / 2)
+          const uint32_t la2 = smem_u32(&recv[b4][rank][(lane < NRV / 2) ? 2 * (lane & 3) : NRV]);
+          if (lane <= NRV / 2)
+            for (int c = 0; c < CC; ++c)
+              st_async_v2f64(map_shared_rank(la2, (uint32_t)c), lane < NRV / 2 ? v0 : fl, lane < NRV / 2 ? v1 : 0.0,
+                             map_shared_rank(lb, (uint32_t)c));
           __syncwarp();
           if (cprof) {
             const long long c_ = clock64();
@@ -1255,11 +1390,7 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
             cc0 = c_;
           }
         }
-        if (i >= 1 && lane == 0) {   // z updates of block i - 1, sequential order
-          const int64_t tp = p.t0 + (i - 1) * B;
-#pragma unroll
-          for (int k = 0; k < B; ++k) zs[ring[(tp + k) & (RK_RING - 1)].j2] += smail[(i - 1) & 3][B + k];
-        }
+        if (i >= 1) zupd(i - 1);   // z updates of block i - 1, sequential order
         continue;
       }
       if (i < 0) continue;
@@ -1335,16 +1466,25 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
         }
       }
     }
+    if (comm) {   // the last block's z updates (and snapshots), once its scalars are posted
+      const int64_t lim = *(volatile int64_t*)&lim_s;
+      while (ld_acquire_cta_s64(&done_s) < lim) {
+      }
+      if (lim >= 1) zupd(lim - 1);
+      __threadfence_block();
+      if (lane == 0) *(volatile int*)&zdone_s = 1;
+    }
   }
   __syncthreads();
-  if (comm && lane == 0 && nblk >= 1) {   // the last block's z updates
-    const int64_t tp = p.t0 + (nblk - 1) * B;
-#pragma unroll
-    for (int k = 0; k < B; ++k) zs[ring[(tp + k) & (RK_RING - 1)].j2] += smail[(nblk - 1) & 3][B + k];
+  const int64_t tstop = stop_t_s;
+  if (rank == 0) {
+    const double* zo = (tstop >= 0) ? p.Zsnap : zs;   // a stop returns z after exactly t_c steps
+    for (int64_t j = tid; j < p.npad; j += NT) p.Z[j] = zo[j];
+    if (tid == 0 && tstop >= 0) {
+      p.st->inner_steps = tstop;
+      p.st->inner_conv = 1;
+    }
   }
-  __syncthreads();
-  if (rank == 0)
-    for (int64_t j = tid; j < p.npad; j += NT) p.Z[j] = zs[j];
   cluster_sync_all();
 }
 
@@ -1435,8 +1575,13 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
                  int64_t check_every, double inner_tol, int64_t* steps_out) {
   const int64_t ce = check_every > 0 ? check_every : h.n;
   const cudaStream_t st = h.stream;
-  if (!h.rk_state) {
-    ILS_CU(cudaMallocAsync(&h.rk_state, (size_t)(3 * h.ppad + h.npad) * sizeof(double), st));
+  {   // w, r, az [ppad], z [npad], z snapshots of the look-ahead kernel [RK_MAXC][npad]
+    const size_t words = (size_t)3 * h.ppad + (size_t)(1 + RK_MAXC) * h.npad;
+    if (!h.rk_state || h.rk_state_words < words) {
+      if (h.rk_state) cudaFreeAsync(h.rk_state, st);
+      ILS_CU(cudaMallocAsync(&h.rk_state, words * sizeof(double), st));
+      h.rk_state_words = words;
+    }
   }
   double* W = h.rk_state;
   double* Rv = W + h.ppad;
@@ -1548,12 +1693,12 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
   size_t smem_la = 0;
   {
     const char* e = getenv("ILS_RK_LA");
-    if (!(e && e[0] == '0') && blocked && C == 16 && Bk == 4 && (U == 2 || U == 4 || U == 8) && nt + 128 <= 384 && !h.large &&
+    if (!(e && e[0] == '0') && blocked && C == 16 && Bk == 4 && (U == 2 || U == 4 || U == 8) && nt + 160 <= 384 && !h.large &&
         !h.sparse) {
       // the Gram ring replaces one column slot when both do not fit (>= 3 slots: blocks i .. i+2 live)
       const size_t ring_bytes = (size_t)LA_GR * LA_NG * sizeof(double), slot_la = (size_t)2 * Bk * p.slicepad * 8;
       smem_la = smem + ring_bytes;
-      const size_t cap = 227 * 1024 - 14 * 1024;   // the kernel's static shared memory (~12.7 KB) counts too
+      const size_t cap = 227 * 1024 - 16 * 1024;   // the kernel's static shared memory (~15.4 KB) counts too
       while (smem_la > cap && p.nslots > 4) {
         p.nslots -= 1;
         smem_la -= slot_la;
@@ -1610,7 +1755,7 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
       const int64_t steps = h.hstat->inner_conv ? h.hstat->inner_steps : max_inner;
       if (steps_out) *steps_out = steps;
       const double pd = (double)h.p, nd = (double)h.n;
-      hot_account(h, 1, (double)steps * 16.0 * pd + (double)(steps / ce) * 8.0 * pd * nd, 1);
+      hot_account(h, 1, (double)steps * 16.0 * pd + (double)(steps / ce) * 16.0 * pd * nd, 1);
       return ILS_OK;
     }
   }
@@ -1618,14 +1763,24 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
   int64_t t = 0, nchecks = 0;
   int pending = 0;
   bool conv = false;
+  if (la) {   // the whole inner solve in one launch, the inner checks inside the kernel
+    p.t0 = 0;
+    p.t1 = max_inner;
+    p.ce = ce;
+    p.inner_tol = inner_tol;
+    p.Zsnap = Z + h.npad;
+    const int r = (U == 2)   ? launch_rkla<16, 2>(h, p, nt + 160, smem_la)
+                  : (U == 4) ? launch_rkla<16, 4>(h, p, nt + 160, smem_la)
+                             : launch_rkla<16, 8>(h, p, nt + 160, smem_la);
+    if (r) return r;
+    nchecks = max_inner / ce;
+    t = max_inner;
+  }
   while (t < max_inner) {
     const int64_t t1 = (t + ce < max_inner) ? t + ce : max_inner;
     p.t0 = t;
     p.t1 = t1;
-    const int r = la ? ((U == 2)   ? launch_rkla<16, 2>(h, p, nt + 128, smem_la)
-                        : (U == 4) ? launch_rkla<16, 4>(h, p, nt + 128, smem_la)
-                                   : launch_rkla<16, 8>(h, p, nt + 128, smem_la))
-                  : blocked ? dispatch_rkb(h, p, U, Bk, nt, smem)
+    const int r = blocked ? dispatch_rkb(h, p, U, Bk, nt, smem)
                             : ((U == 8) ? dispatch_rk_c<8>(h, p, nt, smem) : dispatch_rk_c<4>(h, p, nt, smem));
     if (r) return r;
     t = t1;
@@ -1672,7 +1827,11 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
   }
   if (steps_out) *steps_out = steps;
   const double pd = (double)h.p, nd = (double)h.n;
-  hot_account(h, 1, (double)steps * 16.0 * pd + (double)(steps / ce) * 8.0 * pd * nd, (steps + ce - 1) / ce);
+  // algorithmic bytes: 16p per inner step (two columns of A1); per inner check
+  // 8n^2 (A1bar z, look-ahead kernel) or 16pn (A1^T (A1 z), chunked kernels). Launches: one per
+  // inner solve (look-ahead kernel) or one chunk kernel per check interval.
+  hot_account(h, 1, (double)steps * 16.0 * pd + (double)(steps / ce) * (la ? 8.0 * nd * nd : 16.0 * pd * nd),
+              la ? 1 : (steps + ce - 1) / ce);
   return ILS_OK;
 }
 

@@ -49,7 +49,7 @@ struct SpParams {
   DevStatus* st;
   // SP-RK-RGS inner check mode (rhs_only = 1, b = nullptr, base = nullptr, x = z): rows [0, p) of
   // A1 give az_i = <A1[i,:], z> (stored to az_out) and c = A1^T az; then g = c - b_hat,
-  // stop if ||g|| <= inner_tol ||b_hat|| (inner_steps = t_now), else reset r = w - az.
+  // stop if ||g|| <= inner_tol ||b_hat|| (inner_steps = t_now); z is only read.
   int check;
   double* az_out;
   const double* bhat;
@@ -376,14 +376,9 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sp_persistent_kernel(SpParams p
       double Gs, Bs;
       sp_sum2_over_ctas(prm.red, G, tid, bc, Gs, Bs);
       const bool conv = sqrt(Gs) <= prm.inner_tol * sqrt(Bs);
-      if (conv) {
-        if (bid == 0 && tid == 0) {
-          prm.st->inner_steps = prm.t_now;
-          prm.st->inner_conv = 1;
-        }
-      } else {
-        for (int64_t i = (int64_t)bid * SP_CONS + tid; i < prm.rows_r; i += (int64_t)G * SP_CONS)
-          prm.rst[i] = prm.wst[i] - (i < prm.row_end ? prm.az_out[i] : 0.0);
+      if (conv && bid == 0 && tid == 0) {
+        prm.st->inner_steps = prm.t_now;
+        prm.st->inner_conv = 1;
       }
       break;
     }

@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(SRK_T) sparse_rk_kernel(SpRkParams p) {
   cp_async_wait<0>();
 }
 
-// inner check: az = A1 z (rows, CSR), g = A1^T az - b_hat (CSC), stop / r = w - az (cooperative)
+// inner check: az = A1 z (rows, CSR), g = A1^T az - b_hat (CSC), stop (cooperative; reads z only)
 __global__ void __launch_bounds__(256) sparse_rk_check_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                                               const double* __restrict__ va, int64_t p_rows,
                                                               const int64_t* __restrict__ cp,
@@ -670,8 +670,6 @@ __global__ void __launch_bounds__(256) sparse_rk_check_kernel(const int64_t* __r
       st->inner_steps = t_now;
       st->inner_conv = 1;
     }
-  } else {
-    for (int64_t i = gtid; i < p_rows; i += gsz) Rv[i] = W[i] - az[i];
   }
 }
 
