@@ -39,10 +39,10 @@
  *   j = min{ j : S_j > v }. This realises Pr(j) = ||A1_(j)||^2 / ||A1||_F^2 (PAPER.md:199-202,
  *   :227-230) to within 2^-32 relative.
  *   SP-RK-RGS step t (tag 1): j1 from U = x1:x0 (x1 high), j2 from U = x3:x2.
- *   SP-SCD step t: tag 2 draw A, tag 3 draw B, tag 4 draw C, tag 5 draw D.
+ *   SP-SCD step t: tag 2 draw A, tag 3 draw B, tag 4 draw C.
  *     alpha_t = 1 + floor(A.x0 * n / 2^32) (uniform on {1..n}) or min(alpha_k, n).
- *     Round keys K0..K11 = A.x1, A.x2, A.x3, B.x0..B.x3, C.x0..C.x3, D.x0.
- *     pi = 12-round balanced Feistel permutation of [0, 2^(2h)), h = ceil(ceil(log2 n) / 2),
+ *     Round keys K0..K7 = A.x1, A.x2, A.x3, B.x0, B.x1, B.x2, B.x3, C.x0.
+ *     pi = 8-round balanced Feistel permutation of [0, 2^(2h)), h = ceil(ceil(log2 n) / 2),
  *     round (L, R) -> (R, L xor F(R, K_r)), F(R, K) = mix32(R xor K) & (2^h - 1),
  *     mix32(x): x *= 0x85EBCA6B; x ^= x >> 13; x *= 0xC2B2AE35; x ^= x >> 16 (mod 2^32),
  *     value = (L << h) | R, cycle-walked (re-encrypted) until < n; pi = identity for n = 1.

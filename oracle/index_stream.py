@@ -15,7 +15,7 @@ exact index sequence both sides implement the same counter-based generator
   N_j summed sequentially (DESIGN.md reading R7);
 * alpha_t uniform on [n] (PAPER.md:694, reading R8);
 * the "uniformly random" size-alpha subset -> prefix of a keyed
-  12-round Feistel permutation of [n] with cycle walking (reading R9).
+  8-round Feistel permutation of [n] with cycle walking (reading R9).
 """
 from __future__ import annotations
 
@@ -31,9 +31,8 @@ TAG_RKRGS = 1
 TAG_SCD_A = 2
 TAG_SCD_B = 3
 TAG_SCD_C = 4
-TAG_SCD_D = 5
 TAG_RCD = 6
-FEISTEL_ROUNDS = 12
+FEISTEL_ROUNDS = 8
 
 
 def philox4x32_10(ctr, key):
@@ -156,7 +155,7 @@ def feistel_params(n: int):
 
 
 def feistel_forward(i, keys, n: int):
-    """pi(i) for an int or integer array i: 12-round balanced Feistel on 2h bits
+    """pi(i) for an int or integer array i: 8-round balanced Feistel on 2h bits
     (h = ceil(ceil(log2 n)/2)), round (L, R) -> (R, L ^ F(R, K_r)),
     F(R, K) = mix32(R ^ K) & (2^h - 1), cycle-walked until the value lies in [0, n)."""
     x = np.array(i, dtype=np.uint64)
@@ -182,20 +181,17 @@ def feistel_forward(i, keys, n: int):
 
 
 def scd_alpha_keys(seed: int, k: int, t: int, n: int, alpha_mode: int = 0, alpha_fixed: int = 1):
-    """alpha_t and the twelve Feistel round keys for SCD step t of outer iteration k
+    """alpha_t and the eight Feistel round keys for SCD step t of outer iteration k
     (Alg. 5 steps 7-8). alpha_mode 0: uniform on {1..n} (alpha = 1 + hi32(x0 * n) of the
-    tag-A draw); 1: fixed min(alpha_fixed, n). Round keys K0..K11 = A.x1..x3, B.x0..x3,
-    C.x0..x3, D.x0."""
+    tag-A draw); 1: fixed min(alpha_fixed, n). Round keys K0..K7 = A.x1..x3, B.x0..x3, C.x0."""
     xa = draw(seed, k, t, TAG_SCD_A)
     xb = draw(seed, k, t, TAG_SCD_B)
     xc = draw(seed, k, t, TAG_SCD_C)
-    xd = draw(seed, k, t, TAG_SCD_D)
     if alpha_mode == 0:
         alpha = 1 + ((int(xa[0]) * n) >> 32)
     else:
         alpha = min(int(alpha_fixed), n)
-    keys = [int(v) for v in (xa[1], xa[2], xa[3], xb[0], xb[1], xb[2], xb[3],
-                             xc[0], xc[1], xc[2], xc[3], xd[0])]
+    keys = [int(v) for v in (xa[1], xa[2], xa[3], xb[0], xb[1], xb[2], xb[3], xc[0])]
     return alpha, keys
 
 

@@ -40,6 +40,14 @@ struct BKey {
   uint32_t key[kFeistelRounds];
 };
 
+// batched SP-SCD window entry: alpha_t and the Feistel round tables T_r[v] = F(v, K_r) of step t,
+// packed 4 bits per entry (n <= 32: h <= 3, 8 entries per round)
+struct BKeyT {
+  uint32_t alpha;
+  int32_t j;
+  uint32_t word[kFeistelRounds];
+};
+
 __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
 template <int UP>
@@ -181,8 +189,8 @@ __global__ void __launch_bounds__(32) batched_kernel(BatchParams P) {
         for (int64_t t = 0; t < P.max_inner; ++t) {
           if ((t & 31) == 0) {
             const U4 xw = draw(seed, (uint32_t)it, (uint64_t)(t + lane), kTagRkRgs);
-            my1 = sample_weighted(((uint64_t)xw.y << 32) | xw.x, S, n);
-            my2 = sample_weighted(((uint64_t)xw.w << 32) | xw.z, S, n);
+            my1 = sample_weighted_small(((uint64_t)xw.y << 32) | xw.x, S, n);
+            my2 = sample_weighted_small(((uint64_t)xw.w << 32) | xw.z, S, n);
           }
           const int j1 = __shfl_sync(0xffffffffu, my1, (int)(t & 31));
           const int j2 = __shfl_sync(0xffffffffu, my2, (int)(t & 31));
@@ -250,20 +258,18 @@ __global__ void __launch_bounds__(32) batched_kernel(BatchParams P) {
             const uint64_t tt = (uint64_t)(t + lane);
             if (P.weighted) {
               const U4 xw = draw(seed, (uint32_t)it, tt, kTagRcd);
-              e.j = sample_weighted(((uint64_t)xw.y << 32) | xw.x, S, n);
+              e.j = sample_weighted_small(((uint64_t)xw.y << 32) | xw.x, S, n);
               e.alpha = 1;
             } else {
               const U4 a = draw(seed, (uint32_t)it, tt, kTagScdA);
               const U4 bb = draw(seed, (uint32_t)it, tt, kTagScdB);
-              const U4 cc = draw(seed, (uint32_t)it, tt, kTagScdC);
-              const U4 dd = draw(seed, (uint32_t)it, tt, kTagScdD);
+            const U4 cc = draw(seed, (uint32_t)it, tt, kTagScdC);
               e.alpha = P.alpha_mode == ILS_ALPHA_UNIFORM ? 1u + mulhi32(a.x, (uint32_t)n)
                                                           : (uint32_t)(P.alpha_k < n ? P.alpha_k : n);
               e.j = -1;
               e.key[0] = a.y; e.key[1] = a.z; e.key[2] = a.w;
               e.key[3] = bb.x; e.key[4] = bb.y; e.key[5] = bb.z; e.key[6] = bb.w;
-              e.key[7] = cc.x; e.key[8] = cc.y; e.key[9] = cc.z; e.key[10] = cc.w;
-              e.key[11] = dd.x;
+            e.key[7] = cc.x;
             }
             __syncwarp();
             keys[lane] = e;
@@ -428,8 +434,8 @@ __global__ void __launch_bounds__(32) batched_rk_kernel(BatchParams P) {
         const int kk = (int)(t & 31);
         if (kk == 0) {   // indices and scalars of steps t..t+31, one per lane
           const U4 xw = draw(seed, (uint32_t)it, (uint64_t)(t + lane), kTagRkRgs);
-          my1 = sample_weighted(((uint64_t)xw.y << 32) | xw.x, S, n);
-          my2 = sample_weighted(((uint64_t)xw.w << 32) | xw.z, S, n);
+          my1 = sample_weighted_small(((uint64_t)xw.y << 32) | xw.x, S, n);
+          my2 = sample_weighted_small(((uint64_t)xw.w << 32) | xw.z, S, n);
           mybh = cs[my1];
           myr1 = rns[my1];
           myr2 = rns[my2];
@@ -547,7 +553,7 @@ __global__ void __launch_bounds__(32) batched_scd_kernel(BatchParams P) {
   const uint64_t seed = P.seed + (uint64_t)inst;
   double* G = sm;                                       // [32][32] A1bar (row j at G + 32 j)
   uint64_t* S = reinterpret_cast<uint64_t*>(G + 32 * 32);   // [32]
-  BKey* keys = reinterpret_cast<BKey*>(S + 32);             // [32]
+  BKeyT* keys = reinterpret_cast<BKeyT*>(S + 32);             // [32]
   const bool act = lane < n;
   // column j of A1 in registers one row at a time: Gram by rank-1 updates over the p rows
   double g[32];
@@ -585,24 +591,28 @@ __global__ void __launch_bounds__(32) batched_scd_kernel(BatchParams P) {
       for (int64_t t = 0; t < P.max_inner; ++t) {
         const int kk = (int)(t & 31);
         if (kk == 0) {
-          BKey e;
+          BKeyT e;
           const uint64_t tt = (uint64_t)(t + lane);
           if (P.weighted) {
             const U4 xw = draw(seed, (uint32_t)it, tt, kTagRcd);
-            e.j = sample_weighted(((uint64_t)xw.y << 32) | xw.x, S, n);
+            e.j = sample_weighted_small(((uint64_t)xw.y << 32) | xw.x, S, n);
             e.alpha = 1;
           } else {
             const U4 a = draw(seed, (uint32_t)it, tt, kTagScdA);
             const U4 bb = draw(seed, (uint32_t)it, tt, kTagScdB);
             const U4 cc = draw(seed, (uint32_t)it, tt, kTagScdC);
-            const U4 dd = draw(seed, (uint32_t)it, tt, kTagScdD);
             e.alpha = P.alpha_mode == ILS_ALPHA_UNIFORM ? 1u + mulhi32(a.x, (uint32_t)n)
                                                         : (uint32_t)(P.alpha_k < n ? P.alpha_k : n);
             e.j = -1;
-            e.key[0] = a.y; e.key[1] = a.z; e.key[2] = a.w;
-            e.key[3] = bb.x; e.key[4] = bb.y; e.key[5] = bb.z; e.key[6] = bb.w;
-            e.key[7] = cc.x; e.key[8] = cc.y; e.key[9] = cc.z; e.key[10] = cc.w;
-            e.key[11] = dd.x;
+            const uint32_t key[kFeistelRounds] = {a.y, a.z, a.w, bb.x, bb.y, bb.z, bb.w, cc.x};
+            // round tables of this lane's step: T_r[v] = mix32(v ^ K_r) & (2^hb - 1) for v < 2^hb,
+            // packed 4 bits per entry (hb <= 3 for n <= 32)
+#pragma unroll
+            for (int r = 0; r < kFeistelRounds; ++r) {
+              uint32_t wd = 0;
+              for (uint32_t v = 0; v <= msk; ++v) wd |= (mix32(v ^ key[r]) & msk) << (4 * v);
+              e.word[r] = wd;
+            }
           }
           __syncwarp();
           keys[lane] = e;
@@ -612,17 +622,28 @@ __global__ void __launch_bounds__(32) batched_scd_kernel(BatchParams P) {
         if (P.weighted) {
           j = keys[kk].j;
         } else {
-          uint32_t key[kFeistelRounds];
+          uint32_t wd[kFeistelRounds];
 #pragma unroll
-          for (int qq = 0; qq < kFeistelRounds; ++qq) key[qq] = keys[kk].key[qq];
+          for (int qq = 0; qq < kFeistelRounds; ++qq) wd[qq] = keys[kk].word[qq];
           const uint32_t alpha = keys[kk].alpha;
+          // one round-trip decryption of y (feistel_decrypt_once) from the packed round tables
+          auto dec = [&](uint32_t y) {
+            uint32_t L = y >> hb, R = y & msk;
+#pragma unroll
+            for (int r = kFeistelRounds - 1; r >= 0; --r) {
+              const uint32_t Lp = R ^ ((wd[r] >> (4 * L)) & msk);
+              R = L;
+              L = Lp;
+            }
+            return (L << hb) | R;
+          };
           // pi^{-1}(lane) by cycle walking through a table of one-round-trip decryptions of the
           // whole domain [0, 4^hb) (<= 64 values: lane v holds D(v) and D(v + 32)); a walk step is
-          // then two shuffles instead of a 12-round decryption (the walk diverges across lanes)
+          // then two shuffles instead of a decryption (the walk diverges across lanes)
           const uint32_t dom = 1u << (2 * hb);
           const bool allm = alpha >= (uint32_t)n;   // tau_t = [n] (Motzkin case): no permutation needed
-          const uint32_t d0 = (n == 1 || allm) ? 0u : feistel_decrypt_once((uint32_t)lane & (dom - 1), key, hb, msk);
-          const uint32_t d1 = (n == 1 || allm || dom <= 32) ? 0u : feistel_decrypt_once((uint32_t)lane + 32u, key, hb, msk);
+          const uint32_t d0 = (n == 1 || allm) ? 0u : dec((uint32_t)lane & (dom - 1));
+          const uint32_t d1 = (n == 1 || allm || dom <= 32) ? 0u : dec((uint32_t)lane + 32u);
           uint32_t y = d0;
           if (n > 1 && !allm) {
             while (__any_sync(0xffffffffu, act && y >= (uint32_t)n)) {
@@ -640,7 +661,7 @@ __global__ void __launch_bounds__(32) batched_scd_kernel(BatchParams P) {
         }
         const double sc = __shfl_sync(0xffffffffu, rr, j) * __shfl_sync(0xffffffffu, rn, j);
         if (act) rr = fma(-sc, G[j * 32 + lane], rr);
-        if (lane == j) beta += sc;
+        beta += (lane == j) ? sc : 0.0;
         steps = t + 1;
         if (steps == next_check) {   // inner stop rule: r = b_hat - A1bar beta
           next_check += ce;
@@ -708,8 +729,7 @@ __global__ void __launch_bounds__(32) batched_rkb_kernel(BatchParams P) {
   const uint64_t seed = P.seed + (uint64_t)inst;
   double* A1T = sm;                                     // [n][PP]
   double* G = A1T + n * PP;                             // [32][33] A1bar
-  double* azs = G + 32 * 33;                            // [PP]
-  double* cs = azs + PP;                                // [32]
+  double* cs = G + 32 * 33;                             // [32]
   double* rns = cs + 32;                                // [32]
   uint64_t* S = reinterpret_cast<uint64_t*>(rns + 32);  // [32]
 
@@ -727,7 +747,9 @@ __global__ void __launch_bounds__(32) batched_rkb_kernel(BatchParams P) {
       a1tb1 = fma(v, b[i], a1tb1);
     }
   }
-  // A1bar[i][lane] (rows rotated by lane: conflict-free shared-memory reads)
+  // A1bar[i][lane] (rows rotated by lane: conflict-free shared-memory reads); rows and columns
+  // >= n are zero (the inner check sums over 32 columns)
+  for (int i = n; i < 32; ++i) G[i * 33 + lane] = 0.0;
   for (int i = 0; i < n; ++i) {
     double s = 0.0;
     if (act)
@@ -764,11 +786,12 @@ __global__ void __launch_bounds__(32) batched_rkb_kernel(BatchParams P) {
         const int kk = (int)(t & 31);
         if (kk == 0) {   // indices and scalars of steps t..t+31, one per lane
           const U4 xw = draw(seed, (uint32_t)it, (uint64_t)(t + lane), kTagRkRgs);
-          my1 = sample_weighted(((uint64_t)xw.y << 32) | xw.x, S, n);
-          my2 = sample_weighted(((uint64_t)xw.w << 32) | xw.z, S, n);
+          my1 = sample_weighted_small(((uint64_t)xw.y << 32) | xw.x, S, n);
+          my2 = sample_weighted_small(((uint64_t)xw.w << 32) | xw.z, S, n);
+          const bool live = t + lane < P.max_inner;   // steps past max_inner are masked: s1 = s2 = 0
           mybh = cs[my1];
-          myr1 = rns[my1];
-          myr2 = rns[my2];
+          myr1 = live ? rns[my1] : 0.0;
+          myr2 = live ? rns[my2] : 0.0;
         }
         int j1[B], j2[B];
         double bh[B], rn1[B], rn2[B];
@@ -777,9 +800,8 @@ __global__ void __launch_bounds__(32) batched_rkb_kernel(BatchParams P) {
           j1[i] = __shfl_sync(FULL, my1, kk + i);
           j2[i] = __shfl_sync(FULL, my2, kk + i);
           bh[i] = __shfl_sync(FULL, mybh, kk + i);
-          const bool live = t + i < P.max_inner;   // steps past max_inner are masked: s1 = s2 = 0
-          rn1[i] = live ? __shfl_sync(FULL, myr1, kk + i) : 0.0;
-          rn2[i] = live ? __shfl_sync(FULL, myr2, kk + i) : 0.0;
+          rn1[i] = __shfl_sync(FULL, myr1, kk + i);
+          rn2[i] = __shfl_sync(FULL, myr2, kk + i);
         }
         double x1[B][RPL], x2[B][RPL];
         double acc[8];
@@ -836,51 +858,17 @@ __global__ void __launch_bounds__(32) batched_rkb_kernel(BatchParams P) {
             r[u] = fma(-s2[i], x2[i][u], r[u]);
           }
 #pragma unroll
-        for (int i = 0; i < B; ++i)
-          if (lane == j2[i]) z += s2[i];
+        for (int i = 0; i < B; ++i) z += (lane == j2[i]) ? s2[i] : 0.0;   // z_j2 += s2 (program order)
         steps = (t + B < P.max_inner) ? t + B : P.max_inner;
-        if (t + B == next_check) {   // inner stop rule (include/ils.h): g = A1^T A1 z - b_hat
+        if (t + B == next_check) {   // inner stop rule (include/ils.h): g = A1bar z - b_hat, reads z only
           next_check += ce;
-          double az[RPL], az2[RPL];
-#pragma unroll
-          for (int u = 0; u < RPL; ++u) az[u] = az2[u] = 0.0;
-          int j = 0;
-          for (; j + 1 < n; j += 2) {
-            const double zj = __shfl_sync(FULL, z, j), zk = __shfl_sync(FULL, z, j + 1);
-#pragma unroll
-            for (int u = 0; u < RPL; ++u) {
-              az[u] = fma(A1T[j * PP + lane + 32 * u], zj, az[u]);
-              az2[u] = fma(A1T[(j + 1) * PP + lane + 32 * u], zk, az2[u]);
-            }
+          double g0 = 0.0, g1 = 0.0;   // row lane of A1bar (G[lane][k], stride 33: conflict-free)
+#pragma unroll 8
+          for (int k = 0; k < 32; k += 2) {
+            g0 = fma(G[lane * 33 + k], __shfl_sync(FULL, z, k), g0);
+            g1 = fma(G[lane * 33 + k + 1], __shfl_sync(FULL, z, k + 1), g1);
           }
-          if (j < n) {
-            const double zj = __shfl_sync(FULL, z, j);
-#pragma unroll
-            for (int u = 0; u < RPL; ++u) az[u] = fma(A1T[j * PP + lane + 32 * u], zj, az[u]);
-          }
-#pragma unroll
-          for (int u = 0; u < RPL; ++u) {
-            az[u] += az2[u];
-            azs[lane + 32 * u] = az[u];
-            r[u] = w[u] - az[u];
-          }
-          __syncwarp();
-          double g = 0.0;
-          if (act) {   // rows rotated by lane: conflict-free; two accumulators
-            double g0 = 0.0, g1 = 0.0;
-            const double* col = A1T + lane * PP;
-            int i0 = lane % p;   // rotated start, wrapped incrementally (no modulo in the loop)
-            int ii = 0;
-            for (; ii + 1 < p; ii += 2) {
-              const int i1 = (i0 + 1 == p) ? 0 : i0 + 1;
-              g0 = fma(col[i0], azs[i0], g0);
-              g1 = fma(col[i1], azs[i1], g1);
-              i0 = (i1 + 1 == p) ? 0 : i1 + 1;
-            }
-            if (ii < p) g0 = fma(col[i0], azs[i0], g0);
-            g = (g0 + g1) - c;
-          }
-          __syncwarp();
+          const double g = act ? (g0 + g1) - c : 0.0;
           const double gg = warp_sum(g * g);
           if (sqrt(gg) <= P.inner_tol * cnorm) break;
         }
@@ -937,7 +925,7 @@ int batched_solve(Handle& h, int method, const double* x0, double* x, double tol
   if (method == 1 && P.check_every % 4 == 0 && !getenv("ILS_BATCHED_RK_SINGLE")) {   // blocked, 4 steps/reduction
     const int rpl = (int)((h.p + 31) / 32);
     const int RPL = rpl <= 1 ? 1 : rpl <= 2 ? 2 : rpl <= 3 ? 3 : rpl <= 4 ? 4 : 8;
-    const size_t smem = ((size_t)h.n * 32 * RPL + 32 * 33 + 32 * RPL + 64) * 8 + 32 * 8;
+    const size_t smem = ((size_t)h.n * 32 * RPL + 32 * 33 + 64) * 8 + 32 * 8;
 #define RKBLAUNCH(RR)                                                                                \
   do {                                                                                               \
     ILS_CU(cudaFuncSetAttribute(batched_rkb_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
@@ -975,7 +963,7 @@ int batched_solve(Handle& h, int method, const double* x0, double* x, double tol
     return ILS_OK;
   }
   if (method == 2) {   // SP-SCD / SP-RCD: A1bar resident
-    const size_t smem = (size_t)32 * 32 * 8 + 32 * 8 + 32 * sizeof(BKey);
+    const size_t smem = (size_t)32 * 32 * 8 + 32 * 8 + 32 * sizeof(BKeyT);
     ILS_CU(cudaFuncSetAttribute(batched_scd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     batched_scd_kernel<<<(unsigned)h.batch, 32, smem, h.stream>>>(P);
     ILS_LAUNCHED("batched_scd_kernel");

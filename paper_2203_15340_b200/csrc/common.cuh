@@ -16,9 +16,8 @@ constexpr int kTagRkRgs = 1;
 constexpr int kTagScdA = 2;
 constexpr int kTagScdB = 3;
 constexpr int kTagScdC = 4;
-constexpr int kTagScdD = 5;
 constexpr int kTagRcd = 6;
-constexpr int kFeistelRounds = 12;
+constexpr int kFeistelRounds = 8;
 
 // ---------------------------------------------------------------- Philox4x32-10
 struct U4 { uint32_t x, y, z, w; };
@@ -68,6 +67,20 @@ __device__ __forceinline__ int sample_weighted(uint64_t U, const uint64_t* S, in
   return lo;
 }
 
+// The same index for n <= 32 without a data-dependent loop: j = #{k < n-1 : S_k <= v} (S is
+// strictly increasing and S_{n-1} > v), by five fixed halving steps with selects.
+__device__ __forceinline__ int sample_weighted_small(uint64_t U, const uint64_t* S, int n) {
+  const uint64_t v = mulhi64(U, S[n - 1]);
+  int j = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    const int k = j + step - 1;
+    const uint64_t sk = S[k < n - 1 ? k : 0];
+    j = (k < n - 1 && sk <= v) ? j + step : j;
+  }
+  return j;
+}
+
 // ---------------------------------------------------------------- Feistel permutation of [n]
 __host__ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
   x *= 0x85EBCA6Bu;
@@ -88,7 +101,7 @@ __host__ __device__ __forceinline__ uint32_t feistel_half_bits(uint32_t n) {
   return (b + 1) >> 1;
 }
 
-// inverse of one 12-round encryption: undo rounds 11..0; round r was (L,R)->(R, L^F(R,K_r))
+// inverse of one 8-round encryption: undo rounds 7..0; round r was (L,R)->(R, L^F(R,K_r))
 __device__ __forceinline__ uint32_t feistel_decrypt_once(uint32_t y, const uint32_t* key, uint32_t h,
                                                          uint32_t mask) {
   uint32_t L = y >> h, R = y & mask;

@@ -6,7 +6,7 @@
 //          sc = r_j / A1bar_jj ; beta_j += sc ; r -= sc A1bar_(j)       (steps 10-11, :697-698)
 // SP-RCD (weighted): j_t drawn from the column-norm weights (Remark 4.1).
 //
-// The subsets do not depend on the data, so the integer-heavy membership test (a 12-round
+// The subsets do not depend on the data, so the integer-heavy membership test (an 8-round
 // Feistel inverse per coordinate and step) is taken off the sequential path: before each chunk
 // of check_every steps, scd_masks_kernel evaluates it for the whole chunk on the full GPU and
 // stores, per (step, thread), the bit mask of that thread's coordinates. scd_chunk_kernel (one
@@ -70,14 +70,12 @@ __device__ __forceinline__ void scd_make_key(uint64_t seed, uint32_t k, uint64_t
   const U4 a = draw(seed, k, t, kTagScdA);
   const U4 b = draw(seed, k, t, kTagScdB);
   const U4 c = draw(seed, k, t, kTagScdC);
-  const U4 d = draw(seed, k, t, kTagScdD);
   e.alpha = alpha_mode == ILS_ALPHA_UNIFORM ? 1u + mulhi32(a.x, (uint32_t)n)
                                             : (uint32_t)((alpha_k < n) ? alpha_k : n);
   e.j = -1;
   e.key[0] = a.y; e.key[1] = a.z; e.key[2] = a.w;
   e.key[3] = b.x; e.key[4] = b.y; e.key[5] = b.z; e.key[6] = b.w;
-  e.key[7] = c.x; e.key[8] = c.y; e.key[9] = c.z; e.key[10] = c.w;
-  e.key[11] = d.x;
+  e.key[7] = c.x;
 }
 
 // masks[(u - t0) * NT + tid] bit v  <=>  coordinate tid + v*NT is in tau_u. One CTA per step.
