@@ -132,10 +132,23 @@ typedef struct {
   int32_t sp_form;           /* [0] 0: x = P (A1^T b1 + A2^T (A2 x - b2)) (Sec23); 1: x += P A^T J (b - A x);
                                 2: the paper's literal layout: SP x = B x + c with B = P A2^T A2, c = P A^T J b
                                 formed once (Alg. 1 steps 2-6); RK/RGS b_hat = A2bar x + A^T J b
-                                with A2bar = A2^T A2 formed once (Alg. 2 steps 2-5, Alg. 5 steps 2-4). Dense only. */
+                                with A2bar = A2^T A2 formed once (Alg. 2 steps 2-5, Alg. 5 steps 2-4). Dense only.
+                                3 (ILS_SP_FORM_AUTO): 2 if its precompute pays off over expected_outer outer
+                                steps, else 0 (include/ils.h "Automatic form"). */
   double* x_hist;            /* [NULL] optional [max_iter][n] record of every outer iterate (batch 1) */
   int64_t* inner_hist;       /* [NULL] optional [max_iter] inner step count per outer iteration */
+  int64_t expected_outer;    /* [0] outer steps the caller expects, for ILS_SP_FORM_AUTO (0: min(max_iter, 32)) */
 } ils_opts;
+
+/* Automatic form (sp_form = ILS_SP_FORM_AUTO, PAPER.md:134-139 vs :291, :689): the literal layout
+ * (2) replaces the per-outer-step stream of A2 (8 q (n + 1) bytes) by an n x n GEMV (8 n^2 bytes;
+ * SP already applies P, so its per-step saving is the full A2 stream) at the price of a one-time
+ * DMMA precompute: A2bar = A2^T A2 (q n (n + 1) flops) and, for SP, B = P A2bar (2 n^3 flops).
+ * It is chosen iff K * saved_bytes / 6.0e12 B/s > precompute_flops / 3.0e13 flop/s with
+ * K = expected_outer (the measured HBM copy rate and DMMA DGEMM rate of this B200 pool, rounded
+ * down). CSR input, n > 8192 and row-sharded handles always take form 0. The report's
+ * sp_form_used records the choice. */
+#define ILS_SP_FORM_AUTO 3
 
 typedef struct {
   int64_t outer_iters;       /* completed outer updates (max over instances when batched) */
@@ -156,6 +169,7 @@ typedef struct {
   int64_t hot_launches[4];
   int64_t* inst_iters;       /* [NULL] optional host [batch] outer iterations per instance */
   int32_t* inst_status;      /* [NULL] optional host [batch] 1 = converged */
+  int32_t sp_form_used;      /* the right-hand-side form this call ran (0, 1 or 2; resolves ILS_SP_FORM_AUTO) */
 } ils_report;
 
 ILS_API void ils_default_opts(ils_opts* opts);

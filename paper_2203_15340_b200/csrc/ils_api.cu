@@ -454,6 +454,18 @@ int ils_create(ils_handle* out, const double* A, const double* b, int64_t p, int
 void ils_destroy(ils_handle h) { free_handle(h); }
 
 // method: 0 SP, 1 SP-RK-RGS, 2 SP-SCD/RCD
+// include/ils.h "Automatic form": the literal layout (sp_form 2) iff its one-time DMMA precompute
+// costs less than the A2 stream it saves over the expected outer steps.
+static int auto_sp_form(const Handle& H, int method, int64_t max_iter, int64_t expected_outer) {
+  if (H.sparse || H.large || H.n > 8192 || H.comm != nullptr) return 0;
+  const double K = (double)(expected_outer > 0 ? expected_outer : (max_iter < 32 ? max_iter : 32));
+  const double n = (double)H.n, q = (double)H.q;
+  const double saved = (method == 0) ? 8.0 * q * (n + 1.0) : 8.0 * q * (n + 1.0) - 8.0 * n * n;
+  const double flops = q * n * (n + 1.0) + (method == 0 ? 2.0 * n * n * n : 0.0);
+  constexpr double kHbm = 6.0e12, kDmma = 3.0e13;
+  return (saved > 0.0 && K * saved / kHbm > flops / kDmma) ? 2 : 0;
+}
+
 static int solve_common(ils_handle h, int method, const double* x0, double* x, double tol, int64_t max_iter,
                         const ils_opts* opts_in, ils_report* rep) {
   if (!h || !x) {
@@ -553,8 +565,10 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
   }
 
   const int64_t np = H.npad;
+  if (o.sp_form == ILS_SP_FORM_AUTO) o.sp_form = auto_sp_form(H, method, max_iter, o.expected_outer);
+  if (rep) rep->sp_form_used = o.sp_form;
   if (o.sp_form < 0 || o.sp_form > 2 || (o.sp_form == 1 && method != 0)) {
-    set_error("solve: sp_form must be 0 or 2 (RK/RGS), 0..2 (SP)");
+    set_error("solve: sp_form must be 0, 2 or 3 (RK/RGS), 0..3 (SP)");
     return ILS_ERR_ARG;
   }
   if (H.sparse && o.sp_form == 2) {

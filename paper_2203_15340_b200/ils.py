@@ -20,6 +20,7 @@ ILS_ERR_CUDA, ILS_ERR_NOMEM, ILS_ERR_UNSUPPORTED = -5, -6, -7
 ILS_STOP_XREF, ILS_STOP_RR, ILS_STOP_NONE = 0, 1, 2
 ILS_FORMAT_DENSE, ILS_FORMAT_CSR = 0, 1
 ILS_ALPHA_UNIFORM, ILS_ALPHA_FIXED = 0, 1
+ILS_SP_FORM_AUTO = 3
 
 EXPORTED = [
     "ils_default_opts", "ils_status_string", "ils_last_error", "ils_create", "ils_sp_solve",
@@ -38,7 +39,8 @@ class IlsOpts(C.Structure):
     _fields_ = [("stop", C.c_int32), ("x_ref", C.c_void_p), ("inner_tol", C.c_double),
                 ("max_inner", C.c_int64), ("check_every", C.c_int64), ("seed", C.c_uint64),
                 ("alpha_mode", C.c_int32), ("alpha_k", C.c_int32), ("weighted", C.c_int32),
-                ("sp_form", C.c_int32), ("x_hist", C.c_void_p), ("inner_hist", C.c_void_p)]
+                ("sp_form", C.c_int32), ("x_hist", C.c_void_p), ("inner_hist", C.c_void_p),
+                ("expected_outer", C.c_int64)]
 
 
 class IlsReport(C.Structure):
@@ -46,7 +48,7 @@ class IlsReport(C.Structure):
                 ("final_metric", C.c_double), ("setup_ms", C.c_double), ("solve_ms", C.c_double),
                 ("bytes_touched", C.c_double), ("kernel_launches", C.c_int64),
                 ("hot_ms", C.c_double * 4), ("hot_work", C.c_double * 4), ("hot_launches", C.c_int64 * 4),
-                ("inst_iters", C.c_void_p), ("inst_status", C.c_void_p)]
+                ("inst_iters", C.c_void_p), ("inst_status", C.c_void_p), ("sp_form_used", C.c_int32)]
 
     def as_dict(self):
         d = {}

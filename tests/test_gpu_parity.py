@@ -571,3 +571,29 @@ def test_bitwise_deterministic_runs(cfg):
         outs.append(res)
     for (xa, ia), (xb, ib) in zip(outs[0], outs[1]):
         assert np.array_equal(xa, xb) and np.array_equal(ia, ib)
+
+
+@pytest.mark.parametrize("method", ["sp", "rk"])
+def test_auto_form_choice_and_iterates(method):
+    """sp_form = ILS_SP_FORM_AUTO (include/ils.h "Automatic form"): a short expected
+    horizon keeps the streaming form 0, a long one takes the literal precompute (form 2); either way the
+    iterates equal the oracle's for the form the report names."""
+    pr = make_dense(180, 400, 40, 0.2, noise=0.05, seed=23)   # q >> n: the literal form's saving is large
+    K = 3
+    fn = {"sp": ils.ils_sp_solve, "rk": ils.ils_rk_solve}[method]
+    for exp_outer, want in ((1, 0), (10 ** 6, 2)):
+        hist = np.zeros((K, pr.n))
+        x = np.zeros(pr.n)
+        with H(pr) as hh:
+            o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, sp_form=ils.ILS_SP_FORM_AUTO, expected_outer=exp_outer,
+                                     seed=4, max_inner=200, check_every=40, inner_tol=0.0, x_hist=hist.ctypes.data)
+            st, rep = fn(hh.h, None, x, 0.0, K, o)
+        assert rep.sp_form_used == want, (exp_outer, rep.sp_form_used)
+        kw = dict(max_iter=K, stop=O.STOP_NONE)
+        if method == "sp":
+            ref = O.sp_solve(pr.A1, pr.A2, pr.b1, pr.b2, sp_form=want, **kw)
+        else:
+            ref = O.sp_rk_rgs_solve(pr.A1, pr.A2, pr.b1, pr.b2, seed=4, max_inner=200, check_every=40, inner_tol=0.0,
+                                    rhs_literal=(want == 2), **kw)
+        for k in range(K):
+            assert _par(hist[k], ref.x_hist[k]) <= 1e-9, (exp_outer, k)
