@@ -32,6 +32,7 @@ struct BatchParams {
   int64_t* inst_iters;
   int32_t* inst_status;
   unsigned long long* inner_total;
+  int32_t* err;        // set when an instance's A1^T A1 has a non-positive or non-finite pivot (SP)
 };
 
 struct BKey {
@@ -110,8 +111,12 @@ __global__ void __launch_bounds__(32) batched_kernel(BatchParams P) {
   __syncwarp();
   if (P.method == 0) {
     // Cholesky (lower, in place in G), then P = L^{-T} L^{-1}: lane c solves column c.
+    bool spd = true;
     for (int k = 0; k < n; ++k) {
-      if (lane == 0) G[k * n + k] = sqrt(G[k * n + k]);
+      const double piv = G[k * n + k];
+      spd = spd && piv > 0.0 && isfinite(piv);   // include/ils.h: ILS_ERR_NOT_SPD on breakdown
+      __syncwarp();
+      if (lane == 0) G[k * n + k] = sqrt(piv);
       __syncwarp();
       const double d = G[k * n + k];
       if (act && lane > k) G[lane * n + k] /= d;
@@ -119,6 +124,13 @@ __global__ void __launch_bounds__(32) batched_kernel(BatchParams P) {
       if (act && lane > k)
         for (int j = k + 1; j <= lane; ++j) G[lane * n + j] -= G[lane * n + k] * G[j * n + k];
       __syncwarp();
+    }
+    if (!spd) {
+      if (lane == 0) {
+        atomicExch(P.err, 1);
+        if (P.inst_status) P.inst_status[inst] = -1;
+      }
+      return;
     }
     double y[32];
 #pragma unroll
@@ -922,6 +934,7 @@ int batched_solve(Handle& h, int method, const double* x0, double* x, double tol
   P.inst_iters = inst_iters_dev;
   P.inst_status = inst_status_dev;
   P.inner_total = reinterpret_cast<unsigned long long*>(&h.dstat->inner_steps);
+  P.err = &h.dstat->flag_err;
   if (method == 1 && P.check_every % 4 == 0 && !getenv("ILS_BATCHED_RK_SINGLE")) {   // blocked, 4 steps/reduction
     const int rpl = (int)((h.p + 31) / 32);
     const int RPL = rpl <= 1 ? 1 : rpl <= 2 ? 2 : rpl <= 3 ? 3 : rpl <= 4 ? 4 : 8;

@@ -100,6 +100,18 @@ __global__ void nonfinite_kernel(const double* __restrict__ a, int64_t rows, int
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(flag, 1);
 }
 
+// batched ingest: flag an instance whose A1 has an all-zero column (include/ils.h ILS_ERR_ZERO_COLUMN)
+__global__ void batched_zero_col_kernel(const double* __restrict__ Ab, int64_t batch, int64_t m, int64_t n,
+                                        int64_t p, int32_t* flag) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < batch * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t inst = e / n, j = e - (e / n) * n;
+    const double* a = Ab + inst * m * n + j;
+    bool nz = false;
+    for (int64_t i = 0; i < p && !nz; ++i) nz = a[i * n] != 0.0;
+    if (!nz) atomicExch(flag, 1);
+  }
+}
+
 static int check_finite(Handle& h, const double* a, int64_t rows, int64_t cols, int64_t ld, bool* ok) {
   ILS_CU(cudaMemsetAsync(&h.dstat->flag_err, 0, sizeof(int32_t), h.stream));
   if (rows * cols > 0) {
@@ -328,6 +340,18 @@ int ils_create(ils_handle* out, const double* A, const double* b, int64_t p, int
       set_error("ils_create: non-finite entry in A or b");
       return fail(ILS_ERR_ARG);
     }
+    {
+      int32_t zc = 0;
+      CKC(cudaMemsetAsync(&h->dstat->flag_err, 0, sizeof(int32_t), st));
+      batched_zero_col_kernel<<<h->num_sms * 4, 256, 0, st>>>(h->Ab, batch, m, n, p, &h->dstat->flag_err);
+      ILS_LAUNCHED("batched_zero_col_kernel");
+      CKC(cudaMemcpyAsync(&zc, &h->dstat->flag_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      CKC(cudaStreamSynchronize(st));
+      if (zc) {
+        set_error("ils_create: an instance's A1 has a zero column (||A1_(j)||^2 = 0)");
+        return fail(ILS_ERR_ZERO_COLUMN);
+      }
+    }
     *out = h;
     return ILS_OK;
   }
@@ -533,6 +557,11 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
     ILS_CU(cudaStreamSynchronize(st));
     cudaFreeAsync(it_dev, st);
     cudaFreeAsync(st_dev, st);
+    if (H.hstat->flag_err) {   // batched SP: an instance's A1^T A1 broke down in the Cholesky
+      if (rep && rep->inst_status) std::memcpy(rep->inst_status, sts.data(), B * sizeof(int32_t));
+      set_error("batched SP: Cholesky of an instance's A1^T A1 broke down (inst_status -1)");
+      return ILS_ERR_NOT_SPD;
+    }
     int64_t mx = 0;
     bool all = true;
     for (int64_t i = 0; i < B; ++i) {

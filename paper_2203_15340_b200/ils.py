@@ -115,6 +115,30 @@ def _ptr(a):
     raise TypeError(f"unsupported array type {type(a)}")
 
 
+def _arr(a, dtype, count, what):
+    """Pointer of `a` after checking its element type and that it holds at least `count` elements
+    (argument marshalling: a wrong dtype or a short buffer would make the library read past it)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        ok = a.dtype == np.dtype(dtype)
+        size = a.size
+    elif hasattr(a, "data_ptr"):
+        import torch
+        ok = a.dtype == {"float64": torch.float64, "int64": torch.int64, "int32": torch.int32}[dtype]
+        size = a.numel()
+    else:
+        raise TypeError(f"{what}: unsupported array type {type(a)}")
+    if not ok:
+        raise TypeError(f"{what}: expected {dtype}, got {a.dtype}")
+    if size < count:
+        raise ValueError(f"{what}: {size} elements, the call reads {count}")
+    return _ptr(a)
+
+
+_shape = {}   # handle value -> (n, batch), for the solve-side length checks
+
+
 class IlsError(RuntimeError):
     def __init__(self, status, where):
         lib = load_library()
@@ -145,25 +169,35 @@ def ils_create(A, b, p: int, q: int, n: int, batch: int = 1, lda: int = 0, strea
     comm (ils_comm_create): A, b are this rank's row block, p, q its local row counts."""
     lib = load_library()
     h = C.c_void_p()
+    m = p + q
     if row_ptr is not None:
         nnz = int(A.numel() if hasattr(A, "numel") else A.size)
-        ext = IlsExt(ILS_FORMAT_CSR, 1, 0, stream, _ptr(row_ptr), _ptr(col_idx), nnz, comm)
+        ext = IlsExt(ILS_FORMAT_CSR, 1, 0, stream, _arr(row_ptr, "int64", m + 1, "row_ptr"),
+                     _arr(col_idx, "int32", nnz, "col_idx"), nnz, comm)
+        pa = _arr(A, "float64", nnz, "A (CSR values)")
     else:
         ext = IlsExt(ILS_FORMAT_DENSE, batch, lda, stream, None, None, 0, comm)
-    _check(lib.ils_create(C.byref(h), _ptr(A), _ptr(b), p, q, n, C.byref(ext)), "ils_create")
+        ld = lda if lda else n
+        pa = _arr(A, "float64", (batch * m - 1) * ld + n if m > 0 else 0, "A")
+    pb = _arr(b, "float64", batch * m, "b")
+    _check(lib.ils_create(C.byref(h), pa, pb, p, q, n, C.byref(ext)), "ils_create")
+    _shape[h.value] = (n, batch)
     return h
 
 
 def ils_destroy(h):
+    _shape.pop(getattr(h, "value", None), None)
     load_library().ils_destroy(h)
 
 
 def _solve(fn, name, h, x0, x, tol, max_iter, opts, inst_iters=None, inst_status=None):
     rep = IlsReport()
-    rep.inst_iters = _ptr(inst_iters)
-    rep.inst_status = _ptr(inst_status)
+    n, batch = _shape.get(getattr(h, "value", None), (0, 1))
+    rep.inst_iters = _arr(inst_iters, "int64", batch, "inst_iters")
+    rep.inst_status = _arr(inst_status, "int32", batch, "inst_status")
     o = opts if opts is not None else ils_default_opts()
-    st = _check(fn(h, _ptr(x0), _ptr(x), float(tol), int(max_iter), C.byref(o), C.byref(rep)), name)
+    st = _check(fn(h, _arr(x0, "float64", batch * n, "x0"), _arr(x, "float64", batch * n, "x"), float(tol),
+                   int(max_iter), C.byref(o), C.byref(rep)), name)
     return st, rep
 
 

@@ -53,3 +53,30 @@ def test_struct_layout_matches_header(tmp_path):
     want = [C.sizeof(ils.IlsExt), C.sizeof(ils.IlsOpts), C.sizeof(ils.IlsReport),
             ils.IlsOpts.seed.offset, ils.IlsOpts.x_hist.offset, ils.IlsReport.kernel_launches.offset]
     assert got == want
+
+
+def test_binding_rejects_wrong_dtypes_and_short_buffers():
+    """The binding checks element types and lengths before handing pointers to the library (ADVICE
+    round 1): float32 A / b, an int32 row pointer, a short b or a short x never reach libils."""
+    import numpy as np
+    A = np.ones((6, 3))
+    with pytest.raises(TypeError):
+        ils.ils_create(A.astype(np.float32), np.ones(6), 4, 2, 3)
+    with pytest.raises(TypeError):
+        ils.ils_create(A, np.ones(6, dtype=np.float32), 4, 2, 3)
+    with pytest.raises(ValueError):
+        ils.ils_create(A, np.ones(5), 4, 2, 3)
+    with pytest.raises(ValueError):
+        ils.ils_create(np.ones((5, 3)), np.ones(6), 4, 2, 3)
+    vals = np.ones(6)
+    with pytest.raises(TypeError):
+        ils.ils_create(vals, np.ones(6), 4, 2, 3, row_ptr=np.arange(7, dtype=np.int32),
+                       col_idx=np.zeros(6, dtype=np.int32))
+    with pytest.raises(TypeError):
+        ils.ils_create(vals, np.ones(6), 4, 2, 3, row_ptr=np.arange(7, dtype=np.int64),
+                       col_idx=np.zeros(6, dtype=np.int64))
+    ils._shape[12345] = (3, 1)
+    import ctypes as C
+    with pytest.raises(ValueError):
+        ils.ils_sp_solve(C.c_void_p(12345), None, np.zeros(2), 0.0, 1)
+    ils._shape.pop(12345)

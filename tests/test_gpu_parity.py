@@ -597,3 +597,32 @@ def test_auto_form_choice_and_iterates(method):
                                     rhs_literal=(want == 2), **kw)
         for k in range(K):
             assert _par(hist[k], ref.x_hist[k]) <= 1e-9, (exp_outer, k)
+
+
+def test_batched_zero_column_and_not_spd_errors():
+    """Batched handles report the errors include/ils.h promises: an instance with a
+    zero A1 column fails ils_create with ILS_ERR_ZERO_COLUMN; an instance whose A1^T A1 is singular
+    (two equal columns 2 e_0: the second Cholesky pivot is exactly 4 - 2 * 2 = 0) makes SP return
+    ILS_ERR_NOT_SPD with inst_status -1 for that instance."""
+    from workloads import make_batched
+    bt = make_batched(batch=8, p=96, q=32, n=32, base_seed=500)
+    A = bt.A.copy()
+    A[5, :96, 7] = 0.0
+    with pytest.raises(ils.IlsError) as e:
+        ils.ils_create(A, bt.b, bt.p, bt.q, bt.n, batch=bt.batch)
+    assert e.value.status == ils.ILS_ERR_ZERO_COLUMN
+    A = bt.A.copy()
+    A[3, :96, 0] = 0.0
+    A[3, :96, 1] = 0.0
+    A[3, 0, 0] = 2.0
+    A[3, 0, 1] = 2.0
+    h = ils.ils_create(A, bt.b, bt.p, bt.q, bt.n, batch=bt.batch)
+    try:
+        x = np.zeros((bt.batch, bt.n))
+        sts = np.zeros(bt.batch, dtype=np.int32)
+        with pytest.raises(ils.IlsError) as e:
+            ils.ils_sp_solve(h, None, x, 0.0, 3, ils.ils_default_opts(stop=ils.ILS_STOP_NONE), inst_status=sts)
+        assert e.value.status == ils.ILS_ERR_NOT_SPD
+        assert sts[3] == -1
+    finally:
+        ils.ils_destroy(h)
