@@ -46,7 +46,8 @@
  *     round (L, R) -> (R, L xor F(R, K_r)), F(R, K) = mix32(R xor K) & (2^h - 1),
  *     mix32(x): x *= 0x85EBCA6B; x ^= x >> 13; x *= 0xC2B2AE35; x ^= x >> 16 (mod 2^32),
  *     value = (L << h) | R, cycle-walked (re-encrypted) until < n; pi = identity for n = 1.
- *     tau_t = { pi(0), ..., pi(alpha_t - 1) }; j_t = argmax_{s in tau_t} r_s^2,
+ *     tau_t = { pi(0), ..., pi(alpha_t - 1) } (alpha_mode | ILS_SUBSET_EXACT: see
+ *     below); j_t = argmax_{s in tau_t} r_s^2,
  *     ties to the smallest s.
  *   SP-RCD step t (weighted = 1): tag 6, j from U = x1:x0 with the column weights.
  *   Batched instance i uses seed + i.
@@ -97,6 +98,13 @@ enum {
 enum { ILS_STOP_XREF = 0, ILS_STOP_RR = 1, ILS_STOP_NONE = 2 };
 enum { ILS_FORMAT_DENSE = 0, ILS_FORMAT_CSR = 1 };
 enum { ILS_ALPHA_UNIFORM = 0, ILS_ALPHA_FIXED = 1 };
+/* OR into alpha_mode: exact uniform subsets instead of the Feistel prefix (the
+ * study of reading R9 / Q9): coordinate s at SP-SCD step t gets the key u_s = word (s mod 4) of the
+ * Philox draw with counter (t_lo, t_hi, k, 7 + 256 * floor(s / 4)); tau_t = the alpha_t coordinates
+ * with the smallest (u_s, s) in lexicographic order. The keys are i.i.d. uniform, so every subset
+ * of size alpha_t has probability 1 / C(n, alpha_t) up to equal keys (probability < n^2 / 2^33 per
+ * step). Single-instance handles only (batched: ILS_ERR_UNSUPPORTED). */
+#define ILS_SUBSET_EXACT 0x10
 
 /* Optional creation extras; NULL = dense, batch 1, lda = n, default stream. */
 typedef struct {

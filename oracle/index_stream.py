@@ -32,6 +32,8 @@ TAG_SCD_A = 2
 TAG_SCD_B = 3
 TAG_SCD_C = 4
 TAG_RCD = 6
+TAG_SUBSET = 7
+SUBSET_EXACT = 0x10
 FEISTEL_ROUNDS = 8
 
 
@@ -195,8 +197,27 @@ def scd_alpha_keys(seed: int, k: int, t: int, n: int, alpha_mode: int = 0, alpha
     return alpha, keys
 
 
+def subset_keys(seed: int, k: int, t: int, n: int):
+    """Exact-subset keys (include/ils.h ILS_SUBSET_EXACT): u_s = word (s mod 4) of the Philox draw
+    with counter (t_lo, t_hi, k, 7 + 256 * floor(s / 4)), key (seed_lo, seed_hi)."""
+    nb = (n + 3) // 4
+    b = np.arange(nb, dtype=np.uint64)
+    t = int(t)
+    ctr = np.stack([np.full(nb, t & M32, dtype=np.uint64), np.full(nb, (t >> 32) & M32, dtype=np.uint64),
+                    np.full(nb, k & M32, dtype=np.uint64), np.uint64(TAG_SUBSET) + np.uint64(256) * b], axis=-1)
+    X = philox4x32_10(ctr, (seed & M32, (seed >> 32) & M32))
+    return X.reshape(-1)[:n]
+
+
 def scd_subset(seed: int, k: int, t: int, n: int, alpha_mode: int = 0, alpha_fixed: int = 1):
-    """tau_t = { pi(0), ..., pi(alpha_t - 1) } (Alg. 5 step 8)."""
+    """tau_t = { pi(0), ..., pi(alpha_t - 1) } (Alg. 5 step 8). alpha_mode | SUBSET_EXACT: the
+    alpha_t coordinates with the smallest (key, index) -- an exactly uniform size-alpha_t subset
+    (Alg. 5 step 8 read literally), for the study of reading R9."""
+    if alpha_mode & SUBSET_EXACT:
+        alpha, _ = scd_alpha_keys(seed, k, t, n, alpha_mode & 0xF, alpha_fixed)
+        u = subset_keys(seed, k, t, n)
+        order = np.lexsort((np.arange(n), u))      # by key, then by index
+        return alpha, np.sort(order[:alpha].astype(np.int64))
     alpha, keys = scd_alpha_keys(seed, k, t, n, alpha_mode, alpha_fixed)
     tau = feistel_forward(np.arange(alpha, dtype=np.uint64), keys, n)
     return alpha, np.sort(tau.astype(np.int64))

@@ -506,7 +506,8 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
     set_error("solve: ILS_STOP_XREF needs opts->x_ref");
     return ILS_ERR_ARG;
   }
-  if (o.stop < 0 || o.stop > 2 || (o.alpha_mode == ILS_ALPHA_FIXED && o.alpha_k < 1)) {
+  if (o.stop < 0 || o.stop > 2 || (o.alpha_mode & ~(0xF | ILS_SUBSET_EXACT)) || (o.alpha_mode & 0xF) > ILS_ALPHA_FIXED ||
+      ((o.alpha_mode & 0xF) == ILS_ALPHA_FIXED && o.alpha_k < 1)) {
     set_error("solve: bad option");
     return ILS_ERR_ARG;
   }
@@ -533,8 +534,8 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
   if ((rc = sxr.in(o.x_ref, (size_t)B * n * sizeof(double), st))) return rc;
 
   if (B > 1) {
-    if (o.stop == ILS_STOP_RR) {
-      set_error("batched: ILS_STOP_RR not supported");
+    if (o.stop == ILS_STOP_RR || (method == 2 && (o.alpha_mode & ILS_SUBSET_EXACT))) {
+      set_error("batched: ILS_STOP_RR and exact uniform subsets are not supported");
       return ILS_ERR_UNSUPPORTED;
     }
     ils_opts od = o;

@@ -71,7 +71,7 @@ __device__ __forceinline__ void scd_make_key(uint64_t seed, uint32_t k, uint64_t
   const U4 a = draw(seed, k, t, kTagScdA);
   const U4 b = draw(seed, k, t, kTagScdB);
   const U4 c = draw(seed, k, t, kTagScdC);
-  e.alpha = alpha_mode == ILS_ALPHA_UNIFORM ? 1u + mulhi32(a.x, (uint32_t)n)
+  e.alpha = (alpha_mode & 0xF) == ILS_ALPHA_UNIFORM ? 1u + mulhi32(a.x, (uint32_t)n)
                                             : (uint32_t)((alpha_k < n) ? alpha_k : n);
   e.j = -1;
   e.key[0] = a.y; e.key[1] = a.z; e.key[2] = a.w;
@@ -100,6 +100,131 @@ __global__ void __launch_bounds__(256) scd_masks_kernel(uint64_t seed, uint32_t 
     }
     masks[(int64_t)blockIdx.x * NT + th] = bits;
   }
+}
+
+// ---- exact uniform subsets (alpha_mode | ILS_SUBSET_EXACT, include/ils.h)
+// key of coordinate s at step t: word s & 3 of the Philox draw with counter (t, k, 7 + 256 (s >> 2))
+__device__ __forceinline__ void subset_keys_block(uint64_t seed, uint32_t k, uint64_t t, int n, uint32_t* u) {
+  for (int b = threadIdx.x; 4 * b < n; b += blockDim.x) {
+    const U4 x = draw(seed, k, t, 7u + 256u * (uint32_t)b);
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (4 * b + q < n) u[4 * b + q] = w[q];
+  }
+}
+
+// the alpha-th smallest key T (radix select, four 8-bit passes) and how many keys equal to T are in
+// tau (ties by index); the CTA's threads cooperate, results in *T_out / *need_out (shared)
+__device__ void subset_select(const uint32_t* u, int n, uint32_t alpha, uint32_t* hist, uint32_t* T_out,
+                              int* need_out) {
+  uint32_t prefix = 0, pmask = 0, rank = alpha - 1;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int s = threadIdx.x; s < n; s += blockDim.x)
+      if ((u[s] & pmask) == prefix) atomicAdd(&hist[(u[s] >> shift) & 255u], 1u);
+    __syncthreads();
+    if (threadIdx.x < 32) {   // bin holding rank: lane l scans bins 8l .. 8l+7
+      const int l = threadIdx.x;
+      uint32_t c[8], tot = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        c[q] = hist[8 * l + q];
+        tot += c[q];
+      }
+      uint32_t incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (l >= o) incl += y;
+      }
+      uint32_t before = incl - tot;
+      const bool mine = before <= rank && rank < incl;
+      int bin = 0;
+      uint32_t below = 0;
+      if (mine) {
+        uint32_t acc = before;
+        for (int q = 0; q < 8; ++q) {
+          if (rank < acc + c[q]) {
+            bin = 8 * l + q;
+            below = acc;
+            break;
+          }
+          acc += c[q];
+        }
+      }
+      const unsigned who = __ballot_sync(0xffffffffu, mine);
+      const int src = __ffs(who) - 1;
+      bin = __shfl_sync(0xffffffffu, bin, src);
+      below = __shfl_sync(0xffffffffu, below, src);
+      if (l == 0) {
+        hist[256] = (uint32_t)bin;
+        hist[257] = below;
+      }
+    }
+    __syncthreads();
+    prefix |= hist[256] << shift;
+    pmask |= 255u << shift;
+    rank -= hist[257];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *T_out = prefix;
+    *need_out = (int)rank + 1;
+  }
+  __syncthreads();
+}
+
+// s in tau: u_s < T, or u_s == T and fewer than `need` coordinates s' < s have u_s' == T
+__device__ __forceinline__ bool subset_member(const uint32_t* u, int n, int s, uint32_t T, int need) {
+  const uint32_t v = u[s];
+  if (v != T) return v < T;
+  int before = 0;
+  for (int q = 0; q < s; ++q) before += (u[q] == T);
+  return before < need;
+}
+
+__global__ void __launch_bounds__(256) scd_masks_exact_kernel(uint64_t seed, uint32_t k, int64_t t0, int64_t t1, int n,
+                                                              int alpha_mode, int alpha_k, int NT, int V,
+                                                              uint32_t* __restrict__ masks) {
+  extern __shared__ uint32_t ukeys[];   // [n] keys, then [258] histogram + select scratch
+  uint32_t* hist = ukeys + n;
+  __shared__ ScdKey e;
+  __shared__ uint32_t T_s;
+  __shared__ int need_s;
+  const int64_t u = t0 + blockIdx.x;
+  if (u >= t1) return;
+  if (threadIdx.x == 0) scd_make_key(seed, k, (uint64_t)u, n, alpha_mode, alpha_k, 0, nullptr, e);
+  subset_keys_block(seed, k, (uint64_t)u, n, ukeys);
+  __syncthreads();
+  subset_select(ukeys, n, e.alpha, hist, &T_s, &need_s);
+  const uint32_t T = T_s;
+  const int need = need_s;
+  for (int th = threadIdx.x; th < NT; th += blockDim.x) {
+    uint32_t bits = 0;
+    for (int v = 0; v < V; ++v) {
+      const int s = th + v * NT;
+      if (s < n && subset_member(ukeys, n, s, T, need)) bits |= 1u << v;
+    }
+    masks[(int64_t)blockIdx.x * NT + th] = bits;
+  }
+}
+
+// membership masks of steps [t0, t1) for either subset construction (one CTA per step)
+static int launch_masks(cudaStream_t st, uint64_t seed, uint32_t k, int64_t t0, int64_t t1, int n, int alpha_mode,
+                         int alpha_k, int NT, int V, uint32_t* masks) {
+  if (alpha_mode & ILS_SUBSET_EXACT) {
+    const size_t smem = ((size_t)n + 258) * sizeof(uint32_t);
+    cudaFuncSetAttribute(scd_masks_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    scd_masks_exact_kernel<<<(unsigned)(t1 - t0), 256, smem, st>>>(seed, k, t0, t1, n, alpha_mode, alpha_k, NT, V,
+                                                                    masks);
+    ILS_LAUNCHED("scd_masks_exact_kernel");
+  } else {
+    scd_masks_kernel<<<(unsigned)(t1 - t0), 256, 0, st>>>(seed, k, t0, t1, n, alpha_mode, alpha_k, NT, V, masks);
+    ILS_LAUNCHED("scd_masks_kernel");
+  }
+  return ILS_OK;
 }
 
 // Single-warp SP-SCD for n <= 256 (non-weighted): lane l owns coordinates l + 32 v (v < V) of r
@@ -461,10 +586,7 @@ __global__ void __launch_bounds__(256) scd_check_kernel(const double* __restrict
 int scd_masks(Handle& h, uint64_t seed, int64_t k, int64_t t0, int64_t t1, int alpha_mode, int alpha_k, int NT, int V,
               uint32_t* masks) {
   if (t1 <= t0) return ILS_OK;
-  scd_masks_kernel<<<(unsigned)(t1 - t0), 256, 0, h.stream>>>(seed, (uint32_t)k, t0, t1, (int)h.n, alpha_mode, alpha_k,
-                                                               NT, V, masks);
-  ILS_LAUNCHED("scd_masks_kernel");
-  return ILS_OK;
+  return launch_masks(h.stream, seed, (uint32_t)k, t0, t1, (int)h.n, alpha_mode, alpha_k, NT, V, masks);
 }
 
 int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_t k, int64_t max_inner,
@@ -532,7 +654,7 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
   p.alpha_mode = alpha_mode;
   p.alpha_k = alpha_k;
   p.weighted = weighted;
-  p.all_members = (!weighted && alpha_mode == ILS_ALPHA_FIXED && alpha_k >= h.n) ? 1 : 0;
+  p.all_members = (!weighted && (alpha_mode & 0xF) == ILS_ALPHA_FIXED && alpha_k >= h.n) ? 1 : 0;
   p.st = h.dstat;
   size_t smem = 2 * (size_t)((h.n + 1) & ~1) * 8 + SCD_RING * sizeof(ScdKey);
   {   // candidate-row prefetch (chunk kernel, argmax modes): 2 x NW rows of A1bar + mbarriers
@@ -580,9 +702,8 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
   while (t < max_inner) {
     const int64_t t1 = (t + span < max_inner) ? t + span : max_inner;
     if (!weighted && !p.all_members) {
-      scd_masks_kernel<<<(unsigned)(t1 - t), 256, 0, st>>>(seed, (uint32_t)k, t, t1, nn, alpha_mode, alpha_k, nt,
-                                                            V, masks);
-      ILS_LAUNCHED("scd_masks_kernel");
+      const int rm = launch_masks(st, seed, (uint32_t)k, t, t1, nn, alpha_mode, alpha_k, nt, V, masks);
+      if (rm) return rm;
     }
     p.t0 = t;
     p.t1 = t1;
@@ -619,6 +740,21 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
   return ILS_OK;
 }
 
+__global__ void scd_subset_exact_kernel(int n, uint64_t seed, uint32_t k, uint64_t t, int alpha_mode, int alpha_k,
+                                        int32_t* alpha_out, uint8_t* mask) {
+  extern __shared__ uint32_t ukeys[];
+  uint32_t* hist = ukeys + n;
+  __shared__ ScdKey e;
+  __shared__ uint32_t T_s;
+  __shared__ int need_s;
+  if (threadIdx.x == 0) scd_make_key(seed, k, t, n, alpha_mode, alpha_k, 0, nullptr, e);
+  subset_keys_block(seed, k, t, n, ukeys);
+  __syncthreads();
+  subset_select(ukeys, n, e.alpha, hist, &T_s, &need_s);
+  for (int s = threadIdx.x; s < n; s += blockDim.x) mask[s] = subset_member(ukeys, n, s, T_s, need_s) ? 1 : 0;
+  if (threadIdx.x == 0) *alpha_out = (int32_t)e.alpha;
+}
+
 __global__ void scd_subset_kernel(int n, uint64_t seed, uint32_t k, uint64_t t, int alpha_mode, int alpha_k,
                                   int32_t* alpha_out, uint8_t* mask) {
   __shared__ ScdKey e;
@@ -634,6 +770,15 @@ __global__ void scd_subset_kernel(int n, uint64_t seed, uint32_t k, uint64_t t, 
 
 int scd_subset_mask(int64_t n, uint64_t seed, int64_t k, int64_t t, int alpha_mode, int alpha_k,
                     int32_t* alpha_dev, uint8_t* mask_dev, cudaStream_t st) {
+  if (alpha_mode & ILS_SUBSET_EXACT) {
+    const size_t smem = ((size_t)n + 258) * sizeof(uint32_t);
+    if (smem > 200 * 1024) return ILS_ERR_UNSUPPORTED;
+    ILS_CU(cudaFuncSetAttribute(scd_subset_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    scd_subset_exact_kernel<<<1, 256, smem, st>>>((int)n, seed, (uint32_t)k, (uint64_t)t, alpha_mode, alpha_k,
+                                                  alpha_dev, mask_dev);
+    ILS_LAUNCHED("scd_subset_exact_kernel");
+    return ILS_OK;
+  }
   scd_subset_kernel<<<32, 256, 0, st>>>((int)n, seed, (uint32_t)k, (uint64_t)t, alpha_mode, alpha_k,
                                         alpha_dev, mask_dev);
   ILS_LAUNCHED("scd_subset_kernel");

@@ -1263,7 +1263,7 @@ int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed,
   prm.Bv = Bv;
   prm.masks = masks;
   prm.V = V;
-  prm.all_members = (alpha_mode == ILS_ALPHA_FIXED && alpha_k >= h.n) ? 1 : 0;
+  prm.all_members = ((alpha_mode & 0xF) == ILS_ALPHA_FIXED && alpha_k >= h.n) ? 1 : 0;
   prm.jw = weighted ? reinterpret_cast<const int32_t*>(masks) : nullptr;   // chunk_cap <= the mask space
   prm.st = h.dstat;
   const size_t smem = (size_t)h.npad * sizeof(double);

@@ -21,6 +21,7 @@ ILS_STOP_XREF, ILS_STOP_RR, ILS_STOP_NONE = 0, 1, 2
 ILS_FORMAT_DENSE, ILS_FORMAT_CSR = 0, 1
 ILS_ALPHA_UNIFORM, ILS_ALPHA_FIXED = 0, 1
 ILS_SP_FORM_AUTO = 3
+ILS_SUBSET_EXACT = 0x10
 
 EXPORTED = [
     "ils_default_opts", "ils_status_string", "ils_last_error", "ils_create", "ils_sp_solve",

@@ -626,3 +626,39 @@ def test_batched_zero_column_and_not_spd_errors():
         assert sts[3] == -1
     finally:
         ils.ils_destroy(h)
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 17, 50, 1000, 4000])
+def test_exact_subset_replay(n):
+    """ILS_SUBSET_EXACT: alpha_t and the membership of the key-selection subset are
+    bit-exact against the oracle's independent implementation of the include/ils.h text."""
+    for (seed, k, t) in [(0, 0, 0), (3, 2, 99), (11, 9, 123456)]:
+        for mode, ak in [(0, 1), (1, 1), (1, max(1, n // 3)), (1, n)]:
+            alpha, mask = ils.ils_scd_subset(n, seed, k, t, mode | ils.ILS_SUBSET_EXACT, ak)
+            a_o, tau = ix.scd_subset(seed, k, t, n, mode | ix.SUBSET_EXACT, ak)
+            assert alpha == a_o
+            assert np.array_equal(np.flatnonzero(mask), tau)
+
+
+@pytest.mark.parametrize("shape,force_large", [((200, 100, 50), False), ((1400, 300, 1000), False),
+                                               ((260, 60, 130), True)])
+def test_scd_exact_subsets_fixed_horizon(shape, force_large, monkeypatch):
+    """SP-SCD with exact uniform subsets through the one-warp (n = 50), one-CTA (n = 1000) and
+    forced-large cluster kernels: inner counts and iterates against the oracle."""
+    monkeypatch.setenv("ILS_FORCE_LARGE", "1" if force_large else "0")
+    p, q, n = shape
+    pr = make_dense(p, q, n, 0.3, noise=0.05, seed=24)
+    K, T, ce = 2, 400, 100
+    mode = ils.ILS_ALPHA_UNIFORM | ils.ILS_SUBSET_EXACT
+    ref = O.sp_scd_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE, seed=8, max_inner=T,
+                         check_every=ce, inner_tol=0.0, alpha_mode=mode)
+    hist = np.zeros((K, n))
+    inner = np.zeros(K, dtype=np.int64)
+    x = np.zeros(n)
+    with H(pr) as hh:
+        o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, seed=8, max_inner=T, check_every=ce, inner_tol=0.0,
+                                 alpha_mode=mode, x_hist=hist.ctypes.data, inner_hist=inner.ctypes.data)
+        ils.ils_rgs_solve(hh.h, None, x, 0.0, K, o)
+    assert list(inner) == list(ref.inner_hist)
+    for k in range(K):
+        assert _par(hist[k], ref.x_hist[k]) <= 1e-9, k

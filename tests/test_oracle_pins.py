@@ -539,3 +539,36 @@ def test_oracle_not_imported_by_product():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def test_p16b_exact_subsets_are_uniform_and_match_alg3():
+    """SURVEY.md §8 f3 (include/ils.h ILS_SUBSET_EXACT): the key-selection subsets are exactly uniform
+    -- every size-alpha subset equally likely (chi-square over all C(5,2) pairs) -- and the selected
+    index of Alg. 5 step 9 then follows the exact Alg. 3 step-10 law (Eq. Sec4.111)
+    reweighted to uniform subsets; key ties are broken by index (u, s) lexicographically."""
+    from itertools import combinations
+    from scipy.stats import chisquare
+    n = 5
+    pairs = {c: i for i, c in enumerate(combinations(range(n), 2))}
+    cnt = np.zeros(len(pairs))
+    for t in range(12000):
+        _, tau = ix.scd_subset(2, 1, t, n, alpha_mode=1 | ix.SUBSET_EXACT, alpha_fixed=2)
+        cnt[pairs[tuple(int(v) for v in tau)]] += 1
+    assert chisquare(cnt).pvalue > 1e-3
+    # alpha_t policy unchanged by the flag
+    a0 = [ix.scd_subset(1, 0, t, 9, alpha_mode=0)[0] for t in range(50)]
+    a1 = [ix.scd_subset(1, 0, t, 9, alpha_mode=ix.SUBSET_EXACT)[0] for t in range(50)]
+    assert a0 == a1
+    # the selected index: argmax of r^2 over a uniform 3-subset of 6 -> P(j = the i-th largest) =
+    # C(6-1-i, 2) / C(6, 3) (the subset contains j and two of the smaller ones)
+    r = np.array([0.3, -2.0, 1.1, 0.7, -1.5, 0.1])
+    order = np.argsort(-r * r)
+    exp = np.array([sum(1 for c in combinations(range(6), 3) if order[min(order.tolist().index(s) for s in c)] == j)
+                    for j in range(6)], dtype=float)
+    got = np.zeros(6)
+    for t in range(6000):
+        _, tau = ix.scd_subset(5, 2, t, 6, alpha_mode=1 | ix.SUBSET_EXACT, alpha_fixed=3)
+        got[O.scd_select(r, tau)] += 1
+    sup = exp > 0
+    assert np.all(got[~sup] == 0)
+    assert chisquare(got[sup], exp[sup] / exp.sum() * got.sum()).pvalue > 1e-3

@@ -30,6 +30,9 @@ def main():
     ap.add_argument("--seeds", type=int, default=3)
     ap.add_argument("--max-inner", type=int, default=2_000_000)
     ap.add_argument("--out", default="")
+    ap.add_argument("--subsets", action="store_true",
+                    help="Q9 study: Feistel-prefix subsets (reading R9) against exact uniform subsets "
+                         "(ILS_SUBSET_EXACT) under the same alpha policies")
     a = ap.parse_args()
     pr = make_problem(a.config)
     n = pr.n
@@ -49,6 +52,15 @@ def main():
                 (f"alpha = n/2 = {n // 2}", dict(alpha_mode=ils.ILS_ALPHA_FIXED, alpha_k=n // 2)),
                 (f"alpha = n (Motzkin)", dict(alpha_mode=ils.ILS_ALPHA_FIXED, alpha_k=n)),
                 ("weighted alpha = 1 (SP-RCD)", dict(alpha_mode=ils.ILS_ALPHA_FIXED, alpha_k=1, weighted=1))]
+    if a.subsets:   # quantify the deviation of the pseudo-uniform subsets (Q9)
+        E = ils.ILS_SUBSET_EXACT
+        sq = int(math.isqrt(n))
+        policies = []
+        for nm, am, ak in (("uniform alpha_t (paper)", ils.ILS_ALPHA_UNIFORM, 1),
+                           (f"alpha = sqrt(n) = {sq}", ils.ILS_ALPHA_FIXED, sq),
+                           (f"alpha = n/2 = {n // 2}", ils.ILS_ALPHA_FIXED, n // 2)):
+            policies.append((f"{nm}, Feistel prefix (R9)", dict(alpha_mode=am, alpha_k=ak)))
+            policies.append((f"{nm}, exact uniform subset", dict(alpha_mode=am | E, alpha_k=ak)))
     rows = []
     for name, kw in policies:
         runs = []
