@@ -82,6 +82,7 @@ struct Handle {
   bool sparse = false;
   int64_t nnz = 0, nnz1 = 0;
   double a1_row_sq = 0.0;   // sum over A1 rows of nnz_i^2
+  int64_t maxcol1 = -1;     // longest A1 column (CSC entries), computed on first use
   int64_t* rp = nullptr;    // [m+1]
   int32_t* ci = nullptr;    // [nnz]
   double* va = nullptr;     // [nnz]

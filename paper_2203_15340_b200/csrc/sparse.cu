@@ -20,6 +20,8 @@
 
 #include <cstdlib>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "ils_internal.h"
 
@@ -673,6 +675,226 @@ __global__ void __launch_bounds__(256) sparse_rk_check_kernel(const int64_t* __r
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Look-ahead SP-RK-RGS on CSR input (one CTA, all columns staged: <= SRK_LA_K entries each). The
+// gathers of w at the rows of a_u = A1_(j1_u) and of r at the rows of b_u = A1_(j2_u) are issued
+// two steps ahead, on the state S_g before steps g..u-1 (g = max(t0, u - 2)); the missing updates
+// enter the products through A1bar (dense, resident):
+//   <a_u, w_u> = <a_u, w_g> + sum_m s1_m <a_u, a_m>
+//   <b_u, r_u> = <b_u, r_g> + sum_m (s1_m <b_u, a_m> - s2_m <b_u, b_m>)        (m = g .. u-1)
+// (the identity of rk_rgs.cu's look-ahead kernel; Alg. 2 steps 9 and 11). The
+// updates are applied as floating-point reductions to global memory (one per address per step: a
+// row in both columns is updated once, by its b-entry, with s1 a_i - s2 b_i), ordered across steps
+// by the step barrier, so the result is deterministic. Per step: one block reduction of two values,
+// the gather latency is off the step chain.
+constexpr int SRK_LA_K = 512;   // EPT * SRK_T entries per column
+struct SpRkLaIdx {
+  int32_t j1, j2;
+  double bh1, rn1, rn2, g21;
+  double ga1, ga2, gb1, gb2, gbb1, gbb2;   // <a_t, a_{t-1}>, <a_t, a_{t-2}>, <b_t, a_{t-1}>, <b_t, a_{t-2}>,
+                                           // <b_t, b_{t-1}>, <b_t, b_{t-2}> (0 before the chunk start)
+  int64_t a1, a2;
+  int32_t k1, k2;
+};
+
+__device__ __forceinline__ void srk_la_fill(const SpRkParams& p, const uint64_t* Ss, SpRkLaIdx* ring, int64_t f0,
+                                            int lane) {
+  const int64_t t = f0 + lane;
+  SpRkLaIdx e{};
+  const bool live = t < p.t1;
+  if (live) {
+    const U4 x = draw(p.seed, p.k, (uint64_t)t, kTagRkRgs);
+    e.j1 = sample_weighted(((uint64_t)x.y << 32) | x.x, Ss, p.n);
+    e.j2 = sample_weighted(((uint64_t)x.w << 32) | x.z, Ss, p.n);
+    e.bh1 = p.bhat[e.j1];
+    e.rn1 = 1.0 / p.N[e.j1];
+    e.rn2 = 1.0 / p.N[e.j2];
+    e.a1 = p.cp[e.j1];
+    e.a2 = p.cp[e.j2];
+    e.k1 = (int32_t)(p.cp[e.j1 + 1] - e.a1);
+    e.k2 = (int32_t)(p.cp[e.j2 + 1] - e.a2);
+    ring[t & (SRK_RING - 1)].j1 = e.j1;
+    ring[t & (SRK_RING - 1)].j2 = e.j2;
+  }
+  __syncwarp();
+  if (live) {   // indices of steps t-1, t-2 (this fill or the previous one), then the Gram values
+    const int64_t np = p.npad;
+    const double* Ga = p.G + (int64_t)e.j1 * np;
+    const double* Gb = p.G + (int64_t)e.j2 * np;
+    e.g21 = Gb[e.j1];
+    if (t - 1 >= p.t0) {
+      const SpRkLaIdx& q = ring[(t - 1) & (SRK_RING - 1)];
+      e.ga1 = Ga[q.j1];
+      e.gb1 = Gb[q.j1];
+      e.gbb1 = Gb[q.j2];
+    }
+    if (t - 2 >= p.t0) {
+      const SpRkLaIdx& q = ring[(t - 2) & (SRK_RING - 1)];
+      e.ga2 = Ga[q.j1];
+      e.gb2 = Gb[q.j1];
+      e.gbb2 = Gb[q.j2];
+    }
+  }
+  __syncwarp();
+  if (live) ring[t & (SRK_RING - 1)] = e;
+}
+
+__global__ void __launch_bounds__(SRK_T) sparse_rk_la_kernel(SpRkParams p) {
+  extern __shared__ __align__(16) unsigned char srk_smem[];
+  double (*cvs)[2][SRK_MAXK] = reinterpret_cast<double (*)[2][SRK_MAXK]>(srk_smem);              // [D][2][MAXK]
+  int32_t (*crs)[2][SRK_MAXK] = reinterpret_cast<int32_t (*)[2][SRK_MAXK]>(srk_smem + SRK_D * 2 * SRK_MAXK * 8);
+  uint64_t* Ssm = reinterpret_cast<uint64_t*>(srk_smem + SRK_D * 2 * SRK_MAXK * 12);           // [n]
+  __shared__ SpRkLaIdx ring[SRK_RING];
+  __shared__ double red[2][SRK_T / 32][2];
+  __shared__ double bn_s;
+  constexpr int EPT = SRK_LA_K / SRK_T;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (*(volatile int32_t*)&p.st->inner_conv) return;
+  for (int j = tid; j < p.n; j += SRK_T) Ssm[j] = p.S[j];
+  if (p.t0 == 0) {   // b_hat = 0: z = 0 after 0 steps
+    double v = 0.0;
+    for (int j = tid; j < p.n; j += SRK_T) v = fma(p.bhat[j], p.bhat[j], v);
+    v = warp_sum(v);
+    if (lane == 0) red[0][warp][0] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < SRK_T / 32; ++w) s += red[0][w][0];
+      bn_s = s;
+    }
+    __syncthreads();
+    if (bn_s == 0.0) {
+      if (tid == 0) {
+        p.st->inner_steps = 0;
+        p.st->inner_conv = 1;
+      }
+      return;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) srk_la_fill(p, Ssm, ring, p.t0, lane);
+  __syncthreads();
+  if (warp == 0) srk_la_fill(p, Ssm, ring, p.t0 + 32, lane);
+  __syncthreads();
+  auto stage = [&](int64_t t) {   // cp.async the two columns of step t into slot t % D
+    if (t < p.t1) {
+      const SpRkLaIdx& ix = ring[t & (SRK_RING - 1)];
+      const int sl = (int)(t % SRK_D);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int64_t a = c ? ix.a2 : ix.a1;
+        const int k = c ? ix.k2 : ix.k1;
+        for (int e = tid; e < k; e += SRK_T) {
+          cp_async4(&crs[sl][c][e], p.cr + a + e);
+          cp_async8(&cvs[sl][c][e], p.cv + a + e);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  for (int64_t t = p.t0; t < p.t0 + SRK_D; ++t) stage(t);
+  double gw[3][EPT], gq[3][EPT];   // gathered w at rows of a_u, r at rows of b_u: buffer (u - t0) % 3
+  auto gather = [&](int64_t u, double (&w)[EPT], double (&q)[EPT]) {
+    const SpRkLaIdx& ix = ring[u & (SRK_RING - 1)];
+    const int sl = (int)(u % SRK_D);
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = tid + e * SRK_T;
+      w[e] = (i < ix.k1) ? p.W[crs[sl][0][i]] : 0.0;
+      q[e] = (i < ix.k2) ? p.Rv[crs[sl][1][i]] : 0.0;
+    }
+  };
+  cp_async_wait<SRK_D - 2>();   // slots t0, t0 + 1
+  __syncthreads();
+  if (p.t0 < p.t1) gather(p.t0, gw[0], gq[0]);
+  if (p.t0 + 1 < p.t1) gather(p.t0 + 1, gw[1], gq[1]);
+  double s1m1 = 0.0, s1m2 = 0.0, s2m1 = 0.0, s2m2 = 0.0;   // scalars of steps t-1, t-2
+  auto body = [&](int64_t t, auto phc) {
+    constexpr int PH = decltype(phc)::value, NX = (PH + 2) % 3;
+    const int pb = (int)(t & 1);
+    if (warp == 7 && ((t - p.t0) & 31) == 0 && t + 64 < p.t1) srk_la_fill(p, Ssm, ring, t + 64, lane);
+    cp_async_wait<1>();   // slot of step t + 2 (groups up to t + 3 issued)
+    __syncthreads();
+    if (t + 2 < p.t1) gather(t + 2, gw[NX], gq[NX]);   // on S_t: corrected for steps t, t+1 later
+    const SpRkLaIdx& ix = ring[t & (SRK_RING - 1)];
+    const int sl = (int)(t % SRK_D);
+    const int32_t* R1 = crs[sl][0];
+    const int32_t* R2 = crs[sl][1];
+    double d1 = 0.0, d2 = 0.0;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = tid + e * SRK_T;
+      if (i < ix.k1) d1 = fma(cvs[sl][0][i], gw[PH][e], d1);
+      if (i < ix.k2) d2 = fma(cvs[sl][1][i], gq[PH][e], d2);
+    }
+    d1 = warp_sum(d1);
+    d2 = warp_sum(d2);
+    if (lane == 0) {
+      red[pb][warp][0] = d1;
+      red[pb][warp][1] = d2;
+    }
+    __syncthreads();
+    double D1 = 0.0, D2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < SRK_T / 32; ++w) {
+      D1 += red[pb][w][0];
+      D2 += red[pb][w][1];
+    }
+    // corrections for the steps the gathered state missed (zero Gram values before the chunk start)
+    D1 = fma(s1m1, ix.ga1, D1);
+    D1 = fma(s1m2, ix.ga2, D1);
+    D2 = fma(s1m1, ix.gb1, D2);
+    D2 = fma(s1m2, ix.gb2, D2);
+    D2 = fma(-s2m1, ix.gbb1, D2);
+    D2 = fma(-s2m2, ix.gbb2, D2);
+    const double s1 = (ix.bh1 - D1) * ix.rn1;
+    const double s2 = (D2 + s1 * ix.g21) * ix.rn2;
+    // rows shared by a_t and b_t get one combined update; with <b_t, a_t> = 0 the columns share no
+    // row (but for an exact cancellation, where the two updates of a row stay separate reductions)
+    const bool shared = ix.g21 != 0.0;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = tid + e * SRK_T;
+      if (i < ix.k1) {
+        const int row = R1[i];
+        const double dv = s1 * cvs[sl][0][i];
+        atomicAdd(p.W + row, dv);
+        if (!shared || find_row(R2, ix.k2, row) < 0) atomicAdd(p.Rv + row, dv);
+      }
+      if (i < ix.k2) {
+        const int row = R2[i];
+        const int f = shared ? find_row(R1, ix.k1, row) : -1;
+        const double dv = (f >= 0) ? fma(s1, cvs[sl][0][f], -s2 * cvs[sl][1][i]) : -s2 * cvs[sl][1][i];
+        atomicAdd(p.Rv + row, dv);
+      }
+    }
+    if (tid == 0) atomicAdd(p.Z + ix.j2, s2);
+    s1m2 = s1m1;
+    s1m1 = s1;
+    s2m2 = s2m1;
+    s2m1 = s2;
+    __syncthreads();   // this step's updates precede the next step's gathers; slot sl is free
+    stage(t + SRK_D);
+  };
+  int64_t t = p.t0;
+  for (; t + 2 < p.t1; t += 3) {
+    body(t, std::integral_constant<int, 0>{});
+    body(t + 1, std::integral_constant<int, 1>{});
+    body(t + 2, std::integral_constant<int, 2>{});
+  }
+  if (t < p.t1) body(t, std::integral_constant<int, 0>{});
+  if (t + 1 < p.t1) body(t + 1, std::integral_constant<int, 1>{});
+  cp_async_wait<0>();
+}
+
+__global__ void max_col_kernel(const int64_t* __restrict__ cp, int64_t n, unsigned long long* out) {
+  unsigned long long m = 0;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, (unsigned long long)(cp[j + 1] - cp[j]));
+  m = __reduce_max_sync(0xffffffffu, (unsigned)m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
 int sparse_rk_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_t k, int64_t max_inner,
                     int64_t check_every, double inner_tol, int64_t* steps_out) {
   int rc = build_gram(h);   // <a_j2, a_j1> lookups
@@ -715,6 +937,22 @@ int sparse_rk_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int
     return ILS_ERR_UNSUPPORTED;
   }
   ILS_CU(cudaFuncSetAttribute(sparse_rk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (h.maxcol1 < 0) {
+    unsigned long long* dm = nullptr;
+    unsigned long long hm = 0;
+    ILS_CU(cudaMallocAsync(&dm, sizeof(unsigned long long), st));
+    ILS_CU(cudaMemsetAsync(dm, 0, sizeof(unsigned long long), st));
+    max_col_kernel<<<64, 256, 0, st>>>(h.cp1, h.n, dm);
+    ILS_LAUNCHED("max_col_kernel");
+    ILS_CU(cudaMemcpyAsync(&hm, dm, sizeof(hm), cudaMemcpyDeviceToHost, st));
+    ILS_CU(cudaStreamSynchronize(st));
+    cudaFreeAsync(dm, st);
+    h.maxcol1 = (int64_t)hm;
+  }
+  // look-ahead kernel when every column is staged whole (ILS_SRK_LA=0 keeps the one-step kernel)
+  const char* ela = getenv("ILS_SRK_LA");
+  const bool la = h.maxcol1 <= SRK_LA_K && !(ela && ela[0] == '0');
+  if (la) ILS_CU(cudaFuncSetAttribute(sparse_rk_la_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t prow = h.p, nn = h.n;
   const int64_t* rp = h.rp;
   const int32_t* ci = h.ci;
@@ -731,8 +969,13 @@ int sparse_rk_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int
     const int64_t t1 = (t + ce < max_inner) ? t + ce : max_inner;
     prm.t0 = t;
     prm.t1 = t1;
-    sparse_rk_kernel<<<1, SRK_T, smem, st>>>(prm);
-    ILS_LAUNCHED("sparse_rk_kernel");
+    if (la) {
+      sparse_rk_la_kernel<<<1, SRK_T, smem, st>>>(prm);
+      ILS_LAUNCHED("sparse_rk_la_kernel");
+    } else {
+      sparse_rk_kernel<<<1, SRK_T, smem, st>>>(prm);
+      ILS_LAUNCHED("sparse_rk_kernel");
+    }
     t = t1;
     if (t % ce == 0) {
       double itol = inner_tol;
@@ -1227,9 +1470,11 @@ int sparse_scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed,
     return ILS_ERR_UNSUPPORTED;
   }
   const int64_t chunk_cap = (max_inner < ce) ? max_inner : ce;
-  // dense A1bar rows (large n): the 16-CTA cluster kernel (one or two coordinates per thread)
+  // the 16-CTA cluster kernel over dense A1bar rows (dense input with large n; CSR input too: its
+  // dense A1bar is resident, built for the SP Cholesky and compacted from), up to 8 coordinates of r
+  // per thread in registers (c3: 2.5 us per step against 5.2 for the one-CTA shared-residual kernel)
   const char* ecl = getenv("ILS_SCD_CLUSTER");
-  const bool cl = !weighted && !h.sparse && h.n <= 8 * SCDC_C * SCDC_T && !(ecl && ecl[0] == '0');
+  const bool cl = !weighted && h.G && h.n <= 8 * SCDC_C * SCDC_T && !(ecl && ecl[0] == '0');
   const int Vc = (h.n <= 4 * SCDC_C * SCDC_T) ? 4 : 8;
   const int mask_threads = cl ? SCDC_C * SCDC_T : SSCD_T;
   const size_t need = ((size_t)3 * h.npad + 2 * (size_t)h.num_sms) * sizeof(double) +

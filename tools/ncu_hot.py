@@ -8,9 +8,20 @@ import sys
 def main():
     rep = sys.argv[1]
     top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+    kern = sys.argv[3] if len(sys.argv) > 3 else None
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout.splitlines()
-    rows = list(csv.reader(out[1:]))
+    # one section per kernel: a "Kernel Name" line, then a header row, then SASS rows
+    sections, cur = [], None
+    for line in out:
+        if line.startswith('"Kernel Name"'):
+            cur = [line]
+            sections.append(cur)
+        elif cur is not None:
+            cur.append(line)
+    sec = next((x for x in sections if kern is None or kern in x[0]), sections[0])
+    print(sec[0][:100])
+    rows = list(csv.reader(sec[1:]))
     h = rows[0]
     data = [dict(zip(h, r)) for r in rows[1:] if len(r) == len(h)]
     stall_cols = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
