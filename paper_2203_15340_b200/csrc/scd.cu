@@ -57,7 +57,6 @@ struct ScdParams {
   DevStatus* st;
   int64_t ce;        // scd_warp_kernel: inner check every ce steps inside the launch (0: none)
   double inner_tol;
-  int prefetch;      // scd_chunk_kernel: every warp TMA-copies its candidate row to shared memory
 };
 
 __device__ __forceinline__ void scd_make_key(uint64_t seed, uint32_t k, uint64_t t, int n, int alpha_mode,
@@ -359,9 +358,6 @@ __global__ void __launch_bounds__(SCD_MAXT, 1) scd_chunk_kernel(ScdParams p) {
   double* rNs = reinterpret_cast<double*>(smem_raw);         // [n] 1 / A1bar_jj
   uint64_t* Ss = reinterpret_cast<uint64_t*>(rNs + ((p.n + 1) & ~1));
   ScdKey* ring = reinterpret_cast<ScdKey*>(Ss + ((p.n + 1) & ~1));
-  // candidate rows (prefetch mode): [2][NW][npad], buffer (t - t0) & 1, one mbarrier each
-  double* cand = reinterpret_cast<double*>(ring + SCD_RING);
-  uint64_t* cbar = reinterpret_cast<uint64_t*>(cand + (p.prefetch ? 2 * (int64_t)(blockDim.x >> 5) * p.npad : 0));
   __shared__ double wv[2][SCD_MAXW], wr[2][SCD_MAXW];
   __shared__ int wi[2][SCD_MAXW];
   __shared__ double red[SCD_MAXW];
@@ -398,11 +394,6 @@ __global__ void __launch_bounds__(SCD_MAXT, 1) scd_chunk_kernel(ScdParams p) {
       return;
     }
   }
-  if (p.prefetch && tid == 0) {
-    for (int b = 0; b < 2 * NW; ++b) mbar_init(&cbar[b], 1);
-    fence_mbar_init();
-  }
-  const uint32_t rowbytes = (uint32_t)(p.npad * sizeof(double));
   if (p.weighted && warp == 0) {
     for (int b = 0; b < 2; ++b) {
       const int64_t t = p.t0 + 32 * b + lane;
@@ -467,12 +458,6 @@ __global__ void __launch_bounds__(SCD_MAXT, 1) scd_chunk_kernel(ScdParams p) {
       // winner's lane is its index mod 32 (coordinates tid + v NT, NT a multiple of 32)
       if (bi == INT_MAX) bv = 0.0;
       const int wj = warp_argmax_redux(bv, bi);
-      if (p.prefetch && lane == 0) {   // this warp's candidate row, in flight during the block argmax
-        const int b = (int)((t - p.t0) & 1) * NW + warp;
-        fence_proxy_async();
-        mbar_arrive_expect_tx(&cbar[b], rowbytes);
-        bulk_g2s(cand + (int64_t)b * p.npad, p.G + (int64_t)(wj == INT_MAX ? 0 : wj) * p.npad, rowbytes, &cbar[b]);
-      }
       if (wj == INT_MAX ? lane == 0 : bi == wj) {   // the winning lane (or lane 0: no candidate) records it
         wv[pb][warp] = bv;
         wi[pb][warp] = wj;
@@ -486,33 +471,15 @@ __global__ void __launch_bounds__(SCD_MAXT, 1) scd_chunk_kernel(ScdParams p) {
       rj = wr[pb][(j % NT) >> 5];   // the winning warp's entry
     }
     const double sc = rj * rNs[j];
-    if (p.prefetch) {   // row j from the winning warp's prefetched copy
-      const int b = (int)((t - p.t0) & 1) * NW + ((j % NT) >> 5);
-      mbar_wait(&cbar[b], (uint32_t)(((t - p.t0) >> 1) & 1));
-      const double* grow = cand + (int64_t)b * p.npad;
+    const double* grow = p.G + (int64_t)j * p.npad;
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const int s = tid + v * NT;
-        if (s < n) {
-          r[v] = fma(-sc, grow[s], r[v]);
-          if (s == j) beta[v] += sc;
-        }
-      }
-    } else {
-      const double* grow = p.G + (int64_t)j * p.npad;
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const int s = tid + v * NT;
-        if (s < n) {
-          r[v] = fma(-sc, __ldg(grow + s), r[v]);
-          if (s == j) beta[v] += sc;
-        }
+    for (int v = 0; v < V; ++v) {
+      const int s = tid + v * NT;
+      if (s < n) {
+        r[v] = fma(-sc, __ldg(grow + s), r[v]);
+        if (s == j) beta[v] += sc;
       }
     }
-  }
-  if (p.prefetch && lane == 0) {   // this warp's last two copies land before the CTA exits
-    for (int64_t t = (p.t1 - 2 > p.t0 ? p.t1 - 2 : p.t0); t < p.t1; ++t)
-      mbar_wait(&cbar[(int)((t - p.t0) & 1) * NW + warp], (uint32_t)(((t - p.t0) >> 1) & 1));
   }
 #pragma unroll
   for (int v = 0; v < V; ++v) {
@@ -656,15 +623,7 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
   p.weighted = weighted;
   p.all_members = (!weighted && (alpha_mode & 0xF) == ILS_ALPHA_FIXED && alpha_k >= h.n) ? 1 : 0;
   p.st = h.dstat;
-  size_t smem = 2 * (size_t)((h.n + 1) & ~1) * 8 + SCD_RING * sizeof(ScdKey);
-  {   // candidate-row prefetch (chunk kernel, argmax modes): 2 x NW rows of A1bar + mbarriers
-    const size_t extra = (size_t)2 * (nt / 32) * h.npad * 8 + (size_t)2 * (nt / 32) * 8;
-    // experiment (opt-in, ILS_SCD_PREFETCH=1): measured slower at c1 (157 vs 135 ms per solve: the
-    // eight 8 KB TMA copies per step add more latency than the earlier issue hides)
-    const char* e = getenv("ILS_SCD_PREFETCH");
-    p.prefetch = (!warpk && !weighted && smem + extra <= 200 * 1024 && (e && e[0] == '1')) ? 1 : 0;
-    if (p.prefetch) smem += extra;
-  }
+  const size_t smem = 2 * (size_t)((h.n + 1) & ~1) * 8 + SCD_RING * sizeof(ScdKey);
   void* kern = nullptr;
   if (warpk) {
     switch (V) {

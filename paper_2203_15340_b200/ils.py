@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libils.so")
+LIB_PATH = os.environ.get("ILS_LIB_PATH") or os.path.join(_HERE, "lib", "libils.so")   # override: A/B builds
 
 ILS_OK, ILS_NOT_CONVERGED = 0, 1
 ILS_ERR_ARG, ILS_ERR_SHAPE, ILS_ERR_ZERO_COLUMN, ILS_ERR_NOT_SPD = -1, -2, -3, -4
