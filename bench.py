@@ -44,7 +44,8 @@ FALLBACK_BF16_TFLOPS = 1590.0
 # fp64 DMMA: no measured peak on this pool; B200 nominal FP64 tensor 40 TFLOP/s vs 2250 bf16
 # dense -> measured bf16 x 40/2250 (the guide's rule for another dtype's peak).
 FP64_OVER_BF16 = 40.0 / 2250.0
-KINDS = {0: "sp_persistent_kernel (K1 stream + P apply)", 1: "rk_rgs_kernel (K2a; 16-CTA look-ahead rk_rgs_la_kernel at c1)",
+KINDS = {0: "sp_persistent_kernel (K1 stream + P apply)",
+         1: "rk_rgs_la_kernel (K2a: 16-CTA look-ahead SP-RK-RGS, one launch per inner solve with its checks, at c1)",
          2: "scd_kernel (K2b)", 3: "setup: gemm_dmma_kernel + potf2_trtri_kernel (K3)"}
 
 
@@ -321,8 +322,10 @@ def roofline(steps, peak_hbm, peak_bf16, traffic_map, cfg):
         d = {"bound": "hbm", "unit": "GB/s", "peak_note": "measured hbm_gbs (MEASURED_PEAKS.json)"}
     if c == 1:
         d["limiter"] = ("latency: one 16-CTA DSMEM all-to-all per 4 inner steps (~1000-1300 cycles floor, "
-                        "tools/mb/dsmem_bench2.cu), overlapped with the previous block's update by the look-ahead "
-                        "kernel; the columns are L2-resident at c1 (DESIGN.md §7)")
+                        "tools/mb/dsmem_bench2.cu), two blocks deep in flight; per step the compute warps' "
+                        "products -> recurrence -> axpy chain; the columns are L2-resident at c1 (DESIGN.md §7). "
+                        "Per launch = one inner solve: algorithmic bytes 16p per step + 8n^2 per in-kernel check, "
+                        "time = CUDA events around the launch (kernel time, no host gaps)")
     elif c == 2:
         d["limiter"] = "latency: one dependent A1bar row load plus a CTA argmax per inner step (DESIGN.md §7)"
     tr = traffic_map.get(f"{cfg}:{c}") if traffic_map else None
