@@ -210,9 +210,72 @@ __global__ void __launch_bounds__(256) scd_masks_exact_kernel(uint64_t seed, uin
   }
 }
 
+// The same masks from the forward direction: tau_u = { pi(i) : i < alpha_u } (include/ils.h), pi(i)
+// by cycle-walking the 8-round encryption (round r: (L, R) -> (R, L ^ F(R, K_r)), the inverse of
+// feistel_decrypt_once's round). Three savings over scd_masks_kernel, which decrypts all n
+// coordinates: (1) only alpha_u walks per step (n/2 on average for uniform alpha); (2) the round
+// function F(v, K_r) = mix32(v ^ K_r) & (2^h - 1) is tabulated per step in shared memory (8 * 2^h
+// 16-bit entries, h <= 11), so a round is one table load and an xor; (3) no divergent walks: a thread
+// whose value lands in [n) records it and starts its next i at once, so every loop trip is one
+// encryption in every lane (the old kernel's warps waited for their longest walk: at n = 20000,
+// half-width h = 8, a walk takes 2^16 / n = 3.3 decryptions on average and ~10 for the slowest of 32).
+// Member bits are collected in shared memory (word s % NT, bit s / NT) and written once.
+constexpr int kMaskFwdMaxH = 11;
+__global__ void __launch_bounds__(256) scd_masks_fwd_kernel(uint64_t seed, uint32_t k, int64_t t0, int64_t t1, int n,
+                                                            int alpha_mode, int alpha_k, int NT, int V,
+                                                            uint32_t* __restrict__ masks) {
+  extern __shared__ uint32_t mwords[];   // [NT] member bits, then [8 << h] uint16 round tables
+  __shared__ ScdKey e;
+  const int64_t u = t0 + blockIdx.x;
+  if (u >= t1) return;
+  if (threadIdx.x == 0) scd_make_key(seed, k, (uint64_t)u, n, alpha_mode, alpha_k, 0, nullptr, e);
+  const uint32_t h = feistel_half_bits((uint32_t)n), msk = (1u << h) - 1u;
+  uint16_t* T = reinterpret_cast<uint16_t*>(mwords + NT);
+  for (int th = threadIdx.x; th < NT; th += blockDim.x) mwords[th] = 0u;
+  __syncthreads();
+  for (uint32_t x = threadIdx.x; x < (8u << h); x += blockDim.x)
+    T[x] = (uint16_t)(mix32((x & msk) ^ e.key[x >> h]) & msk);
+  __syncthreads();
+  const uint32_t alpha = e.alpha, nu = (uint32_t)n, nt = (uint32_t)NT;
+  if (alpha >= nu) {   // tau_u = [n]
+    for (uint32_t s = threadIdx.x; s < nu; s += blockDim.x) atomicOr(&mwords[s % nt], 1u << (s / nt));
+  } else {
+    uint32_t i = threadIdx.x, y = threadIdx.x;
+    while (i < alpha) {
+      uint32_t L = y >> h, R = y & msk;
+#pragma unroll
+      for (uint32_t r = 0; r < (uint32_t)kFeistelRounds; ++r) {
+        const uint32_t nl = R;
+        R = L ^ T[(r << h) | R];
+        L = nl;
+      }
+      y = (L << h) | R;
+      if (y < nu) {   // pi(i) = y
+        atomicOr(&mwords[y % nt], 1u << (y / nt));
+        i += blockDim.x;
+        y = i;
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t* out = masks + (int64_t)blockIdx.x * NT;
+  for (int th = threadIdx.x; th < NT; th += blockDim.x) out[th] = mwords[th];
+  (void)V;
+}
+
 // membership masks of steps [t0, t1) for either subset construction (one CTA per step)
 static int launch_masks(cudaStream_t st, uint64_t seed, uint32_t k, int64_t t0, int64_t t1, int n, int alpha_mode,
                          int alpha_k, int NT, int V, uint32_t* masks) {
+  const uint32_t hb = feistel_half_bits((uint32_t)n);
+  const char* efw = getenv("ILS_MASKS_FWD");   // experiment override: 0 = the per-coordinate decryption kernel
+  if (!(alpha_mode & ILS_SUBSET_EXACT) && hb <= (uint32_t)kMaskFwdMaxH && !(efw && efw[0] == '0')) {
+    const size_t smem = (size_t)NT * sizeof(uint32_t) + ((size_t)8 << hb) * sizeof(uint16_t);
+    ILS_CU(cudaFuncSetAttribute(scd_masks_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    scd_masks_fwd_kernel<<<(unsigned)(t1 - t0), 256, smem, st>>>(seed, k, t0, t1, n, alpha_mode, alpha_k, NT, V,
+                                                                  masks);
+    ILS_LAUNCHED("scd_masks_fwd_kernel");
+    return ILS_OK;
+  }
   if (alpha_mode & ILS_SUBSET_EXACT) {
     const size_t smem = ((size_t)n + 258) * sizeof(uint32_t);
     cudaFuncSetAttribute(scd_masks_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -662,3 +662,37 @@ def test_scd_exact_subsets_fixed_horizon(shape, force_large, monkeypatch):
     assert list(inner) == list(ref.inner_hist)
     for k in range(K):
         assert _par(hist[k], ref.x_hist[k]) <= 1e-9, k
+
+
+@pytest.mark.parametrize("shape,force_large", [((40, 5, 1), False), ((60, 10, 3), False), ((200, 100, 50), False),
+                                               ((1400, 300, 1000), False), ((2000, 200, 1500), False),
+                                               ((260, 60, 130), True), ((6000, 300, 5000), True)])
+@pytest.mark.parametrize("mode", [(0, 1), (1, 7), (1, 10 ** 6)])
+def test_scd_masks_forward_kernel_matches_decrypt_kernel(shape, force_large, mode, monkeypatch):
+    """The membership masks of Alg. 5 step 8 built forward (tau_t = {pi(i) : i <
+    alpha_t}, tabulated rounds, scd_masks_fwd_kernel) and by decrypting every coordinate
+    (pi^{-1}(s) < alpha_t, scd_masks_kernel) give bit-identical SP-SCD iterates and inner counts
+    through the one-warp, one-CTA (V = 4, 8) and cluster kernels; one of them against the oracle."""
+    monkeypatch.setenv("ILS_FORCE_LARGE", "1" if force_large else "0")
+    p, q, n = shape
+    pr = make_dense(p, q, n, 0.3, noise=0.05, seed=31)
+    amode, ak = mode
+    K, T, ce = 2, 300, 100
+    runs = []
+    for fwd in ("0", "1"):
+        monkeypatch.setenv("ILS_MASKS_FWD", fwd)
+        hist = np.zeros((K, n))
+        inner = np.zeros(K, dtype=np.int64)
+        x = np.zeros(n)
+        with H(pr) as hh:
+            o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, seed=5, max_inner=T, check_every=ce, inner_tol=0.0,
+                                     alpha_mode=amode, alpha_k=min(ak, 2 ** 31 - 1), x_hist=hist.ctypes.data,
+                                     inner_hist=inner.ctypes.data)
+            ils.ils_rgs_solve(hh.h, None, x, 0.0, K, o)
+        runs.append((hist, inner))
+    assert np.array_equal(runs[0][0], runs[1][0]) and list(runs[0][1]) == list(runs[1][1])
+    if n <= 1000:
+        ref = O.sp_scd_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE, seed=5, max_inner=T,
+                             check_every=ce, inner_tol=0.0, alpha_mode=amode, alpha_fixed=ak)
+        for k in range(K):
+            assert _par(runs[1][0][k], ref.x_hist[k]) <= 1e-9, k
