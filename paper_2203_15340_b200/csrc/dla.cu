@@ -11,6 +11,7 @@
 // All dimensions are multiples of 64 (M, N) and 32 (K): the handle pads every dense
 // operand with zeros (identity on the padded diagonal), so there are no tails.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -391,6 +392,212 @@ __global__ void __launch_bounds__(256) potf2_trtri_kernel(double* __restrict__ L
   if (tid == 0 && bad_s) atomicExch(err, 1);
 }
 
+// ---------------------------------------------------------------- 64x64 base, blocked (default)
+// The same leaf (L = chol(A), Z = L^{-1} of the 64x64 diagonal block at (s0, s0)) as four 16-column
+// panels, so that the sequential part is a 16x16 factorisation done by one warp in registers and
+// everything else is small dense products on the fp64 tensor cores (DMMA m8n8k4, 8x8 output tiles,
+// K = 16) over the whole CTA. Z is built in place of W, the right-hand side of L Z = I (W = I at the
+// start), by the same right-looking sweep. Per panel P:
+//   (a) warp 0, lane l holding row l of A_PP and column l of W_PP = I. Every lane also carries the
+//       16 diagonal entries (updated redundantly with the same fma as their owners, so bitwise equal)
+//       and the current column, broadcast once through shared memory right after its owners updated
+//       it; column k is then: 1 / sqrt(a_kk) by rsqrt (as potf2_trtri_kernel), L_jk = a_jk * rsqrt
+//       for every j locally, the diagonal update, the own row's rank-1 update and Z_PP's row k -- the
+//       step chain is rsqrt -> mul -> fma, with the broadcast of column k + 1 beside it;
+//   (b) L_iP = A_iP Z_PP^T for the rows below and Z_P,<P = Z_PP W_P,<P (12 DMMA tiles);
+//   (c) A_ij -= L_iP L_jP^T (lower tiles) and W_i,<=P -= L_iP Z_P,<=P for the rows below (DMMA).
+// 4 barriers per panel (65 in the column-at-a-time sweep).
+// Row stride of the leaf's shared-memory tiles: 68 = 4 (mod 16) doubles, so the DMMA fragment loads
+// (row fr, column fk of an 8x4 slice, either orientation) hit 16 distinct 8-byte banks per half-warp.
+constexpr int LEAF_LD = 68;
+constexpr int LEAF_SMEM = 2 * 64 * LEAF_LD * (int)sizeof(double);
+
+__device__ __forceinline__ void leaf_mma_k16(double& c0, double& c1, const double* abase, int astr, int acol,
+                                             const double* bbase, int bstr_n, int bstr_k, int lane) {
+  const int fr = lane >> 2, fk = lane & 3;
+#pragma unroll
+  for (int kk = 0; kk < 16; kk += 4) {
+    const double av = abase[fr * astr + acol + kk + fk];
+    const double bv = bbase[fr * bstr_n + (kk + fk) * bstr_k];
+    dmma884(c0, c1, av, bv);
+  }
+}
+
+__global__ void __launch_bounds__(256) potrf_trtri64_kernel(double* __restrict__ L, double* __restrict__ Z,
+                                                            int64_t ld, int64_t s0, int32_t* err) {
+  extern __shared__ __align__(16) double leaf_smem[];
+  double (*a)[LEAF_LD] = reinterpret_cast<double (*)[LEAF_LD]>(leaf_smem);                  // A -> L (lower)
+  double (*z)[LEAF_LD] = reinterpret_cast<double (*)[LEAF_LD]>(leaf_smem + 64 * LEAF_LD);   // W -> Z (lower)
+  __shared__ __align__(16) double colbuf[2][16];
+  __shared__ int bad_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int fr = lane >> 2, fk = lane & 3;
+  double* blk = L + s0 * ld + s0;
+  {
+    double v[16];   // all 16 loads in flight before the first shared-memory store
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int e = tid + 256 * q, i = e >> 6, j = e & 63;
+      v[q] = (j <= i) ? __ldcg(blk + i * ld + j) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int e = tid + 256 * q, i = e >> 6, j = e & 63;
+      a[i][j] = v[q];
+      z[i][j] = (i == j) ? 1.0 : 0.0;
+    }
+  }
+  if (tid == 0) bad_s = 0;
+  __syncthreads();
+  for (int P = 0; P < 64; P += 16) {
+    // (a) L_PP, Z_PP (warp 0): lane l < 16 holds row l of A_PP, lane 16 + l column l of W_PP = I;
+    // both are updated by the same two operations per column (scale by 1 / L_kk, then x_j -= x_k L_jk)
+    if (warp == 0) {
+      const int l = lane & 15;
+      const bool rowlane = lane < 16;
+      double x[16], bk[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        x[c] = rowlane ? a[P + l][P + c] : ((c == l) ? 1.0 : 0.0);
+        bk[c] = a[P + c][P];   // column 0 of A_PP
+      }
+      bool bad = false;
+      double dk = bk[0];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        bad = bad || !(dk > 0.0 && isfinite(dk));   // off the step chain: a breakdown only flags
+        const double rs = rsqrt(dk);
+        x[k] *= rs;   // row lanes: L_lk (lane k: sqrt(a_kk)); column lanes: Z_kl final
+#pragma unroll
+        for (int j = k + 1; j < 16; ++j) x[j] = fma(-x[k], bk[j] * rs, x[j]);   // L_jk = a_jk / sqrt(a_kk)
+        if (k < 15) {   // the updated column k + 1 to every lane: its diagonal by a shuffle (the step
+                        // chain), the rest through shared memory
+          dk = __shfl_sync(0xffffffffu, x[k + 1], k + 1);
+          if (rowlane) colbuf[(k + 1) & 1][l] = x[k + 1];
+          __syncwarp();
+#pragma unroll
+          for (int j = k + 2; j < 16; ++j) bk[j] = colbuf[(k + 1) & 1][j];
+        }
+      }
+      if (rowlane) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) a[P + l][P + c] = (c <= l) ? x[c] : 0.0;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) z[P + i][P + l] = (i >= l) ? x[i] : 0.0;
+      }
+      if (lane == 0 && bad) bad_s = 1;
+    }
+    __syncthreads();
+    // (b) 12 tiles: L_iP = A_iP Z_PP^T (rows below, two column tiles each), then Z_P,<P = Z_PP W_P,<P
+    const int R = 48 - P;
+    double o0[2], o1[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int t = warp + 8 * q;
+      o0[q] = o1[q] = 0.0;
+      if (t < R / 4) {
+        const int i0 = P + 16 + 8 * (t >> 1), c0 = 8 * (t & 1);
+        leaf_mma_k16(o0[q], o1[q], &a[i0][0], LEAF_LD, P, &z[P + c0][P], LEAF_LD, 1, lane);
+      } else if (t < 12) {
+        const int u = t - R / 4, r0 = 8 * (u & 1), c0 = 8 * (u >> 1);
+        leaf_mma_k16(o0[q], o1[q], &z[P + r0][0], LEAF_LD, P, &z[P][c0], 1, LEAF_LD, lane);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int t = warp + 8 * q;
+      if (t < R / 4) {
+        const int i0 = P + 16 + 8 * (t >> 1), c0 = 8 * (t & 1);
+        a[i0 + fr][P + c0 + 2 * fk] = o0[q];
+        a[i0 + fr][P + c0 + 2 * fk + 1] = o1[q];
+      } else if (t < 12) {
+        const int u = t - R / 4, r0 = 8 * (u & 1), c0 = 8 * (u >> 1);
+        z[P + r0 + fr][c0 + 2 * fk] = o0[q];
+        z[P + r0 + fr][c0 + 2 * fk + 1] = o1[q];
+      }
+    }
+    __syncthreads();
+    if (R == 0) break;
+    // (c) lower 8x8 tiles of A below the panel, then W tiles (rows below, columns <= P + 15); a warp
+    // takes two tiles per pass and splits K in two, so four independent DMMA chains of two are in flight
+    {
+      const int nb = R >> 3, nA = nb * (nb + 1) / 2, nW = nb * ((P + 16) >> 3), nT = nA + nW;
+      for (int t0 = warp; t0 < nT; t0 += 16) {
+        const double* ab[2];
+        const double* bb[2];
+        int bn[2], bkst[2], i0[2], j0[2];
+        bool isA[2], live[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int t = t0 + 8 * h;
+          live[h] = t < nT;
+          isA[h] = t < nA;
+          if (isA[h]) {
+            int ti = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);   // exact for t < 21
+            ti += ((ti + 1) * (ti + 2) / 2 <= t) ? 1 : 0;
+            i0[h] = P + 16 + 8 * ti;
+            j0[h] = P + 16 + 8 * (t - ti * (ti + 1) / 2);
+            bb[h] = &a[j0[h]][P];
+            bn[h] = LEAF_LD;
+            bkst[h] = 1;
+          } else {
+            const int w = live[h] ? t - nA : 0, nc = (P + 16) >> 3, ti = w / nc;
+            i0[h] = P + 16 + 8 * ti;
+            j0[h] = 8 * (w - ti * nc);
+            bb[h] = &z[P][j0[h]];
+            bn[h] = 1;
+            bkst[h] = LEAF_LD;
+          }
+          ab[h] = &a[i0[h]][P];
+        }
+        // all 16 fragment loads first (a dead second tile reads the first one's operands), then the DMMAs
+        double af[2][4], bf[2][4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int hh = live[h] ? h : 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            af[h][q] = ab[hh][fr * LEAF_LD + 4 * q + fk];
+            bf[h][q] = bb[hh][fr * bn[hh] + (4 * q + fk) * bkst[hh]];
+          }
+        }
+        double c[2][2][2];   // [tile][K half][pair]
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) c[h][e][0] = c[h][e][1] = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) dmma884(c[h][q & 1][0], c[h][q & 1][1], af[h][q], bf[h][q]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (!live[h]) continue;
+          const double v0 = c[h][0][0] + c[h][1][0], v1 = c[h][0][1] + c[h][1][1];
+          const int i = i0[h] + fr, j = j0[h] + 2 * fk;
+          if (isA[h]) {
+            if (j <= i) a[i][j] -= v0;
+            if (j + 1 <= i) a[i][j + 1] -= v1;
+          } else {
+            z[i][j] -= v0;
+            z[i][j + 1] -= v1;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  double* zb = Z + s0 * ld + s0;
+  for (int e = tid; e < 64 * 64; e += 256) {
+    const int i = e >> 6, j = e & 63;
+    blk[i * ld + j] = (j <= i) ? a[i][j] : 0.0;
+    zb[i * ld + j] = (j <= i) ? z[i][j] : 0.0;
+  }
+  if (tid == 0 && bad_s) atomicExch(err, 1);
+}
+
 // Recursive Cholesky + inverse on blocks [s, e) (units of 64).
 // need_z = false (right spine of a top-level call with full_z = false): the caller never uses this
 // block's inverse as a whole, so Z21 = -Z22 L21 Z11 (two GEMMs) is skipped here; zc_apply_spine
@@ -399,9 +606,19 @@ static int chol_rec(Handle& h, double* L, double* Z, int64_t ld, int64_t s, int6
                     bool need_z) {
   if (e - s == 1) {
     const int smem = 2 * 64 * 65 * (int)sizeof(double);
-    ILS_CU(cudaFuncSetAttribute(potf2_trtri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    potf2_trtri_kernel<<<1, 256, smem, h.stream>>>(L, Z, ld, s * 64, &h.dstat->flag_err);
-    ILS_LAUNCHED("potf2_trtri_kernel");
+    static const bool old_leaf = [] {   // experiment override: 1 = the column-at-a-time leaf
+      const char* e = getenv("ILS_LEAF_OLD");
+      return e && e[0] == '1';
+    }();
+    if (old_leaf) {
+      ILS_CU(cudaFuncSetAttribute(potf2_trtri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      potf2_trtri_kernel<<<1, 256, smem, h.stream>>>(L, Z, ld, s * 64, &h.dstat->flag_err);
+      ILS_LAUNCHED("potf2_trtri_kernel");
+    } else {
+      ILS_CU(cudaFuncSetAttribute(potrf_trtri64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, LEAF_SMEM));
+      potrf_trtri64_kernel<<<1, 256, LEAF_SMEM, h.stream>>>(L, Z, ld, s * 64, &h.dstat->flag_err);
+      ILS_LAUNCHED("potrf_trtri64_kernel");
+    }
     return ILS_OK;
   }
   const int64_t hmid = s + (e - s) / 2;

@@ -51,18 +51,26 @@ __global__ void lat(long long* out, int iters, double seed) {
   for (int i = 0; i < iters; ++i) d = d + 1e-9;
   t1 = clock64();
   if (tid == 0) out[6] = (t1 - t0) / iters;
-  if (a + r + s + d + v + p == 12345.678) out[7] = 1;
+  // 8: dependent DMMA m8n8k4 (accumulator chain)
+  double c0 = 0.0, c1 = 0.0, fa = seed, fb = 1.0;
+  t0 = clock64();
+  for (int i = 0; i < iters; ++i)
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1) : "d"(fa), "d"(fb));
+  t1 = clock64();
+  if (tid == 0) out[7] = (t1 - t0) / iters;
+  if (a + r + s + d + v + p + c0 + c1 == 12345.678) out[8] = 1;
 }
 
 int main() {
   long long* d;
-  cudaMalloc(&d, 8 * sizeof(long long));
+  cudaMalloc(&d, 9 * sizeof(long long));
   for (int nt : {32, 256}) {
     lat<<<1, nt>>>(d, 1000, 0.5);
-    long long h[8];
+    long long h[9];
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
-    printf("threads %d: LDS32 chase %lld, LDS64 dep %lld, DFMA %lld, rsqrt(f64) %lld, SHFL f64 %lld, syncthreads %lld, DADD %lld cycles\n",
-           nt, h[0], h[1], h[2], h[3], h[4], h[5], h[6]);
+    printf("threads %d: LDS32 chase %lld, LDS64 dep %lld, DFMA %lld, rsqrt(f64) %lld, SHFL f64 %lld, syncthreads %lld, DADD %lld, DMMA884 %lld cycles\n",
+           nt, h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
   }
   return 0;
 }
