@@ -606,10 +606,8 @@ static int chol_rec(Handle& h, double* L, double* Z, int64_t ld, int64_t s, int6
                     bool need_z) {
   if (e - s == 1) {
     const int smem = 2 * 64 * 65 * (int)sizeof(double);
-    static const bool old_leaf = [] {   // experiment override: 1 = the column-at-a-time leaf
-      const char* e = getenv("ILS_LEAF_OLD");
-      return e && e[0] == '1';
-    }();
+    const char* ev = getenv("ILS_LEAF_OLD");   // experiment override: 1 = the column-at-a-time leaf
+    const bool old_leaf = ev && ev[0] == '1';
     if (old_leaf) {
       ILS_CU(cudaFuncSetAttribute(potf2_trtri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       potf2_trtri_kernel<<<1, 256, smem, h.stream>>>(L, Z, ld, s * 64, &h.dstat->flag_err);

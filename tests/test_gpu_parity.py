@@ -696,3 +696,22 @@ def test_scd_masks_forward_kernel_matches_decrypt_kernel(shape, force_large, mod
                              check_every=ce, inner_tol=0.0, alpha_mode=amode, alpha_fixed=ak)
         for k in range(K):
             assert _par(runs[1][0][k], ref.x_hist[k]) <= 1e-9, k
+
+
+@pytest.mark.parametrize("shape", [(2600, 300, 2100), (1400, 200, 700)])
+def test_sp_leaf_variants_match_oracle(shape, monkeypatch):
+    """SP (Alg. 1; its setup Gram -> Cholesky -> inverse -> P, step 2) with the blocked
+    64x64 leaf (default) and with the column-at-a-time leaf (ILS_LEAF_OLD=1): both within 1e-9 of the
+    oracle's iterates."""
+    p, q, n = shape
+    pr = make_dense(p, q, n, 0.3, noise=0.05, seed=41)
+    K = 3
+    ref = O.sp_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE)
+    for old in ("0", "1"):
+        monkeypatch.setenv("ILS_LEAF_OLD", old)
+        hist = np.zeros((K, n))
+        x = np.zeros(n)
+        with H(pr) as hh:
+            ils.ils_sp_solve(hh.h, None, x, 0.0, K, ils.ils_default_opts(stop=ils.ILS_STOP_NONE, x_hist=hist.ctypes.data))
+        for k in range(K):
+            assert _par(hist[k], ref.x_hist[k]) <= 1e-9, (old, k)
