@@ -43,11 +43,13 @@ struct BKey {
 
 // batched SP-SCD window entry: alpha_t and the Feistel round tables T_r[v] = F(v, K_r) of step t,
 // packed 4 bits per entry (n <= 32: h <= 3, 8 entries per round)
-struct BKeyT {
+struct __align__(16) BKeyT {
+  uint32_t tb[2 * kFeistelRounds];   // round r: T_r[v] in byte v of (tb[2r], tb[2r+1]) (PRMT lookup)
   uint32_t alpha;
   int32_t j;
-  uint32_t word[kFeistelRounds];
+  uint32_t pad_[2];
 };
+static_assert(sizeof(BKeyT) % 16 == 0, "BKeyT rows are read as uint4");
 
 __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
@@ -617,13 +619,19 @@ __global__ void __launch_bounds__(32) batched_scd_kernel(BatchParams P) {
                                                         : (uint32_t)(P.alpha_k < n ? P.alpha_k : n);
             e.j = -1;
             const uint32_t key[kFeistelRounds] = {a.y, a.z, a.w, bb.x, bb.y, bb.z, bb.w, cc.x};
-            // round tables of this lane's step: T_r[v] = mix32(v ^ K_r) & (2^hb - 1) for v < 2^hb,
-            // packed 4 bits per entry (hb <= 3 for n <= 32)
+            // round tables of this lane's step: T_r[v] = mix32(v ^ K_r) & (2^hb - 1) for v < 2^hb
+            // (hb <= 3 for n <= 32), one byte per entry in two words, so that a decryption round is one
+            // byte permute (PRMT) and one three-input logic op
 #pragma unroll
             for (int r = 0; r < kFeistelRounds; ++r) {
-              uint32_t wd = 0;
-              for (uint32_t v = 0; v <= msk; ++v) wd |= (mix32(v ^ key[r]) & msk) << (4 * v);
-              e.word[r] = wd;
+              uint32_t w0 = 0, w1 = 0;
+#pragma unroll
+              for (uint32_t v = 0; v < 4; ++v) {
+                if (v <= msk) w0 |= (mix32(v ^ key[r]) & msk) << (8 * v);
+                if (v + 4 <= msk) w1 |= (mix32((v + 4) ^ key[r]) & msk) << (8 * v);
+              }
+              e.tb[2 * r] = w0;
+              e.tb[2 * r + 1] = w1;
             }
           }
           __syncwarp();
@@ -634,16 +642,25 @@ __global__ void __launch_bounds__(32) batched_scd_kernel(BatchParams P) {
         if (P.weighted) {
           j = keys[kk].j;
         } else {
-          uint32_t wd[kFeistelRounds];
+          uint32_t tb[2 * kFeistelRounds];
+          {
+            const uint4* kq = reinterpret_cast<const uint4*>(keys[kk].tb);
 #pragma unroll
-          for (int qq = 0; qq < kFeistelRounds; ++qq) wd[qq] = keys[kk].word[qq];
+            for (int qq = 0; qq < kFeistelRounds / 2; ++qq) {
+              const uint4 w = kq[qq];
+              tb[4 * qq] = w.x;
+              tb[4 * qq + 1] = w.y;
+              tb[4 * qq + 2] = w.z;
+              tb[4 * qq + 3] = w.w;
+            }
+          }
           const uint32_t alpha = keys[kk].alpha;
-          // one round-trip decryption of y (feistel_decrypt_once) from the packed round tables
+          // one round-trip decryption of y (feistel_decrypt_once) from the byte round tables
           auto dec = [&](uint32_t y) {
             uint32_t L = y >> hb, R = y & msk;
 #pragma unroll
             for (int r = kFeistelRounds - 1; r >= 0; --r) {
-              const uint32_t Lp = R ^ ((wd[r] >> (4 * L)) & msk);
+              const uint32_t Lp = (R ^ __byte_perm(tb[2 * r], tb[2 * r + 1], L)) & msk;
               R = L;
               L = Lp;
             }
@@ -658,6 +675,31 @@ __global__ void __launch_bounds__(32) batched_scd_kernel(BatchParams P) {
           const uint32_t d1 = (n == 1 || allm || dom <= 32) ? 0u : dec((uint32_t)lane + 32u);
           uint32_t y = d0;
           if (n > 1 && !allm) {
+            // walk ends by pointer jumping (T(v) <- T(T(v)) while T(v) >= n, all v at once): three
+            // uniform rounds resolve every walk of up to 8 hops; the rare longer ones finish below
+            const uint32_t nu = (uint32_t)n;
+            if (n == 32) {   // only the values 32..63 (slot 1, lane v - 32) are ever walked through
+              uint32_t T1 = d1;
+#pragma unroll
+              for (int rnd = 0; rnd < 3; ++rnd) {
+                const uint32_t f = __shfl_sync(0xffffffffu, T1, (int)(T1 & 31));
+                T1 = (T1 >= 32u) ? f : T1;
+              }
+              const uint32_t f = __shfl_sync(0xffffffffu, T1, (int)(d0 & 31));
+              y = (d0 >= 32u) ? f : d0;
+            } else {
+              uint32_t T0 = d0, T1 = d1;
+#pragma unroll
+              for (int rnd = 0; rnd < 3; ++rnd) {
+                const uint32_t a0 = __shfl_sync(0xffffffffu, T0, (int)(T0 & 31));
+                const uint32_t b0 = __shfl_sync(0xffffffffu, T1, (int)(T0 & 31));
+                const uint32_t a1 = __shfl_sync(0xffffffffu, T0, (int)(T1 & 31));
+                const uint32_t b1 = __shfl_sync(0xffffffffu, T1, (int)(T1 & 31));
+                T0 = (T0 >= nu) ? ((T0 < 32u) ? a0 : b0) : T0;
+                T1 = (T1 >= nu) ? ((T1 < 32u) ? a1 : b1) : T1;
+              }
+              y = T0;
+            }
             while (__any_sync(0xffffffffu, act && y >= (uint32_t)n)) {
               const uint32_t t0 = __shfl_sync(0xffffffffu, d0, (int)(y & 31)), t1 = __shfl_sync(0xffffffffu, d1, (int)(y & 31));
               if (act && y >= (uint32_t)n) y = (y < 32) ? t0 : t1;
