@@ -557,18 +557,21 @@ __global__ void __launch_bounds__(32) batched_rk_kernel(BatchParams P) {
 // instances share an SM. Per step: the 12 Feistel round keys and alpha_t come from a 32-step key
 // window in shared memory; lane s tests pi^{-1}(s) < alpha_t; warp argmax of r_s^2 (ties to the
 // smallest s); r -= (r_j / A1bar_jj) A1bar_(j) from shared memory.
+// Template flags: WT = weighted SP-RCD, N32 = n is 32 (every lane owns a coordinate and the Feistel
+// domain is [0, 64): the generic n checks fold away).
+template <bool WT, bool N32>
 __global__ void __launch_bounds__(32) batched_scd_kernel(BatchParams P) {
   extern __shared__ __align__(16) double sm[];
   const int lane = threadIdx.x;
   const int64_t inst = blockIdx.x;
-  const int p = P.p, q = P.q, n = P.n, m = p + q;
+  const int p = P.p, q = P.q, n = N32 ? 32 : P.n, m = p + q;
   const double* A = P.A + inst * (int64_t)m * n;
   const double* b = P.b + inst * (int64_t)m;
   const uint64_t seed = P.seed + (uint64_t)inst;
   double* G = sm;                                       // [32][32] A1bar (row j at G + 32 j)
   uint64_t* S = reinterpret_cast<uint64_t*>(G + 32 * 32);   // [32]
   BKeyT* keys = reinterpret_cast<BKeyT*>(S + 32);             // [32]
-  const bool act = lane < n;
+  const bool act = N32 || lane < n;
   // column j of A1 in registers one row at a time: Gram by rank-1 updates over the p rows
   double g[32];
 #pragma unroll
@@ -583,12 +586,12 @@ __global__ void __launch_bounds__(32) batched_scd_kernel(BatchParams P) {
   }
 #pragma unroll
   for (int i = 0; i < 32; ++i) G[i * 32 + lane] = g[i];   // G[i][lane] (symmetric)
-  if (P.weighted) batched_weights(Nj, act, lane, S);
+  if (WT) batched_weights(Nj, act, lane, S);
   const double rn = act ? 1.0 / Nj : 0.0;
   double x = (act && P.x0) ? P.x0[inst * n + lane] : 0.0;
   const double xr = (act && P.xref) ? P.xref[inst * n + lane] : 0.0;
   const double xr2 = warp_sum(xr * xr);
-  const uint32_t hb = feistel_half_bits((uint32_t)n), msk = (1u << hb) - 1u;
+  const uint32_t hb = N32 ? 3u : feistel_half_bits((uint32_t)n), msk = (1u << hb) - 1u;
   __syncwarp();
 
   const int64_t ce = P.check_every;
@@ -607,7 +610,7 @@ __global__ void __launch_bounds__(32) batched_scd_kernel(BatchParams P) {
         if (kk == 0) {
           BKeyT e;
           const uint64_t tt = (uint64_t)(t + lane);
-          if (P.weighted) {
+          if (WT) {
             const U4 xw = draw(seed, (uint32_t)it, tt, kTagRcd);
             e.j = sample_weighted_small(((uint64_t)xw.y << 32) | xw.x, S, n);
             e.alpha = 1;
@@ -639,7 +642,7 @@ __global__ void __launch_bounds__(32) batched_scd_kernel(BatchParams P) {
           __syncwarp();
         }
         int j;
-        if (P.weighted) {
+        if (WT) {
           j = keys[kk].j;
         } else {
           uint32_t tb[2 * kFeistelRounds];
@@ -1019,8 +1022,11 @@ int batched_solve(Handle& h, int method, const double* x0, double* x, double tol
   }
   if (method == 2) {   // SP-SCD / SP-RCD: A1bar resident
     const size_t smem = (size_t)32 * 32 * 8 + 32 * 8 + 32 * sizeof(BKeyT);
-    ILS_CU(cudaFuncSetAttribute(batched_scd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    batched_scd_kernel<<<(unsigned)h.batch, 32, smem, h.stream>>>(P);
+    const bool n32 = h.n == 32;
+    void (*kern)(BatchParams) = P.weighted ? (n32 ? batched_scd_kernel<true, true> : batched_scd_kernel<true, false>)
+                                           : (n32 ? batched_scd_kernel<false, true> : batched_scd_kernel<false, false>);
+    ILS_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)h.batch, 32, smem, h.stream>>>(P);
     ILS_LAUNCHED("batched_scd_kernel");
     return ILS_OK;
   }

@@ -715,3 +715,28 @@ def test_sp_leaf_variants_match_oracle(shape, monkeypatch):
             ils.ils_sp_solve(hh.h, None, x, 0.0, K, ils.ils_default_opts(stop=ils.ILS_STOP_NONE, x_hist=hist.ctypes.data))
         for k in range(K):
             assert _par(hist[k], ref.x_hist[k]) <= 1e-9, (old, k)
+
+
+@pytest.mark.parametrize("n", [1, 5, 17, 24, 31])
+@pytest.mark.parametrize("method", ["rgs", "rcd"])
+def test_batched_scd_generic_n_vs_oracle(n, method):
+    """Batched SP-SCD / SP-RCD (Alg. 5) at n != 32: the generic kernel (Feistel
+    domains 4^h of 4, 16 and 64 with cycle walking through values >= n) against the oracle per
+    instance; n = 32 (c4) takes the specialised kernel (test_batched_vs_oracle)."""
+    from workloads import make_batched
+    bt = make_batched(batch=12, p=3 * n + 8, q=max(n // 2, 1), n=n, base_seed=300)
+    K, T, ce = 3, 150, 25
+    x = np.zeros((bt.batch, bt.n))
+    h = ils.ils_create(bt.A, bt.b, bt.p, bt.q, bt.n, batch=bt.batch)
+    try:
+        o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, max_inner=T, check_every=ce, inner_tol=0.0, seed=300,
+                                 weighted=1 if method == "rcd" else 0)
+        ils.ils_rgs_solve(h, None, x, 0.0, K, o)
+    finally:
+        ils.ils_destroy(h)
+    for i in range(bt.batch):
+        A1, A2 = bt.A[i, :bt.p], bt.A[i, bt.p:]
+        b1, b2 = bt.b[i, :bt.p], bt.b[i, bt.p:]
+        ref = O.sp_scd_solve(A1, A2, b1, b2, max_iter=K, stop=O.STOP_NONE, seed=300 + i, max_inner=T,
+                             check_every=ce, inner_tol=0.0, weighted=(method == "rcd"))
+        assert _par(x[i], ref.x) <= 1e-9, (method, n, i)
