@@ -55,6 +55,7 @@ struct RkParams {
   int64_t ce;
   double inner_tol;
   double* Zsnap;
+  int nap;             // look-ahead kernel: ns a polling helper warp (fill, TMA, check) sleeps per poll
 };
 
 // Ring entries for steps t0 .. t0+31 (one per lane): Philox draw, two weighted inverse-CDF
@@ -1150,6 +1151,7 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
           quit = true;
           break;
         }
+        if (p.nap) __nanosleep(p.nap);   // leave the issue slots to the compute warp of this SMSP
       }
       if (quit) break;
       rk_fill_indices(p, Ss, ring, p.t0 + 4 * f, lane, bh_tab, rn_tab);
@@ -1169,6 +1171,7 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
             quit = true;
             break;
           }
+          if (p.nap) __nanosleep(p.nap);
         }
         if (quit) break;
         fence_proxy_async();
@@ -1194,6 +1197,7 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
           gone = ld_acquire_cta_s64(&snap_s) <= m;
           break;
         }
+        if (p.nap) __nanosleep(4 * p.nap);   // snapshots come every check_every steps
       }
       if (gone) break;
       double part = 0.0;
@@ -1606,6 +1610,12 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
   p.k = (uint32_t)k;
   p.max_inner = max_inner;
   p.st = h.dstat;
+  {
+    // ns per poll of the look-ahead kernel's helper warps (fill, TMA, check): sleeping polls leave the
+    // issue slots of their SMSPs to the compute warps (c1: 198.8 -> 195.1 ms at 300 ns; 0 = spin)
+    const char* e = getenv("ILS_RK_NAP");
+    p.nap = (e && atoi(e) >= 0) ? atoi(e) : 300;
+  }
   // launch geometry (fixed for the whole solve). Blocked kernel (4 steps per reduction) when the
   // CTA has <= 256 threads and >= 2 slots of 8 column slices fit; else the single-step kernel.
   int C = rk_cluster_size(h);
