@@ -14,6 +14,7 @@
 //         A1bar (prefetched with the index ring). Check: A1 z (CSR) and A1^T (A1 z) (CSC).
 // SP-SCD: A1bar compacted to CSR (~11% dense at c3); one CTA keeps r (n <= 26000) in shared
 //         memory; membership masks precomputed per chunk (scd.cu); check r = b_hat - A1bar beta.
+#include <cstdio>
 #include <climits>
 
 #include <cooperative_groups.h>
@@ -415,6 +416,7 @@ struct SpRkParams {
   uint32_t k;
   int64_t t0, t1;
   DevStatus* st;
+  long long* prof;      // sparse_rk_la_kernel<true>: per-phase cycles (thread 0), ILS_SRK_PROF=1
 };
 
 struct SpRkIdx {
@@ -739,7 +741,17 @@ __device__ __forceinline__ void srk_la_fill(const SpRkParams& p, const uint64_t*
   if (live) ring[t & (SRK_RING - 1)] = e;
 }
 
+template <bool PROF>
 __global__ void __launch_bounds__(SRK_T) sparse_rk_la_kernel(SpRkParams p) {
+  long long pc[6] = {0, 0, 0, 0, 0, 0}, tc0 = PROF ? clock64() : 0;
+#define SLAP(q)                                      \
+  do {                                               \
+    if (PROF && threadIdx.x == 0) {                  \
+      const long long c_ = clock64();                \
+      pc[q] += c_ - tc0;                             \
+      tc0 = c_;                                      \
+    }                                                \
+  } while (0)
   extern __shared__ __align__(16) unsigned char srk_smem[];
   double (*cvs)[2][SRK_MAXK] = reinterpret_cast<double (*)[2][SRK_MAXK]>(srk_smem);              // [D][2][MAXK]
   int32_t (*crs)[2][SRK_MAXK] = reinterpret_cast<int32_t (*)[2][SRK_MAXK]>(srk_smem + SRK_D * 2 * SRK_MAXK * 8);
@@ -813,8 +825,10 @@ __global__ void __launch_bounds__(SRK_T) sparse_rk_la_kernel(SpRkParams p) {
     constexpr int PH = decltype(phc)::value, NX = (PH + 2) % 3;
     const int pb = (int)(t & 1);
     if (warp == 7 && ((t - p.t0) & 31) == 0 && t + 64 < p.t1) srk_la_fill(p, Ssm, ring, t + 64, lane);
+    SLAP(5);
     cp_async_wait<1>();   // slot of step t + 2 (groups up to t + 3 issued)
     __syncthreads();
+    SLAP(0);
     if (t + 2 < p.t1) gather(t + 2, gw[NX], gq[NX]);   // on S_t: corrected for steps t, t+1 later
     const SpRkLaIdx& ix = ring[t & (SRK_RING - 1)];
     const int sl = (int)(t % SRK_D);
@@ -833,7 +847,9 @@ __global__ void __launch_bounds__(SRK_T) sparse_rk_la_kernel(SpRkParams p) {
       red[pb][warp][0] = d1;
       red[pb][warp][1] = d2;
     }
+    SLAP(1);
     __syncthreads();
+    SLAP(2);
     double D1 = 0.0, D2 = 0.0;
 #pragma unroll
     for (int w = 0; w < SRK_T / 32; ++w) {
@@ -869,11 +885,13 @@ __global__ void __launch_bounds__(SRK_T) sparse_rk_la_kernel(SpRkParams p) {
       }
     }
     if (tid == 0) atomicAdd(p.Z + ix.j2, s2);
+    SLAP(3);
     s1m2 = s1m1;
     s1m1 = s1;
     s2m2 = s2m1;
     s2m1 = s2;
     __syncthreads();   // this step's updates precede the next step's gathers; slot sl is free
+    SLAP(4);
     stage(t + SRK_D);
   };
   int64_t t = p.t0;
@@ -885,6 +903,9 @@ __global__ void __launch_bounds__(SRK_T) sparse_rk_la_kernel(SpRkParams p) {
   if (t < p.t1) body(t, std::integral_constant<int, 0>{});
   if (t + 1 < p.t1) body(t + 1, std::integral_constant<int, 1>{});
   cp_async_wait<0>();
+  if (PROF && threadIdx.x == 0)
+    for (int q = 0; q < 6; ++q) atomicAdd(reinterpret_cast<unsigned long long*>(p.prof + q), (unsigned long long)pc[q]);
+#undef SLAP
 }
 
 __global__ void max_col_kernel(const int64_t* __restrict__ cp, int64_t n, unsigned long long* out) {
@@ -952,7 +973,16 @@ int sparse_rk_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int
   // look-ahead kernel when every column is staged whole (ILS_SRK_LA=0 keeps the one-step kernel)
   const char* ela = getenv("ILS_SRK_LA");
   const bool la = h.maxcol1 <= SRK_LA_K && !(ela && ela[0] == '0');
-  if (la) ILS_CU(cudaFuncSetAttribute(sparse_rk_la_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const char* eprof = getenv("ILS_SRK_PROF");
+  const bool sprof = la && eprof && eprof[0] == '1';
+  if (la) {
+    ILS_CU(cudaFuncSetAttribute(sparse_rk_la_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ILS_CU(cudaFuncSetAttribute(sparse_rk_la_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  if (sprof) {
+    ILS_CU(cudaMallocAsync(&prm.prof, 8 * sizeof(long long), st));
+    ILS_CU(cudaMemsetAsync(prm.prof, 0, 8 * sizeof(long long), st));
+  }
   const int64_t prow = h.p, nn = h.n;
   const int64_t* rp = h.rp;
   const int32_t* ci = h.ci;
@@ -970,7 +1000,8 @@ int sparse_rk_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int
     prm.t0 = t;
     prm.t1 = t1;
     if (la) {
-      sparse_rk_la_kernel<<<1, SRK_T, smem, st>>>(prm);
+      if (sprof) sparse_rk_la_kernel<true><<<1, SRK_T, smem, st>>>(prm);
+      else sparse_rk_la_kernel<false><<<1, SRK_T, smem, st>>>(prm);
       ILS_LAUNCHED("sparse_rk_la_kernel");
     } else {
       sparse_rk_kernel<<<1, SRK_T, smem, st>>>(prm);
@@ -998,6 +1029,15 @@ int sparse_rk_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int
   ILS_CU(cudaMemcpyAsync(h.hstat, h.dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
   ILS_CU(cudaStreamSynchronize(st));
   const int64_t steps = h.hstat->inner_conv ? h.hstat->inner_steps : max_inner;
+  if (sprof) {
+    long long hp[6];
+    cudaMemcpy(hp, prm.prof, sizeof(hp), cudaMemcpyDeviceToHost);
+    cudaFree(prm.prof);
+    const double st_ = (double)(steps > 0 ? steps : 1);
+    fprintf(stderr, "ILS_SRK_PROF steps=%lld cycles/step: top-barrier %.0f gather+dots+reduce %.0f barrier2 %.0f "
+            "recurrence+updates %.0f end-barrier %.0f stage+loop %.0f\n", (long long)steps, hp[0] / st_, hp[1] / st_,
+            hp[2] / st_, hp[3] / st_, hp[4] / st_, hp[5] / st_);
+  }
   if (steps_out) *steps_out = steps;
   const double nnz1 = (double)h.nnz1;
   // bytes per step: the two sampled columns (12 B per entry) and the w / r entries they touch
