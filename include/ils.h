@@ -140,7 +140,9 @@ typedef struct {
   int32_t sp_form;           /* [0] 0: x = P (A1^T b1 + A2^T (A2 x - b2)) (Sec23); 1: x += P A^T J (b - A x);
                                 2: the paper's literal layout: SP x = B x + c with B = P A2^T A2, c = P A^T J b
                                 formed once (Alg. 1 steps 2-6); RK/RGS b_hat = A2bar x + A^T J b
-                                with A2bar = A2^T A2 formed once (Alg. 2 steps 2-5, Alg. 5 steps 2-4). Dense only.
+                                with A2bar = A2^T A2 formed once (Alg. 2 steps 2-5, Alg. 5 steps 2-4). CSR input:
+                                A2bar from the CSC of A2 (dense rows, n <= 29000); SP's B = P A2bar needs the
+                                explicit P, so SP at n >= 8192 (dense or CSR) returns ILS_ERR_UNSUPPORTED.
                                 3 (ILS_SP_FORM_AUTO): 2 if its precompute pays off over expected_outer outer
                                 steps, else 0 (include/ils.h "Automatic form"). */
   double* x_hist;            /* [NULL] optional [max_iter][n] record of every outer iterate (batch 1) */
@@ -191,8 +193,8 @@ ILS_API const char* ils_last_error(void);
  * CSR input (ext->format = ILS_FORMAT_CSR): the CSR arrays are validated (ILS_ERR_ARG on an
  * out-of-range / unsorted / duplicated column, a bad row pointer or a non-finite value) and
  * converted to CSC for A1 and A2 (columns sorted by row). SP forms A1^T A1 densely (n <= 29000);
- * SP-SCD/RCD use it compacted to CSR; sp_form = 2 (explicit B = P A2bar) returns
- * ILS_ERR_UNSUPPORTED for CSR input in this release. */
+ * SP-SCD/RCD use it compacted to CSR; sp_form = 2 forms A2bar = A2^T A2 from the CSC of A2
+ * (and, for SP at n < 8192, B = P A2bar). */
 ILS_API int ils_create(ils_handle* h, const double* A, const double* b,
                int64_t p, int64_t q, int64_t n, const ils_ext* ext);
 

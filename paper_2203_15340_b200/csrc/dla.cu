@@ -774,6 +774,12 @@ int build_a2bar(Handle& h) {
   const size_t bytes = (size_t)np * np * sizeof(double);
   if (!h.A2bar) ILS_CU(cudaMallocAsync(&h.A2bar, bytes, h.stream));
   if (!h.lit_vec) ILS_CU(cudaMallocAsync(&h.lit_vec, 2 * (size_t)np * sizeof(double), h.stream));
+  if (h.sparse) {
+    int r = sparse_a2bar(h, h.A2bar, h.lit_vec);
+    if (r) return r;
+    h.have_a2bar = true;
+    return ILS_OK;
+  }
   ILS_CU(cudaMemsetAsync(h.A2bar, 0, bytes, h.stream));
   if (h.q > 0) {
     const int64_t kq = roundup(h.q, 32);

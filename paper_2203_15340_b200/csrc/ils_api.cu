@@ -601,10 +601,6 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
     set_error("solve: sp_form must be 0, 2 or 3 (RK/RGS), 0..3 (SP)");
     return ILS_ERR_ARG;
   }
-  if (H.sparse && o.sp_form == 2) {
-    set_error("CSR input: sp_form 2 (explicit B = P A2bar) is not implemented in this release");
-    return ILS_ERR_UNSUPPORTED;
-  }
   const bool sharded = H.comm != nullptr;
   if (sharded && (method == 1 || o.sp_form == 2)) {
     set_error("row-sharded handle: SP-RK-RGS (needs whole columns of A1) and sp_form 2 are not supported");
@@ -784,7 +780,7 @@ static int solve_common(ils_handle h, int method, const double* x0, double* x, d
     rep->setup_ms = setup_ms;
     rep->solve_ms = solve_ms;
     const double q = (double)H.q, p = (double)H.p, nd = (double)n;
-    if (H.sparse) {   // algorithmic bytes of the sparse path (12 B per CSR/CSC entry)
+    if (H.sparse && o.sp_form != 2) {   // algorithmic bytes of the sparse path (12 B per CSR/CSC entry)
       const double a2 = (method == 0 && o.sp_form == 1) ? 24.0 * (double)H.nnz + 16.0 * (double)H.m
                                                         : 12.0 * (double)(H.nnz - H.nnz1) * 2.0 + 16.0 * q;
       const double rk_step = 2.0 * ((double)H.nnz1 / nd) * 28.0;

@@ -185,6 +185,7 @@ int stop_metric(Handle& h, const double* x, const double* xref, double* out_dev)
 // sparse.cu (CSR input)
 int sparse_ingest(Handle& h, int32_t* d_flag, bool* ok);
 int sparse_gram(Handle& h, double* G, bool subtract_a2);
+int sparse_a2bar(Handle& h, double* A2bar, double* ajb);   // CSR: A2^T A2 (dense rows), A^T J b
 int sparse_rhs(Handle& h, const double* x, double* c, int full);
 int gemv_p(Handle& h, const double* c, double* x);
 int sparse_rk_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_t k, int64_t max_inner,

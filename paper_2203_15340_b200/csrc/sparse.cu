@@ -356,6 +356,45 @@ int sparse_gram(Handle& h, double* G, bool subtract_a2) {
   return ILS_OK;
 }
 
+__global__ void neg_copy_kernel(const double* __restrict__ x, int64_t len, double* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) y[i] = -x[i];
+}
+
+__global__ void zero_pad_diag_kernel(double* __restrict__ G, int64_t n, int64_t npad) {
+  for (int64_t j = n + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < npad; j += (int64_t)gridDim.x * blockDim.x)
+    G[j * npad + j] = 0.0;
+}
+
+// Paper-literal precompute for CSR input (Alg. 1 steps 2-3; Alg. 2 steps 2-3,
+// :291-292; Alg. 5 steps 2-4, :689-691): A2bar = A2^T A2 as dense rows from the CSC of A2 (the Gram
+// kernel of A1bar run over the A2 rows, zero padding), and A^T J b = A1^T b1 - A2^T b2 by one CSC
+// column pass over -b2.
+int sparse_a2bar(Handle& h, double* A2bar, double* ajb) {
+  const cudaStream_t st = h.stream;
+  const size_t smem = (size_t)h.npad * sizeof(double);
+  if (smem > 227 * 1024) {
+    set_error("sparse path: n > 29000 does not fit the shared-memory Gram row");
+    return ILS_ERR_UNSUPPORTED;
+  }
+  ILS_CU(cudaFuncSetAttribute(sparse_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  sparse_gram_kernel<<<(unsigned)h.npad, 256, smem, st>>>(h.rp, h.ci, h.va, h.p, h.cp2, h.cr2, h.cv2, h.n, h.npad, 1.0,
+                                                          0, A2bar);
+  ILS_LAUNCHED("sparse_gram_kernel");
+  if (h.npad > h.n) {   // the Gram kernel writes identity rows for the padding: A2bar is zero there
+    zero_pad_diag_kernel<<<1, 64, 0, st>>>(A2bar, h.n, h.npad);
+    ILS_LAUNCHED("zero_pad_diag_kernel");
+  }
+  if (h.q > 0) {
+    neg_copy_kernel<<<grid_for(h.q, 256), 256, 0, st>>>(h.b + h.p, h.q, h.sp_y);
+    ILS_LAUNCHED("neg_copy_kernel");
+    spmv_cols_kernel<<<grid_for(h.npad, 256), 256, 0, st>>>(h.cp2, h.cr2, h.cv2, h.sp_y, h.a1tb1, h.n, h.npad, 0, ajb);
+    ILS_LAUNCHED("spmv_cols_kernel");
+  } else {
+    ILS_CU(cudaMemcpyAsync(ajb, h.a1tb1, h.npad * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  return ILS_OK;
+}
+
 // ---------------------------------------------------------------------------------------------
 // x = P c (dense, npad x npad): warp per row, 8 outstanding 16-byte loads per lane
 __global__ void __launch_bounds__(256) gemv_p_kernel(const double* __restrict__ P, const double* __restrict__ c,

@@ -109,7 +109,7 @@ def test_sparse_sp_fixed_horizon(shape, form):
         assert _par(hist[kk], ref.x_hist[kk]) <= 1e-9, kk
 
 
-def test_sparse_sp_rr_stop_and_unsupported_modes():
+def test_sparse_sp_rr_stop():
     pr = make_sparse(500, 100, 60, 5, seed=14)
     A1, A2, b1, b2 = _dense(pr)
     ref = O.sp_solve(A1, A2, b1, b2, tol=1e-12, stop=O.STOP_RR, max_iter=100)
@@ -119,9 +119,6 @@ def test_sparse_sp_rr_stop_and_unsupported_modes():
         st, rep = ils.ils_sp_solve(hh.h, None, x, 1e-12, 100, o)
         assert rep.converged and rep.final_metric < 1e-12
         assert abs(rep.outer_iters - ref.outer_iters) <= 1
-        with pytest.raises(ils.IlsError) as e:
-            ils.ils_sp_solve(hh.h, None, x, 1e-12, 5, ils.ils_default_opts(stop=ils.ILS_STOP_NONE, sp_form=2))
-        assert e.value.status == ils.ILS_ERR_UNSUPPORTED
 
 
 @pytest.mark.parametrize("T", [1, 7, 333])
@@ -224,3 +221,34 @@ def test_sparse_c3_full_size_sp():
         st, rep = ils.ils_sp_solve(hh.h, None, x, pr.tol, 100, o)
     assert st == ils.ILS_OK and rep.converged
     assert _rel(x.cpu().numpy(), xref) <= pr.tol
+
+
+@pytest.mark.parametrize("method", ["sp", "rk", "rgs"])
+@pytest.mark.parametrize("shape", [(500, 100, 60, 5), (2000, 400, 300, 8)])
+def test_sparse_literal_precompute_forms(method, shape):
+    """CSR input with the paper-literal precompute (sp_form = 2; Alg. 1 steps 2-3, PAPER.md:134-135:
+    B = P A2bar, c = P A^T J b; Alg. 2 / Alg. 5 step 5: b_hat = A2bar x_k + A^T J b with A2bar =
+    A2^T A2 formed from the CSC of A2) against the oracle's literal forms at a fixed horizon."""
+    p, q, n, k = shape
+    pr = make_sparse(p, q, n, k, seed=23)
+    A1, A2, b1, b2 = _dense(pr)
+    K = 4
+    kw = dict(max_iter=K, stop=O.STOP_NONE)
+    if method == "sp":
+        ref = O.sp_solve(A1, A2, b1, b2, sp_form=2, **kw)
+    elif method == "rk":
+        ref = O.sp_rk_rgs_solve(A1, A2, b1, b2, seed=6, max_inner=300, check_every=50, inner_tol=0.0,
+                                rhs_literal=True, **kw)
+    else:
+        ref = O.sp_scd_solve(A1, A2, b1, b2, seed=6, max_inner=300, check_every=50, inner_tol=0.0,
+                             rhs_literal=True, **kw)
+    hist = np.zeros((K, n))
+    x = np.zeros(n)
+    with HS(pr) as hh:
+        o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, sp_form=2, seed=6, max_inner=300, check_every=50,
+                                 inner_tol=0.0, x_hist=hist.ctypes.data)
+        fn = {"sp": ils.ils_sp_solve, "rk": ils.ils_rk_solve, "rgs": ils.ils_rgs_solve}[method]
+        st, rep = fn(hh.h, None, x, 0.0, K, o)
+        assert rep.sp_form_used == 2
+    for kk in range(K):
+        assert _par(hist[kk], ref.x_hist[kk]) <= 1e-9, kk
