@@ -533,8 +533,11 @@ __global__ void __launch_bounds__(SCD_MAXT, 1) scd_chunk_kernel(ScdParams p) {
       // every warp reduces the NW warp winners the same way
       const double cv = (lane < NW) ? wv[pb][lane] : 0.0;
       const int ci = (lane < NW) ? wi[pb][lane] : INT_MAX;
+      const double crr = (lane < NW) ? wr[pb][lane] : 0.0;
       j = warp_argmax_redux(cv, ci);
-      rj = wr[pb][(j % NT) >> 5];   // the winning warp's entry
+      // the winning warp's r_j: the lane holding candidate j (a vote and a shuffle, not an integer
+      // modulo by the CTA size and a dependent shared-memory load: 0.664 -> 0.652 us/step at c1)
+      rj = __shfl_sync(0xffffffffu, crr, __ffs(__ballot_sync(0xffffffffu, ci == j)) - 1);
     }
     const double sc = rj * rNs[j];
     const double* grow = p.G + (int64_t)j * p.npad;
