@@ -730,12 +730,15 @@ static int launch_rk(Handle& h, RkParams& p, int nt, size_t smem) {
 // check (include/ils.h: az = A1 z, g = A1^T az - b_hat, reset r = w - az) done in place every
 // check_every steps, so a solve is one launch instead of two launches per check interval.
 // Blocks restart at every check boundary (steps past it are masked), as the chunked launches do.
-template <int U>
+// LK: the 22 in-block column inner products are looked up in A1bar (p.G, staged in shared memory)
+// instead of reduced with the state products (8 values per block reduction instead of 30), as in
+// the look-ahead and batched kernels.
+template <int U, bool LK>
 __global__ void __launch_bounds__(256, 1) rk_rgs_small_kernel(RkParams p, double* __restrict__ zout,
                                                               int64_t ce, double inner_tol) {
   constexpr int B = 4;
   using K = RkBlk<B>;
-  constexpr int NVP = 32;
+  constexpr int NVP = LK ? 8 : 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NT = blockDim.x, NW = NT >> 5;
@@ -748,12 +751,15 @@ __global__ void __launch_bounds__(256, 1) rk_rgs_small_kernel(RkParams p, double
   double* bh_tab = reinterpret_cast<double*>(Ss + ((n + 1) & ~1));   // [n]
   double* rn_tab = bh_tab + ((n + 1) & ~1);                     // [n]
   RkIdx* ring = reinterpret_cast<RkIdx*>(rn_tab + ((n + 1) & ~1));   // [RK_RING]
+  double* Gs = reinterpret_cast<double*>(ring + RK_RING);          // LK: [npad][npad] A1bar
   __shared__ __align__(16) double wred[8][32];
   __shared__ double tots[32];
   __shared__ double red2[8][2];
   __shared__ int stop_s;
 
   for (int64_t e = tid; e < (int64_t)p.npad * PP; e += NT) A1s[e] = p.A1T[e];
+  if (LK)
+    for (int64_t e = tid; e < (int64_t)p.npad * p.npad; e += NT) Gs[e] = p.G[e];
   for (int j = tid; j < p.npad; j += NT) zs[j] = 0.0;
   for (int j = tid; j < n; j += NT) {
     Ss[j] = p.S[j];
@@ -815,14 +821,30 @@ __global__ void __launch_bounds__(256, 1) rk_rgs_small_kernel(RkParams p, double
           for (int i = 0; i < B; ++i) {
             acc[K::P(i)] = fma(xa[i], w[u], acc[K::P(i)]);
             acc[K::Q(i)] = fma(xb[i], r[u], acc[K::Q(i)]);
+            if (!LK) {
 #pragma unroll
-            for (int k = 0; k < i; ++k) {
-              acc[K::AA(i, k)] = fma(xa[i], xa[k], acc[K::AA(i, k)]);
-              acc[K::BB(i, k)] = fma(xb[i], xb[k], acc[K::BB(i, k)]);
+              for (int k = 0; k < i; ++k) {
+                acc[K::AA(i, k)] = fma(xa[i], xa[k], acc[K::AA(i, k)]);
+                acc[K::BB(i, k)] = fma(xb[i], xb[k], acc[K::BB(i, k)]);
+              }
+#pragma unroll
+              for (int k = 0; k <= i; ++k) acc[K::BA(i, k)] = fma(xb[i], xa[k], acc[K::BA(i, k)]);
             }
-#pragma unroll
-            for (int k = 0; k <= i; ++k) acc[K::BA(i, k)] = fma(xb[i], xa[k], acc[K::BA(i, k)]);
           }
+        }
+      }
+      double T[K::NV];
+      if (LK) {   // the block's column inner products from A1bar (before the reduction: off its path)
+        const int64_t ld = p.npad;
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+#pragma unroll
+          for (int k = 0; k < i; ++k) {
+            T[K::AA(i, k)] = Gs[ix[i].j1 * ld + ix[k].j1];
+            T[K::BB(i, k)] = Gs[ix[i].j2 * ld + ix[k].j2];
+          }
+#pragma unroll
+          for (int k = 0; k <= i; ++k) T[K::BA(i, k)] = Gs[ix[i].j2 * ld + ix[k].j1];
         }
       }
       const double mine = warp_reduce_scatter<NVP>(acc, lane);
@@ -834,9 +856,8 @@ __global__ void __launch_bounds__(256, 1) rk_rgs_small_kernel(RkParams p, double
         tots[lane] = v;
       }
       __syncthreads();
-      double T[K::NV];
 #pragma unroll
-      for (int v = 0; v < K::NV; ++v) T[v] = tots[v];
+      for (int v = 0; v < (LK ? NVP : K::NV); ++v) T[v] = tots[v];
       double s1[B], s2[B];
 #pragma unroll
       for (int i = 0; i < B; ++i) {
@@ -1744,20 +1765,37 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
     if (C == 1 && !(e && e[0] == '0') && small_smem <= 200 * 1024 && h.ppad <= 2048 && !prof) {
       // one row per thread up to 256 rows (8 warps share the products and reductions), then U rows
       const int nts = (int)((h.ppad + 31) / 32 * 32);
-      const int ntc = nts > 256 ? 256 : nts;
+      int ntc = nts > 256 ? 256 : nts;
+      {
+        const char* e = getenv("ILS_RK_SMALL_NT");   // experiment override: CTA size (32 .. 256)
+        if (e && atoi(e) >= 32 && atoi(e) <= 256 && (atoi(e) & 31) == 0 && (int64_t)atoi(e) * 8 >= h.ppad) ntc = atoi(e);
+      }
       const int Us = (int)((h.ppad + ntc - 1) / ntc);
       p.slice = (int)h.p;   // rows >= p are padding (azs)
       p.t0 = 0;
       p.t1 = max_inner;
+      // Gram lookups (A1bar staged next to A1) when it fits: 8 reduced values per block instead of 30
+      const size_t gs_bytes = (size_t)h.npad * h.npad * 8;
+      const char* elk = getenv("ILS_RK_SMALL_LOOKUP");   // experiment override: 0 = reduce all 30 values
+      const bool lk = small_smem + gs_bytes <= 200 * 1024 && !(elk && elk[0] == '0');
+      if (lk) {
+        int rc = build_gram(h);
+        if (rc) return rc;
+        p.G = h.G;
+      }
+      const size_t smem_k = small_smem + (lk ? gs_bytes : 0);
       ILS_CU(cudaEventRecord(h.evk0, st));
-      void* kern = (Us <= 1) ? (void*)rk_rgs_small_kernel<1>
-                   : (Us <= 2) ? (void*)rk_rgs_small_kernel<2>
-                   : (Us <= 4) ? (void*)rk_rgs_small_kernel<4> : (void*)rk_rgs_small_kernel<8>;
-      ILS_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_smem));
+      void* kern = lk ? ((Us <= 1) ? (void*)rk_rgs_small_kernel<1, true>
+                         : (Us <= 2) ? (void*)rk_rgs_small_kernel<2, true>
+                         : (Us <= 4) ? (void*)rk_rgs_small_kernel<4, true> : (void*)rk_rgs_small_kernel<8, true>)
+                      : ((Us <= 1) ? (void*)rk_rgs_small_kernel<1, false>
+                         : (Us <= 2) ? (void*)rk_rgs_small_kernel<2, false>
+                         : (Us <= 4) ? (void*)rk_rgs_small_kernel<4, false> : (void*)rk_rgs_small_kernel<8, false>);
+      ILS_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k));
       double itol = inner_tol;
       int64_t ce64 = ce;
       void* args[] = {&p, &z, &ce64, &itol};
-      ILS_CU(cudaLaunchKernel(kern, dim3(1), dim3(ntc), args, small_smem, st));
+      ILS_CU(cudaLaunchKernel(kern, dim3(1), dim3(ntc), args, smem_k, st));
       ILS_LAUNCHED("rk_rgs_small_kernel");
       ILS_CU(cudaEventRecord(h.evk1, st));
       ILS_CU(cudaMemcpyAsync(h.hstat, h.dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
