@@ -1339,11 +1339,9 @@ __global__ void __cluster_dims__(SCDC_C, 1, 1) __launch_bounds__(SCDC_T, 1) scd_
   constexpr int NTT = SCDC_C * SCDC_T;
   __shared__ double wv[2][32], wr[2][32], wn[2][32];
   __shared__ int wi[2][32];
-  __shared__ __align__(16) double recv[2][SCDC_C][4];   // [source CTA] (r_j^2, r_j, j, N_j)
+  __shared__ __align__(16) double recv[2][SCDC_C][4];   // [source CTA] (r_j^2, r_j, j, 1 / N_j)
   __shared__ __align__(8) uint64_t rbar[2];
   __shared__ double red[32];
-  __shared__ int win_j[2];
-  __shared__ double win_sc[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rank = (int)cluster_ctarank();
   const int g = rank * SCDC_T + tid;
@@ -1370,7 +1368,7 @@ __global__ void __cluster_dims__(SCDC_C, 1, 1) __launch_bounds__(SCDC_T, 1) scd_
   for (int v = 0; v < V; ++v) {
     const int s = g + v * NTT;
     r[v] = (s < n) ? p.Rv[s] : 0.0;
-    nj[v] = (s < n) ? p.N[s] : 1.0;
+    nj[v] = (s < n) ? 1.0 / p.N[s] : 1.0;   // reciprocal: the step length is one multiply (as scd_chunk_kernel)
     beta[v] = (s < n) ? p.Bv[s] : 0.0;
   }
   uint32_t allbits = 0;
@@ -1428,38 +1426,31 @@ __global__ void __cluster_dims__(SCDC_C, 1, 1) __launch_bounds__(SCDC_T, 1) scd_
       wn[pb][warp] = bn;
     }
     __syncthreads();
-    if (warp == 0) {   // CTA winner, one message to every CTA, then the cluster winner
+    if (warp == 0) {   // CTA winner, one message to every CTA
+      if (lane == 0 && t > p.t0)   // every warp has read step t-1's messages: re-arm that buffer for t+1
+        mbar_arrive_expect_tx(&rbar[pb ^ 1], SCDC_C * 32);
       const double cv0 = (lane < SCDC_T / 32) ? wv[pb][lane] : 0.0;
       const int ci0 = warp_argmax_redux(cv0, (lane < SCDC_T / 32) ? wi[pb][lane] : INT_MAX);
       const int ww = (ci0 == INT_MAX) ? 0 : (((ci0 % NTT) - rank * SCDC_T) >> 5);   // its warp
       const double cv = (ci0 == INT_MAX) ? 0.0 : wv[pb][ww];
       const double cr = wr[pb][ww], cn0 = (ci0 == INT_MAX) ? 1.0 : wn[pb][ww];
-      // lane 0 carries (r_j^2, r_j), lane 1 carries (j, N_j): 32 bytes per destination
+      // lane 0 carries (r_j^2, r_j), lane 1 carries (j, 1 / N_j): 32 bytes per destination
       const double m0 = (lane == 0) ? cv : (double)ci0;
       const double m1 = (lane == 0) ? cr : cn0;
       const uint32_t la = smem_u32(&recv[pb][rank][2 * (lane & 1)]);
       const uint32_t lb = smem_u32(&rbar[pb]);
+      __syncwarp();   // the re-arm precedes this step's sends (the peers' step t+1 messages follow them)
       if (lane < 2)
 #pragma unroll
         for (int c = 0; c < SCDC_C; ++c) st_async_v2f64(map_shared_rank(la, (uint32_t)c), m0, m1, map_shared_rank(lb, (uint32_t)c));
-      mbar_wait_cluster(&rbar[pb], (uint32_t)((t - p.t0) >> 1) & 1u);
-      // the 16 CTA winners, lane c holds candidate c (ties to the smallest index)
-      const double xv = (lane < SCDC_C) ? recv[pb][lane][0] : 0.0;
-      const int xi = warp_argmax_redux(xv, (lane < SCDC_C) ? (int)recv[pb][lane][2] : INT_MAX);
-      const int wc = (xi % NTT) / SCDC_T;   // the CTA that owns coordinate xi
-      const double xr = recv[pb][wc][1], xn = recv[pb][wc][3];
-      __syncwarp();   // warp 0 has read recv[pb]: re-arm it for step t + 2
-      if (lane == 0) {
-        mbar_arrive_expect_tx(&rbar[pb], SCDC_C * 32);
-        win_j[pb] = xi;
-        win_sc[pb] = xr / xn;
-      }
     }
-    __syncthreads();
-    const int ci = win_j[pb];
-    const double cr = win_sc[pb], cn = 1.0;
-    const int j = ci;
-    const double sc = cr / cn;   // = r_j / N_j (computed once by warp 0)
+    // every warp waits for the 16 CTA winners and reduces them the same way (no second CTA barrier):
+    // lane c holds candidate c, ties to the smallest index
+    mbar_wait_cluster(&rbar[pb], (uint32_t)((t - p.t0) >> 1) & 1u);
+    const double xv = (lane < SCDC_C) ? recv[pb][lane][0] : 0.0;
+    const int j = warp_argmax_redux(xv, (lane < SCDC_C) ? (int)recv[pb][lane][2] : INT_MAX);
+    const int wc = (j % NTT) / SCDC_T;   // the CTA that owns coordinate j
+    const double sc = recv[pb][wc][1] * recv[pb][wc][3];   // r_j / N_j as r_j * (1 / N_j)
     const double* grow = p.G + (int64_t)j * p.npad;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
