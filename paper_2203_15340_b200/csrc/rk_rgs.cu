@@ -56,6 +56,7 @@ struct RkParams {
   double inner_tol;
   double* Zsnap;
   int nap;             // look-ahead kernel: ns a polling helper warp (fill, TMA, check) sleeps per poll
+  int s_smem;          // blocked kernel in gmode: the prefix sums S still fit in shared memory
 };
 
 // Ring entries for steps t0 .. t0+31 (one per lane): Philox draw, two weighted inverse-CDF
@@ -388,7 +389,7 @@ __device__ __forceinline__ double warp_reduce_scatter(double (&x)[NVP], int lane
 }
 
 template <int CC, int U, int B>
-__global__ void __launch_bounds__(256, 1) rk_rgs_block_kernel(RkParams p) {
+__global__ void __launch_bounds__(512, 1) rk_rgs_block_kernel(RkParams p) {
   using K = RkBlk<B>;
   static_assert(K::NV <= 32, "block too large for one warp reduce-scatter");
   constexpr int NVP = K::NV <= 4 ? 4 : (K::NV <= 8 ? 8 : (K::NV <= 16 ? 16 : 32));
@@ -401,27 +402,39 @@ __global__ void __launch_bounds__(256, 1) rk_rgs_block_kernel(RkParams p) {
   const int NS = p.nslots, SP = p.slicepad;
   const bool stopped = *(volatile int32_t*)&p.st->inner_conv != 0;
 
+  // gmode (long row slices with large n, e.g. c2): z, the prefix sums and the b_hat / 1/N tables stay
+  // in global memory (L2) so that two slots of 2B column slices fit; z is then updated by rank 0 only
+  const bool gm = p.gmode != 0;
   double* slots = reinterpret_cast<double*>(smem_raw);                 // [NS][2B][slicepad]
-  double* zs = slots + (size_t)NS * 2 * B * SP;                        // [npad]
-  uint64_t* Ss = reinterpret_cast<uint64_t*>(zs + p.npad);             // [n]
-  RkIdx* ring = reinterpret_cast<RkIdx*>(Ss + ((p.n + 1) & ~1));       // [RK_RING]
+  const bool s_sm = !gm || p.s_smem;   // the sampler's prefix sums in shared memory
+  double* zsm = slots + (size_t)NS * 2 * B * SP;                       // [npad] (not gmode)
+  uint64_t* Ssm = reinterpret_cast<uint64_t*>(zsm + (gm ? 0 : p.npad));   // [n] (s_sm)
+  RkIdx* ring = reinterpret_cast<RkIdx*>(Ssm + (s_sm ? ((p.n + 1) & ~1) : 0));   // [RK_RING]
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + RK_RING);        // [NS]
-  double* bh_tab = reinterpret_cast<double*>(bars + 8);                 // [n] b_hat
-  double* rn_tab = bh_tab + ((p.n + 1) & ~1);                          // [n] 1 / N
-  __shared__ __align__(16) double wred[2][8][32];
+  double* bh_sm = reinterpret_cast<double*>(bars + 8);                  // [n] b_hat (not gmode)
+  double* rn_sm = bh_sm + ((p.n + 1) & ~1);                            // [n] 1 / N (not gmode)
+  double* zs = gm ? p.Z : zsm;
+  const uint64_t* Ss = s_sm ? Ssm : p.S;
+  const double* bh_tab = gm ? nullptr : bh_sm;
+  const double* rn_tab = gm ? nullptr : rn_sm;
+  const bool zowner = !gm || rank == 0;   // gmode: one CTA applies the z updates to the global z
+  __shared__ __align__(16) double wred[2][RK_MAXW][32];
   __shared__ __align__(16) double recv1[2][RK_MAXC][32];   // [source rank][value]
   __shared__ __align__(8) uint64_t bar1[2];
-  __shared__ double chkw[8];
-  __shared__ __align__(16) double tots[8][32];
+  __shared__ double chkw[RK_MAXW];
+  __shared__ __align__(16) double tots[RK_MAXW][32];
   __shared__ double bnorm_s;
   if (stopped) return;
 
-  for (int64_t j = tid; j < p.npad; j += NT) zs[j] = p.Z[j];
-  for (int j = tid; j < p.n; j += NT) {
-    Ss[j] = p.S[j];
-    bh_tab[j] = p.bhat[j];
-    rn_tab[j] = 1.0 / p.N[j];
+  if (!gm) {
+    for (int64_t j = tid; j < p.npad; j += NT) zsm[j] = p.Z[j];
+    for (int j = tid; j < p.n; j += NT) {
+      bh_sm[j] = p.bhat[j];
+      rn_sm[j] = 1.0 / p.N[j];
+    }
   }
+  if (s_sm)
+    for (int j = tid; j < p.n; j += NT) Ssm[j] = p.S[j];
   for (int64_t e = tid; e < (int64_t)NS * 2 * B * SP; e += NT) slots[e] = 0.0;
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
@@ -569,7 +582,7 @@ __global__ void __launch_bounds__(256, 1) rk_rgs_block_kernel(RkParams p) {
           for (int c = 0; c < CC; ++c) st_async_v2f64(map_shared_rank(la, (uint32_t)c), v0, v1, map_shared_rank(lb, (uint32_t)c));
       }
       // deferred z updates of the previous block (sequential order), hidden in the reduction wait
-      if (warp == NW - 1 && lane == 0 && blk > 0) {
+      if (warp == NW - 1 && lane == 0 && blk > 0 && zowner) {
 #pragma unroll
         for (int i = 0; i < B; ++i) zs[ring[(t - B + i) & (RK_RING - 1)].j2] += zprev[i];
       }
@@ -640,7 +653,7 @@ __global__ void __launch_bounds__(256, 1) rk_rgs_block_kernel(RkParams p) {
       if (CC > 1) {
 #pragma unroll
         for (int i = 0; i < B; ++i) zprev[i] = s2[i];
-      } else {
+      } else if (zowner) {
 #pragma unroll
         for (int i = 0; i < B; ++i) zs[ring[(t + i) & (RK_RING - 1)].j2] += s2[i];
       }
@@ -652,7 +665,7 @@ __global__ void __launch_bounds__(256, 1) rk_rgs_block_kernel(RkParams p) {
     RKP(7)
   }
 #undef RKP
-  if (CC > 1 && warp == NW - 1 && lane == 0 && nblk > 0) {
+  if (CC > 1 && warp == NW - 1 && lane == 0 && nblk > 0 && zowner) {
     const int64_t tl = p.t0 + (nblk - 1) * B;
 #pragma unroll
     for (int i = 0; i < B; ++i) zs[ring[(tl + i) & (RK_RING - 1)].j2] += zprev[i];
@@ -668,7 +681,7 @@ __global__ void __launch_bounds__(256, 1) rk_rgs_block_kernel(RkParams p) {
     }
   }
   __syncthreads();
-  if (rank == 0)
+  if (rank == 0 && !gm)
     for (int64_t j = tid; j < p.npad; j += NT) p.Z[j] = zs[j];
   if (CC > 1) cluster_sync_all();
 }
@@ -1651,6 +1664,7 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
   }
   int U = 8, nt = 32;
   bool blocked = false;
+  int Bsel = Bk;   // steps per reduction of the blocked kernel actually launched
   size_t smem = 0;
   for (;;) {
     p.C = C;
@@ -1670,14 +1684,35 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
     p.slicepad = U * nt;
     const size_t fixed = (size_t)h.npad * 8 + (size_t)((h.n + 1) & ~1) * 8 + RK_RING * sizeof(RkIdx) + 16 * 8 + 256;
     const size_t budget = 200 * 1024;
-    const size_t slot1 = (size_t)2 * p.slicepad * 8, slot4 = (size_t)Bk * slot1;
+    const size_t slot1 = (size_t)2 * p.slicepad * 8;
     const size_t fixed4 = fixed + 64 + (size_t)2 * ((h.n + 1) & ~1) * 8;   // + b_hat, 1/N tables
-    blocked = !h.rk_single_step && !h.large && Bk > 1 && nt <= 256 && fixed4 + 2 * slot4 <= budget;
-    // large n: z and the prefix sums do not fit next to two slots -> keep them in global memory
-    p.gmode = (!blocked && (h.large || fixed + 2 * slot1 > budget)) ? 1 : 0;
     const size_t fixed_g = (size_t)RK_RING * sizeof(RkIdx) + 16 * 8 + 256;
-    const size_t slot_bytes = blocked ? slot4 : slot1;
-    const size_t fixed_used = blocked ? fixed4 : (p.gmode ? fixed_g : fixed);
+    // blocked kernel (B steps per cluster reduction): with z / sampling tables in shared memory when
+    // two slots of 2B column slices fit next to them, else (long slices at large n, e.g. c2) with
+    // those tables in global memory (gmode) and the largest B whose two slots fit; else one step
+    // per reduction (rk_rgs_kernel; z in global memory when it does not fit either)
+    blocked = false;
+    p.gmode = 0;
+    Bsel = Bk;
+    if (!h.rk_single_step && Bk > 1 && nt <= 512) {
+      if (!h.large && fixed4 + 2 * (size_t)Bk * slot1 <= budget) {
+        blocked = true;
+      } else {
+        for (int bb = Bk; bb >= 2 && !blocked; bb /= 2)
+          if (fixed_g + 2 * (size_t)bb * slot1 <= budget) {
+            blocked = true;
+            p.gmode = 1;
+            Bsel = bb;
+          }
+      }
+    }
+    if (!blocked) p.gmode = (h.large || fixed + 2 * slot1 > budget) ? 1 : 0;
+    // gmode blocked: keep the sampler's prefix sums in shared memory when they fit (the fill warp's
+    // binary search then runs on shared memory instead of dependent L2 loads)
+    const size_t s_bytes = (size_t)((h.n + 1) & ~1) * 8;
+    p.s_smem = (blocked && p.gmode && fixed_g + s_bytes + 2 * (size_t)Bsel * slot1 <= budget) ? 1 : 0;
+    const size_t slot_bytes = blocked ? (size_t)Bsel * slot1 : slot1;
+    const size_t fixed_used = p.gmode ? fixed_g + (p.s_smem ? s_bytes : 0) : (blocked ? fixed4 : fixed);
     if (fixed_used + 2 * slot_bytes > budget) {
       set_error("RK-RGS: shared memory too small for this problem size");
       return ILS_ERR_UNSUPPORTED;
@@ -1700,7 +1735,8 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
       a.val.clusterDim.z = 1;
       cfg.attrs = &a;
       cfg.numAttrs = 1;
-      void* kern = blocked ? ((U == 2) ? (void*)rk_rgs_block_kernel<16, 2, 4>
+      void* kern = blocked ? ((Bsel == 2) ? ((U == 4) ? (void*)rk_rgs_block_kernel<16, 4, 2> : (void*)rk_rgs_block_kernel<16, 8, 2>)
+                              : (U == 2) ? (void*)rk_rgs_block_kernel<16, 2, 4>
                               : (U == 4) ? (void*)rk_rgs_block_kernel<16, 4, 4> : (void*)rk_rgs_block_kernel<16, 8, 4>)
                            : ((U == 4) ? (void*)rk_rgs_kernel<16, 4> : (void*)rk_rgs_kernel<16, 8>);
       cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1724,10 +1760,10 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
   size_t smem_la = 0;
   {
     const char* e = getenv("ILS_RK_LA");
-    if (!(e && e[0] == '0') && blocked && C == 16 && Bk == 4 && (U == 2 || U == 4 || U == 8) && nt + 160 <= 384 && !h.large &&
+    if (!(e && e[0] == '0') && blocked && !p.gmode && C == 16 && Bsel == 4 && (U == 2 || U == 4 || U == 8) && nt + 160 <= 384 && !h.large &&
         !h.sparse) {
       // the Gram ring replaces one column slot when both do not fit (>= 3 slots: blocks i .. i+2 live)
-      const size_t ring_bytes = (size_t)LA_GR * LA_NG * sizeof(double), slot_la = (size_t)2 * Bk * p.slicepad * 8;
+      const size_t ring_bytes = (size_t)LA_GR * LA_NG * sizeof(double), slot_la = (size_t)2 * Bsel * p.slicepad * 8;
       smem_la = smem + ring_bytes;
       const size_t cap = 227 * 1024 - 16 * 1024;   // the kernel's static shared memory (~15.4 KB) counts too
       while (smem_la > cap && p.nslots > 4) {
@@ -1828,7 +1864,7 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
     const int64_t t1 = (t + ce < max_inner) ? t + ce : max_inner;
     p.t0 = t;
     p.t1 = t1;
-    const int r = blocked ? dispatch_rkb(h, p, U, Bk, nt, smem)
+    const int r = blocked ? dispatch_rkb(h, p, U, Bsel, nt, smem)
                             : ((U == 8) ? dispatch_rk_c<8>(h, p, nt, smem) : dispatch_rk_c<4>(h, p, nt, smem));
     if (r) return r;
     t = t1;
@@ -1857,7 +1893,7 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
     long long hp[16 * 16];
     ILS_CU(cudaMemcpy(hp, prof, sizeof(hp), cudaMemcpyDeviceToHost));
     cudaFree(prof);
-    const double nb = (double)((steps + Bk - 1) / Bk);
+    const double nb = (double)((steps + Bsel - 1) / Bsel);
     for (int rk = 0; rk < p.C; ++rk) {
       const long long* q = hp + rk * 8;
       if (la)   // look-ahead kernel phases on compute thread 0 (LAP indices in rk_rgs_la_kernel)

@@ -166,13 +166,17 @@ def test_c3_full_size_scd_mode_f(c3, c3_handle, kw):
 
 
 # ------------------------------------------------------------------ kernel instantiations
-def test_rk_forced_large_u8_gmode(monkeypatch):
+@pytest.mark.parametrize("single,T,ce", [("0", 3000, 1000), ("0", 2999, 997), ("1", 3000, 1000)])
+def test_rk_forced_large_u8_gmode(single, T, ce, monkeypatch):
     """p > 32768 with forced-large routing: the slice exceeds 2048 rows, so U = 8 rows per thread
-    with z and the prefix sums in global memory (`rk_rgs_kernel<16,8>` gmode) -- the kernel the
-    paper's Tables 3-5 sizes run (p = 40000-60000)."""
+    with z and the prefix sums in global memory (gmode) -- the geometry the paper's Tables 3-5 sizes
+    and c2 run (p = 40000-60000): the blocked kernel with B steps per cluster reduction
+    (`rk_rgs_block_kernel<16,8,B>` gmode; T, ce not multiples of B mask the tail steps) and, with
+    ILS_RK_SINGLE_STEP=1, the one-step kernel (`rk_rgs_kernel<16,8>` gmode)."""
     monkeypatch.setenv("ILS_FORCE_LARGE", "1")
+    monkeypatch.setenv("ILS_RK_SINGLE_STEP", single)
     pr = make_dense(40000, 500, 300, 0.4, noise=0.05, seed=61)
-    _mode_f(pr, (pr.A1, pr.A2, pr.b1, pr.b2), "rk", K=2, T=3000, ce=1000, seed=3)
+    _mode_f(pr, (pr.A1, pr.A2, pr.b1, pr.b2), "rk", K=2, T=T, ce=ce, seed=3)
 
 
 def test_rk_single_step_kernel_16cta(monkeypatch):
