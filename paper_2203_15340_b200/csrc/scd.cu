@@ -237,8 +237,15 @@ __global__ void __launch_bounds__(256) scd_masks_fwd_kernel(uint64_t seed, uint3
     T[x] = (uint16_t)(mix32((x & msk) ^ e.key[x >> h]) & msk);
   __syncthreads();
   const uint32_t alpha = e.alpha, nu = (uint32_t)n, nt = (uint32_t)NT;
+  // word and bit of coordinate y: y % NT, y / NT (shift and mask when NT is a power of two)
+  const bool pow2 = (nt & (nt - 1)) == 0;
+  const uint32_t lg = 31u - (uint32_t)__clz((int)nt), ntm = nt - 1u;
+  auto mark = [&](uint32_t y) {
+    if (pow2) atomicOr(&mwords[y & ntm], 1u << (y >> lg));
+    else atomicOr(&mwords[y % nt], 1u << (y / nt));
+  };
   if (alpha >= nu) {   // tau_u = [n]
-    for (uint32_t s = threadIdx.x; s < nu; s += blockDim.x) atomicOr(&mwords[s % nt], 1u << (s / nt));
+    for (uint32_t s = threadIdx.x; s < nu; s += blockDim.x) mark(s);
   } else {
     uint32_t i = threadIdx.x, y = threadIdx.x;
     while (i < alpha) {
@@ -251,7 +258,7 @@ __global__ void __launch_bounds__(256) scd_masks_fwd_kernel(uint64_t seed, uint3
       }
       y = (L << h) | R;
       if (y < nu) {   // pi(i) = y
-        atomicOr(&mwords[y % nt], 1u << (y / nt));
+        mark(y);
         i += blockDim.x;
         y = i;
       }
