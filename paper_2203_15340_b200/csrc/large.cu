@@ -39,16 +39,23 @@ __global__ void __launch_bounds__(256) cols_kernel(const double* __restrict__ X,
     const int64_t j = j0 + lane;
     double s = 0.0;
     if (j < cols) {   // tri_lower: X[i][j] = 0 for i < j, so rows start at the tile's first column
-      double s1 = 0.0, s2 = 0.0, s3 = 0.0;   // four rows in flight per warp
+      // eight rows in flight per warp (all eight loads issued before the first fma)
+      double a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = 0.0;
       int64_t i = (tri_lower ? j0 : 0) + warp;
-      for (; i + 24 < rows; i += 32) {
-        s = fma(X[i * ldx + j], y[i], s);
-        s1 = fma(X[(i + 8) * ldx + j], y[i + 8], s1);
-        s2 = fma(X[(i + 16) * ldx + j], y[i + 16], s2);
-        s3 = fma(X[(i + 24) * ldx + j], y[i + 24], s3);
+      for (; i + 56 < rows; i += 64) {
+        double xv[8], yv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          xv[u] = __ldcs(X + (i + 8 * u) * ldx + j);
+          yv[u] = __ldg(y + i + 8 * u);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = fma(xv[u], yv[u], a[u]);
       }
-      for (; i < rows; i += 8) s = fma(X[i * ldx + j], y[i], s);
-      s = (s + s1) + (s2 + s3);
+      for (; i < rows; i += 8) a[0] = fma(X[i * ldx + j], y[i], a[0]);
+      s = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     }
     part[warp][lane] = s;
     __syncthreads();
@@ -69,21 +76,29 @@ __global__ void __launch_bounds__(256) tri_rows_kernel(const double* __restrict_
   for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < m; i += (int64_t)gridDim.x * 8) {
     const double2* tr = reinterpret_cast<const double2*>(T + i * ld);
     const int64_t k1 = (i >> 1) + 1;   // double2 entries covering columns 0..i (i + 1 is zero if present)
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    double a8[8];   // four 16-byte loads of the row in flight per lane
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a8[u] = 0.0;
     int64_t k = lane;
-    for (; k + 32 < k1; k += 64) {
-      const double2 v = __ldcs(tr + k), w = __ldcs(tr + k + 32), a = __ldg(c2 + k), b = __ldg(c2 + k + 32);
-      s0 = fma(v.x, a.x, s0);
-      s1 = fma(v.y, a.y, s1);
-      s2 = fma(w.x, b.x, s2);
-      s3 = fma(w.y, b.y, s3);
+    for (; k + 96 < k1; k += 128) {
+      double2 tv[4], cv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        tv[u] = __ldcs(tr + k + 32 * u);
+        cv[u] = __ldg(c2 + k + 32 * u);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a8[2 * u] = fma(tv[u].x, cv[u].x, a8[2 * u]);
+        a8[2 * u + 1] = fma(tv[u].y, cv[u].y, a8[2 * u + 1]);
+      }
     }
-    if (k < k1) {
+    for (; k < k1; k += 32) {
       const double2 v = __ldcs(tr + k), a = __ldg(c2 + k);
-      s0 = fma(v.x, a.x, s0);
-      s1 = fma(v.y, a.y, s1);
+      a8[0] = fma(v.x, a.x, a8[0]);
+      a8[1] = fma(v.y, a.y, a8[1]);
     }
-    const double s = warp_sum((s0 + s1) + (s2 + s3));
+    const double s = warp_sum(((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7])));
     if (lane == 0) y[i] = s;
   }
 }
