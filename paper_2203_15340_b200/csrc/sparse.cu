@@ -227,6 +227,119 @@ __global__ void __launch_bounds__(256) sparse_gram_kernel(const int64_t* __restr
   for (int64_t k = threadIdx.x; k < npad; k += blockDim.x) grow[k] = gs[k];
 }
 
+// The same Gram row, with the dependent global loads taken off the applying warp (default; the
+// kernel above is kept as ILS_SPGRAM_OLD=1). Entries of column j are handled in chunks of GS_EC:
+//   (1) every thread loads one entry's row i, value v and row extent [rp[i], rp[i+1]) (two dependent
+//       loads, all entries at once), then a block scan of the extents gives each entry's offset in
+//       the chunk's contribution list;
+//   (2) the contributions (k, a_ik) are loaded by all threads into shared memory, in windows of
+//       ccap (an entry's row may straddle two windows);
+//   (3) warp 0 applies them in stored entry order, a row's contributions lane-parallel (distinct k
+//       within a row), __syncwarp between rows -- the same per-address fma order as the kernel above,
+//       so G is bitwise identical; the next row's (k, a) are read before the current row is applied.
+constexpr int GS_EC = 256;
+constexpr int GS_T = 256;
+__global__ void __launch_bounds__(GS_T) sparse_gram_staged_kernel(
+    const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, const double* __restrict__ va, int64_t r0,
+    const int64_t* __restrict__ cptr, const int32_t* __restrict__ crow, const double* __restrict__ cval, int64_t n,
+    int64_t npad, double alpha, int accumulate, int ccap, double* __restrict__ G) {
+  extern __shared__ __align__(16) double gs[];                                    // [npad]
+  double* ca = gs + npad;                                                         // [ccap]
+  int32_t* ck = reinterpret_cast<int32_t*>(ca + ccap);                            // [ccap]
+  __shared__ double ev[GS_EC];
+  __shared__ int64_t ers[GS_EC];
+  __shared__ int32_t eoff[GS_EC + 1];
+  __shared__ int32_t wsum[GS_T / 32];
+  const int64_t j = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* grow = G + j * npad;
+  if (j >= n) {
+    if (!accumulate)
+      for (int64_t k = tid; k < npad; k += GS_T) grow[k] = (k == j) ? 1.0 : 0.0;
+    return;
+  }
+  for (int64_t k = tid; k < npad; k += GS_T) gs[k] = accumulate ? grow[k] : 0.0;
+  const int64_t e0 = cptr[j], e1 = cptr[j + 1];
+  for (int64_t b = e0; b < e1; b += GS_EC) {
+    const int cnt = (int)((e1 - b) < GS_EC ? (e1 - b) : GS_EC);
+    int len = 0;
+    if (tid < cnt) {
+      const int64_t i = r0 + crow[b + tid];
+      ev[tid] = alpha * cval[b + tid];
+      const int64_t f0 = rp[i];
+      ers[tid] = f0;
+      len = (int)(rp[i + 1] - f0);
+    }
+    // exclusive block scan of the extents
+    int x = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();   // also: the previous chunk's apply is complete (ev / ers / eoff reusable below)
+    int wb = 0;
+#pragma unroll
+    for (int w = 0; w < GS_T / 32; ++w) wb += (w < warp) ? wsum[w] : 0;
+    if (tid < GS_EC) eoff[tid] = wb + x - len;
+    if (tid == GS_T - 1) eoff[GS_EC] = wb + x;
+    __syncthreads();
+    const int total = eoff[GS_EC];
+    int ebeg = 0;   // first entry overlapping the current window (warp 0's cursor)
+    for (int c0 = 0; c0 < total; c0 += ccap) {
+      const int c1 = (c0 + ccap < total) ? c0 + ccap : total;
+      for (int f = c0 + tid; f < c1; f += GS_T) {   // entry of contribution f: last e with eoff[e] <= f
+        int lo = 0, hi = cnt - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (eoff[mid] <= f) lo = mid; else hi = mid - 1;
+        }
+        const int64_t g = ers[lo] + (f - eoff[lo]);
+        ck[f - c0] = ci[g];
+        ca[f - c0] = va[g];
+      }
+      __syncthreads();
+      if (warp == 0) {
+        int e = ebeg;
+        while (e < cnt && eoff[e + 1] <= c0) ++e;   // empty rows / rows finished in the last window
+        // software pipeline: (k, a) of row e read before row e - 1 is applied
+        auto fetch = [&](int ee, int& k, double& a, double& v, int& lo2, int& hi2) {
+          lo2 = eoff[ee] > c0 ? eoff[ee] : c0;
+          hi2 = eoff[ee + 1] < c1 ? eoff[ee + 1] : c1;
+          v = ev[ee];
+          const int f = lo2 + lane;
+          k = (f < hi2) ? ck[f - c0] : -1;
+          a = (f < hi2) ? ca[f - c0] : 0.0;
+        };
+        int k = -1, lo2 = 0, hi2 = 0;
+        double a = 0.0, v = 0.0;
+        if (e < cnt && eoff[e] < c1) fetch(e, k, a, v, lo2, hi2);
+        while (e < cnt && eoff[e] < c1) {
+          int kn = -1, lon = 0, hin = 0;
+          double an = 0.0, vn = 0.0;
+          const bool more = (e + 1 < cnt) && eoff[e + 1] < c1;
+          if (more) fetch(e + 1, kn, an, vn, lon, hin);
+          if (k >= 0) gs[k] = fma(v, a, gs[k]);
+          for (int f = lo2 + 32 + lane; f < hi2; f += 32) gs[ck[f - c0]] = fma(v, ca[f - c0], gs[ck[f - c0]]);
+          __syncwarp();
+          if (eoff[e + 1] > c1) break;   // row continues in the next window
+          ++e;
+          k = kn;
+          a = an;
+          v = vn;
+          lo2 = lon;
+          hi2 = hin;
+        }
+        ebeg = e;
+      }
+      __syncthreads();   // window consumed
+    }
+  }
+  __syncthreads();
+  for (int64_t k = tid; k < npad; k += GS_T) grow[k] = gs[k];
+}
+
 // ---------------------------------------------------------------------------------------------
 // right-hand-side stream
 // y[i - r0] = sigma_i (A_i x - b_i), sigma = -1 for i < psig (A1 rows of the full residual)
@@ -335,25 +448,42 @@ int sparse_ingest(Handle& h, int32_t* d_flag, bool* ok) {
   return ILS_OK;
 }
 
-// dense A1bar (alpha = 1) or M = A1bar - A2^T A2 (into a caller buffer) from the CSR/CSC arrays
-int sparse_gram(Handle& h, double* G, bool subtract_a2) {
+// Gram rows G[j][:] (+)= alpha * sum over the CSC entries of column j (rows r0 + i of the CSR) --
+// the staged kernel by default, the one-warp kernel with ILS_SPGRAM_OLD=1
+static int launch_sparse_gram(Handle& h, int64_t r0, const int64_t* cptr, const int32_t* crow, const double* cval,
+                              double alpha, int accumulate, double* G) {
   const cudaStream_t st = h.stream;
-  const size_t smem = (size_t)h.npad * sizeof(double);
-  if (smem > 227 * 1024) {
+  const size_t row = (size_t)h.npad * sizeof(double);
+  const size_t limit = 227 * 1024 - 6 * 1024;   // dynamic part; the staged kernel's static arrays ~5.2 KB
+  const char* ev = getenv("ILS_SPGRAM_OLD");
+  const bool old = ev && ev[0] == '1';
+  if (!old && row + 256 * 12 <= limit) {
+    int64_t ccap = (int64_t)((limit - row) / 12);
+    if (ccap > 8192) ccap = 8192;
+    const char* ec = getenv("ILS_SPGRAM_CCAP");   // test knob: a small window (rows straddling windows)
+    if (ec && atoi(ec) > 0 && atoi(ec) < ccap) ccap = atoi(ec);
+    const size_t smem = row + (size_t)ccap * 12;
+    ILS_CU(cudaFuncSetAttribute(sparse_gram_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    sparse_gram_staged_kernel<<<(unsigned)h.npad, GS_T, smem, st>>>(h.rp, h.ci, h.va, r0, cptr, crow, cval, h.n, h.npad,
+                                                                    alpha, accumulate, (int)ccap, G);
+    ILS_LAUNCHED("sparse_gram_staged_kernel");
+    return ILS_OK;
+  }
+  if (row > 227 * 1024) {
     set_error("sparse path: n > 29000 does not fit the shared-memory Gram row");
     return ILS_ERR_UNSUPPORTED;
   }
-  ILS_CU(cudaFuncSetAttribute(sparse_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if (!subtract_a2) {
-    sparse_gram_kernel<<<(unsigned)h.npad, 256, smem, st>>>(h.rp, h.ci, h.va, 0, h.cp1, h.cr1, h.cv1, h.n, h.npad, 1.0,
-                                                            0, G);
-    ILS_LAUNCHED("sparse_gram_kernel");
-  } else {
-    sparse_gram_kernel<<<(unsigned)h.npad, 256, smem, st>>>(h.rp, h.ci, h.va, h.p, h.cp2, h.cr2, h.cv2, h.n, h.npad,
-                                                            -1.0, 1, G);
-    ILS_LAUNCHED("sparse_gram_kernel");
-  }
+  ILS_CU(cudaFuncSetAttribute(sparse_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row));
+  sparse_gram_kernel<<<(unsigned)h.npad, 256, row, st>>>(h.rp, h.ci, h.va, r0, cptr, crow, cval, h.n, h.npad, alpha,
+                                                         accumulate, G);
+  ILS_LAUNCHED("sparse_gram_kernel");
   return ILS_OK;
+}
+
+// dense A1bar (alpha = 1) or M = A1bar - A2^T A2 (into a caller buffer) from the CSR/CSC arrays
+int sparse_gram(Handle& h, double* G, bool subtract_a2) {
+  if (!subtract_a2) return launch_sparse_gram(h, 0, h.cp1, h.cr1, h.cv1, 1.0, 0, G);
+  return launch_sparse_gram(h, h.p, h.cp2, h.cr2, h.cv2, -1.0, 1, G);
 }
 
 __global__ void neg_copy_kernel(const double* __restrict__ x, int64_t len, double* __restrict__ y) {
@@ -371,15 +501,8 @@ __global__ void zero_pad_diag_kernel(double* __restrict__ G, int64_t n, int64_t 
 // column pass over -b2.
 int sparse_a2bar(Handle& h, double* A2bar, double* ajb) {
   const cudaStream_t st = h.stream;
-  const size_t smem = (size_t)h.npad * sizeof(double);
-  if (smem > 227 * 1024) {
-    set_error("sparse path: n > 29000 does not fit the shared-memory Gram row");
-    return ILS_ERR_UNSUPPORTED;
-  }
-  ILS_CU(cudaFuncSetAttribute(sparse_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  sparse_gram_kernel<<<(unsigned)h.npad, 256, smem, st>>>(h.rp, h.ci, h.va, h.p, h.cp2, h.cr2, h.cv2, h.n, h.npad, 1.0,
-                                                          0, A2bar);
-  ILS_LAUNCHED("sparse_gram_kernel");
+  int rc = launch_sparse_gram(h, h.p, h.cp2, h.cr2, h.cv2, 1.0, 0, A2bar);
+  if (rc) return rc;
   if (h.npad > h.n) {   // the Gram kernel writes identity rows for the padding: A2bar is zero there
     zero_pad_diag_kernel<<<1, 64, 0, st>>>(A2bar, h.n, h.npad);
     ILS_LAUNCHED("zero_pad_diag_kernel");
@@ -947,6 +1070,360 @@ __global__ void __launch_bounds__(SRK_T) sparse_rk_la_kernel(SpRkParams p) {
 #undef SLAP
 }
 
+// ---------------------------------------------------------------------------------------------
+// 16-CTA cluster SP-RK-RGS on CSR input (default when the sampling table fits shared memory;
+// ILS_SRK_CL=0 keeps the one-CTA look-ahead kernel). CTA c owns rows [c R, (c + 1) R) of w and r
+// (global memory, L2-resident); the entries of a column inside those rows are one contiguous range
+// of the row-sorted CSC (split table: one lower_bound per column and CTA, built once per handle).
+// B = 4 steps per cluster exchange with the blocked recurrence of rk_rgs.cu (RkBlk<4>: identical to
+// four single steps of Alg. 2 steps 9 and 11, in exact arithmetic):
+//   per block each CTA gathers w at its entries of a_k = A1_(j1_k) and r at those of b_k = A1_(j2_k)
+//   (k < 4), forms the 8 partial inner products, sends them to all 16 CTAs (destination-uniform
+//   st.async, mbarrier complete_tx); warp 0 sums the 16 partials in rank order, adds the 22 in-block
+//   Gram values read from A1bar, runs the recurrence for s1_k, s2_k and publishes them; warp 1 then
+//   applies w += s1_k a_k and warp 2 r += s1_k a_k - s2_k b_k to the CTA's rows as floating-point
+//   reductions, column by column in step order with __syncwarp between columns (one reduction per
+//   address per column, so the result is deterministic); rank 0 adds s2_k to z_(j2_k).
+// A fill warp runs up to SRC_NS blocks ahead in rounds of SRC_NS / 2 blocks: indices (Philox +
+// weighted inverse CDF on the shared prefix sums), 1/N, b_hat, Gram values, the CTA's segment of
+// each column and its entries (row, value) copied into the block's shared-memory slot (entries past
+// SRC_CAP per block are read from global memory by the consumers).
+constexpr int SRC_C = 16, SRC_T = 256, SRC_NWC = 7, SRC_CAP = 256;
+struct SrcSlot {
+  int32_t row[SRC_CAP];
+  double val[SRC_CAP];
+  int64_t gbase[8];   // CSC index of each segment's first entry (segments a0, b0, a1, b1, ...)
+  int32_t off[9];     // segment offsets in the block's entry list
+  int32_t j1[4], j2[4];
+  double gv[22];      // in-block Gram values, RkBlk<4> order (value 8 + v)
+  double bh1[4], rn1[4], rn2[4];
+};
+
+// (value v < 22 of the in-block Gram) -> the two columns: (step, is_b) pairs in RkBlk<4> order
+// (AA(i,k) k < i, BA(i,k) k <= i, BB(i,k) k < i)
+__device__ __forceinline__ void src_gram_cols(int v, int& si, int& bi, int& sk, int& bk) {
+  if (v < 6) {            // AA: (1,0) (2,0) (2,1) (3,0) (3,1) (3,2)
+    si = v < 1 ? 1 : (v < 3 ? 2 : 3);
+    sk = v - si * (si - 1) / 2;
+    bi = 0;
+    bk = 0;
+  } else if (v < 16) {    // BA: (0,0) (1,0) (1,1) (2,0) (2,1) (2,2) (3,0) ...
+    const int w = v - 6;
+    si = w < 1 ? 0 : (w < 3 ? 1 : (w < 6 ? 2 : 3));
+    sk = w - si * (si + 1) / 2;
+    bi = 1;
+    bk = 0;
+  } else {                // BB
+    const int w = v - 16;
+    si = w < 1 ? 1 : (w < 3 ? 2 : 3);
+    sk = w - si * (si - 1) / 2;
+    bi = 1;
+    bk = 1;
+  }
+}
+
+struct SrcParams {
+  SpRkParams b;
+  const int32_t* split;   // [n][17]
+  int64_t R;              // rows per CTA
+  int ns;                 // slots (8 or 16)
+};
+
+__global__ void __launch_bounds__(SRC_T, 1) sparse_rk_cl_kernel(SrcParams q) {
+  const SpRkParams& p = q.b;
+  extern __shared__ __align__(16) unsigned char src_smem[];
+  uint64_t* Ssm = reinterpret_cast<uint64_t*>(src_smem);                                   // [n]
+  SrcSlot* slots = reinterpret_cast<SrcSlot*>(src_smem + (((size_t)p.n * 8 + 15) & ~(size_t)15));   // [ns]
+  __shared__ __align__(16) double recv[2][SRC_C][8];
+  __shared__ __align__(8) uint64_t rbar[2];
+  __shared__ __align__(8) uint64_t full[16];
+  __shared__ double part[SRC_NWC][8];
+  __shared__ double sv[2][8];
+  __shared__ __align__(8) int64_t done_s;
+  __shared__ double red0[SRC_T / 32];
+  __shared__ int zero_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = (int)cluster_ctarank();
+  const int NS = q.ns, RD = NS / 2;
+  if (*(volatile int32_t*)&p.st->inner_conv) return;   // the same flag in every CTA
+  for (int j = tid; j < p.n; j += SRC_T) Ssm[j] = p.S[j];
+  if (tid == 0) {
+    mbar_init(&rbar[0], 1);
+    mbar_init(&rbar[1], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(&rbar[0], SRC_C * 64);
+    mbar_arrive_expect_tx(&rbar[1], SRC_C * 64);
+    done_s = 0;
+    zero_s = 0;
+  }
+  if (p.t0 == 0) {   // b_hat = 0: z = 0 after 0 steps (every CTA decides the same)
+    double v = 0.0;
+    for (int j = tid; j < p.n; j += SRC_T) v = fma(p.bhat[j], p.bhat[j], v);
+    v = warp_sum(v);
+    if (lane == 0) red0[warp] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double s_ = 0.0;
+      for (int w = 0; w < SRC_T / 32; ++w) s_ += red0[w];
+      zero_s = (s_ == 0.0);
+    }
+  }
+  __syncthreads();
+  cluster_sync_all();   // barriers initialised everywhere before any remote st.async
+  if (zero_s) {
+    if (rank == 0 && tid == 0) {
+      p.st->inner_steps = 0;
+      p.st->inner_conv = 1;
+    }
+    cluster_sync_all();
+    return;
+  }
+  const int64_t nblk = (p.t1 - p.t0 + 3) / 4;
+  if (warp == SRC_NWC) {   // ---- fill warp
+    for (int64_t f = 0; f < nblk; f += RD) {
+      while (f + RD - NS > ld_acquire_cta_s64(&done_s)) {
+      }
+      const int nb = (int)((nblk - f) < RD ? (nblk - f) : RD);
+      // (1) indices: lane l -> step 4 f + l (l < 4 nb; RD <= 8)
+      int j1 = 0, j2 = 0;
+      bool live = false;
+      if (lane < 4 * nb) {
+        const int64_t t = p.t0 + 4 * f + lane;
+        live = t < p.t1;
+        double bh = 0.0, r1 = 0.0, r2 = 0.0;
+        if (live) {
+          const U4 x = draw(p.seed, p.k, (uint64_t)t, kTagRkRgs);
+          j1 = sample_weighted(((uint64_t)x.y << 32) | x.x, Ssm, p.n);
+          j2 = sample_weighted(((uint64_t)x.w << 32) | x.z, Ssm, p.n);
+          bh = p.bhat[j1];
+          r1 = 1.0 / p.N[j1];
+          r2 = 1.0 / p.N[j2];
+        }
+        SrcSlot& sl = slots[(f + lane / 4) % NS];
+        sl.j1[lane & 3] = j1;
+        sl.j2[lane & 3] = j2;
+        sl.bh1[lane & 3] = bh;
+        sl.rn1[lane & 3] = r1;
+        sl.rn2[lane & 3] = r2;
+      }
+      // (2) segments: pair (block f + u / 8, segment c = u & 7), u = lane, lane + 32
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int u = lane + 32 * h2;
+        const int bl = u >> 3, c = u & 7;
+        const int src = 4 * bl + (c >> 1);
+        const int ja = __shfl_sync(0xffffffffu, j1, src & 31), jb = __shfl_sync(0xffffffffu, j2, src & 31);
+        const bool lv = __shfl_sync(0xffffffffu, live, src & 31);
+        int len = 0;
+        int64_t g0 = 0;
+        if (bl < nb && lv) {
+          const int col = (c & 1) ? jb : ja;
+          const int64_t cb = p.cp[col];
+          const int32_t* spl = q.split + (int64_t)col * (SRC_C + 1) + rank;
+          const int32_t o0 = spl[0], o1 = spl[1];
+          g0 = cb + o0;
+          len = o1 - o0;
+        }
+        int x = len;   // inclusive scan inside the 8-lane group
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o, 8);
+          if (c >= o) x += y;
+        }
+        if (bl < nb) {
+          SrcSlot& sl = slots[(f + bl) % NS];
+          sl.gbase[c] = g0;
+          sl.off[c] = x - len;
+          if (c == 7) sl.off[8] = x;
+        }
+      }
+      __syncwarp();
+      // (3) Gram values: 22 per block
+      for (int u = lane; u < 22 * nb; u += 32) {
+        const int bl = u / 22, v = u - 22 * bl;
+        SrcSlot& sl = slots[(f + bl) % NS];
+        int si, bi, sk, bk;
+        src_gram_cols(v, si, bi, sk, bk);
+        const int ca = bi ? sl.j2[si] : sl.j1[si];
+        const int cb = bk ? sl.j2[sk] : sl.j1[sk];
+        sl.gv[v] = p.G[(int64_t)ca * p.npad + cb];
+      }
+      // (4) entries (row, value) of each block, loads batched 8 per lane
+      for (int bl = 0; bl < nb; ++bl) {
+        SrcSlot& sl = slots[(f + bl) % NS];
+        const int tot = sl.off[8] < SRC_CAP ? sl.off[8] : SRC_CAP;
+        for (int e0 = 0; e0 < tot; e0 += 256) {
+          int32_t rr[8];
+          double vv[8];
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            const int e = e0 + lane + 32 * w;
+            rr[w] = 0;
+            vv[w] = 0.0;
+            if (e < tot) {
+              int c = 0;
+#pragma unroll
+              for (int cc = 1; cc < 8; ++cc) c += (sl.off[cc] <= e);
+              const int64_t g = sl.gbase[c] + (e - sl.off[c]);
+              rr[w] = p.cr[g];
+              vv[w] = p.cv[g];
+            }
+          }
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            const int e = e0 + lane + 32 * w;
+            if (e < tot) {
+              sl.row[e] = rr[w];
+              sl.val[e] = vv[w];
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane < nb) mbar_arrive(&full[(f + lane) % NS]);
+    }
+  } else {   // ---- consumer warps (NWC x 32 threads)
+    constexpr int NTC = SRC_NWC * 32;
+    using K = RkBlk<4>;
+    for (int64_t i = 0; i < nblk; ++i) {
+      const int si = (int)(i % NS);
+      mbar_wait(&full[si], (uint32_t)((i / NS) & 1));
+      const SrcSlot& sl = slots[si];
+      const int tot = sl.off[8];
+      double acc[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+      for (int e = tid; e < tot; e += NTC) {
+        int c = 0;
+#pragma unroll
+        for (int cc = 1; cc < 8; ++cc) c += (sl.off[cc] <= e);
+        int row;
+        double v;
+        if (e < SRC_CAP) {
+          row = sl.row[e];
+          v = sl.val[e];
+        } else {
+          const int64_t g = sl.gbase[c] + (e - sl.off[c]);
+          row = p.cr[g];
+          v = p.cv[g];
+        }
+        const double xg = (c & 1) ? p.Rv[row] : p.W[row];
+        const double d = v * xg;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) acc[cc] += (c == cc) ? d : 0.0;
+      }
+      // value order of RkBlk<4>: P(k) = k (a_k, w), Q(k) = 4 + k (b_k, r); segment c = 2k + is_b
+      double accv[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        accv[K::P(k)] = acc[2 * k];
+        accv[K::Q(k)] = acc[2 * k + 1];
+      }
+      const double ws = warp_reduce_scatter<8>(accv, lane);
+      if (lane < 8) part[warp][lane] = ws;
+      named_bar_sync(1, NTC);
+      const int b2 = (int)(i & 1);
+      if (warp == 0) {
+        double v = 0.0;
+        if (lane < 8)
+#pragma unroll
+          for (int w = 0; w < SRC_NWC; ++w) v += part[w][lane];
+        double vals[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) vals[m] = __shfl_sync(0xffffffffu, v, m);
+        if (lane < SRC_C) {
+          const uint32_t bar = map_shared_rank(smem_u32(&rbar[b2]), (uint32_t)lane);
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+            st_async_v2f64(map_shared_rank(smem_u32(&recv[b2][rank][2 * m]), (uint32_t)lane), vals[2 * m],
+                           vals[2 * m + 1], bar);
+        }
+        mbar_wait_cluster(&rbar[b2], (uint32_t)((i >> 1) & 1));
+        double tv = 0.0;
+        if (lane < 8)
+#pragma unroll
+          for (int c = 0; c < SRC_C; ++c) tv += recv[b2][c][lane];
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(&rbar[b2], SRC_C * 64);   // for block i + 2
+        double T[K::NV];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) T[m] = __shfl_sync(0xffffffffu, tv, m);
+#pragma unroll
+        for (int m = 8; m < K::NV; ++m) T[m] = sl.gv[m - 8];
+        double s1[4], s2[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          double dw = T[K::P(k)];
+#pragma unroll
+          for (int m = 0; m < k; ++m) dw = fma(s1[m], T[K::AA(k, m)], dw);
+          s1[k] = (sl.bh1[k] - dw) * sl.rn1[k];
+          double dr = T[K::Q(k)];
+#pragma unroll
+          for (int m = 0; m < k; ++m) {
+            dr = fma(s1[m], T[K::BA(k, m)], dr);
+            dr = fma(-s2[m], T[K::BB(k, m)], dr);
+          }
+          dr = fma(s1[k], T[K::BA(k, k)], dr);
+          s2[k] = dr * sl.rn2[k];
+        }
+        if (lane < 4) {
+          sv[b2][lane] = s1[lane & 3];
+          sv[b2][4 + lane] = s2[lane & 3];
+        }
+      }
+      named_bar_sync(1, NTC);
+      if (warp == 1 || warp == 2) {   // w (warp 1) / r (warp 2) updates, column by column in step order
+        for (int c = 0; c < 8; ++c) {
+          if (warp == 1 && (c & 1)) continue;
+          const double sc = (c & 1) ? -sv[b2][4 + (c >> 1)] : sv[b2][c >> 1];
+          double* dst = (warp == 1) ? p.W : p.Rv;
+          for (int e = sl.off[c] + lane; e < sl.off[c + 1]; e += 32) {
+            int row;
+            double v;
+            if (e < SRC_CAP) {
+              row = sl.row[e];
+              v = sl.val[e];
+            } else {
+              const int64_t g = sl.gbase[c] + (e - sl.off[c]);
+              row = p.cr[g];
+              v = p.cv[g];
+            }
+            atomicAdd(dst + row, sc * v);
+          }
+          __syncwarp();
+        }
+      } else if (warp == 3 && lane == 0 && rank == 0) {
+        const int64_t tb = p.t0 + 4 * i;
+        for (int k = 0; k < 4; ++k)
+          if (tb + k < p.t1) atomicAdd(p.Z + sl.j2[k], sv[b2][4 + k]);
+      }
+      named_bar_sync(1, NTC);   // this block's updates precede the next block's gathers; slot free
+      if (tid == 0) st_release_cta_s64(&done_s, i + 1);
+    }
+  }
+  __syncthreads();
+  cluster_sync_all();
+}
+
+// split[j][c] = (first CSC entry of column j with row >= c R) - cp[j], c = 0..16
+__global__ void src_split_kernel(const int64_t* __restrict__ cp, const int32_t* __restrict__ cr, int64_t n, int64_t R,
+                                 int32_t* __restrict__ split) {
+  const int64_t tot = n * (SRC_C + 1);
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < tot; u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = u / (SRC_C + 1);
+    const int c = (int)(u - j * (SRC_C + 1));
+    const int64_t a = cp[j], b = cp[j + 1];
+    const int64_t key = (int64_t)c * R;
+    int64_t lo = a, hi = b;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)cr[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    split[u] = (int32_t)(lo - a);
+  }
+}
+
 __global__ void max_col_kernel(const int64_t* __restrict__ cp, int64_t n, unsigned long long* out) {
   unsigned long long m = 0;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
@@ -1008,6 +1485,88 @@ int sparse_rk_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int
     ILS_CU(cudaStreamSynchronize(st));
     cudaFreeAsync(dm, st);
     h.maxcol1 = (int64_t)hm;
+  }
+  // 16-CTA cluster kernel when the sampling table and 8+ slots fit shared memory (ILS_SRK_CL=0: the
+  // one-CTA kernels below)
+  const char* ecl = getenv("ILS_SRK_CL");
+  const size_t cl_base = (((size_t)h.n * 8 + 15) & ~(size_t)15);
+  const size_t cl_static = 8 * 1024;
+  int cl_ns = 0;
+  if (!(ecl && ecl[0] == '0')) {
+    if (cl_base + 16 * sizeof(SrcSlot) + cl_static <= 227 * 1024) cl_ns = 16;
+    else if (cl_base + 8 * sizeof(SrcSlot) + cl_static <= 227 * 1024) cl_ns = 8;
+  }
+  if (cl_ns) {
+    const size_t cl_smem = cl_base + (size_t)cl_ns * sizeof(SrcSlot);
+    const int64_t R = (h.p + SRC_C - 1) / SRC_C;
+    if (!h.sp_split) {
+      ILS_CU(cudaMallocAsync(&h.sp_split, (size_t)h.n * (SRC_C + 1) * sizeof(int32_t), st));
+      src_split_kernel<<<grid_for(h.n * (SRC_C + 1), 256), 256, 0, st>>>(h.cp1, h.cr1, h.n, R, h.sp_split);
+      ILS_LAUNCHED("src_split_kernel");
+    }
+    SrcParams q{};
+    q.b = prm;
+    q.split = h.sp_split;
+    q.R = R;
+    q.ns = cl_ns;
+    ILS_CU(cudaFuncSetAttribute(sparse_rk_cl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cl_smem));
+    ILS_CU(cudaFuncSetAttribute(sparse_rk_cl_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(SRC_C);
+    cfg.blockDim = dim3(SRC_T);
+    cfg.dynamicSmemBytes = cl_smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = SRC_C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ILS_CU(cudaEventRecord(h.evk0, st));
+    int64_t t = 0;
+    int pending = 0;
+    while (t < max_inner) {
+      const int64_t t1 = (t + ce < max_inner) ? t + ce : max_inner;
+      q.b.t0 = t;
+      q.b.t1 = t1;
+      ILS_CU(cudaLaunchKernelEx(&cfg, sparse_rk_cl_kernel, q));
+      ILS_LAUNCHED("sparse_rk_cl_kernel");
+      t = t1;
+      if (t % ce == 0) {
+        double itol = inner_tol;
+        int64_t tn = t;
+        const int64_t prow = h.p, nn = h.n;
+        const int64_t* rp = h.rp;
+        const int32_t* ci = h.ci;
+        const double* va = h.va;
+        const int64_t* cp = h.cp1;
+        const int32_t* cr = h.cr1;
+        const double* cv = h.cv1;
+        DevStatus* dst = h.dstat;
+        void* args[] = {(void*)&rp, (void*)&ci, (void*)&va, (void*)&prow, (void*)&cp, (void*)&cr, (void*)&cv,
+                        (void*)&nn, (void*)&bhat, (void*)&Z, (void*)&W, (void*)&Rv, (void*)&AZ, (void*)&red,
+                        (void*)&itol, (void*)&tn, (void*)&dst};
+        ILS_CU(cudaLaunchCooperativeKernel((void*)sparse_rk_check_kernel, dim3(h.num_sms), dim3(256), args, 0, st));
+        ILS_LAUNCHED("sparse_rk_check_kernel");
+      }
+      if (++pending == 8 || t >= max_inner) {
+        ILS_CU(cudaMemcpyAsync(h.hstat, h.dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+        ILS_CU(cudaStreamSynchronize(st));
+        pending = 0;
+        if (h.hstat->inner_conv) break;
+      }
+    }
+    ILS_CU(cudaEventRecord(h.evk1, st));
+    ILS_CU(cudaMemcpyAsync(z, Z, h.npad * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    ILS_CU(cudaMemcpyAsync(h.hstat, h.dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+    ILS_CU(cudaStreamSynchronize(st));
+    const int64_t steps = h.hstat->inner_conv ? h.hstat->inner_steps : max_inner;
+    if (steps_out) *steps_out = steps;
+    const double nnz1 = (double)h.nnz1;
+    hot_account(h, 1, (double)steps * 2.0 * (nnz1 / (double)h.n) * 28.0 + (double)(steps / ce) * 24.0 * nnz1,
+                (steps + ce - 1) / ce);
+    return ILS_OK;
   }
   // look-ahead kernel when every column is staged whole (ILS_SRK_LA=0 keeps the one-step kernel)
   const char* ela = getenv("ILS_SRK_LA");

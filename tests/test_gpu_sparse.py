@@ -252,3 +252,33 @@ def test_sparse_literal_precompute_forms(method, shape):
         assert rep.sp_form_used == 2
     for kk in range(K):
         assert _par(hist[kk], ref.x_hist[kk]) <= 1e-9, kk
+
+
+@pytest.mark.parametrize("shape", [(3000, 200, 20, 5), (600, 120, 80, 6), (257, 33, 31, 5)])
+def test_sparse_gram_staged_bitwise(shape, monkeypatch):
+    """The staged Gram-row kernel (default) against the one-warp kernel (ILS_SPGRAM_OLD=1): same
+    per-address fma order, so the SP iterates (through P built from A1bar) are bitwise equal, also
+    with a 7-contribution window (rows straddling windows, ILS_SPGRAM_CCAP=7) and columns longer than
+    one 256-entry chunk (3000 rows x 5 nnz over 20 columns: ~750 entries per column); and within
+    1e-9 of the oracle."""
+    p, q, n, k = shape
+    pr = make_sparse(p, q, n, k, seed=21)
+    A1, A2, b1, b2 = _dense(pr)
+    K = 3
+    ref = O.sp_solve(A1, A2, b1, b2, max_iter=K, stop=O.STOP_NONE)
+    hists = []
+    for env in ({"ILS_SPGRAM_OLD": "1"}, {}, {"ILS_SPGRAM_CCAP": "7"}):
+        monkeypatch.delenv("ILS_SPGRAM_OLD", raising=False)
+        monkeypatch.delenv("ILS_SPGRAM_CCAP", raising=False)
+        for kk, v in env.items():
+            monkeypatch.setenv(kk, v)
+        hist = np.zeros((K, n))
+        x = np.zeros(n)
+        with HS(pr) as hh:
+            o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, x_hist=hist.ctypes.data)
+            ils.ils_sp_solve(hh.h, None, x, 0.0, K, o)
+        hists.append(hist)
+    assert np.array_equal(hists[0], hists[1])
+    assert np.array_equal(hists[0], hists[2])
+    for kk in range(K):
+        assert _par(hists[1][kk], ref.x_hist[kk]) <= 1e-9, kk
