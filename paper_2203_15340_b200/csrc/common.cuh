@@ -275,6 +275,67 @@ __device__ __forceinline__ void cluster_sync_all() {
                    : "memory");
 }
 
+// ---------------------------------------------------------------- blocked RK-RGS helpers (rk_rgs.cu, sparse.cu)
+template <int B>
+struct RkBlk {
+  static constexpr int NV = (3 * B * B + 3 * B) / 2;
+  __host__ __device__ static constexpr int P(int i) { return i; }
+  __host__ __device__ static constexpr int Q(int i) { return B + i; }
+  __host__ __device__ static constexpr int AA(int i, int k) { return 2 * B + i * (i - 1) / 2 + k; }
+  __host__ __device__ static constexpr int BA(int i, int k) { return 2 * B + B * (B - 1) / 2 + i * (i + 1) / 2 + k; }
+  __host__ __device__ static constexpr int BB(int i, int k) {
+    return 2 * B + B * (B - 1) / 2 + B * (B + 1) / 2 + i * (i - 1) / 2 + k;
+  }
+};
+
+// butterfly reduce-scatter of NVP (power of two <= 32) values over the warp: on return lane l
+// holds the warp sum of value l & (NVP - 1) (NVP - 1 + log2(32 / NVP) shuffles of doubles)
+// the butterfly levels of warp_reduce_scatter only: lane l holds value l & (NVP - 1) summed over its
+// NVP-lane group (the cross-group sum is left to the consumer)
+template <int NVP>
+__device__ __forceinline__ double warp_reduce_scatter_groups(double (&x)[NVP], int lane) {
+#pragma unroll
+  for (int half = NVP / 2; half >= 1; half /= 2) {
+    const bool hi = (lane & half) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double lo_v = x[i], hi_v = x[i + half];
+      const double send = hi ? lo_v : hi_v;
+      const double keep = hi ? hi_v : lo_v;
+      x[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+    }
+  }
+  return x[0];
+}
+
+template <int NVP>
+__device__ __forceinline__ double warp_reduce_scatter(double (&x)[NVP], int lane) {
+#pragma unroll
+  for (int half = NVP / 2; half >= 1; half /= 2) {
+    const bool hi = (lane & half) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double lo_v = x[i], hi_v = x[i + half];
+      const double send = hi ? lo_v : hi_v;
+      const double keep = hi ? hi_v : lo_v;
+      x[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+    }
+  }
+  double v = x[0];
+#pragma unroll
+  for (int o = NVP; o < 32; o *= 2) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ int64_t ld_acquire_cta_s64(const int64_t* a) {
+  int64_t v;
+  asm volatile("ld.acquire.cta.shared::cta.s64 %0, [%1];" : "=l"(v) : "r"(smem_u32(a)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta_s64(int64_t* a, int64_t v) {
+  asm volatile("st.release.cta.shared::cta.s64 [%0], %1;" ::"r"(smem_u32(a)), "l"(v) : "memory");
+}
+
 // ---------------------------------------------------------------- cp.async (LDGSTS)
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");

@@ -182,7 +182,7 @@ static void free_handle_impl(Handle* h) {
   if (h->scd_ws) cudaFreeAsync(h->scd_ws, s);
   {
     void* sb[] = {h->rp, h->ci, h->va, h->cp1, h->cr1, h->cv1, h->cp2, h->cr2, h->cv2, h->sp_y, h->gcsr_ptr,
-                  h->gcsr_col, h->gcsr_val};
+                  h->gcsr_col, h->gcsr_val, h->sp_split};
     for (void* q : sb)
       if (q) cudaFreeAsync(q, s);
   }

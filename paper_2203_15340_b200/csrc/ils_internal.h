@@ -93,6 +93,7 @@ struct Handle {
   int32_t* cr2 = nullptr;
   double* cv2 = nullptr;
   double* sp_y = nullptr;   // [m] row-pass scratch
+  int32_t* sp_split = nullptr;   // [n][17]: CSC entry offsets of each A1 column at the 16 row-slice bounds
   int64_t* gcsr_ptr = nullptr;   // A1bar compacted to CSR (SP-SCD)
   int32_t* gcsr_col = nullptr;
   double* gcsr_val = nullptr;

@@ -1088,7 +1088,21 @@ __global__ void __launch_bounds__(SRK_T) sparse_rk_la_kernel(SpRkParams p) {
 // weighted inverse CDF on the shared prefix sums), 1/N, b_hat, Gram values, the CTA's segment of
 // each column and its entries (row, value) copied into the block's shared-memory slot (entries past
 // SRC_CAP per block are read from global memory by the consumers).
-constexpr int SRC_C = 16, SRC_T = 256, SRC_NWC = 7, SRC_CAP = 256;
+constexpr int SRC_C = 16, SRC_T = 256, SRC_NWC = 7, SRC_CAP = 256, SRC_HB = 9;
+
+// named barrier over nthreads threads that also ORs a predicate over them
+__device__ __forceinline__ bool bar_red_or(int id, int nthreads, bool pred) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.u32 p, %1, 0;\n\t"
+      "bar.red.or.pred q, %2, %3, p;\n\t"
+      "selp.u32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"((uint32_t)pred), "r"(id), "r"(nthreads)
+      : "memory");
+  return r != 0;
+}
 struct SrcSlot {
   int32_t row[SRC_CAP];
   double val[SRC_CAP];
@@ -1138,6 +1152,7 @@ __global__ void __launch_bounds__(SRC_T, 1) sparse_rk_cl_kernel(SrcParams q) {
   __shared__ __align__(8) uint64_t rbar[2];
   __shared__ __align__(8) uint64_t full[16];
   __shared__ double part[SRC_NWC][8];
+  __shared__ unsigned long long htab[1 << SRC_HB];   // (block tag << 32) | row of the current block's entries
   __shared__ double sv[2][8];
   __shared__ __align__(8) int64_t done_s;
   __shared__ double red0[SRC_T / 32];
@@ -1147,6 +1162,7 @@ __global__ void __launch_bounds__(SRC_T, 1) sparse_rk_cl_kernel(SrcParams q) {
   const int NS = q.ns, RD = NS / 2;
   if (*(volatile int32_t*)&p.st->inner_conv) return;   // the same flag in every CTA
   for (int j = tid; j < p.n; j += SRC_T) Ssm[j] = p.S[j];
+  for (int u = tid; u < (1 << SRC_HB); u += SRC_T) htab[u] = 0ull;
   if (tid == 0) {
     mbar_init(&rbar[0], 1);
     mbar_init(&rbar[1], 1);
@@ -1181,11 +1197,14 @@ __global__ void __launch_bounds__(SRC_T, 1) sparse_rk_cl_kernel(SrcParams q) {
   }
   const int64_t nblk = (p.t1 - p.t0 + 3) / 4;
   if (warp == SRC_NWC) {   // ---- fill warp
+    long long fbusy = 0;
+    const int NSM = NS - 1;   // NS is a power of two
     for (int64_t f = 0; f < nblk; f += RD) {
       while (f + RD - NS > ld_acquire_cta_s64(&done_s)) {
       }
+      const long long fc0 = (p.prof && rank == 0) ? clock64() : 0;
       const int nb = (int)((nblk - f) < RD ? (nblk - f) : RD);
-      // (1) indices: lane l -> step 4 f + l (l < 4 nb; RD <= 8)
+      // (1) indices: lane l -> step 4 f + l (l < 4 nb; RD <= 8), the two inverse-CDF searches interleaved
       int j1 = 0, j2 = 0;
       bool live = false;
       if (lane < 4 * nb) {
@@ -1194,124 +1213,245 @@ __global__ void __launch_bounds__(SRC_T, 1) sparse_rk_cl_kernel(SrcParams q) {
         double bh = 0.0, r1 = 0.0, r2 = 0.0;
         if (live) {
           const U4 x = draw(p.seed, p.k, (uint64_t)t, kTagRkRgs);
-          j1 = sample_weighted(((uint64_t)x.y << 32) | x.x, Ssm, p.n);
-          j2 = sample_weighted(((uint64_t)x.w << 32) | x.z, Ssm, p.n);
+          const uint64_t tot = Ssm[p.n - 1];
+          const uint64_t v1 = mulhi64(((uint64_t)x.y << 32) | x.x, tot);
+          const uint64_t v2 = mulhi64(((uint64_t)x.w << 32) | x.z, tot);
+          int lo1 = 0, hi1 = p.n - 1, lo2 = 0, hi2 = p.n - 1;
+          while (lo1 < hi1 || lo2 < hi2) {   // the searches of sample_weighted, side by side
+            const int m1 = (lo1 + hi1) >> 1, m2 = (lo2 + hi2) >> 1;
+            const uint64_t s1_ = Ssm[m1], s2_ = Ssm[m2];
+            if (lo1 < hi1) {
+              if (s1_ > v1) hi1 = m1; else lo1 = m1 + 1;
+            }
+            if (lo2 < hi2) {
+              if (s2_ > v2) hi2 = m2; else lo2 = m2 + 1;
+            }
+          }
+          j1 = lo1;
+          j2 = lo2;
           bh = p.bhat[j1];
           r1 = 1.0 / p.N[j1];
           r2 = 1.0 / p.N[j2];
         }
-        SrcSlot& sl = slots[(f + lane / 4) % NS];
+        SrcSlot& sl = slots[(f + lane / 4) & NSM];
         sl.j1[lane & 3] = j1;
         sl.j2[lane & 3] = j2;
         sl.bh1[lane & 3] = bh;
         sl.rn1[lane & 3] = r1;
         sl.rn2[lane & 3] = r2;
       }
-      // (2) segments: pair (block f + u / 8, segment c = u & 7), u = lane, lane + 32
+      // (2) segments: pair (block f + u / 8, segment c = u & 7), u = lane, lane + 32 (loads of both first)
+      {
+        int64_t cb[2];
+        int32_t o0[2], o1[2];
 #pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const int u = lane + 32 * h2;
-        const int bl = u >> 3, c = u & 7;
-        const int src = 4 * bl + (c >> 1);
-        const int ja = __shfl_sync(0xffffffffu, j1, src & 31), jb = __shfl_sync(0xffffffffu, j2, src & 31);
-        const bool lv = __shfl_sync(0xffffffffu, live, src & 31);
-        int len = 0;
-        int64_t g0 = 0;
-        if (bl < nb && lv) {
-          const int col = (c & 1) ? jb : ja;
-          const int64_t cb = p.cp[col];
-          const int32_t* spl = q.split + (int64_t)col * (SRC_C + 1) + rank;
-          const int32_t o0 = spl[0], o1 = spl[1];
-          g0 = cb + o0;
-          len = o1 - o0;
-        }
-        int x = len;   // inclusive scan inside the 8-lane group
-#pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, x, o, 8);
-          if (c >= o) x += y;
-        }
-        if (bl < nb) {
-          SrcSlot& sl = slots[(f + bl) % NS];
-          sl.gbase[c] = g0;
-          sl.off[c] = x - len;
-          if (c == 7) sl.off[8] = x;
-        }
-      }
-      __syncwarp();
-      // (3) Gram values: 22 per block
-      for (int u = lane; u < 22 * nb; u += 32) {
-        const int bl = u / 22, v = u - 22 * bl;
-        SrcSlot& sl = slots[(f + bl) % NS];
-        int si, bi, sk, bk;
-        src_gram_cols(v, si, bi, sk, bk);
-        const int ca = bi ? sl.j2[si] : sl.j1[si];
-        const int cb = bk ? sl.j2[sk] : sl.j1[sk];
-        sl.gv[v] = p.G[(int64_t)ca * p.npad + cb];
-      }
-      // (4) entries (row, value) of each block, loads batched 8 per lane
-      for (int bl = 0; bl < nb; ++bl) {
-        SrcSlot& sl = slots[(f + bl) % NS];
-        const int tot = sl.off[8] < SRC_CAP ? sl.off[8] : SRC_CAP;
-        for (int e0 = 0; e0 < tot; e0 += 256) {
-          int32_t rr[8];
-          double vv[8];
-#pragma unroll
-          for (int w = 0; w < 8; ++w) {
-            const int e = e0 + lane + 32 * w;
-            rr[w] = 0;
-            vv[w] = 0.0;
-            if (e < tot) {
-              int c = 0;
-#pragma unroll
-              for (int cc = 1; cc < 8; ++cc) c += (sl.off[cc] <= e);
-              const int64_t g = sl.gbase[c] + (e - sl.off[c]);
-              rr[w] = p.cr[g];
-              vv[w] = p.cv[g];
-            }
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int u = lane + 32 * h2;
+          const int bl = u >> 3, c = u & 7;
+          const int src = 4 * bl + (c >> 1);
+          const int ja = __shfl_sync(0xffffffffu, j1, src & 31), jb = __shfl_sync(0xffffffffu, j2, src & 31);
+          const bool lv = __shfl_sync(0xffffffffu, live, src & 31);
+          cb[h2] = 0;
+          o0[h2] = 0;
+          o1[h2] = 0;
+          if (bl < nb && lv) {
+            const int col = (c & 1) ? jb : ja;
+            cb[h2] = p.cp[col];
+            const int32_t* spl = q.split + (int64_t)col * (SRC_C + 1) + rank;
+            o0[h2] = spl[0];
+            o1[h2] = spl[1];
           }
+        }
 #pragma unroll
-          for (int w = 0; w < 8; ++w) {
-            const int e = e0 + lane + 32 * w;
-            if (e < tot) {
-              sl.row[e] = rr[w];
-              sl.val[e] = vv[w];
-            }
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int u = lane + 32 * h2;
+          const int bl = u >> 3, c = u & 7;
+          const int len = o1[h2] - o0[h2];
+          int x = len;   // inclusive scan inside the 8-lane group
+#pragma unroll
+          for (int o = 1; o < 8; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o, 8);
+            if (c >= o) x += y;
+          }
+          if (bl < nb) {
+            SrcSlot& sl = slots[(f + bl) & NSM];
+            sl.gbase[c] = cb[h2] + o0[h2];
+            sl.off[c] = x - len;
+            if (c == 7) sl.off[8] = x;
           }
         }
       }
       __syncwarp();
-      if (lane < nb) mbar_arrive(&full[(f + lane) % NS]);
+      // (3) Gram values: 22 per block, all loads of the round in flight together
+      {
+        double gq[6];
+#pragma unroll
+        for (int w = 0; w < 6; ++w) {
+          const int u = lane + 32 * w;
+          gq[w] = 0.0;
+          if (u < 22 * nb) {
+            const int bl = u / 22, v = u - 22 * bl;
+            const SrcSlot& sl = slots[(f + bl) & NSM];
+            int si, bi, sk, bk;
+            src_gram_cols(v, si, bi, sk, bk);
+            const int ca = bi ? sl.j2[si] : sl.j1[si];
+            const int cb = bk ? sl.j2[sk] : sl.j1[sk];
+            gq[w] = p.G[(int64_t)ca * p.npad + cb];
+          }
+        }
+#pragma unroll
+        for (int w = 0; w < 6; ++w) {
+          const int u = lane + 32 * w;
+          if (u < 22 * nb) {
+            const int bl = u / 22, v = u - 22 * bl;
+            slots[(f + bl) & NSM].gv[v] = gq[w];
+          }
+        }
+      }
+      // (4) entries (row, value): two blocks per batch, segment by segment (lane = position in the
+      // segment; segments longer than 32 entries continue in a second loop), loads before stores
+      for (int bl = 0; bl < nb; bl += 2) {
+        int32_t rr[16];
+        double vv[16];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const SrcSlot& sl = slots[(f + bl + u) & NSM];
+          const bool on = bl + u < nb;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int e = (on ? sl.off[c] : 0) + lane;
+            const int hi = on ? min(sl.off[c + 1], SRC_CAP) : 0;
+            rr[8 * u + c] = 0;
+            vv[8 * u + c] = 0.0;
+            if (e < hi) {
+              const int64_t g = sl.gbase[c] + lane;
+              rr[8 * u + c] = p.cr[g];
+              vv[8 * u + c] = p.cv[g];
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          SrcSlot& sl = slots[(f + bl + u) & NSM];
+          const bool on = bl + u < nb;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int e = (on ? sl.off[c] : 0) + lane;
+            const int hi = on ? min(sl.off[c + 1], SRC_CAP) : 0;
+            if (e < hi) {
+              sl.row[e] = rr[8 * u + c];
+              sl.val[e] = vv[8 * u + c];
+            }
+            for (int e2 = e + 32; e2 < hi; e2 += 32) {   // long segments
+              const int64_t g = sl.gbase[c] + (e2 - sl.off[c]);
+              sl.row[e2] = p.cr[g];
+              sl.val[e2] = p.cv[g];
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane < nb) mbar_arrive(&full[(f + lane) & NSM]);
+      if (p.prof && rank == 0) fbusy += clock64() - fc0;
     }
+    if (p.prof && rank == 0 && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(p.prof + 6), (unsigned long long)fbusy);
   } else {   // ---- consumer warps (NWC x 32 threads)
     constexpr int NTC = SRC_NWC * 32;
     using K = RkBlk<4>;
+    const bool prof = p.prof && tid == 0 && rank == 0;
+    long long pc[6] = {0, 0, 0, 0, 0, 0}, tc = prof ? clock64() : 0;
+#define CLAP(k_)                      \
+  if (prof) {                         \
+    const long long c_ = clock64();   \
+    pc[k_] += c_ - tc;                \
+    tc = c_;                          \
+  }
     for (int64_t i = 0; i < nblk; ++i) {
-      const int si = (int)(i % NS);
+      const int si = (int)(i & (NS - 1));
       mbar_wait(&full[si], (uint32_t)((i / NS) & 1));
+      CLAP(0)
       const SrcSlot& sl = slots[si];
       const int tot = sl.off[8];
       double acc[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-      for (int e = tid; e < tot; e += NTC) {
-        int c = 0;
+      // register path (at most two staged entries per thread): the thread keeps its entries' old w / r
+      // and, when no row of the CTA appears in two columns of the block (shared-memory hash of the
+      // block's rows, tagged by block), stores the updated values itself (fast update path)
+      const bool regp = tot <= SRC_CAP && tot <= 2 * NTC;
+      int frow[2] = {-1, -1}, fseg[2] = {0, 0};
+      double fv[2] = {0.0, 0.0}, fw[2] = {0.0, 0.0}, fr[2] = {0.0, 0.0};
+      bool dup = !regp;
+      if (regp) {
 #pragma unroll
-        for (int cc = 1; cc < 8; ++cc) c += (sl.off[cc] <= e);
-        int row;
-        double v;
-        if (e < SRC_CAP) {
-          row = sl.row[e];
-          v = sl.val[e];
-        } else {
-          const int64_t g = sl.gbase[c] + (e - sl.off[c]);
-          row = p.cr[g];
-          v = p.cv[g];
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int e = tid + h2 * NTC;
+          if (e < tot) {
+            int c = 0;
+#pragma unroll
+            for (int cc = 1; cc < 8; ++cc) c += (sl.off[cc] <= e);
+            frow[h2] = sl.row[e];
+            fv[h2] = sl.val[e];
+            fseg[h2] = c;
+            fr[h2] = p.Rv[frow[h2]];
+            if (!(c & 1)) fw[h2] = p.W[frow[h2]];
+          }
         }
-        const double xg = (c & 1) ? p.Rv[row] : p.W[row];
-        const double d = v * xg;
+        const unsigned long long tagb = (unsigned long long)(i + 1) << 32;
 #pragma unroll
-        for (int cc = 0; cc < 8; ++cc) acc[cc] += (c == cc) ? d : 0.0;
+        for (int h2 = 0; h2 < 2; ++h2) {
+          if (frow[h2] >= 0) {
+            const unsigned long long key = tagb | (unsigned)frow[h2];
+            uint32_t hs = ((uint32_t)frow[h2] * 2654435761u) >> (32 - SRC_HB);
+            for (int probe = 0;; ++probe) {
+              if (probe == (1 << SRC_HB)) {   // table full: take the ordered path
+                dup = true;
+                break;
+              }
+              unsigned long long cur = htab[hs];
+              if ((cur >> 32) != (tagb >> 32)) {   // stale (an earlier block) or empty: claim it
+                const unsigned long long prev = atomicCAS(&htab[hs], cur, key);
+                if (prev == cur) break;
+                cur = prev;
+              }
+              if ((cur >> 32) == (tagb >> 32)) {
+                if ((uint32_t)cur == (uint32_t)frow[h2]) {   // another column of this block has the row
+                  dup = true;
+                  break;
+                }
+                hs = (hs + 1) & ((1u << SRC_HB) - 1);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          if (frow[h2] >= 0) {
+            const double d = fv[h2] * ((fseg[h2] & 1) ? fr[h2] : fw[h2]);
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc) acc[cc] += (fseg[h2] == cc) ? d : 0.0;
+          }
+        }
+      } else {
+        for (int e = tid; e < tot; e += NTC) {
+          int c = 0;
+#pragma unroll
+          for (int cc = 1; cc < 8; ++cc) c += (sl.off[cc] <= e);
+          int row;
+          double v;
+          if (e < SRC_CAP) {
+            row = sl.row[e];
+            v = sl.val[e];
+          } else {
+            const int64_t g = sl.gbase[c] + (e - sl.off[c]);
+            row = p.cr[g];
+            v = p.cv[g];
+          }
+          const double xg = (c & 1) ? p.Rv[row] : p.W[row];
+          const double d = v * xg;
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) acc[cc] += (c == cc) ? d : 0.0;
+        }
       }
       // value order of RkBlk<4>: P(k) = k (a_k, w), Q(k) = 4 + k (b_k, r); segment c = 2k + is_b
       double accv[8];
@@ -1322,7 +1462,9 @@ __global__ void __launch_bounds__(SRC_T, 1) sparse_rk_cl_kernel(SrcParams q) {
       }
       const double ws = warp_reduce_scatter<8>(accv, lane);
       if (lane < 8) part[warp][lane] = ws;
-      named_bar_sync(1, NTC);
+      CLAP(1)
+      const bool fast = !bar_red_or(1, NTC, dup);
+      CLAP(2)
       const int b2 = (int)(i & 1);
       if (warp == 0) {
         double v = 0.0;
@@ -1340,6 +1482,7 @@ __global__ void __launch_bounds__(SRC_T, 1) sparse_rk_cl_kernel(SrcParams q) {
                            vals[2 * m + 1], bar);
         }
         mbar_wait_cluster(&rbar[b2], (uint32_t)((i >> 1) & 1));
+        CLAP(3)
         double tv = 0.0;
         if (lane < 8)
 #pragma unroll
@@ -1373,7 +1516,27 @@ __global__ void __launch_bounds__(SRC_T, 1) sparse_rk_cl_kernel(SrcParams q) {
         }
       }
       named_bar_sync(1, NTC);
-      if (warp == 1 || warp == 2) {   // w (warp 1) / r (warp 2) updates, column by column in step order
+      CLAP(4)
+      if (fast) {
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          if (frow[h2] >= 0) {
+            const int k = fseg[h2] >> 1;
+            if (fseg[h2] & 1) {
+              p.Rv[frow[h2]] = fma(-sv[b2][4 + k], fv[h2], fr[h2]);
+            } else {
+              const double s1k = sv[b2][k];
+              p.W[frow[h2]] = fma(s1k, fv[h2], fw[h2]);
+              p.Rv[frow[h2]] = fma(s1k, fv[h2], fr[h2]);
+            }
+          }
+        }
+        if (warp == 3 && lane == 0 && rank == 0) {
+          const int64_t tb = p.t0 + 4 * i;
+          for (int k = 0; k < 4; ++k)
+            if (tb + k < p.t1) atomicAdd(p.Z + sl.j2[k], sv[b2][4 + k]);
+        }
+      } else if (warp == 1 || warp == 2) {   // w (warp 1) / r (warp 2) updates, column by column in step order
         for (int c = 0; c < 8; ++c) {
           if (warp == 1 && (c & 1)) continue;
           const double sc = (c & 1) ? -sv[b2][4 + (c >> 1)] : sv[b2][c >> 1];
@@ -1400,7 +1563,11 @@ __global__ void __launch_bounds__(SRC_T, 1) sparse_rk_cl_kernel(SrcParams q) {
       }
       named_bar_sync(1, NTC);   // this block's updates precede the next block's gathers; slot free
       if (tid == 0) st_release_cta_s64(&done_s, i + 1);
+      CLAP(5)
     }
+#undef CLAP
+    if (prof)
+      for (int k = 0; k < 6; ++k) atomicAdd(reinterpret_cast<unsigned long long*>(p.prof + k), (unsigned long long)pc[k]);
   }
   __syncthreads();
   cluster_sync_all();
@@ -1523,6 +1690,11 @@ int sparse_rk_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    const char* eprof = getenv("ILS_SRK_PROF");
+    if (eprof && eprof[0] == '1') {
+      ILS_CU(cudaMallocAsync(&q.b.prof, 8 * sizeof(long long), st));
+      ILS_CU(cudaMemsetAsync(q.b.prof, 0, 8 * sizeof(long long), st));
+    }
     ILS_CU(cudaEventRecord(h.evk0, st));
     int64_t t = 0;
     int pending = 0;
@@ -1562,6 +1734,15 @@ int sparse_rk_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int
     ILS_CU(cudaMemcpyAsync(h.hstat, h.dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
     ILS_CU(cudaStreamSynchronize(st));
     const int64_t steps = h.hstat->inner_conv ? h.hstat->inner_steps : max_inner;
+    if (q.b.prof) {
+      long long hp[8];
+      cudaMemcpy(hp, q.b.prof, sizeof(hp), cudaMemcpyDeviceToHost);
+      cudaFree(q.b.prof);
+      const double blk = (double)(steps > 0 ? steps : 1) / 4.0;
+      fprintf(stderr, "ILS_SRK_PROF cluster steps=%lld cycles/block: wait-full %.0f products %.0f bar1 %.0f "
+              "exchange %.0f recurrence+bar2 %.0f updates+bar3 %.0f | fill busy %.0f\n", (long long)steps, hp[0] / blk,
+              hp[1] / blk, hp[2] / blk, hp[3] / blk, hp[4] / blk, hp[5] / blk, hp[6] / blk);
+    }
     if (steps_out) *steps_out = steps;
     const double nnz1 = (double)h.nnz1;
     hot_account(h, 1, (double)steps * 2.0 * (nnz1 / (double)h.n) * 28.0 + (double)(steps / ce) * 24.0 * nnz1,
