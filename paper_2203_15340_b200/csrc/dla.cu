@@ -599,9 +599,47 @@ __global__ void __launch_bounds__(256) potrf_trtri64_kernel(double* __restrict__
 }
 
 // Recursive Cholesky + inverse on blocks [s, e) (units of 64).
-// need_z = false (right spine of a top-level call with full_z = false): the caller never uses this
-// block's inverse as a whole, so Z21 = -Z22 L21 Z11 (two GEMMs) is skipped here; zc_apply_spine
-// applies Z through L21 instead. The left child's full inverse is always needed (L21 = A21 Z11^T).
+// need_z = true: the node's inverse Z[s:e, s:e] = L[s:e, s:e]^{-1} is formed whole (Z21 = -Z22 L21 Z11,
+// two GEMMs per node). need_z = false (top-level call with full_z = false, n >= 8192): only the
+// children of at most zt_th blocks get whole inverses (node_full); above them L21 = A21 L11^{-T} is a
+// recursive triangular solve over the left child's tree (trsm_rec) and Z is applied to vectors through
+// L21 on the same tree (zc_apply_tree), so the Z21 GEMMs of every large node (~n^3/21 flops with the
+// left children whole, 18.7 of 125 ms at c3) are never run.
+// smallest padded n whose inverse is kept in tree form (sparse / large handles); ILS_ZT_MIN_NPAD is a
+// test hook that takes small problems through the same code
+static int64_t zt_min_npad() {
+  const char* e = getenv("ILS_ZT_MIN_NPAD");
+  return (e && atoll(e) >= 64) ? atoll(e) : 8192;
+}
+
+static inline bool node_full(const Handle& h, bool need_z, int64_t blocks) { return need_z || blocks <= h.zt_th; }
+
+// B <- B L[s:e, s:e]^{-T} for the m rows of L starting at row0, columns [64 s, 64 e)  (B inside L)
+static int trsm_rec(Handle& h, double* L, double* Z, int64_t ld, int64_t s, int64_t e, bool full, int64_t row0,
+                    int64_t m, double* tmp) {
+  double* Bs = L + row0 * ld + s * 64;
+  if (full) {   // X = B Z^T (tmp, then copy back: in-place operands)
+    const int64_t nn = (e - s) * 64;
+    const int sp = pick_splits(h, (m / 64) * (nn / 64), nn);
+    int r = gemm_launch<false, false>(h, m, nn, nn, 1.0, Bs, ld, Z + s * 64 * ld + s * 64, ld, 0.0, tmp, nn, false, 2,
+                                      sp, sp > 1);
+    if (r) return r;
+    ILS_CU(cudaMemcpy2DAsync(Bs, ld * sizeof(double), tmp, nn * sizeof(double), nn * sizeof(double), m,
+                             cudaMemcpyDeviceToDevice, h.stream));
+    return ILS_OK;
+  }
+  const int64_t hmid = s + (e - s) / 2;
+  const int64_t n1 = (hmid - s) * 64, n2 = (e - hmid) * 64;
+  int r = trsm_rec(h, L, Z, ld, s, hmid, node_full(h, false, hmid - s), row0, m, tmp);
+  if (r) return r;
+  // B2 -= X1 L21^T
+  const int sp = pick_splits(h, (m / 64) * (n2 / 64), n1);
+  r = gemm_launch<false, false>(h, m, n2, n1, -1.0, Bs, ld, L + hmid * 64 * ld + s * 64, ld, 1.0,
+                                L + row0 * ld + hmid * 64, ld, false, 0, sp, false);
+  if (r) return r;
+  return trsm_rec(h, L, Z, ld, hmid, e, node_full(h, false, e - hmid), row0, m, tmp);
+}
+
 static int chol_rec(Handle& h, double* L, double* Z, int64_t ld, int64_t s, int64_t e, double* tmp,
                     bool need_z) {
   if (e - s == 1) {
@@ -621,36 +659,24 @@ static int chol_rec(Handle& h, double* L, double* Z, int64_t ld, int64_t s, int6
   }
   const int64_t hmid = s + (e - s) / 2;
   const int64_t n1 = (hmid - s) * 64, n2 = (e - hmid) * 64;
+  const bool lfull = node_full(h, need_z, hmid - s), rfull = node_full(h, need_z, e - hmid);
   double* L21 = L + hmid * 64 * ld + s * 64;
   double* L22 = L + hmid * 64 * ld + hmid * 64;
   double* Z11 = Z + s * 64 * ld + s * 64;
   double* Z21 = Z + hmid * 64 * ld + s * 64;
   double* Z22 = Z + hmid * 64 * ld + hmid * 64;
-  int r = chol_rec(h, L, Z, ld, s, hmid, tmp, true);
+  int r = chol_rec(h, L, Z, ld, s, hmid, tmp, lfull);
   if (r) return r;
-  // L21 = A21 Z11^T  (tmp, then copy back: in-place operands)
+  // L21 = A21 L11^{-T}: A21 Z11^T when Z11 is whole, else the recursive solve
   const int sp1 = pick_splits(h, (n2 / 64) * (n1 / 64), n1);
-  r = gemm_launch<false, false>(h, n2, n1, n1, 1.0, L21, ld, Z11, ld, 0.0, tmp, n1, false, 2, sp1,
-                                sp1 > 1);
+  r = trsm_rec(h, L, Z, ld, s, hmid, lfull, hmid * 64, n2, tmp);
   if (r) return r;
-  ILS_CU(cudaMemcpy2DAsync(L21, ld * sizeof(double), tmp, n1 * sizeof(double), n1 * sizeof(double), n2,
-                           cudaMemcpyDeviceToDevice, h.stream));
   // A22 -= L21 L21^T (lower tiles)
   const int sp2 = pick_splits(h, (n2 / 64) * (n2 / 64 + 1) / 2, n1);
   r = gemm_launch<false, false>(h, n2, n2, n1, -1.0, L21, ld, L21, ld, 1.0, L22, ld, true, 0, sp2,
                                 false);
   if (r) return r;
-  if (!need_z) {
-    if (h.nspine >= 24) {
-      set_error("Cholesky: recursion deeper than the spine table");
-      return ILS_ERR_UNSUPPORTED;
-    }
-    h.spine[3 * h.nspine] = s;
-    h.spine[3 * h.nspine + 1] = hmid;
-    h.spine[3 * h.nspine + 2] = e;
-    ++h.nspine;
-  }
-  r = chol_rec(h, L, Z, ld, hmid, e, tmp, need_z);
+  r = chol_rec(h, L, Z, ld, hmid, e, tmp, rfull);
   if (r) return r;
   if (!need_z) return ILS_OK;
   // Z21 = -Z22 (L21 Z11): T1 = L21 Z11 -> tmp (opB(j,k) = Z11[k][j], N-contiguous)
@@ -667,45 +693,57 @@ int cholesky_inverse(Handle& h, double* L, double* Z, int64_t npad, bool full_z)
   ILS_CU(cudaMemsetAsync(Z, 0, (size_t)npad * npad * sizeof(double), h.stream));
   double* tmp = nullptr;
   ILS_CU(cudaMallocAsync(&tmp, (size_t)npad * npad * sizeof(double), h.stream));
-  h.nspine = 0;
-  int r = chol_rec(h, L, Z, npad, 0, npad / 64, tmp, full_z);
+  {
+    const char* e = getenv("ILS_ZT_TH");   // experiment override: whole inverses up to this many 64-blocks
+    h.zt_th = (e && atoll(e) >= 1) ? atoll(e) : 64;
+  }
+  int r = chol_rec(h, L, Z, npad, 0, npad / 64, tmp, full_z || node_full(h, false, npad / 64));
   cudaFreeAsync(tmp, h.stream);
   return r;
 }
 
-// x = Z^T (Z c) with Z = L^{-1} held only partly: on every right-spine node (s, mid, e) the
-// blocks Z11 = Z[s:mid, s:mid] (complete) and L21 = L[mid:e, s:mid] are used instead of Z21:
-//   Z c:    y1 = Z11 c1 ; c2 <- c2 - L21 y1 ; recurse on [mid, e)      (Z21 = -Z22 L21 Z11)
-//   Z^T y:  x2 = Z22^T y2 (recursively) ; x1 = Z11^T (y1 - L21^T x2)
-// ending in the last leaf block, whose inverse is complete. Two GEMV launches per node and pass.
-int zc_apply_spine(Handle& h, const double* c, double* x) {
+// x = Z^T (Z c) with Z = L^{-1} held only as the whole inverses of the tree's full nodes (node_full);
+// on a split node (s, mid, e), with Z21 = -Z22 L21 Z11:
+//   y = Z w:    y1 = Z11 w1 ; w2 <- w2 - L21 y1 ; y2 = Z22 w2
+//   x = Z^T t:  x2 = Z22^T t2 ; t1 <- t1 - L21^T x2 ; x1 = Z11^T t1
+// One GEMV launch per node and pass (both updates are element-wise in place).
+static int zc_fwd(Handle& h, int64_t s, int64_t e, bool full, double* w, double* y) {
   const int64_t np = h.npad, B = 64;
+  if (full) return launch_tri_rows(h.Z + s * B * np + s * B, np, (e - s) * B, w + s * B, y + s * B, h.stream);
+  const int64_t m = s + (e - s) / 2;
+  int rc = zc_fwd(h, s, m, node_full(h, false, m - s), w, y);
+  if (rc) return rc;
+  rc = launch_gemv_rows(h.L + m * B * np + s * B, np, (e - m) * B, (m - s) * B, y + s * B, w + m * B, -1.0, w + m * B,
+                        h.stream);
+  if (rc) return rc;
+  return zc_fwd(h, m, e, node_full(h, false, e - m), w, y);
+}
+
+static int zc_bwd(Handle& h, int64_t s, int64_t e, bool full, double* t, double* x) {
+  const int64_t np = h.npad, B = 64;
+  if (full)
+    return launch_cols(h.Z + s * B * np + s * B, np, (e - s) * B, (e - s) * B, t + s * B, 1.0, nullptr, x + s * B, 1,
+                       h.stream);
+  const int64_t m = s + (e - s) / 2;
+  int rc = zc_bwd(h, m, e, node_full(h, false, e - m), t, x);
+  if (rc) return rc;
+  rc = launch_cols(h.L + m * B * np + s * B, np, (e - m) * B, (m - s) * B, x + m * B, -1.0, t + s * B, t + s * B, 0,
+                   h.stream);
+  if (rc) return rc;
+  return zc_bwd(h, s, m, node_full(h, false, m - s), t, x);
+}
+
+int zc_apply_tree(Handle& h, const double* c, double* x) {
+  const int64_t np = h.npad;
   const cudaStream_t st = h.stream;
-  double* w = h.vec + 2 * np;    // working copy of c (updated in place on the spine)
-  double* y = h.vec + 4 * np;    // Z c
-  double* t = h.vec + 5 * np;    // scratch
+  double* w = h.vec + 2 * np;    // working copy of c (updated in place on the split nodes)
+  double* y = h.vec + 4 * np;    // Z c (updated in place on the way back)
   ILS_CU(cudaMemcpyAsync(w, c, np * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  const double* Z = h.Z;
-  const double* L = h.L;
-  int rc;
-  int64_t tail = 0;
-  for (int k = 0; k < h.nspine; ++k) {
-    const int64_t s = h.spine[3 * k] * B, m = h.spine[3 * k + 1] * B, e = h.spine[3 * k + 2] * B;
-    if ((rc = launch_tri_rows(Z + s * np + s, np, m - s, w + s, y + s, st))) return rc;
-    // w[m:e] = w[m:e] - L21 y1 (into t, then back: no aliasing inside the kernel)
-    if ((rc = launch_gemv_rows(L + m * np + s, np, e - m, m - s, y + s, t + m, -1.0, w + m, st))) return rc;
-    ILS_CU(cudaMemcpyAsync(w + m, t + m, (e - m) * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    tail = m;
-  }
-  if ((rc = launch_tri_rows(Z + tail * np + tail, np, np - tail, w + tail, y + tail, st))) return rc;
-  // Z^T y, bottom-up: the tail block first, then every spine node's left block
-  if ((rc = launch_cols(Z + tail * np + tail, np, np - tail, np - tail, y + tail, 1.0, nullptr, x + tail, 1, st)))
-    return rc;
-  for (int k = h.nspine - 1; k >= 0; --k) {
-    const int64_t s = h.spine[3 * k] * B, m = h.spine[3 * k + 1] * B, e = h.spine[3 * k + 2] * B;
-    if ((rc = launch_cols(L + m * np + s, np, e - m, m - s, x + m, -1.0, y + s, t + s, 0, st))) return rc;
-    if ((rc = launch_cols(Z + s * np + s, np, m - s, m - s, t + s, 1.0, nullptr, x + s, 1, st))) return rc;
-  }
+  const bool top = node_full(h, false, np / 64);
+  int rc = zc_fwd(h, 0, np / 64, top, w, y);
+  if (rc) return rc;
+  rc = zc_bwd(h, 0, np / 64, top, y, x);
+  if (rc) return rc;
   if (h.n < np) ILS_CU(cudaMemsetAsync(x + h.n, 0, (np - h.n) * sizeof(double), st));
   return ILS_OK;
 }
@@ -743,9 +781,9 @@ int build_inverse(Handle& h) {
   if (!h.L) ILS_CU(cudaMallocAsync(&h.L, bytes, h.stream));
   if (!h.Z) ILS_CU(cudaMallocAsync(&h.Z, bytes, h.stream));
   ILS_CU(cudaMemcpyAsync(h.L, h.G, bytes, cudaMemcpyDeviceToDevice, h.stream));
-  if ((h.sparse || h.large) && np >= 8192) {
-    // large n (few outer steps, setup-dominated): no n^3 GEMM for P and no inverse blocks on the
-    // recursion's right spine; x = Z^T (Z c) is applied through the spine (zc_apply_spine)
+  if ((h.sparse || h.large) && np >= zt_min_npad()) {
+    // large n (few outer steps, setup-dominated): no n^3 GEMM for P and whole inverses only of the
+    // recursion's small diagonal blocks; x = Z^T (Z c) is applied through the tree (zc_apply_tree)
     r = cholesky_inverse(h, h.L, h.Z, np, false);
     if (r) return r;
     h.use_zt = true;
@@ -800,7 +838,7 @@ int build_a2bar(Handle& h) {
 // B = P A2bar (DMMA GEMM) and c0 = P A^T J b (Alg. 1 steps 3-4)
 int build_explicit_b(Handle& h) {
   if (h.have_B) return ILS_OK;
-  if ((h.sparse || h.large) && h.npad >= 8192) {
+  if ((h.sparse || h.large) && h.npad >= zt_min_npad()) {
     set_error("sp_form 2 (explicit B = P A2bar) is not supported for n >= 8192 (P is applied implicitly there)");
     return ILS_ERR_UNSUPPORTED;
   }

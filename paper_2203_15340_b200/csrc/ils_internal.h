@@ -52,10 +52,10 @@ struct Handle {
   double* Z = nullptr;      // npad x npad  L^{-1} (lower, zero upper)
   double* P = nullptr;      // npad x npad  (A1^T A1)^{-1}
   bool have_gram = false, have_P = false;
-  bool use_zt = false;      // P applied as Z^T (Z c) (n >= 8192): Z built without the off-diagonal
-                            // blocks of the recursion's right spine, applied through L (dla.cu)
-  int nspine = 0;           // right-spine nodes (s, mid, e) in 64-blocks, top-down
-  int64_t spine[3 * 24];
+  bool use_zt = false;      // P applied as Z^T (Z c) (n >= 8192): Z holds complete inverses only of the
+                            // recursion's diagonal blocks of <= zt_th 64-blocks; above them L21 comes from
+                            // a recursive triangular solve and Z is applied through L (dla.cu)
+  int64_t zt_th = 64;       // largest node (in 64-blocks) whose inverse is formed whole (ILS_ZT_TH)
   // paper-literal precompute (sp_form = 2): A2bar = A2^T A2, B = P A2bar, c0 = P A^T J b
   double* A2bar = nullptr;
   double* Bmat = nullptr;
@@ -208,7 +208,7 @@ int vec_add(Handle& h, double* x, const double* y, int64_t n);
 int launch_cols(const double* X, int64_t ldx, int64_t rows, int64_t cols, const double* y, double alpha,
                 const double* base, double* c, int tri_lower, cudaStream_t st);
 int launch_tri_rows(const double* T, int64_t ld, int64_t m, const double* c, double* y, cudaStream_t st);
-int zc_apply_spine(Handle& h, const double* c, double* x);
+int zc_apply_tree(Handle& h, const double* c, double* x);
 
 // batched.cu
 int batched_solve(Handle& h, int method, const double* x0, double* x, double tol, int64_t max_iter,

@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(256) gemv_p_kernel(const double* __restrict__ 
 }
 
 int gemv_p(Handle& h, const double* c, double* x) {
-  if (h.use_zt) return zc_apply_spine(h, c, x);   // x = Z^T (Z c) through the recursion's spine (dla.cu)
+  if (h.use_zt) return zc_apply_tree(h, c, x);   // x = Z^T (Z c) through the recursion's spine (dla.cu)
   gemv_p_kernel<<<(unsigned)(h.num_sms * 8), 256, 0, h.stream>>>(h.P, c, h.npad, h.n, x);
   ILS_LAUNCHED("gemv_p_kernel");
   return ILS_OK;

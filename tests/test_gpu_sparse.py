@@ -282,3 +282,29 @@ def test_sparse_gram_staged_bitwise(shape, monkeypatch):
     assert np.array_equal(hists[0], hists[2])
     for kk in range(K):
         assert _par(hists[1][kk], ref.x_hist[kk]) <= 1e-9, kk
+
+
+@pytest.mark.parametrize("th", [1, 2, 3, 64])
+@pytest.mark.parametrize("shape", [(4000, 900, 700, 6), (3000, 0, 333, 5)])
+def test_sparse_sp_tree_inverse(monkeypatch, shape, th):
+    """The n >= 8192 form of P (x = Z^T (Z c) on the Cholesky recursion's tree, whole inverses only of
+    the diagonal blocks of <= ILS_ZT_TH 64-blocks, L21 by the recursive triangular solve), forced at
+    small n (ILS_ZT_MIN_NPAD): SP iterates against the oracle for trees of depth 0 .. 4."""
+    p, q, n, k = shape
+    monkeypatch.setenv("ILS_ZT_MIN_NPAD", "64")
+    monkeypatch.setenv("ILS_ZT_TH", str(th))
+    pr = make_sparse(p, q, n, k, seed=21)
+    A1, A2, b1, b2 = _dense(pr)
+    K = 5
+    ref = O.sp_solve(A1, A2, b1, b2, max_iter=K, stop=O.STOP_NONE)
+    hist = np.zeros((K, n))
+    x = np.zeros(n)
+    with HS(pr) as hh:
+        o = ils.ils_default_opts(stop=ils.ILS_STOP_NONE, x_hist=hist.ctypes.data)
+        st, rep = ils.ils_sp_solve(hh.h, None, x, 0.0, K, o)
+        xd = np.zeros(n)
+        ils.ils_direct_solve(hh.h, xd)
+    assert rep.outer_iters == K
+    for kk in range(K):
+        assert _par(hist[kk], ref.x_hist[kk]) <= 1e-9, kk
+    assert _par(xd, O.direct_solve(A1, A2, b1, b2)) <= 1e-9
