@@ -1036,10 +1036,11 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
   __shared__ double bnorm_s;
   __shared__ __align__(8) int64_t filled_s;   // blocks whose index + Gram entries are written
   __shared__ __align__(8) int64_t done_s;     // blocks whose axpy is complete (compute warps)
-  __shared__ double smail[4][8];              // s1 (0..3), s2 (4..7) of block i, slot i & 3 (compute -> comm, reduce)
-  __shared__ double tsm[2][8];                // finished state products of block i, slot i & 1 (comm -> compute)
-  __shared__ __align__(8) uint64_t tbar[2];   // tsm[s] written (one arrival by the reduce warp)
-  __shared__ __align__(8) uint64_t sbar[2];   // smail of block b posted (one arrival by compute thread 0), slot b & 1
+  __shared__ __align__(16) double smail[4][8];   // s1 (0..3), s2 (4..7) of block i, slot i & 3 (reduce -> compute, comm)
+  // smail[i & 3] written (one arrival by the reduce warp). Four slots: the reduce warp can finish block
+  // i + 4 only after its messages were sent, i.e. after every compute thread passed B1 of iteration
+  // i + 2 and so its wait for block i
+  __shared__ __align__(8) uint64_t tbar[4];
   __shared__ __align__(4) int8_t lam[LA_NG][4];
   if (tid < LA_NG) *reinterpret_cast<int32_t*>(lam[tid]) = *reinterpret_cast<const int32_t*>(la_map[tid]);
 
@@ -1053,8 +1054,7 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
     for (int s = 0; s < 8; ++s) mbar_init(&rbar[s], 1);
-    for (int s = 0; s < 2; ++s) mbar_init(&tbar[s], 1);
-    for (int s = 0; s < 2; ++s) mbar_init(&sbar[s], 1);
+    for (int s = 0; s < 4; ++s) mbar_init(&tbar[s], 1);
     fence_mbar_init();
     for (int s = 0; s < 2; ++s) mbar_init(&cbar[s], 1);
     fence_mbar_init();
@@ -1206,11 +1206,32 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
       }
       if (stop) break;
     }
-  } else if (reducer) {   // ---- reduce warp: finished products of block i once s(i-1) is posted
+  } else if (reducer) {   // ---- reduce warp: finished products of block i, then its B-step recurrence
+    // The scalars s1, s2 of a block are needed by every compute thread, by the z updates and by the
+    // next blocks' corrections: the reduce warp forms them once (every lane redundantly, same
+    // operations in the same order as the compute threads did before) and posts them; the compute
+    // warps only wait for them and run their axpy (the recurrence and its 30 table loads left their
+    // step chain: ~390 of 2140 cycles per block at c1).
     const bool rprof = p.prof && lane == 0;
     long long hr[2] = {0, 0};
     for (int64_t i = 0; i < *(volatile int64_t*)&lim_s; ++i) {
-      if (i >= 1) mbar_wait(&sbar[(i - 1) & 1], (uint32_t)(((i - 1) >> 1) & 1));
+      // in-block Gram values and index entries of block i (filled: block i - 1's messages were sent
+      // after the compute warps saw blocks <= i filled), loaded ahead of the message wait
+      double T[K::NV];
+      {
+        const double* gi = gring[i & (LA_GR - 1)];
+#pragma unroll
+        for (int v = NRV; v < K::NV; ++v) T[v] = gi[v - NRV];
+      }
+      const int64_t t = p.t0 + i * B;
+      double bh1[B], rn1[B], rn2[B];
+#pragma unroll
+      for (int k = 0; k < B; ++k) {
+        const RkIdx ix = ring[(t + k) & (RK_RING - 1)];
+        bh1[k] = ix.bh1;
+        rn1[k] = ix.rn1;
+        rn2[k] = ix.rn2;
+      }
       long long rc0 = rprof ? clock64() : 0;
       const int b4 = (int)(i & 7);
       mbar_wait(&rbar[b4], (uint32_t)((i >> 3) & 1));
@@ -1239,13 +1260,37 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
       }
       tot += __shfl_xor_sync(0xffffffffu, tot, 8);
       tot += __shfl_xor_sync(0xffffffffu, tot, 16);
-      if (lane < NRV) tsm[i & 1][lane] = tot;
+#pragma unroll
+      for (int q = 0; q < NRV; ++q) T[q] = __shfl_sync(0xffffffffu, tot, q);
+      double s1[B], s2[B];
+#pragma unroll
+      for (int kk = 0; kk < B; ++kk) {
+        double dw = T[K::P(kk)];
+#pragma unroll
+        for (int m = 0; m < kk; ++m) dw = fma(s1[m], T[K::AA(kk, m)], dw);
+        s1[kk] = (bh1[kk] - dw) * rn1[kk];
+        double dr = T[K::Q(kk)];
+#pragma unroll
+        for (int m = 0; m < kk; ++m) {
+          dr = fma(s1[m], T[K::BA(kk, m)], dr);
+          dr = fma(-s2[m], T[K::BB(kk, m)], dr);
+        }
+        dr = fma(s1[kk], T[K::BA(kk, kk)], dr);
+        s2[kk] = dr * rn2[kk];
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int kk = 0; kk < B; ++kk) {
+          smail[i & 3][kk] = s1[kk];
+          smail[i & 3][B + kk] = s2[kk];
+        }
+      }
       // stop flags of block i (identical messages in every CTA): end after block i + 2
       const bool flag = __any_sync(0xffffffffu, lane < CC && recv[b4][lane][NRV] != 0.0);
       if (flag && lane == 0 && lim_s > i + 3) lim_s = i + 3;
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&tbar[i & 1]);
+        mbar_arrive(&tbar[i & 3]);
         mbar_arrive_expect_tx(&rbar[b4], CC * NMSG * 8);   // for block i + 8
       }
       if (rprof) hr[1] += clock64() - rc0;
@@ -1372,45 +1417,23 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
         continue;
       }
       if (i < 0) continue;
-      // ---- phase 2 (compute warps): block i
-      double T[K::NV];
-      {
-        const double* gi = gring[i & (LA_GR - 1)];   // in-block Gram values (filled: see phase 1)
-#pragma unroll
-        for (int v = NRV; v < K::NV; ++v) T[v] = gi[v - NRV];
-      }
-      mbar_wait(&tbar[i & 1], (uint32_t)((i >> 1) & 1));
+      // ---- phase 2 (compute warps): block i, with the scalars posted by the reduce warp
+      mbar_wait(&tbar[i & 3], (uint32_t)((i >> 2) & 1));
       LAP(2)
-#pragma unroll
-      for (int v = 0; v < NRV; ++v) T[v] = tsm[i & 1][v];
-      LAP(3)
-      const int64_t t = p.t0 + i * B;
       double s1[B], s2[B];
+      {
+        const double2* sm2 = reinterpret_cast<const double2*>(smail[i & 3]);
 #pragma unroll
-      for (int k = 0; k < B; ++k) {
-        const RkIdx ix = ring[(t + k) & (RK_RING - 1)];
-        double dw = T[K::P(k)];
-#pragma unroll
-        for (int m = 0; m < k; ++m) dw = fma(s1[m], T[K::AA(k, m)], dw);
-        s1[k] = (ix.bh1 - dw) * ix.rn1;
-        double dr = T[K::Q(k)];
-#pragma unroll
-        for (int m = 0; m < k; ++m) {
-          dr = fma(s1[m], T[K::BA(k, m)], dr);
-          dr = fma(-s2[m], T[K::BB(k, m)], dr);
+        for (int k = 0; k < B; k += 2) {
+          const double2 a = sm2[k / 2], b = sm2[(B + k) / 2];
+          s1[k] = a.x;
+          s1[k + 1] = a.y;
+          s2[k] = b.x;
+          s2[k + 1] = b.y;
         }
-        dr = fma(s1[k], T[K::BA(k, k)], dr);
-        s2[k] = dr * ix.rn2;
       }
+      LAP(3)
       LAP(4)
-      if (tid == 0) {   // the reduce warp forms block i+1's products (and the comm warp z) with them
-#pragma unroll
-        for (int k = 0; k < B; ++k) {
-          smail[i & 3][k] = s1[k];
-          smail[i & 3][B + k] = s2[k];
-        }
-        mbar_arrive(&sbar[i & 1]);
-      }
       const double* cols = slots + (size_t)sl_i * 2 * B * SP;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
