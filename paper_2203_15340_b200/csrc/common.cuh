@@ -335,6 +335,14 @@ __device__ __forceinline__ int64_t ld_acquire_cta_s64(const int64_t* a) {
 __device__ __forceinline__ void st_release_cta_s64(int64_t* a, int64_t v) {
   asm volatile("st.release.cta.shared::cta.s64 [%0], %1;" ::"r"(smem_u32(a)), "l"(v) : "memory");
 }
+// Progress counter written after a CTA barrier that every reader of the guarded buffer took part in:
+// the readers' loads have returned (their values were consumed) before the barrier completes, so the
+// counter only has to become visible after it, which program order behind bar.sync gives. The release
+// form above compiles to MEMBAR.ALL.CTA + STS and cost ~250 cycles per block on the compute chain of
+// the look-ahead RK-RGS kernels (ILS_RK_PROF: loop-top 253 cycles).
+__device__ __forceinline__ void st_relaxed_cta_s64(int64_t* a, int64_t v) {
+  asm volatile("st.relaxed.cta.shared::cta.s64 [%0], %1;" ::"r"(smem_u32(a)), "l"(v) : "memory");
+}
 
 // ---------------------------------------------------------------- cp.async (LDGSTS)
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {

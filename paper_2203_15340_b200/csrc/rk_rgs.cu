@@ -916,7 +916,8 @@ __global__ void __launch_bounds__(256, 1) rk_rgs_small_kernel(RkParams p, double
 // compute warps) and hands the 8 finished products to the compute warps through an mbarrier, so
 // the compute warps' own path per block is products -> recurrence -> axpy. A fill warp and a TMA
 // warp run ahead (index / Gram rings, column refills); the compute warps never issue a send.
-constexpr int LA_GR = 16;    // blocks in the Gram ring (the fill warp runs at most LA_GR blocks ahead)
+constexpr int LA_GR = 16;    // blocks in the Gram ring (the fill warp runs at most LA_GR blocks ahead; a 32-block ring
+                             // with 24 blocks of lead measured the same: c1 184.8 vs 184.9 ms)
 constexpr int LA_NG = 118;   // Gram values per block: 22 in-block (RkBlk<4> order) + 48 with block - 1 + 48 with block - 2
 
 // (value v of a block) -> (step of the current block, its column, step relative to the block start
@@ -996,7 +997,7 @@ __device__ __forceinline__ void st_async_f64(uint32_t raddr, double a, uint32_t 
 // block any CTA can have sent -- so no message is left in flight. The output is the snapshot z and
 // the step count t_c, exactly as if the steps had stopped at t_c.
 template <int CC, int U>
-__global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
+__global__ void __launch_bounds__(416, 1) rk_rgs_la_kernel(RkParams p) {
   constexpr int B = 4, NRV = 8;
   static_assert(CC == 16, "the communication warp's cluster sum is written for 16 sources");
   using K = RkBlk<B>;
@@ -1009,10 +1010,21 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
   const int rank = (int)cluster_ctarank();
   const int64_t i0 = (int64_t)rank * p.slice;
   const int own = (int)((i0 + p.slice <= p.ppad) ? p.slice : (p.ppad > i0 ? p.ppad - i0 : 0));
-  const int NS = p.nslots, SP = p.slicepad;
+  // slot count and slice pitch through shared memory, so that they stay in registers: as kernel
+  // parameters they are reloaded from the constant bank (LDC) in every phase of every iteration
+  __shared__ int la_cfg[2];
+  if (tid == 0) {
+    la_cfg[0] = p.nslots;
+    la_cfg[1] = p.slicepad;
+  }
+  __syncthreads();
+  const int NS = *(volatile int*)&la_cfg[0], SP = *(volatile int*)&la_cfg[1];
   if (*(volatile int32_t*)&p.st->inner_conv != 0) return;
 
-  double* slots = reinterpret_cast<double*>(smem_raw);                 // [NS][2B][slicepad]
+  uint32_t dyn32 = smem_u32(smem_raw);   // laundered like the static variables below
+  asm volatile("" : "+r"(dyn32));
+  unsigned char* smem_dyn = reinterpret_cast<unsigned char*>(__cvta_shared_to_generic(dyn32));
+  double* slots = reinterpret_cast<double*>(smem_dyn);                 // [NS][2B][slicepad]
   double* zs = slots + (size_t)NS * 2 * B * SP;                        // [npad]
   uint64_t* Ss = reinterpret_cast<uint64_t*>(zs + p.npad);             // [n]
   RkIdx* ring = reinterpret_cast<RkIdx*>(Ss + ((p.n + 1) & ~1));       // [RK_RING]
@@ -1020,28 +1032,64 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
   double* bh_tab = reinterpret_cast<double*>(bars + 8);                 // [n]
   double* rn_tab = bh_tab + ((p.n + 1) & ~1);                          // [n]
   double (*gring)[LA_NG] = reinterpret_cast<double (*)[LA_NG]>(rn_tab + ((p.n + 1) & ~1));   // [LA_GR][LA_NG]
-  __shared__ __align__(16) double wred[2][8][32];   // per warp: value lane & 7 over lane group lane >> 3
+  // The kernel's static shared variables live in one struct reached through a laundered 32-bit shared
+  // address: referenced by name, every loop iteration of every role re-derived their cluster-window
+  // address with S2UR SR_CgaCtaId (the compiler rematerialises it instead of holding a register), which
+  // sat on the step chain (ILS_RK_PROF: ~280 cycles between the axpy barrier and the next products).
   constexpr int NMSG = NRV + 2;                          // 8 products + stop flag + pad
-  __shared__ __align__(16) double recv[8][RK_MAXC][NMSG];  // block b in buffer b & 7 (sent two blocks ahead)
-  __shared__ __align__(8) double crecv[2][RK_MAXC];       // check m partials in buffer m & 1
-  __shared__ __align__(8) uint64_t cbar[2];
-  __shared__ __align__(8) int64_t lim_s;      // blocks to run (lowered once on a stop)
-  __shared__ __align__(8) int64_t snap_s;     // z snapshots taken (comm warp)
-  __shared__ __align__(8) int64_t chkd_s;     // checks decided (check warp)
-  __shared__ __align__(8) int64_t stop_t_s;   // step of the check that stopped the solve, -1: none
-  __shared__ int stop_req_s;                  // flag the next block messages
-  __shared__ int zdone_s;                     // the communication warp's last z update is done
-  __shared__ __align__(8) uint64_t rbar[8];
-  __shared__ double chkw[12];
-  __shared__ double bnorm_s;
-  __shared__ __align__(8) int64_t filled_s;   // blocks whose index + Gram entries are written
-  __shared__ __align__(8) int64_t done_s;     // blocks whose axpy is complete (compute warps)
-  __shared__ __align__(16) double smail[4][8];   // s1 (0..3), s2 (4..7) of block i, slot i & 3 (reduce -> compute, comm)
-  // smail[i & 3] written (one arrival by the reduce warp). Four slots: the reduce warp can finish block
-  // i + 4 only after its messages were sent, i.e. after every compute thread passed B1 of iteration
-  // i + 2 and so its wait for block i
-  __shared__ __align__(8) uint64_t tbar[4];
-  __shared__ __align__(4) int8_t lam[LA_NG][4];
+  struct LaSh {
+    alignas(16) double wred[2][8][32];   // per warp: value lane & 7 over lane group lane >> 3
+    alignas(16) double recv[8][RK_MAXC][NMSG];  // block b in buffer b & 7 (sent two blocks ahead)
+    alignas(16) double smail[4][8];   // s1 (0..3), s2 (4..7) of block i, slot i & 3 (reduce -> compute, comm)
+    alignas(8) double crecv[2][RK_MAXC];       // check m partials in buffer m & 1
+    alignas(8) uint64_t cbar[2];
+    alignas(8) int64_t lim_s;      // blocks to run (lowered once on a stop)
+    alignas(8) int64_t snap_s;     // z snapshots taken (comm warp)
+    alignas(8) int64_t chkd_s;     // checks decided (check warp)
+    alignas(8) int64_t stop_t_s;   // step of the check that stopped the solve, -1: none
+    alignas(8) uint64_t rbar[8];
+    double chkw[16];
+    double bnorm_s;
+    alignas(8) int64_t filled_s;   // blocks whose index + Gram entries are written
+    alignas(8) int64_t done_w[8];  // per compute warp: blocks whose axpy is complete (readers take the minimum)
+    // smail[i & 3] written (one arrival by the reduce warp). Four slots: the reduce warp can finish block
+    // i + 4 only after its messages were sent, i.e. after every compute thread passed B1 of iteration
+    // i + 2 and so its wait for block i
+    alignas(8) uint64_t tbar[4];
+    int stop_req_s;                  // flag the next block messages
+    int zdone_s;                     // the communication warp's last z update is done
+    alignas(4) int8_t lam[LA_NG][4];
+  };
+  __shared__ LaSh la_static;
+  uint32_t sh32 = smem_u32(&la_static);
+  asm volatile("" : "+r"(sh32));
+  LaSh& sh = *reinterpret_cast<LaSh*>(__cvta_shared_to_generic(sh32));
+#define wred sh.wred
+#define recv sh.recv
+#define smail sh.smail
+#define crecv sh.crecv
+#define cbar sh.cbar
+#define lim_s sh.lim_s
+#define snap_s sh.snap_s
+#define chkd_s sh.chkd_s
+#define stop_t_s sh.stop_t_s
+#define rbar sh.rbar
+#define chkw sh.chkw
+#define bnorm_s sh.bnorm_s
+#define filled_s sh.filled_s
+#define done_w sh.done_w
+#define tbar sh.tbar
+#define stop_req_s sh.stop_req_s
+#define zdone_s sh.zdone_s
+#define lam sh.lam
+  auto done_min = [&]() {   // blocks finished by every compute warp
+    int64_t m = ld_acquire_cta_s64(&done_w[0]);
+    for (int w8 = 1; w8 < NWc; ++w8) {
+      const int64_t v = ld_acquire_cta_s64(&done_w[w8]);
+      m = v < m ? v : m;
+    }
+    return m;
+  };
   if (tid < LA_NG) *reinterpret_cast<int32_t*>(lam[tid]) = *reinterpret_cast<const int32_t*>(la_map[tid]);
 
   for (int64_t j = tid; j < p.npad; j += NT) zs[j] = p.Z[j];
@@ -1060,7 +1108,7 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
     fence_mbar_init();
     for (int s = 0; s < 8; ++s) mbar_arrive_expect_tx(&rbar[s], CC * NMSG * 8);
     for (int s = 0; s < 2; ++s) mbar_arrive_expect_tx(&cbar[s], CC * 8);
-    done_s = 0;
+    for (int s = 0; s < 8; ++s) done_w[s] = 0;
     snap_s = 0;
     chkd_s = 0;
     stop_t_s = -1;
@@ -1119,8 +1167,11 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
   if (filler) {   // ---- fill warp: index + Gram rings, at most 24 blocks ahead of the consumers
     int64_t f = 16;
     bool quit = false;
+    const bool fprof = p.prof && lane == 0;
+    long long hf[2] = {0, 0};   // throttle wait, fill work
+    long long fc0 = fprof ? clock64() : 0;
     while (f < nblk && !quit) {
-      while (f + 8 > ld_acquire_cta_s64(&done_s) + LA_GR) {   // slot of block done must stay
+      while (f + 8 > done_min() + LA_GR) {   // slot of block done must stay
         if (f >= ld_acquire_cta_s64(&lim_s) + 8) {            // stopped: nothing further is needed
           quit = true;
           break;
@@ -1128,11 +1179,25 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
         if (p.nap) __nanosleep(p.nap);   // leave the issue slots to the compute warp of this SMSP
       }
       if (quit) break;
+      if (fprof) {
+        const long long c_ = clock64();
+        hf[0] += c_ - fc0;
+        fc0 = c_;
+      }
       rk_fill_indices(p, Ss, ring, p.t0 + 4 * f, lane, bh_tab, rn_tab);
       la_fill_gram(p, ring, gring, lam, f, lane);
       f += 8;
       __syncwarp();
       if (lane == 0) st_release_cta_s64(&filled_s, f);
+      if (fprof) {
+        const long long c_ = clock64();
+        hf[1] += c_ - fc0;
+        fc0 = c_;
+      }
+    }
+    if (fprof) {
+      p.prof[128 + rank * 8 + 5] += hf[0];
+      p.prof[128 + rank * 8 + 6] += hf[1];
     }
   } else if (tmaw) {   // ---- TMA warp: refill slot (b % NS) once block b - NS is done
     if (lane == 0 && own > 0) {
@@ -1140,7 +1205,7 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
       int64_t b = NS;
       for (; b < nblk; ++b) {
         bool quit = false;
-        while (ld_acquire_cta_s64(&done_s) < b - NS + 1 || ld_acquire_cta_s64(&filled_s) <= b) {
+        while (done_min() < b - NS + 1 || ld_acquire_cta_s64(&filled_s) <= b) {
           if (b >= ld_acquire_cta_s64(&lim_s)) {
             quit = true;
             break;
@@ -1155,7 +1220,7 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
       // drain: blocks issued at or past the final limit were never consumed -- their copies must
       // land before the CTA exits (every block below it was waited for by the compute warps)
       const int64_t issued = (b < nblk) ? b : nblk;
-      const int64_t lim_end = ld_acquire_cta_s64(&done_s);
+      const int64_t lim_end = done_min();
       for (int64_t d = lim_end; d < issued; ++d) mbar_wait(&bars[d % NS], (uint32_t)((d / NS) & 1));
     }
   } else if (checker) {   // ---- check warp: g = A1bar z - b_hat on each snapshot, cluster sum, decide
@@ -1360,6 +1425,7 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
       }
       sl_i = sl_nb - 2 < 0 ? sl_nb - 2 + NS : sl_nb - 2;   // slot of block i (NS >= 3)
       // ---- phase 1 (compute warps): state products of block nb = i + 2 on S_i (blocks i, i+1 not applied)
+      LAP(4)
       if (compute && nb < lim) {
         if (known_filled <= nb + 1 && known_filled < nblk) {   // ring + Gram entries of blocks nb, nb+1
           do {
@@ -1433,7 +1499,6 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
         }
       }
       LAP(3)
-      LAP(4)
       const double* cols = slots + (size_t)sl_i * 2 * B * SP;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -1447,8 +1512,11 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
         }
       }
       LAP(5)
-      named_bar_sync(2, NTc);   // every compute thread finished block i's axpy (slot sl_i reusable)
-      if (tid == 0) st_release_cta_s64(&done_s, i + 1);
+      // this warp finished block i's axpy (its loads of slot sl_i have returned: their values were
+      // consumed); the slot is reusable once every compute warp says so. No CTA barrier here: the warps
+      // meet once per iteration, at B1 (a second barrier cost ~220 cycles of skew per block)
+      __syncwarp();
+      if (lane == 0) st_relaxed_cta_s64(&done_w[warp], i + 1);
       LAP(5)
     }
 #undef LAP
@@ -1469,7 +1537,7 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
     }
     if (comm) {   // the last block's z updates (and snapshots), once its scalars are posted
       const int64_t lim = *(volatile int64_t*)&lim_s;
-      while (ld_acquire_cta_s64(&done_s) < lim) {
+      while (done_min() < lim) {
       }
       if (lim >= 1) zupd(lim - 1);
       __threadfence_block();
@@ -1488,6 +1556,25 @@ __global__ void __launch_bounds__(384, 1) rk_rgs_la_kernel(RkParams p) {
   }
   cluster_sync_all();
 }
+
+#undef wred
+#undef recv
+#undef smail
+#undef crecv
+#undef cbar
+#undef lim_s
+#undef snap_s
+#undef chkd_s
+#undef stop_t_s
+#undef rbar
+#undef chkw
+#undef bnorm_s
+#undef filled_s
+#undef done_w
+#undef tbar
+#undef stop_req_s
+#undef zdone_s
+#undef lam
 
 template <int CC, int U>
 static int launch_rkla(Handle& h, RkParams& p, int nt, size_t smem) {
@@ -1723,7 +1810,7 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
   size_t smem_la = 0;
   {
     const char* e = getenv("ILS_RK_LA");
-    if (!(e && e[0] == '0') && blocked && !p.gmode && C == 16 && Bsel == 4 && (U == 2 || U == 4 || U == 8) && nt + 160 <= 384 && !h.large &&
+    if (!(e && e[0] == '0') && blocked && !p.gmode && C == 16 && Bsel == 4 && (U == 2 || U == 4 || U == 8) && nt + 160 <= 416 && !h.large &&
         !h.sparse) {
       // the Gram ring replaces one column slot when both do not fit (>= 3 slots: blocks i .. i+2 live)
       const size_t ring_bytes = (size_t)LA_GR * LA_NG * sizeof(double), slot_la = (size_t)2 * Bsel * p.slicepad * 8;
@@ -1860,15 +1947,15 @@ int rk_rgs_inner(Handle& h, const double* bhat, double* z, uint64_t seed, int64_
     for (int rk = 0; rk < p.C; ++rk) {
       const long long* q = hp + rk * 8;
       if (la)   // look-ahead kernel phases on compute thread 0 (LAP indices in rk_rgs_la_kernel)
-        fprintf(stderr, "ILS_RK_PROF k=%lld rank=%d blocks=%.0f cycles/block: products %.0f B1 %.0f T-wait %.0f T-read %.0f recurrence %.0f axpy %.0f TMA-wait %.0f fill-wait %.0f\n",
+        fprintf(stderr, "ILS_RK_PROF k=%lld rank=%d blocks=%.0f cycles/block: products %.0f B1 %.0f T-wait %.0f T-read %.0f loop-top %.0f axpy %.0f TMA-wait %.0f fill-wait %.0f\n",
                 (long long)k, rk, nb, q[0] / nb, q[1] / nb, q[2] / nb, q[3] / nb, q[4] / nb, q[5] / nb, q[6] / nb, q[7] / nb);
       else
         fprintf(stderr, "ILS_RK_PROF k=%lld rank=%d blocks=%.0f cycles/block: wait %.0f local %.0f rscatter %.0f bar %.0f send %.0f recv %.0f sum %.0f rest %.0f\n",
                 (long long)k, rk, nb, q[0] / nb, q[1] / nb, q[2] / nb, q[3] / nb, q[4] / nb, q[5] / nb, q[6] / nb, q[7] / nb);
       if (la) {   // look-ahead helper warps: reduce warp (B1 -> data, data -> T posted), comm warp (send issue)
         const long long* r2 = hp + 128 + rk * 8;
-        fprintf(stderr, "ILS_RK_PROF_LA rank=%d reduce: data wait %.0f T %.0f rest %.0f | comm: send %.0f z %.0f\n", rk,
-                r2[0] / nb, r2[1] / nb, r2[2] / nb, r2[3] / nb, r2[4] / nb);
+        fprintf(stderr, "ILS_RK_PROF_LA rank=%d reduce: data wait %.0f T %.0f rest %.0f | comm: send %.0f z %.0f | fill (per block): throttle %.0f work %.0f\n", rk,
+                r2[0] / nb, r2[1] / nb, r2[2] / nb, r2[3] / nb, r2[4] / nb, r2[5] / nb, r2[6] / nb);
       }
     }
   }

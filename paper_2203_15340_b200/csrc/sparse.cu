@@ -1562,7 +1562,7 @@ __global__ void __launch_bounds__(SRC_T, 1) sparse_rk_cl_kernel(SrcParams q) {
           if (tb + k < p.t1) atomicAdd(p.Z + sl.j2[k], sv[b2][4 + k]);
       }
       named_bar_sync(1, NTC);   // this block's updates precede the next block's gathers; slot free
-      if (tid == 0) st_release_cta_s64(&done_s, i + 1);
+      if (tid == 0) st_relaxed_cta_s64(&done_s, i + 1);   // after the barrier: see common.cuh
       CLAP(5)
     }
 #undef CLAP
