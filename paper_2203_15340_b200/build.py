@@ -12,6 +12,7 @@ NVCC = os.environ.get("NVCC", "nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
          "-Xptxas", "-v", "-I", os.path.join(HERE, "..", "include")]
+FLAGS += os.environ.get("ILS_NVCC_EXTRA", "").split()   # development: e.g. -DILS_SP_TRACE (phase timers under ILS_SP_PROF)
 
 
 def build(verbose: bool = False, force: bool = False) -> str:

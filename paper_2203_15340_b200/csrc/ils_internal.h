@@ -22,8 +22,8 @@ struct DevStatus {
   int64_t inner_steps;     // inner steps of the last inner solve
   int32_t inner_conv;      // inner solve met its tolerance
   int32_t flag_nonfinite;  // ingest: a non-finite entry in A or b
-  uint32_t gbar_count;     // software grid barrier of the SP row-stream kernel (arrivals, back to 0)
-  uint32_t gbar_gen;       // its generation counter
+  uint32_t gbar_count;     // software grid barrier of the SP row-stream kernel: arrivals since the launch (zeroed by the host before every launch)
+  uint32_t gbar_gen;       // (unused; keeps the layout)
 };
 
 struct ils_comm_impl {
