@@ -123,17 +123,17 @@ int dense_rhs_twopass(Handle& h, const double* x, double* c, int full) {
   if (!full) {
     rows_minus_b_kernel<<<148 * 16, 256, 0, st>>>(h.Arm + h.p * np, np, h.q, h.n, x, h.b + h.p, h.sp_y);
     ILS_LAUNCHED("rows_minus_b_kernel");
-    cols_kernel<<<grid_cols(h.n), 256, 0, st>>>(h.Arm + h.p * np, np, h.q, h.n, h.sp_y, 1.0, h.a1tb1, c);
-    ILS_LAUNCHED("cols_kernel");
+    { const int rc_ = launch_cols(h.Arm + h.p * np, np, h.q, h.n, h.sp_y, 1.0, h.a1tb1, c, 0, st);
+    if (rc_) return rc_; }
     return ILS_OK;
   }
   // g = A1^T (b1 - A1 x) - A2^T (b2 - A2 x) = -A1^T y1 + A2^T y2 with y = A x - b
   rows_minus_b_kernel<<<148 * 16, 256, 0, st>>>(h.Arm, np, h.m, h.n, x, h.b, h.sp_y);
   ILS_LAUNCHED("rows_minus_b_kernel");
-  cols_kernel<<<grid_cols(h.n), 256, 0, st>>>(h.Arm + h.p * np, np, h.q, h.n, h.sp_y + h.p, 1.0, nullptr, c);
-  ILS_LAUNCHED("cols_kernel");
-  cols_kernel<<<grid_cols(h.n), 256, 0, st>>>(h.Arm, np, h.p, h.n, h.sp_y, -1.0, c, c);   // in place per column
-  ILS_LAUNCHED("cols_kernel");
+  { const int rc_ = launch_cols(h.Arm + h.p * np, np, h.q, h.n, h.sp_y + h.p, 1.0, nullptr, c, 0, st);
+    if (rc_) return rc_; }
+  { const int rc_ = launch_cols(h.Arm, np, h.p, h.n, h.sp_y, -1.0, c, c, 0, st);   // in place per column
+    if (rc_) return rc_; }
   return ILS_OK;
 }
 
@@ -182,8 +182,8 @@ int rk_check_twopass(Handle& h, const double* z, const double* bhat, const doubl
   rows_minus_b_kernel<<<148 * 16, 256, 0, st>>>(h.Arm, np, h.p, h.n, z, nullptr, az);
   ILS_LAUNCHED("rows_minus_b_kernel");
   double* g = h.sp_y + h.m + 64;
-  cols_kernel<<<grid_cols(h.n), 256, 0, st>>>(h.Arm, np, h.p, h.n, az, 1.0, nullptr, g);
-  ILS_LAUNCHED("cols_kernel");
+  { const int rc_ = launch_cols(h.Arm, np, h.p, h.n, az, 1.0, nullptr, g, 0, st);
+    if (rc_) return rc_; }
   check_finish_kernel<<<1, 1024, 0, st>>>(g, bhat, h.n, az, w, r, h.p, h.ppad, inner_tol, t_now, h.dstat);
   ILS_LAUNCHED("check_finish_kernel");
   return ILS_OK;
@@ -194,10 +194,91 @@ __global__ void add_kernel(double* __restrict__ x, const double* __restrict__ y,
     x[i] += y[i];
 }
 
+// The same product as cols_kernel, tiled for HBM: a CTA owns a tile of 512 columns (two per thread, one
+// 16-byte load per row: 4 KB contiguous per row and CTA instead of 256 B per warp) and a chunk of rows,
+// eight rows in flight per thread; the per-chunk partial sums go to a workspace [chunks][cols] and
+// cols_tile_reduce_kernel adds them in chunk order (fixed geometry: deterministic). tri_lower: rows
+// above the tile's first column hold zeros and are skipped.
+constexpr int CT_THREADS = 256, CT_COLS = 2 * CT_THREADS;
+__global__ void __launch_bounds__(CT_THREADS) cols_tile_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows,
+                                                               int64_t cols, const double* __restrict__ y,
+                                                               int64_t rc, int tri_lower, double* __restrict__ part) {
+  const int64_t j0 = (int64_t)blockIdx.x * CT_COLS, jt = j0 + 2 * threadIdx.x;
+  const int64_t chunk = blockIdx.y;
+  int64_t ra = chunk * rc, rb = ra + rc < rows ? ra + rc : rows;
+  if (tri_lower && ra < j0) ra = j0;
+  double sx = 0.0, sy = 0.0;
+  if (jt + 1 < cols) {
+    const double* xp = X + jt;
+    double ax[8], ay[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) ax[u] = ay[u] = 0.0;
+    int64_t i = ra;
+    for (; i + 8 <= rb; i += 8) {
+      double2 xv[8];
+      double yv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        xv[u] = __ldcs(reinterpret_cast<const double2*>(xp + (i + u) * ldx));
+        yv[u] = __ldg(y + i + u);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        ax[u] = fma(xv[u].x, yv[u], ax[u]);
+        ay[u] = fma(xv[u].y, yv[u], ay[u]);
+      }
+    }
+    for (; i < rb; ++i) {
+      const double2 xv = __ldcs(reinterpret_cast<const double2*>(xp + i * ldx));
+      const double yv = __ldg(y + i);
+      ax[0] = fma(xv.x, yv, ax[0]);
+      ay[0] = fma(xv.y, yv, ay[0]);
+    }
+    sx = ((ax[0] + ax[1]) + (ax[2] + ax[3])) + ((ax[4] + ax[5]) + (ax[6] + ax[7]));
+    sy = ((ay[0] + ay[1]) + (ay[2] + ay[3])) + ((ay[4] + ay[5]) + (ay[6] + ay[7]));
+  } else if (jt < cols) {   // odd column count: the last column alone
+    for (int64_t i = ra; i < rb; ++i) sx = fma(X[i * ldx + jt], __ldg(y + i), sx);
+  }
+  if (jt < cols) part[chunk * cols + jt] = sx;
+  if (jt + 1 < cols) part[chunk * cols + jt + 1] = sy;
+}
+
+__global__ void __launch_bounds__(256) cols_tile_reduce_kernel(const double* __restrict__ part, int64_t chunks,
+                                                               int64_t cols, double alpha, const double* base,
+                                                               double* c) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  double t = 0.0;
+  for (int64_t k = 0; k < chunks; ++k) t += part[k * cols + j];
+  c[j] = (base ? base[j] : 0.0) + alpha * t;
+}
+
 // c = base + alpha * X^T y over `rows` rows (tri_lower: X lower triangular, zero rows skipped)
 int launch_cols(const double* X, int64_t ldx, int64_t rows, int64_t cols, const double* y, double alpha,
                 const double* base, double* c, int tri_lower, cudaStream_t st) {
   if (cols <= 0) return ILS_OK;
+  const char* e = getenv("ILS_COLS_TILED");   // override: 0 = the 32-column kernel, 2 = tiled at any size (tests)
+  const bool al16 = ((uintptr_t)X & 15) == 0 && (ldx & 1) == 0;
+  const bool big = (rows >= 256 && cols >= 64) || (e && e[0] == '2');
+  if (al16 && big && !(e && e[0] == '0')) {
+    const int64_t nct = (cols + CT_COLS - 1) / CT_COLS;
+    int cps = 8;                                           // CTAs per SM over the whole panel (ILS_COLS_CPS: experiment)
+    if (const char* ec = getenv("ILS_COLS_CPS")) cps = atoi(ec) > 0 ? atoi(ec) : cps;
+    int64_t chunks = ((int64_t)148 * cps + nct - 1) / nct;
+    if (chunks > rows / 32) chunks = rows / 32;            // at least 32 rows per chunk
+    if (chunks < 1) chunks = 1;
+    const int64_t rc = (rows + chunks - 1) / chunks;
+    chunks = (rows + rc - 1) / rc;
+    double* part = nullptr;
+    ILS_CU(cudaMallocAsync(&part, (size_t)chunks * cols * sizeof(double), st));
+    cols_tile_kernel<<<dim3((unsigned)nct, (unsigned)chunks), CT_THREADS, 0, st>>>(X, ldx, rows, cols, y, rc, tri_lower,
+                                                                                    part);
+    ILS_LAUNCHED("cols_tile_kernel");
+    cols_tile_reduce_kernel<<<(unsigned)((cols + 255) / 256), 256, 0, st>>>(part, chunks, cols, alpha, base, c);
+    ILS_LAUNCHED("cols_tile_reduce_kernel");
+    ILS_CU(cudaFreeAsync(part, st));
+    return ILS_OK;
+  }
   cols_kernel<<<grid_cols(cols), 256, 0, st>>>(X, ldx, rows, cols, y, alpha, base, c, tri_lower);
   ILS_LAUNCHED("cols_kernel");
   return ILS_OK;

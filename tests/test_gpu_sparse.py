@@ -284,15 +284,19 @@ def test_sparse_gram_staged_bitwise(shape, monkeypatch):
         assert _par(hists[1][kk], ref.x_hist[kk]) <= 1e-9, kk
 
 
+@pytest.mark.parametrize("cols", ["0", "2"])
 @pytest.mark.parametrize("th", [1, 2, 3, 64])
 @pytest.mark.parametrize("shape", [(4000, 900, 700, 6), (3000, 0, 333, 5)])
-def test_sparse_sp_tree_inverse(monkeypatch, shape, th):
+def test_sparse_sp_tree_inverse(monkeypatch, shape, th, cols):
     """The n >= 8192 form of P (x = Z^T (Z c) on the Cholesky recursion's tree, whole inverses only of
     the diagonal blocks of <= ILS_ZT_TH 64-blocks, L21 by the recursive triangular solve), forced at
     small n (ILS_ZT_MIN_NPAD): SP iterates against the oracle for trees of depth 0 .. 4."""
     p, q, n, k = shape
     monkeypatch.setenv("ILS_ZT_MIN_NPAD", "64")
     monkeypatch.setenv("ILS_ZT_TH", str(th))
+    # x = Z^T t passes (c = base + alpha X^T y, also lower-triangular X): the 32-column kernel ("0") and
+    # the tiled two-columns-per-thread kernel with its chunk reduction forced at these small panels ("2")
+    monkeypatch.setenv("ILS_COLS_TILED", cols)
     pr = make_sparse(p, q, n, k, seed=21)
     A1, A2, b1, b2 = _dense(pr)
     K = 5
