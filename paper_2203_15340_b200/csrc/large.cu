@@ -28,6 +28,59 @@ __global__ void rows_minus_b_kernel(const double* __restrict__ X, int64_t ldx, i
   }
 }
 
+// The same row pass with 16-byte loads, four of the row and four of v in flight per lane (16-byte
+// aligned rows: every caller's padded layout), as gemv_rows2_kernel (ingest.cu)
+__global__ void rows_minus_b2_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows, int64_t cols,
+                                     const double* __restrict__ v, const double* __restrict__ b,
+                                     double* __restrict__ y) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t c2 = cols >> 1;
+  const double2* v2 = reinterpret_cast<const double2*>(v);
+  for (int64_t i = warp; i < rows; i += nw) {
+    const double2* xr = reinterpret_cast<const double2*>(X + i * ldx);
+    double a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = 0.0;
+    int64_t k = lane;
+    for (; k + 96 < c2; k += 128) {
+      double2 xv[4], vv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        xv[u] = __ldcs(xr + k + 32 * u);
+        vv[u] = __ldg(v2 + k + 32 * u);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[2 * u] = fma(xv[u].x, vv[u].x, a[2 * u]);
+        a[2 * u + 1] = fma(xv[u].y, vv[u].y, a[2 * u + 1]);
+      }
+    }
+    for (; k < c2; k += 32) {
+      const double2 xv = __ldcs(xr + k), vv = __ldg(v2 + k);
+      a[0] = fma(xv.x, vv.x, a[0]);
+      a[1] = fma(xv.y, vv.y, a[1]);
+    }
+    if ((cols & 1) && lane == 0) a[2] = fma(X[i * ldx + cols - 1], v[cols - 1], a[2]);
+    const double s = warp_sum(((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7])));
+    if (lane == 0) y[i] = b ? s - b[i] : s;
+  }
+}
+
+static int launch_rows_minus_b(const double* X, int64_t ldx, int64_t rows, int64_t cols, const double* v,
+                                const double* b, double* y, cudaStream_t st) {
+  const bool al16 = (((uintptr_t)X | (uintptr_t)v) & 15) == 0 && (ldx & 1) == 0;
+  if (al16) {
+    rows_minus_b2_kernel<<<148 * 16, 256, 0, st>>>(X, ldx, rows, cols, v, b, y);
+    ILS_LAUNCHED("rows_minus_b2_kernel");
+  } else {
+    rows_minus_b_kernel<<<148 * 16, 256, 0, st>>>(X, ldx, rows, cols, v, b, y);
+    ILS_LAUNCHED("rows_minus_b_kernel");
+  }
+  return ILS_OK;
+}
+
 // c[j] = (base[j]) + alpha * sum_i X[i][j] y[i]: columns split over CTAs, rows over warps of a CTA
 // (fixed-order combine in shared memory), coalesced row segments
 __global__ void __launch_bounds__(256) cols_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows,
@@ -121,15 +174,15 @@ int dense_rhs_twopass(Handle& h, const double* x, double* c, int full) {
   const int64_t np = h.npad;
   ILS_CU(cudaMemsetAsync(c, 0, np * sizeof(double), st));
   if (!full) {
-    rows_minus_b_kernel<<<148 * 16, 256, 0, st>>>(h.Arm + h.p * np, np, h.q, h.n, x, h.b + h.p, h.sp_y);
-    ILS_LAUNCHED("rows_minus_b_kernel");
+    { const int rr_ = launch_rows_minus_b(h.Arm + h.p * np, np, h.q, h.n, x, h.b + h.p, h.sp_y, st);
+      if (rr_) return rr_; }
     { const int rc_ = launch_cols(h.Arm + h.p * np, np, h.q, h.n, h.sp_y, 1.0, h.a1tb1, c, 0, st);
     if (rc_) return rc_; }
     return ILS_OK;
   }
   // g = A1^T (b1 - A1 x) - A2^T (b2 - A2 x) = -A1^T y1 + A2^T y2 with y = A x - b
-  rows_minus_b_kernel<<<148 * 16, 256, 0, st>>>(h.Arm, np, h.m, h.n, x, h.b, h.sp_y);
-  ILS_LAUNCHED("rows_minus_b_kernel");
+  { const int rr_ = launch_rows_minus_b(h.Arm, np, h.m, h.n, x, h.b, h.sp_y, st);
+    if (rr_) return rr_; }
   { const int rc_ = launch_cols(h.Arm + h.p * np, np, h.q, h.n, h.sp_y + h.p, 1.0, nullptr, c, 0, st);
     if (rc_) return rc_; }
   { const int rc_ = launch_cols(h.Arm, np, h.p, h.n, h.sp_y, -1.0, c, c, 0, st);   // in place per column
@@ -179,8 +232,8 @@ int rk_check_twopass(Handle& h, const double* z, const double* bhat, const doubl
   if (rc) return rc;
   const cudaStream_t st = h.stream;
   const int64_t np = h.npad;
-  rows_minus_b_kernel<<<148 * 16, 256, 0, st>>>(h.Arm, np, h.p, h.n, z, nullptr, az);
-  ILS_LAUNCHED("rows_minus_b_kernel");
+  { const int rr_ = launch_rows_minus_b(h.Arm, np, h.p, h.n, z, nullptr, az, st);
+    if (rr_) return rr_; }
   double* g = h.sp_y + h.m + 64;
   { const int rc_ = launch_cols(h.Arm, np, h.p, h.n, az, 1.0, nullptr, g, 0, st);
     if (rc_) return rc_; }
