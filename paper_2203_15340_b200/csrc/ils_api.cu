@@ -193,6 +193,14 @@ static void free_handle_impl(Handle* h) {
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->evk0) cudaEventDestroy(h->evk0);
   if (h->evk1) cudaEventDestroy(h->evk1);
+  for (int i = 0; i < 2; ++i) {
+    if (h->ev_mask[i]) cudaEventDestroy(h->ev_mask[i]);
+    if (h->ev_chunk[i]) cudaEventDestroy(h->ev_chunk[i]);
+  }
+  if (h->aux) {
+    cudaStreamSynchronize(h->aux);
+    cudaStreamDestroy(h->aux);
+  }
 }
 
 static float elapsed(Handle& h) {

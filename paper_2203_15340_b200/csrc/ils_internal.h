@@ -106,6 +106,9 @@ struct Handle {
 
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t evk0 = nullptr, evk1 = nullptr;   // per-launch timing of the hot kernels
+  // SP-SCD: the membership masks of chunk i + 1 are formed on an auxiliary stream while chunk i runs
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_mask[2] = {nullptr, nullptr}, ev_chunk[2] = {nullptr, nullptr};
   double hot_ms[4] = {0, 0, 0, 0};
   double hot_work[4] = {0, 0, 0, 0};
   int64_t hot_n[4] = {0, 0, 0, 0};

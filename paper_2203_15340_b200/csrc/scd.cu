@@ -663,8 +663,8 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
   const int64_t span = warpk ? kWarpChunks * ce : ce;
   const int64_t chunk_cap = (max_inner < span) ? max_inner : span;
   const size_t state_dbl = (size_t)3 * h.npad + 2 * (size_t)h.num_sms;
-  const size_t mask_bytes = weighted ? 0 : (size_t)chunk_cap * nt * sizeof(uint32_t);
-  const size_t need = state_dbl * sizeof(double) + mask_bytes;
+  const size_t mask_bytes = weighted ? 0 : (size_t)chunk_cap * nt * sizeof(uint32_t);   // one of two buffers
+  const size_t need = state_dbl * sizeof(double) + 2 * mask_bytes;
   if (h.scd_ws_bytes < need) {
     if (h.scd_ws) cudaFreeAsync(h.scd_ws, st);
     h.scd_ws = nullptr;
@@ -734,17 +734,56 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
   int pending = 0;
   p.ce = warpk ? ce : 0;
   p.inner_tol = inner_tol;
+  // The masks are data-independent: those of chunk c + 1 are formed on the auxiliary stream, into the
+  // other of two buffers, while chunk c (one CTA) runs. ev_mask[b]: buffer b written; ev_chunk[b]: the
+  // chunk reading buffer b done. ILS_SCD_MASK_OVERLAP=0: same stream, in turn.
+  const bool use_masks = !weighted && !p.all_members;
+  bool overlap = use_masks;
+  {
+    const char* e = getenv("ILS_SCD_MASK_OVERLAP");
+    if (e && e[0] == '0') overlap = false;
+  }
+  uint32_t* mbuf[2] = {masks, masks + (overlap ? mask_bytes / sizeof(uint32_t) : 0)};
+  if (overlap) {
+    if (!h.aux) ILS_CU(cudaStreamCreateWithFlags(&h.aux, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      if (!h.ev_mask[i]) ILS_CU(cudaEventCreateWithFlags(&h.ev_mask[i], cudaEventDisableTiming));
+      if (!h.ev_chunk[i]) ILS_CU(cudaEventCreateWithFlags(&h.ev_chunk[i], cudaEventDisableTiming));
+    }
+    // the auxiliary stream starts behind everything queued so far (workspace, earlier solves)
+    ILS_CU(cudaEventRecord(h.ev_chunk[0], st));
+    ILS_CU(cudaStreamWaitEvent(h.aux, h.ev_chunk[0], 0));
+    const int64_t t1 = (span < max_inner) ? span : max_inner;
+    const int rm = launch_masks(h.aux, seed, (uint32_t)k, 0, t1, nn, alpha_mode, alpha_k, nt, V, mbuf[0]);
+    if (rm) return rm;
+    ILS_CU(cudaEventRecord(h.ev_mask[0], h.aux));
+  }
+  int64_t ci = 0;   // chunk index
   while (t < max_inner) {
     const int64_t t1 = (t + span < max_inner) ? t + span : max_inner;
-    if (!weighted && !p.all_members) {
-      const int rm = launch_masks(st, seed, (uint32_t)k, t, t1, nn, alpha_mode, alpha_k, nt, V, masks);
+    const int b = (int)(ci & 1);
+    if (use_masks && !overlap) {
+      const int rm = launch_masks(st, seed, (uint32_t)k, t, t1, nn, alpha_mode, alpha_k, nt, V, mbuf[0]);
       if (rm) return rm;
+    }
+    if (overlap) {
+      if (t1 < max_inner) {   // masks of chunk ci + 1 into the other buffer, once chunk ci - 1 has read it
+        const int64_t t2 = (t1 + span < max_inner) ? t1 + span : max_inner;
+        if (ci >= 1) ILS_CU(cudaStreamWaitEvent(h.aux, h.ev_chunk[b ^ 1], 0));
+        const int rm = launch_masks(h.aux, seed, (uint32_t)k, t1, t2, nn, alpha_mode, alpha_k, nt, V, mbuf[b ^ 1]);
+        if (rm) return rm;
+        ILS_CU(cudaEventRecord(h.ev_mask[b ^ 1], h.aux));
+      }
+      ILS_CU(cudaStreamWaitEvent(st, h.ev_mask[b], 0));
+      p.masks = mbuf[b];
     }
     p.t0 = t;
     p.t1 = t1;
     void* args[] = {&p};
     ILS_CU(cudaLaunchKernel(kern, dim3(1), dim3(nt), args, smem, st));
     ILS_LAUNCHED(warpk ? "scd_warp_kernel" : "scd_chunk_kernel");
+    if (overlap) ILS_CU(cudaEventRecord(h.ev_chunk[b], st));
+    ++ci;
     t = t1;
     if (t % ce == 0) {
       double itol = inner_tol;
@@ -762,6 +801,10 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
       pending = 0;
       if (h.hstat->inner_conv) break;
     }
+  }
+  if (overlap) {   // the last masks launch may be one chunk ahead of a stop: the handle's stream follows it
+    ILS_CU(cudaEventRecord(h.ev_mask[0], h.aux));
+    ILS_CU(cudaStreamWaitEvent(st, h.ev_mask[0], 0));
   }
   ILS_CU(cudaEventRecord(h.evk1, st));
   ILS_CU(cudaMemsetAsync(beta, 0, h.npad * sizeof(double), st));
