@@ -342,8 +342,10 @@ int launch_cols(const double* X, int64_t ldx, int64_t rows, int64_t cols, const 
     int64_t chunks = ((int64_t)148 * cps + nct - 1) / nct;
     if (chunks > rows / 32) chunks = rows / 32;            // at least 32 rows per chunk
     if (chunks < 1) chunks = 1;
-    const int64_t rc = (rows + chunks - 1) / chunks;
+    int64_t rc = (rows + chunks - 1) / chunks;
+    if (rc < 1) rc = 1;                                    // rows = 0 (forced mode): one chunk of zeros
     chunks = (rows + rc - 1) / rc;
+    if (chunks < 1) chunks = 1;
     double* part = nullptr;
     ILS_CU(cudaMallocAsync(&part, (size_t)chunks * cols * sizeof(double), st));
     cols_tile_kernel<<<dim3((unsigned)nct, (unsigned)chunks), CT_THREADS, 0, st>>>(X, ldx, rows, cols, y, rc, tri_lower,

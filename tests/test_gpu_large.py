@@ -52,10 +52,15 @@ class Big:
 SHAPES = [(200, 100, 50, 0.3), (257, 33, 31, 0.3), (90, 0, 17, 0.3), (1000, 300, 130, 0.4)]
 
 
+@pytest.mark.parametrize("cols", ["0", "2"])
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("form", [0, 1])
-def test_large_sp_fixed_horizon(shape, form, monkeypatch):
+def test_large_sp_fixed_horizon(shape, form, cols, monkeypatch):
     p, q, n, s = shape
+    # c = base + alpha X^T y of the two-pass right-hand side and of the P apply: the 32-column kernel
+    # ("0") and the tiled kernel forced at these sizes ("2": odd n takes its single-column tail, q = 0
+    # its empty row range, in-place base == c on the correction form)
+    monkeypatch.setenv("ILS_COLS_TILED", cols)
     pr = make_dense(p, q, n, s, seed=31)
     K = 6
     ref = O.sp_solve(pr.A1, pr.A2, pr.b1, pr.b2, max_iter=K, stop=O.STOP_NONE, sp_form=form)
