@@ -197,10 +197,7 @@ static void free_handle_impl(Handle* h) {
     if (h->ev_mask[i]) cudaEventDestroy(h->ev_mask[i]);
     if (h->ev_chunk[i]) cudaEventDestroy(h->ev_chunk[i]);
   }
-  if (h->aux) {
-    cudaStreamSynchronize(h->aux);
-    cudaStreamDestroy(h->aux);
-  }
+  if (h->aux) cudaStreamSynchronize(h->aux);   // shared per device (scd.cu), not owned
 }
 
 static float elapsed(Handle& h) {

@@ -736,16 +736,26 @@ int scd_inner(Handle& h, const double* bhat, double* beta, uint64_t seed, int64_
   p.inner_tol = inner_tol;
   // The masks are data-independent: those of chunk c + 1 are formed on the auxiliary stream, into the
   // other of two buffers, while chunk c (one CTA) runs. ev_mask[b]: buffer b written; ev_chunk[b]: the
-  // chunk reading buffer b done. ILS_SCD_MASK_OVERLAP=0: same stream, in turn.
+  // chunk reading buffer b done. Opt-in (ILS_SCD_MASK_OVERLAP=1): alone, SP-SCD at c1 gains 2 ms per
+  // solve (121.1 -> 118.6-119.3 ms), but inside bench.py's full step (SP, SP-RK-RGS, SP-SCD on one fresh
+  // handle) it measured 0.8-1.0 ms slower (120.0-120.1 -> 120.9-121.0 ms, two boxes, a stream per handle
+  // or one shared per device alike), so the default keeps the masks on the handle's stream, in turn.
   const bool use_masks = !weighted && !p.all_members;
-  bool overlap = use_masks;
+  bool overlap = false;
   {
     const char* e = getenv("ILS_SCD_MASK_OVERLAP");
-    if (e && e[0] == '0') overlap = false;
+    if (e && e[0] == '1') overlap = use_masks;
   }
   uint32_t* mbuf[2] = {masks, masks + (overlap ? mask_bytes / sizeof(uint32_t) : 0)};
   if (overlap) {
-    if (!h.aux) ILS_CU(cudaStreamCreateWithFlags(&h.aux, cudaStreamNonBlocking));
+    if (!h.aux) {   // one auxiliary stream per device and process, shared by the handles
+      static cudaStream_t aux_dev[64] = {};
+      int dev = 0;
+      ILS_CU(cudaGetDevice(&dev));
+      if (dev < 0 || dev >= 64) dev = 0;
+      if (!aux_dev[dev]) ILS_CU(cudaStreamCreateWithFlags(&aux_dev[dev], cudaStreamNonBlocking));
+      h.aux = aux_dev[dev];
+    }
     for (int i = 0; i < 2; ++i) {
       if (!h.ev_mask[i]) ILS_CU(cudaEventCreateWithFlags(&h.ev_mask[i], cudaEventDisableTiming));
       if (!h.ev_chunk[i]) ILS_CU(cudaEventCreateWithFlags(&h.ev_chunk[i], cudaEventDisableTiming));
